@@ -1,0 +1,677 @@
+/*
+ * vf_oracle.c -- CPU restatement of the reference `vidfeat` per-frame hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the CUDA
+ * product path (and the `cpu_baseline` / `--impl reference` arm of bench.py,
+ * kind "port").  Only tests/, __graft_entry__.smoke() and bench.py may load
+ * it.  The product (paper_1503_06959_b200/) never links or calls it.
+ *
+ * Parity pin: this restatement is checked against golden vectors produced by
+ * running the reference itself (tests/golden/make_golden.py imports
+ * /root/reference/pkg/src/vidfeat and commits the tests/golden fixtures); see
+ * tests/test_oracle_golden.py.
+ *
+ * Numerics follow the reference exactly: integer stages are bit-exact; fp64
+ * stages use the same operation order, no FMA contraction
+ * (-ffp-contract=off), and glibc cos/sin/atan2/pow (numba lowers to libm).
+ *
+ * Every function cites the reference file:line it restates.  Paths are
+ * relative to /root/reference/pkg/src/vidfeat/.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define VFO_MAX_LAYERS 32
+
+/* ------------------------------------------------------------------ */
+/* pyramid.py:97-125 -- layer geometry.  Order o0, i0, o1, i1, ...     */
+/* ------------------------------------------------------------------ */
+int vfo_layer_dims(int W, int H, int O, int *ws, int *hs, double *scales)
+{
+    if (O < 1) return -1;                              /* pyramid.py:103-104 */
+    int need = 1 << (O - 1);
+    if (W < need || H < need) return -2;               /* pyramid.py:105-109 */
+    int ow = W, oh = H;
+    int iw = (2 * W) / 3, ih = (2 * H) / 3;            /* pyramid.py:82 m=(2n)//3 */
+    if (iw < 1 || ih < 1) return -3;
+    for (int o = 0; o < O; o++) {
+        if (o > 0) {
+            ow /= 2; oh /= 2; iw /= 2; ih /= 2;        /* pyramid.py:69 */
+            if (ow < 1 || oh < 1 || iw < 1 || ih < 1) return -3;
+        }
+        ws[2 * o] = ow; hs[2 * o] = oh;
+        ws[2 * o + 1] = iw; hs[2 * o + 1] = ih;
+        if (scales) {
+            double sc = ldexp(1.0, -o);                /* 2.0 ** (-o) */
+            scales[2 * o] = sc;
+            scales[2 * o + 1] = sc / 1.5;              /* pyramid.py:123 */
+        }
+    }
+    return 0;
+}
+
+/* pyramid.py:67-73: 2x2 uint16 sum, (s+2)>>2, odd trailing dropped */
+void vfo_halve(const uint8_t *a, int w, int h, uint8_t *out)
+{
+    int w2 = w / 2, h2 = h / 2;
+    for (int y = 0; y < h2; y++)
+        for (int x = 0; x < w2; x++) {
+            unsigned s = a[(2 * y) * w + 2 * x] + a[(2 * y) * w + 2 * x + 1] +
+                         a[(2 * y + 1) * w + 2 * x] + a[(2 * y + 1) * w + 2 * x + 1];
+            out[y * w2 + x] = (uint8_t)((s + 2) >> 2);
+        }
+}
+
+/* pyramid.py:76-94: per-axis (2a+b | a+2b) pair sums, then (v+4)//9 */
+void vfo_two_thirds(const uint8_t *a, int w, int h, uint8_t *out)
+{
+    int mw = (2 * w) / 3, mh = (2 * h) / 3;
+    uint32_t *rows = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)mh * w);
+    for (int j = 0; j < mh; j++) {                     /* axis 0 first (:94) */
+        int k = j / 2;
+        for (int x = 0; x < w; x++) {
+            uint32_t v;
+            if ((j & 1) == 0) v = 2u * a[(3 * k) * w + x] + a[(3 * k + 1) * w + x];
+            else v = a[(3 * k + 1) * w + x] + 2u * a[(3 * k + 2) * w + x];
+            rows[(size_t)j * w + x] = v;
+        }
+    }
+    for (int y = 0; y < mh; y++)
+        for (int i = 0; i < mw; i++) {
+            int k = i / 2;
+            const uint32_t *r = rows + (size_t)y * w;
+            uint32_t v = (i & 1) == 0 ? 2u * r[3 * k] + r[3 * k + 1] : r[3 * k + 1] + 2u * r[3 * k + 2];
+            out[y * mw + i] = (uint8_t)((v + 4) / 9);
+        }
+    free(rows);
+}
+
+/* pyramid.py:111-125.  layers[l] must hold ws[l]*hs[l] bytes (layer 0 is a copy). */
+int vfo_build_pyramid(const uint8_t *frame, int W, int H, int O, uint8_t **layers)
+{
+    int ws[VFO_MAX_LAYERS], hs[VFO_MAX_LAYERS];
+    if (O > VFO_MAX_LAYERS / 2) return -1;
+    int rc = vfo_layer_dims(W, H, O, ws, hs, NULL);
+    if (rc) return rc;
+    memcpy(layers[0], frame, (size_t)W * H);
+    for (int o = 1; o < O; o++) vfo_halve(layers[2 * (o - 1)], ws[2 * (o - 1)], hs[2 * (o - 1)], layers[2 * o]);
+    vfo_two_thirds(frame, W, H, layers[1]);
+    for (int o = 1; o < O; o++)
+        vfo_halve(layers[2 * (o - 1) + 1], ws[2 * (o - 1) + 1], hs[2 * (o - 1) + 1], layers[2 * o + 1]);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* detector.py:20-28 CIRCLE; detector.py:107-158 _score_map_jit          */
+/* ------------------------------------------------------------------ */
+static const int CX[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+static const int CY[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+
+/* mask may be NULL (all ones); it is the per-layer projected mask (h x w). */
+void vfo_score_map(const uint8_t *data, int w, int h, int t, const uint8_t *mask, int32_t *scores)
+{
+    memset(scores, 0, sizeof(int32_t) * (size_t)w * h);
+    for (int y = 3; y < h - 3; y++)
+        for (int x = 3; x < w - 3; x++) {
+            if (mask && mask[(size_t)y * w + x] == 0) continue;       /* :114-115 */
+            int64_t c = data[(size_t)y * w + x];
+            int64_t d0 = (int64_t)data[(size_t)(y - 3) * w + x] - c;
+            int64_t d8 = (int64_t)data[(size_t)(y + 3) * w + x] - c;
+            int64_t d4 = (int64_t)data[(size_t)y * w + x + 3] - c;
+            int64_t d12 = (int64_t)data[(size_t)y * w + x - 3] - c;
+            int bright_ok = (d0 > t || d8 > t) && (d4 > t || d12 > t);  /* :121-123 */
+            int dark_ok = (d0 < -t || d8 < -t) && (d4 < -t || d12 < -t);
+            if (!(bright_ok || dark_ok)) continue;
+            int64_t d[16];
+            for (int k = 0; k < 16; k++) d[k] = (int64_t)data[(size_t)(y + CY[k]) * w + x + CX[k]] - c;
+            int64_t best = 0;
+            for (int pol = 0; pol < 2; pol++) {           /* :128-154 */
+                if (pol == 0 && !bright_ok) continue;
+                if (pol == 1 && !dark_ok) continue;
+                int64_t sg = pol == 0 ? 1 : -1;
+                for (int s0 = 0; s0 < 16; s0++) {
+                    int64_t m = sg * d[s0];
+                    if (m <= best) continue;
+                    for (int k = 1; k < 9; k++) {
+                        int64_t v = sg * d[(s0 + k) & 15];
+                        if (v < m) { m = v; if (m <= best) break; }
+                    }
+                    if (m > best) best = m;
+                }
+            }
+            int64_t score = best - 1;                     /* :155-157 */
+            if (score >= t) scores[(size_t)y * w + x] = (int32_t)score;
+        }
+}
+
+/* detector.py:175-181 _project_mask: floor mapping of a full-res mask */
+void vfo_project_mask(const uint8_t *bits, int mw, int mh, int w, int h, uint8_t *out)
+{
+    for (int y = 0; y < h; y++) {
+        int64_t yy = ((int64_t)y * mh) / h;
+        for (int x = 0; x < w; x++) {
+            int64_t xx = ((int64_t)x * mw) / w;
+            out[(size_t)y * w + x] = bits[yy * mw + xx];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* detector.py:207-228 _fit_quadratic_peak (one patch, same op order)    */
+/* ------------------------------------------------------------------ */
+static void fit_peak(const double p[3][3], double *ox, double *oy, double *val, int *okp)
+{
+    double gx = 0.5 * (p[1][2] - p[1][0]);
+    double gy = 0.5 * (p[2][1] - p[0][1]);
+    double dxx = p[1][2] - 2.0 * p[1][1] + p[1][0];
+    double dyy = p[2][1] - 2.0 * p[1][1] + p[0][1];
+    double dxy = 0.25 * (p[2][2] - p[2][0] - p[0][2] + p[0][0]);
+    double det = dxx * dyy - dxy * dxy;
+    int ok = (dxx < 0.0) && (det > 0.0);
+    double safe = ok ? det : 1.0;
+    double x = ok ? -(dyy * gx - dxy * gy) / safe : 0.0;
+    double y = ok ? -(dxx * gy - dxy * gx) / safe : 0.0;
+    ok = ok && (fabs(x) < 1.0) && (fabs(y) < 1.0);
+    x = ok ? x : 0.0;
+    y = ok ? y : 0.0;
+    *val = p[1][1] + 0.5 * (gx * x + gy * y);
+    *ox = x; *oy = y; *okp = ok;
+}
+
+/* detector.py:231-236 _gather_patches on the 1-pixel zero-padded map */
+static void gather(const int32_t *m, int w, int h, int y, int x, double p[3][3], int32_t *pmax)
+{
+    int32_t mx = INT32_MIN;
+    for (int dy = -1; dy <= 1; dy++)
+        for (int dx = -1; dx <= 1; dx++) {
+            int yy = y + dy, xx = x + dx;
+            int32_t v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? m[(size_t)yy * w + xx] : 0;
+            p[dy + 1][dx + 1] = (double)v;
+            if (v > mx) mx = v;
+        }
+    if (pmax) *pmax = mx;
+}
+
+/* numpy negative-index wrap for smap[ys+dy, xs+dx] (detector.py:260-262) */
+static int wrap_get(const int32_t *m, int w, int h, int y, int x, int32_t *v)
+{
+    if (y >= h || x >= w) return -1;   /* numpy IndexError */
+    if (y < 0) y += h;
+    if (x < 0) x += w;
+    *v = m[(size_t)y * w + x];
+    return 0;
+}
+
+/*
+ * detector.py:239-307 _nms_from_maps.  maps[i] is an int32 (hs[i] x ws[i]) map.
+ * Output arrays must hold `cap` entries; returns the keypoint count, -1 on
+ * overflow, -2 on an IndexError the reference would raise.
+ * layer_out / xi_out / yi_out (nullable) give the integer origin (diagnostics).
+ */
+int vfo_nms(const int32_t *const *maps, const int *ws, const int *hs, const double *scales,
+            int n_layers, int W, int H, int cap, double *kx, double *ky, double *ksig,
+            double *kscore, int32_t *layer_out, int32_t *xi_out, int32_t *yi_out)
+{
+    double sigmas[VFO_MAX_LAYERS];
+    for (int i = 0; i < n_layers; i++) sigmas[i] = 1.0 / scales[i];   /* :243 */
+    int n = 0;
+    for (int i = 0; i < n_layers; i++) {
+        const int32_t *sm = maps[i];
+        int w = ws[i], h = hs[i];
+        for (int y = 0; y < h; y++)
+            for (int x = 0; x < w; x++) {
+                int32_t s = sm[(size_t)y * w + x];
+                if (s == 0) continue;                                     /* :251 nonzero */
+                int keep = 1;
+                for (int dy = -1; dy <= 1; dy++)
+                    for (int dx = -1; dx <= 1; dx++) {
+                        if (dx == 0 && dy == 0) continue;
+                        int32_t v;
+                        if (wrap_get(sm, w, h, y + dy, x + dx, &v)) return -2;
+                        if (!(s > v)) keep = 0;
+                    }
+                int yj[2], xj[2], have[2] = {0, 0};
+                for (int k = 0; k < 2; k++) {                             /* :266-273 */
+                    int j = i - 1 + 2 * k;
+                    if (j < 0 || j >= n_layers) continue;
+                    int hj = hs[j], wj = ws[j];
+                    int64_t a = ((int64_t)y * hj + (h >> 1)) / h;
+                    int64_t b = ((int64_t)x * wj + (w >> 1)) / w;
+                    yj[k] = (int)(a < hj - 1 ? a : hj - 1);
+                    xj[k] = (int)(b < wj - 1 ? b : wj - 1);
+                    have[k] = 1;
+                    if (!(s > maps[j][(size_t)yj[k] * wj + xj[k]])) keep = 0;
+                }
+                if (!keep) continue;
+                double p[3][3], ox, oy, v0;
+                int ok;
+                gather(sm, w, h, y, x, p, NULL);                          /* :277-279 */
+                fit_peak(p, &ox, &oy, &v0, &ok);
+                double nv[2] = {0.0, 0.0};
+                for (int k = 0; k < 2; k++) {                             /* :281-285 */
+                    if (!have[k]) continue;
+                    int j = i - 1 + 2 * k;
+                    double pj[3][3], vj, tx, ty;
+                    int32_t pmax;
+                    int okj;
+                    gather(maps[j], ws[j], hs[j], yj[k], xj[k], pj, &pmax);
+                    fit_peak(pj, &tx, &ty, &vj, &okj);
+                    nv[k] = okj ? vj : (double)pmax;
+                }
+                double sig = sigmas[i];
+                if (have[0] && have[1]) {                                 /* :287-297 */
+                    double vb = nv[0], va = nv[1];
+                    double denom = vb - 2.0 * v0 + va;
+                    int concave = denom < 0.0;
+                    double delta = concave ? 0.5 * (vb - va) / denom : 0.0;
+                    delta = fabs(delta) < 1.0 ? delta : 0.0;
+                    double up = sigmas[i + 1] / sigmas[i];
+                    double down = sigmas[i - 1] / sigmas[i];
+                    double a = delta > 0.0 ? delta : 0.0;
+                    double b = -delta > 0.0 ? -delta : 0.0;
+                    sig = sigmas[i] * pow(up, a) * pow(down, b);
+                }
+                double scale = scales[i];                                 /* :299-302 */
+                double x0 = ((double)x + ox) / scale;
+                double y0 = ((double)y + oy) / scale;
+                double xhi = (double)W - 1e-6, yhi = (double)H - 1e-6;
+                x0 = x0 < 0.0 ? 0.0 : (x0 > xhi ? xhi : x0);
+                y0 = y0 < 0.0 ? 0.0 : (y0 > yhi ? yhi : y0);
+                if (n >= cap) return -1;
+                kx[n] = x0; ky[n] = y0; ksig[n] = sig; kscore[n] = v0;
+                if (layer_out) layer_out[n] = i;
+                if (xi_out) xi_out[n] = x;
+                if (yi_out) yi_out[n] = y;
+                n++;
+            }
+    }
+    return n;
+}
+
+/* ------------------------------------------------------------------ */
+/* descriptor.py:28-32 integral_image (int64, (h+1) x (w+1))             */
+/* ------------------------------------------------------------------ */
+void vfo_integral(const uint8_t *d, int w, int h, int64_t *sat)
+{
+    int W1 = w + 1;
+    memset(sat, 0, sizeof(int64_t) * (size_t)W1);
+    for (int y = 0; y < h; y++) {
+        int64_t row = 0;
+        sat[(size_t)(y + 1) * W1] = 0;
+        for (int x = 0; x < w; x++) {
+            row += d[(size_t)y * w + x];
+            sat[(size_t)(y + 1) * W1 + x + 1] = sat[(size_t)y * W1 + x + 1] + row;
+        }
+    }
+}
+
+/* descriptor.py:85-92 _box_mean_jit */
+static inline int64_t box_mean(const int64_t *sat, int w, int h, int64_t x, int64_t y, int64_t r)
+{
+    int64_t x0 = x - r > 0 ? x - r : 0, x1 = x + r < w - 1 ? x + r : w - 1;
+    int64_t y0 = y - r > 0 ? y - r : 0, y1 = y + r < h - 1 ? y + r : h - 1;
+    int64_t W1 = w + 1;
+    int64_t s = sat[(y1 + 1) * W1 + x1 + 1] - sat[y0 * W1 + x1 + 1] - sat[(y1 + 1) * W1 + x0] + sat[y0 * W1 + x0];
+    return s / ((x1 - x0 + 1) * (y1 - y0 + 1));   /* s >= 0: floor division */
+}
+
+/* descriptor.py:94-115 _point_values_jit for one keypoint */
+static void point_values(const int64_t *sat, int w, int h, double kx, double ky, double sigma,
+                         double theta, const double *pts, const double *radii, int m, int64_t *out)
+{
+    double c = cos(theta), s = sin(theta);
+    for (int j = 0; j < m; j++) {
+        double px = pts[2 * j], py = pts[2 * j + 1];
+        int64_t x = (int64_t)floor(kx + sigma * (c * px - s * py) + 0.5);
+        int64_t y = (int64_t)floor(ky + sigma * (s * px + c * py) + 0.5);
+        if (x < 0) x = 0; else if (x > w - 1) x = w - 1;
+        if (y < 0) y = 0; else if (y > h - 1) y = h - 1;
+        int64_t r = (int64_t)floor(radii[j] * sigma + 0.5);
+        out[j] = box_mean(sat, w, h, x, y, r);
+    }
+}
+
+/* descriptor.py:128-144 _orientations_jit (sequential sum in pair order) */
+void vfo_orientations(const int64_t *sat, int w, int h, int n, const double *kx, const double *ky,
+                      const double *sigma, const double *pts, const double *radii, int m,
+                      const int32_t *li, const int32_t *lj, const double *wx, const double *wy,
+                      int L, double *theta)
+{
+    int64_t *vals = (int64_t *)malloc(sizeof(int64_t) * m);
+    for (int i = 0; i < n; i++) {
+        point_values(sat, w, h, kx[i], ky[i], sigma[i], 0.0, pts, radii, m, vals);
+        double gx = 0.0, gy = 0.0;
+        for (int p = 0; p < L; p++) {
+            double dv = (double)(vals[li[p]] - vals[lj[p]]);
+            gx += dv * wx[p];
+            gy += dv * wy[p];
+        }
+        double t = atan2(gy, gx);
+        theta[i] = t <= -M_PI ? M_PI : t;
+    }
+    free(vals);
+}
+
+/* descriptor.py:117-126 _describe_batch_jit, packed MSB-first (descriptor.py:271-275) */
+void vfo_describe(const int64_t *sat, int w, int h, int n, const double *kx, const double *ky,
+                  const double *sigma, const double *theta, const double *pts, const double *radii,
+                  int m, const int32_t *si, const int32_t *sj, int nbits, uint8_t *packed)
+{
+    int64_t *vals = (int64_t *)malloc(sizeof(int64_t) * m);
+    int nbytes = (nbits + 7) / 8;
+    for (int i = 0; i < n; i++) {
+        point_values(sat, w, h, kx[i], ky[i], sigma[i], theta[i], pts, radii, m, vals);
+        uint8_t *o = packed + (size_t)i * nbytes;
+        memset(o, 0, nbytes);
+        for (int b = 0; b < nbits; b++)
+            if (vals[si[b]] > vals[sj[b]]) o[b >> 3] |= (uint8_t)(0x80u >> (b & 7));
+    }
+    free(vals);
+}
+
+/* ------------------------------------------------------------------ */
+/* masking.py:84-93 intensity_diff_mask (strict, int16 diff vs float t_i) */
+/* ------------------------------------------------------------------ */
+void vfo_intensity_mask(const uint8_t *prev, const uint8_t *cur, int n, double t_i, uint8_t *out)
+{
+    for (int i = 0; i < n; i++) {
+        int d = (int)cur[i] - (int)prev[i];
+        if (d < 0) d = -d;
+        out[i] = (double)d > t_i ? 1 : 0;
+    }
+}
+
+/* masking.py:96-119 binning_histogram (ceil cells, fp64 floor, clamped) */
+void vfo_binning_hist(int n, const double *xs, const double *ys, int W, int H, int rows, int cols,
+                      int64_t *hist)
+{
+    int64_t sx = (W + cols - 1) / cols, sy = (H + rows - 1) / rows;
+    memset(hist, 0, sizeof(int64_t) * (size_t)rows * cols);
+    for (int i = 0; i < n; i++) {
+        double fx = floor(xs[i] / (double)sx), fy = floor(ys[i] / (double)sy);
+        int64_t k = (int64_t)fx, l = (int64_t)fy;
+        if (k < 0) k = 0; if (k > cols - 1) k = cols - 1;
+        if (l < 0) l = 0; if (l > rows - 1) l = rows - 1;
+        hist[l * cols + k]++;
+    }
+}
+
+/* masking.py:139-148 upsample_mask: full[y][x] = bits[y//ch][x//cw] */
+void vfo_upsample(const uint8_t *bits, int rows, int cols, int cw, int ch, int W, int H, uint8_t *full)
+{
+    (void)rows; (void)cols;
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) full[(size_t)y * W + x] = bits[(y / ch) * cols + x / cw];
+}
+
+/* masking.py:151-165 _mask_at / _mask_values */
+static inline int mask_at(const uint8_t *full, int W, int H, double x, double y)
+{
+    int64_t xi = (int64_t)floor(x + 0.5), yi = (int64_t)floor(y + 0.5);
+    if (xi < 0) xi = 0; if (xi > W - 1) xi = W - 1;
+    if (yi < 0) yi = 0; if (yi > H - 1) yi = H - 1;
+    return full[yi * W + xi];
+}
+
+/* ------------------------------------------------------------------ */
+/* pipeline.py:207-278 run_pipeline (modes none / intensity / binning)   */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int n, cap;
+    double *x, *y, *sigma, *theta, *score;
+    uint8_t *origin;   /* 0 detected, 1 propagated */
+    int32_t *age;
+    uint8_t *desc;     /* 64 B packed per feature */
+} vfo_feats;
+
+typedef struct {
+    int W, H, O, threshold, mode, per_layer, mask_level, t_h, grid_rows, grid_cols;
+    double t_i;
+    /* pattern */
+    int m, nbits, L;
+    double *pts, *radii, *wx, *wy;
+    int32_t *si, *sj, *li, *lj;
+    /* geometry */
+    int n_layers, ws[VFO_MAX_LAYERS], hs[VFO_MAX_LAYERS];
+    double scales[VFO_MAX_LAYERS];
+    /* state */
+    int64_t frame_no;
+    uint8_t *layers[VFO_MAX_LAYERS], *prev_layers[VFO_MAX_LAYERS];
+    int32_t *maps[VFO_MAX_LAYERS];
+    uint8_t *full_mask, *level_masks[VFO_MAX_LAYERS / 2], *proj;
+    int64_t *sat;
+    vfo_feats cur, prev;
+    /* report of the last frame */
+    int n_detected, n_propagated, n_total, n_dropped;
+    double coverage;
+} vfo_pipe;
+
+static void feats_reserve(vfo_feats *f, int n)
+{
+    if (n <= f->cap) return;
+    int c = f->cap ? f->cap : 1024;
+    while (c < n) c *= 2;
+    f->x = realloc(f->x, sizeof(double) * c);
+    f->y = realloc(f->y, sizeof(double) * c);
+    f->sigma = realloc(f->sigma, sizeof(double) * c);
+    f->theta = realloc(f->theta, sizeof(double) * c);
+    f->score = realloc(f->score, sizeof(double) * c);
+    f->origin = realloc(f->origin, c);
+    f->age = realloc(f->age, sizeof(int32_t) * c);
+    f->desc = realloc(f->desc, (size_t)64 * c);
+    f->cap = c;
+}
+
+static void feats_free(vfo_feats *f)
+{
+    free(f->x); free(f->y); free(f->sigma); free(f->theta); free(f->score);
+    free(f->origin); free(f->age); free(f->desc);
+    memset(f, 0, sizeof(*f));
+}
+
+/* mode: 0 none, 1 intensity, 2 binning.  mask_level < 0 = top octave. */
+vfo_pipe *vfo_pipe_create(int W, int H, int O, int threshold, int mode, double t_i, int t_h,
+                          int grid_rows, int grid_cols, int mask_level, int per_layer, int m,
+                          const double *pts, const double *radii, int nbits, const int32_t *short_pairs,
+                          int L, const int32_t *long_pairs, int *err)
+{
+    *err = 0;
+    if (threshold < 1) { *err = -10; return NULL; }
+    vfo_pipe *p = (vfo_pipe *)calloc(1, sizeof(vfo_pipe));
+    p->W = W; p->H = H; p->O = O; p->threshold = threshold; p->mode = mode; p->t_i = t_i;
+    p->t_h = t_h; p->grid_rows = grid_rows; p->grid_cols = grid_cols; p->per_layer = per_layer;
+    p->mask_level = mask_level < 0 ? O - 1 : mask_level;
+    if (O > VFO_MAX_LAYERS / 2) { *err = -1; free(p); return NULL; }
+    int rc = vfo_layer_dims(W, H, O, p->ws, p->hs, p->scales);
+    if (rc) { *err = rc; free(p); return NULL; }
+    p->n_layers = 2 * O;
+    for (int l = 0; l < p->n_layers; l++) {
+        size_t sz = (size_t)p->ws[l] * p->hs[l];
+        p->layers[l] = malloc(sz);
+        p->prev_layers[l] = malloc(sz);
+        p->maps[l] = malloc(sizeof(int32_t) * sz);
+    }
+    p->full_mask = malloc((size_t)W * H);
+    for (int o = 0; o < O; o++) p->level_masks[o] = malloc((size_t)W * H);
+    p->proj = malloc((size_t)W * H);
+    p->sat = malloc(sizeof(int64_t) * (size_t)(W + 1) * (H + 1));
+    p->m = m; p->nbits = nbits; p->L = L;
+    p->pts = malloc(sizeof(double) * 2 * m); memcpy(p->pts, pts, sizeof(double) * 2 * m);
+    p->radii = malloc(sizeof(double) * m); memcpy(p->radii, radii, sizeof(double) * m);
+    p->si = malloc(sizeof(int32_t) * nbits); p->sj = malloc(sizeof(int32_t) * nbits);
+    for (int b = 0; b < nbits; b++) { p->si[b] = short_pairs[2 * b]; p->sj[b] = short_pairs[2 * b + 1]; }
+    p->li = malloc(sizeof(int32_t) * L); p->lj = malloc(sizeof(int32_t) * L);
+    p->wx = malloc(sizeof(double) * L); p->wy = malloc(sizeof(double) * L);
+    for (int q = 0; q < L; q++) {                      /* descriptor.py:163-180 _pair_arrays */
+        int a = long_pairs[2 * q], b = long_pairs[2 * q + 1];
+        p->li[q] = a; p->lj[q] = b;
+        double dx = pts[2 * a] - pts[2 * b], dy = pts[2 * a + 1] - pts[2 * b + 1];
+        double inv = 1.0 / (dx * dx + dy * dy);
+        p->wx[q] = dx * inv; p->wy[q] = dy * inv;
+    }
+    return p;
+}
+
+void vfo_pipe_destroy(vfo_pipe *p)
+{
+    if (!p) return;
+    for (int l = 0; l < p->n_layers; l++) { free(p->layers[l]); free(p->prev_layers[l]); free(p->maps[l]); }
+    for (int o = 0; o < p->O; o++) free(p->level_masks[o]);
+    free(p->full_mask); free(p->proj); free(p->sat);
+    free(p->pts); free(p->radii); free(p->si); free(p->sj); free(p->li); free(p->lj); free(p->wx); free(p->wy);
+    feats_free(&p->cur); feats_free(&p->prev);
+    free(p);
+}
+
+static int any_set(const uint8_t *a, size_t n)
+{
+    for (size_t i = 0; i < n; i++) if (a[i]) return 1;
+    return 0;
+}
+
+/* One frame through run_pipeline's loop body (pipeline.py:222-277).  Returns 0 or <0. */
+int vfo_pipe_process(vfo_pipe *p, const uint8_t *frame)
+{
+    int W = p->W, H = p->H, O = p->O, NL = p->n_layers;
+    int rc = vfo_build_pyramid(frame, W, H, O, p->layers);
+    if (rc) return rc;
+    int use_mask = p->mode != 0 && p->frame_no > 0;
+    int per_level = 0;
+    double coverage = 1.0;
+    if (use_mask) {                                        /* pipeline.py:174-204 _build_mask */
+        if (p->mode == 2) {
+            int rows = p->grid_rows, cols = p->grid_cols;
+            int64_t *hist = malloc(sizeof(int64_t) * rows * cols);
+            vfo_binning_hist(p->prev.n, p->prev.x, p->prev.y, W, H, rows, cols, hist);
+            uint8_t *bits = malloc(rows * cols);
+            for (int i = 0; i < rows * cols; i++) bits[i] = hist[i] >= p->t_h;
+            vfo_upsample(bits, rows, cols, (W + cols - 1) / cols, (H + rows - 1) / rows, W, H, p->full_mask);
+            free(hist); free(bits);
+        } else if (p->per_layer) {
+            per_level = 1;
+            memset(p->full_mask, 0, (size_t)W * H);
+            for (int o = 0; o < O; o++) {
+                int l = 2 * o, w = p->ws[l], h = p->hs[l];
+                uint8_t *bits = malloc((size_t)w * h);
+                vfo_intensity_mask(p->prev_layers[l], p->layers[l], w * h, p->t_i, bits);
+                vfo_upsample(bits, h, w, (W + w - 1) / w, (H + h - 1) / h, W, H, p->level_masks[o]);
+                for (size_t i = 0; i < (size_t)W * H; i++) p->full_mask[i] |= p->level_masks[o][i];
+                free(bits);
+            }
+        } else {
+            int l = 2 * p->mask_level, w = p->ws[l], h = p->hs[l];
+            uint8_t *bits = malloc((size_t)w * h);
+            vfo_intensity_mask(p->prev_layers[l], p->layers[l], w * h, p->t_i, bits);
+            vfo_upsample(bits, h, w, (W + w - 1) / w, (H + h - 1) / h, W, H, p->full_mask);
+            free(bits);
+        }
+        size_t cnt = 0;
+        for (size_t i = 0; i < (size_t)W * H; i++) cnt += p->full_mask[i];
+        coverage = (double)cnt / ((double)W * (double)H);   /* masking.py:44-46 */
+    }
+    /* pipeline.py:91-139 _detect_keypoints */
+    int nk = 0;
+    double *kx = NULL, *ky = NULL, *ks = NULL, *kv = NULL;
+    int skip = use_mask && !per_level && !any_set(p->full_mask, (size_t)W * H);
+    if (!skip) {
+        int any_job = 0;
+        for (int l = 0; l < NL; l++) {
+            int w = p->ws[l], h = p->hs[l];
+            const uint8_t *gate = NULL;
+            if (use_mask) {
+                const uint8_t *src = per_level ? p->level_masks[l / 2] : p->full_mask;
+                vfo_project_mask(src, W, H, w, h, p->proj);
+                if (!any_set(p->proj, (size_t)w * h)) {
+                    memset(p->maps[l], 0, sizeof(int32_t) * (size_t)w * h);
+                    continue;
+                }
+                gate = p->proj;
+            }
+            any_job = 1;
+            vfo_score_map(p->layers[l], w, h, p->threshold, gate, p->maps[l]);
+        }
+        if (any_job) {
+            int cap = 1 << 16;
+            for (;;) {
+                kx = realloc(kx, sizeof(double) * cap); ky = realloc(ky, sizeof(double) * cap);
+                ks = realloc(ks, sizeof(double) * cap); kv = realloc(kv, sizeof(double) * cap);
+                nk = vfo_nms((const int32_t *const *)p->maps, p->ws, p->hs, p->scales, NL, W, H, cap,
+                             kx, ky, ks, kv, NULL, NULL, NULL);
+                if (nk != -1) break;
+                cap *= 4;
+            }
+            if (nk < 0) { free(kx); free(ky); free(ks); free(kv); return nk; }
+        }
+    }
+    /* pipeline.py:142-171 _describe_keypoints: border filter then describe kept */
+    int kept = 0;
+    for (int i = 0; i < nk; i++) {
+        double mg = 3.0 * ks[i];
+        if (kx[i] >= mg && ky[i] >= mg && kx[i] <= (double)(W - 1) - mg && ky[i] <= (double)(H - 1) - mg) {
+            kx[kept] = kx[i]; ky[kept] = ky[i]; ks[kept] = ks[i]; kv[kept] = kv[i];
+            kept++;
+        }
+    }
+    int n_dropped = nk - kept;
+    double *th = malloc(sizeof(double) * (kept ? kept : 1));
+    uint8_t *dsc = malloc((size_t)64 * (kept ? kept : 1));
+    if (kept) {
+        vfo_integral(frame, W, H, p->sat);
+        vfo_orientations(p->sat, W, H, kept, kx, ky, ks, p->pts, p->radii, p->m, p->li, p->lj, p->wx,
+                         p->wy, p->L, th);
+        vfo_describe(p->sat, W, H, kept, kx, ky, ks, th, p->pts, p->radii, p->m, p->si, p->sj, p->nbits, dsc);
+    }
+    /* masking.py:168-184 merge_features (or detected only) */
+    vfo_feats *out = &p->cur;
+    feats_reserve(out, kept + p->prev.n);
+    int n = 0;
+    for (int i = 0; i < kept; i++) {
+        if (use_mask && !mask_at(p->full_mask, W, H, kx[i], ky[i])) continue;
+        out->x[n] = kx[i]; out->y[n] = ky[i]; out->sigma[n] = ks[i]; out->theta[n] = th[i];
+        out->score[n] = kv[i]; out->origin[n] = 0; out->age[n] = 0;
+        memcpy(out->desc + (size_t)64 * n, dsc + (size_t)64 * i, 64);
+        n++;
+    }
+    int n_det = n;
+    if (use_mask) {
+        const vfo_feats *pv = &p->prev;
+        for (int i = 0; i < pv->n; i++) {
+            if (mask_at(p->full_mask, W, H, pv->x[i], pv->y[i])) continue;
+            out->x[n] = pv->x[i]; out->y[n] = pv->y[i]; out->sigma[n] = pv->sigma[i];
+            out->theta[n] = pv->theta[i]; out->score[n] = pv->score[i]; out->origin[n] = 1;
+            out->age[n] = pv->age[i] + 1;
+            memcpy(out->desc + (size_t)64 * n, pv->desc + (size_t)64 * i, 64);
+            n++;
+        }
+    }
+    out->n = n;
+    free(kx); free(ky); free(ks); free(kv); free(th); free(dsc);
+    p->n_detected = n_det; p->n_propagated = n - n_det; p->n_total = n;
+    p->n_dropped = n_dropped; p->coverage = coverage;
+    /* state carried to the next frame (pipeline.py:276-277) */
+    vfo_feats tmp = p->prev; p->prev = p->cur; p->cur = tmp;
+    for (int l = 0; l < NL; l++) {
+        uint8_t *t = p->prev_layers[l]; p->prev_layers[l] = p->layers[l]; p->layers[l] = t;
+    }
+    p->frame_no++;
+    return 0;
+}
+
+/* Results of the last processed frame (valid until the next process call). */
+void vfo_pipe_report(const vfo_pipe *p, int32_t *counts /*4*/, double *coverage)
+{
+    counts[0] = p->n_detected; counts[1] = p->n_propagated; counts[2] = p->n_total; counts[3] = p->n_dropped;
+    *coverage = p->coverage;
+}
+
+void vfo_pipe_features(const vfo_pipe *p, double *x, double *y, double *sigma, double *theta, double *score,
+                       uint8_t *origin, int32_t *age, uint8_t *desc)
+{
+    const vfo_feats *f = &p->prev;   /* swapped in at the end of process */
+    size_t n = (size_t)f->n;
+    memcpy(x, f->x, 8 * n); memcpy(y, f->y, 8 * n); memcpy(sigma, f->sigma, 8 * n);
+    memcpy(theta, f->theta, 8 * n); memcpy(score, f->score, 8 * n);
+    memcpy(origin, f->origin, n); memcpy(age, f->age, 4 * n); memcpy(desc, f->desc, 64 * n);
+}

@@ -1,0 +1,270 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    python tests/golden/make_golden.py
+
+It copies /root/reference/pkg to a scratch dir (the mount is read-only and
+misses ``data/sampling_pattern_v1.npz``), regenerates the pattern asset with
+the reference's own ``python -m vidfeat.pattern`` code path, imports
+``vidfeat`` from there (numba path, the reference default, accel.py:33) and
+writes small ``.npz`` fixtures next to this script.  The fixtures hold the
+inputs too, so tests never need the reference at run time.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REF = Path("/root/reference/pkg")
+
+
+def import_reference():
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    os.environ.setdefault("NUMBA_CACHE_DIR", str(Path(tempfile.gettempdir()) / "vidfeat_numba_cache"))
+    sys.dont_write_bytecode = True
+    scratch = Path(tempfile.gettempdir()) / "vidfeat_ref_copy"
+    if not (scratch / "src" / "vidfeat" / "data" / "sampling_pattern_v1.npz").exists():
+        if scratch.exists():
+            shutil.rmtree(scratch)
+        shutil.copytree(REF, scratch)
+        sys.path.insert(0, str(scratch / "src"))
+        import vidfeat.pattern as vp  # noqa: E402
+
+        vp._regenerate()
+    else:
+        sys.path.insert(0, str(scratch / "src"))
+    import vidfeat  # noqa: F401
+
+    return vidfeat
+
+
+def feats_to_arrays(per_frame):
+    """list[list[Feature]] -> flat SoA + frame offsets (packed descriptors)."""
+    offs = [0]
+    cols = {k: [] for k in ("x", "y", "sigma", "theta", "score", "origin", "age", "desc")}
+    for fs in per_frame:
+        for f in fs:
+            cols["x"].append(f.kp.x)
+            cols["y"].append(f.kp.y)
+            cols["sigma"].append(f.kp.sigma)
+            cols["theta"].append(f.kp.theta)
+            cols["score"].append(f.kp.score)
+            cols["origin"].append(0 if f.origin == "detected" else 1)
+            cols["age"].append(f.age)
+            cols["desc"].append(np.packbits(f.desc))
+        offs.append(offs[-1] + len(fs))
+    out = {
+        "offsets": np.array(offs, np.int64),
+        "x": np.array(cols["x"], np.float64),
+        "y": np.array(cols["y"], np.float64),
+        "sigma": np.array(cols["sigma"], np.float64),
+        "theta": np.array(cols["theta"], np.float64),
+        "score": np.array(cols["score"], np.float64),
+        "origin": np.array(cols["origin"], np.uint8),
+        "age": np.array(cols["age"], np.int32),
+        "desc": np.array(cols["desc"], np.uint8).reshape(-1, 64),
+    }
+    return out
+
+
+def reports_to_arrays(reports):
+    return {
+        "r_n_detected": np.array([r.n_detected for r in reports], np.int64),
+        "r_n_propagated": np.array([r.n_propagated for r in reports], np.int64),
+        "r_n_total": np.array([r.n_total for r in reports], np.int64),
+        "r_n_dropped": np.array([r.n_dropped for r in reports], np.int64),
+        "r_coverage": np.array([r.coverage for r in reports], np.float64),
+    }
+
+
+def main():
+    vf = import_reference()
+    from vidfeat import detector, descriptor, masking, pattern, pipeline, pyramid, synth
+    from vidfeat.masking import MaskConfig
+    from vidfeat.pipeline import PipelineConfig, run_pipeline
+    from vidfeat.pyramid import GrayFrame
+
+    assert vf.accel.USE_NUMBA, "golden vectors come from the reference's default (numba) path"
+
+    # 1. pattern (pattern.py:49-72) -----------------------------------------
+    p = pattern.default_pattern()
+    np.savez_compressed(HERE / "pattern_v1.npz", points=p.points, radii=p.radii,
+                        short_pairs=p.short_pairs, long_pairs=p.long_pairs)
+
+    # 2. pyramid (pyramid.py:97-125) ---------------------------------------
+    rng = np.random.default_rng(12345)
+    pyr_out = {}
+    for tag, (w, h, O) in {"a": (200, 150, 4), "b": (97, 61, 3), "c": (64, 64, 4)}.items():
+        f = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        pyr = pyramid.build_pyramid(GrayFrame(f), O)
+        pyr_out[f"{tag}_frame"] = f
+        pyr_out[f"{tag}_O"] = np.array(O)
+        for i, layer in enumerate(pyr.layers):
+            pyr_out[f"{tag}_layer{i}"] = layer.frame.data
+            pyr_out[f"{tag}_scale{i}"] = np.array(layer.scale)
+    np.savez_compressed(HERE / "pyramid.npz", **pyr_out)
+
+    # 3. score maps (detector.py:107-172) incl. gating and KATs --------------
+    sm = {}
+    rng = np.random.default_rng(7)
+    k = 0
+    for trial in range(8):
+        h, w = (64, 64) if trial < 6 else (40, 71)
+        data = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        mask = (rng.random((h, w)) < 0.7).astype(np.uint8) if trial % 2 else None
+        for t in (1, 10, 30, 55, 200):
+            smap = detector._score_map(data, t, mask)
+            sm[f"data{k}"] = data
+            sm[f"mask{k}"] = np.ones((h, w), np.uint8) if mask is None else mask
+            sm[f"t{k}"] = np.array(t)
+            sm[f"score{k}"] = smap.astype(np.uint8)
+            assert smap.max() < 256
+            k += 1
+    sm["n"] = np.array(k)
+    # KATs from tests/test_detector.py:48-73 (ring patterns around (8, 8))
+    rings = [[200] * 12 + [100] * 4, [141] * 9 + [100] * 7, [141] * 8 + [100] * 8,
+             [30] * 10 + [200] * 6, [255] * 5 + [100] * 7 + [255] * 4]
+    centers = [100, 100, 100, 200, 100]
+    kat = []
+    for ring, c in zip(rings, centers):
+        d = np.full((16, 16), c, np.uint8)
+        for (dx, dy), v in zip(detector.CIRCLE, ring):
+            d[8 + dy, 8 + dx] = v
+        kat.append((d, detector.ast_corner_score(GrayFrame(d), 8, 8)))
+    sm["kat_data"] = np.stack([d for d, _ in kat])
+    sm["kat_score"] = np.array([s for _, s in kat], np.int64)
+    np.savez_compressed(HERE / "score_maps.npz", **sm)
+
+    # 4. NMS + refinement (detector.py:239-324) ----------------------------
+    nm = {}
+    rng = np.random.default_rng(99)
+    for tag, (w, h, O, t) in {"a": (128, 128, 3, 20), "b": (160, 120, 4, 30), "c": (97, 75, 2, 15)}.items():
+        f = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        pyr = pyramid.build_pyramid(GrayFrame(f), O)
+        maps = [detector._score_map(l.frame.data, t, None) for l in pyr.layers]
+        kps = detector._nms_from_maps(maps, pyr)
+        nm[f"{tag}_frame"] = f
+        nm[f"{tag}_O"] = np.array(O)
+        nm[f"{tag}_t"] = np.array(t)
+        for i, m in enumerate(maps):
+            nm[f"{tag}_map{i}"] = m.astype(np.uint8)
+        nm[f"{tag}_x"] = np.array([q.x for q in kps])
+        nm[f"{tag}_y"] = np.array([q.y for q in kps])
+        nm[f"{tag}_sigma"] = np.array([q.sigma for q in kps])
+        nm[f"{tag}_score"] = np.array([q.score for q in kps])
+    # the reference's own NMS unit cases (tests/test_detector.py:126-181)
+    pyr = pyramid.build_pyramid(GrayFrame(np.zeros((64, 64), np.uint8)), 2)
+    C = detector.Candidate
+    cases = [
+        {("octave", 0): [C(20, 24, ("octave", 0), 50)]},
+        {("octave", 0): [C(20, 24, ("octave", 0), 10), C(21, 24, ("octave", 0), 12)]},
+        {("octave", 0): [C(20, 24, ("octave", 0), 10), C(21, 24, ("octave", 0), 10)]},
+        {("octave", 0): [C(20, 24, ("octave", 0), 10)], ("intra", 0): [C(13, 16, ("intra", 0), 50)]},
+        {("intra", 1): [C(10, 10, ("intra", 1), 30)]},
+    ]
+    for ci, cands in enumerate(cases):
+        kps = detector.nms_and_refine(cands, pyr)
+        nm[f"case{ci}_cands"] = np.array(
+            [[next(i for i, l in enumerate(pyr.layers) if (l.kind, l.level) == lid), c.x, c.y, c.score]
+             for lid, cl in cands.items() for c in cl], np.int64).reshape(-1, 4)
+        nm[f"case{ci}_kps"] = np.array([[q.x, q.y, q.sigma, q.score] for q in kps]).reshape(-1, 4)
+    nm["n_cases"] = np.array(len(cases))
+    np.savez_compressed(HERE / "nms.npz", **nm)
+
+    # 5. orientation + descriptor (descriptor.py:85-232) -------------------
+    de = {}
+    rng = np.random.default_rng(2024)
+    data = rng.integers(0, 256, (96, 96), dtype=np.uint8)
+    n = 64
+    kx = rng.uniform(30, 66, n)
+    ky = rng.uniform(30, 66, n)
+    sg = rng.choice([1.0, 1.5, 2.0, 2.5], n) * rng.uniform(0.9, 1.1, n)
+    th = rng.uniform(-3.1, 3.1, n)
+    frame = GrayFrame(data)
+    kps = [detector.Keypoint(float(a), float(b), float(c)) for a, b, c in zip(kx, ky, sg)]
+    de["data"] = data
+    de["kx"], de["ky"], de["sigma"], de["theta_in"] = kx, ky, sg, th
+    de["orient"] = descriptor.orientations_batch(frame, kps, p)
+    de["desc_theta_in"] = np.packbits(descriptor.describe_batch(frame, kps, th, p), axis=1)
+    de["desc_orient"] = np.packbits(descriptor.describe_batch(frame, kps, de["orient"], p), axis=1)
+    # KATs (tests/test_descriptor.py:63-81): constant, x-ramp, y-ramp, edge
+    xs, ys = np.meshgrid(np.arange(64), np.arange(64))
+    kat_frames = [np.full((64, 64), 90, np.uint8), np.clip(xs * 3, 0, 255).astype(np.uint8),
+                  np.clip(ys * 3, 0, 255).astype(np.uint8)]
+    edge = np.full((64, 64), 50, np.uint8)
+    edge[:, :32] = 200
+    kat_frames.append(edge)
+    de["kat_frames"] = np.stack(kat_frames)
+    de["kat_orient"] = np.array([descriptor.estimate_orientation(GrayFrame(f), detector.Keypoint(32.0, 32.0, 1.0), p)
+                                 for f in kat_frames])
+    de["kat_desc"] = np.stack([np.packbits(descriptor.describe(GrayFrame(f), detector.Keypoint(32.0, 32.0, 1.0), 0.0, p))
+                               for f in kat_frames])
+    np.savez_compressed(HERE / "describe.npz", **de)
+
+    # 6. masks (masking.py:84-184) -----------------------------------------
+    mk = {}
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 256, (60, 80), dtype=np.uint8)
+    b = np.clip(a.astype(np.int16) + rng.integers(-40, 41, (60, 80)), 0, 255).astype(np.uint8)
+    mk["idm_a"], mk["idm_b"] = a, b
+    for t_i in (-1.0, 0.0, 19.5, 20.0, 30.0):
+        mk[f"idm_{t_i}"] = masking.intensity_diff_mask(GrayFrame(a), GrayFrame(b), t_i).bits
+    xs_ = np.concatenate([rng.uniform(0, 640, 300), [639.0, 0.0, 639.999999]])
+    ys_ = np.concatenate([rng.uniform(0, 480, 300), [479.0, 0.0, 479.999999]])
+    F = masking.Feature
+    feats = [F(detector.Keypoint(float(x), float(y), 1.0), np.zeros(512, np.uint8)) for x, y in zip(xs_, ys_)]
+    mk["bin_x"], mk["bin_y"] = xs_, ys_
+    mk["bin_hist_16"] = masking.binning_histogram(feats, (640, 480), (16, 16))
+    mk["bin_hist_3x5"] = masking.binning_histogram(feats, (640, 480), (3, 5))
+    bits = rng.integers(0, 2, (6, 8)).astype(np.uint8)
+    mk["up_bits"] = bits
+    mk["up_full"] = masking.upsample_mask(masking.SubsampledMask(bits, cell_w=9, cell_h=9), (70, 50)).bits
+    np.savez_compressed(HERE / "masks.npz", **mk)
+
+    # 7. whole-pipeline sequences (pipeline.py:207-278) ---------------------
+    small, _ = synth.synth_sequence(
+        synth.moving_object_scene((128, 96), object_frac=0.2, velocity=(3.0, 0.0), seed=6), 6, (128, 96), seed=6)
+    static, _ = synth.synth_sequence(synth.static_scene(seed=8), 6, (128, 96), seed=8)
+    rng = np.random.default_rng(42)
+    rnd = [GrayFrame(rng.integers(0, 256, (240, 320), dtype=np.uint8), index=i) for i in range(3)]
+    sys.path.insert(0, str(HERE.parents[1]))
+    from paper_1503_06959_b200 import scenes  # our seeded BASELINE config-1 scene generator
+
+    cfg1 = scenes.SceneConfig(320, 240, 5, 1, "objects", (3, 3), (1.0, 3.0), noise_sigma=2.0, seed=11)
+    scn = [GrayFrame(f, i) for i, f in enumerate(scenes.generate(cfg1)[0].numpy())]
+    runs = {
+        "small_none": (small, PipelineConfig(threshold=25, mask=MaskConfig(mode="none"))),
+        "small_intensity": (small, PipelineConfig(threshold=25, mask=MaskConfig(mode="intensity", t_i=15))),
+        "small_binning": (small, PipelineConfig(threshold=25, mask=MaskConfig(mode="binning", t_h=1, grid=(8, 8)))),
+        "small_perlayer": (small, PipelineConfig(threshold=25, mask=MaskConfig(mode="intensity", t_i=15, per_layer=True))),
+        "small_octave1": (small, PipelineConfig(threshold=25, n_octaves=3, mask=MaskConfig(mode="intensity", t_i=10, octave_for_mask=1))),
+        "static_intensity": (static, PipelineConfig(threshold=25, mask=MaskConfig(mode="intensity", t_i=5))),
+        "random_forced": (rnd, PipelineConfig(mask=MaskConfig(mode="intensity", t_i=-1.0))),
+        "random_none": (rnd, PipelineConfig(mask=MaskConfig(mode="none"))),
+        "scene_intensity": (scn, PipelineConfig(mask=MaskConfig(mode="intensity"))),
+        "scene_binning": (scn, PipelineConfig(mask=MaskConfig(mode="binning"))),
+    }
+    for name, (frames, cfg) in runs.items():
+        feats, reports = run_pipeline(frames, cfg)
+        mc = cfg.mask
+        np.savez_compressed(
+            HERE / f"pipeline_{name}.npz",
+            frames=np.stack([f.data for f in frames]),
+            threshold=np.array(cfg.threshold), n_octaves=np.array(cfg.n_octaves),
+            mode=np.array(mc.mode), t_i=np.array(mc.t_i), t_h=np.array(mc.t_h), grid=np.array(mc.grid),
+            octave_for_mask=np.array(-1 if mc.octave_for_mask is None else mc.octave_for_mask),
+            per_layer=np.array(mc.per_layer),
+            **feats_to_arrays(feats), **reports_to_arrays(reports))
+        print(name, [len(f) for f in feats])
+
+
+if __name__ == "__main__":
+    main()
