@@ -1,0 +1,157 @@
+/*
+ * vidfeat_b200.h -- C ABI of the B200-native detect+describe hot path.
+ *
+ * Drop-in boundary for the reference `vidfeat` 0.1.0 per-frame path
+ * (/root/reference/pkg/src/vidfeat/).  The reference has no FFI: its operator
+ * seam is the Python function layer with import-time kernel dispatch
+ * (accel.py:22-57 selects numba or numpy inside _score_map, detector.py:166-172,
+ * orientations_batch / describe_batch, descriptor.py:194-232).  These entry
+ * points replace that seam; the Python package paper_1503_06959_b200 binds
+ * them with ctypes and keeps the reference's function names and dataclasses.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  "_dev" pointers are
+ * CUDA device memory (e.g. a torch CUDA tensor's data_ptr()), "stream" is a
+ * cudaStream_t (0 = legacy default stream).  All calls return VF_OK (0) or a
+ * negative VF_ERR_* code; vf_strerror() gives the reference's exception text.
+ * Calls are asynchronous on `stream` unless documented otherwise.
+ */
+#ifndef VIDFEAT_B200_H
+#define VIDFEAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* --- status codes (each mirrors a reference ValueError / exception) -------- */
+#define VF_OK 0
+#define VF_ERR_THRESHOLD (-1)     /* "detection threshold must be >= 1"      detector.py:195-196 */
+#define VF_ERR_OCTAVES (-2)       /* "n_octaves must be >= 1"                pyramid.py:103-104  */
+#define VF_ERR_FRAME_SMALL (-3)   /* "frame WxH too small for O octaves"     pyramid.py:105-109  */
+#define VF_ERR_UNDERFLOW (-4)     /* "dimension underflow ..."               pyramid.py:70-71,83-84 */
+#define VF_ERR_MODE (-5)          /* "unknown mask mode"                     masking.py:75-77    */
+#define VF_ERR_T_H (-6)           /* "histogram threshold must be >= 0"      masking.py:78-79    */
+#define VF_ERR_GRID (-7)          /* "binning grid must be at least 1x1"     masking.py:80-81    */
+#define VF_ERR_EMPTY (-8)         /* "empty frame sequence"                  pipeline.py:211-212 */
+#define VF_ERR_CAPACITY (-9)      /* keypoint capacity overflow (no reference counterpart)      */
+#define VF_ERR_CUDA (-10)         /* CUDA runtime error                                          */
+#define VF_ERR_ARG (-11)          /* invalid argument                                            */
+#define VF_ERR_INDEX (-12)        /* numpy IndexError (nms_and_refine border candidate)          */
+#define VF_ERR_OCTAVE_KEY (-13)   /* KeyError: no octave layer at octave_for_mask (pyramid.py:61-63) */
+#define VF_ERR_PATTERN (-14)      /* sampling pattern not uploaded / malformed                   */
+
+#define VF_MODE_NONE 0
+#define VF_MODE_INTENSITY 1
+#define VF_MODE_BINNING 2
+
+/* PipelineConfig (pipeline.py:46-54) + MaskConfig (masking.py:66-81), flattened. */
+typedef struct vf_config {
+  int32_t width, height;      /* frame size (all streams of a context share it)        */
+  int32_t n_octaves;          /* PipelineConfig.n_octaves, default 4                   */
+  int32_t threshold;          /* PipelineConfig.threshold, default 55                  */
+  int32_t mask_mode;          /* VF_MODE_*; "temporal" is not part of this path        */
+  double t_i;                 /* MaskConfig.t_i, default 20.0                          */
+  int32_t t_h;                /* MaskConfig.t_h, default 1                             */
+  int32_t grid_rows, grid_cols; /* MaskConfig.grid, default (16, 16)                   */
+  int32_t octave_for_mask;    /* MaskConfig.octave_for_mask, -1 = None (top octave)    */
+  int32_t per_layer;          /* MaskConfig.per_layer                                  */
+  int32_t max_streams;        /* independent video streams processed per call          */
+  int32_t kp_capacity;        /* features per stream and frame, 0 = automatic          */
+} vf_config;
+
+/* FrameReport (pipeline.py:57-71) counts of the last processed frame. */
+typedef struct vf_report {
+  int64_t frame;
+  int32_t n_detected, n_propagated, n_total, n_dropped;
+  double coverage;
+  int32_t n_survivors;        /* NMS survivors before the border filter (diagnostic)   */
+  int32_t n_candidates;       /* FAST candidates (diagnostic)                           */
+} vf_report;
+
+/* Device pointers to a stream's current feature list (Feature, masking.py:58-63),
+ * SoA: keypoint x, y, sigma, theta, score (fp64), origin (0 detected,
+ * 1 propagated), age, and 64-byte MSB-first descriptors (descriptor.py:271-275).
+ * Valid until the next vf_process on the context. */
+typedef struct vf_features {
+  int32_t n;
+  const double *x, *y, *sigma, *theta, *score;
+  const uint8_t *origin;
+  const int32_t *age;
+  const uint8_t *desc;
+} vf_features;
+
+typedef struct vf_ctx vf_ctx;
+
+const char *vf_version(void);
+const char *vf_strerror(int code);
+
+/* Sampling pattern (pattern.py:30-46): points (m x 2), radii (m), short pairs
+ * (nbits x 2), long pairs (L x 2).  m must be 60 and nbits 512 (v1 pattern). */
+int vf_set_pattern(const double *points, const double *radii, int m, const int32_t *short_pairs,
+                   int nbits, const int32_t *long_pairs, int L);
+
+/* --- the per-frame pipeline: run_pipeline's loop body (pipeline.py:222-277) -- */
+int vf_create(const vf_config *cfg, vf_ctx **out);
+int vf_destroy(vf_ctx *ctx);
+/* Geometry of the pyramid (layer order o0, i0, o1, ...): sizes and scales. */
+int vf_layer_geometry(const vf_ctx *ctx, int32_t *ws, int32_t *hs, double *scales);
+/* Forget all temporal state (next frame is "frame 0" on every stream). */
+int vf_reset(vf_ctx *ctx, void *stream);
+/* Process frame n of streams [0, n_streams): frames_dev + s*stream_stride is
+ * stream s's (height x width) uint8 frame with row pitch `row_pitch`. */
+int vf_process(vf_ctx *ctx, const uint8_t *frames_dev, int64_t stream_stride, int64_t row_pitch,
+               int n_streams, void *stream);
+/* Same, from pinned or pageable HOST memory: the host->device copy is part of
+ * the call (double-buffered device staging, stream-ordered). */
+int vf_process_host(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,
+                    int n_streams, void *stream);
+/* Synchronizes `stream`, then reports the last processed frame of `s`.
+ * Returns VF_ERR_CAPACITY if a capacity overflow was flagged on the device. */
+int vf_get_report(vf_ctx *ctx, int s, vf_report *out, void *stream);
+/* Synchronizes `stream`; device pointers of stream s's current features. */
+int vf_get_features(vf_ctx *ctx, int s, vf_features *out, void *stream);
+/* Synchronizes `stream`; copies stream s's features to host arrays of >= cap entries. */
+int vf_copy_features(vf_ctx *ctx, int s, int32_t cap, double *x, double *y, double *sigma, double *theta,
+                     double *score, uint8_t *origin, int32_t *age, uint8_t *desc, int32_t *n_out, void *stream);
+/* Device pointers of layer l of stream s's current pyramid (l >= 1; l = 0 is the input frame). */
+int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch);
+/* Per-stream totals since vf_create/vf_reset: sum n_detected, sum n_total, sum coverage, frames. */
+int vf_get_totals(vf_ctx *ctx, int s, double *out4, void *stream);
+
+/* --- per-stage drop-ins (same device code as the pipeline) ------------------- */
+/* build_pyramid (pyramid.py:97-125): writes layers 1..2O-1 to layers_dev[l] with pitches[l]. */
+int vf_build_pyramid(const uint8_t *frame_dev, int W, int H, int64_t pitch, int n_octaves,
+                     uint8_t *const *layers_dev, const int64_t *pitches, void *stream);
+/* _score_map / detect_candidates (detector.py:166-204): uint8 scores (0 or >= t) of
+ * one layer, gated by an optional full-res mask (mask_dev, mw x mh, floor mapping). */
+int vf_score_map(const uint8_t *layer_dev, int w, int h, int64_t pitch, int t, const uint8_t *mask_dev,
+                 int mw, int mh, uint8_t *scores_dev, int64_t scores_pitch, void *stream);
+/* nms_and_refine / _nms_from_maps (detector.py:239-324) over caller score maps
+ * (uint8, layer geometry of a W x H frame with n_octaves).  Outputs in
+ * reference order; *n_out = count (synchronizes). */
+int vf_nms_refine(const uint8_t *const *maps_dev, const int64_t *pitches, int W, int H, int n_octaves,
+                  int32_t cap, double *x_dev, double *y_dev, double *sigma_dev, double *score_dev,
+                  int32_t *n_out, void *stream);
+/* orientations_batch (theta_in_dev == NULL) or describe_batch at theta_in_dev
+ * (descriptor.py:194-232) on a full-res frame; desc_dev gets n x 64 packed bytes. */
+int vf_describe(const uint8_t *frame_dev, int W, int H, int64_t pitch, int n, const double *kx_dev,
+                const double *ky_dev, const double *sigma_dev, const double *theta_in_dev,
+                double *theta_out_dev, uint8_t *desc_dev, void *stream);
+/* intensity_diff_mask (masking.py:84-93) over n pixels. */
+int vf_intensity_mask(const uint8_t *prev_dev, const uint8_t *cur_dev, int64_t n, double t_i,
+                      uint8_t *out_dev, void *stream);
+/* binning_histogram (masking.py:96-119): hist_dev (rows x cols) uint64, zeroed by the call. */
+int vf_binning_histogram(int n, const double *xs_dev, const double *ys_dev, int W, int H, int rows,
+                         int cols, uint64_t *hist_dev, void *stream);
+/* upsample_mask (masking.py:139-148). */
+int vf_upsample_mask(const uint8_t *bits_dev, int rows, int cols, int cell_w, int cell_h, int W, int H,
+                     uint8_t *full_dev, void *stream);
+/* _mask_values (masking.py:157-165): mask bit under each rounded, clamped position. */
+int vf_mask_values(const uint8_t *full_dev, int W, int H, int n, const double *xs_dev,
+                   const double *ys_dev, uint8_t *out_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VIDFEAT_B200_H */

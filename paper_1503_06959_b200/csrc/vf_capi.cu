@@ -1,0 +1,698 @@
+// vf_capi.cu -- C ABI (include/vidfeat_b200.h): contexts, HBM layout, launches.
+//
+// Single translation unit: includes the kernels.  Built by
+// paper_1503_06959_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
+#include "vf_kernels.cu"
+#include "../../include/vidfeat_b200.h"
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+#define VF_VERSION "vidfeat-b200 0.1.0 (sm_100a)"
+
+namespace {
+
+int g_pattern_ok = 0;
+
+struct Alloc {
+  std::vector<void*> ptrs;
+  cudaError_t err = cudaSuccess;
+  template <typename T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) { err = e; return nullptr; }
+    cudaMemset(p, 0, n * sizeof(T));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+inline long long align_up(long long v, long long a) { return (v + a - 1) / a * a; }
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// pyramid.py:97-125 geometry (+ validation in the reference's order)
+int layer_dims(int W, int H, int O, int* ws, int* hs, double* scales)
+{
+  if (O < 1) return VF_ERR_OCTAVES;
+  if (O > VF_MAXO) return VF_ERR_ARG;
+  int need = 1 << (O - 1);
+  if (W < need || H < need) return VF_ERR_FRAME_SMALL;
+  int ow = W, oh = H, iw = (2 * W) / 3, ih = (2 * H) / 3;
+  if (iw < 1 || ih < 1) return VF_ERR_UNDERFLOW;
+  for (int o = 0; o < O; o++) {
+    if (o > 0) {
+      ow /= 2; oh /= 2; iw /= 2; ih /= 2;
+      if (ow < 1 || oh < 1 || iw < 1 || ih < 1) return VF_ERR_UNDERFLOW;
+    }
+    ws[2 * o] = ow; hs[2 * o] = oh; ws[2 * o + 1] = iw; hs[2 * o + 1] = ih;
+    double sc = ldexp(1.0, -o);
+    scales[2 * o] = sc;
+    scales[2 * o + 1] = sc / 1.5;
+  }
+  return VF_OK;
+}
+
+// Fill Geo for a frame size and config.  lut is filled on the host.
+int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
+{
+  memset(&g, 0, sizeof(g));
+  if (c.threshold < 1) return VF_ERR_THRESHOLD;
+  if (c.mask_mode < 0 || c.mask_mode > 2) return VF_ERR_MODE;
+  if (c.t_h < 0) return VF_ERR_T_H;
+  if (c.grid_rows < 1 || c.grid_cols < 1) return VF_ERR_GRID;
+  int ws[VF_MAXL], hs[VF_MAXL];
+  double sc[VF_MAXL];
+  int rc = layer_dims(c.width, c.height, c.n_octaves, ws, hs, sc);
+  if (rc) return rc;
+  g.W = c.width; g.H = c.height; g.O = c.n_octaves; g.NL = 2 * c.n_octaves;
+  g.threshold = c.threshold;
+  g.mask_mode = c.mask_mode;
+  g.per_layer = c.mask_mode == 1 ? c.per_layer : 0;
+  g.mask_level = c.octave_for_mask < 0 ? g.O - 1 : c.octave_for_mask;
+  if (c.mask_mode == 1 && (g.mask_level < 0 || g.mask_level >= g.O)) return VF_ERR_OCTAVE_KEY;
+  g.t_i = c.t_i; g.t_h = c.t_h;
+  long long lay = 0, smo = 0, bmo = 0;
+  int tb = 0, bb = 0;
+  for (int l = 0; l < g.NL; l++) {
+    LayerGeo& L = g.L[l];
+    L.w = ws[l]; L.h = hs[l];
+    L.pitch = (int)align_up(L.w, 16);
+    L.scale = sc[l];
+    L.sigma = 1.0 / sc[l];
+    L.tiles_x = cdiv(L.w, VF_TILE_W); L.tiles_y = cdiv(L.h, VF_TILE_H);
+    L.tile_base = tb; tb += L.tiles_x * L.tiles_y;
+    L.band_base = bb; bb += L.tiles_y;
+    L.bm_words = cdiv(L.w, 32);
+    if (l >= 1) { L.layer_off = lay; lay += align_up((long long)L.pitch * L.h, 256); }
+    L.sm_off = smo; smo += align_up((long long)L.pitch * L.h + 16, 256);
+    L.bm_off = bmo; bmo += align_up((long long)L.bm_words * L.h, 64);
+  }
+  g.tiles_per_stream = tb; g.bands_per_stream = bb;
+  g.layer_slab = std::max(lay, 256LL); g.sm_slab = smo; g.bm_slab_words = bmo;
+  // mask grids (masking.py:139-148 cell geometry; binning masking.py:132-136)
+  long long co = 0;
+  if (g.mask_mode == 1) {
+    int lv0 = g.per_layer ? 0 : g.mask_level, lv1 = g.per_layer ? g.O - 1 : g.mask_level;
+    for (int lv = lv0; lv <= lv1; lv++) {
+      GridGeo& G = g.grid[g.n_grids++];
+      G.rows = hs[2 * lv]; G.cols = ws[2 * lv];
+      G.cw = cdiv(g.W, G.cols); G.ch = cdiv(g.H, G.rows);
+      G.cell_off = co; co += align_up((long long)G.rows * G.cols, 64);
+    }
+  } else if (g.mask_mode == 2) {
+    GridGeo& G = g.grid[g.n_grids++];
+    G.rows = c.grid_rows; G.cols = c.grid_cols;
+    G.cw = cdiv(g.W, G.cols); G.ch = cdiv(g.H, G.rows);
+    G.cell_off = co; co += align_up((long long)G.rows * G.cols, 64);
+    if ((long long)G.rows * G.cols * 4 > 200 * 1024) return VF_ERR_GRID;
+  }
+  g.cell_slab = std::max(co, 64LL);
+  // row/col -> cell LUTs per layer (detector.py:175-181 floor mapping, then // cell)
+  lut.clear();
+  for (int l = 0; l < g.NL; l++) {
+    LayerGeo& L = g.L[l];
+    L.rc_off = (int)lut.size();
+    L.cc_off = L.rc_off + L.h;
+    if (g.n_grids == 0) { lut.resize(lut.size() + L.h + L.w, 0); continue; }
+    const GridGeo& G = g.grid[g.per_layer ? (l >> 1) : 0];
+    for (int y = 0; y < L.h; y++) lut.push_back((int)(((long long)y * g.H / L.h) / G.ch));
+    for (int x = 0; x < L.w; x++) lut.push_back((int)(((long long)x * g.W / L.w) / G.cw));
+  }
+  g.lut_len = (long long)lut.size();
+  // IDDM state (previous frame's mask-source octave levels)
+  long long so = 0;
+  if (g.mask_mode == 1) {
+    int lv0 = g.per_layer ? 0 : g.mask_level, lv1 = g.per_layer ? g.O - 1 : g.mask_level;
+    for (int lv = lv0; lv <= lv1; lv++) { g.state_off[lv] = so; so += align_up((long long)ws[2 * lv] * hs[2 * lv], 64); }
+  }
+  g.state_slab = std::max(so, 64LL);
+  // pyramid / SAT tiles: multiples of 3 * 2^(O-1)
+  const int unit = 3 << (g.O - 1);
+  g.ptw = unit * std::max(1, 96 / unit);
+  g.pth = unit * std::max(1, 48 / unit);
+  g.ptx = cdiv(g.W, g.ptw); g.pty = cdiv(g.H, g.pth);
+  long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
+  g.kp_cap = (int)std::min(cap, 1LL << 28);
+  g.prop_chunks = cdiv(g.kp_cap, 1024);
+  return VF_OK;
+}
+
+int pyramid_smem(const Geo& g)
+{
+  int acc = 0;
+  for (int l = 0; l < g.NL; l++) {
+    int lw, lh, o = l >> 1;
+    if (l & 1) { lw = (2 * g.ptw / 3) >> o; lh = (2 * g.pth / 3) >> o; }
+    else { lw = g.ptw >> o; lh = g.pth >> o; }
+    acc += (lw * lh + 15) & ~15;
+  }
+  return acc + g.ptw * g.pth * 4;
+}
+
+int g_num_sms = 0;
+
+int cuda_status(cudaError_t e)
+{
+  if (e == cudaSuccess) return VF_OK;
+  fprintf(stderr, "vidfeat_b200: CUDA error %s\n", cudaGetErrorString(e));
+  return VF_ERR_CUDA;
+}
+
+}  // namespace
+
+struct vf_ctx {
+  vf_config cfg;
+  Geo g;
+  Bufs b;
+  Alloc mem;
+  int S;
+  std::vector<long long> frames_done;   // host mirror of per-stream frame counters
+  int pyr_smem;
+  int fast_grid;
+  // host-input staging (vf_process_host)
+  uint8_t* hstage[2] = {nullptr, nullptr};
+  long long hstage_bytes = 0;
+  int hstage_k = 0;
+  cudaEvent_t hstage_free[2] = {nullptr, nullptr};
+};
+
+extern "C" {
+
+const char* vf_version(void) { return VF_VERSION; }
+
+const char* vf_strerror(int code)
+{
+  switch (code) {
+    case VF_OK: return "ok";
+    case VF_ERR_THRESHOLD: return "detection threshold must be >= 1";
+    case VF_ERR_OCTAVES: return "n_octaves must be >= 1";
+    case VF_ERR_FRAME_SMALL: return "frame too small for the requested octaves";
+    case VF_ERR_UNDERFLOW: return "dimension underflow while building the pyramid";
+    case VF_ERR_MODE: return "unknown mask mode";
+    case VF_ERR_T_H: return "histogram threshold must be >= 0";
+    case VF_ERR_GRID: return "binning grid must be at least 1x1";
+    case VF_ERR_EMPTY: return "empty frame sequence";
+    case VF_ERR_CAPACITY: return "keypoint capacity exceeded";
+    case VF_ERR_CUDA: return "CUDA runtime error";
+    case VF_ERR_ARG: return "invalid argument";
+    case VF_ERR_INDEX: return "index out of bounds";
+    case VF_ERR_OCTAVE_KEY: return "no octave layer at octave_for_mask";
+    case VF_ERR_PATTERN: return "sampling pattern not set or malformed";
+    default: return "unknown error";
+  }
+}
+
+int vf_set_pattern(const double* points, const double* radii, int m, const int32_t* short_pairs, int nbits,
+                   const int32_t* long_pairs, int L)
+{
+  if (m != VF_NPTS || nbits != VF_NBITS || L < 1 || L > VF_MAXLONG) return VF_ERR_PATTERN;
+  double px[VF_NPTS], py[VF_NPTS];
+  short si[VF_NBITS], sj[VF_NBITS], li[VF_MAXLONG], lj[VF_MAXLONG];
+  double wx[VF_MAXLONG], wy[VF_MAXLONG];
+  for (int j = 0; j < m; j++) { px[j] = points[2 * j]; py[j] = points[2 * j + 1]; }
+  for (int k = 0; k < nbits; k++) {
+    if (short_pairs[2 * k] < 0 || short_pairs[2 * k] >= m || short_pairs[2 * k + 1] < 0 || short_pairs[2 * k + 1] >= m)
+      return VF_ERR_PATTERN;
+    si[k] = (short)short_pairs[2 * k]; sj[k] = (short)short_pairs[2 * k + 1];
+  }
+  for (int p = 0; p < L; p++) {
+    int a = long_pairs[2 * p], c = long_pairs[2 * p + 1];
+    if (a < 0 || a >= m || c < 0 || c >= m) return VF_ERR_PATTERN;
+    li[p] = (short)a; lj[p] = (short)c;
+    // descriptor.py:169-177 _pair_arrays: dp * (1 / |dp|^2), evaluated as numpy does
+    double dx = points[2 * a] - points[2 * c], dy = points[2 * a + 1] - points[2 * c + 1];
+    volatile double d2 = dx * dx;
+    d2 = d2 + dy * dy;
+    double inv = 1.0 / d2;
+    wx[p] = dx * inv; wy[p] = dy * inv;
+  }
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMemcpyToSymbol(c_px, px, sizeof(px));
+  e = e ? e : cudaMemcpyToSymbol(c_py, py, sizeof(py));
+  e = e ? e : cudaMemcpyToSymbol(c_rad, radii, sizeof(double) * m);
+  e = e ? e : cudaMemcpyToSymbol(c_si, si, sizeof(si));
+  e = e ? e : cudaMemcpyToSymbol(c_sj, sj, sizeof(sj));
+  e = e ? e : cudaMemcpyToSymbol(c_li, li, sizeof(short) * L);
+  e = e ? e : cudaMemcpyToSymbol(c_lj, lj, sizeof(short) * L);
+  e = e ? e : cudaMemcpyToSymbol(c_wx, wx, sizeof(double) * L);
+  e = e ? e : cudaMemcpyToSymbol(c_wy, wy, sizeof(double) * L);
+  e = e ? e : cudaMemcpyToSymbol(c_nlong, &L, sizeof(int));
+  if (e != cudaSuccess) return cuda_status(e);
+  g_pattern_ok = 1;
+  return VF_OK;
+}
+
+int vf_create(const vf_config* cfg, vf_ctx** out)
+{
+  if (!cfg || !out) return VF_ERR_ARG;
+  *out = nullptr;
+  if (cfg->max_streams < 1) return VF_ERR_ARG;
+  vf_ctx* c = new vf_ctx();
+  c->cfg = *cfg;
+  std::vector<int> lut;
+  int rc = make_geo(*cfg, c->g, lut);
+  if (rc) { delete c; return rc; }
+  const Geo& g = c->g;
+  const int S = c->S = cfg->max_streams;
+  Alloc& A = c->mem;
+  Bufs& b = c->b;
+  memset(&b, 0, sizeof(b));
+  const long long cap = g.kp_cap;
+  b.layers = A.get<uint8_t>((size_t)S * g.layer_slab);
+  b.scores = A.get<uint8_t>((size_t)S * g.sm_slab);
+  b.bitmaps = A.get<uint32_t>((size_t)S * g.bm_slab_words);
+  b.tile_stamp = A.get<int>((size_t)S * g.tiles_per_stream);
+  b.band_stamp = A.get<int>((size_t)S * g.bands_per_stream);
+  b.band_rec = A.get<int>((size_t)S * g.bands_per_stream * 4);
+  b.band_out = A.get<int>((size_t)S * g.bands_per_stream);
+  b.prop_cnt = A.get<int>((size_t)S * g.prop_chunks);
+  b.prop_out = A.get<int>((size_t)S * g.prop_chunks);
+  b.cells = A.get<uint8_t>((size_t)S * g.cell_slab);
+  b.state = A.get<uint8_t>((size_t)S * g.state_slab);
+  int* dl = A.get<int>((size_t)g.lut_len);
+  b.lut = dl;
+  b.sat = A.get<uint32_t>((size_t)S * g.W * g.H);
+  b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
+  b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
+  b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
+  b.fs = A.get<double>((size_t)S * 2 * cap); b.ft = A.get<double>((size_t)S * 2 * cap);
+  b.fv = A.get<double>((size_t)S * 2 * cap);
+  b.forg = A.get<uint8_t>((size_t)S * 2 * cap);
+  b.fage = A.get<int>((size_t)S * 2 * cap);
+  b.fdesc = A.get<uint8_t>((size_t)S * 2 * cap * 64);
+  b.ctr = A.get<int>((size_t)S * C_NCTR);
+  b.cov = A.get<unsigned long long>((size_t)S);
+  b.report = A.get<double>((size_t)S * 16);
+  b.worklist = A.get<int>((size_t)S * g.tiles_per_stream);
+  b.work_count = A.get<int>(1);
+  b.epoch = A.get<int>(1);
+  if (A.err != cudaSuccess) { int r = cuda_status(A.err); A.release(); delete c; return r; }
+  cudaError_t e = cudaMemcpy(dl, lut.data(), sizeof(int) * lut.size(), cudaMemcpyHostToDevice);
+  int one = 1;
+  if (e == cudaSuccess) e = cudaMemcpy(b.epoch, &one, sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { int r = cuda_status(e); A.release(); delete c; return r; }
+  c->frames_done.assign(S, 0);
+  c->pyr_smem = pyramid_smem(g);
+  if (c->pyr_smem > 48 * 1024)
+    cudaFuncSetAttribute(k_pyramid, cudaFuncAttributeMaxDynamicSharedMemorySize, c->pyr_smem);
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, 128, 0);
+  c->fast_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  *out = c;
+  return VF_OK;
+}
+
+int vf_destroy(vf_ctx* c)
+{
+  if (!c) return VF_OK;
+  for (int k = 0; k < 2; k++) {
+    if (c->hstage[k]) cudaFree(c->hstage[k]);
+    if (c->hstage_free[k]) cudaEventDestroy(c->hstage_free[k]);
+  }
+  c->mem.release();
+  delete c;
+  return VF_OK;
+}
+
+int vf_layer_geometry(const vf_ctx* c, int32_t* ws, int32_t* hs, double* scales)
+{
+  if (!c) return VF_ERR_ARG;
+  for (int l = 0; l < c->g.NL; l++) {
+    if (ws) ws[l] = c->g.L[l].w;
+    if (hs) hs[l] = c->g.L[l].h;
+    if (scales) scales[l] = c->g.L[l].scale;
+  }
+  return VF_OK;
+}
+
+int vf_reset(vf_ctx* c, void* stream)
+{
+  if (!c) return VF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(c->b.ctr, 0, sizeof(int) * c->S * C_NCTR, st);
+  cudaMemsetAsync(c->b.cov, 0, sizeof(unsigned long long) * c->S, st);
+  cudaMemsetAsync(c->b.report, 0, sizeof(double) * c->S * 16, st);
+  std::fill(c->frames_done.begin(), c->frames_done.end(), 0);
+  return cuda_status(cudaGetLastError());
+}
+
+static int launch_step(vf_ctx* c, int n, cudaStream_t st)
+{
+  const Geo& g = c->g;
+  Bufs b = c->b;
+  if (g.mask_mode == 2) {
+    int smem = g.grid[0].rows * g.grid[0].cols * 4;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_binmask, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_binmask<<<n, 1024, smem, st>>>(g, b);
+  }
+  k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
+  const int tile_ctas = cdiv(g.tiles_per_stream, 8);
+  const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
+  k_worklist<<<dim3(tile_ctas + cov_ctas, n), 256, 0, st>>>(g, b, tile_ctas);
+  k_fast<<<c->fast_grid, 128, 0, st>>>(g, b);
+  k_nms<<<dim3(g.bands_per_stream + g.prop_chunks, n), NMS_THREADS, 0, st>>>(g, b);
+  k_describe<<<dim3(g.bands_per_stream + g.prop_chunks, n), DS_THREADS, 0, st>>>(g, b);
+  k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
+  for (int s = 0; s < n; s++) c->frames_done[s]++;
+  return cuda_status(cudaGetLastError());
+}
+
+int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n_streams,
+               void* stream)
+{
+  if (!c || !frames_dev || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
+  if (!g_pattern_ok) return VF_ERR_PATTERN;
+  c->b.frames = frames_dev;
+  c->b.frame_stride = stream_stride;
+  c->b.frame_pitch = row_pitch;
+  return launch_step(c, n_streams, (cudaStream_t)stream);
+}
+
+int vf_process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch, int n_streams,
+                    void* stream)
+{
+  if (!c || !frames_host || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long fbytes = (long long)c->g.W * c->g.H;
+  if (c->hstage_bytes < fbytes * c->S) {
+    for (int k = 0; k < 2; k++) {
+      if (c->hstage[k]) cudaFree(c->hstage[k]);
+      cudaError_t e = cudaMalloc(&c->hstage[k], fbytes * c->S);
+      if (e != cudaSuccess) return cuda_status(e);
+      if (!c->hstage_free[k]) cudaEventCreateWithFlags(&c->hstage_free[k], cudaEventDisableTiming);
+    }
+    c->hstage_bytes = fbytes * c->S;
+  }
+  const int k = c->hstage_k;
+  c->hstage_k ^= 1;
+  uint8_t* dst = c->hstage[k];
+  cudaError_t e;
+  if (row_pitch == c->g.W && stream_stride == fbytes) {
+    e = cudaMemcpyAsync(dst, frames_host, fbytes * n_streams, cudaMemcpyHostToDevice, st);
+  } else {
+    e = cudaSuccess;
+    for (int s = 0; s < n_streams && e == cudaSuccess; s++)
+      e = cudaMemcpy2DAsync(dst + s * fbytes, c->g.W, frames_host + s * stream_stride, row_pitch, c->g.W, c->g.H,
+                            cudaMemcpyHostToDevice, st);
+  }
+  if (e != cudaSuccess) return cuda_status(e);
+  return vf_process(c, dst, fbytes, c->g.W, n_streams, stream);
+}
+
+int vf_get_report(vf_ctx* c, int s, vf_report* out, void* stream)
+{
+  if (!c || !out || s < 0 || s >= c->S) return VF_ERR_ARG;
+  double rp[16];
+  int ctr[C_NCTR];
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(rp, c->b.report + (long long)s * 16, sizeof(rp), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(ctr, c->b.ctr + (long long)s * C_NCTR, sizeof(ctr), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  out->n_detected = (int32_t)rp[0]; out->n_propagated = (int32_t)rp[1]; out->n_total = (int32_t)rp[2];
+  out->n_dropped = (int32_t)rp[3]; out->coverage = rp[4]; out->frame = (int64_t)rp[5];
+  out->n_survivors = (int32_t)rp[6]; out->n_candidates = (int32_t)rp[7];
+  if (ctr[C_ERR]) return VF_ERR_CAPACITY;
+  return VF_OK;
+}
+
+int vf_get_totals(vf_ctx* c, int s, double* out4, void* stream)
+{
+  if (!c || !out4 || s < 0 || s >= c->S) return VF_ERR_ARG;
+  double rp[16];
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(rp, c->b.report + (long long)s * 16, sizeof(rp), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  for (int k = 0; k < 4; k++) out4[k] = rp[8 + k];
+  return VF_OK;
+}
+
+int vf_get_features(vf_ctx* c, int s, vf_features* out, void* stream)
+{
+  if (!c || !out || s < 0 || s >= c->S) return VF_ERR_ARG;
+  if (c->frames_done[s] == 0) { memset(out, 0, sizeof(*out)); return VF_OK; }
+  int ctr[C_NCTR];
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(ctr, c->b.ctr + (long long)s * C_NCTR, sizeof(ctr), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  const int buf = (int)((c->frames_done[s] - 1) & 1);
+  const long long o = ((long long)s * 2 + buf) * c->g.kp_cap;
+  out->n = ctr[C_NFEAT0 + buf];
+  out->x = c->b.fx + o; out->y = c->b.fy + o; out->sigma = c->b.fs + o; out->theta = c->b.ft + o;
+  out->score = c->b.fv + o; out->origin = c->b.forg + o; out->age = c->b.fage + o; out->desc = c->b.fdesc + o * 64;
+  if (ctr[C_ERR]) return VF_ERR_CAPACITY;
+  return VF_OK;
+}
+
+int vf_copy_features(vf_ctx* c, int s, int32_t cap, double* x, double* y, double* sigma, double* theta, double* score,
+                     uint8_t* origin, int32_t* age, uint8_t* desc, int32_t* n_out, void* stream)
+{
+  vf_features f;
+  int rc = vf_get_features(c, s, &f, stream);
+  if (rc) return rc;
+  if (n_out) *n_out = f.n;
+  if (f.n > cap) return VF_ERR_CAPACITY;
+  if (f.n == 0) return VF_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = (size_t)f.n;
+  if (x) cudaMemcpyAsync(x, f.x, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (y) cudaMemcpyAsync(y, f.y, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (sigma) cudaMemcpyAsync(sigma, f.sigma, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (theta) cudaMemcpyAsync(theta, f.theta, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (score) cudaMemcpyAsync(score, f.score, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (origin) cudaMemcpyAsync(origin, f.origin, n, cudaMemcpyDeviceToHost, st);
+  if (age) cudaMemcpyAsync(age, f.age, 4 * n, cudaMemcpyDeviceToHost, st);
+  if (desc) cudaMemcpyAsync(desc, f.desc, 64 * n, cudaMemcpyDeviceToHost, st);
+  return cuda_status(cudaStreamSynchronize(st));
+}
+
+int vf_get_layer(vf_ctx* c, int s, int l, const uint8_t** ptr, int32_t* pitch)
+{
+  if (!c || s < 0 || s >= c->S || l < 1 || l >= c->g.NL || !ptr) return VF_ERR_ARG;
+  *ptr = c->b.layers + (long long)s * c->g.layer_slab + c->g.L[l].layer_off;
+  if (pitch) *pitch = c->g.L[l].pitch;
+  return VF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// per-stage drop-ins
+// ---------------------------------------------------------------------------
+namespace {
+struct Scratch {          // transient context for a stand-alone stage call
+  vf_ctx* c = nullptr;
+  ~Scratch() { if (c) vf_destroy(c); }
+};
+
+int stage_ctx(int W, int H, int O, int threshold, int kp_cap, Scratch& sc)
+{
+  vf_config cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.width = W; cfg.height = H; cfg.n_octaves = O; cfg.threshold = threshold < 1 ? 1 : threshold;
+  cfg.mask_mode = 0; cfg.t_i = 20.0; cfg.t_h = 1; cfg.grid_rows = 16; cfg.grid_cols = 16;
+  cfg.octave_for_mask = -1; cfg.max_streams = 1; cfg.kp_capacity = kp_cap;
+  return vf_create(&cfg, &sc.c);
+}
+}  // namespace
+
+int vf_build_pyramid(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n_octaves, uint8_t* const* layers_dev,
+                     const int64_t* pitches, void* stream)
+{
+  if (!frame_dev || !layers_dev || !pitches || pitch < W) return VF_ERR_ARG;
+  Scratch sc;
+  int rc = stage_ctx(W, H, n_octaves, 1, 4096, sc);
+  if (rc) return rc;
+  vf_ctx* c = sc.c;
+  cudaStream_t st = (cudaStream_t)stream;
+  Bufs b = c->b;
+  b.frames = frame_dev; b.frame_stride = 0; b.frame_pitch = pitch;
+  k_pyramid<<<dim3(c->g.ptx, c->g.pty, 1), 256, c->pyr_smem, st>>>(c->g, b);
+  for (int l = 1; l < c->g.NL; l++) {
+    const LayerGeo& L = c->g.L[l];
+    cudaMemcpy2DAsync(layers_dev[l], pitches[l], b.layers + L.layer_off, L.pitch, L.w, L.h, cudaMemcpyDeviceToDevice, st);
+  }
+  return cuda_status(cudaStreamSynchronize(st));
+}
+
+int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, const uint8_t* mask_dev, int mw, int mh,
+                 uint8_t* scores_dev, int64_t scores_pitch, void* stream)
+{
+  if (t < 1) return VF_ERR_THRESHOLD;
+  if (!layer_dev || !scores_dev || w < 1 || h < 1 || pitch < w || scores_pitch < w) return VF_ERR_ARG;
+  // One layer treated as "o0" of a single-octave geometry; the gate is the
+  // caller's full-res mask as a 1x1-cell grid (detector.py:175-181).
+  vf_ctx* c = new vf_ctx();
+  Geo& g = c->g;
+  memset(&g, 0, sizeof(g));
+  g.W = mask_dev ? mw : w; g.H = mask_dev ? mh : h; g.O = 1; g.NL = 1; g.threshold = t;
+  LayerGeo& L = g.L[0];
+  L.w = w; L.h = h; L.pitch = (int)align_up(w, 16); L.scale = 1.0; L.sigma = 1.0;
+  L.tiles_x = cdiv(w, VF_TILE_W); L.tiles_y = cdiv(h, VF_TILE_H); L.bm_words = cdiv(w, 32);
+  g.tiles_per_stream = L.tiles_x * L.tiles_y; g.bands_per_stream = L.tiles_y;
+  g.sm_slab = align_up((long long)L.pitch * h + 16, 256); g.bm_slab_words = (long long)L.bm_words * h;
+  std::vector<int> lut;
+  if (mask_dev) {
+    g.mask_mode = 1; g.n_grids = 1;
+    g.grid[0].rows = mh; g.grid[0].cols = mw; g.grid[0].cw = 1; g.grid[0].ch = 1; g.grid[0].cell_off = 0;
+    for (int y = 0; y < h; y++) lut.push_back((int)((long long)y * mh / h));
+    for (int x = 0; x < w; x++) lut.push_back((int)((long long)x * mw / w));
+  } else {
+    lut.assign(h + w, 0);
+  }
+  L.rc_off = 0; L.cc_off = h;
+  Alloc& A = c->mem;
+  Bufs& b = c->b;
+  memset(&b, 0, sizeof(b));
+  b.frames = layer_dev; b.frame_pitch = pitch; b.frame_stride = 0;
+  b.scores = A.get<uint8_t>(g.sm_slab);
+  b.bitmaps = A.get<uint32_t>(g.bm_slab_words);
+  b.tile_stamp = A.get<int>(g.tiles_per_stream);
+  b.band_stamp = A.get<int>(g.bands_per_stream);
+  int* dl = A.get<int>(lut.size());
+  b.lut = dl;
+  b.cells = const_cast<uint8_t*>(mask_dev);
+  b.ctr = A.get<int>(C_NCTR);
+  b.worklist = A.get<int>(g.tiles_per_stream);
+  b.work_count = A.get<int>(1);
+  if (A.err != cudaSuccess) { int r = cuda_status(A.err); A.release(); delete c; return r; }
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int> wl(g.tiles_per_stream);
+  for (int i = 0; i < g.tiles_per_stream; i++) wl[i] = i;
+  int nwl = g.tiles_per_stream;
+  int frame1[C_NCTR] = {0};
+  frame1[C_FRAME] = mask_dev ? 1 : 0;    // use_mask() on when a mask is given
+  cudaMemcpyAsync(dl, lut.data(), sizeof(int) * lut.size(), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b.worklist, wl.data(), sizeof(int) * nwl, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b.work_count, &nwl, sizeof(int), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b.ctr, frame1, sizeof(frame1), cudaMemcpyHostToDevice, st);
+  k_fast<<<std::max(1, std::min(nwl, 148 * 8)), 128, 0, st>>>(g, b);
+  cudaMemcpy2DAsync(scores_dev, scores_pitch, b.scores, L.pitch, w, h, cudaMemcpyDeviceToDevice, st);
+  int rc = cuda_status(cudaStreamSynchronize(st));
+  A.release();
+  delete c;
+  return rc;
+}
+
+__global__ void k_gather_kps(const __grid_constant__ Geo g, const __grid_constant__ Bufs b, double* x, double* y,
+                             double* s, double* v, int cap)
+{
+  const int bid = blockIdx.x;
+  const int* rec = b.band_rec + bid * 4;
+  const int kept = rec[1], base = rec[0], o = b.band_out[bid];
+  for (int i = threadIdx.x; i < kept; i += blockDim.x) {
+    if (o + i >= cap) break;
+    x[o + i] = b.st_x[base + i]; y[o + i] = b.st_y[base + i]; s[o + i] = b.st_s[base + i]; v[o + i] = b.st_v[base + i];
+  }
+}
+
+int vf_nms_refine(const uint8_t* const* maps_dev, const int64_t* pitches, int W, int H, int n_octaves, int32_t cap,
+                  double* x_dev, double* y_dev, double* sigma_dev, double* score_dev, int32_t* n_out, void* stream)
+{
+  if (!maps_dev || !pitches || !n_out) return VF_ERR_ARG;
+  Scratch sc;
+  int rc = stage_ctx(W, H, n_octaves, 1, std::max(cap, 1024), sc);
+  if (rc) return rc;
+  vf_ctx* c = sc.c;
+  Geo g = c->g;
+  g.nms_raw = 1; g.nms_wrap = 1;
+  g.prop_chunks = 0;
+  Bufs b = c->b;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int l = 0; l < g.NL; l++)
+    cudaMemcpy2DAsync(b.scores + g.L[l].sm_off, g.L[l].pitch, maps_dev[l], pitches[l], g.L[l].w, g.L[l].h,
+                      cudaMemcpyDeviceToDevice, st);
+  k_bitmap_from_maps<<<dim3(64, g.NL), 256, 0, st>>>(g, b);
+  // every tile / band active at epoch 1 (frame 0: no gating)
+  std::vector<int> ones(std::max(g.tiles_per_stream, g.bands_per_stream), 1);
+  cudaMemcpyAsync(b.tile_stamp, ones.data(), sizeof(int) * g.tiles_per_stream, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b.band_stamp, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
+  k_nms<<<dim3(g.bands_per_stream, 1), NMS_THREADS, 0, st>>>(g, b);
+  k_gather_kps<<<g.bands_per_stream, 128, 0, st>>>(g, b, x_dev, y_dev, sigma_dev, score_dev, cap);
+  int ctr[C_NCTR];
+  cudaMemcpyAsync(ctr, b.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st);
+  rc = cuda_status(cudaStreamSynchronize(st));
+  if (rc) return rc;
+  *n_out = ctr[C_NDET];
+  if (ctr[C_ERR] || ctr[C_NDET] > cap) return VF_ERR_CAPACITY;
+  return VF_OK;
+}
+
+int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, const double* kx_dev,
+                const double* ky_dev, const double* sigma_dev, const double* theta_in_dev, double* theta_out_dev,
+                uint8_t* desc_dev, void* stream)
+{
+  if (!g_pattern_ok) return VF_ERR_PATTERN;
+  if (!frame_dev || n < 0 || pitch < W) return VF_ERR_ARG;
+  if (n == 0) return VF_OK;
+  // SAT tiles of the frame through k_pyramid with one octave (no derived layers)
+  Scratch sc;
+  int rc = stage_ctx(W, H, 1, 1, 4096, sc);
+  if (rc) return rc;
+  vf_ctx* c = sc.c;
+  cudaStream_t st = (cudaStream_t)stream;
+  Bufs b = c->b;
+  b.frames = frame_dev; b.frame_stride = 0; b.frame_pitch = pitch;
+  k_pyramid<<<dim3(c->g.ptx, c->g.pty, 1), 256, c->pyr_smem, st>>>(c->g, b);
+  k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev, theta_in_dev,
+                                                              theta_out_dev, desc_dev);
+  return cuda_status(cudaStreamSynchronize(st));
+}
+
+int vf_intensity_mask(const uint8_t* prev_dev, const uint8_t* cur_dev, int64_t n, double t_i, uint8_t* out_dev,
+                      void* stream)
+{
+  if (n < 0 || (n > 0 && (!prev_dev || !cur_dev || !out_dev))) return VF_ERR_ARG;
+  if (n == 0) return VF_OK;
+  k_intensity_mask<<<std::min(cdiv(n, 256), 4096), 256, 0, (cudaStream_t)stream>>>(prev_dev, cur_dev, n, t_i, out_dev);
+  return cuda_status(cudaGetLastError());
+}
+
+int vf_binning_histogram(int n, const double* xs_dev, const double* ys_dev, int W, int H, int rows, int cols,
+                         uint64_t* hist_dev, void* stream)
+{
+  if (rows < 1 || cols < 1) return VF_ERR_GRID;
+  if (!hist_dev || n < 0) return VF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(hist_dev, 0, sizeof(uint64_t) * rows * cols, st);
+  if (n > 0)
+    k_binning_hist<<<std::min(cdiv(n, 256), 1024), 256, 0, st>>>(n, xs_dev, ys_dev, W, H, rows, cols,
+                                                                  (unsigned long long*)hist_dev);
+  return cuda_status(cudaGetLastError());
+}
+
+int vf_upsample_mask(const uint8_t* bits_dev, int rows, int cols, int cell_w, int cell_h, int W, int H, uint8_t* full_dev,
+                     void* stream)
+{
+  if (!bits_dev || !full_dev || rows < 1 || cols < 1 || cell_w < 1 || cell_h < 1) return VF_ERR_ARG;
+  if ((long long)cell_w * cols < W || (long long)cell_h * rows < H) return VF_ERR_ARG;
+  k_upsample<<<std::min(cdiv((long long)W * H, 256), 4096), 256, 0, (cudaStream_t)stream>>>(bits_dev, cols, cell_w,
+                                                                                            cell_h, W, H, full_dev);
+  return cuda_status(cudaGetLastError());
+}
+
+int vf_mask_values(const uint8_t* full_dev, int W, int H, int n, const double* xs_dev, const double* ys_dev,
+                   uint8_t* out_dev, void* stream)
+{
+  if (n < 0) return VF_ERR_ARG;
+  if (n == 0) return VF_OK;
+  k_mask_values<<<std::min(cdiv(n, 256), 1024), 256, 0, (cudaStream_t)stream>>>(full_dev, W, H, n, xs_dev, ys_dev,
+                                                                                 out_dev);
+  return cuda_status(cudaGetLastError());
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// vf_common.cuh -- shared device-side definitions of the B200 detect+describe path.
+//
+// Geometry, per-stream slab layout and device helpers shared by every kernel.
+// The reference is a CPU package (vidfeat 0.1.0); citations are file:line in
+// /root/reference/pkg/src/vidfeat/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define VF_MAXO 8                 // max octaves
+#define VF_MAXL (2 * VF_MAXO)     // layers o0,i0,o1,i1,...
+#define VF_MAXG VF_MAXO           // mask grids (per_layer: one per octave level)
+
+// FAST tiles (layer coordinates): 128 columns x 8 rows.  An NMS band is one
+// row of tiles (8 layer rows, full layer width), so bands emit keypoints in
+// the reference's (layer, y, x) order (detector.py:251-253,303-306).
+#define VF_TILE_W 128
+#define VF_TILE_H 8
+#define VF_TILE_WORDS (VF_TILE_W / 32)
+
+// per-stream int32 counters
+enum {
+  C_FRAME = 0,      // frames processed on this stream
+  C_NFEAT0 = 1,     // features in buffer 0
+  C_NFEAT1 = 2,     // features in buffer 1
+  C_NDET = 3, C_NPROP = 4, C_NTOTAL = 5, C_NDROP = 6,
+  C_STAGE = 7,      // staging bump allocator
+  C_TICKET = 8,     // last-CTA ticket (NMS launch)
+  C_ERR = 9,        // sticky error bits
+  C_NSURV = 10,     // NMS survivors (before border filter)
+  C_NCAND = 11,     // FAST candidates
+  C_NCTR = 16
+};
+#define VF_ERRBIT_CAPACITY 1
+#define VF_ERRBIT_STAGING 2
+#define VF_ERRBIT_INDEX 4
+
+struct LayerGeo {
+  int w, h;
+  int pitch;            // derived-layer / score-map pitch (bytes)
+  int tiles_x, tiles_y; // FAST tiles
+  int tile_base;        // first tile id of this layer within a stream
+  int band_base;        // first band id (== tile row) of this layer
+  int bm_words;         // candidate-bitmap words per row
+  long long layer_off;  // byte offset of the derived layer in the layer slab (l >= 1)
+  long long sm_off;     // byte offset of the score map in the score slab
+  long long bm_off;     // word offset of the bitmap in the bitmap slab
+  int rc_off, cc_off;   // offsets of the row/col -> cell LUTs (per grid, see Geo)
+  double scale, sigma;  // pyramid.py:122-124; detector.py:243
+};
+
+struct GridGeo {          // a cell grid of the detection mask (masking.py:30-55)
+  int rows, cols, cw, ch; // cell size in full-res pixels (masking.py:143-144)
+  long long cell_off;     // byte offset in the cell slab
+};
+
+struct Geo {
+  int W, H, O, NL;
+  int threshold;
+  int mask_mode;        // 0 none, 1 intensity, 2 binning
+  int per_layer;        // intensity per octave level (pipeline.py:188-200)
+  int mask_level;       // octave level of the IDDM source (pipeline.py:187)
+  double t_i;           // masking.py:26
+  int t_h;              // masking.py:70
+  int n_grids;
+  GridGeo grid[VF_MAXG];
+  LayerGeo L[VF_MAXL];
+  int tiles_per_stream, bands_per_stream;
+  long long layer_slab, sm_slab, bm_slab_words, cell_slab, lut_len;
+  // pyramid tiles (kernel k_pyramid), also the SAT tiles
+  int ptw, pth, ptx, pty;
+  // IDDM state: octave levels kept for the next frame
+  long long state_off[VF_MAXO]; long long state_slab;
+  int kp_cap;           // feature capacity per stream and buffer
+  int prop_chunks;      // CTAs reserved for propagation chunks
+  int nms_raw;          // stand-alone nms_and_refine: no border / merge filter
+  int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
+};
+
+// Per-launch stream-batch pointers.
+struct Bufs {
+  const uint8_t* frames; long long frame_stride; long long frame_pitch; // o0 of stream s
+  uint8_t* layers;      // [S][layer_slab]
+  uint8_t* scores;      // [S][sm_slab]
+  uint32_t* bitmaps;    // [S][bm_slab_words]
+  int* tile_stamp;      // [S][tiles_per_stream]
+  int* band_stamp;      // [S][bands_per_stream]
+  int* band_rec;        // [S][bands_per_stream][4]: staging base, kept, border-ok, dropped
+  int* band_out;        // [S][bands_per_stream]: output offset of the band's kept keypoints
+  int* prop_cnt;        // [S][prop_chunks]
+  int* prop_out;        // [S][prop_chunks]
+  uint8_t* cells;       // [S][cell_slab]
+  int* cell_row_stamp;  // [S][n_grids][max rows] "row has an active cell" stamps
+  uint8_t* state;       // [S][state_slab]
+  const int* lut;       // [lut_len] row/col -> cell maps (shared by all streams)
+  uint32_t* sat;        // [S][W*H] tile-local summed-area tables
+  double* st_x; double* st_y; double* st_s; double* st_v;   // staging [S][kp_cap]
+  // double-buffered features [S][2][kp_cap]
+  double* fx; double* fy; double* fs; double* ft; double* fv;
+  uint8_t* forg; int* fage; uint8_t* fdesc;  // desc: [S][2][kp_cap][64]
+  int* ctr;             // [S][C_NCTR]
+  unsigned long long* cov;  // [S] covered full-res pixels of this frame
+  double* report;       // [S][8]: n_det, n_prop, n_total, n_dropped, coverage, frame, n_surv, n_cand
+  int* worklist; int* work_count;  // active FAST tiles (s * tiles_per_stream + tile)
+  int* epoch;           // step counter, bumped by k_finalize
+};
+
+// --------------------------------------------------------------------------
+// small helpers
+// --------------------------------------------------------------------------
+__device__ __forceinline__ const uint8_t* layer_ptr(const Geo& g, const Bufs& b, int s, int l, int& pitch)
+{
+  if (l == 0) { pitch = (int)b.frame_pitch; return b.frames + (long long)s * b.frame_stride; }
+  pitch = g.L[l].pitch;
+  return b.layers + (long long)s * g.layer_slab + g.L[l].layer_off;
+}
+
+// Grid used to gate layer l (per_layer: its octave level's grid, else grid 0).
+__device__ __forceinline__ int grid_of_layer(const Geo& g, int l) { return g.per_layer ? (l >> 1) : 0; }
+
+// Gate of layer pixel (y, x): the full-res mask sampled by floor mapping
+// (detector.py:175-181) of the block-replicated cell mask (masking.py:139-148).
+__device__ __forceinline__ int gate_at(const Geo& g, const Bufs& b, int s, int l, int y, int x)
+{
+  const int gi = grid_of_layer(g, l);
+  const int* lut = b.lut + g.L[l].rc_off;      // rows then cols
+  int r = __ldg(lut + y);
+  int c = __ldg(lut + g.L[l].h + x);
+  const GridGeo& G = g.grid[gi];
+  return b.cells[(long long)s * g.cell_slab + G.cell_off + (long long)r * G.cols + c];
+}
+
+// Merge-mask bit at full-res position (masking.py:151-165); per_layer uses the
+// union of the level masks (pipeline.py:196-199).
+__device__ __forceinline__ int merge_mask_at(const Geo& g, const Bufs& b, int s, double x, double y)
+{
+  long long xi = (long long)floor(x + 0.5), yi = (long long)floor(y + 0.5);
+  xi = xi < 0 ? 0 : (xi > g.W - 1 ? g.W - 1 : xi);
+  yi = yi < 0 ? 0 : (yi > g.H - 1 ? g.H - 1 : yi);
+  const uint8_t* cells = b.cells + (long long)s * g.cell_slab;
+  int v = 0;
+  for (int k = 0; k < g.n_grids; k++) {
+    const GridGeo& G = g.grid[k];
+    v |= cells[G.cell_off + (yi / G.ch) * G.cols + xi / G.cw];
+  }
+  return v;
+}
+
+__device__ __forceinline__ int use_mask(const Geo& g, const Bufs& b, int s)
+{
+  return g.mask_mode != 0 && b.ctr[s * C_NCTR + C_FRAME] > 0;   // pipeline.py:234
+}
+
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* sm_warp, T& total)
+{
+  // blockDim.x multiple of 32, <= 1024
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? sm_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) sm_warp[lane] = w;
+  }
+  __syncthreads();
+  T base = wid > 0 ? sm_warp[wid - 1] : T(0);
+  total = sm_warp[nw - 1];
+  __syncthreads();
+  return base + x - v;
+}

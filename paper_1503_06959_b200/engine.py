@@ -1,0 +1,157 @@
+"""FeatureEngine: one C-ABI context (vf_ctx) processing S independent streams.
+
+This is the batched form of the reference's per-frame loop body
+(pipeline.py:222-277): every call processes frame n of each stream with one
+launch per stage over all streams.  Device memory, streams and the
+torch.distributed plumbing belong to PyTorch; all compute is the sm_100a
+library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .types import MaskConfig, PipelineConfig
+
+
+class _CudaArray:
+    """Zero-copy __cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": typestr, "data": (int(ptr), True), "version": 3, "strides": None,
+        }
+
+
+def _mode(mc: MaskConfig) -> int:
+    if mc.mode == "temporal":
+        raise NotImplementedError(
+            "mask mode 'temporal' is the block-matching baseline (temporal.py), outside this hot path")
+    return _native.MODES[mc.mode]
+
+
+class FeatureEngine:
+    def __init__(self, width: int, height: int, cfg: PipelineConfig | None = None, n_streams: int = 1,
+                 kp_capacity: int = 0):
+        cfg = cfg or PipelineConfig()
+        mc = cfg.mask
+        if cfg.threshold < 1:
+            raise ValueError("detection threshold must be >= 1")
+        c = _native.VfConfig(
+            width=width, height=height, n_octaves=cfg.n_octaves, threshold=int(cfg.threshold),
+            mask_mode=_mode(mc), t_i=float(mc.t_i), t_h=int(mc.t_h), grid_rows=int(mc.grid[0]),
+            grid_cols=int(mc.grid[1]), octave_for_mask=-1 if mc.octave_for_mask is None else int(mc.octave_for_mask),
+            per_layer=int(bool(mc.per_layer)), max_streams=int(n_streams), kp_capacity=int(kp_capacity))
+        L = _native.lib()
+        _native.ensure_pattern()
+        h = ctypes.c_void_p()
+        _native.check(L.vf_create(ctypes.byref(c), ctypes.byref(h)), "vf_create")
+        self._h = h
+        self.width, self.height, self.n_streams, self.cfg = width, height, n_streams, cfg
+        n_layers = 2 * cfg.n_octaves
+        ws = np.zeros(n_layers, np.int32)
+        hs = np.zeros(n_layers, np.int32)
+        sc = np.zeros(n_layers, np.float64)
+        _native.check(L.vf_layer_geometry(self._h, ws.ctypes.data, hs.ctypes.data, sc.ctypes.data))
+        self.layer_w, self.layer_h, self.layer_scale = ws, hs, sc
+
+    # -- processing -----------------------------------------------------------
+    def process(self, frames, stream=None) -> None:
+        """frames: CUDA uint8 tensor [S, H, W] (or [H, W] for S = 1), device-resident."""
+        import torch
+
+        if frames.dim() == 2:
+            frames = frames.unsqueeze(0)
+        if frames.dtype != torch.uint8 or not frames.is_cuda:
+            raise ValueError("frames must be a CUDA uint8 tensor")
+        S, H, W = frames.shape
+        if (H, W) != (self.height, self.width):
+            raise ValueError(f"frame {W}x{H} does not match the engine's {self.width}x{self.height}")
+        if frames.stride(2) != 1:
+            frames = frames.contiguous()
+        _native.check(_native.lib().vf_process(self._h, frames.data_ptr(), frames.stride(0), frames.stride(1), S,
+                                               _native.stream_handle(stream)), "vf_process")
+
+    def process_host(self, frames: np.ndarray, stream=None) -> None:
+        """frames: host uint8 array [S, H, W]; the H2D copy is part of the call."""
+        a = np.ascontiguousarray(frames)
+        if a.ndim == 2:
+            a = a[None]
+        S, H, W = a.shape
+        _native.check(_native.lib().vf_process_host(self._h, a.ctypes.data, H * W, W, S, _native.stream_handle(stream)),
+                      "vf_process_host")
+
+    def reset(self, stream=None) -> None:
+        _native.check(_native.lib().vf_reset(self._h, _native.stream_handle(stream)))
+
+    # -- results ----------------------------------------------------------------
+    def report(self, s: int = 0, stream=None) -> _native.VfReport:
+        r = _native.VfReport()
+        _native.check(_native.lib().vf_get_report(self._h, s, ctypes.byref(r), _native.stream_handle(stream)),
+                      "vf_get_report")
+        return r
+
+    def totals(self, s: int = 0, stream=None) -> np.ndarray:
+        out = np.zeros(4, np.float64)
+        _native.check(_native.lib().vf_get_totals(self._h, s, out.ctypes.data, _native.stream_handle(stream)))
+        return out
+
+    def features_device(self, s: int = 0, stream=None) -> dict:
+        """Zero-copy torch views of stream s's current features (valid until the next process)."""
+        import torch
+
+        f = _native.VfFeatures()
+        _native.check(_native.lib().vf_get_features(self._h, s, ctypes.byref(f), _native.stream_handle(stream)))
+        n = int(f.n)
+        out = {"n": n}
+        if n == 0:
+            dev = torch.device("cuda")
+            for k, dt in (("x", torch.float64), ("y", torch.float64), ("sigma", torch.float64),
+                          ("theta", torch.float64), ("score", torch.float64), ("origin", torch.uint8),
+                          ("age", torch.int32)):
+                out[k] = torch.zeros(0, dtype=dt, device=dev)
+            out["desc"] = torch.zeros((0, 64), dtype=torch.uint8, device=dev)
+            return out
+        for k, ts in (("x", "<f8"), ("y", "<f8"), ("sigma", "<f8"), ("theta", "<f8"), ("score", "<f8"),
+                      ("origin", "|u1"), ("age", "<i4")):
+            out[k] = torch.as_tensor(_CudaArray(getattr(f, k), (n,), ts), device="cuda")
+        out["desc"] = torch.as_tensor(_CudaArray(f.desc, (n, 64), "|u1"), device="cuda")
+        return out
+
+    def features_host(self, s: int = 0, stream=None) -> dict:
+        """Copy stream s's current features into numpy arrays (synchronizes)."""
+        f = _native.VfFeatures()
+        L = _native.lib()
+        _native.check(L.vf_get_features(self._h, s, ctypes.byref(f), _native.stream_handle(stream)))
+        n = int(f.n)
+        out = {k: np.zeros(n, np.float64) for k in ("x", "y", "sigma", "theta", "score")}
+        out["origin"] = np.zeros(n, np.uint8)
+        out["age"] = np.zeros(n, np.int32)
+        out["desc"] = np.zeros((n, 64), np.uint8)
+        got = ctypes.c_int32(0)
+        _native.check(L.vf_copy_features(
+            self._h, s, n, out["x"].ctypes.data, out["y"].ctypes.data, out["sigma"].ctypes.data,
+            out["theta"].ctypes.data, out["score"].ctypes.data, out["origin"].ctypes.data, out["age"].ctypes.data,
+            out["desc"].ctypes.data, ctypes.byref(got), _native.stream_handle(stream)), "vf_copy_features")
+        out["n"] = n
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _native.lib().vf_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
