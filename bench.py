@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark: frames/s (and MPix/s) of the per-frame detect+describe hot path.
+
+Workload (BASELINE.json config 5): 64 independent 1920x1080 uint8 streams,
+seeded synthetic scenes (kind = s mod 3: static / pan / objects), reference
+defaults t = 55, O = 4, intensity mask t_i = 20 (the primary mode,
+BASELINE.md section 4).  Streams are sharded contiguously across ranks
+(strong scaling: total 64 streams).  One step = frame n of every local stream
+through the whole path (pyramid -> mask -> score -> NMS/refine -> describe ->
+Eq. 1 merge).  Frames are generated on the GPU and resident in HBM before the
+timed region; each step reads a fresh batch (8-64 x 2.07 MB).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the reference algorithm on the host cores through the
+CPU oracle port (oracle/vf_oracle.c, kind "port"; the reference itself is a
+Python package that cannot travel to the GPU box), rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+TOTAL_STREAMS = 64
+W_FR, H_FR = 1920, 1080
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="intensity", choices=["intensity", "binning", "none"])
+    ap.add_argument("--streams", type=int, default=TOTAL_STREAMS)
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(n_total, rank, world):
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
+    return list(range(lo, hi))
+
+
+def hbm_peak():
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def window(self, t0, t1):
+        """Keep only samples taken inside [t0, t1] (plus one sampling period)."""
+        self.lines = [(t, ln) for t, ln in self.lines if t0 <= t <= t1 + 0.2]
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for _, ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline: the oracle port on the host cores (bounded sample)
+# ----------------------------------------------------------------------------
+def cpu_run(frames_by_stream, mode, threads):
+    """frames_by_stream: list of [F, H, W] uint8 arrays.  Returns (frames, seconds)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle
+    from paper_1503_06959_b200.pattern import default_pattern
+
+    pat = default_pattern()
+
+    def one(frames):
+        p = oracle.OraclePipeline(frames.shape[2], frames.shape[1], pat, mode=mode)
+        try:
+            for f in frames:
+                p.process(f)
+        finally:
+            p.close()
+        return len(frames)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        n = sum(ex.map(one, frames_by_stream))
+    return n, time.perf_counter() - t0
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------
+def gen_frames(streams, n_frames, device):
+    """[n_frames, S, H, W] uint8 on `device` (config 5 scenes)."""
+    import torch
+
+    from paper_1503_06959_b200 import scenes
+
+    cfg = scenes.CONFIGS[5]
+    out = torch.empty((n_frames, len(streams), H_FR, W_FR), dtype=torch.uint8, device=device)
+    for j, s in enumerate(streams):
+        st = scenes.SceneStream(cfg, s, device)
+        for n in range(n_frames):
+            out[n, j] = st.next_frame()
+    return out
+
+
+def algorithmic_bytes(n_frames, cov_sum, k_out, k_prop, O=4):
+    """B_alg = W*H*[1 + 2*4^-(O-1) + 2*a*(rho - 4^-(O-1))] + 109*(K_out + K_prop)."""
+    rho = 0.918
+    top = 4.0 ** -(O - 1)
+    wh = W_FR * H_FR
+    return wh * (n_frames * (1 + 2 * top) + 2 * cov_sum * (rho - top)) + 109.0 * (k_out + k_prop)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_1503_06959_b200 import scenes
+    import torch
+
+    threads = host_threads()
+    n_str = min(args.streams, threads)
+    streams = list(range(n_str))
+    steps = args.warmup + args.steps
+    # frames of the sample streams (CPU-generated; same generator as the GPU arm)
+    data = [scenes.generate(scenes.CONFIGS[5], steps, streams=[s])[0].numpy() for s in streams]
+    # warmup frames then timed frames, stream-sequential
+    from oracle import oracle
+    from paper_1503_06959_b200.pattern import default_pattern
+    from concurrent.futures import ThreadPoolExecutor
+
+    pat = default_pattern()
+    pipes = [oracle.OraclePipeline(W_FR, H_FR, pat, mode=args.mode) for _ in streams]
+
+    def step(n):
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(lambda i: pipes[i].process(data[i][n]), range(n_str)))
+
+    for n in range(args.warmup):
+        step(n)
+    t0 = time.perf_counter()
+    for n in range(args.warmup, steps):
+        step(n)
+    dt = time.perf_counter() - t0
+    for p in pipes:
+        p.close()
+    frames = n_str * args.steps
+    fps = frames / dt
+    line = {
+        "impl": "reference", "metric": "frames/sec (detect+describe)", "value": fps, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"config5: {TOTAL_STREAMS} x 1920x1080 streams, mode {args.mode}, t=55, O=4",
+                   "sample": f"{n_str} streams x 1 frame per step"},
+        "mpix_per_sec": fps * W_FR * H_FR / 1e6,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{n_str} streams x {args.steps} frames after {args.warmup} warm-up frames; "
+                                   f"C oracle (oracle/vf_oracle.c) one thread per stream on {cpu_model()}"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    streams = shard(args.streams, rank, world)
+    S = len(streams)
+    W, K = args.warmup, args.steps
+    e2e_k = 0 if args.no_e2e else max(1, min(args.e2e_steps, K))
+    n_frames = W + K + e2e_k
+    dev = torch.device("cuda", local)
+    frames = gen_frames(streams, n_frames, dev)
+    torch.cuda.synchronize()
+
+    cfg = PipelineConfig(mask=MaskConfig(mode=args.mode))
+    eng = FeatureEngine(W_FR, H_FR, cfg, n_streams=S)
+    stream = torch.cuda.current_stream()
+    for n in range(W):
+        eng.process(frames[n])
+    torch.cuda.synchronize()
+    t_before = np.array([eng.totals(s) for s in range(S)])
+
+    # ---- timed region: K steps, device-resident inputs ----
+    eng.set_timing(True)
+    eng.stage_ms()  # clear
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(1.0)  # let nvidia-smi start sampling
+        tw0 = time.time()
+        ev0.record(stream)
+        for n in range(W, W + K):
+            eng.process(frames[n])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+    clk.window(tw0, tw1)
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    stage, n_steps = eng.stage_ms()
+    eng.set_timing(False)
+    t_after = np.array([eng.totals(s) for s in range(S)])
+    d = t_after - t_before  # per stream: sum n_det, sum n_total, sum coverage, frames
+    # per-rank stats -> max time over ranks, summed work
+    loc = torch.tensor([ms, d[:, 0].sum(), d[:, 1].sum(), d[:, 2].sum(), d[:, 3].sum()], dtype=torch.float64,
+                       device=dev)
+    if world > 1:
+        mx = loc.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        sm = loc.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max = float(mx[0])
+        tot = sm.tolist()
+    else:
+        ms_max = ms
+        tot = loc.tolist()
+    frames_done = tot[4]
+    fps = frames_done / (ms_max / 1e3)
+
+    # ---- e2e: public API with host buffers (H2D of frames + D2H of features inside) ----
+    e2e = None
+    if e2e_k:
+        host = frames[W + K:W + K + e2e_k].cpu().pin_memory()
+        h2d = S * H_FR * W_FR
+        d2h_total = 0
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for n in range(e2e_k):
+            eng.process_host(host[n].numpy())
+            for s in range(S):
+                f = eng.features_host(s)
+                d2h_total += f["n"] * (5 * 8 + 1 + 4 + 64)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
+        tt = torch.tensor([e2e_ms, S * e2e_k, float(d2h_total)], dtype=torch.float64, device=dev)
+        if world > 1:
+            m2 = tt.clone()
+            dist.all_reduce(m2[:1], op=dist.ReduceOp.MAX)
+            s2 = tt.clone()
+            dist.all_reduce(s2, op=dist.ReduceOp.SUM)
+            e2e_ms, e2e_frames, d2h_total = float(m2[0]), float(s2[1]), float(s2[2])
+        else:
+            e2e_frames = S * e2e_k
+        e2e = {"value": e2e_frames / (e2e_ms / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h_total / e2e_k),
+               "steps": e2e_k, "api": "vf_process_host + vf_copy_features (C-ABI via FeatureEngine)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (live CUDA events, timed region) ----
+    peak, peak_kind = hbm_peak()
+    k_out = tot[1]
+    k_total = tot[2]
+    cov_sum = tot[3]
+    b_alg = algorithmic_bytes(frames_done, cov_sum, k_out, k_total - k_out)
+    dom = max((k for k in stage if stage[k] > 0), key=lambda k: stage[k])
+    dom_ms = stage[dom] / max(n_steps, 1)
+    # algorithmic bytes per launch of each stage, this rank
+    per_frame_top = W_FR * H_FR * (4.0 ** -3)
+    f_loc = d[:, 3].sum()
+    alg = {
+        "pyramid": W_FR * H_FR * f_loc * (1 + 0.918) + 2 * per_frame_top * f_loc,
+        "fast": 2 * W_FR * H_FR * 1.918 * d[:, 2].sum(),
+        "describe": 109.0 * d[:, 0].sum(),
+        "propagate": 2 * 109.0 * (d[:, 1].sum() - d[:, 0].sum()),
+        "nms": W_FR * H_FR * 1.918 * d[:, 2].sum() / 8,
+    }
+    dom_bytes = alg.get(dom, 0.0) / max(n_steps, 1)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    step_ms = ms_max / K
+    step_achieved = b_alg / world / K / (step_ms / 1e3) / 1e9 if world == 1 else b_alg / K / (step_ms / 1e3) / 1e9
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None, "kernel": f"k_{dom}", "kernel_ms_per_launch": dom_ms,
+        "kernel_share_of_step": stage[dom] / max(sum(stage.values()), 1e-9),
+        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
+        "step": {"algorithmic_bytes_per_step": b_alg / K, "achieved": step_achieved,
+                 "frac": step_achieved / peak},
+        "stage_ms_per_step": {k: v / max(n_steps, 1) for k, v in stage.items()},
+    }
+
+    # ---- CPU baseline: oracle port on the host cores, bounded sample (rank 0, N = 1) ----
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n_str = min(S, threads)
+        nf = 4  # frame 0 (full detection) + 3 masked frames per sampled stream
+        sample = [frames[:nf, j].cpu().numpy() for j in range(n_str)]
+        n_cpu, dt = cpu_run(sample, args.mode, threads)
+        cpu = {"value": n_cpu / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"{n_str} streams x {nf} frames (frame 0 full detection + {nf - 1} masked) of the "
+                         f"bench workload, C oracle one thread per stream on {cpu_model()}"}
+
+    line = {
+        "metric": "frames/sec (detect+describe)", "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"config5: {args.streams} x 1920x1080 uint8 streams (static/pan/objects), "
+                               f"mode {args.mode}, t=55, O=4, t_i=20",
+                   "streams_total": args.streams, "streams_per_rank": S, "sharding": "contiguous streams per rank",
+                   "l2": "inputs larger than L2: every step reads a fresh batch of frames (no re-use)"},
+        "mpix_per_sec": fps * W_FR * H_FR / 1e6,
+        "features_per_frame": k_total / max(frames_done, 1),
+        "detected_per_frame": k_out / max(frames_done, 1),
+        "mean_coverage": cov_sum / max(frames_done, 1),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": (6 + (1 if args.mode == "binning" else 0) + (2 if args.mode != "none" else 0)) * K,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

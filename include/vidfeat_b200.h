@@ -116,6 +116,12 @@ int vf_copy_features(vf_ctx *ctx, int s, int32_t cap, double *x, double *y, doub
                      double *score, uint8_t *origin, int32_t *age, uint8_t *desc, int32_t *n_out, void *stream);
 /* Device pointers of layer l of stream s's current pyramid (l >= 1; l = 0 is the input frame). */
 int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch);
+/* Live per-stage device timing with CUDA events on the launch stream:
+ * stages = binmask, pyramid, worklist, fast, nms, sat, describe, propagate, finalize (9).
+ * vf_get_stage_ms synchronizes `stream`, returns the summed milliseconds per
+ * stage since the last query and the number of steps, and clears. */
+int vf_set_timing(vf_ctx *ctx, int enable);
+int vf_get_stage_ms(vf_ctx *ctx, double *ms9, int32_t *n_steps, void *stream);
 /* Per-stream totals since vf_create/vf_reset: sum n_detected, sum n_total, sum coverage, frames. */
 int vf_get_totals(vf_ctx *ctx, int s, double *out4, void *stream);
 

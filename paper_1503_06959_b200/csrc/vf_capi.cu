@@ -140,6 +140,9 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.ptw = unit * std::max(1, 96 / unit);
   g.pth = unit * std::max(1, 48 / unit);
   g.ptx = cdiv(g.W, g.ptw); g.pty = cdiv(g.H, g.pth);
+  g.sat_tiles = g.ptx * g.pty;
+  g.pth_magic = (unsigned)((0x100000000ULL + g.pth - 1) / g.pth);
+  if (g.ptx > 32 * 8) return VF_ERR_ARG;   // strip carries: <= 8 x 32 tile columns
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
   g.prop_chunks = cdiv(g.kp_cap, 1024);
@@ -155,7 +158,7 @@ int pyramid_smem(const Geo& g)
     else { lw = g.ptw >> o; lh = g.pth >> o; }
     acc += (lw * lh + 15) & ~15;
   }
-  return acc + g.ptw * g.pth * 4;
+  return acc;
 }
 
 int g_num_sms = 0;
@@ -178,12 +181,30 @@ struct vf_ctx {
   std::vector<long long> frames_done;   // host mirror of per-stream frame counters
   int pyr_smem;
   int fast_grid;
+  int desc_grid;
+  int sat_grid, sat_smem;
   // host-input staging (vf_process_host)
   uint8_t* hstage[2] = {nullptr, nullptr};
   long long hstage_bytes = 0;
   int hstage_k = 0;
   cudaEvent_t hstage_free[2] = {nullptr, nullptr};
+  // live per-stage timing (vf_set_timing): one event before each stage + end
+  int timing = 0;
+  std::vector<cudaEvent_t> ev_pool, ev_used;
+  std::vector<int> ev_stage;   // stage index of each recorded interval start
 };
+
+#define VF_NSTAGES 9   // binmask, pyramid, worklist, fast, nms, sat, describe, propagate, finalize
+static void stage_mark(vf_ctx* c, int stage, cudaStream_t st)
+{
+  if (!c->timing) return;
+  cudaEvent_t e;
+  if (c->ev_pool.empty()) cudaEventCreate(&e);
+  else { e = c->ev_pool.back(); c->ev_pool.pop_back(); }
+  cudaEventRecord(e, st);
+  c->ev_used.push_back(e);
+  c->ev_stage.push_back(stage);
+}
 
 extern "C" {
 
@@ -281,6 +302,11 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   int* dl = A.get<int>((size_t)g.lut_len);
   b.lut = dl;
   b.sat = A.get<uint32_t>((size_t)S * g.W * g.H);
+  b.rowsum = A.get<uint32_t>((size_t)S * g.H * g.ptx);
+  b.carry = A.get<uint32_t>((size_t)S * g.H * g.ptx);
+  b.sat_stamp = A.get<int>((size_t)S * g.sat_tiles);
+  b.sat_work = A.get<int>((size_t)S * g.sat_tiles);
+  b.sat_count = A.get<int>((size_t)S);
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -312,6 +338,14 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, 128, 0);
   c->fast_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  c->sat_smem = ((g.ptw * g.pth + 15) & ~15) + g.ptw * g.pth * 4 + (S + 1) * 4;
+  if (c->sat_smem > 48 * 1024) cudaFuncSetAttribute(k_sat, cudaFuncAttributeMaxDynamicSharedMemorySize, c->sat_smem);
+  occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sat, 256, c->sat_smem);
+  c->sat_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_describe, DS_THREADS, (S + 1) * sizeof(int));
+  c->desc_grid = std::max(1, g_num_sms * std::max(occ, 1));
   *out = c;
   return VF_OK;
 }
@@ -323,6 +357,8 @@ int vf_destroy(vf_ctx* c)
     if (c->hstage[k]) cudaFree(c->hstage[k]);
     if (c->hstage_free[k]) cudaEventDestroy(c->hstage_free[k]);
   }
+  for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->ev_used) cudaEventDestroy(ev);
   c->mem.release();
   delete c;
   return VF_OK;
@@ -336,6 +372,35 @@ int vf_layer_geometry(const vf_ctx* c, int32_t* ws, int32_t* hs, double* scales)
     if (hs) hs[l] = c->g.L[l].h;
     if (scales) scales[l] = c->g.L[l].scale;
   }
+  return VF_OK;
+}
+
+int vf_set_timing(vf_ctx* c, int enable)
+{
+  if (!c) return VF_ERR_ARG;
+  c->timing = enable;
+  return VF_OK;
+}
+
+int vf_get_stage_ms(vf_ctx* c, double* ms7, int* n_steps, void* stream)  /* ms7: VF_NSTAGES entries */
+{
+  if (!c || !ms7) return VF_ERR_ARG;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e);
+  for (int k = 0; k < VF_NSTAGES; k++) ms7[k] = 0.0;
+  int steps = 0;
+  for (size_t i = 0; i + 1 < c->ev_used.size(); i++) {
+    int stg = c->ev_stage[i];
+    if (stg < 0) { steps++; continue; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_used[i], c->ev_used[i + 1]);
+    ms7[stg] += ms;
+  }
+  if (!c->ev_stage.empty() && c->ev_stage.back() < 0) steps++;
+  for (cudaEvent_t ev : c->ev_used) c->ev_pool.push_back(ev);
+  c->ev_used.clear();
+  c->ev_stage.clear();
+  if (n_steps) *n_steps = steps;
   return VF_OK;
 }
 
@@ -355,18 +420,32 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   const Geo& g = c->g;
   Bufs b = c->b;
   if (g.mask_mode == 2) {
+    stage_mark(c, 0, st);
     int smem = g.grid[0].rows * g.grid[0].cols * 4;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_binmask, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_binmask<<<n, 1024, smem, st>>>(g, b);
   }
+  stage_mark(c, 1, st);
   k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
+  stage_mark(c, 2, st);
   const int tile_ctas = cdiv(g.tiles_per_stream, 8);
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
-  k_worklist<<<dim3(tile_ctas + cov_ctas, n), 256, 0, st>>>(g, b, tile_ctas);
+  const int carry_ctas = cdiv(g.pty, 8);
+  k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(
+      g, b, tile_ctas, cov_ctas, carry_ctas);
+  stage_mark(c, 3, st);
   k_fast<<<c->fast_grid, 128, 0, st>>>(g, b);
-  k_nms<<<dim3(g.bands_per_stream + g.prop_chunks, n), NMS_THREADS, 0, st>>>(g, b);
-  k_describe<<<dim3(g.bands_per_stream + g.prop_chunks, n), DS_THREADS, 0, st>>>(g, b);
+  stage_mark(c, 4, st);
+  k_nms<<<dim3(g.bands_per_stream, n), NMS_THREADS, 0, st>>>(g, b);
+  stage_mark(c, 5, st);
+  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
+  stage_mark(c, 6, st);
+  k_describe<<<c->desc_grid, DS_THREADS, (n + 1) * sizeof(int), st>>>(g, b, n);
+  stage_mark(c, 7, st);
+  if (g.mask_mode) k_propagate<<<dim3(PROP_CTAS, n), 256, 0, st>>>(g, b);
+  stage_mark(c, 8, st);
   k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
+  stage_mark(c, -1, st);
   for (int s = 0; s < n; s++) c->frames_done[s]++;
   return cuda_status(cudaGetLastError());
 }
@@ -648,8 +727,10 @@ int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, co
   Bufs b = c->b;
   b.frames = frame_dev; b.frame_stride = 0; b.frame_pitch = pitch;
   k_pyramid<<<dim3(c->g.ptx, c->g.pty, 1), 256, c->pyr_smem, st>>>(c->g, b);
-  k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev, theta_in_dev,
-                                                              theta_out_dev, desc_dev);
+  k_carries<<<dim3(c->g.pty, 1), 32, 0, st>>>(c->g, b);
+  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1);
+  k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev,
+                                                              theta_in_dev, theta_out_dev, desc_dev);
   return cuda_status(cudaStreamSynchronize(st));
 }
 

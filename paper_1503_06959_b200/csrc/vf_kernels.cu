@@ -47,6 +47,136 @@ __device__ __forceinline__ void lvl_dims(const Geo& g, int l, int& lw, int& lh)
   else { lw = g.ptw >> o; lh = g.pth >> o; }
 }
 
+// ----------------------------------------------------------------------------
+// Summed-area tables for the descriptor's box means (descriptor.py:28-32,85-92).
+// The reference builds one (H+1) x (W+1) int64 SAT of the frame.  Here:
+//   L(y, x)  = sum of o0 over [Y0, y] x [X0, x] inside its ptw x pth tile
+//   K(y, tx) = sum of o0 over [Y0, y] x [0, X0(tx))        (strip carry)
+// so S(y, x) = L + K is the SAT of the pth-row strip the pixel lies in, and a
+// box sum is 4 strip-SAT corners per strip it spans (<= 2 strips for O = 4).
+// All values < 2^32 and box sums are exact in uint32.
+// ----------------------------------------------------------------------------
+__device__ void sat_tile(const Geo& g, const Bufs& b, int s, int tx, int ty, int tw, int th, const uint8_t* t0,
+                         uint32_t* ssat)
+{
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int per = (g.ptw + 31) / 32;
+  const int X0 = tx * g.ptw, Y0 = ty * g.pth;
+  for (int y = wid; y < th; y += nw) {
+    uint32_t run = 0;
+    const int xb = lane * per;
+    for (int k = 0; k < per; k++) {
+      const int x = xb + k;
+      if (x < tw) run += t0[y * g.ptw + x];
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    uint32_t r = inc - run;
+    for (int k = 0; k < per; k++) {
+      const int x = xb + k;
+      if (x < tw) { r += t0[y * g.ptw + x]; ssat[y * g.ptw + x] = r; }
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < tw; x += nt) {
+    uint32_t run = 0;
+    for (int y = 0; y < th; y++) { run += ssat[y * g.ptw + x]; ssat[y * g.ptw + x] = run; }
+  }
+  __syncthreads();
+  // S(y, x) = L(y, x) + K(y, tx): the SAT of the pth-row strip
+  uint32_t* gs = b.sat + (long long)s * g.W * g.H;
+  const uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx + tx;
+  for (int i = tid; i < th * tw; i += nt) {
+    const int y = i / tw, x = i - y * tw;
+    gs[(long long)(Y0 + y) * g.W + X0 + x] = ssat[y * g.ptw + x] + __ldg(K + (long long)y * g.ptx);
+  }
+}
+
+// Strip carries of strip ty of stream s: one warp, lanes over tile columns
+// (<= 8 chunks of 32 tile columns, i.e. frames up to 24576 px wide).
+#define VF_MAX_TX_CHUNKS 8
+__device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
+{
+  const int lane = threadIdx.x & 31;
+  const int Y0 = ty * g.pth, th = min(g.pth, g.H - Y0);
+  const uint32_t* rs = b.rowsum + ((long long)s * g.H + Y0) * g.ptx;
+  uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx;
+  const int nch = (g.ptx + 31) / 32;
+  uint32_t acc[VF_MAX_TX_CHUNKS];
+#pragma unroll
+  for (int c = 0; c < VF_MAX_TX_CHUNKS; c++) acc[c] = 0;
+  for (int y = 0; y < th; y++) {
+    uint32_t carry = 0;
+#pragma unroll
+    for (int c = 0; c < VF_MAX_TX_CHUNKS; c++) {
+      if (c < nch) {
+        const int t = 32 * c + lane;
+        acc[c] += t < g.ptx ? rs[(long long)y * g.ptx + t] : 0u;
+        uint32_t inc = acc[c];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += v;
+        }
+        if (t < g.ptx) K[(long long)y * g.ptx + t] = carry + inc - acc[c];
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+  }
+}
+
+// Box sum over [x0, x1] x [y0, y1] (inclusive, inside the frame) from the
+// strip SATs S: per strip the box spans, 4 corners (corners above the strip
+// start or left of column 0 are 0).
+__device__ __forceinline__ uint32_t box_sum(const uint32_t* S, const Geo& g, int x0, int x1, int y0, int y1)
+{
+  const int TH = g.pth;
+  int ys = (int)__umulhi((uint32_t)y0, (uint32_t)g.pth_magic) * TH;   // strip start of y0
+  const bool left = x0 > 0;
+  int yb = min(y1, ys + TH - 1);
+  const uint32_t* rb = S + (long long)yb * g.W;
+  uint32_t sum = __ldg(rb + x1) - (left ? __ldg(rb + x0 - 1) : 0u);
+  if (y0 > ys) {
+    const uint32_t* ra = S + (long long)(y0 - 1) * g.W;
+    sum -= __ldg(ra + x1) - (left ? __ldg(ra + x0 - 1) : 0u);
+  }
+  while (yb < y1) {                 // next strip(s): rows start at the strip top
+    ys += TH;
+    yb = min(y1, ys + TH - 1);
+    const uint32_t* r2 = S + (long long)yb * g.W;
+    sum += __ldg(r2 + x1) - (left ? __ldg(r2 + x0 - 1) : 0u);
+  }
+  return sum;
+}
+
+// o0 tile [X0, X0+ptw) x [Y0, Y0+pth) of stream s into smem (pitch ptw),
+// 16-byte loads when the frame rows allow it.
+__device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s, int X0, int Y0, int tw, int th,
+                                             uint8_t* t0)
+{
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const uint8_t* src = b.frames + (long long)s * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)b.frame_pitch) & 15) == 0 && tw == g.ptw;
+  if (vec) {
+    const int per_row = g.ptw / 16;
+    for (int i = tid; i < th * per_row; i += nt) {
+      const int y = i / per_row, c = i - y * per_row;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (long long)y * b.frame_pitch) + c);
+      *reinterpret_cast<uint4*>(t0 + y * g.ptw + 16 * c) = v;
+    }
+  } else {
+    for (int i = tid; i < th * g.ptw; i += nt) {
+      const int y = i / g.ptw, x = i - y * g.ptw;
+      t0[i] = x < tw ? __ldg(src + (long long)y * b.frame_pitch + x) : 0;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -62,31 +192,17 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
     off[l] = acc;
     acc += (lw * lh + 15) & ~15;
   }
-  uint32_t* ssat = reinterpret_cast<uint32_t*>(smem + acc);
 
   if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
     b.ctr[s * C_NCTR + C_STAGE] = 0;
+    b.sat_count[s] = 0;
     if (s == 0) *b.work_count = 0;
   }
 
   // ---- load the o0 tile ------------------------------------------------------
   const int tw = min(g.ptw, g.W - X0), th = min(g.pth, g.H - Y0);
-  const uint8_t* src = b.frames + (long long)s * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
   uint8_t* t0 = smem + off[0];
-  const bool vec = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)b.frame_pitch) & 15) == 0 && tw == g.ptw;
-  if (vec) {
-    const int per_row = g.ptw / 16;
-    for (int i = tid; i < th * per_row; i += nt) {
-      int y = i / per_row, c = i - y * per_row;
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (long long)y * b.frame_pitch) + c);
-      *reinterpret_cast<uint4*>(t0 + y * g.ptw + 16 * c) = v;
-    }
-  } else {
-    for (int i = tid; i < th * g.ptw; i += nt) {
-      int y = i / g.ptw, x = i - y * g.ptw;
-      t0[i] = x < tw ? __ldg(src + (long long)y * b.frame_pitch + x) : 0;
-    }
-  }
+  load_o0_tile(g, b, s, X0, Y0, tw, th, t0);
   __syncthreads();
 
   // ---- derived layers: level by level, octave and intra chains together ------
@@ -102,35 +218,96 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
       if (vw <= 0 || vh <= 0) continue;
       uint8_t* dst = smem + off[l];
       uint8_t* gdst = b.layers + (long long)s * g.layer_slab + g.L[l].layer_off + (long long)gy0 * g.L[l].pitch + gx0;
+      const int gp = g.L[l].pitch;
       if (l == 1) {
         // i0: area-weighted 2/3 resample of o0 (pyramid.py:76-94): per axis
-        // even output 2a+b, odd a+2b, then (v+4)//9.
-        for (int i = tid; i < vw * vh; i += nt) {
-          int y = i / vw, x = i - y * vw;
-          int ky = y >> 1, kx = x >> 1;
-          int ry0 = (y & 1) ? 3 * ky + 1 : 3 * ky, cy0 = (y & 1) ? 1 : 2, cy1 = (y & 1) ? 2 : 1;
-          int rx0 = (x & 1) ? 3 * kx + 1 : 3 * kx, cx0 = (x & 1) ? 1 : 2, cx1 = (x & 1) ? 2 : 1;
-          const uint8_t* r0 = t0 + ry0 * g.ptw;
-          const uint8_t* r1 = r0 + g.ptw;
-          uint32_t a0 = cy0 * r0[rx0] + cy1 * r1[rx0];
-          uint32_t a1 = cy0 * r0[rx0 + 1] + cy1 * r1[rx0 + 1];
-          uint32_t v = cx0 * a0 + cx1 * a1;
-          uint8_t q = (uint8_t)((v + 4) / 9);
-          dst[y * lw + x] = q;
-          gdst[(long long)y * g.L[l].pitch + x] = q;
+        // even output 2a+b, odd a+2b, then (v+4)//9.  A thread makes a 2 x 4
+        // output block from 3 rows x 6 columns.
+        if ((lw & 3) == 0 && (lh & 1) == 0) {
+          const int wpr = lw >> 2, nblk = (lh >> 1) * wpr;
+          for (int i = tid; i < nblk; i += nt) {
+            const int p = i / wpr, q = i - p * wpr;
+            const int base = 6 * q, al = base & ~3, sh = 8 * (base & 3);
+            uint32_t hsum[3][4];
+#pragma unroll
+            for (int r = 0; r < 3; r++) {
+              const uint8_t* row = t0 + (3 * p + r) * g.ptw + al;
+              // base & 3 is 0 or 2, so the aligned 8 bytes al..al+7 cover base..base+5
+              const uint32_t w0 = *reinterpret_cast<const uint32_t*>(row);
+              const uint32_t w1 = *reinterpret_cast<const uint32_t*>(row + 4);
+              const unsigned long long lo = ((unsigned long long)w1 << 32 | w0) >> sh;
+              const uint32_t c0 = lo & 0xff, c1 = (lo >> 8) & 0xff, c2 = (lo >> 16) & 0xff, c3 = (lo >> 24) & 0xff;
+              const uint32_t c4 = (lo >> 32) & 0xff, c5 = (lo >> 40) & 0xff;
+              hsum[r][0] = 2 * c0 + c1; hsum[r][1] = c1 + 2 * c2;
+              hsum[r][2] = 2 * c3 + c4; hsum[r][3] = c4 + 2 * c5;
+            }
+            uint32_t e = 0, o = 0;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+              e |= ((2 * hsum[0][c] + hsum[1][c] + 4) / 9) << (8 * c);
+              o |= ((hsum[1][c] + 2 * hsum[2][c] + 4) / 9) << (8 * c);
+            }
+            const int y = 2 * p, x = 4 * q;
+            *reinterpret_cast<uint32_t*>(dst + y * lw + x) = e;
+            *reinterpret_cast<uint32_t*>(dst + (y + 1) * lw + x) = o;
+            if (x + 4 <= vw) {
+              if (y < vh) *reinterpret_cast<uint32_t*>(gdst + (long long)y * gp + x) = e;
+              if (y + 1 < vh) *reinterpret_cast<uint32_t*>(gdst + (long long)(y + 1) * gp + x) = o;
+            } else {
+              for (int c = 0; c < 4 && x + c < vw; c++) {
+                if (y < vh) gdst[(long long)y * gp + x + c] = (uint8_t)(e >> (8 * c));
+                if (y + 1 < vh) gdst[(long long)(y + 1) * gp + x + c] = (uint8_t)(o >> (8 * c));
+              }
+            }
+          }
+        } else {
+          for (int i = tid; i < vw * vh; i += nt) {
+            int y = i / vw, x = i - y * vw;
+            int ky = y >> 1, kx = x >> 1;
+            int ry0 = (y & 1) ? 3 * ky + 1 : 3 * ky, cy0 = (y & 1) ? 1 : 2, cy1 = (y & 1) ? 2 : 1;
+            int rx0 = (x & 1) ? 3 * kx + 1 : 3 * kx, cx0 = (x & 1) ? 1 : 2, cx1 = (x & 1) ? 2 : 1;
+            const uint8_t* r0 = t0 + ry0 * g.ptw;
+            const uint8_t* r1 = r0 + g.ptw;
+            uint32_t a0 = cy0 * r0[rx0] + cy1 * r1[rx0];
+            uint32_t a1 = cy0 * r0[rx0 + 1] + cy1 * r1[rx0 + 1];
+            uint8_t q = (uint8_t)((cx0 * a0 + cx1 * a1 + 4) / 9);
+            dst[y * lw + x] = q;
+            gdst[(long long)y * gp + x] = q;
+          }
         }
       } else {
-        // halving of the same chain's previous level (pyramid.py:67-73)
+        // halving of the same chain's previous level (pyramid.py:67-73):
+        // 4 outputs per thread, pair sums in 16-bit lanes
         int pl = l - 2, pw, ph;
         lvl_dims(g, pl, pw, ph);
         const uint8_t* sp = smem + off[pl];
-        for (int i = tid; i < vw * vh; i += nt) {
-          int y = i / vw, x = i - y * vw;
-          const uint8_t* r0 = sp + (2 * y) * pw + 2 * x;
-          uint32_t sum = r0[0] + r0[1] + r0[pw] + r0[pw + 1];
-          uint8_t q = (uint8_t)((sum + 2) >> 2);
-          dst[y * lw + x] = q;
-          gdst[(long long)y * g.L[l].pitch + x] = q;
+        if ((lw & 3) == 0) {
+          const int wpr = lw >> 2;
+          for (int i = tid; i < lh * wpr; i += nt) {
+            const int y = i / wpr, q = i - y * wpr;
+            const uint2 r0 = *reinterpret_cast<const uint2*>(sp + (2 * y) * pw + 8 * q);
+            const uint2 r1 = *reinterpret_cast<const uint2*>(sp + (2 * y + 1) * pw + 8 * q);
+            uint32_t a0 = (r0.x & 0x00ff00ffu) + ((r0.x >> 8) & 0x00ff00ffu) + (r1.x & 0x00ff00ffu) + ((r1.x >> 8) & 0x00ff00ffu);
+            uint32_t a1 = (r0.y & 0x00ff00ffu) + ((r0.y >> 8) & 0x00ff00ffu) + (r1.y & 0x00ff00ffu) + ((r1.y >> 8) & 0x00ff00ffu);
+            a0 = ((a0 + 0x00020002u) >> 2) & 0x00ff00ffu;
+            a1 = ((a1 + 0x00020002u) >> 2) & 0x00ff00ffu;
+            const uint32_t wv = __byte_perm(a0, a1, 0x6420);
+            const int x = 4 * q;
+            *reinterpret_cast<uint32_t*>(dst + y * lw + x) = wv;
+            if (y < vh) {
+              if (x + 4 <= vw) *reinterpret_cast<uint32_t*>(gdst + (long long)y * gp + x) = wv;
+              else for (int c = 0; c < 4 && x + c < vw; c++) gdst[(long long)y * gp + x + c] = (uint8_t)(wv >> (8 * c));
+            }
+          }
+        } else {
+          for (int i = tid; i < vw * vh; i += nt) {
+            int y = i / vw, x = i - y * vw;
+            const uint8_t* r0 = sp + (2 * y) * pw + 2 * x;
+            uint32_t sum = r0[0] + r0[1] + r0[pw] + r0[pw + 1];
+            uint8_t q = (uint8_t)((sum + 2) >> 2);
+            dst[y * lw + x] = q;
+            gdst[(long long)y * gp + x] = q;
+          }
         }
       }
     }
@@ -179,42 +356,67 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
     }
   }
 
-  // ---- tile-local summed-area table (descriptor.py:28-32) ---------------------
-  // L(y, x) = sum of o0 over [tile_y0, y] x [tile_x0, x]; box sums decompose
-  // over the <= 4 tiles a box touches (see box_sum).  Values < 2^32.
+  // ---- summed-area data of the descriptor (descriptor.py:28-32) --------------
+  // Per-row sums of this tile feed the strip carries (k_worklist); the strip
+  // SATs themselves are built by k_sat for the tiles the descriptor reads.
   {
+    // per-row sums of the tile (strip carries, see sat_tile): warp per row
     const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-    const int per = (g.ptw + 31) / 32;
+    const int nwd = g.ptw >> 2;
     for (int y = wid; y < th; y += nw) {
-      uint32_t run = 0;
-      int xb = lane * per;
-      for (int k = 0; k < per; k++) {
-        int x = xb + k;
-        if (x < tw) run += t0[y * g.ptw + x];
+      uint32_t acc = 0;
+      for (int k = lane; k < nwd; k += 32) {
+        uint32_t wv = *reinterpret_cast<const uint32_t*>(t0 + y * g.ptw + 4 * k);
+        if (4 * k + 4 > tw) wv &= 4 * k >= tw ? 0u : (0xffffffffu >> (8 * (4 * k + 4 - tw)));
+        acc = __dp4a(wv, 0x01010101u, acc);
       }
-      uint32_t inc = run;
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      uint32_t r = inc - run;
-      for (int k = 0; k < per; k++) {
-        int x = xb + k;
-        if (x < tw) { r += t0[y * g.ptw + x]; ssat[y * g.ptw + x] = r; }
-      }
-    }
-    __syncthreads();
-    for (int x = tid; x < tw; x += nt) {
-      uint32_t run = 0;
-      for (int y = 0; y < th; y++) { run += ssat[y * g.ptw + x]; ssat[y * g.ptw + x] = run; }
-    }
-    __syncthreads();
-    uint32_t* gs = b.sat + (long long)s * g.W * g.H;
-    for (int i = tid; i < th * tw; i += nt) {
-      int y = i / tw, x = i - y * tw;
-      gs[(long long)(Y0 + y) * g.W + X0 + x] = ssat[y * g.ptw + x];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if (lane == 0) b.rowsum[((long long)s * g.H + Y0 + y) * g.ptx + blockIdx.x] = acc;
     }
   }
+}
+
+// ============================================================================
+// k_sat: strip SATs for the descriptor.  Dense frames (no mask): every tile;
+// masked frames: the tiles kept keypoints' footprints touch (marked by k_nms).
+// Persistent CTAs over the per-stream tile lists, flattened.
+// ============================================================================
+__global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, const __grid_constant__ Bufs b, int n_streams)
+{
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* t0 = smem;
+  uint32_t* ssat = reinterpret_cast<uint32_t*>(smem + ((g.ptw * g.pth + 15) & ~15));
+  int* pre = reinterpret_cast<int*>(ssat + g.ptw * g.pth);
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < n_streams; s++) {
+      pre[s] = acc;
+      acc += use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles;
+    }
+    pre[n_streams] = acc;
+  }
+  __syncthreads();
+  const int n = pre[n_streams];
+  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    int lo = 0, hi = n_streams;
+    while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
+    const int s = lo, i = item - pre[s];
+    const int t = use_mask(g, b, s) ? b.sat_work[(long long)s * g.sat_tiles + i] : i;
+    const int ty = t / g.ptx, tx = t - ty * g.ptx;
+    const int X0 = tx * g.ptw, Y0 = ty * g.pth;
+    const int tw = min(g.ptw, g.W - X0), th = min(g.pth, g.H - Y0);
+    load_o0_tile(g, b, s, X0, Y0, tw, th, t0);
+    __syncthreads();
+    sat_tile(g, b, s, tx, ty, tw, th, t0, ssat);
+    __syncthreads();
+  }
+}
+
+// Strip carries for stand-alone use (the pipeline computes them in k_worklist).
+__global__ void k_carries(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  strip_carries(g, b, blockIdx.y, blockIdx.x);
 }
 
 // ============================================================================
@@ -266,14 +468,43 @@ __global__ void __launch_bounds__(1024) k_binmask(const __grid_constant__ Geo g,
 // inactive tiles are never read or written (pipeline.py:104-117 skips).
 // Extra CTAs compute the union coverage in per_layer mode.
 // ============================================================================
+#define PROP_CHUNK 1024
+#define PROP_CTAS 16
 __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
-                                                   int tile_ctas)
+                                                   int tile_ctas, int cov_ctas, int carry_ctas)
 {
   const int s = blockIdx.y;
   const int* ep = b.epoch;
   const int epoch = *ep;
   const int um = use_mask(g, b, s);
   const int lane = threadIdx.x & 31;
+  if ((int)blockIdx.x >= tile_ctas + cov_ctas && (int)blockIdx.x < tile_ctas + cov_ctas + carry_ctas) {
+    const int ty = (blockIdx.x - tile_ctas - cov_ctas) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (ty < g.pty) strip_carries(g, b, s, ty);
+    return;
+  }
+  if ((int)blockIdx.x >= tile_ctas + cov_ctas + carry_ctas) {
+    // Eq. 1 propagation counts: previous features under a 0 mask bit, per
+    // 1024-feature chunk of the previous list (masking.py:176-183)
+    if (!um) return;
+    __shared__ int sm_warp[32];
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int prev = (ctr[C_FRAME] & 1) ^ 1;
+    const int n_prev = ctr[C_NFEAT0 + prev];
+    const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
+    const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
+    for (int c = blockIdx.x - tile_ctas - cov_ctas - carry_ctas; c < nch; c += PROP_CTAS) {
+      int cnt = 0;
+      for (int j = 0; j < PROP_CHUNK / 256; j++) {
+        const int e = c * PROP_CHUNK + j * 256 + threadIdx.x;
+        if (e < n_prev) cnt += !merge_mask_at(g, b, s, b.fx[fb + e], b.fy[fb + e]);
+      }
+      int tot;
+      block_excl_scan<int>(cnt, sm_warp, tot);
+      if (threadIdx.x == 0) b.prop_cnt[(long long)s * g.prop_chunks + c] = tot;
+    }
+    return;
+  }
   if ((int)blockIdx.x >= tile_ctas) {
     // per_layer union coverage: one warp per full-res row (masking.py:44-46)
     if (!um || !g.per_layer) return;
@@ -516,11 +747,18 @@ __global__ void __launch_bounds__(128) k_fast(const __grid_constant__ Geo g, con
 #define NMS_THREADS 128
 #define NMS_ROUND 512
 
+// Score of layer l at (y, x); 0 outside the layer.  Gated pixels score 0
+// (detector.py:112-114): k_fast stores whole active tiles with 0 at gated
+// pixels, and a tile is active iff one of its pixels is gated on, so a pixel
+// reads 0 unless its tile was stamped active this step (um == 0: all active).
 __device__ __forceinline__ int score_read(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x)
 {
   const LayerGeo& Lg = g.L[l];
   if (y < 0 || y >= Lg.h || x < 0 || x >= Lg.w) return 0;
-  if (um && !gate_at(g, b, s, l, y, x)) return 0;    // gated pixels score 0 (detector.py:112-114)
+  if (um) {
+    const int tile = Lg.tile_base + (y / VF_TILE_H) * Lg.tiles_x + x / VF_TILE_W;
+    if (__ldg(b.tile_stamp + (long long)s * g.tiles_per_stream + tile) != um) return 0;
+  }
   return b.scores[(long long)s * g.sm_slab + Lg.sm_off + (long long)y * Lg.pitch + x];
 }
 
@@ -635,6 +873,27 @@ __device__ NmsOut nms_one(const Geo& g, const Bufs& b, int s, int um, int l, int
   return o;
 }
 
+// Mark the SAT tiles a keypoint's descriptor footprint touches: samples lie
+// within 10.8 sigma (+0.5 rounding) of the centre and boxes add <= 1.69 sigma
+// + 0.5 (pattern.py:22-23,58), plus one pixel for the SAT corner.
+__device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int s, double x, double y, double sg,
+                                               int epoch)
+{
+  const int F = (int)ceil(12.5 * sg) + 2;
+  const int xi = (int)x, yi = (int)y;
+  const int xa = max(0, xi - F), xb = min(g.W - 1, xi + F + 1);
+  const int ya = max(0, yi - F), yb = min(g.H - 1, yi + F + 1);
+  for (int ty = ya / g.pth; ty <= yb / g.pth; ty++)
+    for (int tx = xa / g.ptw; tx <= xb / g.ptw; tx++) {
+      int* st = b.sat_stamp + (long long)s * g.sat_tiles + ty * g.ptx + tx;
+      if (*((volatile int*)st) == epoch) continue;
+      if (atomicExch(st, epoch) != epoch) {
+        const int pos = atomicAdd(b.sat_count + s, 1);
+        b.sat_work[(long long)s * g.sat_tiles + pos] = ty * g.ptx + tx;
+      }
+    }
+}
+
 __device__ void nms_last_cta(const Geo& g, const Bufs& b, int s, int* sm_warp)
 {
   // exclusive scans over band records and propagation chunks of stream s
@@ -666,11 +925,14 @@ __device__ void nms_last_cta(const Geo& g, const Bufs& b, int s, int* sm_warp)
   __syncthreads();
   int* pc = b.prop_cnt + (long long)s * g.prop_chunks;
   int* po = b.prop_out + (long long)s * g.prop_chunks;
-  for (int base = 0; base < g.prop_chunks; base += blockDim.x) {
+  const int* ctr0 = b.ctr + s * C_NCTR;
+  const int n_prev = use_mask(g, b, s) ? ctr0[C_NFEAT0 + ((ctr0[C_FRAME] & 1) ^ 1)] : 0;
+  const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
+  for (int base = 0; base < nch; base += blockDim.x) {
     int i = base + tid;
-    int k = i < g.prop_chunks ? __ldcg(pc + i) : 0;
+    int k = i < nch ? __ldcg(pc + i) : 0;
     int ex = block_excl_scan<int>(k, sm_warp, tot);
-    if (i < g.prop_chunks) po[i] = carry + ex;
+    if (i < nch) po[i] = carry + ex;
     __syncthreads();
     if (tid == 0) carry += tot;
     __syncthreads();
@@ -711,9 +973,8 @@ __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo
   __shared__ uint8_t r_f[NMS_ROUND];
   const int s = blockIdx.y, bid = blockIdx.x, tid = threadIdx.x;
   const int epoch = *b.epoch;
-  const int um = use_mask(g, b, s);
+  const int um = use_mask(g, b, s) ? epoch : 0;   // nonzero: tile-stamp gating at this epoch
   int* ctr = b.ctr + s * C_NCTR;
-  const int cur = ctr[C_FRAME] & 1, prev = cur ^ 1;
 
   if (bid < g.bands_per_stream) {
     int* rec = b.band_rec + ((long long)s * g.bands_per_stream + bid) * 4;
@@ -787,6 +1048,7 @@ __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo
               if (r_f[e] & 4) {
                 b.st_x[dst] = r_x[e]; b.st_y[dst] = r_y[e]; b.st_s[dst] = r_s[e]; b.st_v[dst] = r_v[e];
                 dst++;
+                if (um) mark_sat_tiles(g, b, s, r_x[e], r_y[e], r_s[e], epoch);
               }
             }
             int t2;
@@ -801,20 +1063,6 @@ __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo
       }
     }
     if (tid == 0) { rec[0] = base; rec[1] = kept; rec[2] = n_ok; rec[3] = n_drop; }
-  } else {
-    // propagation chunk: count previous features under a 0 mask bit (masking.py:179-183)
-    const int c = bid - g.bands_per_stream;
-    const int n_prev = ctr[C_NFEAT0 + prev];
-    int cnt = 0;
-    if (um) {
-      const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
-      const int e0 = c * 1024 + tid * 8;
-      for (int e = e0; e < min(n_prev, e0 + 8); e++)
-        cnt += !merge_mask_at(g, b, s, b.fx[fb + e], b.fy[fb + e]);
-    }
-    int tot;
-    block_excl_scan<int>(cnt, sm_warp, tot);
-    if (tid == 0) b.prop_cnt[(long long)s * g.prop_chunks + c] = tot;
   }
   // ---- last CTA of the stream scans ----
   __threadfence();
@@ -834,144 +1082,197 @@ __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo
 // k_describe: descriptor.py:85-144 + pipeline.py:164-170 for kept keypoints,
 // and masking.py:179-183 propagation of previous features.
 // ============================================================================
-#define DS_THREADS 128
 
-// Box sum over [x0,x1] x [y0,y1] from the tile-local SATs (mod 2^32 exact).
-__device__ __forceinline__ uint32_t box_sum(const uint32_t* sat, const Geo& g, int x0, int x1, int y0, int y1)
-{
-  uint32_t sum = 0;
-  const int TW = g.ptw, TH = g.pth, W = g.W;
-  for (int ty = y0 / TH; ty <= y1 / TH; ty++) {
-    const int ty0 = ty * TH;
-    const int ya = max(y0, ty0), yb = min(y1, ty0 + TH - 1);
-    for (int tx = x0 / TW; tx <= x1 / TW; tx++) {
-      const int tx0 = tx * TW;
-      const int xa = max(x0, tx0), xb = min(x1, tx0 + TW - 1);
-      uint32_t A = __ldg(sat + (long long)yb * W + xb);
-      uint32_t Bv = ya > ty0 ? __ldg(sat + (long long)(ya - 1) * W + xb) : 0u;
-      uint32_t Cv = xa > tx0 ? __ldg(sat + (long long)yb * W + xa - 1) : 0u;
-      uint32_t Dv = (ya > ty0 && xa > tx0) ? __ldg(sat + (long long)(ya - 1) * W + xa - 1) : 0u;
-      sum += A - Bv - Cv + Dv;
-    }
-  }
-  return sum;
-}
-
-// _box_mean_jit (descriptor.py:85-92) at a sample position
-__device__ __forceinline__ int box_mean(const uint32_t* sat, const Geo& g, long long x, long long y, long long r)
+// _box_mean_jit (descriptor.py:85-92) at a sample position: clamped box,
+// sum // area (exact: float quotient, then a one-step integer correction).
+__device__ __forceinline__ int box_mean(const uint32_t* S, const Geo& g, long long x, long long y, long long r)
 {
   const int x0 = (int)max(x - r, 0LL), x1 = (int)min(x + r, (long long)g.W - 1);
   const int y0 = (int)max(y - r, 0LL), y1 = (int)min(y + r, (long long)g.H - 1);
-  const uint32_t s = box_sum(sat, g, x0, x1, y0, y1);
-  return (int)(s / (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1)));
+  const uint32_t sm = box_sum(S, g, x0, x1, y0, y1);
+  const uint32_t area = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+  uint32_t q = (uint32_t)((float)sm * __frcp_rn((float)area));
+  if (q * area > sm) q--;
+  else if ((q + 1) * area <= sm) q++;
+  return (int)q;
 }
 
-// One keypoint: theta (descriptor.py:128-144) then 512 bits (descriptor.py:117-126).
-__device__ void describe_one(const Geo& g, const uint32_t* sat, double kx, double ky, double sg, int* sv,
-                             double& theta_out, uint32_t bits[16])
+// ---------------------------------------------------------------------------
+// Warp-batched describe: one warp takes up to 32 keypoints.
+//   A. lanes sample (keypoint, point) pairs at theta = 0: 60 box means each
+//      (descriptor.py:94-115 with cos 0 = 1, sin 0 = 0: the rotation is exact)
+//   B. lane k runs keypoint k's orientation sum sequentially in long-pair
+//      order, fp64 without FMA, exactly as _orientations_jit (:128-144)
+//   C. lanes sample the rotated points (cos/sin of keypoint k's theta)
+//   D. 16 __ballot_sync per keypoint build the 512 bits
+//      (_describe_batch_jit :117-126), bit-reversed per byte into the
+//      MSB-first packing of pack_descriptor (:271-275); 16 lanes store 64 B.
+// ---------------------------------------------------------------------------
+#define DW_WARPS 4
+#define DS_THREADS (32 * DW_WARPS)
+#define DW_ROW 61
+
+struct DescWarp {
+  int v[32 * DW_ROW];
+  double kx[32], ky[32], sg[32], cs[32], sn[32];
+  const uint32_t* sat[32];
+};
+
+__device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, int lane, bool rotated)
 {
-  const int stride = DS_THREADS;
-  // pass 1: theta = 0 (cos 0 = 1, sin 0 = 0 make the rotation exact)
-  for (int j = 0; j < VF_NPTS; j++) {
-    long long x = (long long)floor(kx + sg * c_px[j] + 0.5);
-    long long y = (long long)floor(ky + sg * c_py[j] + 0.5);
-    x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
-    y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
-    long long r = (long long)floor(c_rad[j] * sg + 0.5);
-    sv[j * stride] = box_mean(sat, g, x, y, r);
-  }
-  // sequential fp64 sums in long-pair order (no FMA), as _orientations_jit
-  double gx = 0.0, gy = 0.0;
-  const int L = c_nlong;
-  for (int p = 0; p < L; p++) {
-    const double dv = (double)(sv[c_li[p] * stride] - sv[c_lj[p] * stride]);
-    gx += dv * c_wx[p];
-    gy += dv * c_wy[p];
-  }
-  double th = atan2(gy, gx);
-  th = th <= -CUDART_PI ? CUDART_PI : th;
-  theta_out = th;
-  // pass 2: rotated samples
-  double sn, cs;
-  sincos(th, &sn, &cs);
-  for (int j = 0; j < VF_NPTS; j++) {
-    const double px = c_px[j], py = c_py[j];
-    long long x = (long long)floor(kx + sg * (cs * px - sn * py) + 0.5);
-    long long y = (long long)floor(ky + sg * (sn * px + cs * py) + 0.5);
-    x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
-    y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
-    long long r = (long long)floor(c_rad[j] * sg + 0.5);
-    sv[j * stride] = box_mean(sat, g, x, y, r);
-  }
-#pragma unroll
-  for (int q = 0; q < 16; q++) bits[q] = 0;
-  for (int k = 0; k < VF_NBITS; k++) {
-    if (sv[c_si[k] * stride] > sv[c_sj[k] * stride]) {
-      // MSB-first bytes (descriptor.py:271-275): bit k -> byte k>>3, mask 0x80>>(k&7)
-      const int B = k >> 3;
-      bits[B >> 2] |= (0x80u >> (k & 7)) << (8 * (B & 3));
+#pragma unroll 4
+  for (int q = lane; q < nk * VF_NPTS; q += 32) {
+    const int k = q / VF_NPTS, j = q - k * VF_NPTS;
+    const double sg = w.sg[k];
+    double fx, fy;
+    if (rotated) {
+      const double c = w.cs[k], sn = w.sn[k], px = c_px[j], py = c_py[j];
+      fx = w.kx[k] + sg * (c * px - sn * py) + 0.5;
+      fy = w.ky[k] + sg * (sn * px + c * py) + 0.5;
+    } else {
+      fx = w.kx[k] + sg * c_px[j] + 0.5;
+      fy = w.ky[k] + sg * c_py[j] + 0.5;
     }
+    long long x = (long long)floor(fx), y = (long long)floor(fy);
+    x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
+    y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
+    const long long r = (long long)floor(c_rad[j] * sg + 0.5);
+    w.v[k * DW_ROW + j] = box_mean(w.sat[k], g, x, y, r);
   }
 }
 
-__global__ void __launch_bounds__(DS_THREADS) k_describe(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+// theta_given: w.cs/w.sn already hold cos/sin of the caller's angles.
+// Returns theta of lane's keypoint (lane < nk) via *theta_lane; desc_lane[q]
+// (lane q < 16) receives descriptor word q of each keypoint through `emit`.
+template <typename Emit>
+__device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, int nk, int lane, bool theta_given,
+                                              double& theta_lane, Emit emit)
 {
-  __shared__ int sv_all[VF_NPTS * DS_THREADS];
+  if (!theta_given) {
+    sample_pass(g, w, nk, lane, false);
+    __syncwarp();
+    if (lane < nk) {
+      const int* v = w.v + lane * DW_ROW;
+      double gx = 0.0, gy = 0.0;
+      const int L = c_nlong;
+      for (int p = 0; p < L; p++) {
+        const double dv = (double)(v[c_li[p]] - v[c_lj[p]]);
+        gx += dv * c_wx[p];
+        gy += dv * c_wy[p];
+      }
+      double th = atan2(gy, gx);
+      th = th <= -CUDART_PI ? CUDART_PI : th;
+      theta_lane = th;
+      double sn, cs;
+      sincos(th, &sn, &cs);
+      w.cs[lane] = cs;
+      w.sn[lane] = sn;
+    }
+    __syncwarp();
+  }
+  sample_pass(g, w, nk, lane, true);
+  __syncwarp();
+  // per-lane pair indices of bits 32q + lane
+  int pa[16], pb[16];
+#pragma unroll
+  for (int q = 0; q < 16; q++) { pa[q] = c_si[32 * q + lane]; pb[q] = c_sj[32 * q + lane]; }
+  for (int k = 0; k < nk; k++) {
+    const int* v = w.v + k * DW_ROW;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const uint32_t word = __ballot_sync(0xffffffffu, v[pa[q]] > v[pb[q]]);
+      if (lane == q) mine = word;
+    }
+    emit(k, __byte_perm(__brev(mine), 0, 0x0123));
+  }
+}
+
+// Kept keypoints of all streams flattened: global index -> (stream, rank)
+// through the per-stream n_detected prefix, rank -> band by binary search of
+// the band output offsets, band -> staging slot.
+__global__ void __launch_bounds__(DS_THREADS) k_describe(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
+                                                          int n_streams)
+{
+  __shared__ DescWarp ws[DW_WARPS];
+  extern __shared__ int pre[];   // [n_streams + 1]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    int acc = 0;
+    for (int s = 0; s < n_streams; s++) { pre[s] = acc; acc += b.ctr[s * C_NCTR + C_NDET]; }
+    pre[n_streams] = acc;
+  }
+  __syncthreads();
+  const int total = pre[n_streams];
+  DescWarp& w = ws[wid];
+  const int nwarps = gridDim.x * DW_WARPS;
+  for (int base = (blockIdx.x * DW_WARPS + wid) * 32; base < total; base += nwarps * 32) {
+    const int nk = min(32, total - base);
+    long long out_idx = -1, st_idx = 0;
+    if (lane < nk) {
+      const int gi = base + lane;
+      int lo = 0, hi = n_streams;            // last s with pre[s] <= gi
+      while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= gi) lo = m; else hi = m; }
+      const int s = lo, i = gi - pre[s];
+      const int* bout = b.band_out + (long long)s * g.bands_per_stream;
+      int blo = 0, bhi = g.bands_per_stream;  // last band with band_out <= i
+      while (bhi - blo > 1) { int m = (blo + bhi) >> 1; if (__ldg(bout + m) <= i) blo = m; else bhi = m; }
+      const int* rec = b.band_rec + ((long long)s * g.bands_per_stream + blo) * 4;
+      st_idx = (long long)s * g.kp_cap + rec[0] + (i - __ldg(bout + blo));
+      const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
+      out_idx = ((long long)s * 2 + cur) * g.kp_cap + i;
+      w.kx[lane] = b.st_x[st_idx]; w.ky[lane] = b.st_y[st_idx]; w.sg[lane] = b.st_s[st_idx];
+      w.sat[lane] = b.sat + (long long)s * g.W * g.H;
+    }
+    __syncwarp();
+    double th = 0.0;
+    describe_warp(g, w, nk, lane, false, th, [&](int k, uint32_t word) {
+      const long long o = __shfl_sync(0xffffffffu, out_idx, k);
+      if (lane < 16) reinterpret_cast<uint32_t*>(b.fdesc + o * 64)[lane] = word;
+    });
+    if (lane < nk) {
+      b.fx[out_idx] = w.kx[lane]; b.fy[out_idx] = w.ky[lane]; b.fs[out_idx] = w.sg[lane];
+      b.ft[out_idx] = th; b.fv[out_idx] = b.st_v[st_idx];
+      b.forg[out_idx] = 0; b.fage[out_idx] = 0;
+    }
+    __syncwarp();
+  }
+}
+
+// Eq. 1: previous features under a 0 mask bit, in previous-list order, origin
+// -> propagated, age + 1 (masking.py:179-183).  Coalesced 1024-feature chunks.
+__global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
   __shared__ int sm_warp[32];
-  const int s = blockIdx.y, bid = blockIdx.x, tid = threadIdx.x;
+  const int s = blockIdx.y, tid = threadIdx.x;
+  if (!use_mask(g, b, s)) return;
   const int* ctr = b.ctr + s * C_NCTR;
   const int cur = ctr[C_FRAME] & 1, prev = cur ^ 1;
+  const int n_prev = ctr[C_NFEAT0 + prev];
+  const int n_det = ctr[C_NDET];
+  const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
+  const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
   const long long ob = ((long long)s * 2 + cur) * g.kp_cap;
-  if (bid < g.bands_per_stream) {
-    const int* rec = b.band_rec + ((long long)s * g.bands_per_stream + bid) * 4;
-    const int kept = rec[1];
-    if (kept == 0) return;
-    const long long sb = (long long)s * g.kp_cap + rec[0];
-    const int out0 = b.band_out[(long long)s * g.bands_per_stream + bid];
-    const uint32_t* sat = b.sat + (long long)s * g.W * g.H;
-    int* sv = sv_all + tid;
-    for (int i = tid; i < kept; i += DS_THREADS) {
-      const double kx = b.st_x[sb + i], ky = b.st_y[sb + i], sg = b.st_s[sb + i];
-      double th;
-      uint32_t bits[16];
-      describe_one(g, sat, kx, ky, sg, sv, th, bits);
-      const long long o = ob + out0 + i;
-      if (out0 + i >= g.kp_cap) continue;
-      b.fx[o] = kx; b.fy[o] = ky; b.fs[o] = sg; b.ft[o] = th; b.fv[o] = b.st_v[sb + i];
-      b.forg[o] = 0; b.fage[o] = 0;
-      uint4* d = reinterpret_cast<uint4*>(b.fdesc + o * 64);
-      d[0] = make_uint4(bits[0], bits[1], bits[2], bits[3]);
-      d[1] = make_uint4(bits[4], bits[5], bits[6], bits[7]);
-      d[2] = make_uint4(bits[8], bits[9], bits[10], bits[11]);
-      d[3] = make_uint4(bits[12], bits[13], bits[14], bits[15]);
-    }
-  } else {
-    // Eq. 1: previous features under a 0 mask bit, in previous-list order,
-    // origin -> propagated, age + 1 (masking.py:179-183)
-    if (!use_mask(g, b, s)) return;
-    const int c = bid - g.bands_per_stream;
-    const int n_prev = ctr[C_NFEAT0 + prev];
-    if (c * 1024 >= n_prev) return;
-    const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
-    const int e0 = c * 1024 + tid * 8, e1 = min(n_prev, e0 + 8);
-    uint32_t flags = 0;
-    int cnt = 0;
-    for (int e = e0; e < e1; e++)
-      if (!merge_mask_at(g, b, s, b.fx[fb + e], b.fy[fb + e])) { flags |= 1u << (e - e0); cnt++; }
-    int tot;
-    int ex = block_excl_scan<int>(cnt, sm_warp, tot);
-    long long dst = (long long)ctr[C_NDET] + b.prop_out[(long long)s * g.prop_chunks + c] + ex;
-    for (int e = e0; e < e1; e++) {
-      if (!(flags & (1u << (e - e0)))) continue;
-      if (dst < g.kp_cap) {
-        const long long o = ob + dst, p = fb + e;
-        b.fx[o] = b.fx[p]; b.fy[o] = b.fy[p]; b.fs[o] = b.fs[p]; b.ft[o] = b.ft[p]; b.fv[o] = b.fv[p];
-        b.forg[o] = 1; b.fage[o] = b.fage[p] + 1;
-        const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + p * 64);
-        uint4* dd = reinterpret_cast<uint4*>(b.fdesc + o * 64);
-        dd[0] = sd[0]; dd[1] = sd[1]; dd[2] = sd[2]; dd[3] = sd[3];
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
+    for (int j = 0; j < PROP_CHUNK / 256; j++) {
+      const int e = c * PROP_CHUNK + j * 256 + tid;
+      int f = 0;
+      if (e < n_prev) f = !merge_mask_at(g, b, s, b.fx[fb + e], b.fy[fb + e]);
+      int tot;
+      const int ex = block_excl_scan<int>(f, sm_warp, tot);
+      if (f) {
+        const long long dst = dst0 + ex;
+        if (dst < g.kp_cap) {
+          const long long o = ob + dst, p = fb + e;
+          b.fx[o] = b.fx[p]; b.fy[o] = b.fy[p]; b.fs[o] = b.fs[p]; b.ft[o] = b.ft[p]; b.fv[o] = b.fv[p];
+          b.forg[o] = 1; b.fage[o] = b.fage[p] + 1;
+          const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + p * 64);
+          uint4* dd = reinterpret_cast<uint4*>(b.fdesc + o * 64);
+          dd[0] = sd[0]; dd[1] = sd[1]; dd[2] = sd[2]; dd[3] = sd[3];
+        }
       }
-      dst++;
+      dst0 += tot;
     }
   }
 }
@@ -1042,49 +1343,33 @@ __global__ void k_mask_values(const uint8_t* full, int W, int H, int n, const do
 }
 
 // orientations_batch / describe_batch (descriptor.py:194-232) on caller keypoints.
-// theta_in == nullptr: estimate orientation, else describe at the given angles.
+// theta_in == nullptr: estimate orientation first; else describe at the given angles.
 __global__ void __launch_bounds__(DS_THREADS) k_describe_batch(const __grid_constant__ Geo g, const uint32_t* sat, int n,
                                                                const double* kx, const double* ky, const double* sg,
                                                                const double* theta_in, double* theta_out, uint8_t* desc)
 {
-  __shared__ int sv_all[VF_NPTS * DS_THREADS];
-  const int i = blockIdx.x * DS_THREADS + threadIdx.x;
-  if (i >= n) return;
-  int* sv = sv_all + threadIdx.x;
-  double th;
-  uint32_t bits[16];
-  if (theta_in == nullptr) {
-    describe_one(g, sat, kx[i], ky[i], sg[i], sv, th, bits);
-    if (theta_out) theta_out[i] = th;
-    if (desc) {
-      uint4* d = reinterpret_cast<uint4*>(desc + (long long)i * 64);
-      for (int q = 0; q < 4; q++) d[q] = make_uint4(bits[4 * q], bits[4 * q + 1], bits[4 * q + 2], bits[4 * q + 3]);
+  __shared__ DescWarp ws[DW_WARPS];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  DescWarp& w = ws[wid];
+  const int base = (blockIdx.x * DW_WARPS + wid) * 32;
+  if (base >= n) return;
+  const int nk = min(32, n - base);
+  double th = 0.0;
+  if (lane < nk) {
+    w.kx[lane] = kx[base + lane]; w.ky[lane] = ky[base + lane]; w.sg[lane] = sg[base + lane];
+    w.sat[lane] = sat;
+    if (theta_in) {
+      th = theta_in[base + lane];
+      double sn, cs;
+      sincos(th, &sn, &cs);
+      w.cs[lane] = cs; w.sn[lane] = sn;
     }
-    return;
   }
-  // describe at a given theta: reuse pass 2 of describe_one
-  const double t = theta_in[i];
-  double sn, cs;
-  sincos(t, &sn, &cs);
-  const int stride = DS_THREADS;
-  for (int j = 0; j < VF_NPTS; j++) {
-    const double px = c_px[j], py = c_py[j];
-    long long x = (long long)floor(kx[i] + sg[i] * (cs * px - sn * py) + 0.5);
-    long long y = (long long)floor(ky[i] + sg[i] * (sn * px + cs * py) + 0.5);
-    x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
-    y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
-    long long r = (long long)floor(c_rad[j] * sg[i] + 0.5);
-    sv[j * stride] = box_mean(sat, g, x, y, r);
-  }
-  for (int q = 0; q < 16; q++) bits[q] = 0;
-  for (int k = 0; k < VF_NBITS; k++)
-    if (sv[c_si[k] * stride] > sv[c_sj[k] * stride]) {
-      const int B = k >> 3;
-      bits[B >> 2] |= (0x80u >> (k & 7)) << (8 * (B & 3));
-    }
-  if (theta_out) theta_out[i] = t;
-  uint4* d = reinterpret_cast<uint4*>(desc + (long long)i * 64);
-  for (int q = 0; q < 4; q++) d[q] = make_uint4(bits[4 * q], bits[4 * q + 1], bits[4 * q + 2], bits[4 * q + 3]);
+  __syncwarp();
+  describe_warp(g, w, nk, lane, theta_in != nullptr, th, [&](int k, uint32_t word) {
+    if (desc && lane < 16) reinterpret_cast<uint32_t*>(desc + (long long)(base + k) * 64)[lane] = word;
+  });
+  if (lane < nk && theta_out) theta_out[base + lane] = th;
 }
 
 // Candidate bitmap from caller score maps (nms_and_refine, detector.py:310-324):

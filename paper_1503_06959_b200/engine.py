@@ -139,6 +139,19 @@ class FeatureEngine:
         out["n"] = n
         return out
 
+    STAGES = ("binmask", "pyramid", "worklist", "fast", "nms", "sat", "describe", "propagate", "finalize")
+
+    def set_timing(self, enable: bool) -> None:
+        _native.check(_native.lib().vf_set_timing(self._h, int(enable)))
+
+    def stage_ms(self, stream=None) -> tuple[dict, int]:
+        """Summed per-stage device ms since the last call, and the step count."""
+        out = np.zeros(len(self.STAGES), np.float64)
+        n = ctypes.c_int32(0)
+        _native.check(_native.lib().vf_get_stage_ms(self._h, out.ctypes.data, ctypes.byref(n),
+                                                    _native.stream_handle(stream)))
+        return dict(zip(self.STAGES, out.tolist())), int(n.value)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             _native.lib().vf_destroy(self._h)
