@@ -306,6 +306,7 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     stage, n_steps = eng.stage_ms()
+    diag = eng.diag()
     eng.set_timing(False)
     t_after = np.array([eng.totals(s) for s in range(S)])
     d = t_after - t_before  # per stream: sum n_det, sum n_total, sum coverage, frames
@@ -394,6 +395,7 @@ def main():
         "step": {"algorithmic_bytes_per_step": b_alg / K, "achieved": step_achieved,
                  "frac": step_achieved / peak},
         "stage_ms_per_step": {k: v / max(n_steps, 1) for k, v in stage.items()},
+        "work_last_step": diag,
     }
 
     # ---- CPU baseline: oracle port on the host cores, bounded sample (rank 0, N = 1) ----

@@ -122,6 +122,10 @@ int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch)
  * stage since the last query and the number of steps, and clears. */
 int vf_set_timing(vf_ctx *ctx, int enable);
 int vf_get_stage_ms(vf_ctx *ctx, double *ms9, int32_t *n_steps, void *stream);
+/* Synchronizes `stream`; work counters of the last step: active FAST tiles,
+ * total FAST tiles, SAT tiles built, total SAT tiles, unmasked streams,
+ * staged NMS candidates, bands per stream, feature capacity. */
+int vf_get_diag(vf_ctx *ctx, int64_t *out8, void *stream);
 /* Per-stream totals since vf_create/vf_reset: sum n_detected, sum n_total, sum coverage, frames. */
 int vf_get_totals(vf_ctx *ctx, int s, double *out4, void *stream);
 

@@ -158,7 +158,7 @@ int pyramid_smem(const Geo& g)
     else { lw = g.ptw >> o; lh = g.pth >> o; }
     acc += (lw * lh + 15) & ~15;
   }
-  return acc;
+  return acc + g.pth * 4;   // + row-sum accumulators
 }
 
 int g_num_sms = 0;
@@ -436,7 +436,7 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   stage_mark(c, 3, st);
   k_fast<<<c->fast_grid, 128, 0, st>>>(g, b);
   stage_mark(c, 4, st);
-  k_nms<<<dim3(g.bands_per_stream, n), NMS_THREADS, 0, st>>>(g, b);
+  k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
   stage_mark(c, 6, st);
@@ -559,6 +559,35 @@ int vf_copy_features(vf_ctx* c, int s, int32_t cap, double* x, double* y, double
   if (age) cudaMemcpyAsync(age, f.age, 4 * n, cudaMemcpyDeviceToHost, st);
   if (desc) cudaMemcpyAsync(desc, f.desc, 64 * n, cudaMemcpyDeviceToHost, st);
   return cuda_status(cudaStreamSynchronize(st));
+}
+
+int vf_get_diag(vf_ctx* c, int64_t* out8, void* stream)
+{
+  if (!c || !out8) return VF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int wc = 0;
+  std::vector<int> sc(c->S), ctr((size_t)c->S * C_NCTR);
+  cudaMemcpyAsync(&wc, c->b.work_count, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(sc.data(), c->b.sat_count, sizeof(int) * c->S, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(ctr.data(), c->b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  long long sat = 0, dense = 0, stage = 0;
+  for (int s = 0; s < c->S; s++) {
+    // frame counter already advanced: the last step was masked iff frame >= 2 (or mode none => dense)
+    const bool masked = c->g.mask_mode != 0 && ctr[(size_t)s * C_NCTR + C_FRAME] >= 2;
+    if (masked) sat += sc[s]; else { sat += c->g.sat_tiles; dense++; }
+    stage += ctr[(size_t)s * C_NCTR + C_STAGE];
+  }
+  out8[0] = wc;                                   // active FAST tiles (all streams)
+  out8[1] = (long long)c->g.tiles_per_stream * c->S;  // FAST tiles in total
+  out8[2] = sat;                                  // SAT tiles built
+  out8[3] = (long long)c->g.sat_tiles * c->S;     // SAT tiles in total
+  out8[4] = dense;                                // streams whose last frame was unmasked
+  out8[5] = stage;                                // NMS candidates staged
+  out8[6] = c->g.bands_per_stream;
+  out8[7] = c->g.kp_cap;
+  return VF_OK;
 }
 
 int vf_get_layer(vf_ctx* c, int s, int l, const uint8_t** ptr, int32_t* pitch)
@@ -700,7 +729,7 @@ int vf_nms_refine(const uint8_t* const* maps_dev, const int64_t* pitches, int W,
   std::vector<int> ones(std::max(g.tiles_per_stream, g.bands_per_stream), 1);
   cudaMemcpyAsync(b.tile_stamp, ones.data(), sizeof(int) * g.tiles_per_stream, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.band_stamp, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
-  k_nms<<<dim3(g.bands_per_stream, 1), NMS_THREADS, 0, st>>>(g, b);
+  k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), 1), NMS_THREADS, 0, st>>>(g, b);
   k_gather_kps<<<g.bands_per_stream, 128, 0, st>>>(g, b, x_dev, y_dev, sigma_dev, score_dev, cap);
   int ctr[C_NCTR];
   cudaMemcpyAsync(ctr, b.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st);

@@ -156,8 +156,9 @@ __device__ __forceinline__ uint32_t box_sum(const uint32_t* S, const Geo& g, int
 
 // o0 tile [X0, X0+ptw) x [Y0, Y0+pth) of stream s into smem (pitch ptw),
 // 16-byte loads when the frame rows allow it.
+// rowsum (nullable, zeroed smem [pth]) accumulates the tile's per-row sums.
 __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s, int X0, int Y0, int tw, int th,
-                                             uint8_t* t0)
+                                             uint8_t* t0, uint32_t* rowsum = nullptr)
 {
   const int tid = threadIdx.x, nt = blockDim.x;
   const uint8_t* src = b.frames + (long long)s * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
@@ -168,11 +169,20 @@ __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s,
       const int y = i / per_row, c = i - y * per_row;
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (long long)y * b.frame_pitch) + c);
       *reinterpret_cast<uint4*>(t0 + y * g.ptw + 16 * c) = v;
+      if (rowsum) {
+        uint32_t a = __dp4a(v.x, 0x01010101u, 0u);
+        a = __dp4a(v.y, 0x01010101u, a);
+        a = __dp4a(v.z, 0x01010101u, a);
+        a = __dp4a(v.w, 0x01010101u, a);
+        atomicAdd(rowsum + y, a);
+      }
     }
   } else {
     for (int i = tid; i < th * g.ptw; i += nt) {
       const int y = i / g.ptw, x = i - y * g.ptw;
-      t0[i] = x < tw ? __ldg(src + (long long)y * b.frame_pitch + x) : 0;
+      const uint8_t v = x < tw ? __ldg(src + (long long)y * b.frame_pitch + x) : 0;
+      t0[i] = v;
+      if (rowsum && v) atomicAdd(rowsum + y, (uint32_t)v);
     }
   }
 }
@@ -202,7 +212,10 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
   // ---- load the o0 tile ------------------------------------------------------
   const int tw = min(g.ptw, g.W - X0), th = min(g.pth, g.H - Y0);
   uint8_t* t0 = smem + off[0];
-  load_o0_tile(g, b, s, X0, Y0, tw, th, t0);
+  uint32_t* rsum = reinterpret_cast<uint32_t*>(smem + acc);   // [pth] row sums of the tile
+  for (int y = tid; y < g.pth; y += nt) rsum[y] = 0;
+  __syncthreads();
+  load_o0_tile(g, b, s, X0, Y0, tw, th, t0, rsum);
   __syncthreads();
 
   // ---- derived layers: level by level, octave and intra chains together ------
@@ -359,22 +372,25 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
   // ---- summed-area data of the descriptor (descriptor.py:28-32) --------------
   // Per-row sums of this tile feed the strip carries (k_worklist); the strip
   // SATs themselves are built by k_sat for the tiles the descriptor reads.
-  {
-    // per-row sums of the tile (strip carries, see sat_tile): warp per row
-    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-    const int nwd = g.ptw >> 2;
-    for (int y = wid; y < th; y += nw) {
-      uint32_t acc = 0;
-      for (int k = lane; k < nwd; k += 32) {
-        uint32_t wv = *reinterpret_cast<const uint32_t*>(t0 + y * g.ptw + 4 * k);
-        if (4 * k + 4 > tw) wv &= 4 * k >= tw ? 0u : (0xffffffffu >> (8 * (4 * k + 4 - tw)));
-        acc = __dp4a(wv, 0x01010101u, acc);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-      if (lane == 0) b.rowsum[((long long)s * g.H + Y0 + y) * g.ptx + blockIdx.x] = acc;
-    }
+  for (int y = tid; y < th; y += nt) b.rowsum[((long long)s * g.H + Y0 + y) * g.ptx + blockIdx.x] = rsum[y];
+}
+
+// Exclusive prefix over streams of a per-stream count, computed by the whole
+// block (one load per thread), into pre[0..n_streams].
+template <typename F>
+__device__ __forceinline__ void stream_prefix(int n_streams, int* pre, int* sm_warp, F count)
+{
+  int carry = 0;
+  for (int base = 0; base < n_streams; base += blockDim.x) {
+    const int s = base + threadIdx.x;
+    const int v = s < n_streams ? count(s) : 0;
+    int tot;
+    const int ex = block_excl_scan<int>(v, sm_warp, tot);
+    if (s < n_streams) pre[s] = carry + ex;
+    carry += tot;
   }
+  if (threadIdx.x == 0) pre[n_streams] = carry;
+  __syncthreads();
 }
 
 // ============================================================================
@@ -388,15 +404,8 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
   uint8_t* t0 = smem;
   uint32_t* ssat = reinterpret_cast<uint32_t*>(smem + ((g.ptw * g.pth + 15) & ~15));
   int* pre = reinterpret_cast<int*>(ssat + g.ptw * g.pth);
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int s = 0; s < n_streams; s++) {
-      pre[s] = acc;
-      acc += use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles;
-    }
-    pre[n_streams] = acc;
-  }
-  __syncthreads();
+  __shared__ int sm_warp[32];
+  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles; });
   const int n = pre[n_streams];
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     int lo = 0, hi = n_streams;
@@ -744,8 +753,6 @@ __global__ void __launch_bounds__(128) k_fast(const __grid_constant__ Geo g, con
 // Eq. 1 merge filter (masking.py:176-178, applied before describing: a
 // dropped detection's descriptor is never observable).  The last CTA of each
 // stream scans band counts and propagation-chunk counts into offsets.
-#define NMS_THREADS 128
-#define NMS_ROUND 512
 
 // Score of layer l at (y, x); 0 outside the layer.  Gated pixels score 0
 // (detector.py:112-114): k_fast stores whole active tiles with 0 at gated
@@ -894,187 +901,173 @@ __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int 
     }
 }
 
-__device__ void nms_last_cta(const Geo& g, const Bufs& b, int s, int* sm_warp)
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
 {
-  // exclusive scans over band records and propagation chunks of stream s
-  __shared__ int carry;
-  const int tid = threadIdx.x;
-  int* rec = b.band_rec + (long long)s * g.bands_per_stream * 4;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// Last warp of stream s: band offsets, propagation-chunk offsets, FrameReport.
+__device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
+{
+  const int* rec = b.band_rec + (long long)s * g.bands_per_stream * 4;
   int* bout = b.band_out + (long long)s * g.bands_per_stream;
-  int tot;
-  if (tid == 0) carry = 0;
-  __syncthreads();
-  int n_drop = 0, n_surv = 0;
-  for (int base = 0; base < g.bands_per_stream; base += blockDim.x) {
-    int i = base + tid;
+  int carry = 0, n_drop = 0, n_surv = 0, tot;
+  for (int base = 0; base < g.bands_per_stream; base += 32) {
+    const int i = base + lane;
     int k = 0;
     if (i < g.bands_per_stream) {
-      k = __ldcg(rec + 4 * i + 1);
-      n_drop += __ldcg(rec + 4 * i + 3);
-      n_surv += __ldcg(rec + 4 * i + 2) + __ldcg(rec + 4 * i + 3);
+      const int4 r = __ldcg(reinterpret_cast<const int4*>(rec) + i);
+      k = r.y;
+      n_drop += r.w;
+      n_surv += r.z + r.w;
     }
-    int ex = block_excl_scan<int>(k, sm_warp, tot);
+    const int ex = warp_excl_scan(k, lane, tot);
     if (i < g.bands_per_stream) bout[i] = carry + ex;
-    __syncthreads();
-    if (tid == 0) carry += tot;
-    __syncthreads();
+    carry += tot;
   }
   const int n_det = carry;
-  __syncthreads();
-  if (tid == 0) carry = 0;
-  __syncthreads();
+  carry = 0;
   int* pc = b.prop_cnt + (long long)s * g.prop_chunks;
   int* po = b.prop_out + (long long)s * g.prop_chunks;
   const int* ctr0 = b.ctr + s * C_NCTR;
   const int n_prev = use_mask(g, b, s) ? ctr0[C_NFEAT0 + ((ctr0[C_FRAME] & 1) ^ 1)] : 0;
   const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
-  for (int base = 0; base < nch; base += blockDim.x) {
-    int i = base + tid;
-    int k = i < nch ? __ldcg(pc + i) : 0;
-    int ex = block_excl_scan<int>(k, sm_warp, tot);
+  for (int base = 0; base < nch; base += 32) {
+    const int i = base + lane;
+    const int k = i < nch ? __ldcg(pc + i) : 0;
+    const int ex = warp_excl_scan(k, lane, tot);
     if (i < nch) po[i] = carry + ex;
-    __syncthreads();
-    if (tid == 0) carry += tot;
-    __syncthreads();
+    carry += tot;
   }
   const int n_prop = carry;
-  // block reduce n_drop, n_surv
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n_drop += __shfl_down_sync(0xffffffffu, n_drop, o);
     n_surv += __shfl_down_sync(0xffffffffu, n_surv, o);
   }
-  __shared__ int red[2][32];
-  if ((tid & 31) == 0) { red[0][tid >> 5] = n_drop; red[1][tid >> 5] = n_surv; }
-  __syncthreads();
-  if (tid == 0) {
-    int d = 0, sv = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) { d += red[0][w]; sv += red[1][w]; }
+  if (lane == 0) {
     int* ctr = b.ctr + s * C_NCTR;
     int n_total = n_det + n_prop;
     if (n_total > g.kp_cap) { ctr[C_ERR] |= VF_ERRBIT_CAPACITY; n_total = g.kp_cap; }
-    ctr[C_NDET] = n_det; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = d;
-    ctr[C_NSURV] = sv;
+    ctr[C_NDET] = n_det; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
+    ctr[C_NSURV] = n_surv;
     ctr[C_TICKET] = 0;
     const int um = use_mask(g, b, s);
-    double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
+    const double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
     double* rp = b.report + (long long)s * 16;
-    rp[0] = n_det; rp[1] = n_prop; rp[2] = n_total; rp[3] = d; rp[4] = cov;
-    rp[5] = ctr[C_FRAME]; rp[6] = sv; rp[7] = __ldcg(&ctr[C_NCAND]);
+    rp[0] = n_det; rp[1] = n_prop; rp[2] = n_total; rp[3] = n_drop; rp[4] = cov;
+    rp[5] = ctr[C_FRAME]; rp[6] = n_surv; rp[7] = __ldcg(&ctr[C_NCAND]);
     rp[8] += n_det; rp[9] += n_total; rp[10] += cov; rp[11] += 1.0;
   }
 }
 
+// One warp per band (8 rows of one layer).  Candidates come from the FAST
+// bitmap: lane l owns a contiguous run of bitmap words, so a warp scan gives
+// every candidate its row-major rank.  Candidates are processed 32 at a time
+// (lane = candidate) and the kept ones are compacted in rank order with
+// ballots, so each band emits keypoints in (y, x) order and bands are ordered
+// (layer, y): the reference order.
+#define NMS_WARPS 4
+#define NMS_THREADS (32 * NMS_WARPS)
 __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
-  __shared__ int sm_warp[32];
-  __shared__ int sh_base, sh_last;
-  __shared__ int cand_yx[NMS_ROUND];
-  __shared__ double r_x[NMS_ROUND], r_y[NMS_ROUND], r_s[NMS_ROUND], r_v[NMS_ROUND];
-  __shared__ uint8_t r_f[NMS_ROUND];
-  const int s = blockIdx.y, bid = blockIdx.x, tid = threadIdx.x;
+  __shared__ int cand[NMS_WARPS][32];
+  const int s = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int bid = blockIdx.x * NMS_WARPS + wid;
+  if (bid >= g.bands_per_stream) return;
   const int epoch = *b.epoch;
   const int um = use_mask(g, b, s) ? epoch : 0;   // nonzero: tile-stamp gating at this epoch
   int* ctr = b.ctr + s * C_NCTR;
-
-  if (bid < g.bands_per_stream) {
-    int* rec = b.band_rec + ((long long)s * g.bands_per_stream + bid) * 4;
-    int kept = 0, n_ok = 0, n_drop = 0, base = 0;
-    if (b.band_stamp[(long long)s * g.bands_per_stream + bid] == epoch) {
-      int l = 0;
-      while (l + 1 < g.NL && bid >= g.L[l + 1].band_base) l++;
-      const LayerGeo& Lg = g.L[l];
-      const int ty = bid - Lg.band_base;
-      const int y0 = ty * VF_TILE_H, nrows = min(Lg.h - y0, VF_TILE_H);
-      const int nwords = nrows * Lg.bm_words;
-      const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)y0 * Lg.bm_words;
-      const int* tst = b.tile_stamp + (long long)s * g.tiles_per_stream + Lg.tile_base + ty * Lg.tiles_x;
-      const int per = (nwords + NMS_THREADS - 1) / NMS_THREADS;
-      const int w0 = tid * per, w1 = min(nwords, w0 + per);
-      int cnt = 0;
-      for (int i = w0; i < w1; i++) {
-        const int k = i % Lg.bm_words;
-        if (tst[k / VF_TILE_WORDS] == epoch) cnt += __popc(__ldcg(bm + i));
+  int kept = 0, n_ok = 0, n_drop = 0, base = 0;
+  if (b.band_stamp[(long long)s * g.bands_per_stream + bid] == epoch) {
+    int l = 0;
+    while (l + 1 < g.NL && bid >= g.L[l + 1].band_base) l++;
+    const LayerGeo& Lg = g.L[l];
+    const int ty = bid - Lg.band_base;
+    const int y0 = ty * VF_TILE_H, nrows = min(Lg.h - y0, VF_TILE_H);
+    const int nwords = nrows * Lg.bm_words;
+    const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)y0 * Lg.bm_words;
+    const int* tst = b.tile_stamp + (long long)s * g.tiles_per_stream + Lg.tile_base + ty * Lg.tiles_x;
+    const int per = (nwords + 31) / 32;
+    const int w0 = lane * per, w1 = min(nwords, w0 + per);
+    int cnt = 0;
+    for (int i = w0; i < w1; i++) {
+      const int k = i % Lg.bm_words;
+      if (__ldg(tst + k / VF_TILE_WORDS) == epoch) cnt += __popc(__ldg(bm + i));
+    }
+    int total;
+    const int ex = warp_excl_scan(cnt, lane, total);
+    if (total > 0) {
+      int bs = 0;
+      if (lane == 0) {
+        bs = atomicAdd(&ctr[C_STAGE], total);
+        if (bs + total > g.kp_cap) { atomicOr(&ctr[C_ERR], VF_ERRBIT_STAGING); bs = -1; }
       }
-      int total;
-      const int ex = block_excl_scan<int>(cnt, sm_warp, total);
-      if (total > 0) {
-        if (tid == 0) {
-          int bs = atomicAdd(&ctr[C_STAGE], total);
-          if (bs + total > g.kp_cap) { atomicOr(&ctr[C_ERR], VF_ERRBIT_STAGING); bs = -1; }
-          sh_base = bs;
-        }
-        __syncthreads();
-        base = sh_base;
-        if (base >= 0) {
-          for (int r0 = 0; r0 < total; r0 += NMS_ROUND) {
-            // enumerate this round's candidates in row-major order
-            int idx = ex;
-            for (int i = w0; i < w1 && idx < r0 + NMS_ROUND; i++) {
-              const int k = i % Lg.bm_words;
-              if (tst[k / VF_TILE_WORDS] != epoch) continue;
-              uint32_t word = __ldcg(bm + i);
-              while (word) {
-                const int bit = __ffs(word) - 1;
-                word &= word - 1;
-                if (idx >= r0 && idx < r0 + NMS_ROUND) {
-                  const int yy = y0 + i / Lg.bm_words, xx = 32 * k + bit;
-                  cand_yx[idx - r0] = (yy << 16) | xx;
-                }
-                idx++;
-              }
+      base = __shfl_sync(0xffffffffu, bs, 0);
+      if (base >= 0) {
+        auto load_word = [&](int i) -> uint32_t {
+          return (__ldg(tst + (i % Lg.bm_words) / VF_TILE_WORDS) == epoch) ? __ldg(bm + i) : 0u;
+        };
+        int cursor = w0, idx = ex;             // this lane's enumeration state
+        uint32_t pend = cursor < w1 ? load_word(cursor) : 0u;
+        for (int r0 = 0; r0 < total; r0 += 32) {
+          // emit this round's candidates (ranks r0 .. r0+31) into cand[]
+          while (idx < r0 + 32 && cursor < w1) {
+            if (!pend) {
+              cursor++;
+              pend = cursor < w1 ? load_word(cursor) : 0u;
+              continue;
             }
-            __syncthreads();
-            const int nr = min(NMS_ROUND, total - r0);
-            for (int e = tid; e < nr; e += NMS_THREADS) {
-              const int yx = cand_yx[e];
-              NmsOut o = nms_one(g, b, s, um, l, yx >> 16, yx & 0xffff);
-              r_x[e] = o.x; r_y[e] = o.y; r_s[e] = o.sig; r_v[e] = o.v; r_f[e] = (uint8_t)o.flags;
-            }
-            __syncthreads();
-            // ordered compaction of kept entries
-            const int per2 = (nr + NMS_THREADS - 1) / NMS_THREADS;
-            const int e0 = tid * per2, e1 = min(nr, e0 + per2);
-            int kc = 0, okc = 0, dc = 0;
-            for (int e = e0; e < e1; e++) {
-              const int f = r_f[e];
-              kc += (f >> 2) & 1;
-              okc += (f >> 1) & 1;
-              dc += (f & 1) && !(f & 2);
-            }
-            int rtot;
-            int kex = block_excl_scan<int>(kc, sm_warp, rtot);
-            long long dst = (long long)s * g.kp_cap + base + kept + kex;
-            for (int e = e0; e < e1; e++) {
-              if (r_f[e] & 4) {
-                b.st_x[dst] = r_x[e]; b.st_y[dst] = r_y[e]; b.st_s[dst] = r_s[e]; b.st_v[dst] = r_v[e];
-                dst++;
-                if (um) mark_sat_tiles(g, b, s, r_x[e], r_y[e], r_s[e], epoch);
-              }
-            }
-            int t2;
-            okc = block_excl_scan<int>(okc, sm_warp, t2), n_ok += t2;
-            dc = block_excl_scan<int>(dc, sm_warp, t2), n_drop += t2;
-            kept += rtot;
-            __syncthreads();
+            const int bit = __ffs(pend) - 1;
+            pend &= pend - 1;
+            if (idx >= r0)
+              cand[wid][idx - r0] = ((y0 + cursor / Lg.bm_words) << 16) | (32 * (cursor % Lg.bm_words) + bit);
+            idx++;
           }
-        } else {
-          base = 0;
+          __syncwarp();
+          const int nr = min(32, total - r0);
+          NmsOut o;
+          o.flags = 0;
+          if (lane < nr) {
+            const int yx = cand[wid][lane];
+            o = nms_one(g, b, s, um, l, yx >> 16, yx & 0xffff);
+          }
+          __syncwarp();
+          const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
+          n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
+          n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
+          if (o.flags & 4) {
+            const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
+            b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
+            if (um) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
+          }
+          kept += __popc(kb);
         }
+      } else {
+        base = 0;
       }
     }
-    if (tid == 0) { rec[0] = base; rec[1] = kept; rec[2] = n_ok; rec[3] = n_drop; }
   }
-  // ---- last CTA of the stream scans ----
+  if (lane == 0) {
+    int4* rec = reinterpret_cast<int4*>(b.band_rec) + ((long long)s * g.bands_per_stream + bid);
+    *rec = make_int4(base, kept, n_ok, n_drop);
+  }
+  // ---- last warp of the stream scans ----
   __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    int tk = atomicAdd(&ctr[C_TICKET], 1);
-    sh_last = (tk == (int)gridDim.x - 1);
-  }
-  __syncthreads();
-  if (sh_last) {
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) last = atomicAdd(&ctr[C_TICKET], 1) == g.bands_per_stream - 1;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) {
     __threadfence();
-    nms_last_cta(g, b, s, sm_warp);
+    nms_last_warp(g, b, s, lane);
   }
 }
 
@@ -1110,10 +1103,10 @@ __device__ __forceinline__ int box_mean(const uint32_t* S, const Geo& g, long lo
 // ---------------------------------------------------------------------------
 #define DW_WARPS 4
 #define DS_THREADS (32 * DW_WARPS)
-#define DW_ROW 61
+#define DW_ROW 68   // bytes per keypoint row (17 words: odd, so lane k's rows fall in distinct banks)
 
 struct DescWarp {
-  int v[32 * DW_ROW];
+  uint8_t v[32 * DW_ROW];   // box means are 0..255 (sum // area of uint8 pixels)
   double kx[32], ky[32], sg[32], cs[32], sn[32];
   const uint32_t* sat[32];
 };
@@ -1137,7 +1130,7 @@ __device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, i
     x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
     y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
     const long long r = (long long)floor(c_rad[j] * sg + 0.5);
-    w.v[k * DW_ROW + j] = box_mean(w.sat[k], g, x, y, r);
+    w.v[k * DW_ROW + j] = (uint8_t)box_mean(w.sat[k], g, x, y, r);
   }
 }
 
@@ -1145,14 +1138,14 @@ __device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, i
 // Returns theta of lane's keypoint (lane < nk) via *theta_lane; desc_lane[q]
 // (lane q < 16) receives descriptor word q of each keypoint through `emit`.
 template <typename Emit>
-__device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, int nk, int lane, bool theta_given,
-                                              double& theta_lane, Emit emit)
+__device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, const uint32_t* pairs, int nk, int lane,
+                                              bool theta_given, double& theta_lane, Emit emit)
 {
   if (!theta_given) {
     sample_pass(g, w, nk, lane, false);
     __syncwarp();
     if (lane < nk) {
-      const int* v = w.v + lane * DW_ROW;
+      const uint8_t* v = w.v + lane * DW_ROW;
       double gx = 0.0, gy = 0.0;
       const int L = c_nlong;
       for (int p = 0; p < L; p++) {
@@ -1172,16 +1165,13 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, int nk,
   }
   sample_pass(g, w, nk, lane, true);
   __syncwarp();
-  // per-lane pair indices of bits 32q + lane
-  int pa[16], pb[16];
-#pragma unroll
-  for (int q = 0; q < 16; q++) { pa[q] = c_si[32 * q + lane]; pb[q] = c_sj[32 * q + lane]; }
   for (int k = 0; k < nk; k++) {
-    const int* v = w.v + k * DW_ROW;
+    const uint8_t* v = w.v + k * DW_ROW;
     uint32_t mine = 0;
 #pragma unroll
     for (int q = 0; q < 16; q++) {
-      const uint32_t word = __ballot_sync(0xffffffffu, v[pa[q]] > v[pb[q]]);
+      const uint32_t pr = pairs[32 * q + lane];           // si | sj << 16 (smem, conflict-free)
+      const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
       if (lane == q) mine = word;
     }
     emit(k, __byte_perm(__brev(mine), 0, 0x0123));
@@ -1191,18 +1181,16 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, int nk,
 // Kept keypoints of all streams flattened: global index -> (stream, rank)
 // through the per-stream n_detected prefix, rank -> band by binary search of
 // the band output offsets, band -> staging slot.
-__global__ void __launch_bounds__(DS_THREADS) k_describe(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
-                                                          int n_streams)
+__global__ void __launch_bounds__(DS_THREADS, 8) k_describe(const __grid_constant__ Geo g,
+                                                             const __grid_constant__ Bufs b, int n_streams)
 {
   __shared__ DescWarp ws[DW_WARPS];
+  __shared__ uint32_t pairs[VF_NBITS];
   extern __shared__ int pre[];   // [n_streams + 1]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) {
-    int acc = 0;
-    for (int s = 0; s < n_streams; s++) { pre[s] = acc; acc += b.ctr[s * C_NCTR + C_NDET]; }
-    pre[n_streams] = acc;
-  }
-  __syncthreads();
+  __shared__ int sm_warp[32];
+  for (int k = tid; k < VF_NBITS; k += DS_THREADS) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
+  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
   DescWarp& w = ws[wid];
   const int nwarps = gridDim.x * DW_WARPS;
@@ -1226,7 +1214,7 @@ __global__ void __launch_bounds__(DS_THREADS) k_describe(const __grid_constant__
     }
     __syncwarp();
     double th = 0.0;
-    describe_warp(g, w, nk, lane, false, th, [&](int k, uint32_t word) {
+    describe_warp(g, w, pairs, nk, lane, false, th, [&](int k, uint32_t word) {
       const long long o = __shfl_sync(0xffffffffu, out_idx, k);
       if (lane < 16) reinterpret_cast<uint32_t*>(b.fdesc + o * 64)[lane] = word;
     });
@@ -1349,7 +1337,10 @@ __global__ void __launch_bounds__(DS_THREADS) k_describe_batch(const __grid_cons
                                                                const double* theta_in, double* theta_out, uint8_t* desc)
 {
   __shared__ DescWarp ws[DW_WARPS];
+  __shared__ uint32_t pairs[VF_NBITS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < VF_NBITS; k += DS_THREADS) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
+  __syncthreads();
   DescWarp& w = ws[wid];
   const int base = (blockIdx.x * DW_WARPS + wid) * 32;
   if (base >= n) return;
@@ -1366,7 +1357,7 @@ __global__ void __launch_bounds__(DS_THREADS) k_describe_batch(const __grid_cons
     }
   }
   __syncwarp();
-  describe_warp(g, w, nk, lane, theta_in != nullptr, th, [&](int k, uint32_t word) {
+  describe_warp(g, w, pairs, nk, lane, theta_in != nullptr, th, [&](int k, uint32_t word) {
     if (desc && lane < 16) reinterpret_cast<uint32_t*>(desc + (long long)(base + k) * 64)[lane] = word;
   });
   if (lane < nk && theta_out) theta_out[base + lane] = th;

@@ -152,6 +152,13 @@ class FeatureEngine:
                                                     _native.stream_handle(stream)))
         return dict(zip(self.STAGES, out.tolist())), int(n.value)
 
+    def diag(self, stream=None) -> dict:
+        out = np.zeros(8, np.int64)
+        _native.check(_native.lib().vf_get_diag(self._h, out.ctypes.data, _native.stream_handle(stream)))
+        keys = ("fast_tiles_active", "fast_tiles", "sat_tiles_built", "sat_tiles", "dense_streams",
+                "nms_candidates", "bands_per_stream", "kp_capacity")
+        return dict(zip(keys, out.tolist()))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             _native.lib().vf_destroy(self._h)
