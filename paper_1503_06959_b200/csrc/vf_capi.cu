@@ -142,6 +142,8 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.ptx = cdiv(g.W, g.ptw); g.pty = cdiv(g.H, g.pth);
   g.sat_tiles = g.ptx * g.pty;
   g.pth_magic = (unsigned)((0x100000000ULL + g.pth - 1) / g.pth);
+  // strip-SAT ring: <= 40 MB so it stays in the 126 MB L2 next to the step's other traffic
+  g.sat_slots = c.max_streams;   // one strip-SAT slot per stream
   if (g.ptx > 32 * 8) return VF_ERR_ARG;   // strip carries: <= 8 x 32 tile columns
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
@@ -182,7 +184,7 @@ struct vf_ctx {
   int pyr_smem;
   int fast_grid;
   int desc_grid;
-  int sat_grid, sat_smem;
+  int sat_grid, sat_smem, desc_smem, dsample_grid, dorient_grid;
   // host-input staging (vf_process_host)
   uint8_t* hstage[2] = {nullptr, nullptr};
   long long hstage_bytes = 0;
@@ -301,12 +303,15 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.state = A.get<uint8_t>((size_t)S * g.state_slab);
   int* dl = A.get<int>((size_t)g.lut_len);
   b.lut = dl;
-  b.sat = A.get<uint32_t>((size_t)S * g.W * g.H);
+  b.sat = A.get<uint32_t>((size_t)g.sat_slots * g.W * g.H);
   b.rowsum = A.get<uint32_t>((size_t)S * g.H * g.ptx);
   b.carry = A.get<uint32_t>((size_t)S * g.H * g.ptx);
   b.sat_stamp = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_work = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_count = A.get<int>((size_t)S);
+  b.sat_done = A.get<int>((size_t)S);
+  b.desc_done = A.get<int>((size_t)S);
+  b.q_ctr = A.get<int>(1);
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -344,8 +349,11 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sat, 256, c->sat_smem);
   c->sat_grid = std::max(1, g_num_sms * std::max(occ, 1));
   occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_describe, DS_THREADS, (S + 1) * sizeof(int));
-  c->desc_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_sample, 32 * DSW, (S + 1) * sizeof(int));
+  c->dsample_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_orient, DO_THREADS, (S + 1) * sizeof(int));
+  c->dorient_grid = std::max(1, g_num_sms * std::max(occ, 1));
   *out = c;
   return VF_OK;
 }
@@ -440,7 +448,10 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   stage_mark(c, 5, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
   stage_mark(c, 6, st);
-  k_describe<<<c->desc_grid, DS_THREADS, (n + 1) * sizeof(int), st>>>(g, b, n);
+  const int pre_bytes = (n + 1) * (int)sizeof(int);
+  k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0);
+  k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
+  k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
   stage_mark(c, 7, st);
   if (g.mask_mode) k_propagate<<<dim3(PROP_CTAS, n), 256, 0, st>>>(g, b);
   stage_mark(c, 8, st);
@@ -757,7 +768,7 @@ int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, co
   b.frames = frame_dev; b.frame_stride = 0; b.frame_pitch = pitch;
   k_pyramid<<<dim3(c->g.ptx, c->g.pty, 1), 256, c->pyr_smem, st>>>(c->g, b);
   k_carries<<<dim3(c->g.pty, 1), 32, 0, st>>>(c->g, b);
-  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1);
+  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1);   // stream 0 -> slot 0
   k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev,
                                                               theta_in_dev, theta_out_dev, desc_dev);
   return cuda_status(cudaStreamSynchronize(st));

@@ -74,7 +74,8 @@ struct Geo {
   int kp_cap;           // feature capacity per stream and buffer
   int prop_chunks;      // CTAs reserved for propagation chunks
   int sat_tiles;        // ptx * pty
-  unsigned pth_magic;   // ceil(2^32 / pth): y / pth == umulhi(y, pth_magic) for y < 2^16
+  unsigned pth_magic;
+  int sat_slots;        // strip-SAT ring size (streams), sized to stay in L2   // ceil(2^32 / pth): y / pth == umulhi(y, pth_magic) for y < 2^16
   int nms_raw;          // stand-alone nms_and_refine: no border / merge filter
   int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
 };
@@ -95,11 +96,13 @@ struct Bufs {
   int* cell_row_stamp;  // [S][n_grids][max rows] "row has an active cell" stamps
   uint8_t* state;       // [S][state_slab]
   const int* lut;       // [lut_len] row/col -> cell maps (shared by all streams)
-  uint32_t* sat;        // [S][W*H] tile-local summed-area tables (L)
+  uint32_t* sat;        // [sat_slots][W*H] strip SATs (ring over streams)
   uint32_t* rowsum;     // [S][H][ptx] per-tile row sums of o0
   uint32_t* carry;      // [S][H][ptx] strip carries K(y, tx) (see strip_sum)
   int* sat_stamp;       // [S][sat_tiles] epoch at which the tile's L was written
   int* sat_work; int* sat_count;   // [S][sat_tiles] / [S]: SAT tiles marked this step (masked frames)
+  int* sat_done; int* desc_done;   // [S] k_sat_describe progress counters
+  int* q_ctr;                      // k_sat_describe work-queue ticket
   double* st_x; double* st_y; double* st_s; double* st_v;   // staging [S][kp_cap]
   // double-buffered features [S][2][kp_cap]
   double* fx; double* fy; double* fs; double* ft; double* fv;

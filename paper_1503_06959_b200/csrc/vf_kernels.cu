@@ -57,7 +57,7 @@ __device__ __forceinline__ void lvl_dims(const Geo& g, int l, int& lw, int& lh)
 // All values < 2^32 and box sums are exact in uint32.
 // ----------------------------------------------------------------------------
 __device__ void sat_tile(const Geo& g, const Bufs& b, int s, int tx, int ty, int tw, int th, const uint8_t* t0,
-                         uint32_t* ssat)
+                         uint32_t* ssat, uint32_t* gs)
 {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -89,7 +89,6 @@ __device__ void sat_tile(const Geo& g, const Bufs& b, int s, int tx, int ty, int
   }
   __syncthreads();
   // S(y, x) = L(y, x) + K(y, tx): the SAT of the pth-row strip
-  uint32_t* gs = b.sat + (long long)s * g.W * g.H;
   const uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx + tx;
   for (int i = tid; i < th * tw; i += nt) {
     const int y = i / tw, x = i - y * tw;
@@ -140,16 +139,16 @@ __device__ __forceinline__ uint32_t box_sum(const uint32_t* S, const Geo& g, int
   const bool left = x0 > 0;
   int yb = min(y1, ys + TH - 1);
   const uint32_t* rb = S + (long long)yb * g.W;
-  uint32_t sum = __ldg(rb + x1) - (left ? __ldg(rb + x0 - 1) : 0u);
+  uint32_t sum = __ldca(rb + x1) - (left ? __ldca(rb + x0 - 1) : 0u);
   if (y0 > ys) {
     const uint32_t* ra = S + (long long)(y0 - 1) * g.W;
-    sum -= __ldg(ra + x1) - (left ? __ldg(ra + x0 - 1) : 0u);
+    sum -= __ldca(ra + x1) - (left ? __ldca(ra + x0 - 1) : 0u);
   }
   while (yb < y1) {                 // next strip(s): rows start at the strip top
     ys += TH;
     yb = min(y1, ys + TH - 1);
     const uint32_t* r2 = S + (long long)yb * g.W;
-    sum += __ldg(r2 + x1) - (left ? __ldg(r2 + x0 - 1) : 0u);
+    sum += __ldca(r2 + x1) - (left ? __ldca(r2 + x0 - 1) : 0u);
   }
   return sum;
 }
@@ -206,7 +205,9 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
   if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
     b.ctr[s * C_NCTR + C_STAGE] = 0;
     b.sat_count[s] = 0;
-    if (s == 0) *b.work_count = 0;
+    b.sat_done[s] = 0;
+    b.desc_done[s] = 0;
+    if (s == 0) { *b.work_count = 0; *b.q_ctr = 0; }
   }
 
   // ---- load the o0 tile ------------------------------------------------------
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
     const int tw = min(g.ptw, g.W - X0), th = min(g.pth, g.H - Y0);
     load_o0_tile(g, b, s, X0, Y0, tw, th, t0);
     __syncthreads();
-    sat_tile(g, b, s, tx, ty, tw, th, t0, ssat);
+    sat_tile(g, b, s, tx, ty, tw, th, t0, ssat, b.sat + (long long)(s % g.sat_slots) * g.W * g.H);
     __syncthreads();
   }
 }
@@ -1111,26 +1112,78 @@ struct DescWarp {
   const uint32_t* sat[32];
 };
 
+// Sample (keypoint, point) pairs into w.v: 4 pairs per lane per iteration,
+// every SAT corner load issued before any is consumed (branch-free: a masked
+// corner re-reads corner A and is multiplied by 0).  Boxes spanning three or
+// more strips (only when a box is taller than pth: O > 4) take box_sum.
 __device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, int lane, bool rotated)
 {
-#pragma unroll 4
-  for (int q = lane; q < nk * VF_NPTS; q += 32) {
-    const int k = q / VF_NPTS, j = q - k * VF_NPTS;
-    const double sg = w.sg[k];
-    double fx, fy;
-    if (rotated) {
-      const double c = w.cs[k], sn = w.sn[k], px = c_px[j], py = c_py[j];
-      fx = w.kx[k] + sg * (c * px - sn * py) + 0.5;
-      fy = w.ky[k] + sg * (sn * px + c * py) + 0.5;
-    } else {
-      fx = w.kx[k] + sg * c_px[j] + 0.5;
-      fy = w.ky[k] + sg * c_py[j] + 0.5;
+  const int npair = nk * VF_NPTS;
+  const int TH = g.pth;
+  for (int q0 = lane; q0 < npair; q0 += 128) {
+    const uint32_t* rowp[4][3];
+    int xa[4], xb[4], area[4], dst[4];
+    uint32_t msk[4];
+    bool slow[4];
+    int bx0[4], bx1[4], by0[4], by1[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int q = q0 + 32 * u;
+      const bool valid = q < npair;
+      const int k = valid ? q / VF_NPTS : 0, j = valid ? q - k * VF_NPTS : 0;
+      const double sg = w.sg[k];
+      double fx, fy;
+      if (rotated) {
+        const double c = w.cs[k], sn = w.sn[k], px = c_px[j], py = c_py[j];
+        fx = w.kx[k] + sg * (c * px - sn * py) + 0.5;
+        fy = w.ky[k] + sg * (sn * px + c * py) + 0.5;
+      } else {
+        fx = w.kx[k] + sg * c_px[j] + 0.5;
+        fy = w.ky[k] + sg * c_py[j] + 0.5;
+      }
+      long long x = (long long)floor(fx), y = (long long)floor(fy);
+      x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
+      y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
+      const int r = (int)floor(c_rad[j] * sg + 0.5);
+      const int x0 = max((int)x - r, 0), x1 = min((int)x + r, g.W - 1);
+      const int y0 = max((int)y - r, 0), y1 = min((int)y + r, g.H - 1);
+      const int ys = (int)__umulhi((uint32_t)y0, g.pth_magic) * TH;
+      const int yb = min(y1, ys + TH - 1);
+      const bool left = x0 > 0, top = y0 > ys, cross = y1 > yb;
+      slow[u] = y1 > ys + 2 * TH - 1;
+      const uint32_t* S = w.sat[k];
+      rowp[u][0] = S + (long long)yb * g.W;
+      rowp[u][1] = top ? S + (long long)(y0 - 1) * g.W : rowp[u][0];
+      rowp[u][2] = cross ? S + (long long)y1 * g.W : rowp[u][0];
+      xa[u] = left ? x0 - 1 : x1;
+      xb[u] = x1;
+      msk[u] = (left ? 1u : 0u) | (top ? 2u : 0u) | (cross ? 4u : 0u) | (valid ? 8u : 0u);
+      area[u] = (x1 - x0 + 1) * (y1 - y0 + 1);
+      dst[u] = k * DW_ROW + j;
+      bx0[u] = x0; bx1[u] = x1; by0[u] = y0; by1[u] = y1;
     }
-    long long x = (long long)floor(fx), y = (long long)floor(fy);
-    x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
-    y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
-    const long long r = (long long)floor(c_rad[j] * sg + 0.5);
-    w.v[k * DW_ROW + j] = (uint8_t)box_mean(w.sat[k], g, x, y, r);
+    uint32_t v[4][6];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      v[u][0] = __ldca(rowp[u][0] + xb[u]);
+      v[u][1] = __ldca(rowp[u][0] + xa[u]);
+      v[u][2] = __ldca(rowp[u][1] + xb[u]);
+      v[u][3] = __ldca(rowp[u][1] + xa[u]);
+      v[u][4] = __ldca(rowp[u][2] + xb[u]);
+      v[u][5] = __ldca(rowp[u][2] + xa[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t m = msk[u];
+      const uint32_t L = m & 1u, T = (m >> 1) & 1u, C = (m >> 2) & 1u;
+      uint32_t sm = v[u][0] - L * v[u][1] - T * (v[u][2] - L * v[u][3]) + C * (v[u][4] - L * v[u][5]);
+      if (slow[u]) sm = box_sum(w.sat[dst[u] / DW_ROW], g, bx0[u], bx1[u], by0[u], by1[u]);
+      const uint32_t a = (uint32_t)area[u];
+      uint32_t qv = (uint32_t)((float)sm * __frcp_rn((float)a));
+      if (qv * a > sm) qv--;
+      else if ((qv + 1) * a <= sm) qv++;
+      if (m & 8u) w.v[dst[u]] = (uint8_t)qv;
+    }
   }
 }
 
@@ -1181,49 +1234,166 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, const u
 // Kept keypoints of all streams flattened: global index -> (stream, rank)
 // through the per-stream n_detected prefix, rank -> band by binary search of
 // the band output offsets, band -> staging slot.
-__global__ void __launch_bounds__(DS_THREADS, 8) k_describe(const __grid_constant__ Geo g,
-                                                             const __grid_constant__ Bufs b, int n_streams)
+// ---------------------------------------------------------------------------
+// Pipeline describe in three launches, each shaped for its work:
+//   k_desc_sample(pass 0)  warp per kept keypoint, lanes = sample points:
+//                          theta = 0 box means (2 points per lane, every SAT
+//                          corner load in flight at once) -> 60 bytes parked in
+//                          the keypoint's descriptor slot; keypoint fields out
+//   k_desc_orient          thread per keypoint: the 393-term sequential fp64
+//                          orientation sum (descriptor.py:128-144), atan2
+//   k_desc_sample(pass 1)  warp per keypoint: rotated box means, 16 ballots ->
+//                          512 MSB-first bits (descriptor.py:117-126,271-275)
+// Kept keypoints of all streams are flattened (per-stream n_detected prefix).
+// ---------------------------------------------------------------------------
+// Box mean of pattern point j of a keypoint (descriptor.py:85-115): fp64
+// position in the reference's op order, clamped box, branch-free strip-SAT
+// corners (masked corners re-read corner A and are multiplied by 0), exact
+// sum // area.
+__device__ __forceinline__ uint32_t point_mean(const uint32_t* S, const Geo& g, double kx, double ky, double sg,
+                                               double cs, double sn, int j, bool rotated)
 {
-  __shared__ DescWarp ws[DW_WARPS];
+  double fx, fy;
+  if (rotated) {
+    const double px = c_px[j], py = c_py[j];
+    fx = kx + sg * (cs * px - sn * py) + 0.5;
+    fy = ky + sg * (sn * px + cs * py) + 0.5;
+  } else {
+    fx = kx + sg * c_px[j] + 0.5;
+    fy = ky + sg * c_py[j] + 0.5;
+  }
+  long long x = (long long)floor(fx), y = (long long)floor(fy);
+  x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
+  y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
+  const int r = (int)floor(c_rad[j] * sg + 0.5);
+  const int x0 = max((int)x - r, 0), x1 = min((int)x + r, g.W - 1);
+  const int y0 = max((int)y - r, 0), y1 = min((int)y + r, g.H - 1);
+  const int TH = g.pth;
+  const int ys = (int)__umulhi((uint32_t)y0, g.pth_magic) * TH;
+  const int yb = min(y1, ys + TH - 1);
+  const uint32_t L = x0 > 0, T = y0 > ys, C = y1 > yb;
+  uint32_t sm;
+  if (y1 > ys + 2 * TH - 1) {
+    sm = box_sum(S, g, x0, x1, y0, y1);          // box over >= 3 strips (O > 4 only)
+  } else {
+    const uint32_t* r0 = S + (long long)yb * g.W;
+    const uint32_t* r1 = T ? S + (long long)(y0 - 1) * g.W : r0;
+    const uint32_t* r2 = C ? S + (long long)y1 * g.W : r0;
+    const int xa = L ? x0 - 1 : x1;
+    const uint32_t a0 = __ldca(r0 + x1), a1 = __ldca(r0 + xa), b0 = __ldca(r1 + x1), b1 = __ldca(r1 + xa);
+    const uint32_t c0 = __ldca(r2 + x1), c1 = __ldca(r2 + xa);
+    sm = a0 - L * a1 - T * (b0 - L * b1) + C * (c0 - L * c1);
+  }
+  const uint32_t a = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+  uint32_t q = (uint32_t)((float)sm * __frcp_rn((float)a));
+  if (q * a > sm) q--;
+  else if ((q + 1) * a <= sm) q++;
+  return q;
+}
+
+// Flattened kept-keypoint index -> (stream, rank) via the per-stream prefix.
+__device__ __forceinline__ int find_stream(const int* pre, int n_streams, int gi)
+{
+  int lo = 0, hi = n_streams;
+  while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= gi) lo = m; else hi = m; }
+  return lo;
+}
+
+#define DSW 8   // warps per CTA in the warp-per-keypoint describe kernels
+__global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant__ Geo g,
+                                                          const __grid_constant__ Bufs b, int n_streams, int pass)
+{
+  __shared__ uint8_t vals[DSW][64];
   __shared__ uint32_t pairs[VF_NBITS];
-  extern __shared__ int pre[];   // [n_streams + 1]
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   __shared__ int sm_warp[32];
-  for (int k = tid; k < VF_NBITS; k += DS_THREADS) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
+  extern __shared__ int pre[];   // [n_streams + 1]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
   stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
-  DescWarp& w = ws[wid];
-  const int nwarps = gridDim.x * DW_WARPS;
-  for (int base = (blockIdx.x * DW_WARPS + wid) * 32; base < total; base += nwarps * 32) {
-    const int nk = min(32, total - base);
-    long long out_idx = -1, st_idx = 0;
-    if (lane < nk) {
-      const int gi = base + lane;
-      int lo = 0, hi = n_streams;            // last s with pre[s] <= gi
-      while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= gi) lo = m; else hi = m; }
-      const int s = lo, i = gi - pre[s];
+  for (int gi = blockIdx.x * DSW + wid; gi < total; gi += gridDim.x * DSW) {
+    const int s = find_stream(pre, n_streams, gi), i = gi - pre[s];
+    const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
+    const long long o = ((long long)s * 2 + cur) * g.kp_cap + i;
+    const uint32_t* S = b.sat + (long long)(s % g.sat_slots) * g.W * g.H;
+    double kx, ky, sg, cs = 1.0, sn = 0.0;
+    if (pass == 0) {
+      // band of rank i (last band with band_out <= i) -> staging slot
       const int* bout = b.band_out + (long long)s * g.bands_per_stream;
-      int blo = 0, bhi = g.bands_per_stream;  // last band with band_out <= i
+      int blo = 0, bhi = g.bands_per_stream;
       while (bhi - blo > 1) { int m = (blo + bhi) >> 1; if (__ldg(bout + m) <= i) blo = m; else bhi = m; }
       const int* rec = b.band_rec + ((long long)s * g.bands_per_stream + blo) * 4;
-      st_idx = (long long)s * g.kp_cap + rec[0] + (i - __ldg(bout + blo));
-      const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
-      out_idx = ((long long)s * 2 + cur) * g.kp_cap + i;
-      w.kx[lane] = b.st_x[st_idx]; w.ky[lane] = b.st_y[st_idx]; w.sg[lane] = b.st_s[st_idx];
-      w.sat[lane] = b.sat + (long long)s * g.W * g.H;
+      const long long si = (long long)s * g.kp_cap + rec[0] + (i - __ldg(bout + blo));
+      kx = b.st_x[si]; ky = b.st_y[si]; sg = b.st_s[si];
+      if (lane == 0) {
+        b.fx[o] = kx; b.fy[o] = ky; b.fs[o] = sg; b.fv[o] = b.st_v[si];
+        b.forg[o] = 0; b.fage[o] = 0;
+      }
+    } else {
+      kx = b.fx[o]; ky = b.fy[o]; sg = b.fs[o];
+      sincos(b.ft[o], &sn, &cs);
+    }
+    const uint32_t m0 = point_mean(S, g, kx, ky, sg, cs, sn, lane, pass != 0);
+    uint32_t m1 = 0;
+    if (lane + 32 < VF_NPTS) m1 = point_mean(S, g, kx, ky, sg, cs, sn, lane + 32, pass != 0);
+    uint8_t* v = vals[wid];
+    v[lane] = (uint8_t)m0;
+    if (lane + 32 < VF_NPTS) v[lane + 32] = (uint8_t)m1;
+    __syncwarp();
+    uint32_t* dst = reinterpret_cast<uint32_t*>(b.fdesc + o * 64);
+    if (pass == 0) {
+      // park the 60 theta = 0 means (+4 pad) in the descriptor slot for k_desc_orient
+      if (lane < 16) dst[lane] = reinterpret_cast<const uint32_t*>(v)[lane];
+    } else {
+      uint32_t mine = 0;
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        const uint32_t pr = pairs[32 * q + lane];
+        const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
+        if (lane == q) mine = word;
+      }
+      if (lane < 16) dst[lane] = __byte_perm(__brev(mine), 0, 0x0123);
     }
     __syncwarp();
-    double th = 0.0;
-    describe_warp(g, w, pairs, nk, lane, false, th, [&](int k, uint32_t word) {
-      const long long o = __shfl_sync(0xffffffffu, out_idx, k);
-      if (lane < 16) reinterpret_cast<uint32_t*>(b.fdesc + o * 64)[lane] = word;
-    });
-    if (lane < nk) {
-      b.fx[out_idx] = w.kx[lane]; b.fy[out_idx] = w.ky[lane]; b.fs[out_idx] = w.sg[lane];
-      b.ft[out_idx] = th; b.fv[out_idx] = b.st_v[st_idx];
-      b.forg[out_idx] = 0; b.fage[out_idx] = 0;
+  }
+}
+
+// Thread per keypoint: theta from the parked theta = 0 means, summed
+// sequentially in long-pair order with fp64 products (no FMA), as
+// _orientations_jit; theta <= -pi maps to pi (descriptor.py:142-143).
+#define DO_THREADS 128
+__global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constant__ Geo g,
+                                                            const __grid_constant__ Bufs b, int n_streams)
+{
+  __shared__ __align__(16) uint8_t vv[DO_THREADS * DW_ROW];
+  __shared__ int sm_warp[32];
+  extern __shared__ int pre[];
+  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
+  const int total = pre[n_streams];
+  uint8_t* v = vv + threadIdx.x * DW_ROW;
+  for (int base = blockIdx.x * DO_THREADS; base < total; base += gridDim.x * DO_THREADS) {
+    const int gi = base + threadIdx.x;
+    long long o = -1;
+    if (gi < total) {
+      const int s = find_stream(pre, n_streams, gi), i = gi - pre[s];
+      o = ((long long)s * 2 + (b.ctr[s * C_NCTR + C_FRAME] & 1)) * g.kp_cap + i;
+      const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + o * 64);
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint4 w4 = src[q];
+        uint32_t* d = reinterpret_cast<uint32_t*>(v + 16 * q);
+        d[0] = w4.x; d[1] = w4.y; d[2] = w4.z; d[3] = w4.w;
+      }
+      double gx = 0.0, gy = 0.0;
+      const int L = c_nlong;
+      for (int p = 0; p < L; p++) {
+        const double dv = (double)((int)v[c_li[p]] - (int)v[c_lj[p]]);
+        gx += dv * c_wx[p];
+        gy += dv * c_wy[p];
+      }
+      double th = atan2(gy, gx);
+      b.ft[o] = th <= -CUDART_PI ? CUDART_PI : th;
     }
-    __syncwarp();
   }
 }
 
