@@ -434,9 +434,12 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
     k_binmask<<<n, 1024, smem, st>>>(g, b);
   }
   stage_mark(c, 1, st);
-  k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
+  if (g.O == 4 && g.ptw == 96 && g.pth == 48 && !(g.mask_mode == 1 && (g.per_layer || g.mask_level != 3)))
+    k_pyramid4<<<dim3(g.ptx, g.pty, n), 256, 0, st>>>(g, b);
+  else
+    k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
   stage_mark(c, 2, st);
-  const int tile_ctas = cdiv(g.tiles_per_stream, 8);
+  const int tile_ctas = cdiv(g.tiles_per_stream, 256);   // lane per tile
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
   const int carry_ctas = cdiv(g.pty, 8);
   k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(

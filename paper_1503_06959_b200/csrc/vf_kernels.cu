@@ -430,6 +430,195 @@ __global__ void k_carries(const __grid_constant__ Geo g, const __grid_constant__
 }
 
 // ============================================================================
+// k_pyramid4: k_pyramid specialised for the benchmark geometry -- O = 4,
+// 96 x 48 o0 tiles, IDDM on the top octave.  Same arithmetic, static thread
+// maps: the eight levels are produced in four phases (level pairs that do not
+// depend on each other share a phase), four pixels per 32-bit word.
+// ============================================================================
+__device__ __forceinline__ uint32_t halve4(const uint2 r0, const uint2 r1)
+{
+  uint32_t a0 = (r0.x & 0x00ff00ffu) + ((r0.x >> 8) & 0x00ff00ffu) + (r1.x & 0x00ff00ffu) + ((r1.x >> 8) & 0x00ff00ffu);
+  uint32_t a1 = (r0.y & 0x00ff00ffu) + ((r0.y >> 8) & 0x00ff00ffu) + (r1.y & 0x00ff00ffu) + ((r1.y >> 8) & 0x00ff00ffu);
+  a0 = ((a0 + 0x00020002u) >> 2) & 0x00ff00ffu;
+  a1 = ((a1 + 0x00020002u) >> 2) & 0x00ff00ffu;
+  return __byte_perm(a0, a1, 0x6420);
+}
+
+__device__ __forceinline__ void store_word(uint8_t* gdst, int gp, int y, int x, int vw, int vh, uint32_t w)
+{
+  if (y >= vh || x >= vw) return;
+  if (x + 4 <= vw) *reinterpret_cast<uint32_t*>(gdst + (long long)y * gp + x) = w;
+  else for (int c = 0; c < 4 && x + c < vw; c++) gdst[(long long)y * gp + x + c] = (uint8_t)(w >> (8 * c));
+}
+
+__global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  constexpr int TW = 96, TH = 48;
+  __shared__ __align__(16) uint8_t t0[TH * TW];
+  __shared__ __align__(16) uint8_t si0[32 * 64], so1[24 * 48], si1[16 * 32], so2[12 * 24], si2[8 * 16];
+  __shared__ __align__(16) uint8_t so3[6 * 12 + 8], si3[4 * 8];
+  __shared__ unsigned long long cov_part[4];
+  const int s = blockIdx.z, tid = threadIdx.x;
+  const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    b.ctr[s * C_NCTR + C_STAGE] = 0;
+    b.sat_count[s] = 0;
+    b.sat_done[s] = 0;
+    b.desc_done[s] = 0;
+    if (s == 0) { *b.work_count = 0; *b.q_ctr = 0; }
+  }
+  const int tw = min(TW, g.W - X0), th = min(TH, g.H - Y0);
+  // ---- o0 tile ----
+  {
+    const uint8_t* src = b.frames + (long long)s * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)b.frame_pitch) & 15) == 0 && tw == TW;
+    if (vec) {
+      for (int i = tid; i < th * (TW / 16); i += 256) {
+        const int y = i / (TW / 16), c = i - y * (TW / 16);
+        *reinterpret_cast<uint4*>(t0 + y * TW + 16 * c) =
+            __ldg(reinterpret_cast<const uint4*>(src + (long long)y * b.frame_pitch) + c);
+      }
+    } else {
+      for (int i = tid; i < th * TW; i += 256) {
+        const int y = i / TW, x = i - y * TW;
+        t0[i] = x < tw ? __ldg(src + (long long)y * b.frame_pitch + x) : 0;
+      }
+    }
+  }
+  __syncthreads();
+  uint8_t* lay = b.layers + (long long)s * g.layer_slab;
+  // ---- phase 1: i0 (2/3 resample) + o1 (halving) + row sums ----
+  {
+    // i0: 16 row pairs x 16 words, one 2x4 block per thread
+    const int p = tid >> 4, q = tid & 15;
+    const int base = 6 * q, al = base & ~3, sh = 8 * (base & 3);
+    uint32_t hs[3][4];
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const uint8_t* row = t0 + (3 * p + r) * TW + al;
+      const unsigned long long lo =
+          (((unsigned long long)*reinterpret_cast<const uint32_t*>(row + 4) << 32) | *reinterpret_cast<const uint32_t*>(row)) >> sh;
+      const uint32_t c0 = lo & 0xff, c1 = (lo >> 8) & 0xff, c2 = (lo >> 16) & 0xff, c3 = (lo >> 24) & 0xff;
+      const uint32_t c4 = (lo >> 32) & 0xff, c5 = (lo >> 40) & 0xff;
+      hs[r][0] = 2 * c0 + c1; hs[r][1] = c1 + 2 * c2; hs[r][2] = 2 * c3 + c4; hs[r][3] = c4 + 2 * c5;
+    }
+    uint32_t e = 0, o = 0;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      e |= ((2 * hs[0][c] + hs[1][c] + 4) / 9) << (8 * c);
+      o |= ((hs[1][c] + 2 * hs[2][c] + 4) / 9) << (8 * c);
+    }
+    *reinterpret_cast<uint32_t*>(si0 + (2 * p) * 64 + 4 * q) = e;
+    *reinterpret_cast<uint32_t*>(si0 + (2 * p + 1) * 64 + 4 * q) = o;
+    const LayerGeo& L1 = g.L[1];
+    const int gx0 = 2 * X0 / 3, gy0 = 2 * Y0 / 3;
+    uint8_t* gd = lay + L1.layer_off + (long long)gy0 * L1.pitch + gx0;
+    store_word(gd, L1.pitch, 2 * p, 4 * q, L1.w - gx0, L1.h - gy0, e);
+    store_word(gd, L1.pitch, 2 * p + 1, 4 * q, L1.w - gx0, L1.h - gy0, o);
+  }
+  {
+    const LayerGeo& L2 = g.L[2];
+    const int gx0 = X0 >> 1, gy0 = Y0 >> 1;
+    uint8_t* gd = lay + L2.layer_off + (long long)gy0 * L2.pitch + gx0;
+    for (int i = tid; i < 24 * 12; i += 256) {
+      const int y = i / 12, q = i - y * 12;
+      const uint32_t w = halve4(*reinterpret_cast<const uint2*>(t0 + (2 * y) * TW + 8 * q),
+                                *reinterpret_cast<const uint2*>(t0 + (2 * y + 1) * TW + 8 * q));
+      *reinterpret_cast<uint32_t*>(so1 + y * 48 + 4 * q) = w;
+      store_word(gd, L2.pitch, y, 4 * q, L2.w - gx0, L2.h - gy0, w);
+    }
+  }
+  if (tid < th) {
+    // per-row sums of the tile (strip carries for the descriptor's SATs)
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(t0 + tid * TW);
+    uint32_t a = 0;
+#pragma unroll
+    for (int k = 0; k < TW / 4; k++) a = __dp4a(row[k], 0x01010101u, a);
+    b.rowsum[((long long)s * g.H + Y0 + tid) * g.ptx + blockIdx.x] = a;
+  }
+  __syncthreads();
+  // ---- phase 2: i1 from i0, o2 from o1 ----
+  if (tid < 128) {
+    const int y = tid >> 3, q = tid & 7;
+    const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si0 + (2 * y) * 64 + 8 * q),
+                              *reinterpret_cast<const uint2*>(si0 + (2 * y + 1) * 64 + 8 * q));
+    *reinterpret_cast<uint32_t*>(si1 + y * 32 + 4 * q) = w;
+    const LayerGeo& L = g.L[3];
+    const int gx0 = (2 * X0 / 3) >> 1, gy0 = (2 * Y0 / 3) >> 1;
+    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+  } else if (tid < 128 + 72) {
+    const int i = tid - 128, y = i / 6, q = i - y * 6;
+    const uint32_t w = halve4(*reinterpret_cast<const uint2*>(so1 + (2 * y) * 48 + 8 * q),
+                              *reinterpret_cast<const uint2*>(so1 + (2 * y + 1) * 48 + 8 * q));
+    *reinterpret_cast<uint32_t*>(so2 + y * 24 + 4 * q) = w;
+    const LayerGeo& L = g.L[4];
+    const int gx0 = X0 >> 2, gy0 = Y0 >> 2;
+    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+  }
+  __syncthreads();
+  // ---- phase 3: i2 from i1, o3 from o2 ----
+  if (tid < 32) {
+    const int y = tid >> 2, q = tid & 3;
+    const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si1 + (2 * y) * 32 + 8 * q),
+                              *reinterpret_cast<const uint2*>(si1 + (2 * y + 1) * 32 + 8 * q));
+    *reinterpret_cast<uint32_t*>(si2 + y * 16 + 4 * q) = w;
+    const LayerGeo& L = g.L[5];
+    const int gx0 = (2 * X0 / 3) >> 2, gy0 = (2 * Y0 / 3) >> 2;
+    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+  } else if (tid < 32 + 18) {
+    const int i = tid - 32, y = i / 3, q = i - y * 3;
+    const uint32_t w = halve4(*reinterpret_cast<const uint2*>(so2 + (2 * y) * 24 + 8 * q),
+                              *reinterpret_cast<const uint2*>(so2 + (2 * y + 1) * 24 + 8 * q));
+    *reinterpret_cast<uint32_t*>(so3 + y * 12 + 4 * q) = w;
+    const LayerGeo& L = g.L[6];
+    const int gx0 = X0 >> 3, gy0 = Y0 >> 3;
+    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+  }
+  __syncthreads();
+  // ---- phase 4: i3 from i2; IDDM on o3 (masking.py:84-93) ----
+  if (tid < 8) {
+    const int y = tid >> 1, q = tid & 1;
+    const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si2 + (2 * y) * 16 + 8 * q),
+                              *reinterpret_cast<const uint2*>(si2 + (2 * y + 1) * 16 + 8 * q));
+    *reinterpret_cast<uint32_t*>(si3 + y * 8 + 4 * q) = w;
+    const LayerGeo& L = g.L[7];
+    const int gx0 = (2 * X0 / 3) >> 3, gy0 = (2 * Y0 / 3) >> 3;
+    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+  }
+  if (g.mask_mode == 1 && tid >= 32 && tid < 128) {
+    unsigned long long covered = 0;
+    const int i = tid - 32;
+    const LayerGeo& L = g.L[6];
+    const int gx0 = X0 >> 3, gy0 = Y0 >> 3;
+    if (i < 72) {
+      const int y = i / 12, x = i - y * 12;
+      if (gy0 + y < L.h && gx0 + x < L.w) {
+        const GridGeo& G = g.grid[0];
+        const long long gi = (long long)(gy0 + y) * L.w + gx0 + x;
+        uint8_t* st = b.state + (long long)s * g.state_slab + g.state_off[3];
+        const int c = so3[y * 12 + x];
+        if (use_mask(g, b, s)) {
+          int d = c - (int)st[gi];
+          d = d < 0 ? -d : d;
+          const int bit = (double)d > g.t_i;   // int16 diff vs float t_i, strict
+          b.cells[(long long)s * g.cell_slab + G.cell_off + gi] = (uint8_t)bit;
+          if (bit) {
+            long long hy = g.H - (long long)(gy0 + y) * G.ch, hx = g.W - (long long)(gx0 + x) * G.cw;
+            hy = hy < G.ch ? hy : G.ch;
+            hx = hx < G.cw ? hx : G.cw;
+            if (hy > 0 && hx > 0) covered = (unsigned long long)(hy * hx);
+          }
+        }
+        st[gi] = (uint8_t)c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) covered += __shfl_down_sync(0xffffffffu, covered, o);
+    if ((tid & 31) == 0 && covered) atomicAdd(b.cov + s, covered);
+  }
+}
+
+// ============================================================================
 // k_binmask: masking.py:96-136 (histogram of the previous MERGED features,
 // pipeline.py:184-185), thresholded at t_h; coverage = covered pixels / WH.
 // ============================================================================
@@ -535,7 +724,8 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     if (lane == 0 && cnt) atomicAdd(b.cov + s, cnt);
     return;
   }
-  const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // lane per FAST tile
+  const int tile = blockIdx.x * blockDim.x + threadIdx.x;
   if (tile >= g.tiles_per_stream) return;
   int l = 0;
   while (l + 1 < g.NL && tile >= g.L[l + 1].tile_base) l++;
@@ -551,21 +741,23 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     const int c0 = __ldg(lut + Lg.h + x0), c1 = __ldg(lut + Lg.h + x1);
     const GridGeo& G = g.grid[grid_of_layer(g, l)];
     const uint8_t* cells = b.cells + (long long)s * g.cell_slab + G.cell_off;
-    const int nc = c1 - c0 + 1, ncell = (r1 - r0 + 1) * nc;
-    int any = 0;
-    for (int i = lane; i < ncell && !any; i += 32) {
-      int r = r0 + i / nc, c = c0 + i % nc;
-      any = cells[(long long)r * G.cols + c];
+    active = 0;
+    for (int r = r0; r <= r1 && !active; r++) {
+      const uint8_t* row = cells + (long long)r * G.cols;
+      for (int c = c0; c <= c1; c++)
+        if (row[c]) { active = 1; break; }
     }
-    active = __any_sync(0xffffffffu, any);
   }
-  if (lane == 0) {
-    if (active) {
-      b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
-      b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
-      int pos = atomicAdd(b.work_count, 1);
-      b.worklist[pos] = s * g.tiles_per_stream + tile;
-    }
+  if (active) {
+    b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
+    b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
+    // warp-aggregated append to the work list
+    const unsigned m = __activemask();
+    const int leader = __ffs(m) - 1, rank = __popc(m & ((1u << lane) - 1));
+    int pos = 0;
+    if (lane == leader) pos = atomicAdd(b.work_count, __popc(m));
+    pos = __shfl_sync(m, pos, leader);
+    b.worklist[pos + rank] = s * g.tiles_per_stream + tile;
   }
 }
 
