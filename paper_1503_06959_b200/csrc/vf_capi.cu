@@ -106,13 +106,13 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
       GridGeo& G = g.grid[g.n_grids++];
       G.rows = hs[2 * lv]; G.cols = ws[2 * lv];
       G.cw = cdiv(g.W, G.cols); G.ch = cdiv(g.H, G.rows);
-      G.cell_off = co; co += align_up((long long)G.rows * G.cols, 64);
+      G.cell_off = co; co += align_up((long long)G.rows * G.cols + 4, 64);
     }
   } else if (g.mask_mode == 2) {
     GridGeo& G = g.grid[g.n_grids++];
     G.rows = c.grid_rows; G.cols = c.grid_cols;
     G.cw = cdiv(g.W, G.cols); G.ch = cdiv(g.H, G.rows);
-    G.cell_off = co; co += align_up((long long)G.rows * G.cols, 64);
+    G.cell_off = co; co += align_up((long long)G.rows * G.cols + 4, 64);
     if ((long long)G.rows * G.cols * 4 > 200 * 1024) return VF_ERR_GRID;
   }
   g.cell_slab = std::max(co, 64LL);
@@ -439,7 +439,7 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   else
     k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
   stage_mark(c, 2, st);
-  const int tile_ctas = cdiv(g.tiles_per_stream, 256);   // lane per tile
+  const int tile_ctas = cdiv(g.L[2].tile_base, 256) + cdiv(g.tiles_per_stream - g.L[2].tile_base, 8);
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
   const int carry_ctas = cdiv(g.pty, 8);
   k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(

@@ -456,8 +456,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   constexpr int TW = 96, TH = 48;
   __shared__ __align__(16) uint8_t t0[TH * TW];
   __shared__ __align__(16) uint8_t si0[32 * 64], so1[24 * 48], si1[16 * 32], so2[12 * 24], si2[8 * 16];
-  __shared__ __align__(16) uint8_t so3[6 * 12 + 8], si3[4 * 8];
-  __shared__ unsigned long long cov_part[4];
+  __shared__ __align__(16) uint8_t so3[6 * 12 + 8];
   const int s = blockIdx.z, tid = threadIdx.x;
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
   if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
@@ -580,7 +579,6 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     const int y = tid >> 1, q = tid & 1;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si2 + (2 * y) * 16 + 8 * q),
                               *reinterpret_cast<const uint2*>(si2 + (2 * y + 1) * 16 + 8 * q));
-    *reinterpret_cast<uint32_t*>(si3 + y * 8 + 4 * q) = w;
     const LayerGeo& L = g.L[7];
     const int gx0 = (2 * X0 / 3) >> 3, gy0 = (2 * Y0 / 3) >> 3;
     store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
@@ -724,9 +722,21 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     if (lane == 0 && cnt) atomicAdd(b.cov + s, cnt);
     return;
   }
-  // lane per FAST tile
-  const int tile = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tile >= g.tiles_per_stream) return;
+  // FAST tiles: lane per tile for layers 0-1 (small cell rectangles), warp
+  // per tile for coarser layers (a tile of o3 projects to 8 x 128 cells)
+  const int n_fine = g.L[2].tile_base;            // tiles of layers 0 and 1
+  const int lane_ctas = (n_fine + 255) / 256;
+  int tile;
+  bool warp_mode;
+  if ((int)blockIdx.x < lane_ctas) {
+    tile = blockIdx.x * 256 + threadIdx.x;
+    warp_mode = false;
+    if (tile >= n_fine) return;
+  } else {
+    tile = n_fine + (blockIdx.x - lane_ctas) * 8 + (threadIdx.x >> 5);
+    warp_mode = true;
+    if (tile >= g.tiles_per_stream) return;
+  }
   int l = 0;
   while (l + 1 < g.NL && tile >= g.L[l + 1].tile_base) l++;
   const LayerGeo& Lg = g.L[l];
@@ -741,12 +751,38 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     const int c0 = __ldg(lut + Lg.h + x0), c1 = __ldg(lut + Lg.h + x1);
     const GridGeo& G = g.grid[grid_of_layer(g, l)];
     const uint8_t* cells = b.cells + (long long)s * g.cell_slab + G.cell_off;
-    active = 0;
-    for (int r = r0; r <= r1 && !active; r++) {
-      const uint8_t* row = cells + (long long)r * G.cols;
-      for (int c = c0; c <= c1; c++)
-        if (row[c]) { active = 1; break; }
+    // any set cell in rows r0..r1, columns c0..c1: aligned 32-bit words (the
+    // cell slab is padded), partial words masked
+    const int nrow = r1 - r0 + 1;
+    const uintptr_t first = reinterpret_cast<uintptr_t>(cells + c0) & ~(uintptr_t)3;
+    const int nwd = (int)(((reinterpret_cast<uintptr_t>(cells + c1) & ~(uintptr_t)3) - first) / 4) + 1;
+    const int head = (int)(reinterpret_cast<uintptr_t>(cells + c0) & 3);
+    const int tail = (int)(reinterpret_cast<uintptr_t>(cells + c1) & 3);
+    auto word_any = [&](int r, int k) -> uint32_t {
+      const uint32_t* wp = reinterpret_cast<const uint32_t*>(first + (uintptr_t)r * G.cols) + k;
+      uint32_t v = *wp;
+      if (k == 0) v &= 0xffffffffu << (8 * head);
+      if (k == nwd - 1) v &= 0xffffffffu >> (8 * (3 - tail));
+      return v;
+    };
+    if (!warp_mode) {
+      active = 0;
+      for (int r = r0; r <= r1 && !active; r++)
+        for (int k = 0; k < nwd; k++)
+          if (word_any(r, k)) { active = 1; break; }
+    } else {
+      int any = 0;
+      for (int i = lane; i < nrow * nwd && !any; i += 32) any = word_any(r0 + i / nwd, i % nwd) != 0;
+      active = __any_sync(0xffffffffu, any);
     }
+  }
+  if (warp_mode) {
+    if (lane == 0 && active) {
+      b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
+      b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
+      b.worklist[atomicAdd(b.work_count, 1)] = s * g.tiles_per_stream + tile;
+    }
+    return;
   }
   if (active) {
     b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
