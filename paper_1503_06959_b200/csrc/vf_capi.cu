@@ -341,7 +341,9 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, 128, 0);
+  const int fast_smem = (int)sizeof(FastWarp) * FAST_WARPS;
+  cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, fast_smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, 32 * FAST_WARPS, fast_smem);
   c->fast_grid = std::max(1, g_num_sms * std::max(occ, 1));
   c->sat_smem = ((g.ptw * g.pth + 15) & ~15) + g.ptw * g.pth * 4 + (S + 1) * 4;
   if (c->sat_smem > 48 * 1024) cudaFuncSetAttribute(k_sat, cudaFuncAttributeMaxDynamicSharedMemorySize, c->sat_smem);
@@ -445,7 +447,7 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(
       g, b, tile_ctas, cov_ctas, carry_ctas);
   stage_mark(c, 3, st);
-  k_fast<<<c->fast_grid, 128, 0, st>>>(g, b);
+  k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS, st>>>(g, b);
   stage_mark(c, 4, st);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
@@ -702,7 +704,8 @@ int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, c
   cudaMemcpyAsync(b.worklist, wl.data(), sizeof(int) * nwl, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.work_count, &nwl, sizeof(int), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.ctr, frame1, sizeof(frame1), cudaMemcpyHostToDevice, st);
-  k_fast<<<std::max(1, std::min(nwl, 148 * 8)), 128, 0, st>>>(g, b);
+  cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FastWarp) * FAST_WARPS);
+  k_fast<<<std::max(1, std::min(cdiv(nwl, FAST_WARPS), 148 * 8)), 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS, st>>>(g, b);
   cudaMemcpy2DAsync(scores_dev, scores_pitch, b.scores, L.pitch, w, h, cudaMemcpyDeviceToDevice, st);
   int rc = cuda_status(cudaStreamSynchronize(st));
   A.release();

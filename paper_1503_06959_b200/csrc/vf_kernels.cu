@@ -825,17 +825,26 @@ __device__ __forceinline__ uint32_t arc_max_min9(const uint32_t w[4])
   return m & 0xffu;
 }
 
-__global__ void __launch_bounds__(128) k_fast(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+// Warp per tile (no block barriers): each warp stages its tile, runs the
+// pre-test, scores its queue and stores, with __syncwarp only.
+#define FAST_WARPS 8
+struct FastWarp {
+  uint8_t tile[FT_ROWS][FT_COLS];
+  uint8_t sc[VF_TILE_H][VF_TILE_W];
+  uint16_t queue[VF_TILE_H * VF_TILE_W];
+  int rc[VF_TILE_H];          // cell row of each tile row (gating)
+  uint16_t cc[VF_TILE_W];     // cell column of each tile column
+};
+
+__global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
-  __shared__ __align__(16) uint8_t tile[FT_ROWS][FT_COLS];
-  __shared__ __align__(16) uint8_t sc[VF_TILE_H][VF_TILE_W];
-  __shared__ uint16_t queue[VF_TILE_H * VF_TILE_W];
-  __shared__ int qn;
-  const int tid = threadIdx.x;
+  extern __shared__ __align__(16) uint8_t fsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  FastWarp& fw = reinterpret_cast<FastWarp*>(fsm)[wid];
   const int n_work = *b.work_count;
   const int t = g.threshold;
   const uint32_t tt = (uint32_t)t * 0x01010101u;
-  for (int item = blockIdx.x; item < n_work; item += gridDim.x) {
+  for (int item = blockIdx.x * FAST_WARPS + wid; item < n_work; item += gridDim.x * FAST_WARPS) {
     const int code = b.worklist[item];
     const int s = code / g.tiles_per_stream, tile_id = code - s * g.tiles_per_stream;
     int l = 0;
@@ -848,11 +857,25 @@ __global__ void __launch_bounds__(128) k_fast(const __grid_constant__ Geo g, con
     int pitch;
     const uint8_t* lp = layer_ptr(g, b, s, l, pitch);
     const int um = use_mask(g, b, s);
+    const uint8_t* cells = nullptr;
+    int cols = 0;
+    if (um) {
+      const GridGeo& G = g.grid[grid_of_layer(g, l)];
+      cells = b.cells + (long long)s * g.cell_slab + G.cell_off;
+      cols = G.cols;
+      const int* lut = b.lut + Lg.rc_off;
+      if (lane < VF_TILE_H) fw.rc[lane] = y0 + lane < h ? __ldg(lut + y0 + lane) : 0;
+#pragma unroll
+      for (int k = 0; k < VF_TILE_W / 32; k++) {
+        const int x = x0 + 32 * k + lane;
+        fw.cc[32 * k + lane] = (uint16_t)(x < w ? __ldg(lut + h + x) : 0);
+      }
+    }
     // ---- stage rows y0-3 .. y0+10, cols x0-16 .. x0+143 ----
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(lp) | (uintptr_t)pitch) & 15) == 0;
-    for (int i = tid; i < FT_ROWS * (FT_COLS / 16); i += blockDim.x) {
-      int rr = i / (FT_COLS / 16), cc = i - rr * (FT_COLS / 16);
-      int y = y0 - 3 + rr, x = x0 - 16 + 16 * cc;
+    for (int i = lane; i < FT_ROWS * (FT_COLS / 16); i += 32) {
+      const int rr = i / (FT_COLS / 16), c16 = i - rr * (FT_COLS / 16);
+      const int y = y0 - 3 + rr, x = x0 - 16 + 16 * c16;
       uint4 v = make_uint4(0, 0, 0, 0);
       if (y >= 0 && y < h) {
         const uint8_t* row = lp + (long long)y * pitch;
@@ -865,24 +888,23 @@ __global__ void __launch_bounds__(128) k_fast(const __grid_constant__ Geo g, con
           v = *reinterpret_cast<uint4*>(tmp);
         }
       }
-      *reinterpret_cast<uint4*>(&tile[rr][16 * cc]) = v;
+      *reinterpret_cast<uint4*>(&fw.tile[rr][16 * c16]) = v;
     }
-    for (int i = tid; i < VF_TILE_H * VF_TILE_W / 16; i += blockDim.x)
-      reinterpret_cast<uint4*>(&sc[0][0])[i] = make_uint4(0, 0, 0, 0);
-    if (tid == 0) qn = 0;
-    __syncthreads();
+    for (int i = lane; i < VF_TILE_H * VF_TILE_W / 16; i += 32)
+      reinterpret_cast<uint4*>(&fw.sc[0][0])[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
     // ---- pass 1: 4-point necessary test, 4 pixels per word ----
-    for (int wi = tid; wi < VF_TILE_H * (VF_TILE_W / 4); wi += blockDim.x) {
-      const int r = wi >> 5, k = wi & 31;
-      const int y = y0 + r;
+    int qn = 0;
+    for (int r = 0; r < VF_TILE_H; r++) {
+      const int y = y0 + r, k = lane;       // word k of row r: pixels x0 + 4k .. +3
       uint32_t pass = 0;
       if (y >= 3 && y < h - 3) {
         const int cb = 16 + 4 * k;
-        const uint32_t C = *reinterpret_cast<const uint32_t*>(&tile[r + 3][cb]);
-        const uint32_t P = *reinterpret_cast<const uint32_t*>(&tile[r + 3][cb - 4]);
-        const uint32_t B = *reinterpret_cast<const uint32_t*>(&tile[r + 3][cb + 4]);
-        const uint32_t N = *reinterpret_cast<const uint32_t*>(&tile[r][cb]);
-        const uint32_t S = *reinterpret_cast<const uint32_t*>(&tile[r + 6][cb]);
+        const uint32_t C = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb]);
+        const uint32_t P = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb - 4]);
+        const uint32_t B = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb + 4]);
+        const uint32_t N = *reinterpret_cast<const uint32_t*>(&fw.tile[r][cb]);
+        const uint32_t S = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 6][cb]);
         const uint32_t E = __byte_perm(C, B, 0x6543), Wd = __byte_perm(P, C, 0x4321);
         const uint32_t br = (__vcmpgtu4(__vsubus4(N, C), tt) | __vcmpgtu4(__vsubus4(S, C), tt)) &
                             (__vcmpgtu4(__vsubus4(E, C), tt) | __vcmpgtu4(__vsubus4(Wd, C), tt));
@@ -890,83 +912,77 @@ __global__ void __launch_bounds__(128) k_fast(const __grid_constant__ Geo g, con
                             (__vcmpgtu4(__vsubus4(C, E), tt) | __vcmpgtu4(__vsubus4(C, Wd), tt));
         pass = br | dk;
         if (pass) {
+          const uint8_t* crow = um ? cells + (long long)fw.rc[r] * cols : nullptr;
 #pragma unroll
           for (int i = 0; i < 4; i++) {
-            const int x = x0 + 4 * k + i;
+            const int xl = 4 * k + i, x = x0 + xl;
             bool ok = x >= 3 && x < w - 3;
-            if (ok && um) ok = gate_at(g, b, s, l, y, x);
+            if (ok && um) ok = crow[fw.cc[xl]] != 0;   // gate (detector.py:175-181)
             if (!ok) pass &= ~(0xffu << (8 * i));
           }
         }
       }
       const int np = __popc(pass) >> 3;
-      // warp-aggregated queue append
       int incl = np;
-      const int lane = tid & 31;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
       }
-      int wbase = 0;
-      const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-      if (lane == 31 && wtot) wbase = atomicAdd(&qn, wtot);
-      wbase = __shfl_sync(0xffffffffu, wbase, 31);
-      int pos = wbase + incl - np;
+      int pos = qn + incl - np;
 #pragma unroll
       for (int i = 0; i < 4; i++)
-        if (pass & (0xffu << (8 * i))) queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + i);
+        if (pass & (0xffu << (8 * i))) fw.queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + i);
+      qn += __shfl_sync(0xffffffffu, incl, 31);
     }
-    __syncthreads();
+    __syncwarp();
     // ---- pass 2: exact score of queued pixels ----
-    const int nq = qn;
-    for (int qi = tid; qi < nq; qi += blockDim.x) {
-      const int p = queue[qi];
+    for (int qi = lane; qi < qn; qi += 32) {
+      const int p = fw.queue[qi];
       const int r = p / VF_TILE_W, c = p - r * VF_TILE_W;
       const int R = r + 3, Cc = 16 + c;
-      const uint32_t ctr = tile[R][Cc];
+      const uint32_t ctr = fw.tile[R][Cc];
       uint32_t ring[4];
-      ring[0] = tile[R - 3][Cc] | (tile[R - 3][Cc + 1] << 8) | (tile[R - 2][Cc + 2] << 16) | (tile[R - 1][Cc + 3] << 24);
-      ring[1] = tile[R][Cc + 3] | (tile[R + 1][Cc + 3] << 8) | (tile[R + 2][Cc + 2] << 16) | (tile[R + 3][Cc + 1] << 24);
-      ring[2] = tile[R + 3][Cc] | (tile[R + 3][Cc - 1] << 8) | (tile[R + 2][Cc - 2] << 16) | (tile[R + 1][Cc - 3] << 24);
-      ring[3] = tile[R][Cc - 3] | (tile[R - 1][Cc - 3] << 8) | (tile[R - 2][Cc - 2] << 16) | (tile[R - 3][Cc - 1] << 24);
+      ring[0] = fw.tile[R - 3][Cc] | (fw.tile[R - 3][Cc + 1] << 8) | (fw.tile[R - 2][Cc + 2] << 16) | (fw.tile[R - 1][Cc + 3] << 24);
+      ring[1] = fw.tile[R][Cc + 3] | (fw.tile[R + 1][Cc + 3] << 8) | (fw.tile[R + 2][Cc + 2] << 16) | (fw.tile[R + 3][Cc + 1] << 24);
+      ring[2] = fw.tile[R + 3][Cc] | (fw.tile[R + 3][Cc - 1] << 8) | (fw.tile[R + 2][Cc - 2] << 16) | (fw.tile[R + 1][Cc - 3] << 24);
+      ring[3] = fw.tile[R][Cc - 3] | (fw.tile[R - 1][Cc - 3] << 8) | (fw.tile[R - 2][Cc - 2] << 16) | (fw.tile[R - 3][Cc - 1] << 24);
       const uint32_t c4 = ctr * 0x01010101u;
       uint32_t bw[4], dw[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) { bw[q] = __vsubus4(ring[q], c4); dw[q] = __vsubus4(c4, ring[q]); }
       const int best = (int)max(arc_max_min9(bw), arc_max_min9(dw));
       const int score = best - 1;
-      if (score >= t) sc[r][c] = (uint8_t)score;
+      if (score >= t) fw.sc[r][c] = (uint8_t)score;
     }
-    __syncthreads();
+    __syncwarp();
     // ---- store scores (whole tile: gated pixels read back as 0) + bitmap ----
     uint8_t* smap = b.scores + (long long)s * g.sm_slab + Lg.sm_off;
-    for (int i = tid; i < VF_TILE_H * (VF_TILE_W / 16); i += blockDim.x) {
+    for (int i = lane; i < VF_TILE_H * (VF_TILE_W / 16); i += 32) {
       const int r = i >> 3, cc = i & 7;
       const int y = y0 + r, x = x0 + 16 * cc;
       if (y >= h || x >= w) continue;
-      uint8_t* dst = smap + (long long)y * Lg.pitch + x;
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&sc[r][16 * cc]);  // pitch padded to 16
+      *reinterpret_cast<uint4*>(smap + (long long)y * Lg.pitch + x) = *reinterpret_cast<const uint4*>(&fw.sc[r][16 * cc]);
     }
-    if (tid < VF_TILE_H * VF_TILE_WORDS) {
-      const int r = tid >> 2, kw = tid & 3;
+    {
+      const int r = lane >> 2, kw = lane & 3;
       const int y = y0 + r;
-      if (y < h && x0 + 32 * kw < w) {
-        uint32_t word = 0;
+      uint32_t word = 0;
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-          uint32_t v = *reinterpret_cast<const uint32_t*>(&sc[r][32 * kw + 4 * q]);
-          uint32_t nz = __vcmpne4(v, 0u);
-          // bytes 0xff/0x00 -> 4 bits
-          uint32_t bits = ((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) | ((nz >> 28) & 8u);
-          word |= bits << (4 * q);
-        }
-        b.bitmaps[(long long)s * g.bm_slab_words + Lg.bm_off + (long long)y * Lg.bm_words + 4 * tx + kw] = word;
-        const int n = __popc(word);
-        if (n) atomicAdd(&b.ctr[s * C_NCTR + C_NCAND], n);
+      for (int q = 0; q < 8; q++) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(&fw.sc[r][32 * kw + 4 * q]);
+        const uint32_t nz = __vcmpne4(v, 0u);
+        const uint32_t bits = ((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) | ((nz >> 28) & 8u);
+        word |= bits << (4 * q);
       }
+      if (y < h && x0 + 32 * kw < w)
+        b.bitmaps[(long long)s * g.bm_slab_words + Lg.bm_off + (long long)y * Lg.bm_words + 4 * tx + kw] = word;
+      int n = __popc(word);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+      if (lane == 0 && n) atomicAdd(&b.ctr[s * C_NCTR + C_NCAND], n);
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
