@@ -1221,7 +1221,7 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
 // (layer, y): the reference order.
 #define NMS_WARPS 4
 #define NMS_THREADS (32 * NMS_WARPS)
-__global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+__global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int cand[NMS_WARPS][32];
   const int s = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1242,10 +1242,16 @@ __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo
     const int* tst = b.tile_stamp + (long long)s * g.tiles_per_stream + Lg.tile_base + ty * Lg.tiles_x;
     const int per = (nwords + 31) / 32;
     const int w0 = lane * per, w1 = min(nwords, w0 + per);
+    const int bmw = Lg.bm_words;
     int cnt = 0;
-    for (int i = w0; i < w1; i++) {
-      const int k = i % Lg.bm_words;
-      if (__ldg(tst + k / VF_TILE_WORDS) == epoch) cnt += __popc(__ldg(bm + i));
+    {
+      int k = w0 % bmw;                     // word column, advanced incrementally
+      int stamp_ok = 1;
+      for (int i = w0; i < w1; i++) {
+        if (um && (i == w0 || (k & (VF_TILE_WORDS - 1)) == 0)) stamp_ok = __ldg(tst + k / VF_TILE_WORDS) == epoch;
+        if (stamp_ok) cnt += __popc(__ldg(bm + i));
+        if (++k == bmw) k = 0;
+      }
     }
     int total;
     const int ex = warp_excl_scan(cnt, lane, total);
@@ -1257,23 +1263,24 @@ __global__ void __launch_bounds__(NMS_THREADS) k_nms(const __grid_constant__ Geo
       }
       base = __shfl_sync(0xffffffffu, bs, 0);
       if (base >= 0) {
-        auto load_word = [&](int i) -> uint32_t {
-          return (__ldg(tst + (i % Lg.bm_words) / VF_TILE_WORDS) == epoch) ? __ldg(bm + i) : 0u;
+        int crow = w0 / bmw, ck = w0 - crow * bmw;   // row / column of the cursor word
+        auto load_word = [&]() -> uint32_t {
+          return (!um || __ldg(tst + ck / VF_TILE_WORDS) == epoch) ? __ldg(bm + crow * bmw + ck) : 0u;
         };
         int cursor = w0, idx = ex;             // this lane's enumeration state
-        uint32_t pend = cursor < w1 ? load_word(cursor) : 0u;
+        uint32_t pend = cursor < w1 ? load_word() : 0u;
         for (int r0 = 0; r0 < total; r0 += 32) {
           // emit this round's candidates (ranks r0 .. r0+31) into cand[]
           while (idx < r0 + 32 && cursor < w1) {
             if (!pend) {
               cursor++;
-              pend = cursor < w1 ? load_word(cursor) : 0u;
+              if (++ck == bmw) { ck = 0; crow++; }
+              pend = cursor < w1 ? load_word() : 0u;
               continue;
             }
             const int bit = __ffs(pend) - 1;
             pend &= pend - 1;
-            if (idx >= r0)
-              cand[wid][idx - r0] = ((y0 + cursor / Lg.bm_words) << 16) | (32 * (cursor % Lg.bm_words) + bit);
+            if (idx >= r0) cand[wid][idx - r0] = ((y0 + crow) << 16) | (32 * ck + bit);
             idx++;
           }
           __syncwarp();
