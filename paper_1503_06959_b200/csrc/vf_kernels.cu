@@ -1501,22 +1501,23 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, const u
 // position in the reference's op order, clamped box, branch-free strip-SAT
 // corners (masked corners re-read corner A and are multiplied by 0), exact
 // sum // area.
+// px, py, rad: pattern point j (held in registers by the caller: lane-varying
+// constant-memory reads would serialize).
 __device__ __forceinline__ uint32_t point_mean(const uint32_t* S, const Geo& g, double kx, double ky, double sg,
-                                               double cs, double sn, int j, bool rotated)
+                                               double cs, double sn, double px, double py, double rad, bool rotated)
 {
   double fx, fy;
   if (rotated) {
-    const double px = c_px[j], py = c_py[j];
     fx = kx + sg * (cs * px - sn * py) + 0.5;
     fy = ky + sg * (sn * px + cs * py) + 0.5;
   } else {
-    fx = kx + sg * c_px[j] + 0.5;
-    fy = ky + sg * c_py[j] + 0.5;
+    fx = kx + sg * px + 0.5;
+    fy = ky + sg * py + 0.5;
   }
   long long x = (long long)floor(fx), y = (long long)floor(fy);
   x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
   y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
-  const int r = (int)floor(c_rad[j] * sg + 0.5);
+  const int r = (int)floor(rad * sg + 0.5);
   const int x0 = max((int)x - r, 0), x1 = min((int)x + r, g.W - 1);
   const int y0 = max((int)y - r, 0), y1 = min((int)y + r, g.H - 1);
   const int TH = g.pth;
@@ -1562,6 +1563,10 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
   for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
   stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
+  // this lane's two pattern points (lane, lane + 32)
+  const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
+  const double px0 = c_px[lane], py0 = c_py[lane], rd0 = c_rad[lane];
+  const double px1 = c_px[j1], py1 = c_py[j1], rd1 = c_rad[j1];
   for (int gi = blockIdx.x * DSW + wid; gi < total; gi += gridDim.x * DSW) {
     const int s = find_stream(pre, n_streams, gi), i = gi - pre[s];
     const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
@@ -1584,9 +1589,8 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
       kx = b.fx[o]; ky = b.fy[o]; sg = b.fs[o];
       sincos(b.ft[o], &sn, &cs);
     }
-    const uint32_t m0 = point_mean(S, g, kx, ky, sg, cs, sn, lane, pass != 0);
-    uint32_t m1 = 0;
-    if (lane + 32 < VF_NPTS) m1 = point_mean(S, g, kx, ky, sg, cs, sn, lane + 32, pass != 0);
+    const uint32_t m0 = point_mean(S, g, kx, ky, sg, cs, sn, px0, py0, rd0, pass != 0);
+    const uint32_t m1 = point_mean(S, g, kx, ky, sg, cs, sn, px1, py1, rd1, pass != 0);
     uint8_t* v = vals[wid];
     v[lane] = (uint8_t)m0;
     if (lane + 32 < VF_NPTS) v[lane + 32] = (uint8_t)m1;
