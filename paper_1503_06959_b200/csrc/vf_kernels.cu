@@ -56,9 +56,82 @@ __device__ __forceinline__ void lvl_dims(const Geo& g, int l, int& lw, int& lh)
 // box sum is 4 strip-SAT corners per strip it spans (<= 2 strips for O = 4).
 // All values < 2^32 and box sums are exact in uint32.
 // ----------------------------------------------------------------------------
+// Strip SAT of one tile into gs, from the o0 tile in smem (pitch ptw).
+// Warp w owns rows [w*RPW, (w+1)*RPW), lane l owns columns [l*CPL, (l+1)*CPL):
+// row prefixes by warp scan, column sums accumulated in registers down the
+// warp's rows, one smem exchange of the per-warp column totals, then
+// S(y, x) = column prefix + K(y, tx) stored straight from registers.
+// Needs ptw % 32 == 0, pth % 8 == 0, blockDim == 256 (true for O <= 7).
+template <int CPL>
+__device__ void sat_tile_reg(const Geo& g, const Bufs& b, int s, int tx, int ty, int tw, int th, const uint8_t* t0,
+                             uint32_t* xch, uint32_t* gs)
+{
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int RPW = g.pth >> 3;
+  const int X0 = tx * g.ptw, Y0 = ty * g.pth;
+  const int xb = lane * CPL;
+  uint32_t col[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; c++) col[c] = 0;
+  // pass 1: column totals of this warp's rows
+  for (int r = 0; r < RPW; r++) {
+    const int y = wid * RPW + r;
+    uint32_t v[CPL], run = 0;
+#pragma unroll
+    for (int c = 0; c < CPL; c++) { v[c] = (y < th && xb + c < tw) ? t0[y * g.ptw + xb + c] : 0u; run += v[c]; }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    uint32_t pre = inc - run;
+#pragma unroll
+    for (int c = 0; c < CPL; c++) { pre += v[c]; col[c] += pre; }
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; c++) xch[wid * 32 * CPL + xb + c] = col[c];
+  __syncthreads();
+  // offset of rows above this warp's block
+#pragma unroll
+  for (int c = 0; c < CPL; c++) {
+    uint32_t off = 0;
+    for (int w = 0; w < wid; w++) off += xch[w * 32 * CPL + xb + c];
+    col[c] = off;
+  }
+  // pass 2: recompute the row prefixes, accumulate, add the strip carry, store
+  const uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx + tx;
+  for (int r = 0; r < RPW; r++) {
+    const int y = wid * RPW + r;
+    if (y >= th) break;
+    uint32_t v[CPL], run = 0;
+#pragma unroll
+    for (int c = 0; c < CPL; c++) { v[c] = (xb + c < tw) ? t0[y * g.ptw + xb + c] : 0u; run += v[c]; }
+    uint32_t inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    uint32_t pre = inc - run;
+    const uint32_t k = __ldg(K + (long long)y * g.ptx);
+    uint32_t* dst = gs + (long long)(Y0 + y) * g.W + X0 + xb;
+#pragma unroll
+    for (int c = 0; c < CPL; c++) {
+      pre += v[c];
+      col[c] += pre;
+      if (xb + c < tw) dst[c] = col[c] + k;
+    }
+  }
+}
+
 __device__ void sat_tile(const Geo& g, const Bufs& b, int s, int tx, int ty, int tw, int th, const uint8_t* t0,
                          uint32_t* ssat, uint32_t* gs)
 {
+  if (g.ptw == 96 && (g.pth & 7) == 0 && blockDim.x == 256) {
+    sat_tile_reg<3>(g, b, s, tx, ty, tw, th, t0, ssat, gs);
+    return;
+  }
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   const int per = (g.ptw + 31) / 32;
