@@ -297,6 +297,8 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.band_stamp = A.get<int>((size_t)S * g.bands_per_stream);
   b.band_rec = A.get<int>((size_t)S * g.bands_per_stream * 4);
   b.band_out = A.get<int>((size_t)S * g.bands_per_stream);
+  b.band_cand = A.get<int>((size_t)S * g.bands_per_stream);
+  b.gidx = A.get<int>((size_t)S * cap);
   b.prop_cnt = A.get<int>((size_t)S * g.prop_chunks);
   b.prop_out = A.get<int>((size_t)S * g.prop_chunks);
   b.cells = A.get<uint8_t>((size_t)S * g.cell_slab);
@@ -687,6 +689,7 @@ int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, c
   b.bitmaps = A.get<uint32_t>(g.bm_slab_words);
   b.tile_stamp = A.get<int>(g.tiles_per_stream);
   b.band_stamp = A.get<int>(g.bands_per_stream);
+  b.band_cand = A.get<int>(g.bands_per_stream);
   int* dl = A.get<int>(lut.size());
   b.lut = dl;
   b.cells = const_cast<uint8_t*>(mask_dev);
@@ -746,6 +749,7 @@ int vf_nms_refine(const uint8_t* const* maps_dev, const int64_t* pitches, int W,
   std::vector<int> ones(std::max(g.tiles_per_stream, g.bands_per_stream), 1);
   cudaMemcpyAsync(b.tile_stamp, ones.data(), sizeof(int) * g.tiles_per_stream, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.band_stamp, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(b.band_cand, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), 1), NMS_THREADS, 0, st>>>(g, b);
   k_gather_kps<<<g.bands_per_stream, 128, 0, st>>>(g, b, x_dev, y_dev, sigma_dev, score_dev, cap);
   int ctr[C_NCTR];

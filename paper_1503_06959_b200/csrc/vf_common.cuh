@@ -90,6 +90,8 @@ struct Bufs {
   int* band_stamp;      // [S][bands_per_stream]
   int* band_rec;        // [S][bands_per_stream][4]: staging base, kept, border-ok, dropped
   int* band_out;        // [S][bands_per_stream]: output offset of the band's kept keypoints
+  int* band_cand;       // [S][bands_per_stream]: FAST candidates of the band this step
+  int* gidx;            // [S][kp_cap]: detected rank -> staging slot
   int* prop_cnt;        // [S][prop_chunks]
   int* prop_out;        // [S][prop_chunks]
   uint8_t* cells;       // [S][cell_slab]

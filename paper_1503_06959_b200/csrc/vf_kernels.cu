@@ -479,6 +479,17 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
   uint32_t* ssat = reinterpret_cast<uint32_t*>(smem + ((g.ptw * g.pth + 15) & ~15));
   int* pre = reinterpret_cast<int*>(ssat + g.ptw * g.pth);
   __shared__ int sm_warp[32];
+  // detected rank -> staging slot map for k_desc_sample (thread per band)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)n_streams * g.bands_per_stream;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(i / g.bands_per_stream);
+    const int4 r = __ldcg(reinterpret_cast<const int4*>(b.band_rec) + i);
+    if (r.y > 0) {
+      const int o = __ldcg(b.band_out + i);
+      int* gidx = b.gidx + (long long)s * g.kp_cap;
+      for (int k = 0; k < r.y && o + k < g.kp_cap; k++) gidx[o + k] = r.x + k;
+    }
+  }
   stream_prefix(n_streams, pre, sm_warp, [&](int s) { return use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles; });
   const int n = pre[n_streams];
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
@@ -765,10 +776,10 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
     for (int c = blockIdx.x - tile_ctas - cov_ctas - carry_ctas; c < nch; c += PROP_CTAS) {
       int cnt = 0;
-      for (int j = 0; j < PROP_CHUNK / 256; j++) {
-        const int e = c * PROP_CHUNK + j * 256 + threadIdx.x;
-        if (e < n_prev) cnt += !merge_mask_at(g, b, s, b.fx[fb + e], b.fy[fb + e]);
-      }
+      const int e0 = c * PROP_CHUNK + threadIdx.x * (PROP_CHUNK / 256);
+#pragma unroll
+      for (int k = 0; k < PROP_CHUNK / 256; k++)
+        if (e0 + k < n_prev) cnt += !merge_mask_at(g, b, s, b.fx[fb + e0 + k], b.fy[fb + e0 + k]);
       int tot;
       block_excl_scan<int>(cnt, sm_warp, tot);
       if (threadIdx.x == 0) b.prop_cnt[(long long)s * g.prop_chunks + c] = tot;
@@ -853,6 +864,7 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     if (lane == 0 && active) {
       b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
       b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
+      b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
       b.worklist[atomicAdd(b.work_count, 1)] = s * g.tiles_per_stream + tile;
     }
     return;
@@ -860,6 +872,7 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
   if (active) {
     b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
     b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
+    b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
     // warp-aggregated append to the work list
     const unsigned m = __activemask();
     const int leader = __ffs(m) - 1, rank = __popc(m & ((1u << lane) - 1));
@@ -1053,7 +1066,10 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       int n = __popc(word);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
-      if (lane == 0 && n) atomicAdd(&b.ctr[s * C_NCTR + C_NCAND], n);
+      if (lane == 0 && n) {
+        atomicAdd(&b.ctr[s * C_NCTR + C_NCAND], n);
+        atomicAdd(&b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty], n);
+      }
     }
     __syncwarp();
   }
@@ -1304,7 +1320,8 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
   const int um = use_mask(g, b, s) ? epoch : 0;   // nonzero: tile-stamp gating at this epoch
   int* ctr = b.ctr + s * C_NCTR;
   int kept = 0, n_ok = 0, n_drop = 0, base = 0;
-  if (b.band_stamp[(long long)s * g.bands_per_stream + bid] == epoch) {
+  if (b.band_stamp[(long long)s * g.bands_per_stream + bid] == epoch &&
+      __ldcg(b.band_cand + (long long)s * g.bands_per_stream + bid) > 0) {
     int l = 0;
     while (l + 1 < g.NL && bid >= g.L[l + 1].band_base) l++;
     const LayerGeo& Lg = g.L[l];
@@ -1647,12 +1664,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
     const uint32_t* S = b.sat + (long long)(s % g.sat_slots) * g.W * g.H;
     double kx, ky, sg, cs = 1.0, sn = 0.0;
     if (pass == 0) {
-      // band of rank i (last band with band_out <= i) -> staging slot
-      const int* bout = b.band_out + (long long)s * g.bands_per_stream;
-      int blo = 0, bhi = g.bands_per_stream;
-      while (bhi - blo > 1) { int m = (blo + bhi) >> 1; if (__ldg(bout + m) <= i) blo = m; else bhi = m; }
-      const int* rec = b.band_rec + ((long long)s * g.bands_per_stream + blo) * 4;
-      const long long si = (long long)s * g.kp_cap + rec[0] + (i - __ldg(bout + blo));
+      const long long si = (long long)s * g.kp_cap + __ldg(b.gidx + (long long)s * g.kp_cap + i);   // staging slot
       kx = b.st_x[si]; ky = b.st_y[si]; sg = b.st_s[si];
       if (lane == 0) {
         b.fx[o] = kx; b.fy[o] = ky; b.fs[o] = sg; b.fv[o] = b.st_v[si];
@@ -1739,23 +1751,37 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ Geo g
   const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
   const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
   const long long ob = ((long long)s * 2 + cur) * g.kp_cap;
+  constexpr int PER = PROP_CHUNK / 256;
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-    long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
-    for (int j = 0; j < PROP_CHUNK / 256; j++) {
+    // element j*256 + tid of the chunk: consecutive lanes -> consecutive features
+    double xs[PER], ys[PER];
+    bool f[PER];
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
       const int e = c * PROP_CHUNK + j * 256 + tid;
-      int f = 0;
-      if (e < n_prev) f = !merge_mask_at(g, b, s, b.fx[fb + e], b.fy[fb + e]);
+      xs[j] = e < n_prev ? b.fx[fb + e] : 0.0;
+      ys[j] = e < n_prev ? b.fy[fb + e] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
+      const int e = c * PROP_CHUNK + j * 256 + tid;
+      f[j] = e < n_prev && !merge_mask_at(g, b, s, xs[j], ys[j]);
+    }
+    long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
       int tot;
-      const int ex = block_excl_scan<int>(f, sm_warp, tot);
-      if (f) {
+      const int ex = block_excl_scan<int>(f[j] ? 1 : 0, sm_warp, tot);
+      if (f[j]) {
         const long long dst = dst0 + ex;
         if (dst < g.kp_cap) {
-          const long long o = ob + dst, p = fb + e;
-          b.fx[o] = b.fx[p]; b.fy[o] = b.fy[p]; b.fs[o] = b.fs[p]; b.ft[o] = b.ft[p]; b.fv[o] = b.fv[p];
+          const long long o = ob + dst, p = fb + c * PROP_CHUNK + j * 256 + tid;
+          b.fx[o] = xs[j]; b.fy[o] = ys[j]; b.fs[o] = b.fs[p]; b.ft[o] = b.ft[p]; b.fv[o] = b.fv[p];
           b.forg[o] = 1; b.fage[o] = b.fage[p] + 1;
           const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + p * 64);
           uint4* dd = reinterpret_cast<uint4*>(b.fdesc + o * 64);
-          dd[0] = sd[0]; dd[1] = sd[1]; dd[2] = sd[2]; dd[3] = sd[3];
+          const uint4 d0 = sd[0], d1 = sd[1], d2 = sd[2], d3 = sd[3];
+          dd[0] = d0; dd[1] = d1; dd[2] = d2; dd[3] = d3;
         }
       }
       dst0 += tot;
