@@ -1591,10 +1591,18 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, const u
 // position in the reference's op order, clamped box, branch-free strip-SAT
 // corners (masked corners re-read corner A and are multiplied by 0), exact
 // sum // area.
-// px, py, rad: pattern point j (held in registers by the caller: lane-varying
-// constant-memory reads would serialize).
-__device__ __forceinline__ uint32_t point_mean(const uint32_t* S, const Geo& g, double kx, double ky, double sg,
-                                               double cs, double sn, double px, double py, double rad, bool rotated)
+// Corner addresses of the box of one sample point (descriptor.py:94-115):
+// fp64 position in the reference's op order, clamped box, strip-SAT corners.
+struct BoxQ {
+  const uint32_t *r0, *r1, *r2;
+  int xa, xb, area;
+  uint32_t L, T, C;
+  bool slow;
+  int x0, x1, y0, y1;
+};
+
+__device__ __forceinline__ BoxQ box_query(const uint32_t* S, const Geo& g, double kx, double ky, double sg, double cs,
+                                         double sn, double px, double py, double rad, bool rotated)
 {
   double fx, fy;
   if (rotated) {
@@ -1608,29 +1616,50 @@ __device__ __forceinline__ uint32_t point_mean(const uint32_t* S, const Geo& g, 
   x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
   y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
   const int r = (int)floor(rad * sg + 0.5);
-  const int x0 = max((int)x - r, 0), x1 = min((int)x + r, g.W - 1);
-  const int y0 = max((int)y - r, 0), y1 = min((int)y + r, g.H - 1);
+  BoxQ q;
+  q.x0 = max((int)x - r, 0); q.x1 = min((int)x + r, g.W - 1);
+  q.y0 = max((int)y - r, 0); q.y1 = min((int)y + r, g.H - 1);
   const int TH = g.pth;
-  const int ys = (int)__umulhi((uint32_t)y0, g.pth_magic) * TH;
-  const int yb = min(y1, ys + TH - 1);
-  const uint32_t L = x0 > 0, T = y0 > ys, C = y1 > yb;
-  uint32_t sm;
-  if (y1 > ys + 2 * TH - 1) {
-    sm = box_sum(S, g, x0, x1, y0, y1);          // box over >= 3 strips (O > 4 only)
-  } else {
-    const uint32_t* r0 = S + (long long)yb * g.W;
-    const uint32_t* r1 = T ? S + (long long)(y0 - 1) * g.W : r0;
-    const uint32_t* r2 = C ? S + (long long)y1 * g.W : r0;
-    const int xa = L ? x0 - 1 : x1;
-    const uint32_t a0 = __ldca(r0 + x1), a1 = __ldca(r0 + xa), b0 = __ldca(r1 + x1), b1 = __ldca(r1 + xa);
-    const uint32_t c0 = __ldca(r2 + x1), c1 = __ldca(r2 + xa);
-    sm = a0 - L * a1 - T * (b0 - L * b1) + C * (c0 - L * c1);
-  }
-  const uint32_t a = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+  const int ys = (int)__umulhi((uint32_t)q.y0, g.pth_magic) * TH;
+  const int yb = min(q.y1, ys + TH - 1);
+  q.L = q.x0 > 0; q.T = q.y0 > ys; q.C = q.y1 > yb;
+  q.slow = q.y1 > ys + 2 * TH - 1;
+  q.r0 = S + (long long)yb * g.W;
+  q.r1 = q.T ? S + (long long)(q.y0 - 1) * g.W : q.r0;
+  q.r2 = q.C ? S + (long long)q.y1 * g.W : q.r0;
+  q.xa = q.L ? q.x0 - 1 : q.x1;
+  q.xb = q.x1;
+  q.area = (q.x1 - q.x0 + 1) * (q.y1 - q.y0 + 1);
+  return q;
+}
+
+// sum // area, exact (float quotient + one-step integer correction)
+__device__ __forceinline__ uint32_t exact_div(uint32_t sm, uint32_t a)
+{
   uint32_t q = (uint32_t)((float)sm * __frcp_rn((float)a));
   if (q * a > sm) q--;
   else if ((q + 1) * a <= sm) q++;
   return q;
+}
+
+// Box means of two sample points: both points' corners are computed first and
+// all 12 loads issued together (masked corners re-read corner A, times 0).
+__device__ __forceinline__ void point_means2(const uint32_t* S, const Geo& g, double kx, double ky, double sg,
+                                             double cs, double sn, const double* pa, const double* pb, bool rotated,
+                                             uint32_t& ma, uint32_t& mb)
+{
+  const BoxQ a = box_query(S, g, kx, ky, sg, cs, sn, pa[0], pa[1], pa[2], rotated);
+  const BoxQ c = box_query(S, g, kx, ky, sg, cs, sn, pb[0], pb[1], pb[2], rotated);
+  const uint32_t a0 = __ldca(a.r0 + a.xb), a1 = __ldca(a.r0 + a.xa), a2 = __ldca(a.r1 + a.xb), a3 = __ldca(a.r1 + a.xa);
+  const uint32_t a4 = __ldca(a.r2 + a.xb), a5 = __ldca(a.r2 + a.xa);
+  const uint32_t c0 = __ldca(c.r0 + c.xb), c1 = __ldca(c.r0 + c.xa), c2 = __ldca(c.r1 + c.xb), c3 = __ldca(c.r1 + c.xa);
+  const uint32_t c4 = __ldca(c.r2 + c.xb), c5 = __ldca(c.r2 + c.xa);
+  uint32_t sa = a0 - a.L * a1 - a.T * (a2 - a.L * a3) + a.C * (a4 - a.L * a5);
+  uint32_t sc = c0 - c.L * c1 - c.T * (c2 - c.L * c3) + c.C * (c4 - c.L * c5);
+  if (a.slow) sa = box_sum(S, g, a.x0, a.x1, a.y0, a.y1);   // box over >= 3 strips (O > 4 only)
+  if (c.slow) sc = box_sum(S, g, c.x0, c.x1, c.y0, c.y1);
+  ma = exact_div(sa, (uint32_t)a.area);
+  mb = exact_div(sc, (uint32_t)c.area);
 }
 
 // Flattened kept-keypoint index -> (stream, rank) via the per-stream prefix.
@@ -1647,16 +1676,20 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
 {
   __shared__ uint8_t vals[DSW][64];
   __shared__ uint32_t pairs[VF_NBITS];
+  __shared__ double ptab[64][3];   // pattern point x, y, smoothing radius
   __shared__ int sm_warp[32];
   extern __shared__ int pre[];   // [n_streams + 1]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
   stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
-  // this lane's two pattern points (lane, lane + 32)
+  for (int j = threadIdx.x; j < 64; j += 32 * DSW) {
+    const int jj = j < VF_NPTS ? j : 0;
+    ptab[j][0] = c_px[jj]; ptab[j][1] = c_py[jj]; ptab[j][2] = c_rad[jj];
+  }
+  __syncthreads();
+  // this lane's two pattern points (lane, lane + 32; lanes 28-31 repeat their first)
   const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
-  const double px0 = c_px[lane], py0 = c_py[lane], rd0 = c_rad[lane];
-  const double px1 = c_px[j1], py1 = c_py[j1], rd1 = c_rad[j1];
   for (int gi = blockIdx.x * DSW + wid; gi < total; gi += gridDim.x * DSW) {
     const int s = find_stream(pre, n_streams, gi), i = gi - pre[s];
     const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
@@ -1674,8 +1707,8 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
       kx = b.fx[o]; ky = b.fy[o]; sg = b.fs[o];
       sincos(b.ft[o], &sn, &cs);
     }
-    const uint32_t m0 = point_mean(S, g, kx, ky, sg, cs, sn, px0, py0, rd0, pass != 0);
-    const uint32_t m1 = point_mean(S, g, kx, ky, sg, cs, sn, px1, py1, rd1, pass != 0);
+    uint32_t m0, m1;
+    point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], pass != 0, m0, m1);
     uint8_t* v = vals[wid];
     v[lane] = (uint8_t)m0;
     if (lane + 32 < VF_NPTS) v[lane + 32] = (uint8_t)m1;
