@@ -1705,7 +1705,9 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
       }
     } else {
       kx = b.fx[o]; ky = b.fy[o]; sg = b.fs[o];
-      sincos(b.ft[o], &sn, &cs);
+      const double* park = reinterpret_cast<const double*>(b.fdesc + o * 64);   // from k_desc_orient
+      cs = park[0];
+      sn = park[1];
     }
     uint32_t m0, m1;
     point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], pass != 0, m0, m1);
@@ -1765,7 +1767,14 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
         gy += dv * c_wy[p];
       }
       double th = atan2(gy, gx);
-      b.ft[o] = th <= -CUDART_PI ? CUDART_PI : th;
+      th = th <= -CUDART_PI ? CUDART_PI : th;
+      b.ft[o] = th;
+      // park cos / sin for the rotated pass in the (consumed) descriptor slot
+      double sn, cs;
+      sincos(th, &sn, &cs);
+      double* park = reinterpret_cast<double*>(b.fdesc + o * 64);
+      park[0] = cs;
+      park[1] = sn;
     }
   }
 }
