@@ -114,6 +114,27 @@ int vf_get_features(vf_ctx *ctx, int s, vf_features *out, void *stream);
 /* Synchronizes `stream`; copies stream s's features to host arrays of >= cap entries. */
 int vf_copy_features(vf_ctx *ctx, int s, int32_t cap, double *x, double *y, double *sigma, double *theta,
                      double *score, uint8_t *origin, int32_t *age, uint8_t *desc, int32_t *n_out, void *stream);
+/* All streams [0, n_streams) at once: packs every stream's current features on
+ * the device into one contiguous SoA (stream s at [offsets[s], offsets[s+1])),
+ * then enqueues ONE device->host copy per field into the caller's (pinned)
+ * host arrays of >= cap entries.  Synchronizes `stream` once for the counts;
+ * the field copies are asynchronous on `stream` (synchronize before use). */
+int vf_fetch_features(vf_ctx *ctx, int n_streams, int64_t cap, double *x, double *y, double *sigma,
+                      double *theta, double *score, uint8_t *origin, int32_t *age, uint8_t *desc,
+                      int32_t *offsets, void *stream);
+/* Pipelined host-to-host processing (the e2e API): submit copies step n's
+ * host frames to the device on a copy stream, runs the path and packs the
+ * features on a compute stream; collect returns the oldest submitted step's
+ * features (all streams, packed as in vf_fetch_features) after its
+ * device->host copy on a second copy stream.  At most two steps may be in
+ * flight (submit, submit, collect, submit, collect, ...), so H2D of step n+1,
+ * compute of step n and D2H of step n-1 overlap.  Stream-ordered with respect
+ * to the context's own streams only; not to be mixed with vf_process on the
+ * same context. */
+int vf_pipeline_submit(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,
+                       int n_streams);
+int vf_pipeline_collect(vf_ctx *ctx, int64_t cap, double *x, double *y, double *sigma, double *theta,
+                        double *score, uint8_t *origin, int32_t *age, uint8_t *desc, int32_t *offsets);
 /* Device pointers of layer l of stream s's current pyramid (l >= 1; l = 0 is the input frame). */
 int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch);
 /* Live per-stage device timing with CUDA events on the launch stream:

@@ -78,6 +78,9 @@ def lib():
     L.vf_get_totals.argtypes = [c_void_p, c_int, _P, c_void_p]
     L.vf_set_timing.argtypes = [c_void_p, c_int]
     L.vf_get_diag.argtypes = [c_void_p, _P, c_void_p]
+    L.vf_fetch_features.argtypes = [c_void_p, c_int, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_void_p]
+    L.vf_pipeline_submit.argtypes = [c_void_p, _P, c_int64, c_int64, c_int]
+    L.vf_pipeline_collect.argtypes = [c_void_p, c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P]
     L.vf_get_stage_ms.argtypes = [c_void_p, _P, POINTER(c_int32), c_void_p]
     L.vf_build_pyramid.argtypes = [_P, c_int, c_int, c_int64, c_int, _P, _P, c_void_p]
     L.vf_score_map.argtypes = [_P, c_int, c_int, c_int64, c_int, _P, c_int, c_int, _P, c_int64, c_void_p]
@@ -89,9 +92,11 @@ def lib():
     L.vf_mask_values.argtypes = [_P, c_int, c_int, c_int, _P, _P, _P, c_void_p]
     for name in ("vf_set_pattern", "vf_create", "vf_destroy", "vf_layer_geometry", "vf_reset", "vf_process",
                  "vf_process_host", "vf_get_report", "vf_get_features", "vf_copy_features", "vf_get_layer",
-                 "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe",
+                 "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
+    "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe",
                  "vf_intensity_mask", "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
-                 "vf_set_timing", "vf_get_stage_ms", "vf_get_diag"):
+                 "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
+                 "vf_pipeline_collect"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -101,7 +106,8 @@ def lib():
 EXPORTS = (
     "vf_version", "vf_strerror", "vf_set_pattern", "vf_create", "vf_destroy", "vf_layer_geometry", "vf_reset",
     "vf_process", "vf_process_host", "vf_get_report", "vf_get_features", "vf_copy_features", "vf_get_layer",
-    "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe", "vf_intensity_mask",
+    "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
+    "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe", "vf_intensity_mask",
     "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
 )
 

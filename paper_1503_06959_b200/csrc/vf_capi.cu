@@ -190,11 +190,47 @@ struct vf_ctx {
   long long hstage_bytes = 0;
   int hstage_k = 0;
   cudaEvent_t hstage_free[2] = {nullptr, nullptr};
+  // packed feature output (vf_fetch_features): device SoA + host-visible prefix
+  struct Pack {
+    double *x = nullptr, *y, *s, *t, *v;
+    uint8_t *o, *d;
+    int* a;
+    int* pre = nullptr;        // device [S + 1]
+    int* pre_host = nullptr;   // pinned [S + 1]
+    long long cap = 0;
+  } pack;
+  // pipelined host API (vf_pipeline_submit / vf_pipeline_collect)
+  struct Pipe {
+    bool init = false;
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    uint8_t* frames[2] = {nullptr, nullptr};
+    long long frame_bytes = 0;
+    double *x[2], *y[2], *s[2], *t[2], *v[2];
+    uint8_t *o[2], *d[2];
+    int* a[2];
+    int* pre[2];
+    int* pre_host[2];
+    long long cap = 0;
+    cudaEvent_t ev_h2d[2], ev_comp[2], ev_pre[2], ev_d2h[2];
+    long long submitted = 0, collected = 0;
+    int n_streams[2];
+  } pipe;
   // live per-stage timing (vf_set_timing): one event before each stage + end
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool, ev_used;
   std::vector<int> ev_stage;   // stage index of each recorded interval start
 };
+
+static void pack_free(vf_ctx* c)
+{
+  auto& P = c->pack;
+  for (void* p : {(void*)P.x, (void*)P.y, (void*)P.s, (void*)P.t, (void*)P.v, (void*)P.o, (void*)P.d, (void*)P.a})
+    if (p) cudaFree(p);
+  P.x = P.y = P.s = P.t = P.v = nullptr;
+  P.o = P.d = nullptr;
+  P.a = nullptr;
+  P.cap = 0;
+}
 
 #define VF_NSTAGES 9   // binmask, pyramid, worklist, fast, nms, sat, describe, propagate, finalize
 static void stage_mark(vf_ctx* c, int stage, cudaStream_t st)
@@ -362,6 +398,8 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   return VF_OK;
 }
 
+static void pipe_free(vf_ctx* c);
+
 int vf_destroy(vf_ctx* c)
 {
   if (!c) return VF_OK;
@@ -369,6 +407,10 @@ int vf_destroy(vf_ctx* c)
     if (c->hstage[k]) cudaFree(c->hstage[k]);
     if (c->hstage_free[k]) cudaEventDestroy(c->hstage_free[k]);
   }
+  pipe_free(c);
+  pack_free(c);
+  if (c->pack.pre) cudaFree(c->pack.pre);
+  if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : c->ev_used) cudaEventDestroy(ev);
   c->mem.release();
@@ -577,6 +619,179 @@ int vf_copy_features(vf_ctx* c, int s, int32_t cap, double* x, double* y, double
   if (age) cudaMemcpyAsync(age, f.age, 4 * n, cudaMemcpyDeviceToHost, st);
   if (desc) cudaMemcpyAsync(desc, f.desc, 64 * n, cudaMemcpyDeviceToHost, st);
   return cuda_status(cudaStreamSynchronize(st));
+}
+
+int vf_fetch_features(vf_ctx* c, int n_streams, int64_t cap, double* x, double* y, double* sigma, double* theta,
+                      double* score, uint8_t* origin, int32_t* age, uint8_t* desc, int32_t* offsets, void* stream)
+{
+  if (!c || n_streams < 1 || n_streams > c->S || !offsets) return VF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto& P = c->pack;
+  if (!P.pre) {
+    if (cudaMalloc(&P.pre, sizeof(int) * (c->S + 1)) != cudaSuccess) return VF_ERR_CUDA;
+    if (cudaMallocHost(&P.pre_host, sizeof(int) * (c->S + 1)) != cudaSuccess) return VF_ERR_CUDA;
+  }
+  // size the pack buffers from the current counts (grow only)
+  std::vector<int> ctr((size_t)c->S * C_NCTR);
+  cudaMemcpyAsync(ctr.data(), c->b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  long long need = 0;
+  for (int s = 0; s < n_streams; s++) {
+    const int* cs = &ctr[(size_t)s * C_NCTR];
+    if (cs[C_FRAME] > 0) need += cs[C_NFEAT0 + ((cs[C_FRAME] - 1) & 1)];
+  }
+  if (need > P.cap) {
+    pack_free(c);
+    const long long nc = std::max(need + need / 4, 65536LL);
+    bool ok = cudaMalloc(&P.x, 8 * nc) == cudaSuccess && cudaMalloc(&P.y, 8 * nc) == cudaSuccess &&
+              cudaMalloc(&P.s, 8 * nc) == cudaSuccess && cudaMalloc(&P.t, 8 * nc) == cudaSuccess &&
+              cudaMalloc(&P.v, 8 * nc) == cudaSuccess && cudaMalloc(&P.o, nc) == cudaSuccess &&
+              cudaMalloc(&P.a, 4 * nc) == cudaSuccess && cudaMalloc(&P.d, 64 * nc) == cudaSuccess;
+    if (!ok) { pack_free(c); return VF_ERR_CUDA; }
+    P.cap = nc;
+  }
+  k_pack<<<std::max(1, std::min(cdiv(need, 256), g_num_sms * 8)), 256, (n_streams + 1) * sizeof(int), st>>>(
+      c->g, c->b, n_streams, -1, P.x, P.y, P.s, P.t, P.v, P.o, P.a, P.d, P.pre, P.cap);
+  cudaMemcpyAsync(P.pre_host, P.pre, sizeof(int) * (n_streams + 1), cudaMemcpyDeviceToHost, st);
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  const long long n = P.pre_host[n_streams];
+  for (int s = 0; s <= n_streams; s++) offsets[s] = P.pre_host[s];
+  if (n > cap) return VF_ERR_CAPACITY;
+  if (n == 0) return VF_OK;
+  if (x) cudaMemcpyAsync(x, P.x, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (y) cudaMemcpyAsync(y, P.y, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (sigma) cudaMemcpyAsync(sigma, P.s, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (theta) cudaMemcpyAsync(theta, P.t, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (score) cudaMemcpyAsync(score, P.v, 8 * n, cudaMemcpyDeviceToHost, st);
+  if (origin) cudaMemcpyAsync(origin, P.o, n, cudaMemcpyDeviceToHost, st);
+  if (age) cudaMemcpyAsync(age, P.a, 4 * n, cudaMemcpyDeviceToHost, st);
+  if (desc) cudaMemcpyAsync(desc, P.d, 64 * n, cudaMemcpyDeviceToHost, st);
+  return cuda_status(cudaGetLastError());
+}
+
+static int pipe_init(vf_ctx* c)
+{
+  auto& P = c->pipe;
+  if (P.init) return VF_OK;
+  const long long fb = (long long)c->g.W * c->g.H * c->S;
+  P.frame_bytes = fb;
+  P.cap = (long long)c->S * c->g.kp_cap;
+  bool ok = true;
+  ok = ok && cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking) == cudaSuccess;
+  for (int k = 0; k < 2 && ok; k++) {
+    ok = ok && cudaMalloc(&P.frames[k], fb) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.x[k], 8 * P.cap) == cudaSuccess && cudaMalloc(&P.y[k], 8 * P.cap) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.s[k], 8 * P.cap) == cudaSuccess && cudaMalloc(&P.t[k], 8 * P.cap) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.v[k], 8 * P.cap) == cudaSuccess && cudaMalloc(&P.o[k], P.cap) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.a[k], 4 * P.cap) == cudaSuccess && cudaMalloc(&P.d[k], 64 * P.cap) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.pre[k], sizeof(int) * (c->S + 1)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&P.pre_host[k], sizeof(int) * (c->S + 1)) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&P.ev_h2d[k], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&P.ev_comp[k], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&P.ev_pre[k], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&P.ev_d2h[k], cudaEventDisableTiming) == cudaSuccess;
+  }
+  if (!ok) return VF_ERR_CUDA;
+  P.init = true;
+  return VF_OK;
+}
+
+static void pipe_free(vf_ctx* c)
+{
+  auto& P = c->pipe;
+  if (!P.init) return;
+  cudaStreamSynchronize(P.h2d); cudaStreamSynchronize(P.comp); cudaStreamSynchronize(P.d2h);
+  for (int k = 0; k < 2; k++) {
+    for (void* p : {(void*)P.frames[k], (void*)P.x[k], (void*)P.y[k], (void*)P.s[k], (void*)P.t[k], (void*)P.v[k],
+                    (void*)P.o[k], (void*)P.a[k], (void*)P.d[k], (void*)P.pre[k]})
+      cudaFree(p);
+    cudaFreeHost(P.pre_host[k]);
+    cudaEventDestroy(P.ev_h2d[k]); cudaEventDestroy(P.ev_comp[k]); cudaEventDestroy(P.ev_pre[k]);
+    cudaEventDestroy(P.ev_d2h[k]);
+  }
+  cudaStreamDestroy(P.h2d); cudaStreamDestroy(P.comp); cudaStreamDestroy(P.d2h);
+  P.init = false;
+}
+
+int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch, int n_streams)
+{
+  if (!c || !frames_host || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
+  if (!g_pattern_ok) return VF_ERR_PATTERN;
+  int rc = pipe_init(c);
+  if (rc) return rc;
+  auto& P = c->pipe;
+  if (P.submitted - P.collected >= 2) return VF_ERR_ARG;   // collect the oldest step first
+  const int k = (int)(P.submitted & 1);
+  const long long fbytes = (long long)c->g.W * c->g.H;
+  // frames -> device (buffer k was last read by compute of step submitted-2: ev_comp[k])
+  cudaStreamWaitEvent(P.h2d, P.ev_comp[k], 0);
+  cudaError_t e = cudaSuccess;
+  if (row_pitch == c->g.W && stream_stride == fbytes)
+    e = cudaMemcpyAsync(P.frames[k], frames_host, fbytes * n_streams, cudaMemcpyHostToDevice, P.h2d);
+  else
+    for (int s = 0; s < n_streams && e == cudaSuccess; s++)
+      e = cudaMemcpy2DAsync(P.frames[k] + s * fbytes, c->g.W, frames_host + s * stream_stride, row_pitch, c->g.W,
+                            c->g.H, cudaMemcpyHostToDevice, P.h2d);
+  if (e != cudaSuccess) return cuda_status(e);
+  cudaEventRecord(P.ev_h2d[k], P.h2d);
+  // the whole path, then pack (pack buffer k was last read by the d2h of step submitted-2)
+  cudaStreamWaitEvent(P.comp, P.ev_h2d[k], 0);
+  c->b.frames = P.frames[k];
+  c->b.frame_stride = fbytes;
+  c->b.frame_pitch = c->g.W;
+  rc = launch_step(c, n_streams, P.comp);
+  if (rc) return rc;
+  cudaStreamWaitEvent(P.comp, P.ev_d2h[k], 0);
+  k_pack<<<g_num_sms * 8, 256, (n_streams + 1) * sizeof(int), P.comp>>>(
+      c->g, c->b, n_streams, -1, P.x[k], P.y[k], P.s[k], P.t[k], P.v[k], P.o[k], P.a[k], P.d[k], P.pre[k], P.cap);
+  cudaMemcpyAsync(P.pre_host[k], P.pre[k], sizeof(int) * (n_streams + 1), cudaMemcpyDeviceToHost, P.comp);
+  cudaEventRecord(P.ev_pre[k], P.comp);
+  cudaEventRecord(P.ev_comp[k], P.comp);
+  P.n_streams[k] = n_streams;
+  P.submitted++;
+  return cuda_status(cudaGetLastError());
+}
+
+int vf_pipeline_collect(vf_ctx* c, int64_t cap, double* x, double* y, double* sigma, double* theta, double* score,
+                        uint8_t* origin, int32_t* age, uint8_t* desc, int32_t* offsets)
+{
+  if (!c || !offsets) return VF_ERR_ARG;
+  auto& P = c->pipe;
+  if (!P.init || P.collected >= P.submitted) return VF_ERR_ARG;
+  const int k = (int)(P.collected & 1);
+  cudaError_t e = cudaEventSynchronize(P.ev_pre[k]);
+  if (e != cudaSuccess) return cuda_status(e);
+  const int ns = P.n_streams[k];
+  const long long n = std::min((long long)P.pre_host[k][ns], P.cap);
+  for (int s = 0; s <= ns; s++) offsets[s] = P.pre_host[k][s];
+  if (n > cap) return VF_ERR_CAPACITY;
+  cudaStreamWaitEvent(P.d2h, P.ev_comp[k], 0);
+  if (n > 0) {
+    if (x) cudaMemcpyAsync(x, P.x[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (y) cudaMemcpyAsync(y, P.y[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (sigma) cudaMemcpyAsync(sigma, P.s[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (theta) cudaMemcpyAsync(theta, P.t[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (score) cudaMemcpyAsync(score, P.v[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (origin) cudaMemcpyAsync(origin, P.o[k], n, cudaMemcpyDeviceToHost, P.d2h);
+    if (age) cudaMemcpyAsync(age, P.a[k], 4 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (desc) cudaMemcpyAsync(desc, P.d[k], 64 * n, cudaMemcpyDeviceToHost, P.d2h);
+  }
+  cudaEventRecord(P.ev_d2h[k], P.d2h);
+  e = cudaEventSynchronize(P.ev_d2h[k]);
+  if (e != cudaSuccess) return cuda_status(e);
+  P.collected++;
+  // sticky capacity flags: checked every 64 steps (one small copy)
+  if ((P.collected & 63) == 1) {
+    std::vector<int> ctr((size_t)ns * C_NCTR);
+    cudaMemcpy(ctr.data(), c->b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost);
+    for (int s = 0; s < ns; s++)
+      if (ctr[(size_t)s * C_NCTR + C_ERR]) return VF_ERR_CAPACITY;
+  }
+  return VF_OK;
 }
 
 int vf_get_diag(vf_ctx* c, int64_t* out8, void* stream)

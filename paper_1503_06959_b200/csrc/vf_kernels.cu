@@ -1832,6 +1832,41 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ Geo g
 }
 
 // ============================================================================
+// k_pack: features of streams [0, n) into one contiguous SoA (for a single
+// device->host copy per field); pre[s] = first index of stream s.
+// ============================================================================
+__global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
+                                              int n_streams, int buf_override, double* px, double* py, double* ps,
+                                              double* pt, double* pv, uint8_t* po, int* pa, uint8_t* pd,
+                                              int* pre_out, long long pack_cap)
+{
+  __shared__ int sm_warp[32];
+  extern __shared__ int pre[];
+  stream_prefix(n_streams, pre, sm_warp, [&](int s) {
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int buf = buf_override >= 0 ? buf_override : ((ctr[C_FRAME] - 1) & 1);   // last finished frame
+    return ctr[C_NFEAT0 + buf];
+  });
+  if (blockIdx.x == 0)
+    for (int s = threadIdx.x; s <= n_streams; s += blockDim.x) pre_out[s] = pre[s];
+  const int total = pre[n_streams];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total && i < pack_cap;
+       i += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = n_streams;
+    while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= i) lo = m; else hi = m; }
+    const int s = lo, k = (int)(i - pre[s]);
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int buf = buf_override >= 0 ? buf_override : ((ctr[C_FRAME] - 1) & 1);
+    const long long f = ((long long)s * 2 + buf) * g.kp_cap + k;
+    px[i] = b.fx[f]; py[i] = b.fy[f]; ps[i] = b.fs[f]; pt[i] = b.ft[f]; pv[i] = b.fv[f];
+    po[i] = b.forg[f]; pa[i] = b.fage[f];
+    const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + f * 64);
+    uint4* dd = reinterpret_cast<uint4*>(pd + i * 64);
+    dd[0] = sd[0]; dd[1] = sd[1]; dd[2] = sd[2]; dd[3] = sd[3];
+  }
+}
+
+// ============================================================================
 // k_finalize: state carried to the next frame (pipeline.py:276-277)
 // ============================================================================
 __global__ void k_finalize(const __grid_constant__ Geo g, const __grid_constant__ Bufs b, int n_streams)

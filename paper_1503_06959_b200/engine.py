@@ -139,6 +139,52 @@ class FeatureEngine:
         out["n"] = n
         return out
 
+    def fetch_all(self, out: dict | None = None, stream=None) -> dict:
+        """Every stream's current features in one packed SoA (host arrays; pinned if `out` was
+        made by alloc_host).  out["offsets"][s] .. [s+1] is stream s.  Synchronize before use."""
+        if out is None:
+            out = self.alloc_host(self.n_streams * 65536)
+        n = ctypes.c_int64(len(out["x"]))
+        _native.check(_native.lib().vf_fetch_features(
+            self._h, self.n_streams, n, out["x"].ctypes.data, out["y"].ctypes.data, out["sigma"].ctypes.data,
+            out["theta"].ctypes.data, out["score"].ctypes.data, out["origin"].ctypes.data, out["age"].ctypes.data,
+            out["desc"].ctypes.data, out["offsets"].ctypes.data, _native.stream_handle(stream)), "vf_fetch_features")
+        return out
+
+    def submit(self, frames: np.ndarray) -> None:
+        """Pipelined e2e API: enqueue host frames [S, H, W] (pinned for overlap) for one step."""
+        a = np.ascontiguousarray(frames)
+        if a.ndim == 2:
+            a = a[None]
+        S, H, W = a.shape
+        self._keep = getattr(self, "_keep", [])[-1:] + [a]   # host memory must live until its copy ran
+        _native.check(_native.lib().vf_pipeline_submit(self._h, a.ctypes.data, H * W, W, S), "vf_pipeline_submit")
+
+    def collect(self, out: dict) -> dict:
+        """Features of the oldest submitted step (packed SoA, see fetch_all); blocks until copied."""
+        n = ctypes.c_int64(len(out["x"]))
+        _native.check(_native.lib().vf_pipeline_collect(
+            self._h, n, out["x"].ctypes.data, out["y"].ctypes.data, out["sigma"].ctypes.data, out["theta"].ctypes.data,
+            out["score"].ctypes.data, out["origin"].ctypes.data, out["age"].ctypes.data, out["desc"].ctypes.data,
+            out["offsets"].ctypes.data), "vf_pipeline_collect")
+        return out
+
+    @staticmethod
+    def alloc_host(cap: int, pinned: bool = True) -> dict:
+        """Host SoA buffers for fetch_all (torch pinned memory viewed as numpy)."""
+        import torch
+
+        def arr(shape, dt):
+            t = torch.empty(shape, dtype=dt, pin_memory=pinned)
+            return t.numpy()
+
+        out = {k: arr(cap, torch.float64) for k in ("x", "y", "sigma", "theta", "score")}
+        out["origin"] = arr(cap, torch.uint8)
+        out["age"] = arr(cap, torch.int32)
+        out["desc"] = arr((cap, 64), torch.uint8)
+        out["offsets"] = np.zeros(4096 + 1, np.int32)
+        return out
+
     STAGES = ("binmask", "pyramid", "worklist", "fast", "nms", "sat", "describe", "propagate", "finalize")
 
     def set_timing(self, enable: bool) -> None:
