@@ -210,6 +210,7 @@ struct vf_ctx {
     int* a[2];
     int* pre[2];
     int* pre_host[2];
+    int* ctr_host[2];          // pinned copy of the counters after each step
     long long cap = 0;
     cudaEvent_t ev_h2d[2], ev_comp[2], ev_pre[2], ev_d2h[2];
     long long submitted = 0, collected = 0;
@@ -690,6 +691,7 @@ static int pipe_init(vf_ctx* c)
     ok = ok && cudaMalloc(&P.a[k], 4 * P.cap) == cudaSuccess && cudaMalloc(&P.d[k], 64 * P.cap) == cudaSuccess;
     ok = ok && cudaMalloc(&P.pre[k], sizeof(int) * (c->S + 1)) == cudaSuccess;
     ok = ok && cudaMallocHost(&P.pre_host[k], sizeof(int) * (c->S + 1)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&P.ctr_host[k], sizeof(int) * c->S * C_NCTR) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&P.ev_h2d[k], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&P.ev_comp[k], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&P.ev_pre[k], cudaEventDisableTiming) == cudaSuccess;
@@ -710,6 +712,7 @@ static void pipe_free(vf_ctx* c)
                     (void*)P.o[k], (void*)P.a[k], (void*)P.d[k], (void*)P.pre[k]})
       cudaFree(p);
     cudaFreeHost(P.pre_host[k]);
+    cudaFreeHost(P.ctr_host[k]);
     cudaEventDestroy(P.ev_h2d[k]); cudaEventDestroy(P.ev_comp[k]); cudaEventDestroy(P.ev_pre[k]);
     cudaEventDestroy(P.ev_d2h[k]);
   }
@@ -749,6 +752,7 @@ int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_str
   k_pack<<<g_num_sms * 8, 256, (n_streams + 1) * sizeof(int), P.comp>>>(
       c->g, c->b, n_streams, -1, P.x[k], P.y[k], P.s[k], P.t[k], P.v[k], P.o[k], P.a[k], P.d[k], P.pre[k], P.cap);
   cudaMemcpyAsync(P.pre_host[k], P.pre[k], sizeof(int) * (n_streams + 1), cudaMemcpyDeviceToHost, P.comp);
+  cudaMemcpyAsync(P.ctr_host[k], c->b.ctr, sizeof(int) * n_streams * C_NCTR, cudaMemcpyDeviceToHost, P.comp);
   cudaEventRecord(P.ev_pre[k], P.comp);
   cudaEventRecord(P.ev_comp[k], P.comp);
   P.n_streams[k] = n_streams;
@@ -784,13 +788,8 @@ int vf_pipeline_collect(vf_ctx* c, int64_t cap, double* x, double* y, double* si
   e = cudaEventSynchronize(P.ev_d2h[k]);
   if (e != cudaSuccess) return cuda_status(e);
   P.collected++;
-  // sticky capacity flags: checked every 64 steps (one small copy)
-  if ((P.collected & 63) == 1) {
-    std::vector<int> ctr((size_t)ns * C_NCTR);
-    cudaMemcpy(ctr.data(), c->b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost);
-    for (int s = 0; s < ns; s++)
-      if (ctr[(size_t)s * C_NCTR + C_ERR]) return VF_ERR_CAPACITY;
-  }
+  for (int s = 0; s < ns; s++)   // sticky device capacity flags of this step
+    if (P.ctr_host[k][(size_t)s * C_NCTR + C_ERR]) return VF_ERR_CAPACITY;
   return VF_OK;
 }
 

@@ -261,3 +261,43 @@ def test_run_streams_equals_per_stream():
                 assert o["n"] == e.n_total, (mode, s, n)
                 assert np.array_equal(o["x"], e.x) and np.array_equal(o["desc"], e.desc), (mode, s, n)
                 assert reps[s][n].coverage == e.coverage
+
+
+def test_packed_and_pipelined_outputs_match_per_stream():
+    """vf_fetch_features (packed, all streams) and the pipelined submit/collect
+    e2e API return exactly the per-stream feature lists."""
+    import torch
+
+    from paper_1503_06959_b200 import scenes
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    cfg = scenes.SceneConfig(640, 480, 5, 3, "mixed", (3, 6), (0.0, 4.0), (0.5, 2.0), noise_sigma=2.0,
+                             block_contrast=120.0, seed=91)
+    frames = scenes.generate(cfg).numpy()  # [S, N, H, W]
+    S, N = frames.shape[:2]
+    pcfg = PipelineConfig(mask=MaskConfig(mode="intensity"))
+    ref = FeatureEngine(640, 480, pcfg, n_streams=S)
+    pipe = FeatureEngine(640, 480, pcfg, n_streams=S)
+    out_fetch = ref.alloc_host(S * 20000, pinned=False)
+    out_pipe = pipe.alloc_host(S * 20000)
+    dev = torch.from_numpy(np.ascontiguousarray(frames.transpose(1, 0, 2, 3))).cuda()
+    host = [np.ascontiguousarray(frames[:, n]) for n in range(N)]
+    pipe.submit(host[0])
+    for n in range(N):
+        ref.process(dev[n])
+        per = [ref.features_host(s) for s in range(S)]
+        ref.fetch_all(out_fetch)
+        torch.cuda.synchronize()
+        if n + 1 < N:
+            pipe.submit(host[n + 1])
+        pipe.collect(out_pipe)
+        for out in (out_fetch, out_pipe):
+            offs = out["offsets"]
+            for s in range(S):
+                a, b = int(offs[s]), int(offs[s + 1])
+                assert b - a == per[s]["n"], (n, s)
+                for k in ("x", "y", "sigma", "theta", "score", "origin", "age", "desc"):
+                    assert np.array_equal(out[k][a:b], per[s][k]), (n, s, k)
+    ref.close()
+    pipe.close()
