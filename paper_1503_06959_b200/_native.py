@@ -57,8 +57,12 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
+    import os
+
     path = _build.LIB
-    if _build.needs_build():
+    if os.environ.get("VF_LIB"):          # experiment builds
+        path = os.environ["VF_LIB"]
+    elif _build.needs_build():
         path = _build.build()
     L = ctypes.CDLL(str(path))
     L.vf_version.restype = ctypes.c_char_p

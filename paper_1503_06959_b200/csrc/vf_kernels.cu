@@ -1094,13 +1094,19 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
 // reads 0 unless its tile was stamped active this step (um == 0: all active).
 __device__ __forceinline__ int score_read(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x)
 {
+  // branch-free (um is warp-uniform): the score and the tile stamp are loaded
+  // unconditionally from a clamped in-bounds address and then selected, so a
+  // caller's reads can all be in flight at once
   const LayerGeo& Lg = g.L[l];
-  if (y < 0 || y >= Lg.h || x < 0 || x >= Lg.w) return 0;
+  const bool in = (unsigned)y < (unsigned)Lg.h && (unsigned)x < (unsigned)Lg.w;
+  const int yc = in ? y : 0, xc = in ? x : 0;
+  const int v = __ldg(b.scores + (long long)s * g.sm_slab + Lg.sm_off + (long long)yc * Lg.pitch + xc);
+  bool ok = in;
   if (um) {
-    const int tile = Lg.tile_base + (y / VF_TILE_H) * Lg.tiles_x + x / VF_TILE_W;
-    if (__ldg(b.tile_stamp + (long long)s * g.tiles_per_stream + tile) != um) return 0;
+    const int tile = Lg.tile_base + (yc / VF_TILE_H) * Lg.tiles_x + xc / VF_TILE_W;
+    ok = ok && __ldg(b.tile_stamp + (long long)s * g.tiles_per_stream + tile) == um;
   }
-  return b.scores[(long long)s * g.sm_slab + Lg.sm_off + (long long)y * Lg.pitch + x];
+  return ok ? v : 0;
 }
 
 __device__ __forceinline__ void fit_peak(const double p[3][3], double& ox, double& oy, double& val, int& okp)
@@ -1123,17 +1129,22 @@ __device__ __forceinline__ void fit_peak(const double p[3][3], double& ox, doubl
   ox = x; oy = y; okp = ok;
 }
 
-__device__ __forceinline__ int patch_read(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x, double p[3][3])
+__device__ __forceinline__ void patch_load(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x, int v[9])
 {
-  int mx = INT_MIN;
 #pragma unroll
   for (int dy = -1; dy <= 1; dy++)
 #pragma unroll
-    for (int dx = -1; dx <= 1; dx++) {
-      int v = score_read(g, b, s, um, l, y + dy, x + dx);
-      p[dy + 1][dx + 1] = (double)v;
-      mx = v > mx ? v : mx;
-    }
+    for (int dx = -1; dx <= 1; dx++) v[(dy + 1) * 3 + dx + 1] = score_read(g, b, s, um, l, y + dy, x + dx);
+}
+
+__device__ __forceinline__ int patch_to_double(const int v[9], double p[3][3])
+{
+  int mx = INT_MIN;
+#pragma unroll
+  for (int i = 0; i < 9; i++) {
+    p[i / 3][i % 3] = (double)v[i];
+    mx = v[i] > mx ? v[i] : mx;
+  }
   return mx;
 }
 
@@ -1143,47 +1154,58 @@ __device__ NmsOut nms_one(const Geo& g, const Bufs& b, int s, int um, int l, int
 {
   NmsOut o; o.flags = 0; o.x = o.y = o.sig = o.v = 0.0;
   const LayerGeo& Lg = g.L[l];
+  // batch 1: centre, 8 neighbours, projected pixels of layers l-1, l+1
   const int sv = score_read(g, b, s, um, l, y, x);
-  if (sv == 0) return o;
-  bool keep = true;
+  int nb[8];
 #pragma unroll
-  for (int dy = -1; dy <= 1; dy++)
-#pragma unroll
-    for (int dx = -1; dx <= 1; dx++)
-      if (dx || dy) {
-        int yy = y + dy, xx = x + dx;
-        if (g.nms_wrap) {                                // smap[ys+dy, xs+dx] (detector.py:260-262)
-          yy = yy < 0 ? yy + Lg.h : yy;
-          xx = xx < 0 ? xx + Lg.w : xx;
-        }
-        keep &= sv > score_read(g, b, s, um, l, yy, xx);
-      }
-  int yj[2], xj[2];
+  for (int i = 0; i < 8; i++) {
+    const int dy = i < 3 ? -1 : (i < 5 ? 0 : 1);
+    const int dx = i < 3 ? i - 1 : (i == 3 ? -1 : (i == 4 ? 1 : i - 6));
+    int yy = y + dy, xx = x + dx;
+    if (g.nms_wrap) {                                    // smap[ys+dy, xs+dx] (detector.py:260-262)
+      yy = yy < 0 ? yy + Lg.h : yy;
+      xx = xx < 0 ? xx + Lg.w : xx;
+    }
+    nb[i] = score_read(g, b, s, um, l, yy, xx);
+  }
+  int yj[2] = {0, 0}, xj[2] = {0, 0}, cj[2] = {0, 0};
+  const bool has[2] = {l >= 1, l + 1 < g.NL};
 #pragma unroll
   for (int k = 0; k < 2; k++) {                          // detector.py:264-273
+    if (!has[k]) continue;
     const int j = l - 1 + 2 * k;
-    if (j < 0 || j >= g.NL) continue;
     const int hj = g.L[j].h, wj = g.L[j].w;
-    long long a = ((long long)y * hj + (Lg.h >> 1)) / Lg.h;
-    long long c = ((long long)x * wj + (Lg.w >> 1)) / Lg.w;
+    const long long a = ((long long)y * hj + (Lg.h >> 1)) / Lg.h;
+    const long long c = ((long long)x * wj + (Lg.w >> 1)) / Lg.w;
     yj[k] = (int)(a < hj - 1 ? a : hj - 1);
     xj[k] = (int)(c < wj - 1 ? c : wj - 1);
-    keep &= sv > score_read(g, b, s, um, j, yj[k], xj[k]);
+    cj[k] = score_read(g, b, s, um, j, yj[k], xj[k]);
   }
+  bool keep = sv > 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) keep &= sv > nb[i];
+#pragma unroll
+  for (int k = 0; k < 2; k++) keep &= !has[k] || sv > cj[k];
   if (!keep) return o;
   o.flags = 1;
+  // batch 2: the three 3x3 patches (zero-padded maps, detector.py:231-236)
+  int pv[3][9];
+  patch_load(g, b, s, um, l, y, x, pv[0]);
+#pragma unroll
+  for (int k = 0; k < 2; k++)
+    if (has[0] && has[1]) patch_load(g, b, s, um, l - 1 + 2 * k, yj[k], xj[k], pv[1 + k]);
   double p[3][3], ox, oy, v0;
   int ok;
-  patch_read(g, b, s, um, l, y, x, p);
+  patch_to_double(pv[0], p);
   fit_peak(p, ox, oy, v0, ok);
   double nv[2] = {0.0, 0.0};
+  const bool both = has[0] && has[1];                    // neighbour values only feed the scale fit
 #pragma unroll
   for (int k = 0; k < 2; k++) {                          // detector.py:281-285
-    const int j = l - 1 + 2 * k;
-    if (j < 0 || j >= g.NL) continue;
+    if (!both) continue;
     double pj[3][3], tx, ty, vj;
     int okj;
-    int pmax = patch_read(g, b, s, um, j, yj[k], xj[k], pj);
+    const int pmax = patch_to_double(pv[1 + k], pj);
     fit_peak(pj, tx, ty, vj, okj);
     nv[k] = okj ? vj : (double)pmax;
   }
@@ -1199,8 +1221,16 @@ __device__ NmsOut nms_one(const Geo& g, const Bufs& b, int s, int um, int l, int
     const double c = -delta > 0.0 ? -delta : 0.0;
     sig = Lg.sigma * pow(up, a) * pow(down, c);
   }
-  double xf = ((double)x + ox) / Lg.scale;               // detector.py:299-302
-  double yf = ((double)y + oy) / Lg.scale;
+  // detector.py:299-302; dividing by an octave scale 2^-o is exactly x * 2^o
+  double xf, yf;
+  if ((l & 1) == 0) {
+    const double inv = (double)(1 << (l >> 1));
+    xf = ((double)x + ox) * inv;
+    yf = ((double)y + oy) * inv;
+  } else {
+    xf = ((double)x + ox) / Lg.scale;
+    yf = ((double)y + oy) / Lg.scale;
+  }
   const double xhi = (double)g.W - 1e-6, yhi = (double)g.H - 1e-6;
   xf = xf < 0.0 ? 0.0 : (xf > xhi ? xhi : xf);
   yf = yf < 0.0 ? 0.0 : (yf > yhi ? yhi : yf);
@@ -1310,7 +1340,7 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
 // (layer, y): the reference order.
 #define NMS_WARPS 4
 #define NMS_THREADS (32 * NMS_WARPS)
-__global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+__global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int cand[NMS_WARPS][32];
   const int s = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
