@@ -220,6 +220,13 @@ struct vf_ctx {
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool, ev_used;
   std::vector<int> ev_stage;   // stage index of each recorded interval start
+  std::vector<int> ev_group;   // stream group of each mark
+  int cur_group = 0;
+  // stream groups: independent stream ranges launched on their own CUDA streams
+  int n_groups_max = 0;
+  std::vector<cudaStream_t> gstreams;
+  std::vector<cudaEvent_t> gjoin;
+  cudaEvent_t gfork = nullptr;
 };
 
 static void pack_free(vf_ctx* c)
@@ -243,6 +250,7 @@ static void stage_mark(vf_ctx* c, int stage, cudaStream_t st)
   cudaEventRecord(e, st);
   c->ev_used.push_back(e);
   c->ev_stage.push_back(stage);
+  c->ev_group.push_back(c->cur_group);
 }
 
 extern "C" {
@@ -348,9 +356,6 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.sat_stamp = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_work = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_count = A.get<int>((size_t)S);
-  b.sat_done = A.get<int>((size_t)S);
-  b.desc_done = A.get<int>((size_t)S);
-  b.q_ctr = A.get<int>(1);
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -363,12 +368,9 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.cov = A.get<unsigned long long>((size_t)S);
   b.report = A.get<double>((size_t)S * 16);
   b.worklist = A.get<int>((size_t)S * g.tiles_per_stream);
-  b.work_count = A.get<int>(1);
-  b.epoch = A.get<int>(1);
+  b.work_count = A.get<int>((size_t)S);
   if (A.err != cudaSuccess) { int r = cuda_status(A.err); A.release(); delete c; return r; }
   cudaError_t e = cudaMemcpy(dl, lut.data(), sizeof(int) * lut.size(), cudaMemcpyHostToDevice);
-  int one = 1;
-  if (e == cudaSuccess) e = cudaMemcpy(b.epoch, &one, sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { int r = cuda_status(e); A.release(); delete c; return r; }
   c->frames_done.assign(S, 0);
   c->pyr_smem = pyramid_smem(g);
@@ -380,7 +382,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int occ = 0;
-  const int fast_smem = (int)sizeof(FastWarp) * FAST_WARPS;
+  const int fast_smem = (int)sizeof(FastWarp) * FAST_WARPS + (S + 1) * (int)sizeof(int);
   cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, fast_smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, 32 * FAST_WARPS, fast_smem);
   c->fast_grid = std::max(1, g_num_sms * std::max(occ, 1));
@@ -410,6 +412,8 @@ int vf_destroy(vf_ctx* c)
   }
   pipe_free(c);
   pack_free(c);
+  for (size_t k = 0; k < c->gstreams.size(); k++) { cudaStreamDestroy(c->gstreams[k]); cudaEventDestroy(c->gjoin[k]); }
+  if (c->gfork) cudaEventDestroy(c->gfork);
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
@@ -444,17 +448,30 @@ int vf_get_stage_ms(vf_ctx* c, double* ms7, int* n_steps, void* stream)  /* ms7:
   if (e != cudaSuccess) return cuda_status(e);
   for (int k = 0; k < VF_NSTAGES; k++) ms7[k] = 0.0;
   int steps = 0;
-  for (size_t i = 0; i + 1 < c->ev_used.size(); i++) {
-    int stg = c->ev_stage[i];
-    if (stg < 0) { steps++; continue; }
+  // intervals between consecutive marks of the same group; stage times are
+  // summed over groups and divided by the group count (average launch time)
+  const size_t m = c->ev_used.size();
+  std::vector<int> groups_seen;
+  for (size_t i = 0; i < m; i++) {
+    if (c->ev_stage[i] < 0) {
+      if (c->ev_group[i] == 0) steps++;
+      continue;
+    }
+    size_t j = i + 1;
+    while (j < m && c->ev_group[j] != c->ev_group[i]) j++;
+    if (j >= m) continue;
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, c->ev_used[i], c->ev_used[i + 1]);
-    ms7[stg] += ms;
+    cudaEventElapsedTime(&ms, c->ev_used[i], c->ev_used[j]);
+    ms7[c->ev_stage[i]] += ms;
+    if (std::find(groups_seen.begin(), groups_seen.end(), c->ev_group[i]) == groups_seen.end())
+      groups_seen.push_back(c->ev_group[i]);
   }
-  if (!c->ev_stage.empty() && c->ev_stage.back() < 0) steps++;
+  if (groups_seen.size() > 1)
+    for (int k = 0; k < VF_NSTAGES; k++) ms7[k] /= (double)groups_seen.size();
   for (cudaEvent_t ev : c->ev_used) c->ev_pool.push_back(ev);
   c->ev_used.clear();
   c->ev_stage.clear();
+  c->ev_group.clear();
   if (n_steps) *n_steps = steps;
   return VF_OK;
 }
@@ -463,17 +480,16 @@ int vf_reset(vf_ctx* c, void* stream)
 {
   if (!c) return VF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaMemsetAsync(c->b.ctr, 0, sizeof(int) * c->S * C_NCTR, st);
-  cudaMemsetAsync(c->b.cov, 0, sizeof(unsigned long long) * c->S, st);
-  cudaMemsetAsync(c->b.report, 0, sizeof(double) * c->S * 16, st);
+  k_reset<<<cdiv(c->S, 128), 128, 0, st>>>(c->b.ctr, c->b.cov, c->b.report, c->S);
   std::fill(c->frames_done.begin(), c->frames_done.end(), 0);
   return cuda_status(cudaGetLastError());
 }
 
-static int launch_step(vf_ctx* c, int n, cudaStream_t st)
+static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
 {
   const Geo& g = c->g;
   Bufs b = c->b;
+  b.s0 = s0;
   if (g.mask_mode == 2) {
     stage_mark(c, 0, st);
     int smem = g.grid[0].rows * g.grid[0].cols * 4;
@@ -492,13 +508,13 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(
       g, b, tile_ctas, cov_ctas, carry_ctas);
   stage_mark(c, 3, st);
-  k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS, st>>>(g, b);
+  const int pre_bytes = (n + 1) * (int)sizeof(int);
+  k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n);
   stage_mark(c, 4, st);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
   stage_mark(c, 6, st);
-  const int pre_bytes = (n + 1) * (int)sizeof(int);
   k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0);
   k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
   k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
@@ -507,8 +523,46 @@ static int launch_step(vf_ctx* c, int n, cudaStream_t st)
   stage_mark(c, 8, st);
   k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
   stage_mark(c, -1, st);
-  for (int s = 0; s < n; s++) c->frames_done[s]++;
+  for (int s = s0; s < s0 + n; s++) c->frames_done[s]++;
   return cuda_status(cudaGetLastError());
+}
+
+// Streams [0, n) in G groups on separate CUDA streams (forked from / joined
+// into `st`), so the launches of one group fill the gaps and tails of another.
+static int launch_grouped(vf_ctx* c, int n, cudaStream_t st)
+{
+  int G = n >= 32 ? 4 : (n >= 8 ? 2 : 1);
+  if (const char* e = getenv("VF_STREAM_GROUPS")) G = std::max(1, std::min(n, atoi(e)));
+  if (G == 1) {
+    c->cur_group = 0;
+    return launch_step(c, 0, n, st);
+  }
+  if ((int)c->gstreams.size() < G) {
+    if (!c->gfork) cudaEventCreateWithFlags(&c->gfork, cudaEventDisableTiming);
+    while ((int)c->gstreams.size() < G) {
+      cudaStream_t gs;
+      cudaEvent_t ge;
+      if (cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking) != cudaSuccess) return VF_ERR_CUDA;
+      cudaEventCreateWithFlags(&ge, cudaEventDisableTiming);
+      c->gstreams.push_back(gs);
+      c->gjoin.push_back(ge);
+    }
+  }
+  cudaEventRecord(c->gfork, st);
+  const uint8_t* base = c->b.frames;
+  int rc = VF_OK;
+  for (int k = 0; k < G && rc == VF_OK; k++) {
+    const int s0 = (int)((long long)n * k / G), s1 = (int)((long long)n * (k + 1) / G);
+    cudaStreamWaitEvent(c->gstreams[k], c->gfork, 0);
+    c->b.frames = base + (long long)s0 * c->b.frame_stride;
+    c->cur_group = k;
+    rc = launch_step(c, s0, s1 - s0, c->gstreams[k]);
+    cudaEventRecord(c->gjoin[k], c->gstreams[k]);
+  }
+  c->b.frames = base;
+  c->cur_group = 0;
+  for (int k = 0; k < G; k++) cudaStreamWaitEvent(st, c->gjoin[k], 0);
+  return rc;
 }
 
 int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n_streams,
@@ -519,7 +573,7 @@ int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int6
   c->b.frames = frames_dev;
   c->b.frame_stride = stream_stride;
   c->b.frame_pitch = row_pitch;
-  return launch_step(c, n_streams, (cudaStream_t)stream);
+  return launch_grouped(c, n_streams, (cudaStream_t)stream);
 }
 
 int vf_process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch, int n_streams,
@@ -746,7 +800,7 @@ int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_str
   c->b.frames = P.frames[k];
   c->b.frame_stride = fbytes;
   c->b.frame_pitch = c->g.W;
-  rc = launch_step(c, n_streams, P.comp);
+  rc = launch_grouped(c, n_streams, P.comp);
   if (rc) return rc;
   cudaStreamWaitEvent(P.comp, P.ev_d2h[k], 0);
   k_pack<<<g_num_sms * 8, 256, (n_streams + 1) * sizeof(int), P.comp>>>(
@@ -797,9 +851,8 @@ int vf_get_diag(vf_ctx* c, int64_t* out8, void* stream)
 {
   if (!c || !out8) return VF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  int wc = 0;
-  std::vector<int> sc(c->S), ctr((size_t)c->S * C_NCTR);
-  cudaMemcpyAsync(&wc, c->b.work_count, sizeof(int), cudaMemcpyDeviceToHost, st);
+  std::vector<int> wcs(c->S), sc(c->S), ctr((size_t)c->S * C_NCTR);
+  cudaMemcpyAsync(wcs.data(), c->b.work_count, sizeof(int) * c->S, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(sc.data(), c->b.sat_count, sizeof(int) * c->S, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(ctr.data(), c->b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
@@ -811,6 +864,8 @@ int vf_get_diag(vf_ctx* c, int64_t* out8, void* stream)
     if (masked) sat += sc[s]; else { sat += c->g.sat_tiles; dense++; }
     stage += ctr[(size_t)s * C_NCTR + C_STAGE];
   }
+  long long wc = 0;
+  for (int v : wcs) wc += v;
   out8[0] = wc;                                   // active FAST tiles (all streams)
   out8[1] = (long long)c->g.tiles_per_stream * c->S;  // FAST tiles in total
   out8[2] = sat;                                  // SAT tiles built
@@ -921,8 +976,9 @@ int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, c
   cudaMemcpyAsync(b.worklist, wl.data(), sizeof(int) * nwl, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.work_count, &nwl, sizeof(int), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.ctr, frame1, sizeof(frame1), cudaMemcpyHostToDevice, st);
-  cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FastWarp) * FAST_WARPS);
-  k_fast<<<std::max(1, std::min(cdiv(nwl, FAST_WARPS), 148 * 8)), 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS, st>>>(g, b);
+  cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FastWarp) * FAST_WARPS + 8);
+  k_fast<<<std::max(1, std::min(cdiv(nwl, FAST_WARPS), 148 * 8)), 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + 8, st>>>(
+      g, b, 1);
   cudaMemcpy2DAsync(scores_dev, scores_pitch, b.scores, L.pitch, w, h, cudaMemcpyDeviceToDevice, st);
   int rc = cuda_status(cudaStreamSynchronize(st));
   A.release();
@@ -992,6 +1048,9 @@ int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, co
   b.frames = frame_dev; b.frame_stride = 0; b.frame_pitch = pitch;
   k_pyramid<<<dim3(c->g.ptx, c->g.pty, 1), 256, c->pyr_smem, st>>>(c->g, b);
   k_carries<<<dim3(c->g.pty, 1), 32, 0, st>>>(c->g, b);
+  int ctr0[C_NCTR] = {0};
+  ctr0[C_NDET] = n;              // k_sat builds every tile of a stream with keypoints (unmasked)
+  cudaMemcpyAsync(b.ctr, ctr0, sizeof(ctr0), cudaMemcpyHostToDevice, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1);   // stream 0 -> slot 0
   k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev,
                                                               theta_in_dev, theta_out_dev, desc_dev);

@@ -29,6 +29,7 @@ enum {
   C_ERR = 9,        // sticky error bits
   C_NSURV = 10,     // NMS survivors (before border filter)
   C_NCAND = 11,     // FAST candidates
+  C_EPOCH = 12,     // monotonic step id (activity stamps), survives vf_reset
   C_NCTR = 16
 };
 #define VF_ERRBIT_CAPACITY 1
@@ -82,7 +83,8 @@ struct Geo {
 
 // Per-launch stream-batch pointers.
 struct Bufs {
-  const uint8_t* frames; long long frame_stride; long long frame_pitch; // o0 of stream s
+  int s0;               // first stream of this launch (stream groups run on separate CUDA streams)
+  const uint8_t* frames; long long frame_stride; long long frame_pitch; // o0 of stream s (relative to s0)
   uint8_t* layers;      // [S][layer_slab]
   uint8_t* scores;      // [S][sm_slab]
   uint32_t* bitmaps;    // [S][bm_slab_words]
@@ -103,8 +105,6 @@ struct Bufs {
   uint32_t* carry;      // [S][H][ptx] strip carries K(y, tx) (see strip_sum)
   int* sat_stamp;       // [S][sat_tiles] epoch at which the tile's L was written
   int* sat_work; int* sat_count;   // [S][sat_tiles] / [S]: SAT tiles marked this step (masked frames)
-  int* sat_done; int* desc_done;   // [S] k_sat_describe progress counters
-  int* q_ctr;                      // k_sat_describe work-queue ticket
   double* st_x; double* st_y; double* st_s; double* st_v;   // staging [S][kp_cap]
   // double-buffered features [S][2][kp_cap]
   double* fx; double* fy; double* fs; double* ft; double* fv;
@@ -112,16 +112,19 @@ struct Bufs {
   int* ctr;             // [S][C_NCTR]
   unsigned long long* cov;  // [S] covered full-res pixels of this frame
   double* report;       // [S][8]: n_det, n_prop, n_total, n_dropped, coverage, frame, n_surv, n_cand
-  int* worklist; int* work_count;  // active FAST tiles (s * tiles_per_stream + tile)
-  int* epoch;           // step counter, bumped by k_finalize
+  int* worklist; int* work_count;  // [S][tiles_per_stream] / [S]: active FAST tiles per stream
 };
 
 // --------------------------------------------------------------------------
 // small helpers
 // --------------------------------------------------------------------------
+// Per-stream monotonic step id: activity stamps compare against it, so nothing
+// has to be cleared between steps (or across vf_reset).
+__device__ __forceinline__ int stream_epoch(const Bufs& b, int s) { return b.ctr[s * C_NCTR + C_EPOCH] + 1; }
+
 __device__ __forceinline__ const uint8_t* layer_ptr(const Geo& g, const Bufs& b, int s, int l, int& pitch)
 {
-  if (l == 0) { pitch = (int)b.frame_pitch; return b.frames + (long long)s * b.frame_stride; }
+  if (l == 0) { pitch = (int)b.frame_pitch; return b.frames + (long long)(s - b.s0) * b.frame_stride; }
   pitch = g.L[l].pitch;
   return b.layers + (long long)s * g.layer_slab + g.L[l].layer_off;
 }

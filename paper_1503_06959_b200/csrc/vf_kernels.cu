@@ -233,7 +233,7 @@ __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s,
                                              uint8_t* t0, uint32_t* rowsum = nullptr)
 {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const uint8_t* src = b.frames + (long long)s * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
+  const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
   const bool vec = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)b.frame_pitch) & 15) == 0 && tw == g.ptw;
   if (vec) {
     const int per_row = g.ptw / 16;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s,
 __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int s = blockIdx.z;
+  const int s = b.s0 + blockIdx.z;
   const int X0 = blockIdx.x * g.ptw, Y0 = blockIdx.y * g.pth;
   const int tid = threadIdx.x, nt = blockDim.x;
   // carve smem: level tiles then SAT
@@ -278,9 +278,7 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
   if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
     b.ctr[s * C_NCTR + C_STAGE] = 0;
     b.sat_count[s] = 0;
-    b.sat_done[s] = 0;
-    b.desc_done[s] = 0;
-    if (s == 0) { *b.work_count = 0; *b.q_ctr = 0; }
+    b.work_count[s] = 0;
   }
 
   // ---- load the o0 tile ------------------------------------------------------
@@ -480,9 +478,10 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
   int* pre = reinterpret_cast<int*>(ssat + g.ptw * g.pth);
   __shared__ int sm_warp[32];
   // detected rank -> staging slot map for k_desc_sample (thread per band)
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)n_streams * g.bands_per_stream;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int s = (int)(i / g.bands_per_stream);
+  for (long long il = (long long)blockIdx.x * blockDim.x + threadIdx.x; il < (long long)n_streams * g.bands_per_stream;
+       il += (long long)gridDim.x * blockDim.x) {
+    const int s = b.s0 + (int)(il / g.bands_per_stream);
+    const long long i = (long long)b.s0 * g.bands_per_stream + il;
     const int4 r = __ldcg(reinterpret_cast<const int4*>(b.band_rec) + i);
     if (r.y > 0) {
       const int o = __ldcg(b.band_out + i);
@@ -490,12 +489,15 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
       for (int k = 0; k < r.y && o + k < g.kp_cap; k++) gidx[o + k] = r.x + k;
     }
   }
-  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles; });
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) {
+    const int s = b.s0 + sl;
+    return b.ctr[s * C_NCTR + C_NDET] == 0 ? 0 : (use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles);
+  });
   const int n = pre[n_streams];
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     int lo = 0, hi = n_streams;
     while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
-    const int s = lo, i = item - pre[s];
+    const int s = b.s0 + lo, i = item - pre[lo];
     const int t = use_mask(g, b, s) ? b.sat_work[(long long)s * g.sat_tiles + i] : i;
     const int ty = t / g.ptx, tx = t - ty * g.ptx;
     const int X0 = tx * g.ptw, Y0 = ty * g.pth;
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
 // Strip carries for stand-alone use (the pipeline computes them in k_worklist).
 __global__ void k_carries(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
-  strip_carries(g, b, blockIdx.y, blockIdx.x);
+  strip_carries(g, b, b.s0 + blockIdx.y, blockIdx.x);
 }
 
 // ============================================================================
@@ -541,19 +543,17 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   __shared__ __align__(16) uint8_t t0[TH * TW];
   __shared__ __align__(16) uint8_t si0[32 * 64], so1[24 * 48], si1[16 * 32], so2[12 * 24], si2[8 * 16];
   __shared__ __align__(16) uint8_t so3[6 * 12 + 8];
-  const int s = blockIdx.z, tid = threadIdx.x;
+  const int s = b.s0 + blockIdx.z, tid = threadIdx.x;
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
   if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
     b.ctr[s * C_NCTR + C_STAGE] = 0;
     b.sat_count[s] = 0;
-    b.sat_done[s] = 0;
-    b.desc_done[s] = 0;
-    if (s == 0) { *b.work_count = 0; *b.q_ctr = 0; }
+    b.work_count[s] = 0;
   }
   const int tw = min(TW, g.W - X0), th = min(TH, g.H - Y0);
   // ---- o0 tile ----
   {
-    const uint8_t* src = b.frames + (long long)s * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
+    const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
     const bool vec = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)b.frame_pitch) & 15) == 0 && tw == TW;
     if (vec) {
       for (int i = tid; i < th * (TW / 16); i += 256) {
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
 __global__ void __launch_bounds__(1024) k_binmask(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   extern __shared__ int hist[];
-  const int s = blockIdx.x;
+  const int s = b.s0 + blockIdx.x;
   if (!use_mask(g, b, s)) return;
   const GridGeo& G = g.grid[0];
   const int n_cells = G.rows * G.cols;
@@ -754,9 +754,8 @@ __global__ void __launch_bounds__(1024) k_binmask(const __grid_constant__ Geo g,
 __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
                                                    int tile_ctas, int cov_ctas, int carry_ctas)
 {
-  const int s = blockIdx.y;
-  const int* ep = b.epoch;
-  const int epoch = *ep;
+  const int s = b.s0 + blockIdx.y;
+  const int epoch = stream_epoch(b, s);
   const int um = use_mask(g, b, s);
   const int lane = threadIdx.x & 31;
   if ((int)blockIdx.x >= tile_ctas + cov_ctas && (int)blockIdx.x < tile_ctas + cov_ctas + carry_ctas) {
@@ -865,7 +864,7 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
       b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
       b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
       b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
-      b.worklist[atomicAdd(b.work_count, 1)] = s * g.tiles_per_stream + tile;
+      b.worklist[(long long)s * g.tiles_per_stream + atomicAdd(b.work_count + s, 1)] = tile;
     }
     return;
   }
@@ -877,9 +876,9 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     const unsigned m = __activemask();
     const int leader = __ffs(m) - 1, rank = __popc(m & ((1u << lane) - 1));
     int pos = 0;
-    if (lane == leader) pos = atomicAdd(b.work_count, __popc(m));
+    if (lane == leader) pos = atomicAdd(b.work_count + s, __popc(m));
     pos = __shfl_sync(m, pos, leader);
-    b.worklist[pos + rank] = s * g.tiles_per_stream + tile;
+    b.worklist[(long long)s * g.tiles_per_stream + pos + rank] = tile;
   }
 }
 
@@ -922,17 +921,23 @@ struct FastWarp {
   uint16_t cc[VF_TILE_W];     // cell column of each tile column
 };
 
-__global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+__global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
+                                                          int n_streams)
 {
   extern __shared__ __align__(16) uint8_t fsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   FastWarp& fw = reinterpret_cast<FastWarp*>(fsm)[wid];
-  const int n_work = *b.work_count;
+  int* pre = reinterpret_cast<int*>(fsm + sizeof(FastWarp) * FAST_WARPS);   // [n_streams + 1]
+  __shared__ int sm_warp[32];
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.work_count[b.s0 + sl]; });
+  const int n_work = pre[n_streams];
   const int t = g.threshold;
   const uint32_t tt = (uint32_t)t * 0x01010101u;
   for (int item = blockIdx.x * FAST_WARPS + wid; item < n_work; item += gridDim.x * FAST_WARPS) {
-    const int code = b.worklist[item];
-    const int s = code / g.tiles_per_stream, tile_id = code - s * g.tiles_per_stream;
+    int lo = 0, hi = n_streams;
+    while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
+    const int s = b.s0 + lo;
+    const int tile_id = b.worklist[(long long)s * g.tiles_per_stream + (item - pre[lo])];
     int l = 0;
     while (l + 1 < g.NL && tile_id >= g.L[l + 1].tile_base) l++;
     const LayerGeo& Lg = g.L[l];
@@ -1343,10 +1348,10 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
 __global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int cand[NMS_WARPS][32];
-  const int s = blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int bid = blockIdx.x * NMS_WARPS + wid;
   if (bid >= g.bands_per_stream) return;
-  const int epoch = *b.epoch;
+  const int epoch = stream_epoch(b, s);
   const int um = use_mask(g, b, s) ? epoch : 0;   // nonzero: tile-stamp gating at this epoch
   int* ctr = b.ctr + s * C_NCTR;
   int kept = 0, n_ok = 0, n_drop = 0, base = 0;
@@ -1711,7 +1716,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
   extern __shared__ int pre[];   // [n_streams + 1]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
-  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
   for (int j = threadIdx.x; j < 64; j += 32 * DSW) {
     const int jj = j < VF_NPTS ? j : 0;
@@ -1721,7 +1726,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
   // this lane's two pattern points (lane, lane + 32; lanes 28-31 repeat their first)
   const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
   for (int gi = blockIdx.x * DSW + wid; gi < total; gi += gridDim.x * DSW) {
-    const int s = find_stream(pre, n_streams, gi), i = gi - pre[s];
+    const int sl = find_stream(pre, n_streams, gi), s = b.s0 + sl, i = gi - pre[sl];
     const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
     const long long o = ((long long)s * 2 + cur) * g.kp_cap + i;
     const uint32_t* S = b.sat + (long long)(s % g.sat_slots) * g.W * g.H;
@@ -1773,14 +1778,14 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
   __shared__ __align__(16) uint8_t vv[DO_THREADS * DW_ROW];
   __shared__ int sm_warp[32];
   extern __shared__ int pre[];
-  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
   uint8_t* v = vv + threadIdx.x * DW_ROW;
   for (int base = blockIdx.x * DO_THREADS; base < total; base += gridDim.x * DO_THREADS) {
     const int gi = base + threadIdx.x;
     long long o = -1;
     if (gi < total) {
-      const int s = find_stream(pre, n_streams, gi), i = gi - pre[s];
+      const int sl = find_stream(pre, n_streams, gi), s = b.s0 + sl, i = gi - pre[sl];
       o = ((long long)s * 2 + (b.ctr[s * C_NCTR + C_FRAME] & 1)) * g.kp_cap + i;
       const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + o * 64);
 #pragma unroll
@@ -1814,7 +1819,7 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
 __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int sm_warp[32];
-  const int s = blockIdx.y, tid = threadIdx.x;
+  const int s = b.s0 + blockIdx.y, tid = threadIdx.x;
   if (!use_mask(g, b, s)) return;
   const int* ctr = b.ctr + s * C_NCTR;
   const int cur = ctr[C_FRAME] & 1, prev = cur ^ 1;
@@ -1901,16 +1906,30 @@ __global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, con
 // ============================================================================
 __global__ void k_finalize(const __grid_constant__ Geo g, const __grid_constant__ Bufs b, int n_streams)
 {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < n_streams) {
+  const int sl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sl < n_streams) {
+    const int s = b.s0 + sl;
     int* ctr = b.ctr + s * C_NCTR;
     const int cur = ctr[C_FRAME] & 1;
     ctr[C_NFEAT0 + cur] = ctr[C_NTOTAL];
     ctr[C_FRAME] += 1;
+    ctr[C_EPOCH] += 1;
     ctr[C_NCAND] = 0;
     b.cov[s] = 0ull;
   }
-  if (s == 0) *b.epoch += 1;
+}
+
+// vf_reset: forget the temporal state; the activity epoch stays monotonic so
+// stamps written before the reset can never match again.
+__global__ void k_reset(int* ctr, unsigned long long* cov, double* report, int n_streams)
+{
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_streams) return;
+  for (int k = 0; k < C_NCTR; k++)
+    if (k != C_EPOCH) ctr[s * C_NCTR + k] = 0;
+  ctr[s * C_NCTR + C_EPOCH] += 1;
+  cov[s] = 0ull;
+  for (int k = 0; k < 16; k++) report[(long long)s * 16 + k] = 0.0;
 }
 
 // ============================================================================
