@@ -531,7 +531,9 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
 // into `st`), so the launches of one group fill the gaps and tails of another.
 static int launch_grouped(vf_ctx* c, int n, cudaStream_t st)
 {
-  int G = n >= 32 ? 4 : (n >= 8 ? 2 : 1);
+  // one group measured fastest once NMS refines survivors densely (r01: 55.9k
+  // vs 54.8k frames/s at 64 x 1080p with 4 groups); VF_STREAM_GROUPS overrides
+  int G = 1;
   if (const char* e = getenv("VF_STREAM_GROUPS")) G = std::max(1, std::min(n, atoi(e)));
   if (G == 1) {
     c->cur_group = 0;

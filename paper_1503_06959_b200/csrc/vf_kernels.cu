@@ -1155,9 +1155,10 @@ __device__ __forceinline__ int patch_to_double(const int v[9], double p[3][3])
 
 struct NmsOut { double x, y, sig, v; int flags; };  // flags: 1 survivor, 2 border ok, 4 kept
 
-__device__ NmsOut nms_one(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x)
+// Batch 1 of detector.py:251-275: strict 3x3 maximum and strict vs the rounded
+// projection into layers l-1, l+1.
+__device__ __forceinline__ bool nms_test(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x)
 {
-  NmsOut o; o.flags = 0; o.x = o.y = o.sig = o.v = 0.0;
   const LayerGeo& Lg = g.L[l];
   // batch 1: centre, 8 neighbours, projected pixels of layers l-1, l+1
   const int sv = score_read(g, b, s, um, l, y, x);
@@ -1191,8 +1192,27 @@ __device__ NmsOut nms_one(const Geo& g, const Bufs& b, int s, int um, int l, int
   for (int i = 0; i < 8; i++) keep &= sv > nb[i];
 #pragma unroll
   for (int k = 0; k < 2; k++) keep &= !has[k] || sv > cj[k];
-  if (!keep) return o;
+  return keep;
+}
+
+// Survivor refinement (detector.py:277-302) + border / merge filters.
+__device__ NmsOut nms_refine(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x)
+{
+  NmsOut o;
   o.flags = 1;
+  const LayerGeo& Lg = g.L[l];
+  const bool has[2] = {l >= 1, l + 1 < g.NL};
+  int yj[2] = {0, 0}, xj[2] = {0, 0};
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    if (!has[k]) continue;
+    const int j = l - 1 + 2 * k;
+    const int hj = g.L[j].h, wj = g.L[j].w;
+    const long long a = ((long long)y * hj + (Lg.h >> 1)) / Lg.h;
+    const long long c = ((long long)x * wj + (Lg.w >> 1)) / Lg.w;
+    yj[k] = (int)(a < hj - 1 ? a : hj - 1);
+    xj[k] = (int)(c < wj - 1 ? c : wj - 1);
+  }
   // batch 2: the three 3x3 patches (zero-padded maps, detector.py:231-236)
   int pv[3][9];
   patch_load(g, b, s, um, l, y, x, pv[0]);
@@ -1348,6 +1368,7 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
 __global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int cand[NMS_WARPS][32];
+  __shared__ int sq[NMS_WARPS][64];   // survivor queue (y << 16 | x)
   const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int bid = blockIdx.x * NMS_WARPS + wid;
   if (bid >= g.bands_per_stream) return;
@@ -1393,6 +1414,7 @@ __global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ 
           return (!um || __ldg(tst + ck / VF_TILE_WORDS) == epoch) ? __ldg(bm + crow * bmw + ck) : 0u;
         };
         int cursor = w0, idx = ex;             // this lane's enumeration state
+        int qn = 0;                            // survivors queued (warp-uniform)
         uint32_t pend = cursor < w1 ? load_word() : 0u;
         for (int r0 = 0; r0 < total; r0 += 32) {
           // emit this round's candidates (ranks r0 .. r0+31) into cand[]
@@ -1410,22 +1432,40 @@ __global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ 
           }
           __syncwarp();
           const int nr = min(32, total - r0);
-          NmsOut o;
-          o.flags = 0;
+          bool keep = false;
+          int yx = 0;
           if (lane < nr) {
-            const int yx = cand[wid][lane];
-            o = nms_one(g, b, s, um, l, yx >> 16, yx & 0xffff);
+            yx = cand[wid][lane];
+            keep = nms_test(g, b, s, um, l, yx >> 16, yx & 0xffff);
           }
+          const unsigned sm = __ballot_sync(0xffffffffu, keep);
+          if (keep) sq[wid][qn + __popc(sm & ((1u << lane) - 1))] = yx;
+          qn += __popc(sm);
           __syncwarp();
-          const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
-          n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
-          n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
-          if (o.flags & 4) {
-            const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
-            b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
-            if (um) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
+          // refine survivors 32 at a time (FIFO: rank order is preserved)
+          const bool last_round = r0 + 32 >= total;
+          while (qn >= 32 || (last_round && qn > 0)) {
+            const int nb = min(32, qn);
+            NmsOut o;
+            o.flags = 0;
+            if (lane < nb) {
+              const int v = sq[wid][lane];
+              o = nms_refine(g, b, s, um, l, v >> 16, v & 0xffff);
+            }
+            const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
+            n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
+            n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
+            if (o.flags & 4) {
+              const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
+              b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
+              if (um) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
+            }
+            kept += __popc(kb);
+            __syncwarp();
+            if (lane + nb < qn) sq[wid][lane] = sq[wid][lane + nb];
+            qn -= nb;
+            __syncwarp();
           }
-          kept += __popc(kb);
         }
       } else {
         base = 0;
