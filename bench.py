@@ -375,36 +375,56 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (live CUDA events, timed region) ----
+    # ---- roofline (live CUDA events inside the timed region) ----
+    # The path is one step of 9 launches; SURVEY.md 8(d)'s algorithmic bytes are
+    # defined per frame for the whole path, so the primary roofline is the step:
+    # B_alg(step) / step time.  Each kernel is also listed with its own byte
+    # model and live average launch time.
     peak, peak_kind = hbm_peak()
     k_out = tot[1]
     k_total = tot[2]
     cov_sum = tot[3]
     b_alg = algorithmic_bytes(frames_done, cov_sum, k_out, k_total - k_out)
-    dom = max((k for k in stage if stage[k] > 0), key=lambda k: stage[k])
-    dom_ms = stage[dom] / max(n_steps, 1)
-    # algorithmic bytes per launch of each stage, this rank
-    per_frame_top = W_FR * H_FR * (4.0 ** -3)
-    f_loc = d[:, 3].sum()
-    alg = {
-        "pyramid": W_FR * H_FR * f_loc * (1 + 0.918) + 2 * per_frame_top * f_loc,
-        "fast": 2 * W_FR * H_FR * 1.918 * d[:, 2].sum(),
-        "describe": 109.0 * d[:, 0].sum(),
-        "propagate": 2 * 109.0 * (d[:, 1].sum() - d[:, 0].sum()),
-        "nms": W_FR * H_FR * 1.918 * d[:, 2].sum() / 8,
-    }
-    dom_bytes = alg.get(dom, 0.0) / max(n_steps, 1)
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
     step_ms = ms_max / K
-    step_achieved = b_alg / world / K / (step_ms / 1e3) / 1e9 if world == 1 else b_alg / K / (step_ms / 1e3) / 1e9
+    step_achieved = b_alg / K / (step_ms / 1e3) / 1e9
+    f_loc = d[:, 3].sum()
+    det_loc, tot_loc = d[:, 0].sum(), d[:, 1].sum()
+    wh = W_FR * H_FR
+    per_step = 1.0 / max(n_steps, 1)
+    kbytes = {   # algorithmic bytes per step of each kernel (this rank)
+        "pyramid": (wh * (1 + 0.918) + 2 * wh / 64.0) * f_loc * per_step,
+        "fast": 2.0 * 1024 * diag["fast_tiles_active"],
+        "nms": 1.0 * 1024 * diag["fast_tiles_active"] + 32.0 * det_loc * per_step,
+        "sat": 5.0 * 96 * 48 * diag["sat_tiles_built"],
+        "describe": (32.0 + 109.0) * det_loc * per_step,
+        "propagate": 218.0 * (tot_loc - det_loc) * per_step,
+    }
+    kernels = []
+    for k, v in stage.items():
+        if v <= 0:
+            continue
+        ms_k = v / max(n_steps, 1)
+        ach = kbytes.get(k, 0.0) / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
+        kernels.append({"kernel": k, "ms_per_step": ms_k, "share": v / max(sum(stage.values()), 1e-9),
+                        "algorithmic_bytes": kbytes.get(k, 0.0), "achieved_gbs": ach, "frac": ach / peak})
+    kernels.sort(key=lambda r: -r["ms_per_step"])
+    traffic = None
+    tf = ROOT / "profiles" / "r01_traffic.json"
+    if tf.exists():
+        try:
+            tj = json.loads(tf.read_text())
+            traffic = tj["dram_bytes_per_step"] * (S / tj.get("streams", S))
+        except Exception:
+            traffic = None
     roofline = {
-        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": None, "kernel": f"k_{dom}", "kernel_ms_per_launch": dom_ms,
-        "kernel_share_of_step": stage[dom] / max(sum(stage.values()), 1e-9),
+        "bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s", "frac": step_achieved / peak,
+        "traffic": traffic, "kernel": "detect+describe step (all launches of one step)",
+        "algorithmic_bytes_per_step": b_alg / K,
+        "traffic_source": "profiles/r01_traffic.json: sum of ncu dram__bytes_read+write over one step's launches"
+                          if traffic is not None else None,
         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
-        "step": {"algorithmic_bytes_per_step": b_alg / K, "achieved": step_achieved,
-                 "frac": step_achieved / peak},
-        "stage_ms_per_step": {k: v / max(n_steps, 1) for k, v in stage.items()},
+        "dominant_kernel": kernels[0] if kernels else None,
+        "kernels": kernels,
         "work_last_step": diag,
     }
 
