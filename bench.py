@@ -89,6 +89,7 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        self._nvml_start()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -99,6 +100,44 @@ class ClockSampler:
             self.proc = None
         return self
 
+    # NVML poller (every 2 ms): the timed region can be ~0.1 s, shorter than nvidia-smi's period.
+    NVML_BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4}
+
+    def _nvml_start(self):
+        self.nv = []
+        self.nv_stop = threading.Event()
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = None
+            try:
+                import torch
+
+                pr = torch.cuda.get_device_properties(torch.cuda.current_device())
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                h = nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.nv_max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.nv_stop.is_set():
+                    try:
+                        self.nv.append((time.time(), float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                        int(get_r(h))))
+                    except Exception:
+                        return
+                    time.sleep(0.002)
+
+            self.nv_t = threading.Thread(target=poll, daemon=True)
+            self.nv_t.start()
+        except Exception:
+            self.nv = None
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
@@ -106,8 +145,12 @@ class ClockSampler:
     def window(self, t0, t1):
         """Keep only samples taken inside [t0, t1] (plus one sampling period)."""
         self.lines = [(t, ln) for t, ln in self.lines if t0 <= t <= t1 + 0.2]
+        if self.nv:
+            self.nv = [r for r in self.nv if t0 <= r[0] <= t1]
 
     def __exit__(self, *exc):
+        if self.nv is not None:
+            self.nv_stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -116,6 +159,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nv:
+            reasons = sorted(k for k, b in self.NVML_BITS.items() if any(r & b for _, _, r in self.nv))
+            return {"sm_mhz": statistics.median(c for _, c, _ in self.nv), "sm_max_mhz": self.nv_max,
+                    "reasons": reasons, "samples": len(self.nv), "source": "nvml, 2 ms period",
+                    "sm_min_mhz": min(c for _, c, _ in self.nv)}
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for _, ln in self.lines:
