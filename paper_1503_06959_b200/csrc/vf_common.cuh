@@ -148,9 +148,12 @@ __device__ __forceinline__ int gate_at(const Geo& g, const Bufs& b, int s, int l
 // union of the level masks (pipeline.py:196-199).
 __device__ __forceinline__ int merge_mask_at(const Geo& g, const Bufs& b, int s, double x, double y)
 {
-  long long xi = (long long)floor(x + 0.5), yi = (long long)floor(y + 0.5);
-  xi = xi < 0 ? 0 : (xi > g.W - 1 ? g.W - 1 : xi);
-  yi = yi < 0 ? 0 : (yi > g.H - 1 ? g.H - 1 : yi);
+  // clamp in fp64 first (same result as clamping the rounded integer), then
+  // 32-bit integer cell arithmetic
+  double xr = floor(x + 0.5), yr = floor(y + 0.5);
+  xr = xr < 0.0 ? 0.0 : (xr > (double)(g.W - 1) ? (double)(g.W - 1) : xr);
+  yr = yr < 0.0 ? 0.0 : (yr > (double)(g.H - 1) ? (double)(g.H - 1) : yr);
+  const int xi = (int)xr, yi = (int)yr;
   const uint8_t* cells = b.cells + (long long)s * g.cell_slab;
   int v = 0;
   for (int k = 0; k < g.n_grids; k++) {

@@ -174,31 +174,48 @@ __device__ void sat_tile(const Geo& g, const Bufs& b, int s, int tx, int ty, int
 #define VF_MAX_TX_CHUNKS 8
 __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
 {
+  // K[y][t] = sum over rows y' <= y of the strip and tiles t' < t of the row
+  // sums.  Warp per strip; 32 tile columns per chunk (warp scan across lanes),
+  // rows accumulated per lane.  Chunk c hands its per-row inclusive total to
+  // chunk c + 1 through K[y][32(c+1)] (the value that slot takes anyway).
+  // Row loads are issued RB at a time so the strip is not a chain of latencies.
   const int lane = threadIdx.x & 31;
   const int Y0 = ty * g.pth, th = min(g.pth, g.H - Y0);
   const uint32_t* rs = b.rowsum + ((long long)s * g.H + Y0) * g.ptx;
   uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx;
   const int nch = (g.ptx + 31) / 32;
-  uint32_t acc[VF_MAX_TX_CHUNKS];
+  constexpr int RB = 16;
+#pragma unroll 1
+  for (int c = 0; c < nch; c++) {
+    const int t = 32 * c + lane;
+    const bool in = t < g.ptx;
+    const bool hand = lane == 31 && t + 1 < g.ptx;
+    uint32_t acc = 0;
+#pragma unroll 1
+    for (int y0 = 0; y0 < th; y0 += RB) {
+      uint32_t v[RB], left[RB];
 #pragma unroll
-  for (int c = 0; c < VF_MAX_TX_CHUNKS; c++) acc[c] = 0;
-  for (int y = 0; y < th; y++) {
-    uint32_t carry = 0;
+      for (int k = 0; k < RB; k++) {
+        const bool r = y0 + k < th;
+        v[k] = (in && r) ? rs[(long long)(y0 + k) * g.ptx + t] : 0u;
+        left[k] = (c > 0 && r) ? K[(long long)(y0 + k) * g.ptx + 32 * c] : 0u;
+      }
 #pragma unroll
-    for (int c = 0; c < VF_MAX_TX_CHUNKS; c++) {
-      if (c < nch) {
-        const int t = 32 * c + lane;
-        acc[c] += t < g.ptx ? rs[(long long)y * g.ptx + t] : 0u;
-        uint32_t inc = acc[c];
+      for (int k = 0; k < RB; k++) {
+        acc += v[k];
+        uint32_t inc = acc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += v;
+          const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
         }
-        if (t < g.ptx) K[(long long)y * g.ptx + t] = carry + inc - acc[c];
-        carry += __shfl_sync(0xffffffffu, inc, 31);
+        if (y0 + k < th) {
+          if (in) K[(long long)(y0 + k) * g.ptx + t] = left[k] + inc - acc;
+          if (hand) K[(long long)(y0 + k) * g.ptx + t + 1] = left[k] + inc;
+        }
       }
     }
+    __syncwarp();
   }
 }
 
@@ -849,10 +866,21 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
       return v;
     };
     if (!warp_mode) {
-      active = 0;
-      for (int r = r0; r <= r1 && !active; r++)
-        for (int k = 0; k < nwd; k++)
-          if (word_any(r, k)) { active = 1; break; }
+      // all words of the rectangle, four loads in flight (no early exit)
+      uint32_t any = 0;
+      const int n = nrow * nwd;
+      int r = r0, k = 0;
+#pragma unroll 1
+      for (int i = 0; i < n; i += 4) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          w[j] = i + j < n ? word_any(r, k) : 0u;
+          if (++k == nwd) { k = 0; r++; }
+        }
+        any |= w[0] | w[1] | w[2] | w[3];
+      }
+      active = any != 0;
     } else {
       int any = 0;
       for (int i = lane; i < nrow * nwd && !any; i += 32) any = word_any(r0 + i / nwd, i % nwd) != 0;
@@ -1855,11 +1883,18 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
 }
 
 // Eq. 1: previous features under a 0 mask bit, in previous-list order, origin
-// -> propagated, age + 1 (masking.py:179-183).  Coalesced 1024-feature chunks.
-__global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+// -> propagated, age + 1 (masking.py:179-183).  CTA per 1024-feature chunk of
+// the previous list (chunk output offsets from k_worklist's counts): every
+// field of the chunk is loaded up front (most features propagate), one
+// ballot-based chunk scan gives the destinations, then the 64-B descriptors
+// are copied by the whole CTA as consecutive 16-B words (coalesced).
+#define PROP_PER (PROP_CHUNK / 256)
+static_assert(PROP_PER * 7 <= 32, "flag + rank packing");
+__global__ void __launch_bounds__(256, 3) k_propagate(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
-  __shared__ int sm_warp[32];
-  const int s = b.s0 + blockIdx.y, tid = threadIdx.x;
+  __shared__ int wsum[PROP_PER][8];
+  __shared__ int dsts[PROP_CHUNK];
+  const int s = b.s0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (!use_mask(g, b, s)) return;
   const int* ctr = b.ctr + s * C_NCTR;
   const int cur = ctr[C_FRAME] & 1, prev = cur ^ 1;
@@ -1868,41 +1903,73 @@ __global__ void __launch_bounds__(256) k_propagate(const __grid_constant__ Geo g
   const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
   const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
   const long long ob = ((long long)s * 2 + cur) * g.kp_cap;
-  constexpr int PER = PROP_CHUNK / 256;
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
-    // element j*256 + tid of the chunk: consecutive lanes -> consecutive features
-    double xs[PER], ys[PER];
-    bool f[PER];
+    const int base = c * PROP_CHUNK;
+    double xs[PROP_PER], ys[PROP_PER], ss[PROP_PER], ts[PROP_PER], vs[PROP_PER];
+    int ag[PROP_PER];
 #pragma unroll
-    for (int j = 0; j < PER; j++) {
-      const int e = c * PROP_CHUNK + j * 256 + tid;
-      xs[j] = e < n_prev ? b.fx[fb + e] : 0.0;
-      ys[j] = e < n_prev ? b.fy[fb + e] : 0.0;
+    for (int j = 0; j < PROP_PER; j++) {
+      const int e = base + j * 256 + tid;
+      const bool ok = e < n_prev;
+      const long long p = fb + (ok ? e : 0);
+      xs[j] = b.fx[p]; ys[j] = b.fy[p]; ss[j] = b.fs[p]; ts[j] = b.ft[p]; vs[j] = b.fv[p]; ag[j] = b.fage[p];
     }
+    unsigned fl = 0;
 #pragma unroll
-    for (int j = 0; j < PER; j++) {
-      const int e = c * PROP_CHUNK + j * 256 + tid;
-      f[j] = e < n_prev && !merge_mask_at(g, b, s, xs[j], ys[j]);
+    for (int j = 0; j < PROP_PER; j++) {
+      const int e = base + j * 256 + tid;
+      const bool f = e < n_prev && !merge_mask_at(g, b, s, xs[j], ys[j]);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wsum[j][wid] = __popc(bal);
+      fl |= (f ? 1u : 0u) << j;
+      fl |= (unsigned)__popc(bal & ((1u << lane) - 1)) << (4 + 6 * j);   // rank within the warp (<= 31)
     }
-    long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
+    __syncthreads();
+    // element (j, tid) goes after all of group j' < j and warps w < wid of group j
+    int before = 0, acc = 0;
+    const long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
 #pragma unroll
-    for (int j = 0; j < PER; j++) {
-      int tot;
-      const int ex = block_excl_scan<int>(f[j] ? 1 : 0, sm_warp, tot);
-      if (f[j]) {
-        const long long dst = dst0 + ex;
-        if (dst < g.kp_cap) {
-          const long long o = ob + dst, p = fb + c * PROP_CHUNK + j * 256 + tid;
-          b.fx[o] = xs[j]; b.fy[o] = ys[j]; b.fs[o] = b.fs[p]; b.ft[o] = b.ft[p]; b.fv[o] = b.fv[p];
-          b.forg[o] = 1; b.fage[o] = b.fage[p] + 1;
-          const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + p * 64);
-          uint4* dd = reinterpret_cast<uint4*>(b.fdesc + o * 64);
-          const uint4 d0 = sd[0], d1 = sd[1], d2 = sd[2], d3 = sd[3];
-          dd[0] = d0; dd[1] = d1; dd[2] = d2; dd[3] = d3;
-        }
+    for (int j = 0; j < PROP_PER; j++) {
+      int inwarp = 0, grp = 0;
+#pragma unroll
+      for (int w = 0; w < 8; w++) {
+        const int v = wsum[j][w];
+        inwarp += w < wid ? v : 0;
+        grp += v;
       }
-      dst0 += tot;
+      before = acc + inwarp;
+      acc += grp;
+      const bool f = (fl >> j) & 1u;
+      const long long dst = dst0 + before + ((fl >> (4 + 6 * j)) & 0x3fu);
+      const bool w_ = f && dst < g.kp_cap;
+      dsts[j * 256 + tid] = w_ ? (int)dst : -1;
+      if (w_) {
+        const long long o = ob + dst;
+        b.fx[o] = xs[j]; b.fy[o] = ys[j]; b.fs[o] = ss[j]; b.ft[o] = ts[j]; b.fv[o] = vs[j];
+        b.forg[o] = 1; b.fage[o] = ag[j] + 1;
+      }
     }
+    __syncthreads();
+    // descriptors: 4 x 16 B per feature, word q = feature q / 4, part q % 4
+    const int nvalid = min(PROP_CHUNK, n_prev - base);
+    const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + (fb + base) * 64);
+    uint4* dstd = reinterpret_cast<uint4*>(b.fdesc + ob * 64);
+#pragma unroll
+    for (int half = 0; half < 2; half++) {
+      uint4 d[8];
+      int dq[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const int q = (half * 8 + i) * 256 + tid, f = q >> 2;
+        const int dst = f < nvalid ? dsts[f] : -1;
+        dq[i] = dst < 0 ? -1 : dst * 4 + (q & 3);
+        if (dst >= 0) d[i] = src[q];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (dq[i] >= 0) dstd[dq[i]] = d[i];
+    }
+    __syncthreads();
   }
 }
 
