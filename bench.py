@@ -443,7 +443,7 @@ def main():
         "pyramid": (wh * (1 + 0.918) + 2 * wh / 64.0) * f_loc * per_step,
         "fast": 2.0 * 1024 * diag["fast_tiles_active"],
         "nms": 1.0 * 1024 * diag["fast_tiles_active"] + 32.0 * det_loc * per_step,
-        "sat": 5.0 * 96 * 48 * diag["sat_tiles_built"],
+        "sat": 5.0 * 32 * 32 * diag["sat_tiles_built"],   # read 1 B + write 4 B per pixel of a built 32x32 tile
         "describe": (32.0 + 109.0) * det_loc * per_step,
         "propagate": 218.0 * (tot_loc - det_loc) * per_step,
     }

@@ -140,11 +140,13 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.ptw = unit * std::max(1, 96 / unit);
   g.pth = unit * std::max(1, 48 / unit);
   g.ptx = cdiv(g.W, g.ptw); g.pty = cdiv(g.H, g.pth);
-  g.sat_tiles = g.ptx * g.pty;
-  g.pth_magic = (unsigned)((0x100000000ULL + g.pth - 1) / g.pth);
-  // strip-SAT ring: <= 40 MB so it stays in the 126 MB L2 next to the step's other traffic
+  // strip-SAT tiles, independent of the pyramid tiles (ptw is a multiple of VF_ST)
+  g.stx = cdiv(g.W, VF_ST); g.sty = cdiv(g.H, VF_ST);
+  g.sat_tiles = g.stx * g.sty;
+  g.stw_words = cdiv(g.stx, 32);
+  g.sth_magic = (unsigned)((0x100000000ULL + VF_ST - 1) / VF_ST);
   g.sat_slots = c.max_streams;   // one strip-SAT slot per stream
-  if (g.ptx > 32 * 8) return VF_ERR_ARG;   // strip carries: <= 8 x 32 tile columns
+  if (g.ptw % VF_ST) return VF_ERR_ARG;
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
   g.prop_chunks = cdiv(g.kp_cap, 1024);
@@ -160,7 +162,7 @@ int pyramid_smem(const Geo& g)
     else { lw = g.ptw >> o; lh = g.pth >> o; }
     acc += (lw * lh + 15) & ~15;
   }
-  return acc + g.pth * 4;   // + row-sum accumulators
+  return acc + g.pth * (g.ptw / VF_ST) * 4;   // + row-sum accumulators per SAT column
 }
 
 int g_num_sms = 0;
@@ -351,9 +353,9 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   int* dl = A.get<int>((size_t)g.lut_len);
   b.lut = dl;
   b.sat = A.get<uint32_t>((size_t)g.sat_slots * g.W * g.H);
-  b.rowsum = A.get<uint32_t>((size_t)S * g.H * g.ptx);
-  b.carry = A.get<uint32_t>((size_t)S * g.H * g.ptx);
-  b.sat_stamp = A.get<int>((size_t)S * g.sat_tiles);
+  b.rowsum = A.get<uint32_t>((size_t)S * g.H * g.stx);
+  b.carry = A.get<uint32_t>((size_t)S * g.H * g.stx);
+  b.sat_bits = A.get<unsigned>((size_t)S * g.sty * g.stw_words);
   b.sat_work = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_count = A.get<int>((size_t)S);
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
@@ -386,7 +388,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, fast_smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, 32 * FAST_WARPS, fast_smem);
   c->fast_grid = std::max(1, g_num_sms * std::max(occ, 1));
-  c->sat_smem = ((g.ptw * g.pth + 15) & ~15) + g.ptw * g.pth * 4 + (S + 1) * 4;
+  c->sat_smem = SAT_WARPS * VF_ST * SAT_PITCH * 4 + (S + 1) * 4;
   if (c->sat_smem > 48 * 1024) cudaFuncSetAttribute(k_sat, cudaFuncAttributeMaxDynamicSharedMemorySize, c->sat_smem);
   occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sat, 256, c->sat_smem);
@@ -504,7 +506,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   stage_mark(c, 2, st);
   const int tile_ctas = cdiv(g.L[2].tile_base, 256) + cdiv(g.tiles_per_stream - g.L[2].tile_base, 8);
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
-  const int carry_ctas = cdiv(g.pty, 8);
+  const int carry_ctas = cdiv(g.sty, 8);
   k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(
       g, b, tile_ctas, cov_ctas, carry_ctas);
   stage_mark(c, 3, st);
@@ -1049,7 +1051,7 @@ int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, co
   Bufs b = c->b;
   b.frames = frame_dev; b.frame_stride = 0; b.frame_pitch = pitch;
   k_pyramid<<<dim3(c->g.ptx, c->g.pty, 1), 256, c->pyr_smem, st>>>(c->g, b);
-  k_carries<<<dim3(c->g.pty, 1), 32, 0, st>>>(c->g, b);
+  k_carries<<<dim3(c->g.sty, 1), 32, 0, st>>>(c->g, b);
   int ctr0[C_NCTR] = {0};
   ctr0[C_NDET] = n;              // k_sat builds every tile of a stream with keypoints (unmasked)
   cudaMemcpyAsync(b.ctr, ctr0, sizeof(ctr0), cudaMemcpyHostToDevice, st);

@@ -36,6 +36,8 @@ enum {
 #define VF_ERRBIT_STAGING 2
 #define VF_ERRBIT_INDEX 4
 
+#define VF_ST 32   // strip-SAT tile edge and strip height (o0 pixels)
+
 struct LayerGeo {
   int w, h;
   int pitch;            // derived-layer / score-map pitch (bytes)
@@ -69,14 +71,16 @@ struct Geo {
   int tiles_per_stream, bands_per_stream;
   long long layer_slab, sm_slab, bm_slab_words, cell_slab, lut_len;
   // pyramid tiles (kernel k_pyramid), also the SAT tiles
-  int ptw, pth, ptx, pty;
+  int ptw, pth, ptx, pty;   // pyramid tiles (o0 pixels)
+  int stx, sty;             // strip-SAT tiles: VF_ST x VF_ST o0 pixels, stx x sty per frame
+  int stw_words;            // 32-bit words per tile row of the SAT-tile bitmap
   // IDDM state: octave levels kept for the next frame
   long long state_off[VF_MAXO]; long long state_slab;
   int kp_cap;           // feature capacity per stream and buffer
   int prop_chunks;      // CTAs reserved for propagation chunks
-  int sat_tiles;        // ptx * pty
-  unsigned pth_magic;
-  int sat_slots;        // strip-SAT ring size (streams), sized to stay in L2   // ceil(2^32 / pth): y / pth == umulhi(y, pth_magic) for y < 2^16
+  int sat_tiles;        // stx * sty
+  unsigned sth_magic;   // ceil(2^32 / VF_ST): y / VF_ST == umulhi(y, sth_magic) for y < 2^16
+  int sat_slots;        // strip-SAT ring size (streams)
   int nms_raw;          // stand-alone nms_and_refine: no border / merge filter
   int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
 };
@@ -101,9 +105,9 @@ struct Bufs {
   uint8_t* state;       // [S][state_slab]
   const int* lut;       // [lut_len] row/col -> cell maps (shared by all streams)
   uint32_t* sat;        // [sat_slots][W*H] strip SATs (ring over streams)
-  uint32_t* rowsum;     // [S][H][ptx] per-tile row sums of o0
-  uint32_t* carry;      // [S][H][ptx] strip carries K(y, tx) (see strip_sum)
-  int* sat_stamp;       // [S][sat_tiles] epoch at which the tile's L was written
+  uint32_t* rowsum;     // [S][H][stx] row sums of o0 per SAT-tile column
+  uint32_t* carry;      // [S][H][stx] strip carries K(y, tx) (see strip_carries)
+  unsigned* sat_bits;   // [S][sty][stw_words] SAT tiles marked this step (cleared by k_pyramid)
   int* sat_work; int* sat_count;   // [S][sat_tiles] / [S]: SAT tiles marked this step (masked frames)
   double* st_x; double* st_y; double* st_s; double* st_v;   // staging [S][kp_cap]
   // double-buffered features [S][2][kp_cap]

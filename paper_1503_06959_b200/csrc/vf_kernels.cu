@@ -50,128 +50,14 @@ __device__ __forceinline__ void lvl_dims(const Geo& g, int l, int& lw, int& lh)
 // ----------------------------------------------------------------------------
 // Summed-area tables for the descriptor's box means (descriptor.py:28-32,85-92).
 // The reference builds one (H+1) x (W+1) int64 SAT of the frame.  Here:
-//   L(y, x)  = sum of o0 over [Y0, y] x [X0, x] inside its ptw x pth tile
+//   L(y, x)  = sum of o0 over [Y0, y] x [X0, x] inside its VF_ST x VF_ST tile
 //   K(y, tx) = sum of o0 over [Y0, y] x [0, X0(tx))        (strip carry)
-// so S(y, x) = L + K is the SAT of the pth-row strip the pixel lies in, and a
-// box sum is 4 strip-SAT corners per strip it spans (<= 2 strips for O = 4).
+// so S(y, x) = L + K is the SAT of the VF_ST-row strip the pixel lies in, and
+// a box sum is 4 strip-SAT corners per strip it spans (<= 2 strips for box
+// radii < VF_ST / 2, i.e. sigma < ~9 with the default pattern).
 // All values < 2^32 and box sums are exact in uint32.
 // ----------------------------------------------------------------------------
-// Strip SAT of one tile into gs, from the o0 tile in smem (pitch ptw).
-// Warp w owns rows [w*RPW, (w+1)*RPW), lane l owns columns [l*CPL, (l+1)*CPL):
-// row prefixes by warp scan, column sums accumulated in registers down the
-// warp's rows, one smem exchange of the per-warp column totals, then
-// S(y, x) = column prefix + K(y, tx) stored straight from registers.
-// Needs ptw % 32 == 0, pth % 8 == 0, blockDim == 256 (true for O <= 7).
-template <int CPL>
-__device__ void sat_tile_reg(const Geo& g, const Bufs& b, int s, int tx, int ty, int tw, int th, const uint8_t* t0,
-                             uint32_t* xch, uint32_t* gs)
-{
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int RPW = g.pth >> 3;
-  const int X0 = tx * g.ptw, Y0 = ty * g.pth;
-  const int xb = lane * CPL;
-  uint32_t col[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; c++) col[c] = 0;
-  // pass 1: column totals of this warp's rows
-  for (int r = 0; r < RPW; r++) {
-    const int y = wid * RPW + r;
-    uint32_t v[CPL], run = 0;
-#pragma unroll
-    for (int c = 0; c < CPL; c++) { v[c] = (y < th && xb + c < tw) ? t0[y * g.ptw + xb + c] : 0u; run += v[c]; }
-    uint32_t inc = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    uint32_t pre = inc - run;
-#pragma unroll
-    for (int c = 0; c < CPL; c++) { pre += v[c]; col[c] += pre; }
-  }
-#pragma unroll
-  for (int c = 0; c < CPL; c++) xch[wid * 32 * CPL + xb + c] = col[c];
-  __syncthreads();
-  // offset of rows above this warp's block
-#pragma unroll
-  for (int c = 0; c < CPL; c++) {
-    uint32_t off = 0;
-    for (int w = 0; w < wid; w++) off += xch[w * 32 * CPL + xb + c];
-    col[c] = off;
-  }
-  // pass 2: recompute the row prefixes, accumulate, add the strip carry, store
-  const uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx + tx;
-  for (int r = 0; r < RPW; r++) {
-    const int y = wid * RPW + r;
-    if (y >= th) break;
-    uint32_t v[CPL], run = 0;
-#pragma unroll
-    for (int c = 0; c < CPL; c++) { v[c] = (xb + c < tw) ? t0[y * g.ptw + xb + c] : 0u; run += v[c]; }
-    uint32_t inc = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    uint32_t pre = inc - run;
-    const uint32_t k = __ldg(K + (long long)y * g.ptx);
-    uint32_t* dst = gs + (long long)(Y0 + y) * g.W + X0 + xb;
-#pragma unroll
-    for (int c = 0; c < CPL; c++) {
-      pre += v[c];
-      col[c] += pre;
-      if (xb + c < tw) dst[c] = col[c] + k;
-    }
-  }
-}
-
-__device__ void sat_tile(const Geo& g, const Bufs& b, int s, int tx, int ty, int tw, int th, const uint8_t* t0,
-                         uint32_t* ssat, uint32_t* gs)
-{
-  if (g.ptw == 96 && (g.pth & 7) == 0 && blockDim.x == 256) {
-    sat_tile_reg<3>(g, b, s, tx, ty, tw, th, t0, ssat, gs);
-    return;
-  }
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const int per = (g.ptw + 31) / 32;
-  const int X0 = tx * g.ptw, Y0 = ty * g.pth;
-  for (int y = wid; y < th; y += nw) {
-    uint32_t run = 0;
-    const int xb = lane * per;
-    for (int k = 0; k < per; k++) {
-      const int x = xb + k;
-      if (x < tw) run += t0[y * g.ptw + x];
-    }
-    uint32_t inc = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    uint32_t r = inc - run;
-    for (int k = 0; k < per; k++) {
-      const int x = xb + k;
-      if (x < tw) { r += t0[y * g.ptw + x]; ssat[y * g.ptw + x] = r; }
-    }
-  }
-  __syncthreads();
-  for (int x = tid; x < tw; x += nt) {
-    uint32_t run = 0;
-    for (int y = 0; y < th; y++) { run += ssat[y * g.ptw + x]; ssat[y * g.ptw + x] = run; }
-  }
-  __syncthreads();
-  // S(y, x) = L(y, x) + K(y, tx): the SAT of the pth-row strip
-  const uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx + tx;
-  for (int i = tid; i < th * tw; i += nt) {
-    const int y = i / tw, x = i - y * tw;
-    gs[(long long)(Y0 + y) * g.W + X0 + x] = ssat[y * g.ptw + x] + __ldg(K + (long long)y * g.ptx);
-  }
-}
-
-// Strip carries of strip ty of stream s: one warp, lanes over tile columns
-// (<= 8 chunks of 32 tile columns, i.e. frames up to 24576 px wide).
-#define VF_MAX_TX_CHUNKS 8
+// Strip carries of SAT strip ty of stream s: one warp, lanes over tile columns.
 __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
 {
   // K[y][t] = sum over rows y' <= y of the strip and tiles t' < t of the row
@@ -180,16 +66,16 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
   // chunk c + 1 through K[y][32(c+1)] (the value that slot takes anyway).
   // Row loads are issued RB at a time so the strip is not a chain of latencies.
   const int lane = threadIdx.x & 31;
-  const int Y0 = ty * g.pth, th = min(g.pth, g.H - Y0);
-  const uint32_t* rs = b.rowsum + ((long long)s * g.H + Y0) * g.ptx;
-  uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.ptx;
-  const int nch = (g.ptx + 31) / 32;
+  const int Y0 = ty * VF_ST, th = min(VF_ST, g.H - Y0);
+  const uint32_t* rs = b.rowsum + ((long long)s * g.H + Y0) * g.stx;
+  uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.stx;
+  const int nch = (g.stx + 31) / 32;
   constexpr int RB = 16;
 #pragma unroll 1
   for (int c = 0; c < nch; c++) {
     const int t = 32 * c + lane;
-    const bool in = t < g.ptx;
-    const bool hand = lane == 31 && t + 1 < g.ptx;
+    const bool in = t < g.stx;
+    const bool hand = lane == 31 && t + 1 < g.stx;
     uint32_t acc = 0;
 #pragma unroll 1
     for (int y0 = 0; y0 < th; y0 += RB) {
@@ -197,8 +83,8 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
 #pragma unroll
       for (int k = 0; k < RB; k++) {
         const bool r = y0 + k < th;
-        v[k] = (in && r) ? rs[(long long)(y0 + k) * g.ptx + t] : 0u;
-        left[k] = (c > 0 && r) ? K[(long long)(y0 + k) * g.ptx + 32 * c] : 0u;
+        v[k] = (in && r) ? rs[(long long)(y0 + k) * g.stx + t] : 0u;
+        left[k] = (c > 0 && r) ? K[(long long)(y0 + k) * g.stx + 32 * c] : 0u;
       }
 #pragma unroll
       for (int k = 0; k < RB; k++) {
@@ -210,8 +96,8 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
           if (lane >= o) inc += u;
         }
         if (y0 + k < th) {
-          if (in) K[(long long)(y0 + k) * g.ptx + t] = left[k] + inc - acc;
-          if (hand) K[(long long)(y0 + k) * g.ptx + t + 1] = left[k] + inc;
+          if (in) K[(long long)(y0 + k) * g.stx + t] = left[k] + inc - acc;
+          if (hand) K[(long long)(y0 + k) * g.stx + t + 1] = left[k] + inc;
         }
       }
     }
@@ -224,8 +110,8 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
 // start or left of column 0 are 0).
 __device__ __forceinline__ uint32_t box_sum(const uint32_t* S, const Geo& g, int x0, int x1, int y0, int y1)
 {
-  const int TH = g.pth;
-  int ys = (int)__umulhi((uint32_t)y0, (uint32_t)g.pth_magic) * TH;   // strip start of y0
+  const int TH = VF_ST;
+  int ys = (int)__umulhi((uint32_t)y0, (uint32_t)g.sth_magic) * TH;   // strip start of y0
   const bool left = x0 > 0;
   int yb = min(y1, ys + TH - 1);
   const uint32_t* rb = S + (long long)yb * g.W;
@@ -245,7 +131,8 @@ __device__ __forceinline__ uint32_t box_sum(const uint32_t* S, const Geo& g, int
 
 // o0 tile [X0, X0+ptw) x [Y0, Y0+pth) of stream s into smem (pitch ptw),
 // 16-byte loads when the frame rows allow it.
-// rowsum (nullable, zeroed smem [pth]) accumulates the tile's per-row sums.
+// rowsum (nullable, zeroed smem [pth][ptw / VF_ST]) accumulates the tile's
+// row sums per SAT-tile column.
 __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s, int X0, int Y0, int tw, int th,
                                              uint8_t* t0, uint32_t* rowsum = nullptr)
 {
@@ -263,7 +150,7 @@ __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s,
         a = __dp4a(v.y, 0x01010101u, a);
         a = __dp4a(v.z, 0x01010101u, a);
         a = __dp4a(v.w, 0x01010101u, a);
-        atomicAdd(rowsum + y, a);
+        atomicAdd(rowsum + y * (g.ptw / VF_ST) + (16 * c) / VF_ST, a);
       }
     }
   } else {
@@ -271,7 +158,7 @@ __device__ __forceinline__ void load_o0_tile(const Geo& g, const Bufs& b, int s,
       const int y = i / g.ptw, x = i - y * g.ptw;
       const uint8_t v = x < tw ? __ldg(src + (long long)y * b.frame_pitch + x) : 0;
       t0[i] = v;
-      if (rowsum && v) atomicAdd(rowsum + y, (uint32_t)v);
+      if (rowsum && v) atomicAdd(rowsum + y * (g.ptw / VF_ST) + x / VF_ST, (uint32_t)v);
     }
   }
 }
@@ -292,17 +179,21 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
     acc += (lw * lh + 15) & ~15;
   }
 
-  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
-    b.ctr[s * C_NCTR + C_STAGE] = 0;
-    b.sat_count[s] = 0;
-    b.work_count[s] = 0;
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    if (tid == 0) {
+      b.ctr[s * C_NCTR + C_STAGE] = 0;
+      b.sat_count[s] = 0;
+      b.work_count[s] = 0;
+    }
+    for (int i = tid; i < g.sty * g.stw_words; i += blockDim.x) b.sat_bits[(long long)s * g.sty * g.stw_words + i] = 0u;
   }
 
   // ---- load the o0 tile ------------------------------------------------------
   const int tw = min(g.ptw, g.W - X0), th = min(g.pth, g.H - Y0);
   uint8_t* t0 = smem + off[0];
-  uint32_t* rsum = reinterpret_cast<uint32_t*>(smem + acc);   // [pth] row sums of the tile
-  for (int y = tid; y < g.pth; y += nt) rsum[y] = 0;
+  uint32_t* rsum = reinterpret_cast<uint32_t*>(smem + acc);   // [pth][ptw / VF_ST] row sums
+  const int nseg = g.ptw / VF_ST;
+  for (int y = tid; y < g.pth * nseg; y += nt) rsum[y] = 0;
   __syncthreads();
   load_o0_tile(g, b, s, X0, Y0, tw, th, t0, rsum);
   __syncthreads();
@@ -461,7 +352,10 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
   // ---- summed-area data of the descriptor (descriptor.py:28-32) --------------
   // Per-row sums of this tile feed the strip carries (k_worklist); the strip
   // SATs themselves are built by k_sat for the tiles the descriptor reads.
-  for (int y = tid; y < th; y += nt) b.rowsum[((long long)s * g.H + Y0 + y) * g.ptx + blockIdx.x] = rsum[y];
+  for (int i = tid; i < th * nseg; i += nt) {
+    const int y = i / nseg, k = i - y * nseg, col = blockIdx.x * nseg + k;
+    if (col < g.stx) b.rowsum[((long long)s * g.H + Y0 + y) * g.stx + col] = rsum[i];
+  }
 }
 
 // Exclusive prefix over streams of a per-stream count, computed by the whole
@@ -485,15 +379,23 @@ __device__ __forceinline__ void stream_prefix(int n_streams, int* pre, int* sm_w
 // ============================================================================
 // k_sat: strip SATs for the descriptor.  Dense frames (no mask): every tile;
 // masked frames: the tiles kept keypoints' footprints touch (marked by k_nms).
-// Persistent CTAs over the per-stream tile lists, flattened.
+// Persistent CTAs, one warp per VF_ST x VF_ST tile, flattened over streams:
+//   lane r: row r of the tile (two 16-B loads), its running row prefix plus
+//           d(r) = K(r) - K(r-1) (the part of row r left of the tile), into a
+//           padded smem tile;
+//   lane x: column x accumulated down the rows = L(y, x) + K(y, tx), stored as
+//           one coalesced 128-B row segment per row.
 // ============================================================================
-__global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, const __grid_constant__ Bufs b, int n_streams)
+#define SAT_WARPS 8
+#define SAT_PITCH (VF_ST + 4)   // words; 16-B row stores of 8 lanes hit distinct banks
+__global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
+                                                        int n_streams)
 {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* t0 = smem;
-  uint32_t* ssat = reinterpret_cast<uint32_t*>(smem + ((g.ptw * g.pth + 15) & ~15));
-  int* pre = reinterpret_cast<int*>(ssat + g.ptw * g.pth);
+  uint32_t* tile = reinterpret_cast<uint32_t*>(smem) + (threadIdx.x >> 5) * VF_ST * SAT_PITCH;
+  int* pre = reinterpret_cast<int*>(smem + SAT_WARPS * VF_ST * SAT_PITCH * 4);
   __shared__ int sm_warp[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // detected rank -> staging slot map for k_desc_sample (thread per band)
   for (long long il = (long long)blockIdx.x * blockDim.x + threadIdx.x; il < (long long)n_streams * g.bands_per_stream;
        il += (long long)gridDim.x * blockDim.x) {
@@ -511,18 +413,59 @@ __global__ void __launch_bounds__(256) k_sat(const __grid_constant__ Geo g, cons
     return b.ctr[s * C_NCTR + C_NDET] == 0 ? 0 : (use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles);
   });
   const int n = pre[n_streams];
-  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+  for (int item = blockIdx.x * SAT_WARPS + wid; item < n; item += gridDim.x * SAT_WARPS) {
     int lo = 0, hi = n_streams;
     while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
     const int s = b.s0 + lo, i = item - pre[lo];
     const int t = use_mask(g, b, s) ? b.sat_work[(long long)s * g.sat_tiles + i] : i;
-    const int ty = t / g.ptx, tx = t - ty * g.ptx;
-    const int X0 = tx * g.ptw, Y0 = ty * g.pth;
-    const int tw = min(g.ptw, g.W - X0), th = min(g.pth, g.H - Y0);
-    load_o0_tile(g, b, s, X0, Y0, tw, th, t0);
-    __syncthreads();
-    sat_tile(g, b, s, tx, ty, tw, th, t0, ssat, b.sat + (long long)(s % g.sat_slots) * g.W * g.H);
-    __syncthreads();
+    const int ty = t / g.stx, tx = t - ty * g.stx;
+    const int X0 = tx * VF_ST, Y0 = ty * VF_ST;
+    const int tw = min(VF_ST, g.W - X0), th = min(VF_ST, g.H - Y0);
+    // ---- lane = row ----
+    const bool rin = lane < th;
+    const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)(Y0 + lane) * b.frame_pitch + X0;
+    const uint32_t kr = rin ? __ldg(b.carry + ((long long)s * g.H + Y0 + lane) * g.stx + tx) : 0u;
+    uint32_t w[8];
+    if (tw == VF_ST && ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch |
+                         (uintptr_t)b.frame_stride) & 15) == 0) {
+      uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+      if (rin) { v0 = __ldg(reinterpret_cast<const uint4*>(src)); v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1); }
+      w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w; w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          const int x = 4 * q + c;
+          if (rin && x < tw) v |= (uint32_t)src[x] << (8 * c);
+        }
+        w[q] = v;
+      }
+    }
+    const uint32_t kp = __shfl_up_sync(0xffffffffu, kr, 1);
+    uint32_t run = lane == 0 ? kr : kr - kp;   // d(r)
+    uint32_t* trow = tile + lane * SAT_PITCH;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      uint4 o;
+      run += w[q] & 0xff;         o.x = run;
+      run += (w[q] >> 8) & 0xff;  o.y = run;
+      run += (w[q] >> 16) & 0xff; o.z = run;
+      run += w[q] >> 24;          o.w = run;
+      *reinterpret_cast<uint4*>(trow + 4 * q) = o;
+    }
+    __syncwarp();
+    // ---- lane = column ----
+    uint32_t* dst = b.sat + (long long)(s % g.sat_slots) * g.W * g.H + (long long)Y0 * g.W + X0 + lane;
+    uint32_t col = 0;
+    const bool cin = lane < tw;
+#pragma unroll 8
+    for (int r = 0; r < th; r++) {
+      col += tile[r * SAT_PITCH + lane];
+      if (cin) dst[(long long)r * g.W] = col;
+    }
+    __syncwarp();
   }
 }
 
@@ -562,10 +505,13 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   __shared__ __align__(16) uint8_t so3[6 * 12 + 8];
   const int s = b.s0 + blockIdx.z, tid = threadIdx.x;
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
-    b.ctr[s * C_NCTR + C_STAGE] = 0;
-    b.sat_count[s] = 0;
-    b.work_count[s] = 0;
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    if (tid == 0) {
+      b.ctr[s * C_NCTR + C_STAGE] = 0;
+      b.sat_count[s] = 0;
+      b.work_count[s] = 0;
+    }
+    for (int i = tid; i < g.sty * g.stw_words; i += blockDim.x) b.sat_bits[(long long)s * g.sty * g.stw_words + i] = 0u;
   }
   const int tw = min(TW, g.W - X0), th = min(TH, g.H - Y0);
   // ---- o0 tile ----
@@ -628,13 +574,14 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
       store_word(gd, L2.pitch, y, 4 * q, L2.w - gx0, L2.h - gy0, w);
     }
   }
-  if (tid < th) {
-    // per-row sums of the tile (strip carries for the descriptor's SATs)
-    const uint32_t* row = reinterpret_cast<const uint32_t*>(t0 + tid * TW);
+  if (tid < 3 * th) {
+    // row sums per 32-px SAT column of the tile (strip carries of the SATs)
+    const int y = tid / 3, k = tid - 3 * y, col = 3 * blockIdx.x + k;
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(t0 + y * TW + VF_ST * k);
     uint32_t a = 0;
 #pragma unroll
-    for (int k = 0; k < TW / 4; k++) a = __dp4a(row[k], 0x01010101u, a);
-    b.rowsum[((long long)s * g.H + Y0 + tid) * g.ptx + blockIdx.x] = a;
+    for (int q = 0; q < VF_ST / 4; q++) a = __dp4a(row[q], 0x01010101u, a);
+    if (col < g.stx) b.rowsum[((long long)s * g.H + Y0 + y) * g.stx + col] = a;
   }
   __syncthreads();
   // ---- phase 2: i1 from i0, o2 from o1 ----
@@ -777,7 +724,7 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
   const int lane = threadIdx.x & 31;
   if ((int)blockIdx.x >= tile_ctas + cov_ctas && (int)blockIdx.x < tile_ctas + cov_ctas + carry_ctas) {
     const int ty = (blockIdx.x - tile_ctas - cov_ctas) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (ty < g.pty) strip_carries(g, b, s, ty);
+    if (ty < g.sty) strip_carries(g, b, s, ty);
     return;
   }
   if ((int)blockIdx.x >= tile_ctas + cov_ctas + carry_ctas) {
@@ -1303,19 +1250,47 @@ __device__ NmsOut nms_refine(const Geo& g, const Bufs& b, int s, int um, int l, 
 __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int s, double x, double y, double sg,
                                                int epoch)
 {
+  // footprint bound of the 60 boxes (|p| <= 10.8, radius <= 1.69 sigma): tile
+  // rows x column runs set in the stream's tile bitmap; bits newly set by this
+  // call append their tiles to the k_sat list.  The atomics of up to four
+  // (row, word) runs are issued before any result is used.
+  (void)epoch;
   const int F = (int)ceil(12.5 * sg) + 2;
   const int xi = (int)x, yi = (int)y;
   const int xa = max(0, xi - F), xb = min(g.W - 1, xi + F + 1);
   const int ya = max(0, yi - F), yb = min(g.H - 1, yi + F + 1);
-  for (int ty = ya / g.pth; ty <= yb / g.pth; ty++)
-    for (int tx = xa / g.ptw; tx <= xb / g.ptw; tx++) {
-      int* st = b.sat_stamp + (long long)s * g.sat_tiles + ty * g.ptx + tx;
-      if (*((volatile int*)st) == epoch) continue;
-      if (atomicExch(st, epoch) != epoch) {
-        const int pos = atomicAdd(b.sat_count + s, 1);
-        b.sat_work[(long long)s * g.sat_tiles + pos] = ty * g.ptx + tx;
+  const int txa = xa / VF_ST, txb = xb / VF_ST, tya = ya / VF_ST, tyb = yb / VF_ST;
+  const int wa = txa >> 5, wb = txb >> 5, nw = wb - wa + 1;
+  const int nrun = (tyb - tya + 1) * nw;
+  unsigned* bits = b.sat_bits + (long long)s * g.sty * g.stw_words;
+  for (int r0 = 0; r0 < nrun; r0 += 4) {
+    unsigned got[4], msk[4];
+    int tyv[4], wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      got[u] = 0xffffffffu; msk[u] = 0; tyv[u] = 0; wv[u] = 0;
+      const int r = r0 + u;
+      if (r < nrun) {
+        const int ty = tya + r / nw, w = wa + r % nw;
+        const int lo = max(txa, 32 * w) - 32 * w, hi = min(txb, 32 * w + 31) - 32 * w;
+        const unsigned m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+        tyv[u] = ty; wv[u] = w; msk[u] = m;
+        got[u] = atomicOr(bits + ty * g.stw_words + w, m);
       }
     }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      unsigned nb = msk[u] & ~got[u];
+      if (nb) {
+        int pos = atomicAdd(b.sat_count + s, __popc(nb));
+        while (nb) {
+          const int bit = __ffs(nb) - 1;
+          nb &= nb - 1;
+          b.sat_work[(long long)s * g.sat_tiles + pos++] = tyv[u] * g.stx + 32 * wv[u] + bit;
+        }
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
@@ -1559,11 +1534,11 @@ struct DescWarp {
 // Sample (keypoint, point) pairs into w.v: 4 pairs per lane per iteration,
 // every SAT corner load issued before any is consumed (branch-free: a masked
 // corner re-reads corner A and is multiplied by 0).  Boxes spanning three or
-// more strips (only when a box is taller than pth: O > 4) take box_sum.
+// more strips (boxes taller than VF_ST rows) take box_sum.
 __device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, int lane, bool rotated)
 {
   const int npair = nk * VF_NPTS;
-  const int TH = g.pth;
+  const int TH = VF_ST;
   for (int q0 = lane; q0 < npair; q0 += 128) {
     const uint32_t* rowp[4][3];
     int xa[4], xb[4], area[4], dst[4];
@@ -1591,7 +1566,7 @@ __device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, i
       const int r = (int)floor(c_rad[j] * sg + 0.5);
       const int x0 = max((int)x - r, 0), x1 = min((int)x + r, g.W - 1);
       const int y0 = max((int)y - r, 0), y1 = min((int)y + r, g.H - 1);
-      const int ys = (int)__umulhi((uint32_t)y0, g.pth_magic) * TH;
+      const int ys = (int)__umulhi((uint32_t)y0, g.sth_magic) * TH;
       const int yb = min(y1, ys + TH - 1);
       const bool left = x0 > 0, top = y0 > ys, cross = y1 > yb;
       slow[u] = y1 > ys + 2 * TH - 1;
@@ -1722,8 +1697,8 @@ __device__ __forceinline__ BoxQ box_query(const uint32_t* S, const Geo& g, doubl
   BoxQ q;
   q.x0 = max((int)x - r, 0); q.x1 = min((int)x + r, g.W - 1);
   q.y0 = max((int)y - r, 0); q.y1 = min((int)y + r, g.H - 1);
-  const int TH = g.pth;
-  const int ys = (int)__umulhi((uint32_t)q.y0, g.pth_magic) * TH;
+  const int TH = VF_ST;
+  const int ys = (int)__umulhi((uint32_t)q.y0, g.sth_magic) * TH;
   const int yb = min(q.y1, ys + TH - 1);
   q.L = q.x0 > 0; q.T = q.y0 > ys; q.C = q.y1 > yb;
   q.slow = q.y1 > ys + 2 * TH - 1;
@@ -1793,25 +1768,41 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
   __syncthreads();
   // this lane's two pattern points (lane, lane + 32; lanes 28-31 repeat their first)
   const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
-  for (int gi = blockIdx.x * DSW + wid; gi < total; gi += gridDim.x * DSW) {
-    const int sl = find_stream(pre, n_streams, gi), s = b.s0 + sl, i = gi - pre[sl];
-    const int cur = b.ctr[s * C_NCTR + C_FRAME] & 1;
-    const long long o = ((long long)s * 2 + cur) * g.kp_cap + i;
-    const uint32_t* S = b.sat + (long long)(s % g.sat_slots) * g.W * g.H;
-    double kx, ky, sg, cs = 1.0, sn = 0.0;
-    if (pass == 0) {
-      const long long si = (long long)s * g.kp_cap + __ldg(b.gidx + (long long)s * g.kp_cap + i);   // staging slot
-      kx = b.st_x[si]; ky = b.st_y[si]; sg = b.st_s[si];
-      if (lane == 0) {
-        b.fx[o] = kx; b.fy[o] = ky; b.fs[o] = sg; b.fv[o] = b.st_v[si];
-        b.forg[o] = 0; b.fage[o] = 0;
+  // The warp's keypoints are gi = g0 + k * Wt.  Their headers (position,
+  // scale, rotation, output slot) are fetched 32 at a time, lane k for
+  // keypoint k, so the per-keypoint loop only waits on its SAT corners.
+  const int Wt = gridDim.x * DSW;
+  for (int g0 = blockIdx.x * DSW + wid; g0 < total; g0 += 32 * Wt) {
+    const int gl = g0 + lane * Wt;
+    long long o_l = 0;
+    int s_l = 0;
+    double kx_l = 0.0, ky_l = 0.0, sg_l = 0.0, cs_l = 1.0, sn_l = 0.0;
+    if (gl < total) {
+      const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
+      s_l = b.s0 + sl;
+      const int cur = b.ctr[s_l * C_NCTR + C_FRAME] & 1;
+      o_l = ((long long)s_l * 2 + cur) * g.kp_cap + i;
+      if (pass == 0) {
+        const long long si = (long long)s_l * g.kp_cap + __ldg(b.gidx + (long long)s_l * g.kp_cap + i);   // staging slot
+        kx_l = b.st_x[si]; ky_l = b.st_y[si]; sg_l = b.st_s[si];
+        b.fx[o_l] = kx_l; b.fy[o_l] = ky_l; b.fs[o_l] = sg_l; b.fv[o_l] = b.st_v[si];
+        b.forg[o_l] = 0; b.fage[o_l] = 0;
+      } else {
+        kx_l = b.fx[o_l]; ky_l = b.fy[o_l]; sg_l = b.fs[o_l];
+        const double* park = reinterpret_cast<const double*>(b.fdesc + o_l * 64);   // from k_desc_orient
+        cs_l = park[0];
+        sn_l = park[1];
       }
-    } else {
-      kx = b.fx[o]; ky = b.fy[o]; sg = b.fs[o];
-      const double* park = reinterpret_cast<const double*>(b.fdesc + o * 64);   // from k_desc_orient
-      cs = park[0];
-      sn = park[1];
     }
+    const int nk = min(32, (total - g0 + Wt - 1) / Wt);
+#pragma unroll 1
+  for (int k = 0; k < nk; k++) {
+    const long long o = __shfl_sync(0xffffffffu, o_l, k);
+    const int s = __shfl_sync(0xffffffffu, s_l, k);
+    const double kx = __shfl_sync(0xffffffffu, kx_l, k), ky = __shfl_sync(0xffffffffu, ky_l, k);
+    const double sg = __shfl_sync(0xffffffffu, sg_l, k);
+    const double cs = __shfl_sync(0xffffffffu, cs_l, k), sn = __shfl_sync(0xffffffffu, sn_l, k);
+    const uint32_t* S = b.sat + (long long)(s % g.sat_slots) * g.W * g.H;
     uint32_t m0, m1;
     point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], pass != 0, m0, m1);
     uint8_t* v = vals[wid];
@@ -1833,6 +1824,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
       if (lane < 16) dst[lane] = __byte_perm(__brev(mine), 0, 0x0123);
     }
     __syncwarp();
+  }
   }
 }
 
@@ -1862,10 +1854,24 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
         uint32_t* d = reinterpret_cast<uint32_t*>(v + 16 * q);
         d[0] = w4.x; d[1] = w4.y; d[2] = w4.z; d[3] = w4.w;
       }
+      // exact int -> double without I2F: (2^52 + 2^51 + 2^31 + n) - (2^52 + 2^51 + 2^31)
+      auto i2d = [](int n) {
+        return __hiloint2double(0x43380000, (int)(0x80000000u + (unsigned)n)) - 6755401588539392.0;
+      };
       double gx = 0.0, gy = 0.0;
       const int L = c_nlong;
-      for (int p = 0; p < L; p++) {
-        const double dv = (double)((int)v[c_li[p]] - (int)v[c_lj[p]]);
+      int p = 0;
+#pragma unroll 1
+      for (; p + 4 <= L; p += 4) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const double dv = i2d((int)v[c_li[p + k]] - (int)v[c_lj[p + k]]);
+          gx += dv * c_wx[p + k];
+          gy += dv * c_wy[p + k];
+        }
+      }
+      for (; p < L; p++) {
+        const double dv = i2d((int)v[c_li[p]] - (int)v[c_lj[p]]);
         gx += dv * c_wx[p];
         gy += dv * c_wy[p];
       }
