@@ -10,6 +10,7 @@
 #include <cstring>
 #include <vector>
 #include <algorithm>
+#include <climits>
 
 #define VF_VERSION "vidfeat-b200 0.1.0 (sm_100a)"
 
@@ -146,6 +147,9 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.stw_words = cdiv(g.stx, 32);
   g.sth_magic = (unsigned)((0x100000000ULL + VF_ST - 1) / VF_ST);
   g.sat_slots = c.max_streams;   // one strip-SAT slot per stream
+  // bit-packed IDDM mask from k_pyramid4 (its geometry, default mask source)
+  g.use_cbits = g.mask_mode == 1 && !g.per_layer && g.mask_level == 3 && g.O == 4 && g.ptw == 96 && g.pth == 48;
+  g.cbits_words = g.use_cbits ? cdiv(g.grid[0].cols, 32) : 0;
   if (g.ptw % VF_ST) return VF_ERR_ARG;
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
@@ -349,6 +353,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.prop_cnt = A.get<int>((size_t)S * g.prop_chunks);
   b.prop_out = A.get<int>((size_t)S * g.prop_chunks);
   b.cells = A.get<uint8_t>((size_t)S * g.cell_slab);
+  b.cbits = g.use_cbits ? A.get<uint32_t>((size_t)S * 2 * g.grid[0].rows * g.cbits_words) : nullptr;
   b.state = A.get<uint8_t>((size_t)S * g.state_slab);
   int* dl = A.get<int>((size_t)g.lut_len);
   b.lut = dl;
@@ -499,12 +504,12 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     k_binmask<<<n, 1024, smem, st>>>(g, b);
   }
   stage_mark(c, 1, st);
-  if (g.O == 4 && g.ptw == 96 && g.pth == 48 && !(g.mask_mode == 1 && (g.per_layer || g.mask_level != 3)))
+  if (g.O == 4 && g.ptw == 96 && g.pth == 48 && !(g.mask_mode == 1 && !g.use_cbits))
     k_pyramid4<<<dim3(g.ptx, g.pty, n), 256, 0, st>>>(g, b);
   else
     k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
   stage_mark(c, 2, st);
-  const int tile_ctas = cdiv(g.L[2].tile_base, 256) + cdiv(g.tiles_per_stream - g.L[2].tile_base, 8);
+  const int tile_ctas = cdiv(g.tiles_per_stream, 256);   // lane per FAST tile
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
   const int carry_ctas = cdiv(g.sty, 8);
   k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(

@@ -74,6 +74,8 @@ struct Geo {
   int ptw, pth, ptx, pty;   // pyramid tiles (o0 pixels)
   int stx, sty;             // strip-SAT tiles: VF_ST x VF_ST o0 pixels, stx x sty per frame
   int stw_words;            // 32-bit words per tile row of the SAT-tile bitmap
+  int use_cbits;            // IDDM mask also emitted as bits by k_pyramid4 (grid 0)
+  int cbits_words;          // 32-bit words per cell row of the bit mask
   // IDDM state: octave levels kept for the next frame
   long long state_off[VF_MAXO]; long long state_slab;
   int kp_cap;           // feature capacity per stream and buffer
@@ -107,6 +109,7 @@ struct Bufs {
   uint32_t* sat;        // [sat_slots][W*H] strip SATs (ring over streams)
   uint32_t* rowsum;     // [S][H][stx] row sums of o0 per SAT-tile column
   uint32_t* carry;      // [S][H][stx] strip carries K(y, tx) (see strip_carries)
+  uint32_t* cbits;      // [S][2 (epoch parity)][rows][cbits_words] IDDM cells as bits
   unsigned* sat_bits;   // [S][sty][stw_words] SAT tiles marked this step (cleared by k_pyramid)
   int* sat_work; int* sat_count;   // [S][sat_tiles] / [S]: SAT tiles marked this step (masked frames)
   double* st_x; double* st_y; double* st_s; double* st_v;   // staging [S][kp_cap]

@@ -70,12 +70,16 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
   const uint32_t* rs = b.rowsum + ((long long)s * g.H + Y0) * g.stx;
   uint32_t* K = b.carry + ((long long)s * g.H + Y0) * g.stx;
   const int nch = (g.stx + 31) / 32;
+  const int P = g.stx;
   constexpr int RB = 16;
 #pragma unroll 1
   for (int c = 0; c < nch; c++) {
     const int t = 32 * c + lane;
-    const bool in = t < g.stx;
-    const bool hand = lane == 31 && t + 1 < g.stx;
+    const bool in = t < P;
+    const bool hand = lane == 31 && t + 1 < P;
+    const uint32_t* rsp = rs + (in ? t : 0);
+    const uint32_t* lp = K + 32 * c;
+    uint32_t* kp = K + t;
     uint32_t acc = 0;
 #pragma unroll 1
     for (int y0 = 0; y0 < th; y0 += RB) {
@@ -83,8 +87,9 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
 #pragma unroll
       for (int k = 0; k < RB; k++) {
         const bool r = y0 + k < th;
-        v[k] = (in && r) ? rs[(long long)(y0 + k) * g.stx + t] : 0u;
-        left[k] = (c > 0 && r) ? K[(long long)(y0 + k) * g.stx + 32 * c] : 0u;
+        const int off = (y0 + k) * P;
+        v[k] = (in && r) ? rsp[off] : 0u;
+        left[k] = (c > 0 && r) ? lp[off] : 0u;
       }
 #pragma unroll
       for (int k = 0; k < RB; k++) {
@@ -96,8 +101,9 @@ __device__ void strip_carries(const Geo& g, const Bufs& b, int s, int ty)
           if (lane >= o) inc += u;
         }
         if (y0 + k < th) {
-          if (in) K[(long long)(y0 + k) * g.stx + t] = left[k] + inc - acc;
-          if (hand) K[(long long)(y0 + k) * g.stx + t + 1] = left[k] + inc;
+          const int off = (y0 + k) * P;
+          if (in) kp[off] = left[k] + inc - acc;
+          if (hand) kp[off + 1] = left[k] + inc;
         }
       }
     }
@@ -512,6 +518,13 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
       b.work_count[s] = 0;
     }
     for (int i = tid; i < g.sty * g.stw_words; i += blockDim.x) b.sat_bits[(long long)s * g.sty * g.stw_words + i] = 0u;
+    if (g.use_cbits) {
+      // the other parity's bit mask, written by the next step (this step's
+      // other CTAs write parity epoch & 1)
+      const int nw = g.grid[0].rows * g.cbits_words;
+      uint32_t* nb = b.cbits + ((long long)s * 2 + ((stream_epoch(b, s) + 1) & 1)) * nw;
+      for (int i = tid; i < nw; i += blockDim.x) nb[i] = 0u;
+    }
   }
   const int tw = min(TW, g.W - X0), th = min(TH, g.H - Y0);
   // ---- o0 tile ----
@@ -636,6 +649,8 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     const int i = tid - 32;
     const LayerGeo& L = g.L[6];
     const int gx0 = X0 >> 3, gy0 = Y0 >> 3;
+    const bool um = use_mask(g, b, s);
+    int mybit = 0;
     if (i < 72) {
       const int y = i / 12, x = i - y * 12;
       if (gy0 + y < L.h && gx0 + x < L.w) {
@@ -643,11 +658,12 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
         const long long gi = (long long)(gy0 + y) * L.w + gx0 + x;
         uint8_t* st = b.state + (long long)s * g.state_slab + g.state_off[3];
         const int c = so3[y * 12 + x];
-        if (use_mask(g, b, s)) {
+        if (um) {
           int d = c - (int)st[gi];
           d = d < 0 ? -d : d;
           const int bit = (double)d > g.t_i;   // int16 diff vs float t_i, strict
           b.cells[(long long)s * g.cell_slab + G.cell_off + gi] = (uint8_t)bit;
+          mybit = bit;
           if (bit) {
             long long hy = g.H - (long long)(gy0 + y) * G.ch, hx = g.W - (long long)(gx0 + x) * G.cw;
             hy = hy < G.ch ? hy : G.ch;
@@ -661,6 +677,26 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) covered += __shfl_down_sync(0xffffffffu, covered, o);
     if ((tid & 31) == 0 && covered) atomicAdd(b.cov + s, covered);
+    if (g.use_cbits && um) {
+      // cells i = 32 (w - 1) + lane of this warp as bits: the pieces of tile
+      // rows (12 cells each) OR-ed into the stream's cell-row words
+      const unsigned bal = __ballot_sync(0xffffffffu, mybit);
+      const int lane = tid & 31, ibase = i - lane;
+      if (bal && lane < 4) {
+        const int y = ibase / 12 + lane;            // rows meeting this warp's 32 cells
+        const int a = max(12 * y, ibase), e = min(min(12 * y + 12, ibase + 32), 72);
+        if (a < e && gy0 + y < g.grid[0].rows) {
+          const uint32_t piece = (bal >> (a - ibase)) & ((1u << (e - a)) - 1u);
+          if (piece) {
+            const int gx = gx0 + (a - 12 * y), sh = gx & 31;
+            uint32_t* row = b.cbits + ((long long)s * 2 + (stream_epoch(b, s) & 1)) * g.grid[0].rows * g.cbits_words +
+                            (long long)(gy0 + y) * g.cbits_words + (gx >> 5);
+            atomicOr(row, piece << sh);
+            if (sh + (e - a) > 32) atomicOr(row + 1, piece >> (32 - sh));
+          }
+        }
+      }
+    }
   }
 }
 
@@ -769,92 +805,94 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     if (lane == 0 && cnt) atomicAdd(b.cov + s, cnt);
     return;
   }
-  // FAST tiles: lane per tile for layers 0-1 (small cell rectangles), warp
-  // per tile for coarser layers (a tile of o3 projects to 8 x 128 cells)
-  const int n_fine = g.L[2].tile_base;            // tiles of layers 0 and 1
-  const int lane_ctas = (n_fine + 255) / 256;
-  int tile;
-  bool warp_mode;
-  if ((int)blockIdx.x < lane_ctas) {
-    tile = blockIdx.x * 256 + threadIdx.x;
-    warp_mode = false;
-    if (tile >= n_fine) return;
-  } else {
-    tile = n_fine + (blockIdx.x - lane_ctas) * 8 + (threadIdx.x >> 5);
-    warp_mode = true;
-    if (tile >= g.tiles_per_stream) return;
-  }
-  int l = 0;
-  while (l + 1 < g.NL && tile >= g.L[l + 1].tile_base) l++;
-  const LayerGeo& Lg = g.L[l];
-  const int t = tile - Lg.tile_base;
-  const int ty = t / Lg.tiles_x, tx = t - ty * Lg.tiles_x;
-  int active = 1;
-  if (um) {
-    const int y0 = ty * VF_TILE_H, y1 = min(Lg.h, y0 + VF_TILE_H) - 1;
-    const int x0 = tx * VF_TILE_W, x1 = min(Lg.w, x0 + VF_TILE_W) - 1;
-    const int* lut = b.lut + Lg.rc_off;
-    const int r0 = __ldg(lut + y0), r1 = __ldg(lut + y1);
-    const int c0 = __ldg(lut + Lg.h + x0), c1 = __ldg(lut + Lg.h + x1);
-    const GridGeo& G = g.grid[grid_of_layer(g, l)];
-    const uint8_t* cells = b.cells + (long long)s * g.cell_slab + G.cell_off;
-    // any set cell in rows r0..r1, columns c0..c1: aligned 32-bit words (the
-    // cell slab is padded), partial words masked
-    const int nrow = r1 - r0 + 1;
-    const uintptr_t first = reinterpret_cast<uintptr_t>(cells + c0) & ~(uintptr_t)3;
-    const int nwd = (int)(((reinterpret_cast<uintptr_t>(cells + c1) & ~(uintptr_t)3) - first) / 4) + 1;
-    const int head = (int)(reinterpret_cast<uintptr_t>(cells + c0) & 3);
-    const int tail = (int)(reinterpret_cast<uintptr_t>(cells + c1) & 3);
-    auto word_any = [&](int r, int k) -> uint32_t {
-      const uint32_t* wp = reinterpret_cast<const uint32_t*>(first + (uintptr_t)r * G.cols) + k;
-      uint32_t v = *wp;
-      if (k == 0) v &= 0xffffffffu << (8 * head);
-      if (k == nwd - 1) v &= 0xffffffffu >> (8 * (3 - tail));
-      return v;
-    };
-    if (!warp_mode) {
-      // all words of the rectangle, four loads in flight (no early exit)
+  // ---- FAST-tile activity (detector.py:175-181, pipeline.py:104-117) -------
+  // Lane per tile: a tile is active when any cell its pixels project to is
+  // set.  The default IDDM mask is read as bits (k_pyramid4), other masks as
+  // bytes; the rectangle's words are loaded four at a time.
+  const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = tile < g.tiles_per_stream;
+  int l = 0, ty = 0;
+  bool active = false;
+  if (valid) {
+    while (l + 1 < g.NL && tile >= g.L[l + 1].tile_base) l++;
+    const LayerGeo& Lg = g.L[l];
+    const int t = tile - Lg.tile_base;
+    ty = t / Lg.tiles_x;
+    const int tx = t - ty * Lg.tiles_x;
+    active = true;
+    if (um) {
+      const int y0 = ty * VF_TILE_H, y1 = min(Lg.h, y0 + VF_TILE_H) - 1;
+      const int x0 = tx * VF_TILE_W, x1 = min(Lg.w, x0 + VF_TILE_W) - 1;
+      const int* lut = b.lut + Lg.rc_off;
+      const int r0 = __ldg(lut + y0), r1 = __ldg(lut + y1);
+      const int c0 = __ldg(lut + Lg.h + x0), c1 = __ldg(lut + Lg.h + x1);
+      const int nrow = r1 - r0 + 1;
       uint32_t any = 0;
-      const int n = nrow * nwd;
-      int r = r0, k = 0;
+      if (g.use_cbits) {
+        const GridGeo& G = g.grid[0];
+        const uint32_t* bits = b.cbits + ((long long)s * 2 + (epoch & 1)) * G.rows * g.cbits_words +
+                               (long long)r0 * g.cbits_words;
+        const int wa = c0 >> 5, nwd = (c1 >> 5) - wa + 1, n = nrow * nwd;
+        const uint32_t mh = 0xffffffffu << (c0 & 31), mt = 0xffffffffu >> (31 - (c1 & 31));
+        int r = 0, k = 0;
 #pragma unroll 1
-      for (int i = 0; i < n; i += 4) {
-        uint32_t w[4];
+        for (int i = 0; i < n; i += 4) {
+          uint32_t w[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          w[j] = i + j < n ? word_any(r, k) : 0u;
-          if (++k == nwd) { k = 0; r++; }
+          for (int j = 0; j < 4; j++) {
+            uint32_t v = 0;
+            if (i + j < n) {
+              v = __ldcg(bits + r * g.cbits_words + wa + k);
+              if (k == 0) v &= mh;
+              if (k == nwd - 1) v &= mt;
+            }
+            w[j] = v;
+            if (++k == nwd) { k = 0; r++; }
+          }
+          any |= w[0] | w[1] | w[2] | w[3];
         }
-        any |= w[0] | w[1] | w[2] | w[3];
+      } else {
+        const GridGeo& G = g.grid[grid_of_layer(g, l)];
+        const uint8_t* cells = b.cells + (long long)s * g.cell_slab + G.cell_off;
+        // aligned 32-bit words (the cell slab is padded), partial words masked
+        const uintptr_t first = reinterpret_cast<uintptr_t>(cells + c0) & ~(uintptr_t)3;
+        const int nwd = (int)(((reinterpret_cast<uintptr_t>(cells + c1) & ~(uintptr_t)3) - first) / 4) + 1;
+        const int head = (int)(reinterpret_cast<uintptr_t>(cells + c0) & 3);
+        const int tail = (int)(reinterpret_cast<uintptr_t>(cells + c1) & 3);
+        const int n = nrow * nwd;
+        int r = r0, k = 0;
+#pragma unroll 1
+        for (int i = 0; i < n; i += 4) {
+          uint32_t w[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            uint32_t v = 0;
+            if (i + j < n) {
+              v = *(reinterpret_cast<const uint32_t*>(first + (uintptr_t)r * G.cols) + k);
+              if (k == 0) v &= 0xffffffffu << (8 * head);
+              if (k == nwd - 1) v &= 0xffffffffu >> (8 * (3 - tail));
+            }
+            w[j] = v;
+            if (++k == nwd) { k = 0; r++; }
+          }
+          any |= w[0] | w[1] | w[2] | w[3];
+        }
       }
       active = any != 0;
-    } else {
-      int any = 0;
-      for (int i = lane; i < nrow * nwd && !any; i += 32) any = word_any(r0 + i / nwd, i % nwd) != 0;
-      active = __any_sync(0xffffffffu, any);
     }
-  }
-  if (warp_mode) {
-    if (lane == 0 && active) {
-      b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
-      b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
-      b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
-      b.worklist[(long long)s * g.tiles_per_stream + atomicAdd(b.work_count + s, 1)] = tile;
-    }
-    return;
   }
   if (active) {
+    const LayerGeo& Lg = g.L[l];
     b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
     b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
     b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
-    // warp-aggregated append to the work list
-    const unsigned m = __activemask();
-    const int leader = __ffs(m) - 1, rank = __popc(m & ((1u << lane) - 1));
-    int pos = 0;
-    if (lane == leader) pos = atomicAdd(b.work_count + s, __popc(m));
-    pos = __shfl_sync(m, pos, leader);
-    b.worklist[(long long)s * g.tiles_per_stream + pos + rank] = tile;
   }
+  // warp-aggregated append to the work list
+  const unsigned m = __ballot_sync(0xffffffffu, active);
+  int pos = 0;
+  if (lane == 0 && m) pos = atomicAdd(b.work_count + s, __popc(m));
+  pos = __shfl_sync(0xffffffffu, pos, 0);
+  if (active) b.worklist[(long long)s * g.tiles_per_stream + pos + __popc(m & ((1u << lane) - 1))] = tile;
 }
 
 // ============================================================================
