@@ -908,19 +908,34 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
 // uint8 (<= 254) plus a 1-bit candidate bitmap for the NMS.
 #define FT_ROWS (VF_TILE_H + 6)
 #define FT_COLS (VF_TILE_W + 32)
-__device__ __forceinline__ uint32_t arc_max_min9(const uint32_t w[4])
+// Exact FAST score of one pixel from its 16-pixel ring (detector.py:127-158):
+// with d_i = r_i - c, the best arc of 9 is max(max_arcs min9(r) - c,
+// c - min_arcs max9(r), 0) (saturating differences are monotone in r).  The
+// ring is held as 8 words of 16x2 lanes (r_2k, r_2k+1); sliding minima and
+// maxima of 9 use the native 3-input VIMNMX3.U16x2.
+__device__ __forceinline__ uint32_t pair_shift1(uint32_t a, uint32_t b) { return __byte_perm(a, b, 0x5432); }
+__device__ __forceinline__ int fast_best(const uint32_t w[8], int c)
 {
-  uint32_t m2[4], m4[4], m9[4];
+  uint32_t s1[8], mn3[8], mx3[8];
 #pragma unroll
-  for (int q = 0; q < 4; q++) m2[q] = __vminu4(w[q], __byte_perm(w[q], w[(q + 1) & 3], 0x4321));
+  for (int k = 0; k < 8; k++) s1[k] = pair_shift1(w[k], w[(k + 1) & 7]);
 #pragma unroll
-  for (int q = 0; q < 4; q++) m4[q] = __vminu4(m2[q], __byte_perm(m2[q], m2[(q + 1) & 3], 0x5432));
+  for (int k = 0; k < 8; k++) {
+    mn3[k] = __vimin3_u16x2(w[k], s1[k], w[(k + 1) & 7]);
+    mx3[k] = __vimax3_u16x2(w[k], s1[k], w[(k + 1) & 7]);
+  }
+  uint32_t mn9[8], mx9[8];
 #pragma unroll
-  for (int q = 0; q < 4; q++) m9[q] = __vminu4(__vminu4(m4[q], m4[(q + 1) & 3]), w[(q + 2) & 3]);
-  uint32_t m = __vmaxu4(__vmaxu4(m9[0], m9[1]), __vmaxu4(m9[2], m9[3]));
-  m = __vmaxu4(m, m >> 16);
-  m = __vmaxu4(m, m >> 8);
-  return m & 0xffu;
+  for (int k = 0; k < 8; k++) {
+    mn9[k] = __vimin3_u16x2(mn3[k], pair_shift1(mn3[(k + 1) & 7], mn3[(k + 2) & 7]), mn3[(k + 3) & 7]);
+    mx9[k] = __vimax3_u16x2(mx3[k], pair_shift1(mx3[(k + 1) & 7], mx3[(k + 2) & 7]), mx3[(k + 3) & 7]);
+  }
+  uint32_t hi = __vimax3_u16x2(__vimax3_u16x2(mn9[0], mn9[1], mn9[2]), __vimax3_u16x2(mn9[3], mn9[4], mn9[5]),
+                               __vimax3_u16x2(mn9[6], mn9[7], mn9[7]));
+  uint32_t lo = __vimin3_u16x2(__vimin3_u16x2(mx9[0], mx9[1], mx9[2]), __vimin3_u16x2(mx9[3], mx9[4], mx9[5]),
+                               __vimin3_u16x2(mx9[6], mx9[7], mx9[7]));
+  const int bmax = (int)max(hi & 0xffffu, hi >> 16), dmin = (int)min(lo & 0xffffu, lo >> 16);
+  return max(max(bmax - c, c - dmin), 0);
 }
 
 // Warp per tile (no block barriers): each warp stages its tile, runs the
@@ -997,11 +1012,14 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
     for (int i = lane; i < VF_TILE_H * VF_TILE_W / 16; i += 32)
       reinterpret_cast<uint4*>(&fw.sc[0][0])[i] = make_uint4(0, 0, 0, 0);
     __syncwarp();
-    // ---- pass 1: 4-point necessary test, 4 pixels per word ----
+    // ---- pass 1: exact 4-point necessary test (detector.py:117-125) ----
+    // 16x2 lanes: N + 512 - C - (t+1) has bit 9 set iff N > C + t (bright),
+    // C + 512 - (t+1) - N iff N < C - t (dark); no borrow crosses a lane.
+    const uint32_t T1 = (uint32_t)(t + 1) * 0x00010001u, BIAS = 0x02000200u;
     int qn = 0;
     for (int r = 0; r < VF_TILE_H; r++) {
       const int y = y0 + r, k = lane;       // word k of row r: pixels x0 + 4k .. +3
-      uint32_t pass = 0;
+      uint32_t pass = 0;                    // bit 8i + 7: pixel i passes
       if (y >= 3 && y < h - 3) {
         const int cb = 16 + 4 * k;
         const uint32_t C = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb]);
@@ -1009,24 +1027,40 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
         const uint32_t B = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb + 4]);
         const uint32_t N = *reinterpret_cast<const uint32_t*>(&fw.tile[r][cb]);
         const uint32_t S = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 6][cb]);
-        const uint32_t E = __byte_perm(C, B, 0x6543), Wd = __byte_perm(P, C, 0x4321);
-        const uint32_t br = (__vcmpgtu4(__vsubus4(N, C), tt) | __vcmpgtu4(__vsubus4(S, C), tt)) &
-                            (__vcmpgtu4(__vsubus4(E, C), tt) | __vcmpgtu4(__vsubus4(Wd, C), tt));
-        const uint32_t dk = (__vcmpgtu4(__vsubus4(C, N), tt) | __vcmpgtu4(__vsubus4(C, S), tt)) &
-                            (__vcmpgtu4(__vsubus4(C, E), tt) | __vcmpgtu4(__vsubus4(C, Wd), tt));
-        pass = br | dk;
+        const uint32_t E = __byte_perm(C, B, 0x6543), Wd = __byte_perm(P, C, 0x4321);   // x + 3, x - 3
+        uint32_t res[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const uint32_t sel = hh ? 0x4342u : 0x4140u;
+          const uint32_t c2 = __byte_perm(C, 0, sel), n2 = __byte_perm(N, 0, sel), s2 = __byte_perm(S, 0, sel);
+          const uint32_t e2 = __byte_perm(E, 0, sel), w2 = __byte_perm(Wd, 0, sel);
+          const uint32_t ct = c2 + T1, cb2 = c2 + BIAS - T1;
+          const uint32_t bN = n2 + BIAS - ct, bS = s2 + BIAS - ct, bE = e2 + BIAS - ct, bW = w2 + BIAS - ct;
+          const uint32_t dN = cb2 - n2, dS = cb2 - s2, dE = cb2 - e2, dW = cb2 - w2;
+          res[hh] = (((bN | bS) & (bE | bW)) | ((dN | dS) & (dE | dW))) & BIAS;
+        }
+        // bits 9 / 25 of res[0] = pixels 0 / 1, of res[1] = pixels 2 / 3 -> bit 8i + 7
+        pass = ((res[0] >> 2) & 0x80u) | ((res[0] >> 10) & 0x8000u) | ((res[1] << 14) & 0x800000u) |
+               ((res[1] << 6) & 0x80000000u);
         if (pass) {
           const uint8_t* crow = um ? cells + (long long)fw.rc[r] * cols : nullptr;
+          uint32_t gate = 0xffffffffu;
+          if (um) {
+            uint32_t gv[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) gv[i] = (pass >> (8 * i + 7)) & 1u ? crow[fw.cc[4 * k + i]] : 0u;
+            gate = (gv[0] ? 0xffu : 0u) | (gv[1] ? 0xff00u : 0u) | (gv[2] ? 0xff0000u : 0u) | (gv[3] ? 0xff000000u : 0u);
+          }
+          uint32_t inb = 0;
 #pragma unroll
           for (int i = 0; i < 4; i++) {
-            const int xl = 4 * k + i, x = x0 + xl;
-            bool ok = x >= 3 && x < w - 3;
-            if (ok && um) ok = crow[fw.cc[xl]] != 0;   // gate (detector.py:175-181)
-            if (!ok) pass &= ~(0xffu << (8 * i));
+            const int x = x0 + 4 * k + i;
+            inb |= (x >= 3 && x < w - 3) ? (0xffu << (8 * i)) : 0u;
           }
+          pass &= gate & inb;
         }
       }
-      const int np = __popc(pass) >> 3;
+      const int np = __popc(pass);
       int incl = np;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1036,7 +1070,7 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       int pos = qn + incl - np;
 #pragma unroll
       for (int i = 0; i < 4; i++)
-        if (pass & (0xffu << (8 * i))) fw.queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + i);
+        if (pass & (0x80u << (8 * i))) fw.queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + i);
       qn += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
@@ -1045,18 +1079,19 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       const int p = fw.queue[qi];
       const int r = p / VF_TILE_W, c = p - r * VF_TILE_W;
       const int R = r + 3, Cc = 16 + c;
-      const uint32_t ctr = fw.tile[R][Cc];
-      uint32_t ring[4];
-      ring[0] = fw.tile[R - 3][Cc] | (fw.tile[R - 3][Cc + 1] << 8) | (fw.tile[R - 2][Cc + 2] << 16) | (fw.tile[R - 1][Cc + 3] << 24);
-      ring[1] = fw.tile[R][Cc + 3] | (fw.tile[R + 1][Cc + 3] << 8) | (fw.tile[R + 2][Cc + 2] << 16) | (fw.tile[R + 3][Cc + 1] << 24);
-      ring[2] = fw.tile[R + 3][Cc] | (fw.tile[R + 3][Cc - 1] << 8) | (fw.tile[R + 2][Cc - 2] << 16) | (fw.tile[R + 1][Cc - 3] << 24);
-      ring[3] = fw.tile[R][Cc - 3] | (fw.tile[R - 1][Cc - 3] << 8) | (fw.tile[R - 2][Cc - 2] << 16) | (fw.tile[R - 3][Cc - 1] << 24);
-      const uint32_t c4 = ctr * 0x01010101u;
-      uint32_t bw[4], dw[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) { bw[q] = __vsubus4(ring[q], c4); dw[q] = __vsubus4(c4, ring[q]); }
-      const int best = (int)max(arc_max_min9(bw), arc_max_min9(dw));
-      const int score = best - 1;
+      // ring order of detector.py:34-40 (clockwise from north), as 16x2 pairs
+      const uint8_t* t0p = &fw.tile[0][0];
+      auto px = [&](int dy, int dx) { return (uint32_t)t0p[(R + dy) * FT_COLS + Cc + dx]; };
+      uint32_t wr[8];
+      wr[0] = px(-3, 0) | (px(-3, 1) << 16);
+      wr[1] = px(-2, 2) | (px(-1, 3) << 16);
+      wr[2] = px(0, 3) | (px(1, 3) << 16);
+      wr[3] = px(2, 2) | (px(3, 1) << 16);
+      wr[4] = px(3, 0) | (px(3, -1) << 16);
+      wr[5] = px(2, -2) | (px(1, -3) << 16);
+      wr[6] = px(0, -3) | (px(-1, -3) << 16);
+      wr[7] = px(-2, -2) | (px(-3, -1) << 16);
+      const int score = fast_best(wr, (int)px(0, 0)) - 1;
       if (score >= t) fw.sc[r][c] = (uint8_t)score;
     }
     __syncwarp();
