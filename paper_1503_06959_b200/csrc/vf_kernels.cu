@@ -960,7 +960,6 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
   stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.work_count[b.s0 + sl]; });
   const int n_work = pre[n_streams];
   const int t = g.threshold;
-  const uint32_t tt = (uint32_t)t * 0x01010101u;
   for (int item = blockIdx.x * FAST_WARPS + wid; item < n_work; item += gridDim.x * FAST_WARPS) {
     int lo = 0, hi = n_streams;
     while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
