@@ -89,6 +89,7 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
     L.pitch = (int)align_up(L.w, 16);
     L.scale = sc[l];
     L.sigma = 1.0 / sc[l];
+    L.rinv_h = 1.0 / L.h; L.rinv_w = 1.0 / L.w;
     L.tiles_x = cdiv(L.w, VF_TILE_W); L.tiles_y = cdiv(L.h, VF_TILE_H);
     L.tile_base = tb; tb += L.tiles_x * L.tiles_y;
     L.band_base = bb; bb += L.tiles_y;
@@ -946,6 +947,7 @@ int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, c
   g.W = mask_dev ? mw : w; g.H = mask_dev ? mh : h; g.O = 1; g.NL = 1; g.threshold = t;
   LayerGeo& L = g.L[0];
   L.w = w; L.h = h; L.pitch = (int)align_up(w, 16); L.scale = 1.0; L.sigma = 1.0;
+  L.rinv_h = 1.0 / h; L.rinv_w = 1.0 / w;
   L.tiles_x = cdiv(w, VF_TILE_W); L.tiles_y = cdiv(h, VF_TILE_H); L.bm_words = cdiv(w, 32);
   g.tiles_per_stream = L.tiles_x * L.tiles_y; g.bands_per_stream = L.tiles_y;
   g.sm_slab = align_up((long long)L.pitch * h + 16, 256); g.bm_slab_words = (long long)L.bm_words * h;

@@ -50,6 +50,7 @@ struct LayerGeo {
   long long bm_off;     // word offset of the bitmap in the bitmap slab
   int rc_off, cc_off;   // offsets of the row/col -> cell LUTs (per grid, see Geo)
   double scale, sigma;  // pyramid.py:122-124; detector.py:243
+  double rinv_h, rinv_w;  // 1 / h, 1 / w (exact integer division by h, w)
 };
 
 struct GridGeo {          // a cell grid of the detection mask (masking.py:30-55)

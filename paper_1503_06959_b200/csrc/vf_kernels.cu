@@ -751,6 +751,7 @@ __global__ void __launch_bounds__(1024) k_binmask(const __grid_constant__ Geo g,
 // ============================================================================
 #define PROP_CHUNK 1024
 #define PROP_CTAS 16
+#define VF_CLEAR (1 << 30)   // work-list flag: zero the tile's scores and bitmap words
 __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
                                                    int tile_ctas, int cov_ctas, int carry_ctas)
 {
@@ -881,18 +882,29 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
       active = any != 0;
     }
   }
-  if (active) {
-    const LayerGeo& Lg = g.L[l];
-    b.tile_stamp[(long long)s * g.tiles_per_stream + tile] = epoch;
-    b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
-    b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
+  // Invariant: a tile not active this step holds zero scores and bitmap words,
+  // so k_nms reads maps without activity checks.  A tile active last step but
+  // not now becomes a clear item (tile | VF_CLEAR) that k_fast zeroes.
+  bool clear = false;
+  if (valid) {
+    int* st = b.tile_stamp + (long long)s * g.tiles_per_stream + tile;
+    if (active) {
+      const LayerGeo& Lg = g.L[l];
+      *st = epoch;
+      b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
+      b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
+    } else {
+      clear = *st == epoch - 1;
+    }
   }
   // warp-aggregated append to the work list
-  const unsigned m = __ballot_sync(0xffffffffu, active);
+  const bool item = active || clear;
+  const unsigned m = __ballot_sync(0xffffffffu, item);
   int pos = 0;
   if (lane == 0 && m) pos = atomicAdd(b.work_count + s, __popc(m));
   pos = __shfl_sync(0xffffffffu, pos, 0);
-  if (active) b.worklist[(long long)s * g.tiles_per_stream + pos + __popc(m & ((1u << lane) - 1))] = tile;
+  if (item)
+    b.worklist[(long long)s * g.tiles_per_stream + pos + __popc(m & ((1u << lane) - 1))] = tile | (clear ? VF_CLEAR : 0);
 }
 
 // ============================================================================
@@ -964,7 +976,9 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
     int lo = 0, hi = n_streams;
     while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
     const int s = b.s0 + lo;
-    const int tile_id = b.worklist[(long long)s * g.tiles_per_stream + (item - pre[lo])];
+    const int witem = b.worklist[(long long)s * g.tiles_per_stream + (item - pre[lo])];
+    const bool clear_only = (witem & VF_CLEAR) != 0;
+    const int tile_id = witem & (VF_CLEAR - 1);
     int l = 0;
     while (l + 1 < g.NL && tile_id >= g.L[l + 1].tile_base) l++;
     const LayerGeo& Lg = g.L[l];
@@ -974,6 +988,9 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
     const int w = Lg.w, h = Lg.h;
     int pitch;
     const uint8_t* lp = layer_ptr(g, b, s, l, pitch);
+    for (int i = lane; i < VF_TILE_H * VF_TILE_W / 16; i += 32)
+      reinterpret_cast<uint4*>(&fw.sc[0][0])[i] = make_uint4(0, 0, 0, 0);
+    if (!clear_only) {
     const int um = use_mask(g, b, s);
     const uint8_t* cells = nullptr;
     int cols = 0;
@@ -1008,8 +1025,6 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       }
       *reinterpret_cast<uint4*>(&fw.tile[rr][16 * c16]) = v;
     }
-    for (int i = lane; i < VF_TILE_H * VF_TILE_W / 16; i += 32)
-      reinterpret_cast<uint4*>(&fw.sc[0][0])[i] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     // ---- pass 1: exact 4-point necessary test (detector.py:117-125) ----
     // 16x2 lanes: N + 512 - C - (t+1) has bit 9 set iff N > C + t (bright),
@@ -1094,6 +1109,8 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       if (score >= t) fw.sc[r][c] = (uint8_t)score;
     }
     __syncwarp();
+    }
+    __syncwarp();
     // ---- store scores (whole tile: gated pixels read back as 0) + bitmap ----
     uint8_t* smap = b.scores + (long long)s * g.sm_slab + Lg.sm_off;
     for (int i = lane; i < VF_TILE_H * (VF_TILE_W / 16); i += 32) {
@@ -1142,23 +1159,28 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
 
 // Score of layer l at (y, x); 0 outside the layer.  Gated pixels score 0
 // (detector.py:112-114): k_fast stores whole active tiles with 0 at gated
-// pixels, and a tile is active iff one of its pixels is gated on, so a pixel
-// reads 0 unless its tile was stamped active this step (um == 0: all active).
+// pixels, and tiles not active this step hold zeros (cleared by k_fast when
+// they stop being active), so a map read needs no activity check.  Branch-free:
+// the load uses a clamped in-bounds address, so a caller's reads overlap.
 __device__ __forceinline__ int score_read(const Geo& g, const Bufs& b, int s, int um, int l, int y, int x)
 {
-  // branch-free (um is warp-uniform): the score and the tile stamp are loaded
-  // unconditionally from a clamped in-bounds address and then selected, so a
-  // caller's reads can all be in flight at once
+  (void)um;
   const LayerGeo& Lg = g.L[l];
   const bool in = (unsigned)y < (unsigned)Lg.h && (unsigned)x < (unsigned)Lg.w;
-  const int yc = in ? y : 0, xc = in ? x : 0;
-  const int v = __ldg(b.scores + (long long)s * g.sm_slab + Lg.sm_off + (long long)yc * Lg.pitch + xc);
-  bool ok = in;
-  if (um) {
-    const int tile = Lg.tile_base + (yc / VF_TILE_H) * Lg.tiles_x + xc / VF_TILE_W;
-    ok = ok && __ldg(b.tile_stamp + (long long)s * g.tiles_per_stream + tile) == um;
-  }
-  return ok ? v : 0;
+  const int off = in ? y * Lg.pitch + x : 0;
+  const int v = __ldg(b.scores + (long long)s * g.sm_slab + Lg.sm_off + off);
+  return in ? v : 0;
+}
+
+// floor((n + d / 2) / d) for 0 <= n < 2^40 (detector.py:266-269 rounding of
+// the projected coordinate), exact: fp64 reciprocal estimate, one correction.
+__device__ __forceinline__ int round_div(int y, int num, int d, double rd)
+{
+  const long long n = (long long)y * num + (d >> 1);
+  long long q = (long long)((double)n * rd);
+  if (q * d > n) q--;
+  else if ((q + 1) * d <= n) q++;
+  return (int)q;
 }
 
 __device__ __forceinline__ void fit_peak(const double p[3][3], double& ox, double& oy, double& val, int& okp)
@@ -1228,10 +1250,9 @@ __device__ __forceinline__ bool nms_test(const Geo& g, const Bufs& b, int s, int
     if (!has[k]) continue;
     const int j = l - 1 + 2 * k;
     const int hj = g.L[j].h, wj = g.L[j].w;
-    const long long a = ((long long)y * hj + (Lg.h >> 1)) / Lg.h;
-    const long long c = ((long long)x * wj + (Lg.w >> 1)) / Lg.w;
-    yj[k] = (int)(a < hj - 1 ? a : hj - 1);
-    xj[k] = (int)(c < wj - 1 ? c : wj - 1);
+    const int a = round_div(y, hj, Lg.h, Lg.rinv_h), c = round_div(x, wj, Lg.w, Lg.rinv_w);
+    yj[k] = a < hj - 1 ? a : hj - 1;
+    xj[k] = c < wj - 1 ? c : wj - 1;
     cj[k] = score_read(g, b, s, um, j, yj[k], xj[k]);
   }
   bool keep = sv > 0;
@@ -1255,10 +1276,9 @@ __device__ NmsOut nms_refine(const Geo& g, const Bufs& b, int s, int um, int l, 
     if (!has[k]) continue;
     const int j = l - 1 + 2 * k;
     const int hj = g.L[j].h, wj = g.L[j].w;
-    const long long a = ((long long)y * hj + (Lg.h >> 1)) / Lg.h;
-    const long long c = ((long long)x * wj + (Lg.w >> 1)) / Lg.w;
-    yj[k] = (int)(a < hj - 1 ? a : hj - 1);
-    xj[k] = (int)(c < wj - 1 ? c : wj - 1);
+    const int a = round_div(y, hj, Lg.h, Lg.rinv_h), c = round_div(x, wj, Lg.w, Lg.rinv_w);
+    yj[k] = a < hj - 1 ? a : hj - 1;
+    xj[k] = c < wj - 1 ? c : wj - 1;
   }
   // batch 2: the three 3x3 patches (zero-padded maps, detector.py:231-236)
   int pv[3][9];
@@ -1289,9 +1309,10 @@ __device__ NmsOut nms_refine(const Geo& g, const Bufs& b, int s, int um, int l, 
     delta = fabs(delta) < 1.0 ? delta : 0.0;
     const double up = g.L[l + 1].sigma / Lg.sigma;
     const double down = g.L[l - 1].sigma / Lg.sigma;
-    const double a = delta > 0.0 ? delta : 0.0;
-    const double c = -delta > 0.0 ? -delta : 0.0;
-    sig = Lg.sigma * pow(up, a) * pow(down, c);
+    // sigma_i * up^a * down^c with a = max(delta, 0), c = max(-delta, 0): one
+    // factor is x^0 = 1 exactly, so one pow gives the same product
+    const double f = pow(delta > 0.0 ? up : down, fabs(delta));
+    sig = delta > 0.0 ? Lg.sigma * f * 1.0 : Lg.sigma * 1.0 * f;
   }
   // detector.py:299-302; dividing by an octave scale 2^-o is exactly x * 2^o
   double xf, yf;
@@ -1460,20 +1481,11 @@ __global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ 
     const int y0 = ty * VF_TILE_H, nrows = min(Lg.h - y0, VF_TILE_H);
     const int nwords = nrows * Lg.bm_words;
     const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)y0 * Lg.bm_words;
-    const int* tst = b.tile_stamp + (long long)s * g.tiles_per_stream + Lg.tile_base + ty * Lg.tiles_x;
     const int per = (nwords + 31) / 32;
     const int w0 = lane * per, w1 = min(nwords, w0 + per);
     const int bmw = Lg.bm_words;
     int cnt = 0;
-    {
-      int k = w0 % bmw;                     // word column, advanced incrementally
-      int stamp_ok = 1;
-      for (int i = w0; i < w1; i++) {
-        if (um && (i == w0 || (k & (VF_TILE_WORDS - 1)) == 0)) stamp_ok = __ldg(tst + k / VF_TILE_WORDS) == epoch;
-        if (stamp_ok) cnt += __popc(__ldg(bm + i));
-        if (++k == bmw) k = 0;
-      }
-    }
+    for (int i = w0; i < w1; i++) cnt += __popc(__ldg(bm + i));   // inactive tiles hold zero words
     int total;
     const int ex = warp_excl_scan(cnt, lane, total);
     if (total > 0) {
@@ -1485,9 +1497,7 @@ __global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ 
       base = __shfl_sync(0xffffffffu, bs, 0);
       if (base >= 0) {
         int crow = w0 / bmw, ck = w0 - crow * bmw;   // row / column of the cursor word
-        auto load_word = [&]() -> uint32_t {
-          return (!um || __ldg(tst + ck / VF_TILE_WORDS) == epoch) ? __ldg(bm + crow * bmw + ck) : 0u;
-        };
+        auto load_word = [&]() -> uint32_t { return __ldg(bm + crow * bmw + ck); };
         int cursor = w0, idx = ex;             // this lane's enumeration state
         int qn = 0;                            // survivors queued (warp-uniform)
         uint32_t pend = cursor < w1 ? load_word() : 0u;
