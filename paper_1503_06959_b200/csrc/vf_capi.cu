@@ -147,7 +147,6 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.sat_tiles = g.stx * g.sty;
   g.stw_words = cdiv(g.stx, 32);
   g.sth_magic = (unsigned)((0x100000000ULL + VF_ST - 1) / VF_ST);
-  g.sat_slots = c.max_streams;   // one strip-SAT slot per stream
   // bit-packed IDDM mask from k_pyramid4 (its geometry, default mask source)
   g.use_cbits = g.mask_mode == 1 && !g.per_layer && g.mask_level == 3 && g.O == 4 && g.ptw == 96 && g.pth == 48;
   g.cbits_words = g.use_cbits ? cdiv(g.grid[0].cols, 32) : 0;
@@ -358,7 +357,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.state = A.get<uint8_t>((size_t)S * g.state_slab);
   int* dl = A.get<int>((size_t)g.lut_len);
   b.lut = dl;
-  b.sat = A.get<uint32_t>((size_t)g.sat_slots * g.W * g.H);
+  b.sat = A.get<uint32_t>((size_t)S * g.W * g.H);   // one strip SAT per stream
   b.rowsum = A.get<uint32_t>((size_t)S * g.H * g.stx);
   b.carry = A.get<uint32_t>((size_t)S * g.H * g.stx);
   b.sat_bits = A.get<unsigned>((size_t)S * g.sty * g.stw_words);

@@ -83,7 +83,6 @@ struct Geo {
   int prop_chunks;      // CTAs reserved for propagation chunks
   int sat_tiles;        // stx * sty
   unsigned sth_magic;   // ceil(2^32 / VF_ST): y / VF_ST == umulhi(y, sth_magic) for y < 2^16
-  int sat_slots;        // strip-SAT ring size (streams)
   int nms_raw;          // stand-alone nms_and_refine: no border / merge filter
   int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
 };
@@ -107,7 +106,7 @@ struct Bufs {
   int* cell_row_stamp;  // [S][n_grids][max rows] "row has an active cell" stamps
   uint8_t* state;       // [S][state_slab]
   const int* lut;       // [lut_len] row/col -> cell maps (shared by all streams)
-  uint32_t* sat;        // [sat_slots][W*H] strip SATs (ring over streams)
+  uint32_t* sat;        // [max_streams][W*H] strip SATs
   uint32_t* rowsum;     // [S][H][stx] row sums of o0 per SAT-tile column
   uint32_t* carry;      // [S][H][stx] strip carries K(y, tx) (see strip_carries)
   uint32_t* cbits;      // [S][2 (epoch parity)][rows][cbits_words] IDDM cells as bits

@@ -121,16 +121,16 @@ __device__ __forceinline__ uint32_t box_sum(const uint32_t* S, const Geo& g, int
   const bool left = x0 > 0;
   int yb = min(y1, ys + TH - 1);
   const uint32_t* rb = S + (long long)yb * g.W;
-  uint32_t sum = __ldca(rb + x1) - (left ? __ldca(rb + x0 - 1) : 0u);
+  uint32_t sum = __ldg(rb + x1) - (left ? __ldg(rb + x0 - 1) : 0u);
   if (y0 > ys) {
     const uint32_t* ra = S + (long long)(y0 - 1) * g.W;
-    sum -= __ldca(ra + x1) - (left ? __ldca(ra + x0 - 1) : 0u);
+    sum -= __ldg(ra + x1) - (left ? __ldg(ra + x0 - 1) : 0u);
   }
   while (yb < y1) {                 // next strip(s): rows start at the strip top
     ys += TH;
     yb = min(y1, ys + TH - 1);
     const uint32_t* r2 = S + (long long)yb * g.W;
-    sum += __ldca(r2 + x1) - (left ? __ldca(r2 + x0 - 1) : 0u);
+    sum += __ldg(r2 + x1) - (left ? __ldg(r2 + x0 - 1) : 0u);
   }
   return sum;
 }
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
     }
     __syncwarp();
     // ---- lane = column ----
-    uint32_t* dst = b.sat + (long long)(s % g.sat_slots) * g.W * g.H + (long long)Y0 * g.W + X0 + lane;
+    uint32_t* dst = b.sat + (long long)s * g.W * g.H + (long long)Y0 * g.W + X0 + lane;
     uint32_t col = 0;
     const bool cin = lane < tw;
 #pragma unroll 8
@@ -1772,13 +1772,14 @@ __device__ __forceinline__ BoxQ box_query(const uint32_t* S, const Geo& g, doubl
     fx = kx + sg * px + 0.5;
     fy = ky + sg * py + 0.5;
   }
-  long long x = (long long)floor(fx), y = (long long)floor(fy);
-  x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
-  y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
+  // clamp in fp64 (same as clamping the floored integer), then 32-bit ints
+  const double xd = fmin(fmax(floor(fx), 0.0), (double)(g.W - 1));
+  const double yd = fmin(fmax(floor(fy), 0.0), (double)(g.H - 1));
+  const int x = (int)xd, y = (int)yd;
   const int r = (int)floor(rad * sg + 0.5);
   BoxQ q;
-  q.x0 = max((int)x - r, 0); q.x1 = min((int)x + r, g.W - 1);
-  q.y0 = max((int)y - r, 0); q.y1 = min((int)y + r, g.H - 1);
+  q.x0 = max(x - r, 0); q.x1 = min(x + r, g.W - 1);
+  q.y0 = max(y - r, 0); q.y1 = min(y + r, g.H - 1);
   const int TH = VF_ST;
   const int ys = (int)__umulhi((uint32_t)q.y0, g.sth_magic) * TH;
   const int yb = min(q.y1, ys + TH - 1);
@@ -1810,14 +1811,18 @@ __device__ __forceinline__ void point_means2(const uint32_t* S, const Geo& g, do
 {
   const BoxQ a = box_query(S, g, kx, ky, sg, cs, sn, pa[0], pa[1], pa[2], rotated);
   const BoxQ c = box_query(S, g, kx, ky, sg, cs, sn, pb[0], pb[1], pb[2], rotated);
-  const uint32_t a0 = __ldca(a.r0 + a.xb), a1 = __ldca(a.r0 + a.xa), a2 = __ldca(a.r1 + a.xb), a3 = __ldca(a.r1 + a.xa);
-  const uint32_t a4 = __ldca(a.r2 + a.xb), a5 = __ldca(a.r2 + a.xa);
-  const uint32_t c0 = __ldca(c.r0 + c.xb), c1 = __ldca(c.r0 + c.xa), c2 = __ldca(c.r1 + c.xb), c3 = __ldca(c.r1 + c.xa);
-  const uint32_t c4 = __ldca(c.r2 + c.xb), c5 = __ldca(c.r2 + c.xa);
-  uint32_t sa = a0 - a.L * a1 - a.T * (a2 - a.L * a3) + a.C * (a4 - a.L * a5);
-  uint32_t sc = c0 - c.L * c1 - c.T * (c2 - c.L * c3) + c.C * (c4 - c.L * c5);
-  if (a.slow) sa = box_sum(S, g, a.x0, a.x1, a.y0, a.y1);   // box over >= 3 strips (O > 4 only)
-  if (c.slow) sc = box_sum(S, g, c.x0, c.x1, c.y0, c.y1);
+  // predicated corner loads: a corner the box does not use issues no request
+  auto ld = [](bool p, const uint32_t* q) -> uint32_t { return p ? __ldg(q) : 0u; };
+  const uint32_t a0 = __ldg(a.r0 + a.xb), a1 = ld(a.L, a.r0 + a.xa), a2 = ld(a.T, a.r1 + a.xb);
+  const uint32_t a3 = ld(a.T && a.L, a.r1 + a.xa), a4 = ld(a.C, a.r2 + a.xb), a5 = ld(a.C && a.L, a.r2 + a.xa);
+  const uint32_t c0 = __ldg(c.r0 + c.xb), c1 = ld(c.L, c.r0 + c.xa), c2 = ld(c.T, c.r1 + c.xb);
+  const uint32_t c3 = ld(c.T && c.L, c.r1 + c.xa), c4 = ld(c.C, c.r2 + c.xb), c5 = ld(c.C && c.L, c.r2 + c.xa);
+  uint32_t sa = a0 - a1 - (a2 - a3) + (a4 - a5);
+  uint32_t sc = c0 - c1 - (c2 - c3) + (c4 - c5);
+  if (__any_sync(0xffffffffu, a.slow || c.slow)) {   // a box over >= 3 strips (sigma >~ 9): rare
+    if (a.slow) sa = box_sum(S, g, a.x0, a.x1, a.y0, a.y1);
+    if (c.slow) sc = box_sum(S, g, c.x0, c.x1, c.y0, c.y1);
+  }
   ma = exact_div(sa, (uint32_t)a.area);
   mb = exact_div(sc, (uint32_t)c.area);
 }
@@ -1884,7 +1889,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
     const double kx = __shfl_sync(0xffffffffu, kx_l, k), ky = __shfl_sync(0xffffffffu, ky_l, k);
     const double sg = __shfl_sync(0xffffffffu, sg_l, k);
     const double cs = __shfl_sync(0xffffffffu, cs_l, k), sn = __shfl_sync(0xffffffffu, sn_l, k);
-    const uint32_t* S = b.sat + (long long)(s % g.sat_slots) * g.W * g.H;
+    const uint32_t* S = b.sat + (long long)s * g.W * g.H;
     uint32_t m0, m1;
     point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], pass != 0, m0, m1);
     uint8_t* v = vals[wid];
