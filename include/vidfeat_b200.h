@@ -40,6 +40,7 @@ extern "C" {
 #define VF_ERR_INDEX (-12)        /* numpy IndexError (nms_and_refine border candidate)          */
 #define VF_ERR_OCTAVE_KEY (-13)   /* KeyError: no octave layer at octave_for_mask (pyramid.py:61-63) */
 #define VF_ERR_PATTERN (-14)      /* sampling pattern not uploaded / malformed                   */
+#define VF_ERR_MATCH_CAPACITY (-15) /* radius_match output buffer too small (*n_matches = needed)  */
 
 #define VF_MODE_NONE 0
 #define VF_MODE_INTENSITY 1
@@ -181,6 +182,20 @@ int vf_upsample_mask(const uint8_t *bits_dev, int rows, int cols, int cell_w, in
 /* _mask_values (masking.py:157-165): mask bit under each rounded, clamped position. */
 int vf_mask_values(const uint8_t *full_dev, int W, int H, int n, const double *xs_dev,
                    const double *ys_dev, uint8_t *out_dev, void *stream);
+
+/* --- descriptor matching (matching.py:47-94) -------- */
+/* hamming_matrix (matching.py:73-77, _hamming_matrix_jit :56-66): out[i * ld + j]
+ * = popcount(q_i XOR r_j) over nbytes packed bytes (any nbytes >= 1; int32).
+ * q_dev: nq x nbytes, r_dev: nr x nbytes, row-major packed (np.packbits rows). */
+int vf_hamming_matrix(const uint8_t *q_dev, int64_t nq, const uint8_t *r_dev, int64_t nr, int nbytes,
+                      int32_t *out_dev, int64_t ld, void *stream);
+/* radius_match (matching.py:80-94): every (i, j) with Hamming distance <= t_m,
+ * in np.nonzero order (query-major, then reference), as three int32 arrays of
+ * capacity cap.  Synchronizes; *n_matches = number of matches.  If cap is too
+ * small returns VF_ERR_MATCH_CAPACITY with *n_matches = the required count. */
+int vf_radius_match(const uint8_t *q_dev, int64_t nq, const uint8_t *r_dev, int64_t nr, int nbytes, int t_m,
+                    int32_t *q_idx_dev, int32_t *r_idx_dev, int32_t *dist_dev, int64_t cap,
+                    int64_t *n_matches, void *stream);
 
 #ifdef __cplusplus
 }

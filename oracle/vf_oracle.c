@@ -675,3 +675,27 @@ void vfo_pipe_features(const vfo_pipe *p, double *x, double *y, double *sigma, d
     memcpy(theta, f->theta, 8 * n); memcpy(score, f->score, 8 * n);
     memcpy(origin, f->origin, n); memcpy(age, f->age, 4 * n); memcpy(desc, f->desc, 64 * n);
 }
+
+/* ------------------------------------------------------------------ */
+/* matching.py:22,47-66 -- Hamming distance of packed descriptor rows:  */
+/* sum over bytes of popcount(q XOR r) through the 256-entry LUT.       */
+/* ------------------------------------------------------------------ */
+void vfo_hamming_matrix(const uint8_t *q, long nq, const uint8_t *r, long nr, int nbytes, int32_t *out)
+{
+  static uint8_t lut[256];
+  static int ready = 0;
+  if (!ready) {
+    for (int i = 0; i < 256; i++) {
+      int c = 0;
+      for (int b = 0; b < 8; b++) c += (i >> b) & 1;
+      lut[i] = (uint8_t)c;
+    }
+    ready = 1;
+  }
+  for (long i = 0; i < nq; i++)
+    for (long j = 0; j < nr; j++) {
+      int32_t acc = 0;
+      for (int b = 0; b < nbytes; b++) acc += lut[q[i * nbytes + b] ^ r[j * nbytes + b]];
+      out[i * nr + j] = acc;
+    }
+}

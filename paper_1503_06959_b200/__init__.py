@@ -23,6 +23,8 @@ _LAZY = {
     "merge_features": "masking", "binning_histogram": "masking",
     "run_pipeline": "pipeline", "run_streams": "pipeline",
     "FeatureEngine": "engine",
+    "hamming_matrix": "matching", "radius_match": "matching", "Match": "matching",
+    "DEFAULT_MATCH_RADIUS": "matching",
 }
 
 

@@ -18,7 +18,7 @@ VF_OK = 0
 ERRORS = {
     -1: ValueError, -2: ValueError, -3: ValueError, -4: ValueError, -5: ValueError, -6: ValueError,
     -7: ValueError, -8: ValueError, -9: RuntimeError, -10: RuntimeError, -11: ValueError,
-    -12: IndexError, -13: KeyError, -14: RuntimeError,
+    -12: IndexError, -13: KeyError, -14: RuntimeError, -15: RuntimeError,
 }
 MODES = {"none": 0, "intensity": 1, "binning": 2}
 
@@ -94,13 +94,16 @@ def lib():
     L.vf_binning_histogram.argtypes = [c_int, _P, _P, c_int, c_int, c_int, c_int, _P, c_void_p]
     L.vf_upsample_mask.argtypes = [_P, c_int, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]
     L.vf_mask_values.argtypes = [_P, c_int, c_int, c_int, _P, _P, _P, c_void_p]
+    L.vf_hamming_matrix.argtypes = [_P, c_int64, _P, c_int64, c_int, _P, c_int64, c_void_p]
+    L.vf_radius_match.argtypes = [_P, c_int64, _P, c_int64, c_int, c_int, _P, _P, _P, c_int64,
+                                  POINTER(c_int64), c_void_p]
     for name in ("vf_set_pattern", "vf_create", "vf_destroy", "vf_layer_geometry", "vf_reset", "vf_process",
                  "vf_process_host", "vf_get_report", "vf_get_features", "vf_copy_features", "vf_get_layer",
                  "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe",
                  "vf_intensity_mask", "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
                  "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
-                 "vf_pipeline_collect"):
+                 "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -112,7 +115,7 @@ EXPORTS = (
     "vf_process", "vf_process_host", "vf_get_report", "vf_get_features", "vf_copy_features", "vf_get_layer",
     "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe", "vf_intensity_mask",
-    "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
+    "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values", "vf_hamming_matrix", "vf_radius_match",
 )
 
 

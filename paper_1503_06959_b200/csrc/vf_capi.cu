@@ -281,6 +281,7 @@ const char* vf_strerror(int code)
     case VF_ERR_INDEX: return "index out of bounds";
     case VF_ERR_OCTAVE_KEY: return "no octave layer at octave_for_mask";
     case VF_ERR_PATTERN: return "sampling pattern not set or malformed";
+    case VF_ERR_MATCH_CAPACITY: return "match buffer capacity exceeded";
     default: return "unknown error";
   }
 }

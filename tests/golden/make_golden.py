@@ -266,5 +266,53 @@ def main():
         print(name, [len(f) for f in feats])
 
 
+def make_matching():
+    """8. descriptor matching (matching.py:47-94), SURVEY.md 8(f) rank 1."""
+    import_reference()
+    from vidfeat import matching
+    from vidfeat.detector import Keypoint
+    from vidfeat.masking import Feature
+
+    mt = {}
+    rng = np.random.default_rng(31)
+    # tests/test_kernel_equivalence.py:74-79 shapes, plus a larger random pair
+    for tag, (nq, nr, nb) in {"a": (17, 23, 64), "b": (150, 133, 64), "c": (9, 11, 7), "d": (33, 5, 32)}.items():
+        q = rng.integers(0, 256, (nq, nb), dtype=np.uint8)
+        r = rng.integers(0, 256, (nr, nb), dtype=np.uint8)
+        mt[f"{tag}_q"], mt[f"{tag}_r"] = q, r
+        mt[f"{tag}_d"] = matching.hamming_matrix(q, r)
+    # planted near-duplicates (tests/test_matching.py:30-64 style): distances
+    # 0, 10, 50, 101, 102, 103, 200 from each query, shuffled into the refs
+    base = rng.integers(0, 2, (40, 512)).astype(np.uint8)
+    refs = []
+    for i in range(40):
+        for k in (0, 10, 50, 101, 102, 103, 200):
+            b = base[i].copy()
+            b[rng.choice(512, k, replace=False)] ^= 1
+            refs.append(b)
+    refs = np.stack(refs)[rng.permutation(len(refs))]
+
+    def feats(bits):
+        return [Feature(Keypoint(0.0, 0.0, 1.0), b.astype(np.uint8), "detected", 0) for b in bits]
+
+    mt["plant_q_bits"], mt["plant_r_bits"] = base, refs
+    for t_m in (0, 50, 102, 260):
+        ms = matching.radius_match(feats(base), feats(refs), t_m)
+        mt[f"plant_{t_m}"] = np.array([[m.query_idx, m.ref_idx, m.distance] for m in ms], np.int64).reshape(-1, 3)
+    # 56-bit descriptors (7 packed bytes)
+    q56 = rng.integers(0, 2, (12, 56)).astype(np.uint8)
+    r56 = rng.integers(0, 2, (15, 56)).astype(np.uint8)
+    mt["w56_q_bits"], mt["w56_r_bits"] = q56, r56
+    ms = matching.radius_match(feats(q56), feats(r56), 24)
+    mt["w56_24"] = np.array([[m.query_idx, m.ref_idx, m.distance] for m in ms], np.int64).reshape(-1, 3)
+    mt["default_radius"] = np.array(matching.DEFAULT_MATCH_RADIUS)
+    np.savez_compressed(HERE / "matching.npz", **mt)
+    print("matching", {k: v.shape for k, v in mt.items() if k.startswith("plant_") and v.ndim == 2})
+
+
 if __name__ == "__main__":
-    main()
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "matching":
+        make_matching()
+    else:
+        main()
+        make_matching()

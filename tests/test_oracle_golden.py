@@ -125,3 +125,28 @@ def test_pipeline_goldens(name):
         mode=str(g["mode"]), t_i=float(g["t_i"]), t_h=int(g["t_h"]), grid=tuple(int(v) for v in g["grid"]),
         octave_for_mask=None if ofm < 0 else ofm, per_layer=bool(g["per_layer"]))
     compare_frames(outs, g)
+
+
+def test_oracle_hamming_matrix_golden():
+    """vfo_hamming_matrix == the reference's hamming_matrix (matching.py:73-77)."""
+    from oracle import oracle
+
+    g = golden("matching.npz")
+    for tag in "abcd":
+        assert np.array_equal(oracle.hamming_matrix(g[f"{tag}_q"], g[f"{tag}_r"]), g[f"{tag}_d"]), tag
+
+
+def test_oracle_radius_match_golden():
+    """Oracle radius match == the reference's radius_match (matching.py:80-94),
+    planted distances 0..200 around t_m in {0, 50, 102, 260} and 56-bit rows."""
+    from oracle import oracle
+
+    g = golden("matching.npz")
+    q = np.packbits(g["plant_q_bits"], axis=1)
+    r = np.packbits(g["plant_r_bits"], axis=1)
+    for t_m in (0, 50, 102, 260):
+        qi, ri, d = oracle.radius_match(q, r, t_m)
+        assert np.array_equal(np.stack([qi, ri, d], 1).reshape(-1, 3), g[f"plant_{t_m}"]), t_m
+    qi, ri, d = oracle.radius_match(np.packbits(g["w56_q_bits"], axis=1), np.packbits(g["w56_r_bits"], axis=1), 24)
+    assert np.array_equal(np.stack([qi, ri, d], 1).reshape(-1, 3), g["w56_24"])
+    assert int(g["default_radius"]) == 102
