@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="detect", choices=["detect", "match"],
+                    help="detect: the headline detect+describe path; match: Hamming radius matching (SURVEY 8(f))")
+    ap.add_argument("--match-pairs", type=int, default=8, help="frame pairs per step (match workload)")
     return ap.parse_args()
 
 
@@ -300,9 +303,194 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------
+# Hamming radius matching workload
+# ----------------------------------------------------------------------------
+POPC_PEAK_PER_CLK_SM = 15.6   # measured, tools/micro/popc_bench.cu (profiles/r01_popc_peak.txt)
+T_M = 102
+
+
+def match_descriptors(pairs, device):
+    """Packed descriptors of frames 1 and 2 of config-5 streams 0..pairs-1,
+    produced by the engine (intensity mode).  Returns [(a, b)] uint8 tensors."""
+    import torch
+
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    streams = list(range(pairs))
+    frames = gen_frames(streams, 3, device)
+    eng = FeatureEngine(W_FR, H_FR, PipelineConfig(mask=MaskConfig(mode="intensity")), n_streams=len(streams))
+    got = []
+    for n in range(3):
+        eng.process(frames[n])
+        if n >= 1:
+            got.append([torch.from_numpy(eng.features_host(s)["desc"]).to(device) for s in range(len(streams))])
+    eng.close()
+    return [(got[1][s], got[0][s]) for s in range(len(streams))]   # query = frame 2, reference = frame 1
+
+
+def run_match(args, rank, world, local):
+    """One step = radius_match (t_m = 102) of the current frame's features
+    against the previous frame's, for every local stream pair (whole 25.7k x
+    25.7k all-pairs per stream at 1080p)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_06959_b200.matching import radius_match_device
+
+    impl_ref = args.impl == "reference"
+    if impl_ref and rank != 0:
+        return
+    if not impl_ref:
+        torch.cuda.set_device(local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if impl_ref:
+        # same inputs, produced on the host by the oracle (the reference arm uses no GPU code)
+        from oracle import oracle
+        from paper_1503_06959_b200 import scenes
+        from paper_1503_06959_b200.pattern import default_pattern
+
+        pairs = []
+        for s_ in range(args.match_pairs):
+            fr = scenes.generate(scenes.CONFIGS[5], 3, streams=[s_])[0].numpy()
+            seq = oracle.run_sequence(list(fr), default_pattern(), mode="intensity")
+            pairs.append((torch.from_numpy(seq[2].desc), torch.from_numpy(seq[1].desc)))
+    else:
+        dev = torch.device("cuda", local)
+        mine = shard(args.match_pairs, rank, world)
+        pairs_all = match_descriptors(args.match_pairs, dev)
+        pairs = [pairs_all[i] for i in mine]
+    n_pairs_step = float(sum(a.shape[0] * b.shape[0] for a, b in pairs))
+    cfg = {"workload": f"match: radius_match t_m={T_M} of frame-2 vs frame-1 packed 512-bit descriptors of "
+                       f"{args.match_pairs} config-5 1080p streams (intensity mode)",
+           "pairs_per_step": n_pairs_step * (world if not impl_ref else 1),
+           "descriptors_per_frame": float(np.mean([a.shape[0] for a, _ in pairs]))}
+    if impl_ref:
+        from concurrent.futures import ThreadPoolExecutor
+
+        from oracle import oracle
+
+        threads = host_threads()
+        host = [(a.cpu().numpy(), b.cpu().numpy()) for a, b in pairs]
+        rows = 256   # bounded sample per step: 256 query rows of every pair
+        jobs = [(a[i:i + 16], b) for a, b in host for i in range(0, rows, 16)]
+
+        def step():
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                return sum(ex.map(lambda j: len(oracle.radius_match(j[0], j[1], T_M)[0]), jobs))
+
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dt = (time.perf_counter() - t0) / args.steps
+        pps = sum(j[0].shape[0] * j[1].shape[0] for j in jobs) / dt
+        line = {"impl": "reference", "metric": "descriptor pairs/s (Hamming radius match)", "value": pps,
+                "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "u32 (popcount)", "data": "synthetic", "config": cfg,
+                "cpu_baseline": {"value": pps, "unit": "pairs/s", "cores": threads, "kind": "port",
+                                 "sample": f"{rows} query rows x all reference rows of each of {len(host)} pairs per "
+                                           f"step; C oracle (LUT popcount, matching.py:47-66) on {cpu_model()}"},
+                "e2e": {"value": pps, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > L2 (126 MB): written between steps
+    n_match = 0
+
+    def step():
+        nonlocal n_match
+        n = 0
+        for a, b in pairs:
+            qi, _, _ = radius_match_device(a, b, T_M)
+            n += qi.numel()
+        n_match = n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = 0.0
+    with ClockSampler(local) as clk:
+        time.sleep(1.0)
+        tw0 = time.time()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()      # radius_match synchronizes (match count) -- inside the events
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        tw1 = time.time()
+    clk.window(tw0, tw1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0])
+    pps = n_pairs_step * world * args.steps / (ms_max / 1e3)
+    # kernel-only time of the distance kernel (hamming_matrix over the same pairs)
+    from paper_1503_06959_b200.matching import hamming_matrix_device
+
+    for a, b in pairs[:1]:
+        hamming_matrix_device(a, b)
+    torch.cuda.synchronize()
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for a, b in pairs:
+        hamming_matrix_device(a, b)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kms = k0.elapsed_time(k1)
+    popc = 16.0 * n_pairs_step          # 16 x 32-bit popcounts per pair of 512-bit descriptors
+    peak = POPC_PEAK_PER_CLK_SM * 148 * 1.965e9 / 1e12
+    ach = popc / (kms / 1e3) / 1e12
+    # e2e: host packed descriptors (pinned) -> H2D -> radius match -> D2H of the matches
+    host = [(a.cpu().pin_memory(), b.cpu().pin_memory()) for a, b in pairs]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for a, b in host:
+        ad, bd = a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
+        qi, ri, d = radius_match_device(ad, bd, T_M)
+        out = torch.stack([qi, ri, d]).cpu()
+        h2d += a.numel() + b.numel()
+        d2h += out.numel() * 4
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if rank == 0:
+        line = {"metric": "descriptor pairs/s (Hamming radius match)", "value": pps, "unit": "pairs/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32 (popcount)",
+                "data": "synthetic", "config": dict(cfg, l2="256 MB buffer written between timed steps (outside "
+                                                         "the events)", matches_per_step=n_match * world),
+                "roofline": {"bound": "compute (POPC pipe)", "achieved": ach, "peak": peak, "unit": "Tpopc/s",
+                             "frac": ach / peak, "traffic": None, "kernel": "k_hamming_matrix (same pairs, live "
+                             "CUDA events)", "peak_source": "measured POPC rate, tools/micro/popc_bench.cu",
+                             "kernel_ms_per_step": kms},
+                "e2e": {"value": n_pairs_step / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "api": "pinned packed descriptors -> radius_match_device -> "
+                                                          "matches to host"},
+                "gpu_launches": args.steps * len(pairs) * 3, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.workload == "match":
+        run_match(args, rank, world, local)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

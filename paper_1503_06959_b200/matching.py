@@ -23,6 +23,7 @@ from . import _dev, _native
 from .types import Feature
 
 DEFAULT_MATCH_RADIUS = 102  # matching.py:20, Hamming threshold on 512-bit descriptors
+_density = 0.0              # matches per pair seen by the last radius_match_device call
 
 
 @dataclass(frozen=True, slots=True)
@@ -89,7 +90,9 @@ def radius_match_device(q, r, t_m: int = DEFAULT_MATCH_RADIUS):
     nq, nb = q.shape
     nr = r.shape[0]
     L = _native.lib()
-    cap = max(1024, 4 * max(nq, nr))
+    global _density
+    # size the output from the last observed match density (an overflow costs a recompute)
+    cap = max(1 << 21, int(1.5 * _density * nq * nr) + 1024)
     while True:
         qi = t.empty(cap, dtype=t.int32, device=q.device)
         ri = t.empty(cap, dtype=t.int32, device=q.device)
@@ -102,6 +105,7 @@ def radius_match_device(q, r, t_m: int = DEFAULT_MATCH_RADIUS):
             continue
         _native.check(rc, "vf_radius_match")
         k = int(n.value)
+        _density = max(_density * 0.5, k / max(1, nq * nr))
         return qi[:k], ri[:k], d[:k]
 
 
