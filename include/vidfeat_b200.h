@@ -41,9 +41,14 @@ extern "C" {
 #define VF_ERR_OCTAVE_KEY (-13)   /* KeyError: no octave layer at octave_for_mask (pyramid.py:61-63) */
 #define VF_ERR_PATTERN (-14)      /* sampling pattern not uploaded / malformed                   */
 #define VF_ERR_MATCH_CAPACITY (-15) /* radius_match output buffer too small (*n_matches = needed)  */
+#define VF_ERR_GOP_DELTA (-16)    /* "GOP length must be >= 1"               temporal.py:34-35   */
+#define VF_ERR_GOP_PATCH (-17)    /* "patch side must be even and positive"  temporal.py:36-37   */
+#define VF_ERR_GOP_STEP (-18)     /* "fine_step must not exceed coarse_step" temporal.py:38-39   */
+#define VF_ERR_GOP_SAD (-19)      /* "SAD thresholds must be positive"       temporal.py:40-41   */
 
 #define VF_MODE_NONE 0
 #define VF_MODE_INTENSITY 1
+#define VF_MODE_TEMPORAL 3   /* block-matching baseline: full detection at GOP starts, spiral SAD search between */
 #define VF_MODE_BINNING 2
 
 /* PipelineConfig (pipeline.py:46-54) + MaskConfig (masking.py:66-81), flattened. */
@@ -51,7 +56,7 @@ typedef struct vf_config {
   int32_t width, height;      /* frame size (all streams of a context share it)        */
   int32_t n_octaves;          /* PipelineConfig.n_octaves, default 4                   */
   int32_t threshold;          /* PipelineConfig.threshold, default 55                  */
-  int32_t mask_mode;          /* VF_MODE_*; "temporal" is not part of this path        */
+  int32_t mask_mode;          /* VF_MODE_* (pipeline.py:215-216 for temporal)          */
   double t_i;                 /* MaskConfig.t_i, default 20.0                          */
   int32_t t_h;                /* MaskConfig.t_h, default 1                             */
   int32_t grid_rows, grid_cols; /* MaskConfig.grid, default (16, 16)                   */
@@ -59,6 +64,10 @@ typedef struct vf_config {
   int32_t per_layer;          /* MaskConfig.per_layer                                  */
   int32_t max_streams;        /* independent video streams processed per call          */
   int32_t kp_capacity;        /* features per stream and frame, 0 = automatic          */
+  /* GopConfig (temporal.py:23-43), used when mask_mode == VF_MODE_TEMPORAL.  All
+   * zero = the reference defaults (10, 16, 1800, 1000, 12, 2, 1.75, 0.25). */
+  int32_t gop_delta, gop_patch;
+  double gop_t_bm, gop_t_et, gop_coarse_window, gop_coarse_step, gop_fine_window, gop_fine_step;
 } vf_config;
 
 /* FrameReport (pipeline.py:57-71) counts of the last processed frame. */
@@ -182,6 +191,16 @@ int vf_upsample_mask(const uint8_t *bits_dev, int rows, int cols, int cell_w, in
 /* _mask_values (masking.py:157-165): mask bit under each rounded, clamped position. */
 int vf_mask_values(const uint8_t *full_dev, int W, int H, int n, const double *xs_dev,
                    const double *ys_dev, uint8_t *out_dev, void *stream);
+
+/* --- temporal block-matching baseline (temporal.py) --- */
+/* baseline_step's per-feature search (temporal.py:274-308 with spiral_search
+ * :183-226) for n features of one stream: the patch x patch block around the
+ * rounded (x, y) of prev_dev is searched in cur_dev (both w x h, row pitch).
+ * found_dev[i] = 1 with the new position and SAD when the best SAD < t_bm.
+ * gop: GopConfig fields as in vf_config (zero = defaults).  Async on stream. */
+int vf_block_match(const uint8_t *prev_dev, const uint8_t *cur_dev, int w, int h, int64_t pitch, int n,
+                   const double *x_dev, const double *y_dev, const vf_config *gop, double *nx_dev, double *ny_dev,
+                   double *sad_dev, uint8_t *found_dev, void *stream);
 
 /* --- descriptor matching (matching.py:47-94) -------- */
 /* hamming_matrix (matching.py:73-77, _hamming_matrix_jit :56-66): out[i * ld + j]

@@ -446,7 +446,15 @@ typedef struct {
     /* report of the last frame */
     int n_detected, n_propagated, n_total, n_dropped;
     double coverage;
+    /* temporal baseline (mode 3): GopConfig and the previous frame */
+    int gop_delta, gop_patch, n_coarse, n_fine;
+    double gop_t_bm, gop_t_et, *coarse, *fine;
+    uint8_t *prev_frame;
 } vfo_pipe;
+
+void vfo_block_match(const uint8_t *prev, const uint8_t *cur, int w, int h, int n, const double *x, const double *y,
+                     int patch, double t_bm, double t_et, const double *coarse, int nc, const double *fine, int nf,
+                     double *nx, double *ny, double *sad_out, uint8_t *found);
 
 static void feats_reserve(vfo_feats *f, int n)
 {
@@ -471,7 +479,7 @@ static void feats_free(vfo_feats *f)
     memset(f, 0, sizeof(*f));
 }
 
-/* mode: 0 none, 1 intensity, 2 binning.  mask_level < 0 = top octave. */
+/* mode: 0 none, 1 intensity, 2 binning, 3 temporal (vfo_pipe_set_gop).  mask_level < 0 = top octave. */
 vfo_pipe *vfo_pipe_create(int W, int H, int O, int threshold, int mode, double t_i, int t_h,
                           int grid_rows, int grid_cols, int mask_level, int per_layer, int m,
                           const double *pts, const double *radii, int nbits, const int32_t *short_pairs,
@@ -522,7 +530,50 @@ void vfo_pipe_destroy(vfo_pipe *p)
     free(p->full_mask); free(p->proj); free(p->sat);
     free(p->pts); free(p->radii); free(p->si); free(p->sj); free(p->li); free(p->lj); free(p->wx); free(p->wy);
     feats_free(&p->cur); feats_free(&p->prev);
+    free(p->coarse); free(p->fine); free(p->prev_frame);
     free(p);
+}
+
+/* GopConfig (temporal.py:23-43) + spiral offsets (coarse; fine without (0, 0)). */
+void vfo_pipe_set_gop(vfo_pipe *p, int delta, int patch, double t_bm, double t_et, const double *coarse, int nc,
+                      const double *fine, int nf)
+{
+    p->gop_delta = delta; p->gop_patch = patch; p->gop_t_bm = t_bm; p->gop_t_et = t_et;
+    p->n_coarse = nc; p->n_fine = nf;
+    p->coarse = realloc(p->coarse, sizeof(double) * 2 * (nc ? nc : 1));
+    p->fine = realloc(p->fine, sizeof(double) * 2 * (nf ? nf : 1));
+    memcpy(p->coarse, coarse, sizeof(double) * 2 * nc);
+    memcpy(p->fine, fine, sizeof(double) * 2 * nf);
+    if (!p->prev_frame) p->prev_frame = malloc((size_t)p->W * p->H);
+}
+
+/* pipeline.py:281-345 _run_temporal, off-GOP frame: baseline_step's block matching. */
+static int temporal_step(vfo_pipe *p, const uint8_t *frame)
+{
+    const vfo_feats *pv = &p->prev;
+    vfo_feats *out = &p->cur;
+    feats_reserve(out, pv->n);
+    int n = pv->n;
+    double *nx = malloc(sizeof(double) * (n ? n : 1)), *ny = malloc(sizeof(double) * (n ? n : 1));
+    double *sd = malloc(sizeof(double) * (n ? n : 1));
+    uint8_t *fd = malloc(n ? n : 1);
+    vfo_block_match(p->prev_frame, frame, p->W, p->H, n, pv->x, pv->y, p->gop_patch, p->gop_t_bm, p->gop_t_et,
+                    p->coarse, p->n_coarse, p->fine, p->n_fine, nx, ny, sd, fd);
+    int k = 0;
+    for (int i = 0; i < n; i++) {
+        if (!fd[i]) continue;
+        out->x[k] = nx[i]; out->y[k] = ny[i]; out->sigma[k] = pv->sigma[i]; out->theta[k] = pv->theta[i];
+        out->score[k] = pv->score[i]; out->origin[k] = 1; out->age[k] = pv->age[i] + 1;
+        memcpy(out->desc + (size_t)64 * k, pv->desc + (size_t)64 * i, 64);
+        k++;
+    }
+    out->n = k;
+    free(nx); free(ny); free(sd); free(fd);
+    p->n_detected = 0; p->n_propagated = k; p->n_total = k; p->n_dropped = 0; p->coverage = 0.0;
+    vfo_feats tmp = p->prev; p->prev = p->cur; p->cur = tmp;
+    memcpy(p->prev_frame, frame, (size_t)p->W * p->H);
+    p->frame_no++;
+    return 0;
 }
 
 static int any_set(const uint8_t *a, size_t n)
@@ -535,9 +586,10 @@ static int any_set(const uint8_t *a, size_t n)
 int vfo_pipe_process(vfo_pipe *p, const uint8_t *frame)
 {
     int W = p->W, H = p->H, O = p->O, NL = p->n_layers;
+    if (p->mode == 3 && p->frame_no % p->gop_delta != 0) return temporal_step(p, frame);   /* off-GOP */
     int rc = vfo_build_pyramid(frame, W, H, O, p->layers);
     if (rc) return rc;
-    int use_mask = p->mode != 0 && p->frame_no > 0;
+    int use_mask = p->mode != 0 && p->mode != 3 && p->frame_no > 0;   /* GOP start: full detection */
     int per_level = 0;
     double coverage = 1.0;
     if (use_mask) {                                        /* pipeline.py:174-204 _build_mask */
@@ -655,6 +707,7 @@ int vfo_pipe_process(vfo_pipe *p, const uint8_t *frame)
     for (int l = 0; l < NL; l++) {
         uint8_t *t = p->prev_layers[l]; p->prev_layers[l] = p->layers[l]; p->layers[l] = t;
     }
+    if (p->mode == 3) memcpy(p->prev_frame, frame, (size_t)W * H);
     p->frame_no++;
     return 0;
 }
@@ -698,4 +751,100 @@ void vfo_hamming_matrix(const uint8_t *q, long nq, const uint8_t *r, long nr, in
       for (int b = 0; b < nbytes; b++) acc += lut[q[i * nbytes + b] ^ r[j * nbytes + b]];
       out[i * nr + j] = acc;
     }
+}
+
+/* ------------------------------------------------------------------ */
+/* temporal.py:64-226 -- two-stage spiral SAD search of one 16x16 (or  */
+/* patch x patch) block; baseline_step's per-feature part :274-308.     */
+/* offsets: (n x 2) doubles in spiral order (fine set without (0, 0)).  */
+/* ------------------------------------------------------------------ */
+static void coarse_search(const uint8_t *patch, int ph, int pw, const uint8_t *frame, int w, int h,
+                          int64_t base_x, int64_t base_y, const double *offs, int n, double t_et,
+                          int *best_k, int64_t *best_sad, int *early)
+{                                                        /* temporal.py:125-145 (_coarse_search_jit) */
+    int64_t best = (int64_t)1 << 60;
+    int bk = -1;
+    *early = 0;
+    for (int k = 0; k < n; k++) {
+        int64_t tlx = base_x + (int64_t)offs[2 * k], tly = base_y + (int64_t)offs[2 * k + 1];
+        if (tlx < 0 || tly < 0 || tlx + pw > w || tly + ph > h) continue;
+        int64_t sad = 0;
+        for (int r = 0; r < ph; r++)
+            for (int c = 0; c < pw; c++) {
+                int64_t d = (int64_t)patch[r * pw + c] - (int64_t)frame[(tly + r) * w + tlx + c];
+                sad += d < 0 ? -d : d;
+            }
+        if (sad < best) {
+            best = sad;
+            bk = k;
+            if ((double)sad < t_et) { *early = 1; break; }
+        }
+    }
+    *best_k = bk;
+    *best_sad = best;
+}
+
+static void fine_search(const uint8_t *patch, int ph, int pw, const uint8_t *frame, int w, int h, double base_x,
+                        double base_y, const double *offs, int n, double t_et, double init, int *best_k,
+                        double *best_sad)
+{                                                        /* temporal.py:147-180 (_fine_search_jit) */
+    double best = init;
+    int bk = -1;
+    for (int k = 0; k < n; k++) {
+        double fx = base_x + offs[2 * k], fy = base_y + offs[2 * k + 1];
+        int64_t ix = (int64_t)floor(fx), iy = (int64_t)floor(fy);
+        if (ix < 0 || iy < 0 || ix + pw >= w || iy + ph >= h) continue;
+        double ax = fx - (double)ix, ay = fy - (double)iy;
+        double w00 = (1.0 - ax) * (1.0 - ay), w10 = ax * (1.0 - ay), w01 = (1.0 - ax) * ay, w11 = ax * ay;
+        double sad = 0.0;
+        for (int r = 0; r < ph; r++)
+            for (int c = 0; c < pw; c++) {
+                const uint8_t *f0 = frame + (iy + r) * w + ix + c, *f1 = f0 + w;
+                double v = w00 * f0[0] + w10 * f0[1] + w01 * f1[0] + w11 * f1[1];
+                sad += fabs((double)patch[r * pw + c] - v);
+            }
+        if (sad < best) {
+            best = sad;
+            bk = k;
+            if (sad < t_et) break;
+        }
+    }
+    *best_k = bk;
+    *best_sad = best;
+}
+
+/* found[i] = 1 and (nx, ny, sad) when feature i is tracked into cur (temporal.py:274-308). */
+void vfo_block_match(const uint8_t *prev, const uint8_t *cur, int w, int h, int n, const double *x, const double *y,
+                     int patch, double t_bm, double t_et, const double *coarse, int nc, const double *fine, int nf,
+                     double *nx, double *ny, double *sad_out, uint8_t *found)
+{
+    int half = patch / 2;
+    uint8_t *pb = (uint8_t *)malloc((size_t)patch * patch);
+    for (int i = 0; i < n; i++) {
+        found[i] = 0; nx[i] = 0.0; ny[i] = 0.0; sad_out[i] = 0.0;
+        int64_t cxi = (int64_t)floor(x[i] + 0.5), cyi = (int64_t)floor(y[i] + 0.5);
+        int64_t tlx = cxi - half, tly = cyi - half;
+        if (tlx < 0 || tly < 0 || tlx + patch > w || tly + patch > h) continue;
+        for (int r = 0; r < patch; r++) memcpy(pb + r * patch, prev + (tly + r) * w + tlx, (size_t)patch);
+        /* spiral_search (temporal.py:200-226): same rounded centre */
+        int64_t base_x = cxi - patch / 2, base_y = cyi - patch / 2;
+        int k, early;
+        int64_t isad;
+        coarse_search(pb, patch, patch, cur, w, h, base_x, base_y, coarse, nc, t_et, &k, &isad, &early);
+        if (k < 0) continue;
+        double ox = coarse[2 * k], oy = coarse[2 * k + 1], best = (double)isad;
+        if (!early) {
+            int fk;
+            double fsad;
+            fine_search(pb, patch, patch, cur, w, h, (double)base_x + ox, (double)base_y + oy, fine, nf, t_et, best,
+                        &fk, &fsad);
+            if (fk >= 0) { ox += fine[2 * fk]; oy += fine[2 * fk + 1]; best = fsad; }
+        }
+        if (best >= t_bm) continue;
+        found[i] = 1;
+        nx[i] = (double)cxi + ox;
+        ny[i] = (double)cyi + oy;
+        sad_out[i] = best;
+    }
+    free(pb);
 }

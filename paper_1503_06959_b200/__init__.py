@@ -9,7 +9,8 @@ machine without a GPU; any compute call without a CUDA device raises.
 """
 
 from .pattern import SamplingPattern, build_default_pattern, default_pattern
-from .types import (DETECTED, INTRA, OCTAVE, PROPAGATED, Candidate, DetectionMask, Feature, FrameReport, GrayFrame,
+from .types import (DETECTED, INTRA, OCTAVE, PROPAGATED, Candidate, DetectionMask, Feature, FrameReport, GopConfig,
+                    GrayFrame,
                     Keypoint, MaskConfig, PipelineConfig, PyramidLayer, ScaleSpacePyramid, SubsampledMask)
 
 __version__ = "0.1.0"
@@ -25,6 +26,7 @@ _LAZY = {
     "FeatureEngine": "engine",
     "hamming_matrix": "matching", "radius_match": "matching", "Match": "matching",
     "DEFAULT_MATCH_RADIUS": "matching",
+    "spiral_offsets": "temporal", "spiral_search": "temporal", "baseline_step": "temporal",
 }
 
 
@@ -38,7 +40,7 @@ def __getattr__(name):
 
 
 __all__ = sorted(list(_LAZY) + [
-    "SamplingPattern", "build_default_pattern", "default_pattern", "Candidate", "DetectionMask", "Feature",
+    "SamplingPattern", "build_default_pattern", "default_pattern", "Candidate", "DetectionMask", "Feature", "GopConfig",
     "FrameReport", "GrayFrame", "Keypoint", "MaskConfig", "PipelineConfig", "PyramidLayer", "ScaleSpacePyramid",
     "SubsampledMask", "OCTAVE", "INTRA", "DETECTED", "PROPAGATED",
 ])

@@ -18,9 +18,10 @@ VF_OK = 0
 ERRORS = {
     -1: ValueError, -2: ValueError, -3: ValueError, -4: ValueError, -5: ValueError, -6: ValueError,
     -7: ValueError, -8: ValueError, -9: RuntimeError, -10: RuntimeError, -11: ValueError,
-    -12: IndexError, -13: KeyError, -14: RuntimeError, -15: RuntimeError,
+    -12: IndexError, -13: KeyError, -14: RuntimeError, -15: RuntimeError, -16: ValueError, -17: ValueError,
+    -18: ValueError, -19: ValueError,
 }
-MODES = {"none": 0, "intensity": 1, "binning": 2}
+MODES = {"none": 0, "intensity": 1, "binning": 2, "temporal": 3}
 
 
 class VfConfig(ctypes.Structure):
@@ -29,6 +30,9 @@ class VfConfig(ctypes.Structure):
         ("mask_mode", c_int32), ("t_i", c_double), ("t_h", c_int32), ("grid_rows", c_int32),
         ("grid_cols", c_int32), ("octave_for_mask", c_int32), ("per_layer", c_int32),
         ("max_streams", c_int32), ("kp_capacity", c_int32),
+        ("gop_delta", c_int32), ("gop_patch", c_int32), ("gop_t_bm", c_double), ("gop_t_et", c_double),
+        ("gop_coarse_window", c_double), ("gop_coarse_step", c_double), ("gop_fine_window", c_double),
+        ("gop_fine_step", c_double),
     ]
 
 
@@ -95,6 +99,8 @@ def lib():
     L.vf_upsample_mask.argtypes = [_P, c_int, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]
     L.vf_mask_values.argtypes = [_P, c_int, c_int, c_int, _P, _P, _P, c_void_p]
     L.vf_hamming_matrix.argtypes = [_P, c_int64, _P, c_int64, c_int, _P, c_int64, c_void_p]
+    L.vf_block_match.argtypes = [_P, _P, c_int, c_int, c_int64, c_int, _P, _P, POINTER(VfConfig), _P, _P, _P, _P,
+                                 c_void_p]
     L.vf_radius_match.argtypes = [_P, c_int64, _P, c_int64, c_int, c_int, _P, _P, _P, c_int64,
                                   POINTER(c_int64), c_void_p]
     for name in ("vf_set_pattern", "vf_create", "vf_destroy", "vf_layer_geometry", "vf_reset", "vf_process",
@@ -103,7 +109,7 @@ def lib():
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe",
                  "vf_intensity_mask", "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
                  "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
-                 "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match"):
+                 "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match", "vf_block_match"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -116,6 +122,7 @@ EXPORTS = (
     "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe", "vf_intensity_mask",
     "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values", "vf_hamming_matrix", "vf_radius_match",
+    "vf_block_match",
 )
 
 

@@ -3,6 +3,7 @@
 // Single translation unit: includes the kernels.  Built by
 // paper_1503_06959_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
 #include "vf_kernels.cu"
+#include "vf_temporal.cuh"
 #include "../../include/vidfeat_b200.h"
 
 #include <cstdio>
@@ -62,12 +63,49 @@ int layer_dims(int W, int H, int O, int* ws, int* hs, double* scales)
   return VF_OK;
 }
 
+// GopConfig (temporal.py:23-43): all gop_* fields zero = the defaults;
+// otherwise validated in the reference's order.
+struct Gop { int delta, patch; double t_bm, t_et, cw, cs, fw, fs; };
+int gop_from_config(const vf_config& c, Gop& o)
+{
+  const bool zero = !c.gop_delta && !c.gop_patch && c.gop_t_bm == 0.0 && c.gop_t_et == 0.0 &&
+                    c.gop_coarse_window == 0.0 && c.gop_coarse_step == 0.0 && c.gop_fine_window == 0.0 &&
+                    c.gop_fine_step == 0.0;
+  if (zero) { o = Gop{10, 16, 1800.0, 1000.0, 12.0, 2.0, 1.75, 0.25}; return VF_OK; }
+  o = Gop{c.gop_delta, c.gop_patch, c.gop_t_bm, c.gop_t_et, c.gop_coarse_window, c.gop_coarse_step,
+          c.gop_fine_window, c.gop_fine_step};
+  if (o.delta < 1) return VF_ERR_GOP_DELTA;
+  if (o.patch % 2 != 0 || o.patch < 2) return VF_ERR_GOP_PATCH;
+  if (o.fs > o.cs) return VF_ERR_GOP_STEP;
+  if (o.t_bm <= 0 || o.t_et <= 0) return VF_ERR_GOP_SAD;
+  if (!(o.cs > 0) || !(o.fs > 0) || o.cw < 0 || o.fw < 0 || o.cw / o.cs > 4096 || o.fw / o.fs > 4096) return VF_ERR_ARG;
+  return VF_OK;
+}
+
+// Spiral offsets + search set-up of a GopConfig; offsets stay on the host in co / fi.
+void gop_setup(const Gop& o, vft::Setup& q, std::vector<double>& co, std::vector<double>& fi)
+{
+  co = vft::spiral_offsets(o.cw, o.cs);
+  fi = vft::spiral_offsets(o.fw, o.fs);
+  fi.erase(fi.begin(), fi.begin() + 2);             // skip (0, 0) (temporal.py:216)
+  q.P = o.patch; q.nc = (int)co.size() / 2; q.nf = (int)fi.size() / 2;
+  q.t_bm = o.t_bm; q.t_et = o.t_et;
+  double mc = 0, mf = 0;
+  bool dy = true;
+  for (double v : co) { mc = std::max(mc, std::fabs(v)); dy = dy && v == std::floor(v); }
+  for (double v : fi) { mf = std::max(mf, std::fabs(v)); dy = dy && v * 4.0 == std::floor(v * 4.0); }
+  q.rc = (int)std::ceil(mc);
+  q.rfc = std::max(1, (int)std::ceil(mf));
+  q.dyadic = dy && o.patch * o.patch * 255LL * 16 < (1LL << 24);
+  vft::layout(q);
+}
+
 // Fill Geo for a frame size and config.  lut is filled on the host.
 int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
 {
   memset(&g, 0, sizeof(g));
   if (c.threshold < 1) return VF_ERR_THRESHOLD;
-  if (c.mask_mode < 0 || c.mask_mode > 2) return VF_ERR_MODE;
+  if (c.mask_mode < 0 || c.mask_mode > 3) return VF_ERR_MODE;
   if (c.t_h < 0) return VF_ERR_T_H;
   if (c.grid_rows < 1 || c.grid_cols < 1) return VF_ERR_GRID;
   int ws[VF_MAXL], hs[VF_MAXL];
@@ -78,6 +116,12 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.threshold = c.threshold;
   g.mask_mode = c.mask_mode;
   g.per_layer = c.mask_mode == 1 ? c.per_layer : 0;
+  if (c.mask_mode == 3) {
+    Gop o;
+    const int grc = gop_from_config(c, o);
+    if (grc) return grc;
+    g.gop_delta = o.delta; g.gop_patch = o.patch; g.gop_t_bm = o.t_bm; g.gop_t_et = o.t_et;
+  }
   g.mask_level = c.octave_for_mask < 0 ? g.O - 1 : c.octave_for_mask;
   if (c.mask_mode == 1 && (g.mask_level < 0 || g.mask_level >= g.O)) return VF_ERR_OCTAVE_KEY;
   g.t_i = c.t_i; g.t_h = c.t_h;
@@ -191,6 +235,8 @@ struct vf_ctx {
   int fast_grid;
   int desc_grid;
   int sat_grid, sat_smem, desc_smem, dsample_grid, dorient_grid;
+  vft::Setup bmq{};                     // temporal mode: block-match set-up (device offsets)
+  int bm_grid = 0, bm_smem = 0;
   // host-input staging (vf_process_host)
   uint8_t* hstage[2] = {nullptr, nullptr};
   long long hstage_bytes = 0;
@@ -282,6 +328,10 @@ const char* vf_strerror(int code)
     case VF_ERR_OCTAVE_KEY: return "no octave layer at octave_for_mask";
     case VF_ERR_PATTERN: return "sampling pattern not set or malformed";
     case VF_ERR_MATCH_CAPACITY: return "match buffer capacity exceeded";
+    case VF_ERR_GOP_DELTA: return "GOP length must be >= 1";
+    case VF_ERR_GOP_PATCH: return "patch side must be even and positive";
+    case VF_ERR_GOP_STEP: return "fine_step must not exceed coarse_step";
+    case VF_ERR_GOP_SAD: return "SAD thresholds must be positive";
     default: return "unknown error";
   }
 }
@@ -405,6 +455,28 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_orient, DO_THREADS, (S + 1) * sizeof(int));
   c->dorient_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  if (g.mask_mode == 3) {                    // temporal baseline state
+    Gop o;
+    gop_from_config(*cfg, o);
+    std::vector<double> co, fi;
+    gop_setup(o, c->bmq, co, fi);
+    double* dco = A.get<double>(co.size());
+    double* dfi = A.get<double>(std::max<size_t>(fi.size(), 2));
+    b.prev_frame = A.get<uint8_t>((size_t)S * g.W * g.H);
+    b.bm_found = A.get<uint8_t>((size_t)S * cap);
+    b.bm_chunk = A.get<int>((size_t)S * g.prop_chunks);
+    if (A.err != cudaSuccess) { int r = cuda_status(A.err); vf_destroy(c); return r; }
+    cudaMemcpy(dco, co.data(), sizeof(double) * co.size(), cudaMemcpyHostToDevice);
+    if (!fi.empty()) cudaMemcpy(dfi, fi.data(), sizeof(double) * fi.size(), cudaMemcpyHostToDevice);
+    b.bm_coarse = dco; b.bm_fine = dfi;
+    c->bmq.coarse = dco; c->bmq.fine = dfi;
+    c->bm_smem = BM_WARPS * c->bmq.sm_words * 4 + (S + 1) * 4;
+    if (c->bm_smem > 227 * 1024) { vf_destroy(c); return VF_ERR_ARG; }
+    if (c->bm_smem > 48 * 1024) cudaFuncSetAttribute(k_blockmatch, cudaFuncAttributeMaxDynamicSharedMemorySize, c->bm_smem);
+    occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_blockmatch, 32 * BM_WARPS, c->bm_smem);
+    c->bm_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  }
   *out = c;
   return VF_OK;
 }
@@ -575,6 +647,88 @@ static int launch_grouped(vf_ctx* c, int n, cudaStream_t st)
   return rc;
 }
 
+// Temporal mode, off-GOP run of streams [s0, s0 + n): block matching of the
+// previous features (temporal.py:274-308), order-preserving compaction and
+// report, then the current frames become the previous ones.
+static int launch_temporal(vf_ctx* c, int s0, int n, cudaStream_t st)
+{
+  const Geo& g = c->g;
+  Bufs b = c->b;
+  b.s0 = s0;
+  cudaMemsetAsync(b.bm_chunk + (long long)s0 * g.prop_chunks, 0, sizeof(int) * (size_t)n * g.prop_chunks, st);
+  k_blockmatch<<<c->bm_grid, 32 * BM_WARPS, c->bm_smem, st>>>(g, b, c->bmq, n);
+  k_bm_write<<<dim3(std::max(g.prop_chunks, 1), n), 256, 0, st>>>(g, b);
+  k_copy_frames<<<dim3(64, n), 256, 0, st>>>(g, b);
+  k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
+  for (int s = s0; s < s0 + n; s++) c->frames_done[s]++;
+  return cuda_status(cudaGetLastError());
+}
+
+// Streams [0, n): detection (grouped) in the mask modes; in temporal mode,
+// contiguous runs of streams at a GOP start run full detection and keep their
+// frame, the others block-match (pipeline.py:299-307).
+static int launch_frames(vf_ctx* c, int n, cudaStream_t st)
+{
+  if (c->g.mask_mode != 3) return launch_grouped(c, n, st);
+  const uint8_t* base = c->b.frames;
+  int rc = VF_OK;
+  for (int s0 = 0; s0 < n && rc == VF_OK;) {
+    const bool gop = c->frames_done[s0] % c->g.gop_delta == 0;
+    int s1 = s0 + 1;
+    while (s1 < n && (c->frames_done[s1] % c->g.gop_delta == 0) == gop) s1++;
+    c->b.frames = base + (long long)s0 * c->b.frame_stride;
+    if (gop) {
+      rc = launch_step(c, s0, s1 - s0, st);
+      Bufs b = c->b;
+      b.s0 = s0;
+      k_copy_frames<<<dim3(64, s1 - s0), 256, 0, st>>>(c->g, b);
+    } else {
+      rc = launch_temporal(c, s0, s1 - s0, st);
+    }
+    s0 = s1;
+  }
+  c->b.frames = base;
+  return rc == VF_OK ? cuda_status(cudaGetLastError()) : rc;
+}
+
+int vf_block_match(const uint8_t* prev_dev, const uint8_t* cur_dev, int w, int h, int64_t pitch, int n,
+                   const double* x_dev, const double* y_dev, const vf_config* gop, double* nx_dev, double* ny_dev,
+                   double* sad_dev, uint8_t* found_dev, void* stream)
+{
+  if (n < 0 || w < 1 || h < 1 || pitch < w) return VF_ERR_ARG;
+  vf_config zero;
+  memset(&zero, 0, sizeof(zero));
+  Gop o;
+  int rc = gop_from_config(gop ? *gop : zero, o);
+  if (rc) return rc;
+  if (n == 0) return VF_OK;
+  if (!prev_dev || !cur_dev || !x_dev || !y_dev || !nx_dev || !ny_dev || !sad_dev || !found_dev) return VF_ERR_ARG;
+  if (!g_num_sms) { cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0); }
+  vft::Setup q{};
+  std::vector<double> co, fi;
+  gop_setup(o, q, co, fi);
+  cudaStream_t st = (cudaStream_t)stream;
+  double *dco = nullptr, *dfi = nullptr;
+  cudaError_t e = cudaMallocAsync(&dco, sizeof(double) * co.size(), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dfi, sizeof(double) * std::max<size_t>(fi.size(), 2), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dco, co.data(), sizeof(double) * co.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && !fi.empty())
+    e = cudaMemcpyAsync(dfi, fi.data(), sizeof(double) * fi.size(), cudaMemcpyHostToDevice, st);
+  const int smem = BM_WARPS * q.sm_words * 4;
+  if (e == cudaSuccess && smem > 227 * 1024) e = cudaErrorInvalidValue;
+  if (e == cudaSuccess) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_block_match, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    q.coarse = dco; q.fine = dfi;
+    const int grid = std::max(1, std::min(cdiv(n, BM_WARPS), g_num_sms * 8));
+    k_block_match<<<grid, 32 * BM_WARPS, smem, st>>>(q, prev_dev, cur_dev, w, h, pitch, n, x_dev, y_dev, nx_dev,
+                                                    ny_dev, sad_dev, found_dev);
+    e = cudaGetLastError();
+  }
+  if (dco) cudaFreeAsync(dco, st);
+  if (dfi) cudaFreeAsync(dfi, st);
+  return cuda_status(e);
+}
+
 int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n_streams,
                void* stream)
 {
@@ -583,7 +737,7 @@ int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int6
   c->b.frames = frames_dev;
   c->b.frame_stride = stream_stride;
   c->b.frame_pitch = row_pitch;
-  return launch_grouped(c, n_streams, (cudaStream_t)stream);
+  return launch_frames(c, n_streams, (cudaStream_t)stream);
 }
 
 int vf_process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch, int n_streams,
@@ -810,7 +964,7 @@ int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_str
   c->b.frames = P.frames[k];
   c->b.frame_stride = fbytes;
   c->b.frame_pitch = c->g.W;
-  rc = launch_grouped(c, n_streams, P.comp);
+  rc = launch_frames(c, n_streams, P.comp);
   if (rc) return rc;
   cudaStreamWaitEvent(P.comp, P.ev_d2h[k], 0);
   k_pack<<<g_num_sms * 8, 256, (n_streams + 1) * sizeof(int), P.comp>>>(
@@ -870,7 +1024,7 @@ int vf_get_diag(vf_ctx* c, int64_t* out8, void* stream)
   long long sat = 0, dense = 0, stage = 0;
   for (int s = 0; s < c->S; s++) {
     // frame counter already advanced: the last step was masked iff frame >= 2 (or mode none => dense)
-    const bool masked = c->g.mask_mode != 0 && ctr[(size_t)s * C_NCTR + C_FRAME] >= 2;
+    const bool masked = (c->g.mask_mode == 1 || c->g.mask_mode == 2) && ctr[(size_t)s * C_NCTR + C_FRAME] >= 2;
     if (masked) sat += sc[s]; else { sat += c->g.sat_tiles; dense++; }
     stage += ctr[(size_t)s * C_NCTR + C_STAGE];
   }

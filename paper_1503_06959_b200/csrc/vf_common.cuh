@@ -80,6 +80,9 @@ struct Geo {
   // IDDM state: octave levels kept for the next frame
   long long state_off[VF_MAXO]; long long state_slab;
   int kp_cap;           // feature capacity per stream and buffer
+  // temporal baseline (mask_mode 3, temporal.py:23-43): GOP and search set-up
+  int gop_delta, gop_patch, bm_nc, bm_nf, bm_rc, bm_rf, bm_dyadic;
+  double gop_t_bm, gop_t_et;
   int prop_chunks;      // CTAs reserved for propagation chunks
   int sat_tiles;        // stx * sty
   unsigned sth_magic;   // ceil(2^32 / VF_ST): y / VF_ST == umulhi(y, sth_magic) for y < 2^16
@@ -113,6 +116,10 @@ struct Bufs {
   unsigned* sat_bits;   // [S][sty][stw_words] SAT tiles marked this step (cleared by k_pyramid)
   int* sat_work; int* sat_count;   // [S][sat_tiles] / [S]: SAT tiles marked this step (masked frames)
   double* st_x; double* st_y; double* st_s; double* st_v;   // staging [S][kp_cap]
+  const double* bm_coarse; const double* bm_fine;         // spiral offsets (x, y) pairs (temporal mode)
+  uint8_t* prev_frame;     // [S][H][W] previous frame (temporal mode)
+  uint8_t* bm_found;       // [S][kp_cap] block-match result flags
+  int* bm_chunk;           // [S][prop_chunks] found counts per 1024-feature chunk
   // double-buffered features [S][2][kp_cap]
   double* fx; double* fy; double* fs; double* ft; double* fv;
   uint8_t* forg; int* fage; uint8_t* fdesc;  // desc: [S][2][kp_cap][64]
@@ -172,7 +179,8 @@ __device__ __forceinline__ int merge_mask_at(const Geo& g, const Bufs& b, int s,
 
 __device__ __forceinline__ int use_mask(const Geo& g, const Bufs& b, int s)
 {
-  return g.mask_mode != 0 && b.ctr[s * C_NCTR + C_FRAME] > 0;   // pipeline.py:234
+  // pipeline.py:234; temporal mode detects without a mask at GOP starts (temporal.py:287-288)
+  return g.mask_mode != 0 && g.mask_mode != 3 && b.ctr[s * C_NCTR + C_FRAME] > 0;
 }
 
 template <typename T>

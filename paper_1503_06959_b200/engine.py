@@ -27,10 +27,17 @@ class _CudaArray:
 
 
 def _mode(mc: MaskConfig) -> int:
-    if mc.mode == "temporal":
-        raise NotImplementedError(
-            "mask mode 'temporal' is the block-matching baseline (temporal.py), outside this hot path")
     return _native.MODES[mc.mode]
+
+
+def gop_fields(gop) -> dict:
+    """GopConfig -> the vf_config gop_* fields (None = reference defaults)."""
+    from .types import GopConfig
+
+    g = gop if gop is not None else GopConfig()
+    return dict(gop_delta=int(g.delta), gop_patch=int(g.patch), gop_t_bm=float(g.t_bm), gop_t_et=float(g.t_et),
+                gop_coarse_window=float(g.coarse_window), gop_coarse_step=float(g.coarse_step),
+                gop_fine_window=float(g.fine_window), gop_fine_step=float(g.fine_step))
 
 
 class FeatureEngine:
@@ -44,7 +51,8 @@ class FeatureEngine:
             width=width, height=height, n_octaves=cfg.n_octaves, threshold=int(cfg.threshold),
             mask_mode=_mode(mc), t_i=float(mc.t_i), t_h=int(mc.t_h), grid_rows=int(mc.grid[0]),
             grid_cols=int(mc.grid[1]), octave_for_mask=-1 if mc.octave_for_mask is None else int(mc.octave_for_mask),
-            per_layer=int(bool(mc.per_layer)), max_streams=int(n_streams), kp_capacity=int(kp_capacity))
+            per_layer=int(bool(mc.per_layer)), max_streams=int(n_streams), kp_capacity=int(kp_capacity),
+            **gop_fields(getattr(cfg, "gop", None)))
         L = _native.lib()
         _native.ensure_pattern()
         h = ctypes.c_void_p()

@@ -49,8 +49,6 @@ def run_pipeline_arrays(frames: list[GrayFrame], cfg: PipelineConfig):
 
     if not frames:
         raise ValueError("empty frame sequence")
-    if cfg.mask.mode == "temporal":
-        raise NotImplementedError("mask mode 'temporal' (block-matching baseline) is outside this hot path")
     H, W = frames[0].data.shape
     eng = FeatureEngine(W, H, cfg, n_streams=1)
     eng.set_timing(True)
@@ -86,8 +84,6 @@ def run_streams(frames, cfg: PipelineConfig, collect: bool = True):
     """
     import torch
 
-    if cfg.mask.mode == "temporal":
-        raise NotImplementedError("mask mode 'temporal' (block-matching baseline) is outside this hot path")
     if isinstance(frames, np.ndarray):
         frames_t = torch.from_numpy(np.ascontiguousarray(frames))
     else:

@@ -144,11 +144,35 @@ class MaskConfig:
 
 
 @dataclass(frozen=True)
+class GopConfig:
+    """temporal.py:23-43: the block-matching baseline's GOP and search parameters."""
+
+    delta: int = 10  # GOP length
+    patch: int = 16  # patch side length, pixels
+    t_bm: float = 1800.0  # SAD accept threshold
+    t_et: float = 1000.0  # early-termination SAD threshold
+    coarse_window: float = 12.0  # search extends +/- this many pixels
+    coarse_step: float = 2.0
+    fine_window: float = 1.75  # refinement extends +/- this around the coarse winner
+    fine_step: float = 0.25
+
+    def __post_init__(self):
+        if self.delta < 1:
+            raise ValueError("GOP length must be >= 1")
+        if self.patch % 2 != 0 or self.patch < 2:
+            raise ValueError("patch side must be even and positive")
+        if self.fine_step > self.coarse_step:
+            raise ValueError("fine_step must not exceed coarse_step")
+        if self.t_bm <= 0 or self.t_et <= 0:
+            raise ValueError("SAD thresholds must be positive")
+
+
+@dataclass(frozen=True)
 class PipelineConfig:
     threshold: int = DEFAULT_THRESHOLD
     n_octaves: int = 4
     mask: MaskConfig = field(default_factory=MaskConfig)
-    gop: object = None  # GopConfig of the temporal baseline (out of this path's scope)
+    gop: GopConfig = field(default_factory=GopConfig)  # temporal mode (pipeline.py:52)
     match: object = None  # MatchConfig (matching is downstream of this path)
     seed: int = 0
     parallel: bool = False  # accepted and ignored: the device path is always parallel

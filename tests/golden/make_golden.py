@@ -310,9 +310,97 @@ def make_matching():
     print("matching", {k: v.shape for k, v in mt.items() if k.startswith("plant_") and v.ndim == 2})
 
 
+def make_temporal():
+    """9. temporal block-matching baseline (temporal.py, pipeline.py:281-345), SURVEY.md 8(f) rank 2."""
+    import_reference()
+    import math
+
+    from vidfeat import synth, temporal
+    from vidfeat.masking import MaskConfig
+    from vidfeat.pipeline import PipelineConfig, run_pipeline
+    from vidfeat.pyramid import GrayFrame
+
+    tm = {}
+    tm["coarse_12_2"] = temporal.spiral_offsets(12.0, 2.0)
+    tm["fine_175_025"] = temporal.spiral_offsets(1.75, 0.25)
+    tm["odd_5_1"] = temporal.spiral_offsets(5.0, 1.0)
+    # per-feature searches: prev = smooth texture, cur = prev shifted (integer
+    # and quarter-pixel bilinear) + noise; centres include border cases
+    rng = np.random.default_rng(77)
+    H, W = 120, 160
+    base = rng.integers(0, 256, (H + 8, W + 8)).astype(np.float64)
+    k = np.ones(5) / 5
+    base = np.apply_along_axis(lambda r: np.convolve(r, k, "same"), 0, base)
+    base = np.apply_along_axis(lambda r: np.convolve(r, k, "same"), 1, base)
+    prev = np.clip(base[4:4 + H, 4:4 + W] * 1.6 - 60, 0, 255).astype(np.uint8)
+    cases = []
+    for ci, (sx, sy, noise) in enumerate([(3.0, -2.0, 0.0), (1.25, 0.5, 2.0), (-5.5, 4.75, 4.0), (9.0, 9.0, 8.0),
+                                          (0.0, 0.0, 30.0)]):
+        yy, xx = np.mgrid[0:H, 0:W].astype(np.float64)
+        srcx, srcy = np.clip(xx - sx, 0, W - 1.001), np.clip(yy - sy, 0, H - 1.001)
+        x0, y0 = np.floor(srcx).astype(int), np.floor(srcy).astype(int)
+        ax, ay = srcx - x0, srcy - y0
+        pf = prev.astype(np.float64)
+        cur = ((1 - ax) * (1 - ay) * pf[y0, x0] + ax * (1 - ay) * pf[y0, x0 + 1] + (1 - ax) * ay * pf[y0 + 1, x0]
+               + ax * ay * pf[y0 + 1, x0 + 1])
+        cur = np.clip(np.rint(cur + rng.normal(0, noise, cur.shape)), 0, 255).astype(np.uint8)
+        xs = np.concatenate([rng.uniform(0, W, 60), [7.5, 8.0, W - 8.5, W - 8.0, 152.4]])
+        ys = np.concatenate([rng.uniform(0, H, 60), [7.5, 8.0, H - 8.5, H - 8.0, 3.0]])
+        for gi, g in enumerate([temporal.GopConfig(), temporal.GopConfig(t_et=50.0, t_bm=2500.0),
+                                temporal.GopConfig(t_et=1.0, t_bm=900.0, coarse_window=6.0)]):
+            found, nx, ny, sad = [], [], [], []
+            half = g.patch // 2
+            for x, y in zip(xs, ys):
+                cxi, cyi = int(math.floor(x + 0.5)), int(math.floor(y + 0.5))
+                tlx, tly = cxi - half, cyi - half
+                ok = not (tlx < 0 or tly < 0 or tlx + g.patch > W or tly + g.patch > H)
+                res = (temporal.spiral_search(prev[tly:tly + g.patch, tlx:tlx + g.patch], GrayFrame(cur),
+                                              (float(x), float(y)), g) if ok else None)
+                found.append(res is not None)
+                nx.append(res[0][0] if res else 0.0)
+                ny.append(res[0][1] if res else 0.0)
+                sad.append(res[1] if res else 0.0)
+            key = f"bm{ci}_{gi}"
+            tm[f"{key}_found"] = np.array(found)
+            tm[f"{key}_nx"], tm[f"{key}_ny"], tm[f"{key}_sad"] = np.array(nx), np.array(ny), np.array(sad)
+            tm[f"{key}_gop"] = np.array([g.delta, g.patch, g.t_bm, g.t_et, g.coarse_window, g.coarse_step,
+                                         g.fine_window, g.fine_step])
+        tm[f"bm{ci}_prev"], tm[f"bm{ci}_cur"], tm[f"bm{ci}_x"], tm[f"bm{ci}_y"] = prev, cur, xs, ys
+    tm["n_bm"] = np.array(5)
+    np.savez_compressed(HERE / "temporal.npz", **tm)
+    # whole temporal pipeline runs (pipeline.py:281-345)
+    small, _ = synth.synth_sequence(
+        synth.moving_object_scene((128, 96), object_frac=0.2, velocity=(3.0, 0.0), seed=6), 7, (128, 96), seed=6)
+    sys.path.insert(0, str(HERE.parents[1]))
+    from paper_1503_06959_b200 import scenes
+
+    cfg1 = scenes.SceneConfig(320, 240, 7, 1, "objects", (3, 3), (1.0, 3.0), noise_sigma=2.0, seed=11)
+    scn = [GrayFrame(f, i) for i, f in enumerate(scenes.generate(cfg1)[0].numpy())]
+    runs = {
+        "small_temporal": (small, PipelineConfig(threshold=25, mask=MaskConfig(mode="temporal"),
+                                                 gop=temporal.GopConfig(delta=3))),
+        "scene_temporal": (scn, PipelineConfig(mask=MaskConfig(mode="temporal"), gop=temporal.GopConfig(delta=4))),
+    }
+    for name, (frames, cfg) in runs.items():
+        feats, reports = run_pipeline(frames, cfg)
+        g = cfg.gop
+        np.savez_compressed(
+            HERE / f"pipeline_{name}.npz",
+            frames=np.stack([f.data for f in frames]), threshold=np.array(cfg.threshold),
+            n_octaves=np.array(cfg.n_octaves), mode=np.array("temporal"),
+            gop=np.array([g.delta, g.patch, g.t_bm, g.t_et, g.coarse_window, g.coarse_step, g.fine_window,
+                          g.fine_step]),
+            **feats_to_arrays(feats), **reports_to_arrays(reports))
+        print(name, [len(f) for f in feats])
+
+
 if __name__ == "__main__":
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "temporal":
+        make_temporal()
+        sys.exit(0)
     if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "matching":
         make_matching()
     else:
         main()
         make_matching()
+        make_temporal()

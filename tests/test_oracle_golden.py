@@ -12,7 +12,7 @@ from conftest import GOLDEN, golden
 from oracle import oracle
 from paper_1503_06959_b200.pattern import build_default_pattern
 
-PIPELINES = sorted(p.stem[len("pipeline_"):] for p in GOLDEN.glob("pipeline_*.npz"))
+PIPELINES = sorted(p.stem[len("pipeline_"):] for p in GOLDEN.glob("pipeline_*.npz") if not p.stem.endswith("_temporal"))
 
 
 def test_pattern_matches_reference_builder():
@@ -150,3 +150,65 @@ def test_oracle_radius_match_golden():
     qi, ri, d = oracle.radius_match(np.packbits(g["w56_q_bits"], axis=1), np.packbits(g["w56_r_bits"], axis=1), 24)
     assert np.array_equal(np.stack([qi, ri, d], 1).reshape(-1, 3), g["w56_24"])
     assert int(g["default_radius"]) == 102
+
+
+def _gop_kw(gp):
+    return dict(delta=int(gp[0]), patch=int(gp[1]), t_bm=float(gp[2]), t_et=float(gp[3]),
+                coarse_window=float(gp[4]), coarse_step=float(gp[5]), fine_window=float(gp[6]),
+                fine_step=float(gp[7]))
+
+
+def test_spiral_offsets_golden():
+    """temporal.py:46-61 order: the oracle's and the product's host constants."""
+    from oracle import oracle
+    from paper_1503_06959_b200.temporal import spiral_offsets
+
+    g = golden("temporal.npz")
+    for key, (r, st) in {"coarse_12_2": (12.0, 2.0), "fine_175_025": (1.75, 0.25), "odd_5_1": (5.0, 1.0)}.items():
+        assert np.array_equal(oracle.spiral_offsets(r, st), g[key])
+        assert np.array_equal(spiral_offsets(r, st), g[key])
+
+
+def test_oracle_block_match_golden():
+    """Oracle spiral search == the reference's spiral_search (temporal.py:183-226) on
+    integer / quarter-pixel shifts, noise, border centres and three GopConfigs."""
+    from oracle import oracle
+
+    g = golden("temporal.npz")
+    for ci in range(int(g["n_bm"])):
+        for gi in range(3):
+            k = f"bm{ci}_{gi}"
+            f, nx, ny, sd = oracle.block_match(g[f"bm{ci}_prev"], g[f"bm{ci}_cur"], g[f"bm{ci}_x"], g[f"bm{ci}_y"],
+                                               **_gop_kw(g[f"{k}_gop"]))
+            assert np.array_equal(f, g[f"{k}_found"]), k
+            assert np.array_equal(nx, g[f"{k}_nx"]) and np.array_equal(ny, g[f"{k}_ny"]), k
+            assert np.array_equal(sd, g[f"{k}_sad"]), k
+
+
+@pytest.mark.parametrize("name", ["small_temporal", "scene_temporal"])
+def test_oracle_temporal_pipeline_golden(name):
+    """Oracle run_pipeline(mode='temporal') == the reference (pipeline.py:281-345)."""
+    from oracle import oracle
+    from paper_1503_06959_b200.pattern import default_pattern
+
+    g = golden(f"pipeline_{name}.npz")
+    ref = oracle.run_sequence(list(g["frames"]), default_pattern(), threshold=int(g["threshold"]),
+                              n_octaves=int(g["n_octaves"]), mode="temporal", gop=_gop_kw(g["gop"]))
+    off = g["offsets"]
+    for n, e in enumerate(ref):
+        a, b = off[n], off[n + 1]
+        for k in ("x", "y", "score", "origin", "age", "desc"):
+            assert np.array_equal(getattr(e, k), g[k][a:b]), (n, k)
+        assert np.abs(e.sigma - g["sigma"][a:b]).max(initial=0) <= 1e-12
+        assert np.abs(e.theta - g["theta"][a:b]).max(initial=0) <= 1e-9
+        assert (e.n_detected, e.n_total, e.n_dropped) == (g["r_n_detected"][n], g["r_n_total"][n], g["r_n_dropped"][n])
+        assert e.coverage == g["r_coverage"][n]
+
+
+def test_gop_config_validation():
+    from paper_1503_06959_b200.types import GopConfig
+
+    for kw, msg in [({"delta": 0}, "GOP length"), ({"patch": 15}, "patch side"), ({"fine_step": 3.0}, "fine_step"),
+                    ({"t_et": 0.0}, "SAD thresholds")]:
+        with pytest.raises(ValueError, match=msg):
+            GopConfig(**kw)
