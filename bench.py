@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="intensity", choices=["intensity", "binning", "none"])
+    ap.add_argument("--mode", default="intensity", choices=["intensity", "binning", "none", "temporal"])
     ap.add_argument("--streams", type=int, default=TOTAL_STREAMS)
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")

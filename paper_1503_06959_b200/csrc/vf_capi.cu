@@ -97,6 +97,9 @@ void gop_setup(const Gop& o, vft::Setup& q, std::vector<double>& co, std::vector
   q.rc = (int)std::ceil(mc);
   q.rfc = std::max(1, (int)std::ceil(mf));
   q.dyadic = dy && o.patch * o.patch * 255LL * 16 < (1LL << 24);
+  const int M = q.rc + q.rfc + 1;
+  (void)M;
+  q.shmask = 1;                                      // window only (shifted copies measured slower)
   vft::layout(q);
 }
 

@@ -59,6 +59,7 @@ struct Setup {
   int M;                  // window margin around the block: rc + rfc + 1
   int win_w, win_words;   // window bytes per row (P + 2M), words per row (+1 for funnel reads)
   int ht_w, ht_rows;      // fine tables: values per row (P + 2 rfc), rows (P + 2 rfc + 1)
+  int shmask;             // byte shifts (xr & 3) of coarse candidates: window copies kept
   int sm_words;           // shared words per warp
 };
 
@@ -72,7 +73,9 @@ inline void layout(Setup& q)
   const int patch_words = (q.P * q.P + 3) / 4, p16_words = (q.P * q.P + 1) / 2;
   const int win = q.win_w * q.win_words;
   const int tables = q.dyadic ? 4 * q.ht_rows * (q.ht_w / 2) * 2 : 0;
-  q.sm_words = patch_words + p16_words + win + tables;
+  // copy 0 is the window itself; copies for the other shifts coarse candidates use
+  const int ncopy = 1 + __builtin_popcount(q.shmask & 0xe);
+  q.sm_words = patch_words + p16_words + win * ncopy + tables;
 }
 
 #define BM_WARPS 4
@@ -92,23 +95,73 @@ __device__ bool search(const Setup& q, uint32_t* sm, const uint8_t* prev, long l
   uint32_t* pw = sm;                                   // block bytes, row-major, as words
   uint32_t* p16 = pw + (P * P + 3) / 4;                // 16 * block value, 16x2 pairs
   uint32_t* win = p16 + (P * P + 1) / 2;               // window rows
-  uint32_t* ht = win + q.win_w * q.win_words;          // fine tables (dyadic path)
+  const int wsz = q.win_w * q.win_words;
+  uint32_t* ht = win + wsz * (1 + __popc(q.shmask & 0xe));   // fine tables (dyadic path)
+  // copy c (c = 1..3, when used) holds the window shifted left by c bytes
+  auto copy_of = [&](int c) -> uint32_t* { return c == 0 ? win : win + wsz * __popc(q.shmask & 0xe & ((2 << c) - 1)); };
   uint8_t* pb = reinterpret_cast<uint8_t*>(pw);
-  for (int i = lane; i < P * P; i += 32) pb[i] = __ldg(prev + (long long)(tly + i / P) * prev_pitch + tlx + i % P);
-  // window [tlx - M, tlx + P + M) x [tly - M, tly + P + M) of cur, zero outside the frame
-  const int wx0 = tlx - q.M, wy0 = tly - q.M;
-  for (int i = lane; i < q.win_w * q.win_words; i += 32) {
-    const int r = i / q.win_words, k = i - r * q.win_words, yy = wy0 + r;
+  // word (r, k) of a w-word-wide region at (x0, y0) of a frame: aligned 4-byte
+  // loads + funnel shift when the row span lies inside the frame and rows are
+  // 4-byte aligned, else bytes (zero outside the frame)
+  auto fetch = [&](const uint8_t* f, long long fp, int x0, int yy, int k) -> uint32_t {
+    if (yy < 0 || yy >= h) return 0u;
+    const uint8_t* row = f + (long long)yy * fp;
+    const int xb = x0 + 4 * k;
+    // w % 4 == 0: the second aligned word of an in-row span never passes the row's end
+    if (xb >= 0 && xb + 4 <= w && (w & 3) == 0 && ((reinterpret_cast<uintptr_t>(row) | (uintptr_t)fp) & 3) == 0) {
+      const uint32_t* r32 = reinterpret_cast<const uint32_t*>(row) + (xb >> 2);
+      const uint32_t lo = __ldg(r32), hi = (xb & 3) ? __ldg(r32 + 1) : 0u;
+      return __funnelshift_r(lo, hi, 8 * (xb & 3));
+    }
     uint32_t v = 0;
-    if (yy >= 0 && yy < h) {
-      const uint8_t* row = cur + (long long)yy * pitch;
 #pragma unroll
-      for (int c = 0; c < 4; c++) {
-        const int xx = wx0 + 4 * k + c;
-        if (xx >= 0 && xx < w) v |= (uint32_t)__ldg(row + xx) << (8 * c);
+    for (int c = 0; c < 4; c++) {
+      const int xx = xb + c;
+      if (xx >= 0 && xx < w) v |= (uint32_t)__ldg(row + xx) << (8 * c);
+    }
+    return v;
+  };
+  if ((P & 3) == 0) {
+    const int pwr0 = P / 4;
+    for (int i = lane; i < P * pwr0; i += 32) pw[i] = fetch(prev, prev_pitch, tlx, tly + i / pwr0, i % pwr0);
+  } else {
+    for (int i = lane; i < P * P; i += 32) pb[i] = __ldg(prev + (long long)(tly + i / P) * prev_pitch + tlx + i % P);
+  }
+  // window [tlx - M, tlx + P + M) x [tly - M, tly + P + M) of cur, zero outside the frame;
+  // (row, word) of element i advanced incrementally (no division)
+  const int wx0 = tlx - q.M, wy0 = tly - q.M;
+  {
+    const int dr = 32 / q.win_words, dk = 32 - dr * q.win_words;
+    int r = lane / q.win_words, k = lane - r * q.win_words;
+    const bool inside = wx0 >= 0 && wy0 >= 0 && wx0 + 4 * q.win_words + 4 <= w && wy0 + q.win_w <= h && (w & 3) == 0 &&
+                        ((reinterpret_cast<uintptr_t>(cur) | (uintptr_t)pitch) & 3) == 0;
+    if (inside) {                                      // whole window in the frame: aligned funnel loads
+      const uint32_t* b32 = reinterpret_cast<const uint32_t*>(cur + (long long)wy0 * pitch) + (wx0 >> 2);
+      const int ps = (int)(pitch >> 2), sh = 8 * (wx0 & 3);
+      for (int i = lane; i < wsz; i += 32) {
+        const uint32_t* a = b32 + r * ps + k;
+        win[i] = __funnelshift_r(__ldg(a), __ldg(a + 1), sh);
+        r += dr;
+        k += dk;
+        if (k >= q.win_words) { k -= q.win_words; r++; }
+      }
+    } else {
+      for (int i = lane; i < wsz; i += 32) {
+        win[i] = fetch(cur, pitch, wx0, wy0 + r, k);
+        r += dr;
+        k += dk;
+        if (k >= q.win_words) { k -= q.win_words; r++; }
       }
     }
-    win[i] = v;
+  }
+  __syncwarp();
+  for (int c = 1; c < 4; c++) {                        // shifted copies (last word of a row: pad)
+    if (!((q.shmask >> c) & 1)) continue;
+    uint32_t* dst = copy_of(c);
+    for (int i = lane; i < wsz; i += 32) {
+      const bool last = (i + 1) % q.win_words == 0;
+      dst[i] = __funnelshift_r(win[i], last ? 0u : win[i + 1], 8 * c);
+    }
   }
   __syncwarp();
   for (int i = lane; i < (P * P + 1) / 2; i += 32) {
@@ -133,14 +186,17 @@ __device__ bool search(const Setup& q, uint32_t* sm, const uint8_t* prev, long l
     }
     const int xr = q.M + dx, yr = q.M + dy;            // window coordinates of the candidate
     const int o = xr >> 2, sh = 8 * (xr & 3);
+    const uint32_t* cw = copy_of(0) + yr * q.win_words + o;
     int sad = 0;
     for (int r = 0; r < P; r++) {
       if (valid) {
-        const uint32_t* row = win + (yr + r) * q.win_words + o;
+        const uint32_t* row = cw + r * q.win_words;
         const uint32_t* pr = pw + r * P / 4;
         if ((P & 3) == 0) {
-          for (int t = 0; t < pwr; t++)
-            sad = (int)__vsadu4(__funnelshift_r(row[t], row[t + 1], sh), pr[t]) + sad;
+          for (int t = 0; t < pwr; t++) {
+            const uint32_t a = __funnelshift_r(row[t], row[t + 1], sh);
+            asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %0;" : "+r"(sad) : "r"(a), "r"(pr[t]));
+          }
         } else {
           const uint8_t* wb = reinterpret_cast<const uint8_t*>(win + (yr + r) * q.win_words) + xr;
           const uint8_t* bb = pb + r * P;
@@ -185,9 +241,13 @@ __device__ bool search(const Setup& q, uint32_t* sm, const uint8_t* prev, long l
       const uint8_t* wb = reinterpret_cast<const uint8_t*>(win);
       const int wbp = 4 * q.win_words;
       auto raw = [&](int yy, int xx) -> uint32_t { return wb[(yy - wy0) * wbp + (xx - wx0)]; };
+      const int dr = 32 / pairs, dk = 32 - dr * pairs;
+      int rr = lane / pairs, kk = lane - rr * pairs;   // (phase-major row, pair) of element i
       for (int i = lane; i < 4 * q.ht_rows * pairs; i += 32) {
-        const int a = i / (q.ht_rows * pairs), rem = i - a * q.ht_rows * pairs;
-        const int r = rem / pairs, k = rem - r * pairs, yy = hy0 + r, xx = hx0 + 2 * k;
+        const int a = rr / q.ht_rows, r = rr - a * q.ht_rows, k = kk, yy = hy0 + r, xx = hx0 + 2 * k;
+        kk += dk;
+        rr += dr;
+        if (kk >= pairs) { kk -= pairs; rr++; }
         const uint32_t i0 = raw(yy, xx), i1 = raw(yy, xx + 1), i2 = raw(yy, xx + 2), i3 = raw(yy, xx + 3);
         const uint32_t h0 = (4 - a) * i0 + a * i1, h1 = (4 - a) * i1 + a * i2, h2 = (4 - a) * i2 + a * i3;
         uint32_t* te = ht + (a * q.ht_rows + r) * pairs * 2;
@@ -340,8 +400,12 @@ __global__ void __launch_bounds__(32 * BM_WARPS) k_blockmatch(const __grid_const
   const int total = pre[n_streams];
   uint32_t* sm = bm_sm + (threadIdx.x >> 5) * q.sm_words;
   for (int gi = blockIdx.x * BM_WARPS + (threadIdx.x >> 5); gi < total; gi += gridDim.x * BM_WARPS) {
-    int lo = 0, hi = n_streams;
-    while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= gi) lo = m; else hi = m; }
+    // stream of gi: number of stream starts <= gi, minus one (lanes test 32 starts at a time)
+    int lo = -1;
+    for (int base = 0; base < n_streams; base += 32) {
+      const int sl = base + (threadIdx.x & 31);
+      lo += __popc(__ballot_sync(0xffffffffu, sl < n_streams && pre[sl] <= gi));
+    }
     const int s = b.s0 + lo, i = gi - pre[lo];
     const int prevbuf = (b.ctr[s * C_NCTR + C_FRAME] & 1) ^ 1;
     const long long p = ((long long)s * 2 + prevbuf) * g.kp_cap + i;
