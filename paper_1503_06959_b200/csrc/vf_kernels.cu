@@ -1461,7 +1461,7 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
 // (layer, y): the reference order.
 #define NMS_WARPS 4
 #define NMS_THREADS (32 * NMS_WARPS)
-__global__ void __launch_bounds__(NMS_THREADS, 6) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+__global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int cand[NMS_WARPS][32];
   __shared__ int sq[NMS_WARPS][64];   // survivor queue (y << 16 | x)
