@@ -527,6 +527,15 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     }
   }
   const int tw = min(TW, g.W - X0), th = min(TH, g.H - Y0);
+  // an o0 tile inside the frame has every derived tile inside its layer (the
+  // tile origin is a multiple of 3 * 2^(O-1)): plain word stores, no bounds
+  const bool interior = tw == TW && th == TH;
+  auto put = [&](int l, int gx0, int gy0, int y, int x, uint32_t w) {
+    const LayerGeo& L = g.L[l];
+    uint8_t* gd = b.layers + (long long)s * g.layer_slab + L.layer_off + (long long)gy0 * L.pitch + gx0;
+    if (interior) *reinterpret_cast<uint32_t*>(gd + y * L.pitch + x) = w;
+    else store_word(gd, L.pitch, y, x, L.w - gx0, L.h - gy0, w);
+  };
   // ---- o0 tile ----
   {
     const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y0 * b.frame_pitch + X0;
@@ -545,7 +554,6 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     }
   }
   __syncthreads();
-  uint8_t* lay = b.layers + (long long)s * g.layer_slab;
   // ---- phase 1: i0 (2/3 resample) + o1 (halving) + row sums ----
   {
     // i0: 16 row pairs x 16 words, one 2x4 block per thread
@@ -563,29 +571,21 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     }
     uint32_t e = 0, o = 0;
 #pragma unroll
-    for (int c = 0; c < 4; c++) {
-      e |= ((2 * hs[0][c] + hs[1][c] + 4) / 9) << (8 * c);
-      o |= ((hs[1][c] + 2 * hs[2][c] + 4) / 9) << (8 * c);
+    for (int c = 0; c < 4; c++) {   // (v + 4) // 9 == ((v + 4) * 7282) >> 16 for v + 4 < 32768
+      e |= (((2 * hs[0][c] + hs[1][c] + 4) * 7282u) >> 16) << (8 * c);
+      o |= (((hs[1][c] + 2 * hs[2][c] + 4) * 7282u) >> 16) << (8 * c);
     }
     *reinterpret_cast<uint32_t*>(si0 + (2 * p) * 64 + 4 * q) = e;
     *reinterpret_cast<uint32_t*>(si0 + (2 * p + 1) * 64 + 4 * q) = o;
-    const LayerGeo& L1 = g.L[1];
-    const int gx0 = 2 * X0 / 3, gy0 = 2 * Y0 / 3;
-    uint8_t* gd = lay + L1.layer_off + (long long)gy0 * L1.pitch + gx0;
-    store_word(gd, L1.pitch, 2 * p, 4 * q, L1.w - gx0, L1.h - gy0, e);
-    store_word(gd, L1.pitch, 2 * p + 1, 4 * q, L1.w - gx0, L1.h - gy0, o);
+    put(1, 2 * X0 / 3, 2 * Y0 / 3, 2 * p, 4 * q, e);
+    put(1, 2 * X0 / 3, 2 * Y0 / 3, 2 * p + 1, 4 * q, o);
   }
-  {
-    const LayerGeo& L2 = g.L[2];
-    const int gx0 = X0 >> 1, gy0 = Y0 >> 1;
-    uint8_t* gd = lay + L2.layer_off + (long long)gy0 * L2.pitch + gx0;
-    for (int i = tid; i < 24 * 12; i += 256) {
-      const int y = i / 12, q = i - y * 12;
-      const uint32_t w = halve4(*reinterpret_cast<const uint2*>(t0 + (2 * y) * TW + 8 * q),
-                                *reinterpret_cast<const uint2*>(t0 + (2 * y + 1) * TW + 8 * q));
-      *reinterpret_cast<uint32_t*>(so1 + y * 48 + 4 * q) = w;
-      store_word(gd, L2.pitch, y, 4 * q, L2.w - gx0, L2.h - gy0, w);
-    }
+  for (int i = tid; i < 24 * 12; i += 256) {
+    const int y = i / 12, q = i - y * 12;
+    const uint32_t w = halve4(*reinterpret_cast<const uint2*>(t0 + (2 * y) * TW + 8 * q),
+                              *reinterpret_cast<const uint2*>(t0 + (2 * y + 1) * TW + 8 * q));
+    *reinterpret_cast<uint32_t*>(so1 + y * 48 + 4 * q) = w;
+    put(2, X0 >> 1, Y0 >> 1, y, 4 * q, w);
   }
   if (tid < 3 * th) {
     // row sums per 32-px SAT column of the tile (strip carries of the SATs)
@@ -603,17 +603,13 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si0 + (2 * y) * 64 + 8 * q),
                               *reinterpret_cast<const uint2*>(si0 + (2 * y + 1) * 64 + 8 * q));
     *reinterpret_cast<uint32_t*>(si1 + y * 32 + 4 * q) = w;
-    const LayerGeo& L = g.L[3];
-    const int gx0 = (2 * X0 / 3) >> 1, gy0 = (2 * Y0 / 3) >> 1;
-    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+    put(3, (2 * X0 / 3) >> 1, (2 * Y0 / 3) >> 1, y, 4 * q, w);
   } else if (tid < 128 + 72) {
     const int i = tid - 128, y = i / 6, q = i - y * 6;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(so1 + (2 * y) * 48 + 8 * q),
                               *reinterpret_cast<const uint2*>(so1 + (2 * y + 1) * 48 + 8 * q));
     *reinterpret_cast<uint32_t*>(so2 + y * 24 + 4 * q) = w;
-    const LayerGeo& L = g.L[4];
-    const int gx0 = X0 >> 2, gy0 = Y0 >> 2;
-    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+    put(4, X0 >> 2, Y0 >> 2, y, 4 * q, w);
   }
   __syncthreads();
   // ---- phase 3: i2 from i1, o3 from o2 ----
@@ -622,17 +618,13 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si1 + (2 * y) * 32 + 8 * q),
                               *reinterpret_cast<const uint2*>(si1 + (2 * y + 1) * 32 + 8 * q));
     *reinterpret_cast<uint32_t*>(si2 + y * 16 + 4 * q) = w;
-    const LayerGeo& L = g.L[5];
-    const int gx0 = (2 * X0 / 3) >> 2, gy0 = (2 * Y0 / 3) >> 2;
-    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+    put(5, (2 * X0 / 3) >> 2, (2 * Y0 / 3) >> 2, y, 4 * q, w);
   } else if (tid < 32 + 18) {
     const int i = tid - 32, y = i / 3, q = i - y * 3;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(so2 + (2 * y) * 24 + 8 * q),
                               *reinterpret_cast<const uint2*>(so2 + (2 * y + 1) * 24 + 8 * q));
     *reinterpret_cast<uint32_t*>(so3 + y * 12 + 4 * q) = w;
-    const LayerGeo& L = g.L[6];
-    const int gx0 = X0 >> 3, gy0 = Y0 >> 3;
-    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+    put(6, X0 >> 3, Y0 >> 3, y, 4 * q, w);
   }
   __syncthreads();
   // ---- phase 4: i3 from i2; IDDM on o3 (masking.py:84-93) ----
@@ -640,9 +632,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     const int y = tid >> 1, q = tid & 1;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si2 + (2 * y) * 16 + 8 * q),
                               *reinterpret_cast<const uint2*>(si2 + (2 * y + 1) * 16 + 8 * q));
-    const LayerGeo& L = g.L[7];
-    const int gx0 = (2 * X0 / 3) >> 3, gy0 = (2 * Y0 / 3) >> 3;
-    store_word(lay + L.layer_off + (long long)gy0 * L.pitch + gx0, L.pitch, y, 4 * q, L.w - gx0, L.h - gy0, w);
+    put(7, (2 * X0 / 3) >> 3, (2 * Y0 / 3) >> 3, y, 4 * q, w);
   }
   if (g.mask_mode == 1 && tid >= 32 && tid < 128) {
     unsigned long long covered = 0;
