@@ -963,8 +963,9 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
   const int n_work = pre[n_streams];
   const int t = g.threshold;
   for (int item = blockIdx.x * FAST_WARPS + wid; item < n_work; item += gridDim.x * FAST_WARPS) {
-    int lo = 0, hi = n_streams;
-    while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
+    int lo = -1;                           // stream of item: stream starts <= item, minus one
+    for (int sb = 0; sb < n_streams; sb += 32)
+      lo += __popc(__ballot_sync(0xffffffffu, sb + lane < n_streams && pre[sb + lane] <= item));
     const int s = b.s0 + lo;
     const int witem = b.worklist[(long long)s * g.tiles_per_stream + (item - pre[lo])];
     const bool clear_only = (witem & VF_CLEAR) != 0;
@@ -1002,7 +1003,7 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       const int rr = i / (FT_COLS / 16), c16 = i - rr * (FT_COLS / 16);
       const int y = y0 - 3 + rr, x = x0 - 16 + 16 * c16;
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (y >= 0 && y < h) {
+      if (y >= 0 && y < h && x + 16 > 0 && x < w) {   // chunks wholly outside the layer stay zero
         const uint8_t* row = lp + (long long)y * pitch;
         if (vec_ok && x >= 0 && x + 16 <= pitch && x + 16 <= ((w + 15) & ~15)) {
           v = __ldg(reinterpret_cast<const uint4*>(row + x));
@@ -1064,18 +1065,16 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
           pass &= gate & inb;
         }
       }
+      // queue slots: exclusive prefix of the per-lane counts (0..4) from
+      // bit-plane ballots; only set pass bits are written
       const int np = __popc(pass);
-      int incl = np;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      int pos = qn + incl - np;
-#pragma unroll
-      for (int i = 0; i < 4; i++)
-        if (pass & (0x80u << (8 * i))) fw.queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + i);
-      qn += __shfl_sync(0xffffffffu, incl, 31);
+      const unsigned b0 = __ballot_sync(0xffffffffu, np & 1), b1 = __ballot_sync(0xffffffffu, np & 2),
+                     b2 = __ballot_sync(0xffffffffu, np & 4);
+      const unsigned lt = (1u << lane) - 1u;
+      int pos = qn + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+      for (uint32_t pm = pass; pm; pm &= pm - 1u)
+        fw.queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + ((__ffs(pm) - 1) >> 3));
+      qn += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
     }
     __syncwarp();
     // ---- pass 2: exact score of queued pixels ----
