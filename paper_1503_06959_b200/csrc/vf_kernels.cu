@@ -1761,11 +1761,10 @@ __device__ __forceinline__ BoxQ box_query(const uint32_t* S, const Geo& g, doubl
     fx = kx + sg * px + 0.5;
     fy = ky + sg * py + 0.5;
   }
-  // clamp in fp64 (same as clamping the floored integer), then 32-bit ints
-  const double xd = fmin(fmax(floor(fx), 0.0), (double)(g.W - 1));
-  const double yd = fmin(fmax(floor(fy), 0.0), (double)(g.H - 1));
-  const int x = (int)xd, y = (int)yd;
-  const int r = (int)floor(rad * sg + 0.5);
+  // floor to int in one conversion (positions are within +/-2^31), then clamp
+  const int x = min(max(__double2int_rd(fx), 0), g.W - 1);
+  const int y = min(max(__double2int_rd(fy), 0), g.H - 1);
+  const int r = __double2int_rd(rad * sg + 0.5);
   BoxQ q;
   q.x0 = max(x - r, 0); q.x1 = min(x + r, g.W - 1);
   q.y0 = max(y - r, 0); q.y1 = min(y + r, g.H - 1);
