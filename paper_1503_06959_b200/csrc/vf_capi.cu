@@ -279,6 +279,10 @@ struct vf_ctx {
   int cur_group = 0;
   // stream groups: independent stream ranges launched on their own CUDA streams
   int n_groups_max = 0;
+  // side stream per launch group: the worklist's carries / propagation counts
+  // run concurrently with k_fast and join before k_nms
+  std::vector<cudaStream_t> aux;
+  std::vector<cudaEvent_t> aux_in, aux_out;
   std::vector<cudaStream_t> gstreams;
   std::vector<cudaEvent_t> gjoin;
   cudaEvent_t gfork = nullptr;
@@ -496,6 +500,9 @@ int vf_destroy(vf_ctx* c)
   pipe_free(c);
   pack_free(c);
   for (size_t k = 0; k < c->gstreams.size(); k++) { cudaStreamDestroy(c->gstreams[k]); cudaEventDestroy(c->gjoin[k]); }
+  for (size_t k = 0; k < c->aux.size(); k++) {
+    cudaStreamDestroy(c->aux[k]); cudaEventDestroy(c->aux_in[k]); cudaEventDestroy(c->aux_out[k]);
+  }
   if (c->gfork) cudaEventDestroy(c->gfork);
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
@@ -588,12 +595,28 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   const int tile_ctas = cdiv(g.tiles_per_stream, 256);   // lane per FAST tile
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
   const int carry_ctas = cdiv(g.sty, 8);
-  k_worklist<<<dim3(tile_ctas + cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, st>>>(
-      g, b, tile_ctas, cov_ctas, carry_ctas);
+  // strip carries, propagation counts and per_layer coverage on the side stream
+  // (needed from k_nms on), the tile work list on the main stream (k_fast)
+  const int gi = c->cur_group;
+  while ((int)c->aux.size() <= gi) {
+    cudaStream_t as;
+    cudaEvent_t ei, eo;
+    if (cudaStreamCreateWithFlags(&as, cudaStreamNonBlocking) != cudaSuccess) return VF_ERR_CUDA;
+    cudaEventCreateWithFlags(&ei, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&eo, cudaEventDisableTiming);
+    c->aux.push_back(as); c->aux_in.push_back(ei); c->aux_out.push_back(eo);
+  }
+  cudaEventRecord(c->aux_in[gi], st);
+  k_worklist<<<dim3(tile_ctas, n), 256, 0, st>>>(g, b, tile_ctas, 0, 0);
+  cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
+  k_worklist<<<dim3(cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, c->aux[gi]>>>(
+      g, b, 0, cov_ctas, carry_ctas);
+  cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n);
   stage_mark(c, 4, st);
+  cudaStreamWaitEvent(st, c->aux_out[gi], 0);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
