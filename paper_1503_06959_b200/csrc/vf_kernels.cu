@@ -1971,7 +1971,7 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
 // are copied by the whole CTA as consecutive 16-B words (coalesced).
 #define PROP_PER (PROP_CHUNK / 256)
 static_assert(PROP_PER * 7 <= 32, "flag + rank packing");
-__global__ void __launch_bounds__(256, 3) k_propagate(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+__global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   __shared__ int wsum[PROP_PER][8];
   __shared__ int dsts[PROP_CHUNK];
@@ -1986,14 +1986,14 @@ __global__ void __launch_bounds__(256, 3) k_propagate(const __grid_constant__ Ge
   const long long ob = ((long long)s * 2 + cur) * g.kp_cap;
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const int base = c * PROP_CHUNK;
-    double xs[PROP_PER], ys[PROP_PER], ss[PROP_PER], ts[PROP_PER], vs[PROP_PER];
-    int ag[PROP_PER];
+    // phase 1: the merge bit of every feature of the chunk -> destination slots
+    double xs[PROP_PER], ys[PROP_PER];
 #pragma unroll
     for (int j = 0; j < PROP_PER; j++) {
       const int e = base + j * 256 + tid;
-      const bool ok = e < n_prev;
-      const long long p = fb + (ok ? e : 0);
-      xs[j] = b.fx[p]; ys[j] = b.fy[p]; ss[j] = b.fs[p]; ts[j] = b.ft[p]; vs[j] = b.fv[p]; ag[j] = b.fage[p];
+      const long long p = fb + (e < n_prev ? e : 0);
+      xs[j] = b.fx[p];
+      ys[j] = b.fy[p];
     }
     unsigned fl = 0;
 #pragma unroll
@@ -2007,7 +2007,7 @@ __global__ void __launch_bounds__(256, 3) k_propagate(const __grid_constant__ Ge
     }
     __syncthreads();
     // element (j, tid) goes after all of group j' < j and warps w < wid of group j
-    int before = 0, acc = 0;
+    int acc = 0;
     const long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
 #pragma unroll
     for (int j = 0; j < PROP_PER; j++) {
@@ -2018,21 +2018,27 @@ __global__ void __launch_bounds__(256, 3) k_propagate(const __grid_constant__ Ge
         inwarp += w < wid ? v : 0;
         grp += v;
       }
-      before = acc + inwarp;
+      const long long dst = dst0 + acc + inwarp + ((fl >> (4 + 6 * j)) & 0x3fu);
       acc += grp;
-      const bool f = (fl >> j) & 1u;
-      const long long dst = dst0 + before + ((fl >> (4 + 6 * j)) & 0x3fu);
-      const bool w_ = f && dst < g.kp_cap;
-      dsts[j * 256 + tid] = w_ ? (int)dst : -1;
-      if (w_) {
-        const long long o = ob + dst;
-        b.fx[o] = xs[j]; b.fy[o] = ys[j]; b.fs[o] = ss[j]; b.ft[o] = ts[j]; b.fv[o] = vs[j];
-        b.forg[o] = 1; b.fage[o] = ag[j] + 1;
-      }
+      dsts[j * 256 + tid] = ((fl >> j) & 1u) && dst < g.kp_cap ? (int)dst : -1;
     }
     __syncthreads();
-    // descriptors: 4 x 16 B per feature, word q = feature q / 4, part q % 4
+    // phase 2: every field copied by the whole CTA in source order (loads
+    // independent of each other, stores mostly contiguous)
     const int nvalid = min(PROP_CHUNK, n_prev - base);
+#pragma unroll
+    for (int j = 0; j < PROP_PER; j++) {
+      const int f = j * 256 + tid;
+      const int dst = f < nvalid ? dsts[f] : -1;
+      if (dst >= 0) {
+        const long long p = fb + base + f, o = ob + dst;
+        const double x = b.fx[p], y = b.fy[p], sg = b.fs[p], th = b.ft[p], v = b.fv[p];
+        const int ag = b.fage[p];
+        b.fx[o] = x; b.fy[o] = y; b.fs[o] = sg; b.ft[o] = th; b.fv[o] = v;
+        b.forg[o] = 1; b.fage[o] = ag + 1;
+      }
+    }
+    // descriptors: 4 x 16 B per feature, word q = feature q / 4, part q % 4
     const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + (fb + base) * 64);
     uint4* dstd = reinterpret_cast<uint4*>(b.fdesc + ob * 64);
 #pragma unroll
