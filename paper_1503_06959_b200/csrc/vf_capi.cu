@@ -282,7 +282,7 @@ struct vf_ctx {
   // side stream per launch group: the worklist's carries / propagation counts
   // run concurrently with k_fast and join before k_nms
   std::vector<cudaStream_t> aux;
-  std::vector<cudaEvent_t> aux_in, aux_out;
+  std::vector<cudaEvent_t> aux_in, aux_mid, aux_out;
   std::vector<cudaStream_t> gstreams;
   std::vector<cudaEvent_t> gjoin;
   cudaEvent_t gfork = nullptr;
@@ -501,7 +501,8 @@ int vf_destroy(vf_ctx* c)
   pack_free(c);
   for (size_t k = 0; k < c->gstreams.size(); k++) { cudaStreamDestroy(c->gstreams[k]); cudaEventDestroy(c->gjoin[k]); }
   for (size_t k = 0; k < c->aux.size(); k++) {
-    cudaStreamDestroy(c->aux[k]); cudaEventDestroy(c->aux_in[k]); cudaEventDestroy(c->aux_out[k]);
+    cudaStreamDestroy(c->aux[k]); cudaEventDestroy(c->aux_in[k]); cudaEventDestroy(c->aux_mid[k]);
+    cudaEventDestroy(c->aux_out[k]);
   }
   if (c->gfork) cudaEventDestroy(c->gfork);
   if (c->pack.pre) cudaFree(c->pack.pre);
@@ -600,23 +601,29 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   const int gi = c->cur_group;
   while ((int)c->aux.size() <= gi) {
     cudaStream_t as;
-    cudaEvent_t ei, eo;
+    cudaEvent_t ei, em, eo;
     if (cudaStreamCreateWithFlags(&as, cudaStreamNonBlocking) != cudaSuccess) return VF_ERR_CUDA;
     cudaEventCreateWithFlags(&ei, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&em, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&eo, cudaEventDisableTiming);
-    c->aux.push_back(as); c->aux_in.push_back(ei); c->aux_out.push_back(eo);
+    c->aux.push_back(as); c->aux_in.push_back(ei); c->aux_mid.push_back(em); c->aux_out.push_back(eo);
   }
   cudaEventRecord(c->aux_in[gi], st);
   k_worklist<<<dim3(tile_ctas, n), 256, 0, st>>>(g, b, tile_ctas, 0, 0);
   cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
-  k_worklist<<<dim3(cov_ctas + carry_ctas + (g.mask_mode ? PROP_CTAS : 0), n), 256, 0, c->aux[gi]>>>(
+  const bool prop = g.mask_mode == 1 || g.mask_mode == 2;
+  k_worklist<<<dim3(cov_ctas + carry_ctas + (prop ? PROP_CTAS : 0), n), 256, 0, c->aux[gi]>>>(
       g, b, 0, cov_ctas, carry_ctas);
+  cudaEventRecord(c->aux_mid[gi], c->aux[gi]);
+  // Eq. 1 propagation into the last n_prop slots of the list: independent of
+  // the detection, so it runs beside k_fast / k_nms
+  if (prop) k_propagate<<<dim3(PROP_CTAS, n), 256, 0, c->aux[gi]>>>(g, b);
   cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n);
   stage_mark(c, 4, st);
-  cudaStreamWaitEvent(st, c->aux_out[gi], 0);
+  cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
@@ -625,7 +632,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
   k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
   stage_mark(c, 7, st);
-  if (g.mask_mode) k_propagate<<<dim3(PROP_CTAS, n), 256, 0, st>>>(g, b);
+  cudaStreamWaitEvent(st, c->aux_out[gi], 0);
   stage_mark(c, 8, st);
   k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
   stage_mark(c, -1, st);
@@ -836,8 +843,8 @@ int vf_get_features(vf_ctx* c, int s, vf_features* out, void* stream)
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_status(e);
   const int buf = (int)((c->frames_done[s] - 1) & 1);
-  const long long o = ((long long)s * 2 + buf) * c->g.kp_cap;
   out->n = ctr[C_NFEAT0 + buf];
+  const long long o = ((long long)s * 2 + buf) * c->g.kp_cap + (c->g.kp_cap - out->n);   // lists end at the buffer end
   out->x = c->b.fx + o; out->y = c->b.fy + o; out->sigma = c->b.fs + o; out->theta = c->b.ft + o;
   out->score = c->b.fv + o; out->origin = c->b.forg + o; out->age = c->b.fage + o; out->desc = c->b.fdesc + o * 64;
   if (ctr[C_ERR]) return VF_ERR_CAPACITY;
@@ -1241,6 +1248,7 @@ int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, co
   k_carries<<<dim3(c->g.sty, 1), 32, 0, st>>>(c->g, b);
   int ctr0[C_NCTR] = {0};
   ctr0[C_NDET] = n;              // k_sat builds every tile of a stream with keypoints (unmasked)
+  ctr0[C_NTOTAL] = n;            // the describe kernels write the n outputs as a full list
   cudaMemcpyAsync(b.ctr, ctr0, sizeof(ctr0), cudaMemcpyHostToDevice, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1);   // stream 0 -> slot 0
   k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev,

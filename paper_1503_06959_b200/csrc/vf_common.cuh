@@ -30,6 +30,7 @@ enum {
   C_NSURV = 10,     // NMS survivors (before border filter)
   C_NCAND = 11,     // FAST candidates
   C_EPOCH = 12,     // monotonic step id (activity stamps), survives vf_reset
+  C_PTICKET = 13,   // last-CTA ticket of the propagation-count CTAs (k_worklist)
   C_NCTR = 16
 };
 #define VF_ERRBIT_CAPACITY 1
@@ -177,10 +178,31 @@ __device__ __forceinline__ int merge_mask_at(const Geo& g, const Bufs& b, int s,
   return v;
 }
 
+// Feature lists are stored at the END of their buffer: buffer `buf` of stream s
+// holding n features uses slots [kp_cap - n, kp_cap), detected first, then
+// propagated.  Propagated features (slots >= kp_cap - n_prop) can then be
+// written before the detected count is known.
+__device__ __forceinline__ long long feat_base(const Geo& g, int s, int buf, int n)
+{
+  return ((long long)s * 2 + buf) * g.kp_cap + (g.kp_cap - n);
+}
+
 __device__ __forceinline__ int use_mask(const Geo& g, const Bufs& b, int s)
 {
   // pipeline.py:234; temporal mode detects without a mask at GOP starts (temporal.py:287-288)
   return g.mask_mode != 0 && g.mask_mode != 3 && b.ctr[s * C_NCTR + C_FRAME] > 0;
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
+{
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
 }
 
 template <typename T>

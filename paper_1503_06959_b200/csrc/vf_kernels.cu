@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(1024) k_binmask(const __grid_constant__ Geo g,
   const int* ctr = b.ctr + s * C_NCTR;
   const int prev = (ctr[C_FRAME] & 1) ^ 1;
   const int n_prev = ctr[C_NFEAT0 + prev];
-  const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
+  const long long fb = feat_base(g, s, prev, n_prev);
   const double sx = (double)G.cw, sy = (double)G.ch;   // ceil(W/cols), ceil(H/rows)
   for (int i = threadIdx.x; i < n_prev; i += blockDim.x) {
     double fx = floor(b.fx[fb + i] / sx), fy = floor(b.fy[fb + i] / sy);
@@ -759,11 +759,12 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
     // 1024-feature chunk of the previous list (masking.py:176-183)
     if (!um) return;
     __shared__ int sm_warp[32];
-    const int* ctr = b.ctr + s * C_NCTR;
+    __shared__ int last_sm;
+    int* ctr = b.ctr + s * C_NCTR;
     const int prev = (ctr[C_FRAME] & 1) ^ 1;
     const int n_prev = ctr[C_NFEAT0 + prev];
     const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
-    const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
+    const long long fb = feat_base(g, s, prev, n_prev);
     for (int c = blockIdx.x - tile_ctas - cov_ctas - carry_ctas; c < nch; c += PROP_CTAS) {
       int cnt = 0;
       const int e0 = c * PROP_CHUNK + threadIdx.x * (PROP_CHUNK / 256);
@@ -774,6 +775,28 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
       block_excl_scan<int>(cnt, sm_warp, tot);
       if (threadIdx.x == 0) b.prop_cnt[(long long)s * g.prop_chunks + c] = tot;
     }
+    // the last of the stream's count CTAs scans the chunk counts into output
+    // offsets and the propagated total (known before the detection finishes)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      last_sm = atomicAdd(ctr + C_PTICKET, 1) == PROP_CTAS - 1;
+      if (last_sm) ctr[C_PTICKET] = 0;
+    }
+    __syncthreads();
+    if (!last_sm || threadIdx.x >= 32) return;
+    __threadfence();
+    const int* pc = b.prop_cnt + (long long)s * g.prop_chunks;
+    int* po = b.prop_out + (long long)s * g.prop_chunks;
+    int carry = 0, tot;
+    for (int base = 0; base < nch; base += 32) {
+      const int i = base + lane;
+      const int k = i < nch ? __ldcg(pc + i) : 0;
+      const int ex = warp_excl_scan(k, lane, tot);
+      if (i < nch) po[i] = carry + ex;
+      carry += tot;
+    }
+    if (lane == 0) ctr[C_NPROP] = carry;
     return;
   }
   if ((int)blockIdx.x >= tile_ctas) {
@@ -1375,18 +1398,6 @@ __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int 
   }
 }
 
-__device__ __forceinline__ int warp_excl_scan(int v, int lane, int& total)
-{
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
-}
-
 // Last warp of stream s: band offsets, propagation-chunk offsets, FrameReport.
 __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
 {
@@ -1407,20 +1418,8 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
     carry += tot;
   }
   const int n_det = carry;
-  carry = 0;
-  int* pc = b.prop_cnt + (long long)s * g.prop_chunks;
-  int* po = b.prop_out + (long long)s * g.prop_chunks;
-  const int* ctr0 = b.ctr + s * C_NCTR;
-  const int n_prev = use_mask(g, b, s) ? ctr0[C_NFEAT0 + ((ctr0[C_FRAME] & 1) ^ 1)] : 0;
-  const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
-  for (int base = 0; base < nch; base += 32) {
-    const int i = base + lane;
-    const int k = i < nch ? __ldcg(pc + i) : 0;
-    const int ex = warp_excl_scan(k, lane, tot);
-    if (i < nch) po[i] = carry + ex;
-    carry += tot;
-  }
-  const int n_prop = carry;
+  // propagated total: scanned by k_worklist (joined before this launch)
+  const int n_prop = use_mask(g, b, s) ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     n_drop += __shfl_down_sync(0xffffffffu, n_drop, o);
@@ -1856,7 +1855,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
       const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
       s_l = b.s0 + sl;
       const int cur = b.ctr[s_l * C_NCTR + C_FRAME] & 1;
-      o_l = ((long long)s_l * 2 + cur) * g.kp_cap + i;
+      o_l = feat_base(g, s_l, cur, b.ctr[s_l * C_NCTR + C_NTOTAL]) + i;
       if (pass == 0) {
         const long long si = (long long)s_l * g.kp_cap + __ldg(b.gidx + (long long)s_l * g.kp_cap + i);   // staging slot
         kx_l = b.st_x[si]; ky_l = b.st_y[si]; sg_l = b.st_s[si];
@@ -1921,7 +1920,7 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
     long long o = -1;
     if (gi < total) {
       const int sl = find_stream(pre, n_streams, gi), s = b.s0 + sl, i = gi - pre[sl];
-      o = ((long long)s * 2 + (b.ctr[s * C_NCTR + C_FRAME] & 1)) * g.kp_cap + i;
+      o = feat_base(g, s, b.ctr[s * C_NCTR + C_FRAME] & 1, b.ctr[s * C_NCTR + C_NTOTAL]) + i;
       const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + o * 64);
 #pragma unroll
       for (int q = 0; q < 4; q++) {
@@ -1980,10 +1979,10 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
   const int* ctr = b.ctr + s * C_NCTR;
   const int cur = ctr[C_FRAME] & 1, prev = cur ^ 1;
   const int n_prev = ctr[C_NFEAT0 + prev];
-  const int n_det = ctr[C_NDET];
+  const int n_prop = ctr[C_NPROP];                       // from k_worklist (same stream, earlier)
   const int nch = (n_prev + PROP_CHUNK - 1) / PROP_CHUNK;
-  const long long fb = ((long long)s * 2 + prev) * g.kp_cap;
-  const long long ob = ((long long)s * 2 + cur) * g.kp_cap;
+  const long long fb = feat_base(g, s, prev, n_prev);
+  const long long ob = feat_base(g, s, cur, n_prop);     // the propagated segment: the last n_prop slots
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const int base = c * PROP_CHUNK;
     // phase 1: the merge bit of every feature of the chunk -> destination slots
@@ -2008,7 +2007,7 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
     __syncthreads();
     // element (j, tid) goes after all of group j' < j and warps w < wid of group j
     int acc = 0;
-    const long long dst0 = (long long)n_det + b.prop_out[(long long)s * g.prop_chunks + c];
+    const long long dst0 = b.prop_out[(long long)s * g.prop_chunks + c];
 #pragma unroll
     for (int j = 0; j < PROP_PER; j++) {
       int inwarp = 0, grp = 0;
@@ -2020,7 +2019,7 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
       }
       const long long dst = dst0 + acc + inwarp + ((fl >> (4 + 6 * j)) & 0x3fu);
       acc += grp;
-      dsts[j * 256 + tid] = ((fl >> j) & 1u) && dst < g.kp_cap ? (int)dst : -1;
+      dsts[j * 256 + tid] = ((fl >> j) & 1u) && dst < n_prop ? (int)dst : -1;
     }
     __syncthreads();
     // phase 2: every field copied by the whole CTA in source order (loads
@@ -2031,7 +2030,7 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
       const int f = j * 256 + tid;
       const int dst = f < nvalid ? dsts[f] : -1;
       if (dst >= 0) {
-        const long long p = fb + base + f, o = ob + dst;
+        const long long p = fb + base + f, o = ob + dst;   // ob: segment start
         const double x = b.fx[p], y = b.fy[p], sg = b.fs[p], th = b.ft[p], v = b.fv[p];
         const int ag = b.fage[p];
         b.fx[o] = x; b.fy[o] = y; b.fs[o] = sg; b.ft[o] = th; b.fv[o] = v;
@@ -2040,7 +2039,7 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
     }
     // descriptors: 4 x 16 B per feature, word q = feature q / 4, part q % 4
     const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + (fb + base) * 64);
-    uint4* dstd = reinterpret_cast<uint4*>(b.fdesc + ob * 64);
+    uint4* dstd = reinterpret_cast<uint4*>(b.fdesc + ob * 64);   // segment start
 #pragma unroll
     for (int half = 0; half < 2; half++) {
       uint4 d[8];
@@ -2086,7 +2085,7 @@ __global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, con
     const int s = lo, k = (int)(i - pre[s]);
     const int* ctr = b.ctr + s * C_NCTR;
     const int buf = buf_override >= 0 ? buf_override : ((ctr[C_FRAME] - 1) & 1);
-    const long long f = ((long long)s * 2 + buf) * g.kp_cap + k;
+    const long long f = feat_base(g, s, buf, ctr[C_NFEAT0 + buf]) + k;
     px[i] = b.fx[f]; py[i] = b.fy[f]; ps[i] = b.fs[f]; pt[i] = b.ft[f]; pv[i] = b.fv[f];
     po[i] = b.forg[f]; pa[i] = b.fage[f];
     const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + f * 64);

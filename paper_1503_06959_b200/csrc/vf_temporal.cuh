@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(32 * BM_WARPS) k_blockmatch(const __grid_const
     }
     const int s = b.s0 + lo, i = gi - pre[lo];
     const int prevbuf = (b.ctr[s * C_NCTR + C_FRAME] & 1) ^ 1;
-    const long long p = ((long long)s * 2 + prevbuf) * g.kp_cap + i;
+    const long long p = feat_base(g, s, prevbuf, b.ctr[s * C_NCTR + C_NFEAT0 + prevbuf]) + i;
     const uint8_t* cur = b.frames + (long long)(s - b.s0) * b.frame_stride;
     const uint8_t* prv = b.prev_frame + (long long)s * g.W * g.H;
     double ax = 0, ay = 0, as = 0;
@@ -441,16 +441,24 @@ __global__ void __launch_bounds__(256) k_bm_write(const __grid_constant__ Geo g,
   const int nch = (n_prev + 1023) / 1024;
   if (c >= max(nch, 1)) return;
   const int* cnt = b.bm_chunk + (long long)s * g.prop_chunks;
+  __shared__ int tot_sm;
   if (wid == 0) {
-    int acc = 0;
-    for (int k = lane; k < (c == 0 ? nch : c); k += 32) acc += cnt[k];
+    int before = 0, all = 0;
+    for (int k = lane; k < nch; k += 32) {
+      const int v = cnt[k];
+      all += v;
+      before += k < c ? v : 0;
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) base_sm = acc;
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if (lane == 0) { base_sm = before; tot_sm = all; }
   }
   __syncthreads();
   if (c == 0) {
-    const int total = base_sm;
+    const int total = tot_sm;
     if (tid == 0) {
       ctr[C_NDET] = 0; ctr[C_NPROP] = total; ctr[C_NTOTAL] = total; ctr[C_NDROP] = 0; ctr[C_NSURV] = 0;
       double* rp = b.report + (long long)s * 16;
@@ -458,12 +466,9 @@ __global__ void __launch_bounds__(256) k_bm_write(const __grid_constant__ Geo g,
       rp[5] = ctr[C_FRAME]; rp[6] = 0; rp[7] = 0;
       rp[9] += total; rp[11] += 1.0;
     }
-    __syncthreads();
-    if (tid == 0) base_sm = 0;
-    __syncthreads();
   }
   if (nch == 0) return;
-  const long long fb = ((long long)s * 2 + prev) * g.kp_cap, ob = ((long long)s * 2 + cur) * g.kp_cap;
+  const long long fb = feat_base(g, s, prev, n_prev), ob = feat_base(g, s, cur, tot_sm);
   const long long so = (long long)s * g.kp_cap;
   int f[4];
 #pragma unroll
