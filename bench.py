@@ -307,6 +307,7 @@ def run_reference(args, rank, world):
 # Hamming radius matching workload
 # ----------------------------------------------------------------------------
 POPC_PEAK_PER_CLK_SM = 15.6   # measured, tools/micro/popc_bench.cu (profiles/r01_popc_peak.txt)
+IMMA_PEAK_TOPS = 1112.0       # measured mma.sync m16n8k32 u8, tools/micro/imma_bench.cu (same file)
 T_M = 102
 
 
@@ -450,9 +451,10 @@ def run_match(args, rank, world, local):
     k1.record(stream)
     torch.cuda.synchronize()
     kms = k0.elapsed_time(k1)
-    popc = 16.0 * n_pairs_step          # 16 x 32-bit popcounts per pair of 512-bit descriptors
-    peak = POPC_PEAK_PER_CLK_SM * 148 * 1.965e9 / 1e12
-    ach = popc / (kms / 1e3) / 1e12
+    # tensor-core path: q.r of 512 0/1 bytes per pair (2 x 512 int8 ops per pair)
+    ops = 2.0 * 512 * n_pairs_step
+    peak = IMMA_PEAK_TOPS
+    ach = ops / (kms / 1e3) / 1e12
     # e2e: host packed descriptors (pinned) -> H2D -> radius match -> D2H of the matches
     host = [(a.cpu().pin_memory(), b.cpu().pin_memory()) for a, b in pairs]
     torch.cuda.synchronize()
@@ -472,10 +474,10 @@ def run_match(args, rank, world, local):
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32 (popcount)",
                 "data": "synthetic", "config": dict(cfg, l2="256 MB buffer written between timed steps (outside "
                                                          "the events)", matches_per_step=n_match * world),
-                "roofline": {"bound": "compute (POPC pipe)", "achieved": ach, "peak": peak, "unit": "Tpopc/s",
-                             "frac": ach / peak, "traffic": None, "kernel": "k_hamming_matrix (same pairs, live "
-                             "CUDA events)", "peak_source": "measured POPC rate, tools/micro/popc_bench.cu",
-                             "kernel_ms_per_step": kms},
+                "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)",
+                             "frac": ach / peak, "traffic": None, "kernel": "k_hamming_mma (IMMA u8, same pairs, "
+                             "live CUDA events)", "peak_source": "measured mma.sync m16n8k32 u8 rate, "
+                             "tools/micro/imma_bench.cu", "kernel_ms_per_step": kms},
                 "e2e": {"value": n_pairs_step / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "api": "pinned packed descriptors -> radius_match_device -> "
                                                           "matches to host"},
