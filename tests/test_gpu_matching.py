@@ -123,3 +123,25 @@ def test_frame_features_properties():
     assert torch.equal(qi.long(), m[:, 0]) and torch.equal(ri.long(), m[:, 1])
     assert torch.equal(d, hab[m[:, 0], m[:, 1]])
     assert qi.numel() > 0            # propagated features re-match across frames
+
+
+def test_unaligned_rows_take_popc_path():
+    """Rows at an odd byte address (4-byte alignment fails) use the POPC kernels: same distances."""
+    import torch
+
+    from oracle import oracle
+    from paper_1503_06959_b200.matching import hamming_matrix_device, radius_match_device
+
+    rng = np.random.default_rng(5)
+    q = rng.integers(0, 256, (300, 64), dtype=np.uint8)
+    r = rng.integers(0, 256, (257, 64), dtype=np.uint8)
+    buf = torch.zeros(300 * 64 + 1, dtype=torch.uint8, device="cuda")
+    buf[1:] = torch.from_numpy(q.reshape(-1)).cuda()
+    qd = buf[1:].view(300, 64)                     # data_ptr % 4 == 1
+    assert qd.data_ptr() % 4 == 1
+    rd = torch.from_numpy(r).cuda()
+    assert np.array_equal(hamming_matrix_device(qd, rd).cpu().numpy(), oracle.hamming_matrix(q, r))
+    qi, ri, d = radius_match_device(qd, rd, 240)
+    eq, er, ed = oracle.radius_match(q, r, 240)
+    assert np.array_equal(qi.cpu().numpy(), eq) and np.array_equal(ri.cpu().numpy(), er)
+    assert np.array_equal(d.cpu().numpy(), ed)
