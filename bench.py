@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="detect", choices=["detect", "match"],
+    ap.add_argument("--workload", default="detect", choices=["detect", "match", "dump"],
                     help="detect: the headline detect+describe path; match: Hamming radius matching (SURVEY 8(f))")
     ap.add_argument("--match-pairs", type=int, default=8, help="frame pairs per step (match workload)")
     return ap.parse_args()
@@ -487,9 +487,76 @@ def run_match(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_dump(args):
+    """Feature-dump formatting (report.py:96-113): the
+    features of one config-5 step (all streams, one frame) as dump_features
+    text, native formatter vs the reference's Python f-string loop."""
+    import torch
+
+    from oracle import oracle
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.report import format_features
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    streams = list(range(min(args.streams, 64)))
+    frames = gen_frames(streams, 3, torch.device("cuda", 0))
+    eng = FeatureEngine(W_FR, H_FR, PipelineConfig(mask=MaskConfig(mode="intensity")), n_streams=len(streams))
+    for n in range(3):
+        eng.process(frames[n])
+    soas = [eng.features_host(s) for s in range(len(streams))]
+    eng.close()
+    n_feat = sum(len(f["x"]) for f in soas)
+    threads = host_threads()
+    if args.impl == "reference":
+        sample = soas[:2]
+        n_s = sum(len(f["x"]) for f in sample)
+        t0 = time.perf_counter()
+        for _ in range(max(1, args.steps)):
+            for f in sample:
+                oracle.dump_lines(f["x"], f["y"], f["sigma"], f["theta"], f["origin"], f["desc"])
+        dt = (time.perf_counter() - t0) / max(1, args.steps)
+        v = n_s / dt
+        print(json.dumps({"impl": "reference", "metric": "features/s (feature dump text)", "value": v,
+                          "unit": "features/s", "n_gpus": 1, "steps": args.steps, "warmup": 0,
+                          "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "text", "data": "synthetic",
+                          "config": {"workload": "dump: report.dump_features lines of config-5 features",
+                                     "features": n_s},
+                          "cpu_baseline": {"value": v, "unit": "features/s", "cores": 1, "kind": "port",
+                                           "sample": f"{len(sample)} streams x 1 frame ({n_s} features), Python "
+                                                     "f-string loop of report.py:102-113 (oracle.dump_lines)"},
+                          "e2e": {"value": v, "unit": "features/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    for _ in range(args.warmup):
+        for f in soas:
+            format_features(f)
+    t0 = time.perf_counter()
+    nbytes = 0
+    for _ in range(args.steps):
+        for f in soas:
+            nbytes += len(format_features(f))
+    dt = (time.perf_counter() - t0) / args.steps
+    print(json.dumps({"metric": "features/s (feature dump text)", "value": n_feat / dt, "unit": "features/s",
+                      "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+                      "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "text",
+                      "data": "synthetic",
+                      "config": {"workload": f"dump: report.dump_features lines of {len(streams)} config-5 streams "
+                                             f"(one frame each)", "features": n_feat,
+                                 "text_mb_per_step": nbytes / args.steps / 1e6},
+                      "roofline": {"bound": "host", "achieved": nbytes / args.steps / dt / 1e9, "peak": None,
+                                   "unit": "GB/s of text", "frac": None, "traffic": None,
+                                   "kernel": f"vf_format_features (C++, {threads} host threads)"},
+                      "gpu_launches": 0}), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.workload == "dump":
+        if rank == 0:
+            run_dump(args)
+        return
     if args.workload == "match":
         run_match(args, rank, world, local)
         return

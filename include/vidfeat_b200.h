@@ -202,6 +202,15 @@ int vf_block_match(const uint8_t *prev_dev, const uint8_t *cur_dev, int w, int h
                    const double *x_dev, const double *y_dev, const vf_config *gop, double *nx_dev, double *ny_dev,
                    double *sad_dev, uint8_t *found_dev, void *stream);
 
+/* --- output formats (report.py:102-113) ----------------- */
+/* The feature lines of report.dump_features for n features (HOST buffers):
+ * "%.4f %.4f %.4f %.6f <origin> <128 hex>\n" per feature, origin "detected"
+ * (0) or "propagated" (1), desc64 = 64 packed bytes per feature.  Writes at
+ * most cap bytes to out; *len = the full text length (VF_ERR_CAPACITY with the
+ * needed length if cap is too small).  Multi-threaded, host only. */
+int vf_format_features(int64_t n, const double *x, const double *y, const double *sigma, const double *theta,
+                       const uint8_t *origin, const uint8_t *desc64, char *out, int64_t cap, int64_t *len);
+
 /* --- descriptor matching (matching.py:47-94) -------- */
 /* hamming_matrix (matching.py:73-77, _hamming_matrix_jit :56-66): out[i * ld + j]
  * = popcount(q_i XOR r_j) over nbytes packed bytes (any nbytes >= 1; int32).

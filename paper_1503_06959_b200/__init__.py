@@ -27,6 +27,8 @@ _LAZY = {
     "hamming_matrix": "matching", "radius_match": "matching", "Match": "matching",
     "DEFAULT_MATCH_RADIUS": "matching",
     "spiral_offsets": "temporal", "spiral_search": "temporal", "baseline_step": "temporal",
+    "dump_features": "report", "parse_features": "report", "emit_report": "report", "summarize": "report",
+    "load_sequence": "io", "write_frame": "io",
 }
 
 

@@ -99,6 +99,7 @@ def lib():
     L.vf_upsample_mask.argtypes = [_P, c_int, c_int, c_int, c_int, c_int, c_int, _P, c_void_p]
     L.vf_mask_values.argtypes = [_P, c_int, c_int, c_int, _P, _P, _P, c_void_p]
     L.vf_hamming_matrix.argtypes = [_P, c_int64, _P, c_int64, c_int, _P, c_int64, c_void_p]
+    L.vf_format_features.argtypes = [c_int64, _P, _P, _P, _P, _P, _P, _P, c_int64, POINTER(c_int64)]
     L.vf_block_match.argtypes = [_P, _P, c_int, c_int, c_int64, c_int, _P, _P, POINTER(VfConfig), _P, _P, _P, _P,
                                  c_void_p]
     L.vf_radius_match.argtypes = [_P, c_int64, _P, c_int64, c_int, c_int, _P, _P, _P, c_int64,
@@ -109,7 +110,8 @@ def lib():
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe",
                  "vf_intensity_mask", "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
                  "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
-                 "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match", "vf_block_match"):
+                 "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match", "vf_block_match",
+                 "vf_format_features"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -122,7 +124,7 @@ EXPORTS = (
     "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe", "vf_intensity_mask",
     "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values", "vf_hamming_matrix", "vf_radius_match",
-    "vf_block_match",
+    "vf_block_match", "vf_format_features",
 )
 
 

@@ -394,7 +394,75 @@ def make_temporal():
         print(name, [len(f) for f in feats])
 
 
+def make_formats():
+    """10. output formats + sequence loading (report.py, io.py), SURVEY.md 8(f) rank 3."""
+    import_reference()
+    from vidfeat import io as vio
+    from vidfeat import report as vrep
+    from vidfeat.detector import Keypoint
+    from vidfeat.masking import Feature
+    from vidfeat.pipeline import FrameReport
+
+    g = np.load(HERE / "pipeline_scene_intensity.npz")
+    off = g["offsets"]
+    frames = []
+    for n in range(len(off) - 1):
+        a, b = off[n], off[n + 1]
+        fs = [Feature(Keypoint(float(g["x"][i]), float(g["y"][i]), float(g["sigma"][i]), float(g["theta"][i]),
+                               float(g["score"][i])), np.unpackbits(g["desc"][i]),
+                      "propagated" if g["origin"][i] else "detected", int(g["age"][i])) for i in range(a, b)]
+        frames.append(fs)
+    # edge values: -0.0, halfway cases, large coordinates, 1e-5 theta
+    edge = [Feature(Keypoint(-0.0, 0.00005, 1.00005, -0.0000005), np.zeros(512, np.uint8), "detected", 0),
+            Feature(Keypoint(1919.99995, 1079.12345, 12.0, 3.14159265), np.ones(512, np.uint8), "propagated", 3),
+            Feature(Keypoint(0.125, 2.5e-5, 7.75, -3.1415926535), np.arange(512) % 2, "detected", 0)]
+    frames.append(edge)
+    frames.append([])
+    tmp = Path(tempfile.mkdtemp())
+    vrep.dump_features(frames, tmp / "features.txt")
+    reps = [FrameReport(n, int(g["r_n_detected"][n]), int(g["r_n_propagated"][n]), int(g["r_n_total"][n]),
+                        float(g["r_coverage"][n]), 1.234567 * n, 0.1 * n + 0.00005, 2.0 / 3.0, 12.5, 100.0 / 7.0,
+                        n_dropped=int(g["r_n_dropped"][n]), accuracy=None if n % 2 else 0.123456789 * n)
+            for n in range(len(off) - 1)]
+    vrep.emit_report(reps, tmp, prefix="frames")
+    vrep.write_sweep_summary([{"t": 10, "mpr": 12.5}, {"t": 20, "mpr": None}], tmp)
+    fm = {"features_txt": np.frombuffer((tmp / "features.txt").read_bytes(), np.uint8),
+          "frames_csv": np.frombuffer((tmp / "frames.csv").read_bytes(), np.uint8),
+          "frames_json": np.frombuffer((tmp / "frames_summary.json").read_bytes(), np.uint8),
+          "sweep_json": np.frombuffer((tmp / "sweep_summary.json").read_bytes(), np.uint8)}
+    for k in ("frame", "n_detected", "n_propagated", "n_total", "n_dropped"):
+        fm[f"rep_{k}"] = np.array([getattr(r, k) for r in reps])
+    for k in ("coverage", "t_pyramid_ms", "t_mask_ms", "t_detect_ms", "t_describe_ms", "t_total_ms"):
+        fm[f"rep_{k}"] = np.array([getattr(r, k) for r in reps])
+    fm["rep_accuracy"] = np.array([np.nan if r.accuracy is None else r.accuracy for r in reps])
+    # sequence loading: numeric order, no-digit names last, colour -> L, PGM + PNG
+    rng = np.random.default_rng(8)
+    seq = tmp / "seq"
+    seq.mkdir()
+    names = ["f_10.png", "f_2.pgm", "f_1.png", "zz.png", "f_003.pgm"]
+    for k, nm in enumerate(names):
+        vio.write_frame(seq / nm, rng.integers(0, 256, (24, 32), dtype=np.uint8))
+    from PIL import Image
+    Image.fromarray(rng.integers(0, 256, (24, 32, 3), dtype=np.uint8), mode="RGB").save(seq / "f_7.png")
+    (seq / "notes.txt").write_text("ignored")
+    loaded = vio.load_sequence(seq)
+    fm["seq_files"] = np.array(sorted(p.name for p in seq.iterdir()))
+    fm["seq_file_bytes"] = np.array([np.frombuffer((seq / nm).read_bytes(), np.uint8) for nm in fm["seq_files"]],
+                                    dtype=object)
+    fm["seq_loaded"] = np.stack([fr.data for fr in loaded])
+    fm["seq_index"] = np.array([fr.index for fr in loaded])
+    np.savez_compressed(HERE / "formats.npz", **{k: v for k, v in fm.items() if k != "seq_file_bytes"})
+    # file bytes as separate entries (object arrays are not allowed without pickle)
+    extra = {f"seqfile_{i}": b for i, b in enumerate(fm["seq_file_bytes"])}
+    np.savez_compressed(HERE / "formats_seq.npz", names=fm["seq_files"], **extra)
+    shutil.rmtree(tmp)
+    print("formats", len(fm["features_txt"]), "bytes of dump")
+
+
 if __name__ == "__main__":
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "formats":
+        make_formats()
+        sys.exit(0)
     if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "temporal":
         make_temporal()
         sys.exit(0)
@@ -404,3 +472,4 @@ if __name__ == "__main__":
         main()
         make_matching()
         make_temporal()
+        make_formats()
