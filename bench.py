@@ -714,7 +714,7 @@ def main():
                         "algorithmic_bytes": kbytes.get(k, 0.0), "achieved_gbs": ach, "frac": ach / peak})
     kernels.sort(key=lambda r: -r["ms_per_step"])
     traffic = None
-    tf = ROOT / "profiles" / "r01b_traffic.json"
+    tf = ROOT / "profiles" / "r01c_traffic.json"
     if tf.exists():
         try:
             tj = json.loads(tf.read_text())
