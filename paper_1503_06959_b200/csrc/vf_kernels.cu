@@ -419,24 +419,28 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
     return b.ctr[s * C_NCTR + C_NDET] == 0 ? 0 : (use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles);
   });
   const int n = pre[n_streams];
-  for (int item = blockIdx.x * SAT_WARPS + wid; item < n; item += gridDim.x * SAT_WARPS) {
+  // one-tile software pipeline per warp: tile k + 1's work-list entry, carry
+  // word and row loads are in flight while tile k is built
+  struct TileIn { int s, X0, Y0, tw, th; uint32_t kr, w[8]; };
+  const bool vec = ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) &
+                    15) == 0;
+  auto fetch = [&](int item, TileIn& in) {
     int lo = 0, hi = n_streams;
     while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
     const int s = b.s0 + lo, i = item - pre[lo];
     const int t = use_mask(g, b, s) ? b.sat_work[(long long)s * g.sat_tiles + i] : i;
     const int ty = t / g.stx, tx = t - ty * g.stx;
-    const int X0 = tx * VF_ST, Y0 = ty * VF_ST;
-    const int tw = min(VF_ST, g.W - X0), th = min(VF_ST, g.H - Y0);
-    // ---- lane = row ----
-    const bool rin = lane < th;
-    const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)(Y0 + lane) * b.frame_pitch + X0;
-    const uint32_t kr = rin ? __ldg(b.carry + ((long long)s * g.H + Y0 + lane) * g.stx + tx) : 0u;
-    uint32_t w[8];
-    if (tw == VF_ST && ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch |
-                         (uintptr_t)b.frame_stride) & 15) == 0) {
+    in.s = s; in.X0 = tx * VF_ST; in.Y0 = ty * VF_ST;
+    in.tw = min(VF_ST, g.W - in.X0); in.th = min(VF_ST, g.H - in.Y0);
+    const bool rin = lane < in.th;
+    const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)(in.Y0 + lane) * b.frame_pitch +
+                         in.X0;
+    in.kr = rin ? __ldg(b.carry + ((long long)s * g.H + in.Y0 + lane) * g.stx + tx) : 0u;
+    if (in.tw == VF_ST && vec) {
       uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
       if (rin) { v0 = __ldg(reinterpret_cast<const uint4*>(src)); v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1); }
-      w[0] = v0.x; w[1] = v0.y; w[2] = v0.z; w[3] = v0.w; w[4] = v1.x; w[5] = v1.y; w[6] = v1.z; w[7] = v1.w;
+      in.w[0] = v0.x; in.w[1] = v0.y; in.w[2] = v0.z; in.w[3] = v0.w;
+      in.w[4] = v1.x; in.w[5] = v1.y; in.w[6] = v1.z; in.w[7] = v1.w;
     } else {
 #pragma unroll
       for (int q = 0; q < 8; q++) {
@@ -444,34 +448,44 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
 #pragma unroll
         for (int c = 0; c < 4; c++) {
           const int x = 4 * q + c;
-          if (rin && x < tw) v |= (uint32_t)src[x] << (8 * c);
+          if (rin && x < in.tw) v |= (uint32_t)src[x] << (8 * c);
         }
-        w[q] = v;
+        in.w[q] = v;
       }
     }
-    const uint32_t kp = __shfl_up_sync(0xffffffffu, kr, 1);
-    uint32_t run = lane == 0 ? kr : kr - kp;   // d(r)
+  };
+  const int stride = gridDim.x * SAT_WARPS;
+  int item = blockIdx.x * SAT_WARPS + wid;
+  TileIn cur;
+  if (item < n) fetch(item, cur);
+  for (; item < n; item += stride) {
+    TileIn nxt;
+    if (item + stride < n) fetch(item + stride, nxt);
+    // ---- lane = row: running row prefix + d(r) = K(r) - K(r - 1) ----
+    const uint32_t kp = __shfl_up_sync(0xffffffffu, cur.kr, 1);
+    uint32_t run = lane == 0 ? cur.kr : cur.kr - kp;
     uint32_t* trow = tile + lane * SAT_PITCH;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       uint4 o;
-      run += w[q] & 0xff;         o.x = run;
-      run += (w[q] >> 8) & 0xff;  o.y = run;
-      run += (w[q] >> 16) & 0xff; o.z = run;
-      run += w[q] >> 24;          o.w = run;
+      run += cur.w[q] & 0xff;         o.x = run;
+      run += (cur.w[q] >> 8) & 0xff;  o.y = run;
+      run += (cur.w[q] >> 16) & 0xff; o.z = run;
+      run += cur.w[q] >> 24;          o.w = run;
       *reinterpret_cast<uint4*>(trow + 4 * q) = o;
     }
     __syncwarp();
     // ---- lane = column ----
-    uint32_t* dst = b.sat + (long long)s * g.W * g.H + (long long)Y0 * g.W + X0 + lane;
+    uint32_t* dst = b.sat + (long long)cur.s * g.W * g.H + (long long)cur.Y0 * g.W + cur.X0 + lane;
     uint32_t col = 0;
-    const bool cin = lane < tw;
+    const bool cin = lane < cur.tw;
 #pragma unroll 8
-    for (int r = 0; r < th; r++) {
+    for (int r = 0; r < cur.th; r++) {
       col += tile[r * SAT_PITCH + lane];
       if (cin) dst[(long long)r * g.W] = col;
     }
     __syncwarp();
+    cur = nxt;
   }
 }
 
