@@ -225,6 +225,24 @@ int vf_radius_match(const uint8_t *q_dev, int64_t nq, const uint8_t *r_dev, int6
                     int32_t *q_idx_dev, int32_t *r_idx_dev, int32_t *dist_dev, int64_t cap,
                     int64_t *n_matches, void *stream);
 
+/* --- geometric verification (matching.py:97-220) ---- */
+/* ransac_homography (matching.py:151-192) for n_problems match sets at once.
+ * offsets (HOST, n_problems + 1, offsets[0] = 0): problem p owns points
+ * [offsets[p], offsets[p+1]) of src_dev / dst_dev, (x, y) fp64 pairs (16-byte
+ * aligned) of the matched query / reference keypoints.  Every problem draws
+ * its minimal samples from np.random.default_rng(seed) exactly as the
+ * reference.  Outputs (device): H_dev[9 p ..] the row-major homography (NaN if
+ * none), inlier_dev[i] 1 for a final inlier, n_inliers_dev[p] the inlier
+ * count or -1 when the reference returns (None, []).  Asynchronous. */
+int vf_ransac_homography(int n_problems, const int64_t *offsets, const double *src_dev, const double *dst_dev,
+                         int iters, double reproj_tol, uint64_t seed, double *H_dev, uint8_t *inlier_dev,
+                         int32_t *n_inliers_dev, void *stream);
+/* The minimal-sample table of the above: out[4 k ..] = the k-th
+ * default_rng(seed).choice(n, 4, replace=False), n >= 4.  Device generator
+ * (jump-ahead, asynchronous) and the same stream on the host (no GPU needed). */
+int vf_ransac_samples(uint64_t seed, int64_t n, int iters, int32_t *out_dev, void *stream);
+int vf_ransac_samples_host(uint64_t seed, int64_t n, int iters, int32_t *out);
+
 #ifdef __cplusplus
 }
 #endif

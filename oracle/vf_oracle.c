@@ -848,3 +848,263 @@ void vfo_block_match(const uint8_t *prev, const uint8_t *cur, int w, int h, int 
     }
     free(pb);
 }
+
+/* ================================================================== */
+/* Geometric verification: matching.py:97-192 (ransac_homography).    */
+/* ================================================================== */
+
+/* numpy 2.3's default_rng(seed) = Generator(PCG64(SeedSequence(seed)))
+ * (third-party, not vendored in /root/reference), restated from its
+ * published algorithm: SeedSequence hash-mixing into a 4-word pool and
+ * generate_state(4, uint64); PCG64 setseq-128 with XSL-RR output; 32-bit
+ * draws take the low half of a 64-bit output first and buffer the high half;
+ * choice(n, 4, replace=False) = Floyd's sampling with Lemire bounded draws,
+ * then a Fisher-Yates pass with Lemire draws.  Sequential (no jump-ahead). */
+typedef unsigned __int128 vfo_u128;
+typedef struct { vfo_u128 state, inc; uint32_t buf; int has; } vfo_pcg;
+
+static uint32_t vfo_hashmix(uint32_t v, uint32_t *hc)
+{
+    v ^= *hc;
+    *hc *= 0x931e8875u;
+    v *= *hc;
+    return v ^ (v >> 16);
+}
+
+static void vfo_pcg_seed(vfo_pcg *g, uint64_t seed)
+{
+    uint32_t ent[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)}, pool[4], hc = 0x43b0d7e5u, hb = 0x8b51f9ddu, w[8];
+    int ne = (seed >> 32) ? 2 : 1;
+    for (int i = 0; i < 4; i++) pool[i] = vfo_hashmix(i < ne ? ent[i] : 0u, &hc);
+    for (int a = 0; a < 4; a++)
+        for (int b = 0; b < 4; b++)
+            if (a != b) {
+                uint32_t y = vfo_hashmix(pool[a], &hc);
+                uint32_t r = 0xca01f9ddu * pool[b] - 0x4973f715u * y;
+                pool[b] = r ^ (r >> 16);
+            }
+    for (int i = 0; i < 8; i++) {
+        uint32_t d = pool[i % 4] ^ hb;
+        hb *= 0x58f38dedu;
+        d *= hb;
+        w[i] = d ^ (d >> 16);
+    }
+    uint64_t s[4];
+    for (int i = 0; i < 4; i++) s[i] = (uint64_t)w[2 * i] | ((uint64_t)w[2 * i + 1] << 32);
+    const vfo_u128 mult = ((vfo_u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    g->inc = ((((vfo_u128)s[2] << 64) | s[3]) << 1) | 1u;
+    g->state = g->inc;                                  /* 0 * mult + inc */
+    g->state += ((vfo_u128)s[0] << 64) | s[1];
+    g->state = g->state * mult + g->inc;
+    g->has = 0;
+}
+
+static uint32_t vfo_next32(vfo_pcg *g)
+{
+    if (g->has) { g->has = 0; return g->buf; }
+    const vfo_u128 mult = ((vfo_u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    g->state = g->state * mult + g->inc;
+    uint64_t hi = (uint64_t)(g->state >> 64), x = hi ^ (uint64_t)g->state;
+    unsigned rot = (unsigned)(hi >> 58);
+    uint64_t v = (x >> rot) | (x << ((64 - rot) & 63));
+    g->has = 1;
+    g->buf = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+
+static uint32_t vfo_bounded(vfo_pcg *g, uint32_t rng)     /* [0, rng], Lemire */
+{
+    if (rng == 0) return 0;
+    uint64_t ex = (uint64_t)rng + 1, m = (uint64_t)vfo_next32(g) * ex;
+    uint32_t left = (uint32_t)m;
+    if (left < ex) {
+        uint32_t th = (uint32_t)((0xffffffffu - rng) % ex);
+        while (left < th) { m = (uint64_t)vfo_next32(g) * ex; left = (uint32_t)m; }
+    }
+    return (uint32_t)(m >> 32);
+}
+
+int vfo_ransac_samples(uint64_t seed, int64_t n, int iters, int32_t *out)
+{
+    if (n < 4 || n > 0x7fffffff) return -1;
+    vfo_pcg g;
+    vfo_pcg_seed(&g, seed);
+    for (int k = 0; k < iters; k++) {
+        int64_t v[4];
+        for (int64_t j = n - 4; j < n; j++) {             /* Floyd */
+            int64_t x = vfo_bounded(&g, (uint32_t)j), c = j - (n - 4);
+            for (int q = 0; q < c; q++) if (v[q] == x) { x = j; break; }
+            v[c] = x;
+        }
+        for (int i = 3; i >= 1; i--) {                    /* shuffle */
+            int64_t j = vfo_bounded(&g, (uint32_t)i), t = v[i];
+            v[i] = v[j]; v[j] = t;
+        }
+        for (int q = 0; q < 4; q++) out[4 * k + q] = (int32_t)v[q];
+    }
+    return 0;
+}
+
+/* matching.py:97-106: similarity conditioning; 0 if mean distance < 1e-12 */
+static int vfo_normalize(const double *p, int n, double t[9])
+{
+    double cx = 0, cy = 0, d = 0;
+    for (int i = 0; i < n; i++) { cx += p[2 * i]; cy += p[2 * i + 1]; }
+    cx /= n; cy /= n;
+    for (int i = 0; i < n; i++)
+        d += sqrt((p[2 * i] - cx) * (p[2 * i] - cx) + (p[2 * i + 1] - cy) * (p[2 * i + 1] - cy));
+    d /= n;
+    if (d < 1e-12) return 0;
+    double s = sqrt(2.0) / d;
+    double tt[9] = {s, 0, -s * cx, 0, s, -s * cy, 0, 0, 1};
+    memcpy(t, tt, sizeof tt);
+    return 1;
+}
+
+static void vfo_mat3(const double *a, const double *b, double *c)
+{
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) c[3 * i + j] = a[3 * i] * b[j] + a[3 * i + 1] * b[3 + j] + a[3 * i + 2] * b[6 + j];
+}
+
+/* one-sided Jacobi SVD of the m x k column-major matrix a (k <= 9): on return
+ * the columns of a are U*S and v (k x k, row-major) holds V; sv[j] = |a_j| */
+static void vfo_jacobi_svd(double *a, int m, int k, double *v, double *sv)
+{
+    for (int i = 0; i < k * k; i++) v[i] = (i / k == i % k);
+    for (int sweep = 0; sweep < 80; sweep++) {
+        int rot = 0;
+        for (int p = 0; p < k - 1; p++)
+            for (int q = p + 1; q < k; q++) {
+                double al = 0, be = 0, ga = 0;
+                double *cp = a + (size_t)p * m, *cq = a + (size_t)q * m;
+                for (int i = 0; i < m; i++) { al += cp[i] * cp[i]; be += cq[i] * cq[i]; ga += cp[i] * cq[i]; }
+                if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+                rot = 1;
+                double zeta = (be - al) / (2.0 * ga);
+                double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                for (int i = 0; i < m; i++) {
+                    double x = cp[i], y = cq[i];
+                    cp[i] = c * x - s * y; cq[i] = s * x + c * y;
+                }
+                for (int i = 0; i < k; i++) {
+                    double x = v[i * k + p], y = v[i * k + q];
+                    v[i * k + p] = c * x - s * y; v[i * k + q] = s * x + c * y;
+                }
+            }
+        if (!rot) break;
+    }
+    for (int j = 0; j < k; j++) {
+        double s = 0;
+        for (int i = 0; i < m; i++) s += a[(size_t)j * m + i] * a[(size_t)j * m + i];
+        sv[j] = sqrt(s);
+    }
+}
+
+/* matching.py:109-137 (_dlt): normalized DLT, h = right singular vector of
+ * the smallest singular value (vt[-1]); 0 when _dlt returns None */
+static int vfo_dlt(const double *src, const double *dst, int n, double h[9])
+{
+    double ts[9], td[9];
+    if (!vfo_normalize(src, n, ts) || !vfo_normalize(dst, n, td)) return 0;
+    int m = 2 * n, k = 9;
+    /* m >= 9 for the SVD's null space to be the smallest column; pad rows */
+    int mr = m < 9 ? 9 : m;
+    double *a = calloc((size_t)mr * 9, sizeof(double)), v[81], sv[9];
+    for (int i = 0; i < n; i++) {
+        double sh[3], dh[3], x = src[2 * i], y = src[2 * i + 1], u = dst[2 * i], w = dst[2 * i + 1];
+        for (int r = 0; r < 3; r++) {
+            sh[r] = ts[3 * r] * x + ts[3 * r + 1] * y + ts[3 * r + 2];
+            dh[r] = td[3 * r] * u + td[3 * r + 1] * w + td[3 * r + 2];
+        }
+        for (int c = 0; c < 3; c++) {
+            a[(size_t)c * mr + 2 * i] = -sh[c];                      /* a[0::2, 0:3] = -sh */
+            a[(size_t)(6 + c) * mr + 2 * i] = sh[c] * dh[0];         /* a[0::2, 6:9]       */
+            a[(size_t)(3 + c) * mr + 2 * i + 1] = -sh[c];            /* a[1::2, 3:6] = -sh */
+            a[(size_t)(6 + c) * mr + 2 * i + 1] = sh[c] * dh[1];     /* a[1::2, 6:9]       */
+        }
+    }
+    vfo_jacobi_svd(a, mr, k, v, sv);
+    free(a);
+    int j = 0;
+    for (int c = 1; c < 9; c++) if (sv[c] < sv[j]) j = c;
+    double hn[9], tdi[9] = {1.0 / td[0], 0, -td[2] / td[0], 0, 1.0 / td[4], -td[5] / td[4], 0, 0, 1}, t[9];
+    for (int r = 0; r < 9; r++) hn[r] = v[r * 9 + j];
+    vfo_mat3(hn, ts, t);
+    vfo_mat3(tdi, t, h);
+    for (int r = 0; r < 9; r++) if (!isfinite(h[r])) return 0;
+    if (fabs(h[8]) > 1e-12) { double d = h[8]; for (int r = 0; r < 9; r++) h[r] /= d; }
+    return 1;
+}
+
+/* matching.py:140-146 (_usable): finite, |det| >= 1e-12, cond_2 < 1e12 */
+static int vfo_usable(const double h[9])
+{
+    for (int r = 0; r < 9; r++) if (!isfinite(h[r])) return 0;
+    double det = h[0] * (h[4] * h[8] - h[5] * h[7]) - h[1] * (h[3] * h[8] - h[5] * h[6])
+               + h[2] * (h[3] * h[7] - h[4] * h[6]);
+    if (fabs(det) < 1e-12) return 0;
+    double a[9], v[9], sv[3];
+    for (int r = 0; r < 3; r++) for (int c = 0; c < 3; c++) a[c * 3 + r] = h[3 * r + c];
+    vfo_jacobi_svd(a, 3, 3, v, sv);
+    double mx = fmax(sv[0], fmax(sv[1], sv[2])), mn = fmin(sv[0], fmin(sv[1], sv[2]));
+    return mn > 0 && mx / mn < 1e12;
+}
+
+/* matching.py:149-154 + :177: reprojection error under h, inlier iff < tol */
+static int64_t vfo_inliers(const double h[9], const double *src, const double *dst, int64_t n, double tol,
+                           uint8_t *inl)
+{
+    int64_t c = 0;
+    for (int64_t i = 0; i < n; i++) {
+        double x = src[2 * i], y = src[2 * i + 1];
+        double px = x * h[0] + y * h[1] + h[2], py = x * h[3] + y * h[4] + h[5], z = x * h[6] + y * h[7] + h[8];
+        if (fabs(z) < 1e-12) z = 1e-12;
+        double ex = px / z - dst[2 * i], ey = py / z - dst[2 * i + 1];
+        inl[i] = sqrt(ex * ex + ey * ey) < tol;
+        c += inl[i];
+    }
+    return c;
+}
+
+/* matching.py:157-192: returns the final inlier count (inl[] marks them,
+ * h the model) or -1 for (None, []) */
+int64_t vfo_ransac_homography(int64_t n, const double *src, const double *dst, int iters, double tol, uint64_t seed,
+                              double *h_out, uint8_t *inl)
+{
+    if (n < 4) { memset(inl, 0, (size_t)n); return -1; }
+    int32_t *tab = malloc(sizeof(int32_t) * 4 * (size_t)(iters > 0 ? iters : 1));
+    vfo_ransac_samples(seed, n, iters, tab);
+    uint8_t *cur = malloc((size_t)n), *best = malloc((size_t)n);
+    int64_t best_count = 0;
+    int have = 0;
+    for (int k = 0; k < iters; k++) {
+        double s4[8], d4[8], h[9];
+        for (int q = 0; q < 4; q++) {
+            int32_t i = tab[4 * k + q];
+            s4[2 * q] = src[2 * i]; s4[2 * q + 1] = src[2 * i + 1];
+            d4[2 * q] = dst[2 * i]; d4[2 * q + 1] = dst[2 * i + 1];
+        }
+        if (!vfo_dlt(s4, d4, 4, h) || !vfo_usable(h)) continue;
+        int64_t c = vfo_inliers(h, src, dst, n, tol, cur);
+        if (c > best_count) { best_count = c; memcpy(best, cur, (size_t)n); have = 1; }
+    }
+    int64_t result = -1;
+    if (have && best_count >= 4) {
+        double *bs = malloc(sizeof(double) * 2 * (size_t)best_count), *bd = malloc(sizeof(double) * 2 * (size_t)best_count);
+        int64_t m = 0;
+        for (int64_t i = 0; i < n; i++)
+            if (best[i]) { bs[2 * m] = src[2 * i]; bs[2 * m + 1] = src[2 * i + 1];
+                           bd[2 * m] = dst[2 * i]; bd[2 * m + 1] = dst[2 * i + 1]; m++; }
+        double h[9];
+        if (vfo_dlt(bs, bd, (int)m, h) && vfo_usable(h)) {
+            result = vfo_inliers(h, src, dst, n, tol, inl);
+            memcpy(h_out, h, sizeof h);
+        }
+        free(bs); free(bd);
+    }
+    if (result < 0) memset(inl, 0, (size_t)n);
+    free(tab); free(cur); free(best);
+    return result;
+}

@@ -25,7 +25,13 @@ _LAZY = {
     "run_pipeline": "pipeline", "run_streams": "pipeline",
     "FeatureEngine": "engine",
     "hamming_matrix": "matching", "radius_match": "matching", "Match": "matching",
-    "DEFAULT_MATCH_RADIUS": "matching",
+    "DEFAULT_MATCH_RADIUS": "matching", "MatchConfig": "matching", "project_points": "matching",
+    "ransac_homography": "matching", "match_and_verify": "matching", "count_mpr": "matching",
+    "RankedList": "evaluation", "ObjectModel": "evaluation", "ObjectEstimate": "evaluation",
+    "GroundTruthRecord": "evaluation", "average_precision": "evaluation", "sequence_ap": "evaluation",
+    "mean_average_precision": "evaluation", "corner_geometry": "evaluation", "locate_object": "evaluation",
+    "tracking_accuracy": "evaluation", "save_ground_truth": "evaluation", "load_ground_truth": "evaluation",
+    "load_relevance": "evaluation", "TRACKING_TOLERANCE_PX": "evaluation",
     "spiral_offsets": "temporal", "spiral_search": "temporal", "baseline_step": "temporal",
     "dump_features": "report", "parse_features": "report", "emit_report": "report", "summarize": "report",
     "load_sequence": "io", "write_frame": "io",

@@ -104,6 +104,9 @@ def lib():
                                  c_void_p]
     L.vf_radius_match.argtypes = [_P, c_int64, _P, c_int64, c_int, c_int, _P, _P, _P, c_int64,
                                   POINTER(c_int64), c_void_p]
+    L.vf_ransac_homography.argtypes = [c_int, _P, _P, _P, c_int, c_double, c_uint64, _P, _P, _P, c_void_p]
+    L.vf_ransac_samples.argtypes = [c_uint64, c_int64, c_int, _P, c_void_p]
+    L.vf_ransac_samples_host.argtypes = [c_uint64, c_int64, c_int, _P]
     for name in ("vf_set_pattern", "vf_create", "vf_destroy", "vf_layer_geometry", "vf_reset", "vf_process",
                  "vf_process_host", "vf_get_report", "vf_get_features", "vf_copy_features", "vf_get_layer",
                  "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
@@ -111,7 +114,7 @@ def lib():
                  "vf_intensity_mask", "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values",
                  "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
                  "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match", "vf_block_match",
-                 "vf_format_features"):
+                 "vf_format_features", "vf_ransac_homography", "vf_ransac_samples", "vf_ransac_samples_host"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -124,7 +127,7 @@ EXPORTS = (
     "vf_get_totals", "vf_set_timing", "vf_get_stage_ms", "vf_get_diag", "vf_fetch_features", "vf_pipeline_submit",
     "vf_pipeline_collect", "vf_build_pyramid", "vf_score_map", "vf_nms_refine", "vf_describe", "vf_intensity_mask",
     "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values", "vf_hamming_matrix", "vf_radius_match",
-    "vf_block_match", "vf_format_features",
+    "vf_block_match", "vf_format_features", "vf_ransac_homography", "vf_ransac_samples", "vf_ransac_samples_host",
 )
 
 

@@ -19,8 +19,9 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libvidfeat_b200.so"
-SOURCES = ["vf_capi.cu", "vf_match.cu", "vf_format.cpp"]
-DEPS = ["vf_capi.cu", "vf_kernels.cu", "vf_common.cuh", "vf_match.cu", "vf_temporal.cuh", "vf_format.cpp"]
+SOURCES = ["vf_capi.cu", "vf_match.cu", "vf_ransac.cu", "vf_format.cpp"]
+DEPS = ["vf_capi.cu", "vf_kernels.cu", "vf_common.cuh", "vf_match.cu", "vf_temporal.cuh", "vf_format.cpp", "vf_ransac.cu",
+        "vf_rng.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -459,12 +459,148 @@ def make_formats():
     print("formats", len(fm["features_txt"]), "bytes of dump")
 
 
+def make_ransac():
+    """9. geometric verification + evaluation (matching.py:97-220,
+    evaluation.py:60-171), SURVEY.md 8(f) rank 4."""
+    import_reference()
+    from vidfeat import evaluation, matching
+    from vidfeat.detector import Keypoint
+    from vidfeat.masking import Feature
+
+    rng = np.random.default_rng(57)
+    out = {}
+
+    def proj(h, p):
+        ph = np.column_stack([p, np.ones(len(p))]) @ h.T
+        return ph[:, :2] / ph[:, 2:]
+
+    def scene(h, n_in, n_out, noise=0.0, w=640, hgt=480, tol=3.0):
+        src = rng.uniform([40, 40], [w - 40, hgt - 40], (n_in, 2))
+        dst = proj(h, src) + (rng.normal(0.0, noise, (n_in, 2)) if noise else 0.0)
+        os_, od = [], []
+        while len(os_) < n_out:
+            a = rng.uniform([0, 0], [w, hgt], 2)
+            b = rng.uniform([0, 0], [w, hgt], 2)
+            if np.linalg.norm(proj(h, a[None])[0] - b) > 4.0 * tol:
+                os_.append(a)
+                od.append(b)
+        src = np.vstack([src, np.array(os_).reshape(-1, 2)])
+        dst = np.vstack([dst, np.array(od).reshape(-1, 2)])
+        perm = rng.permutation(len(src))
+        return src[perm], dst[perm]
+
+    persp = np.array([[0.92, 0.11, 35.0], [-0.07, 1.05, -12.0], [1.2e-4, -8e-5, 1.0]])
+    cases = []
+    pts = rng.uniform(50, 400, (8, 2))
+    cases.append((pts, pts.copy(), 200, 3.0, 1))                                     # identity, exact
+    cases.append((*scene(np.array([[1.02, 0.03, 8.0], [-0.02, 0.98, -5.0], [1e-5, -2e-5, 1.0]]), 70, 30), 1000, 3.0, 3))
+    cases.append((*scene(np.array([[0.9, 0.05, 20.0], [0.02, 1.1, -8.0], [0.0, 0.0, 1.0]]), 40, 20), 500, 3.0, 5))
+    cases.append((*scene(np.array([[1.0, 0.0, 12.0], [0.0, 1.0, 7.0], [0.0, 0.0, 1.0]]), 30, 30), 300, 3.0, 7))
+    line = np.array([[i * 10.0, 0.0] for i in range(8)])
+    cases.append((line, line.copy(), 50, 3.0, 0))                                    # collinear -> None
+    tri = np.array([[i * 10.0, i * 5.0] for i in range(3)])
+    cases.append((tri, tri.copy(), 1000, 3.0, 0))                                    # < 4 matches -> None
+    cases.append((*scene(persp, 300, 700, noise=0.7, w=1280, hgt=720), 1000, 3.0, 11))  # 30 % inliers, noisy
+    cases.append((*scene(persp, 1200, 1800, noise=0.5, w=1920, hgt=1080), 1000, 3.0, 2**33 + 1))
+    cases.append((rng.uniform(0, 640, (50, 2)), rng.uniform(0, 480, (50, 2)), 200, 3.0, 4))   # all outliers
+    q4 = rng.uniform(60, 500, (4, 2))
+    cases.append((q4, proj(persp, q4), 10, 3.0, 2))                                  # n == 4
+    dup = np.vstack([np.repeat(rng.uniform(100, 300, (1, 2)), 6, 0), rng.uniform(50, 500, (6, 2))])
+    cases.append((dup, proj(persp, dup), 100, 3.0, 9))                               # coincident samples
+    cases.append((*scene(persp, 20, 10), 0, 3.0, 0))                                 # iters = 0 -> None
+    cases.append((*scene(persp, 150, 150, noise=0.4), 800, 1.0, 12))                # tight tolerance
+    for i, (src, dst, iters, tol, seed) in enumerate(cases):
+        kq = [Keypoint(float(x), float(y), 1.0) for x, y in src]
+        kr = [Keypoint(float(x), float(y), 1.0) for x, y in dst]
+        ms = [matching.Match(j, j, 0) for j in range(len(src))]
+        h, inl = matching.ransac_homography(ms, kq, kr, iters=iters, reproj_tol=tol, seed=seed)
+        out[f"r{i}_src"], out[f"r{i}_dst"] = np.asarray(src, np.float64), np.asarray(dst, np.float64)
+        out[f"r{i}_par"] = np.array([iters, tol, seed], np.float64)
+        out[f"r{i}_seed"] = np.array(seed, np.uint64)
+        out[f"r{i}_H"] = np.full((3, 3), np.nan) if h is None else h
+        out[f"r{i}_inl"] = np.array(inl, np.int64)
+    out["n_ransac"] = np.array(len(cases))
+
+    # sample tables straight from numpy (the RNG the reference seeds)
+    for i, (seed, n) in enumerate([(0, 4), (0, 100), (3, 70), (2**33 + 1, 3000), (7, 2**31 - 1)]):
+        r = np.random.default_rng(seed)
+        out[f"s{i}_seed"], out[f"s{i}_n"] = np.array(seed, np.uint64), np.array(n)
+        out[f"s{i}_tab"] = np.array([r.choice(n, 4, replace=False) for _ in range(400)], np.int32)
+    out["n_samples"] = np.array(5)
+
+    def feat(bits, x, y):
+        return Feature(Keypoint(float(x), float(y), 1.0), bits.astype(np.uint8), "detected", 0)
+
+    # match_and_verify / count_mpr on features (tests/test_matching.py:153-170 style)
+    descs = rng.integers(0, 2, (60, 512)).astype(np.uint8)
+    src = rng.uniform(60, 600, (60, 2))
+    dst = proj(persp, src)
+    dst[45:] = rng.uniform(0, 640, (15, 2))                       # 15 displaced: outliers
+    noise_r = rng.integers(0, 2, (40, 512)).astype(np.uint8)
+    q = [feat(d, *p) for d, p in zip(descs, src)]
+    r = [feat(d, *p) for d, p in zip(np.vstack([descs, noise_r]), np.vstack([dst, rng.uniform(0, 640, (40, 2))]))]
+    out["mv_q_bits"], out["mv_q_xy"] = descs, src
+    out["mv_r_bits"] = np.vstack([descs, noise_r])
+    out["mv_r_xy"] = np.array([[f.kp.x, f.kp.y] for f in r])
+    cfg = matching.MatchConfig(t_m=102, iters=1000, reproj_tol=3.0, seed=0)
+    h, ms = matching.match_and_verify(q, r, cfg)
+    out["mv_H"] = h
+    out["mv_matches"] = np.array([[m.query_idx, m.ref_idx, m.distance] for m in ms], np.int64).reshape(-1, 3)
+    out["mv_mpr"] = np.array([matching.count_mpr(q, r, t, cfg) for t in (0, 102, 200)])
+    out["mv_mpr_disjoint"] = np.array(matching.count_mpr(q[:20], [feat(b, 0, 0) for b in noise_r[:20]], 102, cfg))
+
+    # locate_object over a 3-object database (evaluation.py:95-121)
+    objs, frame = [], []
+    hs = [np.array([[1.0, 0.0, 300.0], [0.0, 1.0, 120.0], [0.0, 0.0, 1.0]]), persp,
+          np.array([[0.8, -0.1, 500.0], [0.1, 0.8, 300.0], [0.0, 0.0, 1.0]])]
+    n_vis = [25, 0, 40]
+    for oid in range(3):
+        bits = rng.integers(0, 2, (50, 512)).astype(np.uint8)
+        xy = rng.uniform(0, 200, (50, 2))
+        objs.append((oid, bits, xy))
+        k = n_vis[oid]
+        if k:
+            fx = proj(hs[oid], xy[:k]) + rng.normal(0.0, 0.3, (k, 2))
+            frame += [feat(b, *p) for b, p in zip(bits[:k], fx)]
+    fb = rng.integers(0, 2, (60, 512)).astype(np.uint8)
+    frame += [feat(b, *p) for b, p in zip(fb, rng.uniform(0, 1280, (60, 2)))]
+    db = [evaluation.ObjectModel(oid, [feat(b, *p) for b, p in zip(bits, xy)], evaluation.corner_geometry(200, 200))
+          for oid, bits, xy in objs]
+    est = evaluation.locate_object(frame, db, cfg)
+    for oid, bits, xy in objs:
+        out[f"lo_obj{oid}_bits"], out[f"lo_obj{oid}_xy"] = bits, xy
+    out["lo_frame_bits"] = np.stack([f.desc for f in frame])
+    out["lo_frame_xy"] = np.array([[f.kp.x, f.kp.y] for f in frame])
+    out["lo_id"] = np.array(est.object_id)
+    out["lo_corners"] = est.corners
+    out["lo_mpr"] = np.array(est.mpr)
+
+    # average precision on random ranked lists (evaluation.py:60-68)
+    aps, rels, tots = [], [], []
+    for _ in range(60):
+        z = int(rng.integers(1, 40))
+        rel = (rng.random(z) < 0.3).astype(np.int64)
+        tot = int(rel.sum() + rng.integers(0, 3))
+        if tot == 0:
+            continue
+        rels.append(np.pad(rel, (0, 40 - z), constant_values=-1))
+        tots.append(tot)
+        aps.append(evaluation.average_precision(evaluation.RankedList(list(range(z)), rel, tot)))
+    out["ap_rel"], out["ap_tot"], out["ap_val"] = np.array(rels), np.array(tots), np.array(aps)
+    np.savez_compressed(HERE / "ransac.npz", **out)
+    print("ransac", [(i, int(np.isnan(out[f"r{i}_H"]).any()), len(out[f"r{i}_inl"])) for i in range(len(cases))],
+          "mpr", out["mv_mpr"], "locate", int(est.object_id), int(est.mpr))
+
+
 if __name__ == "__main__":
     if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "formats":
         make_formats()
         sys.exit(0)
     if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "temporal":
         make_temporal()
+        sys.exit(0)
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "ransac":
+        make_ransac()
         sys.exit(0)
     if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "matching":
         make_matching()
@@ -473,3 +609,4 @@ if __name__ == "__main__":
         make_matching()
         make_temporal()
         make_formats()
+        make_ransac()

@@ -1,0 +1,164 @@
+"""GPU parity of geometric verification through the C
+ABI (vf_ransac_homography / vf_ransac_samples) against the reference's own
+outputs (tests/golden/ransac.npz) and the pinned CPU oracle: the same minimal
+samples bit for bit, the same best model, the same final inlier sets, H within
+H_RTOL (the minimal models and the refit use a different, equally exact
+solver than numpy's LAPACK SVD, so entries differ by rounding only)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+H_RTOL = 1e-9
+
+
+def _feat(bits, x, y):
+    from paper_1503_06959_b200.types import Feature, Keypoint
+
+    return Feature(Keypoint(float(x), float(y), 1.0), np.asarray(bits, np.uint8), "detected", 0)
+
+
+def _close(h, H):
+    return np.abs(h - H).max() <= H_RTOL * np.abs(H).max()
+
+
+def test_device_sample_tables():
+    """The jump-ahead generator (one thread per iteration) == numpy, including
+    n = 2^31 - 1 where Lemire rejections shift later iterations (fix-up path)."""
+    from paper_1503_06959_b200.matching import ransac_samples
+
+    g = golden("ransac.npz")
+    for i in range(int(g["n_samples"])):
+        seed, n, tab = int(g[f"s{i}_seed"]), int(g[f"s{i}_n"]), g[f"s{i}_tab"]
+        assert np.array_equal(ransac_samples(seed, n, len(tab), device=True), tab), (seed, n)
+    for seed, n in [(0, 2**31 - 1), (1, 2**31 - 7), (5, 3_000_000_000 // 2)]:
+        host = ransac_samples(seed, n, 5000)
+        assert np.array_equal(ransac_samples(seed, n, 5000, device=True), host), (seed, n)
+
+
+def test_ransac_golden_each_and_batched():
+    from paper_1503_06959_b200.matching import Match, ransac_homography, ransac_homography_batch
+    from paper_1503_06959_b200.types import Keypoint
+
+    g = golden("ransac.npz")
+    n_cases = int(g["n_ransac"])
+    for i in range(n_cases):
+        iters, tol, _ = g[f"r{i}_par"]
+        src, dst = g[f"r{i}_src"], g[f"r{i}_dst"]
+        kq = [Keypoint(float(x), float(y), 1.0) for x, y in src]
+        kr = [Keypoint(float(x), float(y), 1.0) for x, y in dst]
+        h, inl = ransac_homography([Match(j, j, 0) for j in range(len(src))], kq, kr, int(iters), float(tol),
+                                   int(g[f"r{i}_seed"]))
+        H = g[f"r{i}_H"]
+        if np.isnan(H).any():
+            assert h is None and inl == [], i
+        else:
+            assert _close(h, H), i
+            assert inl == list(g[f"r{i}_inl"]), i
+    # one launch over every case with the same (iters, tol, seed): same answers
+    for iters, tol, seed in {(int(g[f"r{i}_par"][0]), float(g[f"r{i}_par"][1]), int(g[f"r{i}_seed"]))
+                             for i in range(n_cases)}:
+        idx = [i for i in range(n_cases) if (int(g[f"r{i}_par"][0]), float(g[f"r{i}_par"][1]),
+                                             int(g[f"r{i}_seed"])) == (iters, tol, seed)]
+        res = ransac_homography_batch([(g[f"r{i}_src"], g[f"r{i}_dst"]) for i in idx], iters, tol, seed)
+        for i, (h, inl) in zip(idx, res):
+            H = g[f"r{i}_H"]
+            assert (h is None) == bool(np.isnan(H).any()), i
+            if h is not None:
+                assert _close(h, H) and inl == list(g[f"r{i}_inl"]), i
+
+
+def test_batch_vs_oracle_random_scenes():
+    """48 planted-homography scenes (20-80 % inliers, 0.5 px noise, 50-3000
+    matches) in one call == the oracle run per scene."""
+    from oracle import oracle
+    from paper_1503_06959_b200.matching import ransac_homography_batch
+
+    rng = np.random.default_rng(21)
+    probs = []
+    for _ in range(48):
+        n = int(rng.integers(50, 3000))
+        k = int(n * rng.uniform(0.2, 0.8))
+        h = np.array([[rng.uniform(0.8, 1.2), rng.uniform(-0.2, 0.2), rng.uniform(-50, 50)],
+                      [rng.uniform(-0.2, 0.2), rng.uniform(0.8, 1.2), rng.uniform(-50, 50)],
+                      [rng.uniform(-2e-4, 2e-4), rng.uniform(-2e-4, 2e-4), 1.0]])
+        src = rng.uniform(0, [1920, 1080], (n, 2))
+        ph = np.column_stack([src, np.ones(n)]) @ h.T
+        dst = ph[:, :2] / ph[:, 2:] + rng.normal(0, 0.5, (n, 2))
+        dst[k:] = rng.uniform(0, [1920, 1080], (n - k, 2))
+        probs.append((src, dst))
+    res = ransac_homography_batch(probs, 1000, 3.0, 0)
+    for p, ((src, dst), (h, inl)) in enumerate(zip(probs, res)):
+        eh, einl = oracle.ransac_homography(src, dst, 1000, 3.0, 0)
+        assert (h is None) == (eh is None), p
+        if h is not None:
+            assert _close(h, eh), p
+            assert inl == einl, p
+
+
+def test_reference_unit_cases():
+    """tests/test_matching.py TestRansac semantics (identity, planted model
+    recovered, degenerate inputs, exact inlier consistency, determinism)."""
+    from paper_1503_06959_b200.matching import Match, project_points, ransac_homography
+    from paper_1503_06959_b200.types import Keypoint
+
+    rng = np.random.default_rng(8)
+    pts = rng.uniform(50, 400, (8, 2))
+    kps = [Keypoint(float(x), float(y), 1.0) for x, y in pts]
+    h, inl = ransac_homography([Match(i, i, 0) for i in range(8)], kps, kps, iters=200, seed=1)
+    assert np.allclose(h, np.eye(3), atol=1e-6) and len(inl) == 8
+    three = [Keypoint(float(i * 10), float(i * 5), 1.0) for i in range(3)]
+    assert ransac_homography([Match(i, i, 0) for i in range(3)], three, three) == (None, [])
+    line = [Keypoint(float(i * 10), 0.0, 1.0) for i in range(8)]
+    assert ransac_homography([Match(i, i, 0) for i in range(8)], line, line, iters=50, seed=0) == (None, [])
+    h_true = np.array([[0.9, 0.05, 20.0], [0.02, 1.1, -8.0], [0.0, 0.0, 1.0]])
+    src = rng.uniform(40, [600, 440], (40, 2))
+    dst = np.vstack([project_points(h_true, src[:30]), rng.uniform(0, [640, 480], (10, 2))])
+    q = [Keypoint(float(x), float(y), 1.0) for x, y in src]
+    r = [Keypoint(float(x), float(y), 1.0) for x, y in dst]
+    ms = [Match(i, i, 0) for i in range(40)]
+    h, inl = ransac_homography(ms, q, r, iters=500, reproj_tol=3.0, seed=5)
+    err = np.linalg.norm(project_points(h, src) - dst, axis=1)
+    assert set(inl) == set(np.nonzero(err < 3.0)[0].tolist())
+    a = ransac_homography(ms, q, r, iters=300, seed=7)
+    b = ransac_homography(ms, q, r, iters=300, seed=7)
+    assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+
+
+def test_match_and_verify_count_mpr_golden():
+    from paper_1503_06959_b200.matching import MatchConfig, count_mpr, match_and_verify
+
+    g = golden("ransac.npz")
+    q = [_feat(b, *p) for b, p in zip(g["mv_q_bits"], g["mv_q_xy"])]
+    r = [_feat(b, *p) for b, p in zip(g["mv_r_bits"], g["mv_r_xy"])]
+    cfg = MatchConfig(t_m=102, iters=1000, reproj_tol=3.0, seed=0)
+    h, ms = match_and_verify(q, r, cfg)
+    assert _close(h, g["mv_H"])
+    assert np.array_equal(np.array([[m.query_idx, m.ref_idx, m.distance] for m in ms]).reshape(-1, 3), g["mv_matches"])
+    assert [count_mpr(q, r, t, cfg) for t in (0, 102, 200)] == list(g["mv_mpr"])
+    noise = [_feat(b, 0, 0) for b in g["mv_r_bits"][60:80]]
+    assert count_mpr(q[:20], noise, 102, cfg) == int(g["mv_mpr_disjoint"]) == 0
+
+
+def test_locate_object_golden():
+    from paper_1503_06959_b200.evaluation import ObjectModel, corner_geometry, locate_object, locate_objects
+    from paper_1503_06959_b200.matching import MatchConfig
+
+    g = golden("ransac.npz")
+    db = [ObjectModel(oid, [_feat(b, *p) for b, p in zip(g[f"lo_obj{oid}_bits"], g[f"lo_obj{oid}_xy"])],
+                      corner_geometry(200, 200)) for oid in range(3)]
+    frame = [_feat(b, *p) for b, p in zip(g["lo_frame_bits"], g["lo_frame_xy"])]
+    cfg = MatchConfig()
+    est = locate_object(frame, db[::-1], cfg)       # database order does not matter
+    assert est.object_id == int(g["lo_id"]) and est.mpr == int(g["lo_mpr"])
+    assert np.abs(est.corners - g["lo_corners"]).max() < 1e-6
+    # several frames in one launch; a frame with nothing verifiable -> None
+    empty = [_feat(b, *p) for b, p in zip(g["lo_frame_bits"][-60:], g["lo_frame_xy"][-60:])]
+    many = locate_objects([frame, empty, frame], db, cfg)
+    assert many[1] is None
+    assert many[0].object_id == many[2].object_id == est.object_id and many[0].mpr == est.mpr
+    with pytest.raises(ValueError):
+        locate_object(frame, [], cfg)
