@@ -3,20 +3,25 @@
 // 151-192) for many match sets in one call, as count_mpr / locate_object
 // (matching.py:209-220, evaluation.py:95-121) consume it.
 //
-// Per call (all problems at once, four launches on `stream`):
+// Per call (all problems at once, on `stream`):
 //   k_rs_samples   thread per (problem, iteration): the reference's minimal
 //                  samples, rng.choice(n, 4, replace=False) of
 //                  default_rng(seed), by PCG64 jump-ahead (vf_rng.cuh)
 //   k_rs_fixup     thread per problem: iterations after a (rare) Lemire
 //                  rejection regenerated sequentially
-//   k_rs_score     CTA per (problem, 64 iterations): 64 minimal homographies
-//                  solved into shared memory, then every match point scored
-//                  against all 64 (thread per point, ballot + popc counts);
-//                  best (max count, first iteration) by a 64-bit atomicMax
-//   k_rs_refit     CTA per problem: the best consensus set, the normalized DLT
-//                  refit (matching.py:109-137) as the least eigenvector of the
-//                  9x9 normal matrix, the usable test (matching.py:140-146),
-//                  the final inlier mask and count (matching.py:187-192)
+//   k_rs_score     CTA per (problem, 64 iterations, 4096-point chunk): 64
+//                  minimal homographies solved into shared memory, then every
+//                  point of the chunk scored against all 64 (thread per point,
+//                  ballot + popc counts), counts added per iteration
+//   refit          k_rs_best (CTA per problem: the best iteration, max count /
+//                  first index, and its model), then grid-wide passes over
+//                  4096-point chunks with per-chunk partials summed in chunk
+//                  order (bitwise reproducible): k_rs_pass<0> consensus set +
+//                  centroids, <1> mean distances, <2> the 9x9 normal matrix of
+//                  the normalized DLT (matching.py:109-137); k_rs_solve (warp
+//                  per problem: least eigenvector by Jacobi, de-normalize, the
+//                  usable test, matching.py:140-146); k_rs_pass<3> final
+//                  inlier mask + counts; k_rs_out (matching.py:187-192)
 // Minimal models: for 4 points the normalized DLT's null vector is the
 // homography through the 4 correspondences; it is computed in closed form
 // (unit square -> quad maps, H = Q_dst adj(Q_src)) on centred, scaled
@@ -25,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "../../include/vidfeat_b200.h"
@@ -33,6 +39,7 @@
 namespace {
 
 constexpr int RS_HB = 64;        // hypotheses per scoring CTA
+constexpr int RS_PCH = 4096;     // points per scoring CTA
 constexpr int RS_THREADS = 256;
 
 // ---- 3x3 helpers ---------------------------------------------------------
@@ -180,14 +187,44 @@ __device__ __forceinline__ bool reproj_inlier(const double* h, double2 s, double
   return __dsqrt_rn(__fma_rn(ex, ex, __dmul_rn(ey, ey))) < tol;
 }
 
+// The same decision without the divisions and the square root, when it is
+// clear: with z the (unclamped) denominator, err < tol <=> |p - d z|^2 <
+// tol^2 z^2.  Taken only when both sides differ by more than 1e-6 relative
+// (fp64 rounding of either form is ~1e-13 here), z is not near its clamp or
+// cancelling, and the coordinates are below 1e7 (`plain`); every other case
+// -- and any NaN -- goes to the exact reference form above.  So each
+// decision equals reproj_inlier's.
+__device__ __forceinline__ bool reproj_inlier_fast(const double* h, double2 s, double2 d, double tol, double tol2,
+                                                   bool plain)
+{
+  if (plain) {
+    const double px = __fma_rn(s.x, h[0], __fma_rn(s.y, h[1], h[2]));
+    const double py = __fma_rn(s.x, h[3], __fma_rn(s.y, h[4], h[5]));
+    const double z = __fma_rn(s.x, h[6], __fma_rn(s.y, h[7], h[8]));
+    const double zb = __fma_rn(fabs(s.x), fabs(h[6]), __fma_rn(fabs(s.y), fabs(h[7]), fabs(h[8])));
+    if (fabs(z) > 1e-6 * zb && fabs(z) >= 1e-9) {
+      const double ex = __fma_rn(-d.x, z, px), ey = __fma_rn(-d.y, z, py);
+      const double e = __fma_rn(ex, ex, __dmul_rn(ey, ey)), t = __dmul_rn(tol2, __dmul_rn(z, z));
+      if (e < t * (1.0 - 1e-6)) return true;
+      if (e > t * (1.0 + 1e-6)) return false;
+    }
+  }
+  return reproj_inlier(h, s, d, tol);
+}
+
+__device__ __forceinline__ bool plain_point(double2 s, double2 d)
+{
+  return fmax(fmax(fabs(s.x), fabs(s.y)), fmax(fabs(d.x), fabs(d.y))) < 1e7;
+}
+
 struct RsProb {
   const int64_t* off;      // [P + 1] point offsets
   const double2* src;      // query points
   const double2* dst;      // reference points
   int32_t* table;          // [P][iters][4] minimal samples
-  unsigned long long* best;  // [P] (count << 32) | ~iteration
+  int32_t* cnt;            // [P][iters] inlier count per iteration (0 if not usable)
   int32_t* first_rej;      // [P] first iteration whose draws rejected
-  int P, iters;
+  int P, iters, chunks;    // chunks: point chunks of the largest problem
   uint64_t seed;
   double tol;
 };
@@ -216,54 +253,105 @@ __global__ void k_rs_fixup(RsProb q)
   for (int k = k0; k < q.iters; k++) vfr::choice4(g, (uint32_t)n, q.table + ((long long)p * q.iters + k) * 4);
 }
 
+// Fast decision of reproj_inlier_fast for a hypothesis row hv = (h0..h8,
+// 1e-6|h6|, 1e-6|h7|, 1e-6|h8|): returns 1 inlier, 0 outlier, -1 undecided
+// (then the exact form decides).
+__device__ __forceinline__ int fast_decide(const double* hv, double2 s, double2 d, double tlo, double thi)
+{
+  const double px = __fma_rn(s.x, hv[0], __fma_rn(s.y, hv[1], hv[2]));
+  const double py = __fma_rn(s.x, hv[3], __fma_rn(s.y, hv[4], hv[5]));
+  const double z = __fma_rn(s.x, hv[6], __fma_rn(s.y, hv[7], hv[8]));
+  const double zb = fmax(__fma_rn(fabs(s.x), hv[9], __fma_rn(fabs(s.y), hv[10], hv[11])), 1e-9);
+  const double ex = __fma_rn(-d.x, z, px), ey = __fma_rn(-d.y, z, py);
+  const double e = __fma_rn(ex, ex, __dmul_rn(ey, ey)), z2 = __dmul_rn(z, z);
+  const bool zok = fabs(z) > zb;
+  return zok && e < tlo * z2 ? 1 : (zok && e > thi * z2 ? 0 : -1);
+}
+
+constexpr int RS_PPT = 4;   // points per thread per hypothesis in k_rs_score
+
 __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
 {
-  __shared__ __align__(16) double hs[RS_HB][10];
+  __shared__ __align__(16) double hs[RS_HB][12];
   __shared__ int cnt[RS_HB];
-  __shared__ unsigned vm32[2];
-  const int p = blockIdx.y, k0 = blockIdx.x * RS_HB;
+  __shared__ int vlist[RS_HB];
+  __shared__ int nvalid;
+  const int p = blockIdx.y, kb = blockIdx.x / q.chunks, ch = blockIdx.x - kb * q.chunks, k0 = kb * RS_HB;
   const int64_t base = q.off[p], n = q.off[p + 1] - base;
-  if (n < 4 || k0 >= q.iters) return;
+  const int64_t c_lo = (int64_t)ch * RS_PCH, c_hi = min(n, c_lo + RS_PCH);
+  if (n < 4 || k0 >= q.iters || c_lo >= n) return;
   const double2* src = q.src + base;
   const double2* dst = q.dst + base;
   const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ unsigned vb[2];
+  bool ok = false;
   if (tid < RS_HB) {   // warps 0 and 1: one minimal model each
     const int k = k0 + tid;
-    bool ok = false;
     cnt[tid] = 0;
     if (k < q.iters) ok = minimal_h(src, dst, q.table + ((long long)p * q.iters + k) * 4, hs[tid]);
+    if (ok) {
+      hs[tid][9] = 1e-6 * fabs(hs[tid][6]);
+      hs[tid][10] = 1e-6 * fabs(hs[tid][7]);
+      hs[tid][11] = 1e-6 * fabs(hs[tid][8]);
+    }
     const unsigned b = __ballot_sync(0xffffffffu, ok);
-    if (lane == 0) vm32[tid >> 5] = b;
+    if (lane == 0) vb[tid >> 5] = b;
   }
   __syncthreads();
-  const unsigned long long vm = (unsigned long long)vm32[0] | ((unsigned long long)vm32[1] << 32);
+  if (ok)   // compacted list of the usable models
+    vlist[(tid >= 32 ? __popc(vb[0]) : 0) + __popc(vb[tid >> 5] & ((1u << lane) - 1))] = tid;
+  if (tid == 0) nvalid = __popc(vb[0]) + __popc(vb[1]);
+  __syncthreads();
+  const int nv = nvalid;
+  const bool fast = q.tol > 0.0;
+  const double tlo = q.tol * q.tol * (1.0 - 1e-6), thi = q.tol * q.tol * (1.0 + 1e-6);
   int c0 = 0, c1 = 0;
-  for (int64_t i0 = 0; i0 < n; i0 += RS_THREADS) {
-    const int64_t i = i0 + tid;
-    const bool in = i < n;
-    const double2 s = in ? src[i] : make_double2(0.0, 0.0), d = in ? dst[i] : make_double2(0.0, 0.0);
-    for (unsigned long long m = vm; m; m &= m - 1) {
-      const int h = __ffsll((long long)m) - 1;
-      const unsigned b = __ballot_sync(0xffffffffu, in && reproj_inlier(hs[h], s, d, q.tol));
+  for (int64_t i0 = c_lo; i0 < c_hi; i0 += RS_THREADS * RS_PPT) {
+    double2 s[RS_PPT], d[RS_PPT];
+    unsigned live = 0, plain = 0;
+#pragma unroll
+    for (int u = 0; u < RS_PPT; u++) {
+      const int64_t i = i0 + tid + u * RS_THREADS;
+      const bool in = i < c_hi;
+      s[u] = in ? src[i] : make_double2(0.0, 0.0);
+      d[u] = in ? dst[i] : make_double2(0.0, 0.0);
+      live |= (unsigned)in << u;
+      plain |= (unsigned)(in && fast && plain_point(s[u], d[u])) << u;
+    }
+    for (int j = 0; j < nv; j++) {
+      const int h = vlist[j];
+      double hv[12];
+#pragma unroll
+      for (int e = 0; e < 12; e += 2) {
+        const double2 w = *reinterpret_cast<const double2*>(&hs[h][e]);
+        hv[e] = w.x;
+        hv[e + 1] = w.y;
+      }
+      int c = 0;
+      unsigned und = 0;
+#pragma unroll
+      for (int u = 0; u < RS_PPT; u++) {
+        const int r = fast_decide(hv, s[u], d[u], tlo, thi);
+        c += r == 1 && ((plain >> u) & 1);
+        und |= (unsigned)(r < 0 || !((plain >> u) & 1)) << u;
+      }
+      und &= live;
+      if (__any_sync(0xffffffffu, und != 0)) {   // rare: the exact reference form
+#pragma unroll
+        for (int u = 0; u < RS_PPT; u++)
+          if ((und >> u) & 1) c += reproj_inlier(hv, s[u], d[u], q.tol);
+      }
+      const int tot = __reduce_add_sync(0xffffffffu, c);
       if (lane == (h & 31)) {
-        if (h < 32) c0 += __popc(b);
-        else c1 += __popc(b);
+        if (h < 32) c0 += tot;
+        else c1 += tot;
       }
     }
   }
   atomicAdd(&cnt[lane], c0);
   atomicAdd(&cnt[lane + 32], c1);
   __syncthreads();
-  if (tid < RS_HB) {
-    const int k = k0 + tid, c = cnt[tid];
-    unsigned long long key = ((vm >> tid) & 1ull) && c > 0 ? ((unsigned long long)c << 32) | (0xffffffffu - (unsigned)k) : 0ull;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-      key = other > key ? other : key;
-    }
-    if (lane == 0 && key) atomicMax(q.best + p, key);
-  }
+  if (tid < RS_HB && cnt[tid] > 0) atomicAdd(q.cnt + (long long)p * q.iters + k0 + tid, cnt[tid]);
 }
 
 // block-wide sum of NV doubles per thread (RS_THREADS threads)
@@ -292,188 +380,348 @@ __device__ void block_sum(double* v, double* red /* [RS_THREADS / 32][NV] */)
   __syncthreads();
 }
 
-// least eigenvector of the symmetric 9x9 A (cyclic Jacobi); A destroyed
-__device__ void least_eigvec9(double (*A)[9], double* out)
+// Least eigenvector of the symmetric 9x9 A (cyclic Jacobi), one warp: every
+// lane computes the rotation, lanes 0..8 apply it to their row / column; A
+// and V in shared memory, A destroyed.
+__device__ void least_eigvec9_warp(double (*A)[9], double (*V)[9], double* out)
 {
-  double V[9][9];
-  for (int i = 0; i < 9; i++)
-    for (int j = 0; j < 9; j++) V[i][j] = i == j ? 1.0 : 0.0;
-  for (int sweep = 0; sweep < 60; sweep++) {
-    double off = 0.0, dia = 0.0;
-    for (int p = 0; p < 9; p++) {
-      dia += A[p][p] * A[p][p];
-      for (int r = p + 1; r < 9; r++) off += A[p][r] * A[p][r];
-    }
-    if (off <= 1e-34 * dia || off == 0.0) break;
+  const int lane = threadIdx.x & 31;
+  if (lane < 9)
+    for (int j = 0; j < 9; j++) V[lane][j] = lane == j ? 1.0 : 0.0;
+  __syncwarp();
+  // rotations below 1e-18 of ||A||_F are skipped (their effect on the
+  // eigenvectors is far below the rounding of the sums); stop after a sweep
+  // without rotations
+  double fro = 0.0;
+  if (lane < 9)
+    for (int j = 0; j < 9; j++) fro += A[lane][j] * A[lane][j];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  const double small = 1e-18 * sqrt(fro);
+  for (int sweep = 0; sweep < 30; sweep++) {
+    bool rot = false;
     for (int p = 0; p < 8; p++)
       for (int r = p + 1; r < 9; r++) {
         const double apq = A[p][r];
-        if (apq == 0.0) continue;
+        if (!(fabs(apq) > small)) continue;
+        rot = true;
         const double theta = (A[r][r] - A[p][p]) / (2.0 * apq);
         const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < 9; k++) {   // A <- A J
-          const double akp = A[k][p], akq = A[k][r];
-          A[k][p] = c * akp - s * akq;
-          A[k][r] = s * akp + c * akq;
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        __syncwarp();
+        if (lane < 9) {   // A <- A J
+          const double akp = A[lane][p], akq = A[lane][r];
+          A[lane][p] = c * akp - sn * akq;
+          A[lane][r] = sn * akp + c * akq;
         }
-        for (int k = 0; k < 9; k++) {   // A <- J^T A
-          const double apk = A[p][k], aqk = A[r][k];
-          A[p][k] = c * apk - s * aqk;
-          A[r][k] = s * apk + c * aqk;
+        __syncwarp();
+        if (lane < 9) {   // A <- J^T A
+          const double apk = A[p][lane], aqk = A[r][lane];
+          A[p][lane] = c * apk - sn * aqk;
+          A[r][lane] = sn * apk + c * aqk;
+          const double vkp = V[lane][p], vkq = V[lane][r];
+          V[lane][p] = c * vkp - sn * vkq;
+          V[lane][r] = sn * vkp + c * vkq;
         }
-        for (int k = 0; k < 9; k++) {
-          const double vkp = V[k][p], vkq = V[k][r];
-          V[k][p] = c * vkp - s * vkq;
-          V[k][r] = s * vkp + c * vkq;
-        }
+        __syncwarp();
       }
+    if (!rot) break;
   }
   int m = 0;
   for (int i = 1; i < 9; i++)
     if (A[i][i] < A[m][m]) m = i;
-  for (int i = 0; i < 9; i++) out[i] = V[i][m];
+  if (lane < 9) out[lane] = V[lane][m];
+  __syncwarp();
 }
 
-__global__ void __launch_bounds__(RS_THREADS) k_rs_refit(RsProb q, double* H_out, uint8_t* inl_out, int32_t* n_out)
+// ---- refit (matching.py:183-192), split into grid-wide passes ------------
+// Per problem: status 0 = (None, []), 1 = best model found, 2 = final model.
+// Every pass sums the per-chunk partials of the earlier passes in chunk
+// order, so results are bitwise reproducible (no floating-point atomics).
+constexpr int RS_RCH = 4096;   // points per refit-pass CTA
+constexpr int RS_NPART = 32;   // partial slots per (problem, chunk)
+//   [0] m  [1..4] sum x, y, dx, dy  [5, 6] sum distances  [7] final count
+//   [8..31] normal-matrix sums
+
+struct RsRefit {
+  double* part;     // [P][rchunks][RS_NPART]
+  double* hbest;    // [P][9]
+  double* hfin;     // [P][9]
+  int32_t* status;  // [P]
+  int rchunks;
+};
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_best(RsProb q, RsRefit r)
 {
-  __shared__ double red[RS_THREADS / 32 * 24];
-  __shared__ double hsm[9];
-  __shared__ double G[9][9];
-  __shared__ int ok;
+  __shared__ unsigned long long wkey[RS_THREADS / 32];
   const int p = blockIdx.x, tid = threadIdx.x;
   const int64_t base = q.off[p], n = q.off[p + 1] - base;
+  // best iteration: max count, first index (the strict > of matching.py:180)
+  unsigned long long key = 0ull;
+  if (n >= 4)
+    for (int k = tid; k < q.iters; k += RS_THREADS) {
+      const int c = q.cnt[(long long)p * q.iters + k];
+      const unsigned long long kk = ((unsigned long long)(unsigned)c << 32) | (0xffffffffu - (unsigned)k);
+      key = c > 0 && kk > key ? kk : key;
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+    key = other > key ? other : key;
+  }
+  if ((tid & 31) == 0) wkey[tid >> 5] = key;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 0; w < RS_THREADS / 32; w++) key = wkey[w] > key ? wkey[w] : key;
+    int st = 0;
+    if ((int)(key >> 32) >= 4) {   // matching.py:183-184
+      const int kb = (int)(0xffffffffu - (unsigned)(key & 0xffffffffu));
+      st = minimal_h(q.src + base, q.dst + base, q.table + ((long long)p * q.iters + kb) * 4, r.hbest + 9 * p) ? 1 : 0;
+    }
+    r.status[p] = st;
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void part_sum(const RsRefit& r, int p, int slot, double* out)
+{
+  for (int j = 0; j < NV; j++) out[j] = 0.0;
+  const double* pp = r.part + (long long)p * r.rchunks * RS_NPART + slot;
+  for (int c = 0; c < r.rchunks; c++)
+    for (int j = 0; j < NV; j++) out[j] += pp[(long long)c * RS_NPART + j];
+}
+
+// conditioning of the consensus set from the pass-0 / pass-1 partials
+struct RsNorm {
+  double m, scx, scy, dcx, dcy, ss, ds;
+  bool ok;
+};
+
+__device__ __forceinline__ RsNorm rs_norm(const RsRefit& r, int p, bool with_scale)
+{
+  double v[7];
+  part_sum<7>(r, p, 0, v);
+  RsNorm o;
+  o.m = v[0];
+  o.scx = v[1] / o.m; o.scy = v[2] / o.m; o.dcx = v[3] / o.m; o.dcy = v[4] / o.m;
+  o.ok = true;
+  o.ss = o.ds = 0.0;
+  if (with_scale) {
+    const double sd_s = v[5] / o.m, sd_d = v[6] / o.m;
+    o.ok = !(sd_s < 1e-12 || sd_d < 1e-12);   // _normalize_points -> None (matching.py:100-101)
+    o.ss = 1.4142135623730951 / sd_s;
+    o.ds = 1.4142135623730951 / sd_d;
+  }
+  return o;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_pass(RsProb q, RsRefit r, uint8_t* inl_out)
+{
+  __shared__ double red[RS_THREADS / 32 * 24];
+  const int p = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
+  const int64_t base = q.off[p], n = q.off[p + 1] - base;
+  const int64_t lo = (int64_t)ch * RS_RCH, hi = min(n, lo + RS_RCH);
+  if (lo >= n) return;
   const double2* src = q.src + base;
   const double2* dst = q.dst + base;
   uint8_t* mask = inl_out + base;
-  const unsigned long long key = n >= 4 ? q.best[p] : 0ull;
-  const int bc = (int)(key >> 32);
-  auto fail = [&]() {
-    for (int64_t i = tid; i < n; i += RS_THREADS) mask[i] = 0;
-    if (tid < 9) H_out[9 * p + tid] = NAN;
-    if (tid == 0) n_out[p] = -1;
-  };
-  if (bc < 4) { fail(); return; }   // matching.py:183-184
-  if (tid == 0) {
-    const int kb = (int)(0xffffffffu - (unsigned)(key & 0xffffffffu));
-    ok = minimal_h(src, dst, q.table + ((long long)p * q.iters + kb) * 4, hsm);
-  }
-  __syncthreads();
-  double hb[9];
-  for (int j = 0; j < 9; j++) hb[j] = hsm[j];
-  // consensus set of the best model: centroids (matching.py:98)
-  double v[24];
-  for (int j = 0; j < 5; j++) v[j] = 0.0;
-  for (int64_t i = tid; i < n; i += RS_THREADS) {
-    const double2 s = src[i], d = dst[i];
-    const bool in = reproj_inlier(hb, s, d, q.tol);
-    mask[i] = in;
-    if (in) { v[0] += 1.0; v[1] += s.x; v[2] += s.y; v[3] += d.x; v[4] += d.y; }
-  }
-  block_sum<5>(v, red);
-  const double m = v[0];
-  const double scx = v[1] / m, scy = v[2] / m, dcx = v[3] / m, dcy = v[4] / m;
-  // mean distances (matching.py:99)
-  v[0] = v[1] = 0.0;
-  for (int64_t i = tid; i < n; i += RS_THREADS)
-    if (mask[i]) {
-      const double2 s = src[i], d = dst[i];
-      v[0] += sqrt((s.x - scx) * (s.x - scx) + (s.y - scy) * (s.y - scy));
-      v[1] += sqrt((d.x - dcx) * (d.x - dcx) + (d.y - dcy) * (d.y - dcy));
-    }
-  block_sum<2>(v, red);
-  const double sd_s = v[0] / m, sd_d = v[1] / m;
-  if (sd_s < 1e-12 || sd_d < 1e-12) { fail(); return; }   // _normalize_points -> None
-  const double ss = 1.4142135623730951 / sd_s, ds = 1.4142135623730951 / sd_d;
-  // normal matrix A^T A of the DLT rows (matching.py:114-119): with
-  // s = (u, v, 1) and d = (a, b), it is built from sum w * s s^T for
-  // w in {1, a, b, a^2 + b^2} (4 x 6 distinct sums)
-  for (int j = 0; j < 24; j++) v[j] = 0.0;
-  for (int64_t i = tid; i < n; i += RS_THREADS)
-    if (mask[i]) {
-      const double2 s = src[i], d = dst[i];
-      const double u = ss * s.x - ss * scx, w = ss * s.y - ss * scy;
-      const double a = ds * d.x - ds * dcx, b = ds * d.y - ds * dcy;
-      const double ssT[6] = {u * u, u * w, u, w * w, w, 1.0};
-      const double wt[4] = {1.0, a, b, a * a + b * b};
-#pragma unroll
-      for (int c = 0; c < 4; c++)
-#pragma unroll
-        for (int e = 0; e < 6; e++) v[6 * c + e] += wt[c] * ssT[e];
-    }
-  block_sum<24>(v, red);
-  if (tid == 0) {
-    auto S = [&](int c, int i, int j) {   // (sum w_c s s^T)[i][j]
-      const int lo = i < j ? i : j, hi = i < j ? j : i;
-      const int e = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-      return v[6 * c + e];
-    };
-    for (int i = 0; i < 9; i++)
-      for (int j = 0; j < 9; j++) G[i][j] = 0.0;
-    for (int i = 0; i < 3; i++)
-      for (int j = 0; j < 3; j++) {
-        G[i][j] = G[3 + i][3 + j] = S(0, i, j);
-        G[i][6 + j] = G[6 + j][i] = -S(1, i, j);
-        G[3 + i][6 + j] = G[6 + j][3 + i] = -S(2, i, j);
-        G[6 + i][6 + j] = S(3, i, j);
+  const int st = r.status[p];
+  double* out = r.part + ((long long)p * r.rchunks + ch) * RS_NPART;
+  const double tol2 = q.tol * q.tol;
+  const bool fast = q.tol > 0.0;
+  if (PASS == 3) {   // final inliers (matching.py:190-192)
+    int c = 0;
+    double h[9];
+    for (int j = 0; j < 9; j++) h[j] = st == 2 ? r.hfin[9 * p + j] : 0.0;
+    for (int64_t i = lo + tid; i < hi; i += RS_THREADS) {
+      bool in = false;
+      if (st == 2) {
+        const double2 s = src[i], d = dst[i];
+        in = reproj_inlier_fast(h, s, d, q.tol, tol2, fast && plain_point(s, d));
       }
-    double hn[9], t[9], h[9];
-    least_eigvec9(G, hn);
-    const double ts[9] = {ss, 0.0, -ss * scx, 0.0, ss, -ss * scy, 0.0, 0.0, 1.0};
-    const double tdi[9] = {1.0 / ds, 0.0, dcx, 0.0, 1.0 / ds, dcy, 0.0, 0.0, 1.0};
-    mat3mul(hn, ts, t);
-    mat3mul(tdi, t, h);
-    ok = finish_usable(h);
-    for (int j = 0; j < 9; j++) hsm[j] = h[j];
+      mask[i] = in;
+      c += in;
+    }
+    double v[1] = {(double)c};
+    block_sum<1>(v, red);
+    if (tid == 0) out[7] = v[0];
+    return;
   }
-  __syncthreads();
-  if (!ok) { fail(); return; }
-  for (int j = 0; j < 9; j++) hb[j] = hsm[j];
-  int c = 0;
-  for (int64_t i = tid; i < n; i += RS_THREADS) {
-    const bool in = reproj_inlier(hb, src[i], dst[i], q.tol);
-    mask[i] = in;
-    c += in;
+  if (st != 1) return;
+  if (PASS == 0) {   // consensus set of the best model + centroid sums (matching.py:98,177-182)
+    double h[9], v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int j = 0; j < 9; j++) h[j] = r.hbest[9 * p + j];
+    for (int64_t i = lo + tid; i < hi; i += RS_THREADS) {
+      const double2 s = src[i], d = dst[i];
+      const bool in = reproj_inlier_fast(h, s, d, q.tol, tol2, fast && plain_point(s, d));
+      mask[i] = in;
+      if (in) { v[0] += 1.0; v[1] += s.x; v[2] += s.y; v[3] += d.x; v[4] += d.y; }
+    }
+    block_sum<5>(v, red);
+    if (tid < 5) out[tid] = v[tid];
+  } else if (PASS == 1) {   // mean distances to the centroids (matching.py:99)
+    const RsNorm nm = rs_norm(r, p, false);
+    double v[2] = {0.0, 0.0};
+    for (int64_t i = lo + tid; i < hi; i += RS_THREADS)
+      if (mask[i]) {
+        const double2 s = src[i], d = dst[i];
+        v[0] += sqrt((s.x - nm.scx) * (s.x - nm.scx) + (s.y - nm.scy) * (s.y - nm.scy));
+        v[1] += sqrt((d.x - nm.dcx) * (d.x - nm.dcx) + (d.y - nm.dcy) * (d.y - nm.dcy));
+      }
+    block_sum<2>(v, red);
+    if (tid < 2) out[5 + tid] = v[tid];
+  } else {   // PASS 2: normal matrix A^T A of the DLT rows (matching.py:114-119)
+    const RsNorm nm = rs_norm(r, p, true);
+    // with s = (u, v, 1) and d = (a, b): sums of w s s^T, w in {1, a, b, a^2 + b^2}
+    double v[24];
+    for (int j = 0; j < 24; j++) v[j] = 0.0;
+    if (nm.ok)
+      for (int64_t i = lo + tid; i < hi; i += RS_THREADS)
+        if (mask[i]) {
+          const double2 s = src[i], d = dst[i];
+          const double u = nm.ss * s.x - nm.ss * nm.scx, w = nm.ss * s.y - nm.ss * nm.scy;
+          const double a = nm.ds * d.x - nm.ds * nm.dcx, b = nm.ds * d.y - nm.ds * nm.dcy;
+          const double ssT[6] = {u * u, u * w, u, w * w, w, 1.0};
+          const double wt[4] = {1.0, a, b, a * a + b * b};
+#pragma unroll
+          for (int c = 0; c < 4; c++)
+#pragma unroll
+            for (int e = 0; e < 6; e++) v[6 * c + e] += wt[c] * ssT[e];
+        }
+    block_sum<24>(v, red);
+    if (tid < 24) out[8 + tid] = v[tid];
   }
-  c = __reduce_add_sync(0xffffffffu, c);
-  __shared__ int csum;
-  if (tid == 0) csum = 0;
-  __syncthreads();
-  if ((tid & 31) == 0) atomicAdd(&csum, c);
-  __syncthreads();
-  if (tid < 9) H_out[9 * p + tid] = hb[tid];
-  if (tid == 0) n_out[p] = csum;
 }
 
-__global__ void k_rs_init(int P, unsigned long long* best, int32_t* first_rej, int iters)
+// warp per problem: assemble A^T A, least eigenvector, de-normalize, _usable
+__global__ void __launch_bounds__(32) k_rs_solve(RsProb q, RsRefit r)
+{
+  __shared__ double G[9][9], V[9][9], hn[9];
+  const int p = blockIdx.x, lane = threadIdx.x;
+  if (r.status[p] != 1) return;
+  const RsNorm nm = rs_norm(r, p, true);
+  if (!nm.ok) {
+    if (lane == 0) r.status[p] = 0;
+    return;
+  }
+  double v[24];
+  part_sum<24>(r, p, 8, v);
+  auto S = [&](int c, int i, int j) {   // (sum w_c s s^T)[i][j]
+    const int lo = i < j ? i : j, hi = i < j ? j : i;
+    const int e = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+    return v[6 * c + e];
+  };
+  if (lane < 9) {
+    const int i = lane;
+    for (int j = 0; j < 9; j++) G[i][j] = 0.0;
+    if (i < 3) {
+      for (int j = 0; j < 3; j++) { G[i][j] = S(0, i, j); G[i][6 + j] = -S(1, i, j); }
+    } else if (i < 6) {
+      for (int j = 0; j < 3; j++) { G[i][3 + j] = S(0, i - 3, j); G[i][6 + j] = -S(2, i - 3, j); }
+    } else {
+      for (int j = 0; j < 3; j++) {
+        G[i][j] = -S(1, j, i - 6);
+        G[i][3 + j] = -S(2, j, i - 6);
+        G[i][6 + j] = S(3, i - 6, j);
+      }
+    }
+  }
+  __syncwarp();
+  least_eigvec9_warp(G, V, hn);
+  if (lane == 0) {
+    double h[9], t[9], hh[9];
+    for (int j = 0; j < 9; j++) hh[j] = hn[j];
+    const double ts[9] = {nm.ss, 0.0, -nm.ss * nm.scx, 0.0, nm.ss, -nm.ss * nm.scy, 0.0, 0.0, 1.0};
+    const double tdi[9] = {1.0 / nm.ds, 0.0, nm.dcx, 0.0, 1.0 / nm.ds, nm.dcy, 0.0, 0.0, 1.0};
+    mat3mul(hh, ts, t);
+    mat3mul(tdi, t, h);
+    const bool ok = finish_usable(h);
+    for (int j = 0; j < 9; j++) r.hfin[9 * p + j] = h[j];
+    r.status[p] = ok ? 2 : 0;
+  }
+}
+
+__global__ void k_rs_out(RsRefit r, int P, double* H_out, int32_t* n_out)
 {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < P) { best[p] = 0ull; first_rej[p] = iters; }
+  if (p >= P) return;
+  if (r.status[p] != 2) {
+    for (int j = 0; j < 9; j++) H_out[9 * p + j] = NAN;
+    n_out[p] = -1;
+    return;
+  }
+  double c[1];
+  part_sum<1>(r, p, 7, c);
+  for (int j = 0; j < 9; j++) H_out[9 * p + j] = r.hfin[9 * p + j];
+  n_out[p] = (int32_t)c[0];
 }
 
-int rs_scratch(int P, int iters, const int64_t* off_host, cudaStream_t st, void** mem, RsProb& q)
+__global__ void k_rs_init(int P, int32_t* first_rej, int iters)
 {
-  const size_t o_off = 0, o_best = ((size_t)(P + 1) * 8 + 255) & ~(size_t)255;
-  const size_t o_rej = o_best + (((size_t)P * 8 + 255) & ~(size_t)255);
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < P) first_rej[p] = iters;
+}
+
+// Stream-ordered scratch from a private pool that keeps its memory (release
+// threshold = max), so repeated calls reuse it without remapping.
+cudaMemPool_t rs_pool()
+{
+  static cudaMemPool_t pool = [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &pp) != cudaSuccess) return (cudaMemPool_t) nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    return p;
+  }();
+  return pool;
+}
+
+int rs_scratch(int P, int iters, const int64_t* off_host, cudaStream_t st, void** mem, RsProb& q, RsRefit* rf = nullptr,
+               int rchunks = 0)
+{
+  const size_t o_off = 0, o_cnt = ((size_t)(P + 1) * 8 + 255) & ~(size_t)255;
+  const size_t o_rej = o_cnt + (((size_t)P * iters * 4 + 255) & ~(size_t)255);
   const size_t o_tab = o_rej + (((size_t)P * 4 + 255) & ~(size_t)255);
-  const size_t bytes = o_tab + (size_t)P * iters * 16 + 16;
+  const size_t o_part = o_tab + (((size_t)P * iters * 16 + 255) & ~(size_t)255);
+  const size_t o_hb = o_part + (size_t)P * rchunks * RS_NPART * 8;
+  const size_t o_hf = o_hb + (size_t)P * 9 * 8, o_st = o_hf + (size_t)P * 9 * 8;
+  const size_t bytes = o_st + (size_t)P * 4 + 16;
   char* m = nullptr;
-  if (cudaMallocAsync((void**)&m, bytes, st) != cudaSuccess) return VF_ERR_CUDA;
+  cudaMemPool_t pool = rs_pool();
+  if (!pool || cudaMallocFromPoolAsync((void**)&m, bytes, pool, st) != cudaSuccess) return VF_ERR_CUDA;
   if (cudaMemcpyAsync(m + o_off, off_host, (size_t)(P + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
     cudaFreeAsync(m, st);
     return VF_ERR_CUDA;
   }
   q.off = reinterpret_cast<const int64_t*>(m + o_off);
-  q.best = reinterpret_cast<unsigned long long*>(m + o_best);
+  q.cnt = reinterpret_cast<int32_t*>(m + o_cnt);
+  if (cudaMemsetAsync(m + o_cnt, 0, (size_t)P * iters * 4, st) != cudaSuccess) {
+    cudaFreeAsync(m, st);
+    return VF_ERR_CUDA;
+  }
   q.first_rej = reinterpret_cast<int32_t*>(m + o_rej);
   q.table = reinterpret_cast<int32_t*>(m + o_tab);
+  if (rf) {
+    rf->part = reinterpret_cast<double*>(m + o_part);
+    rf->hbest = reinterpret_cast<double*>(m + o_hb);
+    rf->hfin = reinterpret_cast<double*>(m + o_hf);
+    rf->status = reinterpret_cast<int32_t*>(m + o_st);
+    rf->rchunks = rchunks;
+  }
   *mem = m;
   return VF_OK;
 }
 
 void rs_samples(const RsProb& q, cudaStream_t st)
 {
-  k_rs_init<<<(q.P + 255) / 256, 256, 0, st>>>(q.P, q.best, q.first_rej, q.iters);
+  k_rs_init<<<(q.P + 255) / 256, 256, 0, st>>>(q.P, q.first_rej, q.iters);
   const long long nt = (long long)q.P * q.iters;
   if (nt > 0) k_rs_samples<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(q);
   k_rs_fixup<<<(q.P + 127) / 128, 128, 0, st>>>(q);
@@ -499,9 +747,13 @@ extern "C" int vf_ransac_homography(int n_problems, const int64_t* offsets, cons
   if (offsets[n_problems] > 0 && (!src_dev || !dst_dev || !inlier_dev)) return VF_ERR_ARG;
   if (((uintptr_t)src_dev | (uintptr_t)dst_dev) & 15) return VF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  int64_t n_max = 0;
+  for (int p = 0; p < n_problems; p++) n_max = std::max(n_max, offsets[p + 1] - offsets[p]);
+  const int rchunks = (int)std::max<int64_t>(1, (n_max + RS_RCH - 1) / RS_RCH);
   RsProb q;
+  RsRefit rf;
   void* mem = nullptr;
-  const int rc = rs_scratch(n_problems, iters, offsets, st, &mem, q);
+  const int rc = rs_scratch(n_problems, iters, offsets, st, &mem, q, &rf, rchunks);
   if (rc != VF_OK) return rc;
   q.src = reinterpret_cast<const double2*>(src_dev);
   q.dst = reinterpret_cast<const double2*>(dst_dev);
@@ -510,8 +762,18 @@ extern "C" int vf_ransac_homography(int n_problems, const int64_t* offsets, cons
   q.seed = seed;
   q.tol = reproj_tol;
   rs_samples(q, st);
-  if (iters > 0) k_rs_score<<<dim3((unsigned)((iters + RS_HB - 1) / RS_HB), (unsigned)n_problems), RS_THREADS, 0, st>>>(q);
-  k_rs_refit<<<n_problems, RS_THREADS, 0, st>>>(q, H_dev, inlier_dev, n_inliers_dev);
+  q.chunks = (int)std::max<int64_t>(1, (n_max + RS_PCH - 1) / RS_PCH);
+  const long long gx = (long long)((iters + RS_HB - 1) / RS_HB) * q.chunks;
+  if (gx > INT32_MAX) { cudaFreeAsync(mem, st); return VF_ERR_ARG; }
+  if (iters > 0) k_rs_score<<<dim3((unsigned)gx, (unsigned)n_problems), RS_THREADS, 0, st>>>(q);
+  const dim3 pg((unsigned)rchunks, (unsigned)n_problems);
+  k_rs_best<<<n_problems, RS_THREADS, 0, st>>>(q, rf);
+  k_rs_pass<0><<<pg, RS_THREADS, 0, st>>>(q, rf, inlier_dev);
+  k_rs_pass<1><<<pg, RS_THREADS, 0, st>>>(q, rf, inlier_dev);
+  k_rs_pass<2><<<pg, RS_THREADS, 0, st>>>(q, rf, inlier_dev);
+  k_rs_solve<<<n_problems, 32, 0, st>>>(q, rf);
+  k_rs_pass<3><<<pg, RS_THREADS, 0, st>>>(q, rf, inlier_dev);
+  k_rs_out<<<(n_problems + 127) / 128, 128, 0, st>>>(rf, n_problems, H_dev, n_inliers_dev);
   cudaFreeAsync(mem, st);
   return cudaGetLastError() == cudaSuccess ? VF_OK : VF_ERR_CUDA;
 }

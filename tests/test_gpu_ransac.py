@@ -162,3 +162,27 @@ def test_locate_object_golden():
     assert many[0].object_id == many[2].object_id == est.object_id and many[0].mpr == est.mpr
     with pytest.raises(ValueError):
         locate_object(frame, [], cfg)
+
+
+def test_exact_fallback_paths():
+    """Points beyond the fast test's range (|coord| >= 1e7) and tol <= 0
+    decide as the oracle does."""
+    from oracle import oracle
+    from paper_1503_06959_b200.matching import project_points, ransac_homography_batch
+
+    rng = np.random.default_rng(4)
+    src = 3e7 + rng.uniform(0, 500, (60, 2))
+    dst = src + [5.0, -2.0]
+    dst[40:] += rng.uniform(20, 80, (20, 2))
+    probs = [(src, dst)]
+    for tol in (3.0, 0.0, -1.0):
+        got = ransac_homography_batch(probs, 300, tol, 3)
+        for p, (a, b) in enumerate(probs):
+            eh, einl = oracle.ransac_homography(a, b, 300, tol, 3)
+            h, inl = got[p]
+            assert (h is None) == (eh is None), (tol, p)
+            if h is not None:
+                assert inl == einl, (tol, p)
+                # far from the origin H's entries are ill-conditioned (linear part
+                # vs translation); the mapping itself must agree
+                assert np.abs(project_points(h, a) - project_points(eh, a)).max() < 1e-3, (tol, p)
