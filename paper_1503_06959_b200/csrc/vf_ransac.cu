@@ -253,21 +253,6 @@ __global__ void k_rs_fixup(RsProb q)
   for (int k = k0; k < q.iters; k++) vfr::choice4(g, (uint32_t)n, q.table + ((long long)p * q.iters + k) * 4);
 }
 
-// Fast decision of reproj_inlier_fast for a hypothesis row hv = (h0..h8,
-// 1e-6|h6|, 1e-6|h7|, 1e-6|h8|): returns 1 inlier, 0 outlier, -1 undecided
-// (then the exact form decides).
-__device__ __forceinline__ int fast_decide(const double* hv, double2 s, double2 d, double tlo, double thi)
-{
-  const double px = __fma_rn(s.x, hv[0], __fma_rn(s.y, hv[1], hv[2]));
-  const double py = __fma_rn(s.x, hv[3], __fma_rn(s.y, hv[4], hv[5]));
-  const double z = __fma_rn(s.x, hv[6], __fma_rn(s.y, hv[7], hv[8]));
-  const double zb = fmax(__fma_rn(fabs(s.x), hv[9], __fma_rn(fabs(s.y), hv[10], hv[11])), 1e-9);
-  const double ex = __fma_rn(-d.x, z, px), ey = __fma_rn(-d.y, z, py);
-  const double e = __fma_rn(ex, ex, __dmul_rn(ey, ey)), z2 = __dmul_rn(z, z);
-  const bool zok = fabs(z) > zb;
-  return zok && e < tlo * z2 ? 1 : (zok && e > thi * z2 ? 0 : -1);
-}
-
 constexpr int RS_PPT = 4;   // points per thread per hypothesis in k_rs_score
 
 __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
@@ -289,10 +274,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
     const int k = k0 + tid;
     cnt[tid] = 0;
     if (k < q.iters) ok = minimal_h(src, dst, q.table + ((long long)p * q.iters + k) * 4, hs[tid]);
-    if (ok) {
-      hs[tid][9] = 1e-6 * fabs(hs[tid][6]);
-      hs[tid][10] = 1e-6 * fabs(hs[tid][7]);
-      hs[tid][11] = 1e-6 * fabs(hs[tid][8]);
+    if (ok) {   // z-guard coefficients (see the point loop)
+      hs[tid][9] = 1e-6 * (fabs(hs[tid][6]) + fabs(hs[tid][7]));
+      hs[tid][10] = 1e-6 * fabs(hs[tid][8]);
+      hs[tid][11] = 0.0;
     }
     const unsigned b = __ballot_sync(0xffffffffu, ok);
     if (lane == 0) vb[tid >> 5] = b;
@@ -303,12 +288,19 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
   if (tid == 0) nvalid = __popc(vb[0]) + __popc(vb[1]);
   __syncthreads();
   const int nv = nvalid;
+  // Decisions without division / square root (as reproj_inlier_fast): with
+  // z unclamped, err < tol <=> |p - d z|^2 < tol^2 z^2, taken when the two
+  // sides differ by > 1e-6 relative and |z| > zt = 1e-6 ((|h6| + |h7|) B +
+  // |h8|) (>= 1e-6 (|h6 x| + |h7 y| + |h8|) for the thread's points, |x|, |y|
+  // <= B: no cancellation in z) and > 1e-9 (far from the clamp); all else,
+  // and coordinates >= 1e7, by the exact form.
   const bool fast = q.tol > 0.0;
   const double tlo = q.tol * q.tol * (1.0 - 1e-6), thi = q.tol * q.tol * (1.0 + 1e-6);
   int c0 = 0, c1 = 0;
   for (int64_t i0 = c_lo; i0 < c_hi; i0 += RS_THREADS * RS_PPT) {
     double2 s[RS_PPT], d[RS_PPT];
     unsigned live = 0, plain = 0;
+    double bnd = 0.0;
 #pragma unroll
     for (int u = 0; u < RS_PPT; u++) {
       const int64_t i = i0 + tid + u * RS_THREADS;
@@ -316,7 +308,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
       s[u] = in ? src[i] : make_double2(0.0, 0.0);
       d[u] = in ? dst[i] : make_double2(0.0, 0.0);
       live |= (unsigned)in << u;
-      plain |= (unsigned)(in && fast && plain_point(s[u], d[u])) << u;
+      const bool pl = in && fast && plain_point(s[u], d[u]);
+      plain |= (unsigned)pl << u;
+      if (pl) bnd = fmax(bnd, fmax(fabs(s[u].x), fabs(s[u].y)));
     }
     for (int j = 0; j < nv; j++) {
       const int h = vlist[j];
@@ -327,15 +321,24 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
         hv[e] = w.x;
         hv[e + 1] = w.y;
       }
+      double zt = __fma_rn(hv[9], bnd, hv[10]);
+      zt = zt > 1e-9 ? zt : 1e-9;
       int c = 0;
-      unsigned und = 0;
+      unsigned dec = 0;
 #pragma unroll
       for (int u = 0; u < RS_PPT; u++) {
-        const int r = fast_decide(hv, s[u], d[u], tlo, thi);
-        c += r == 1 && ((plain >> u) & 1);
-        und |= (unsigned)(r < 0 || !((plain >> u) & 1)) << u;
+        const double px = __fma_rn(s[u].x, hv[0], __fma_rn(s[u].y, hv[1], hv[2]));
+        const double py = __fma_rn(s[u].x, hv[3], __fma_rn(s[u].y, hv[4], hv[5]));
+        const double z = __fma_rn(s[u].x, hv[6], __fma_rn(s[u].y, hv[7], hv[8]));
+        const double ex = __fma_rn(-d[u].x, z, px), ey = __fma_rn(-d[u].y, z, py);
+        const double e = __fma_rn(ex, ex, __dmul_rn(ey, ey)), z2 = __dmul_rn(z, z);
+        const bool zok = fabs(z) > zt;
+        const bool inl = zok && e < tlo * z2, outl = zok && e > thi * z2;
+        const bool pl = (plain >> u) & 1;
+        c += inl && pl;
+        dec |= (unsigned)((inl || outl) && pl) << u;
       }
-      und &= live;
+      const unsigned und = live & ~dec;
       if (__any_sync(0xffffffffu, und != 0)) {   // rare: the exact reference form
 #pragma unroll
         for (int u = 0; u < RS_PPT; u++)
@@ -389,15 +392,15 @@ __device__ void least_eigvec9_warp(double (*A)[9], double (*V)[9], double* out)
   if (lane < 9)
     for (int j = 0; j < 9; j++) V[lane][j] = lane == j ? 1.0 : 0.0;
   __syncwarp();
-  // rotations below 1e-18 of ||A||_F are skipped (their effect on the
-  // eigenvectors is far below the rounding of the sums); stop after a sweep
-  // without rotations
+  // rotations below 1e-15 ||A||_F are skipped: cyclic Jacobi in fp64 leaves
+  // off-diagonals at ~eps ||A|| anyway, the accuracy the normal matrix
+  // carries; stop after a sweep without rotations
   double fro = 0.0;
   if (lane < 9)
     for (int j = 0; j < 9; j++) fro += A[lane][j] * A[lane][j];
 #pragma unroll
   for (int o = 16; o; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
-  const double small = 1e-18 * sqrt(fro);
+  const double small = 1e-15 * sqrt(fro);
   for (int sweep = 0; sweep < 30; sweep++) {
     bool rot = false;
     for (int p = 0; p < 8; p++)
