@@ -19,7 +19,8 @@
 //                  order (bitwise reproducible): k_rs_pass<0> consensus set +
 //                  centroids, <1> mean distances, <2> the 9x9 normal matrix of
 //                  the normalized DLT (matching.py:109-137); k_rs_solve (warp
-//                  per problem: least eigenvector by Jacobi, de-normalize, the
+//                  per problem: least eigenvector by inverse iteration,
+//                  de-normalize, the
 //                  usable test, matching.py:140-146); k_rs_pass<3> final
 //                  inlier mask + counts; k_rs_out (matching.py:187-192)
 // Minimal models: for 4 points the normalized DLT's null vector is the
@@ -383,58 +384,64 @@ __device__ void block_sum(double* v, double* red /* [RS_THREADS / 32][NV] */)
   __syncthreads();
 }
 
-// Least eigenvector of the symmetric 9x9 A (cyclic Jacobi), one warp: every
-// lane computes the rotation, lanes 0..8 apply it to their row / column; A
-// and V in shared memory, A destroyed.
-__device__ void least_eigvec9_warp(double (*A)[9], double (*V)[9], double* out)
+// Least eigenvector of the symmetric positive semi-definite 9x9 G by inverse
+// iteration on G + mu I (mu = 1e-12 trace keeps the Cholesky factor real
+// under rounding; the shift does not move eigenvectors).  Iterates until the
+// unit iterate changes by < 1e-15 (the accuracy limit eps ||G|| / gap of any
+// method on G); false if G is zero or not finite.  One thread, registers.
+__device__ bool least_eigvec9(const double (*G)[9], double* out)
 {
-  const int lane = threadIdx.x & 31;
-  if (lane < 9)
-    for (int j = 0; j < 9; j++) V[lane][j] = lane == j ? 1.0 : 0.0;
-  __syncwarp();
-  // rotations below 1e-15 ||A||_F are skipped: cyclic Jacobi in fp64 leaves
-  // off-diagonals at ~eps ||A|| anyway, the accuracy the normal matrix
-  // carries; stop after a sweep without rotations
-  double fro = 0.0;
-  if (lane < 9)
-    for (int j = 0; j < 9; j++) fro += A[lane][j] * A[lane][j];
+  double L[9][9];
+  double tr = 0.0;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
-  const double small = 1e-15 * sqrt(fro);
-  for (int sweep = 0; sweep < 30; sweep++) {
-    bool rot = false;
-    for (int p = 0; p < 8; p++)
-      for (int r = p + 1; r < 9; r++) {
-        const double apq = A[p][r];
-        if (!(fabs(apq) > small)) continue;
-        rot = true;
-        const double theta = (A[r][r] - A[p][p]) / (2.0 * apq);
-        const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
-        __syncwarp();
-        if (lane < 9) {   // A <- A J
-          const double akp = A[lane][p], akq = A[lane][r];
-          A[lane][p] = c * akp - sn * akq;
-          A[lane][r] = sn * akp + c * akq;
-        }
-        __syncwarp();
-        if (lane < 9) {   // A <- J^T A
-          const double apk = A[p][lane], aqk = A[r][lane];
-          A[p][lane] = c * apk - sn * aqk;
-          A[r][lane] = sn * apk + c * aqk;
-          const double vkp = V[lane][p], vkq = V[lane][r];
-          V[lane][p] = c * vkp - sn * vkq;
-          V[lane][r] = sn * vkp + c * vkq;
-        }
-        __syncwarp();
-      }
-    if (!rot) break;
+  for (int i = 0; i < 9; i++) tr += G[i][i];
+  if (!(tr > 0.0) || !isfinite(tr)) return false;
+  const double mu = 1e-12 * tr;
+#pragma unroll
+  for (int i = 0; i < 9; i++)
+#pragma unroll
+    for (int j = 0; j <= i; j++) {
+      double s = G[i][j] + (i == j ? mu : 0.0);
+#pragma unroll
+      for (int k = 0; k < j; k++) s -= L[i][k] * L[j][k];
+      if (i == j) L[i][i] = sqrt(s > 0.0 ? s : mu);
+      else L[i][j] = s / L[j][j];
+    }
+  double x[9];
+#pragma unroll
+  for (int i = 0; i < 9; i++) x[i] = 1.0 / 3.0;
+  for (int it = 0; it < 300; it++) {
+    double z[9], y[9];
+#pragma unroll
+    for (int i = 0; i < 9; i++) {   // L z = x
+      double s = x[i];
+#pragma unroll
+      for (int k = 0; k < i; k++) s -= L[i][k] * z[k];
+      z[i] = s / L[i][i];
+    }
+#pragma unroll
+    for (int i = 8; i >= 0; i--) {   // L^T y = z
+      double s = z[i];
+#pragma unroll
+      for (int k = i + 1; k < 9; k++) s -= L[k][i] * y[k];
+      y[i] = s / L[i][i];
+    }
+    double nrm = 0.0, dot = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; i++) { nrm += y[i] * y[i]; dot += y[i] * x[i]; }
+    const double inv = (dot < 0.0 ? -1.0 : 1.0) / sqrt(nrm);
+    double diff = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+      const double v = y[i] * inv;
+      diff = fmax(diff, fabs(v - x[i]));
+      x[i] = v;
+    }
+    if (!(diff >= 1e-15) && it > 0) break;
   }
-  int m = 0;
-  for (int i = 1; i < 9; i++)
-    if (A[i][i] < A[m][m]) m = i;
-  if (lane < 9) out[lane] = V[lane][m];
-  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 9; i++) out[i] = x[i];
+  return true;
 }
 
 // ---- refit (matching.py:183-192), split into grid-wide passes ------------
@@ -485,13 +492,27 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_best(RsProb q, RsRefit r)
   }
 }
 
+// Sum of NV partial slots over the problem's chunks by one full warp: lane l
+// takes chunks l, l + 32, ...; the 32 lane sums are then added in lane order
+// by every lane, so the result is the same in all lanes and in every run.
 template <int NV>
 __device__ __forceinline__ void part_sum(const RsRefit& r, int p, int slot, double* out)
 {
-  for (int j = 0; j < NV; j++) out[j] = 0.0;
+  const int lane = threadIdx.x & 31;
+  double acc[NV];
+#pragma unroll
+  for (int j = 0; j < NV; j++) acc[j] = 0.0;
   const double* pp = r.part + (long long)p * r.rchunks * RS_NPART + slot;
-  for (int c = 0; c < r.rchunks; c++)
-    for (int j = 0; j < NV; j++) out[j] += pp[(long long)c * RS_NPART + j];
+  for (int c = lane; c < r.rchunks; c += 32)
+#pragma unroll
+    for (int j = 0; j < NV; j++) acc[j] += pp[(long long)c * RS_NPART + j];
+#pragma unroll
+  for (int j = 0; j < NV; j++) {
+    double t = 0.0;
+#pragma unroll
+    for (int l = 0; l < 32; l++) t += __shfl_sync(0xffffffffu, acc[j], l);
+    out[j] = t;
+  }
 }
 
 // conditioning of the consensus set from the pass-0 / pass-1 partials
@@ -597,10 +618,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_pass(RsProb q, RsRefit r, uin
   }
 }
 
-// warp per problem: assemble A^T A, least eigenvector, de-normalize, _usable
+// warp per problem: assemble A^T A, least eigenvector (inverse iteration),
+// de-normalize, _usable
 __global__ void __launch_bounds__(32) k_rs_solve(RsProb q, RsRefit r)
 {
-  __shared__ double G[9][9], V[9][9], hn[9];
+  __shared__ double G[9][9];
   const int p = blockIdx.x, lane = threadIdx.x;
   if (r.status[p] != 1) return;
   const RsNorm nm = rs_norm(r, p, true);
@@ -631,33 +653,31 @@ __global__ void __launch_bounds__(32) k_rs_solve(RsProb q, RsRefit r)
     }
   }
   __syncwarp();
-  least_eigvec9_warp(G, V, hn);
   if (lane == 0) {
     double h[9], t[9], hh[9];
-    for (int j = 0; j < 9; j++) hh[j] = hn[j];
+    const bool eig = least_eigvec9(G, hh);
     const double ts[9] = {nm.ss, 0.0, -nm.ss * nm.scx, 0.0, nm.ss, -nm.ss * nm.scy, 0.0, 0.0, 1.0};
     const double tdi[9] = {1.0 / nm.ds, 0.0, nm.dcx, 0.0, 1.0 / nm.ds, nm.dcy, 0.0, 0.0, 1.0};
     mat3mul(hh, ts, t);
     mat3mul(tdi, t, h);
-    const bool ok = finish_usable(h);
+    const bool ok = eig && finish_usable(h);
     for (int j = 0; j < 9; j++) r.hfin[9 * p + j] = h[j];
     r.status[p] = ok ? 2 : 0;
   }
 }
 
-__global__ void k_rs_out(RsRefit r, int P, double* H_out, int32_t* n_out)
+__global__ void __launch_bounds__(32) k_rs_out(RsRefit r, double* H_out, int32_t* n_out)
 {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
+  const int p = blockIdx.x, lane = threadIdx.x;
   if (r.status[p] != 2) {
-    for (int j = 0; j < 9; j++) H_out[9 * p + j] = NAN;
-    n_out[p] = -1;
+    if (lane < 9) H_out[9 * p + lane] = NAN;
+    if (lane == 0) n_out[p] = -1;
     return;
   }
   double c[1];
   part_sum<1>(r, p, 7, c);
-  for (int j = 0; j < 9; j++) H_out[9 * p + j] = r.hfin[9 * p + j];
-  n_out[p] = (int32_t)c[0];
+  if (lane < 9) H_out[9 * p + lane] = r.hfin[9 * p + lane];
+  if (lane == 0) n_out[p] = (int32_t)c[0];
 }
 
 __global__ void k_rs_init(int P, int32_t* first_rej, int iters)
@@ -776,7 +796,7 @@ extern "C" int vf_ransac_homography(int n_problems, const int64_t* offsets, cons
   k_rs_pass<2><<<pg, RS_THREADS, 0, st>>>(q, rf, inlier_dev);
   k_rs_solve<<<n_problems, 32, 0, st>>>(q, rf);
   k_rs_pass<3><<<pg, RS_THREADS, 0, st>>>(q, rf, inlier_dev);
-  k_rs_out<<<(n_problems + 127) / 128, 128, 0, st>>>(rf, n_problems, H_dev, n_inliers_dev);
+  k_rs_out<<<n_problems, 32, 0, st>>>(rf, H_dev, n_inliers_dev);
   cudaFreeAsync(mem, st);
   return cudaGetLastError() == cudaSuccess ? VF_OK : VF_ERR_CUDA;
 }
