@@ -256,7 +256,8 @@ __global__ void k_rs_fixup(RsProb q)
 
 constexpr int RS_PPT = 4;   // points per thread per hypothesis in k_rs_score
 
-__global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
+static_assert(RS_HB * 4 == RS_THREADS, "one model per 4 threads");
+__global__ void __launch_bounds__(RS_THREADS, 2) k_rs_score(RsProb q)
 {
   __shared__ __align__(16) double hs[RS_HB][12];
   __shared__ int cnt[RS_HB];
@@ -269,24 +270,34 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_score(RsProb q)
   const double2* src = q.src + base;
   const double2* dst = q.dst + base;
   const int tid = threadIdx.x, lane = tid & 31;
-  __shared__ unsigned vb[2];
+  __shared__ unsigned vb[RS_THREADS / 32];
+  // model h is solved by thread 4 h (8 lanes in each of the 8 warps)
+  const int hm = tid >> 2;
+  const bool solver = (tid & 3) == 0;
   bool ok = false;
-  if (tid < RS_HB) {   // warps 0 and 1: one minimal model each
-    const int k = k0 + tid;
-    cnt[tid] = 0;
-    if (k < q.iters) ok = minimal_h(src, dst, q.table + ((long long)p * q.iters + k) * 4, hs[tid]);
+  if (tid < RS_HB) cnt[tid] = 0;
+  if (solver) {
+    const int k = k0 + hm;
+    if (k < q.iters) ok = minimal_h(src, dst, q.table + ((long long)p * q.iters + k) * 4, hs[hm]);
     if (ok) {   // z-guard coefficients (see the point loop)
-      hs[tid][9] = 1e-6 * (fabs(hs[tid][6]) + fabs(hs[tid][7]));
-      hs[tid][10] = 1e-6 * fabs(hs[tid][8]);
-      hs[tid][11] = 0.0;
+      hs[hm][9] = 1e-6 * (fabs(hs[hm][6]) + fabs(hs[hm][7]));
+      hs[hm][10] = 1e-6 * fabs(hs[hm][8]);
+      hs[hm][11] = 0.0;
     }
-    const unsigned b = __ballot_sync(0xffffffffu, ok);
-    if (lane == 0) vb[tid >> 5] = b;
   }
+  const unsigned b = __ballot_sync(0xffffffffu, ok);
+  if (lane == 0) vb[tid >> 5] = b;
   __syncthreads();
-  if (ok)   // compacted list of the usable models
-    vlist[(tid >= 32 ? __popc(vb[0]) : 0) + __popc(vb[tid >> 5] & ((1u << lane) - 1))] = tid;
-  if (tid == 0) nvalid = __popc(vb[0]) + __popc(vb[1]);
+  if (ok) {   // compacted list of the usable models, in model order
+    int before = __popc(b & ((1u << lane) - 1));
+    for (int w = 0; w < (tid >> 5); w++) before += __popc(vb[w]);
+    vlist[before] = hm;
+  }
+  if (tid == 0) {
+    int t = 0;
+    for (int w = 0; w < RS_THREADS / 32; w++) t += __popc(vb[w]);
+    nvalid = t;
+  }
   __syncthreads();
   const int nv = nvalid;
   // Decisions without division / square root (as reproj_inlier_fast): with
@@ -386,10 +397,11 @@ __device__ void block_sum(double* v, double* red /* [RS_THREADS / 32][NV] */)
 
 // Least eigenvector of the symmetric positive semi-definite 9x9 G by inverse
 // iteration on G + mu I (mu = 1e-12 trace keeps the Cholesky factor real
-// under rounding; the shift does not move eigenvectors).  Iterates until the
+// under rounding; the shift does not move eigenvectors), started from x0
+// (the best minimal model in the same coordinates).  Iterates until the
 // unit iterate changes by < 1e-15 (the accuracy limit eps ||G|| / gap of any
 // method on G); false if G is zero or not finite.  One thread, registers.
-__device__ bool least_eigvec9(const double (*G)[9], double* out)
+__device__ bool least_eigvec9(const double (*G)[9], const double* x0, double* out)
 {
   double L[9][9];
   double tr = 0.0;
@@ -407,9 +419,12 @@ __device__ bool least_eigvec9(const double (*G)[9], double* out)
       if (i == j) L[i][i] = sqrt(s > 0.0 ? s : mu);
       else L[i][j] = s / L[j][j];
     }
-  double x[9];
+  double x[9], n0 = 0.0;
 #pragma unroll
-  for (int i = 0; i < 9; i++) x[i] = 1.0 / 3.0;
+  for (int i = 0; i < 9; i++) n0 += x0[i] * x0[i];
+  n0 = n0 > 0.0 && isfinite(n0) ? 1.0 / sqrt(n0) : 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; i++) x[i] = n0 > 0.0 ? x0[i] * n0 : 1.0 / 3.0;
   for (int it = 0; it < 300; it++) {
     double z[9], y[9];
 #pragma unroll
@@ -654,8 +669,17 @@ __global__ void __launch_bounds__(32) k_rs_solve(RsProb q, RsRefit r)
   }
   __syncwarp();
   if (lane == 0) {
-    double h[9], t[9], hh[9];
-    const bool eig = least_eigvec9(G, hh);
+    double h[9], t[9], hh[9], x0[9];
+    {   // warm start: T_d H_best T_s^-1
+      const double* hb = r.hbest + 9 * p;
+      const double tsi[9] = {1.0 / nm.ss, 0.0, nm.scx, 0.0, 1.0 / nm.ss, nm.scy, 0.0, 0.0, 1.0};
+      const double td[9] = {nm.ds, 0.0, -nm.ds * nm.dcx, 0.0, nm.ds, -nm.ds * nm.dcy, 0.0, 0.0, 1.0};
+      double hb9[9];
+      for (int j = 0; j < 9; j++) hb9[j] = hb[j];
+      mat3mul(hb9, tsi, t);
+      mat3mul(td, t, x0);
+    }
+    const bool eig = least_eigvec9(G, x0, hh);
     const double ts[9] = {nm.ss, 0.0, -nm.ss * nm.scx, 0.0, nm.ss, -nm.ss * nm.scy, 0.0, 0.0, 1.0};
     const double tdi[9] = {1.0 / nm.ds, 0.0, nm.dcx, 0.0, 1.0 / nm.ds, nm.dcy, 0.0, 0.0, 1.0};
     mat3mul(hh, ts, t);
