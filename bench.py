@@ -491,10 +491,11 @@ def run_match(args, rank, world, local):
 
 def verify_sets(pairs, n_max, device, impl_ref):
     """(src, dst) match coordinates of radius_match(frame 2, frame 1, t_m) for
-    config-5 streams 0..pairs-1: the count_mpr input between consecutive
-    frames (matching.py:209-220).  Each set is the first n_max matches in
-    np.nonzero order.  Built on the GPU (engine + radius match) for our arm,
-    by the oracle on the host for the reference arm."""
+    config-5 streams 0..pairs-1 (CPU-generated frames in both arms): the
+    count_mpr input between consecutive frames (matching.py:209-220).  Each
+    set is the first n_max matches in np.nonzero order (all if n_max <= 0).
+    Built on the GPU (engine + radius match) for our arm, by the oracle on the
+    host for the reference arm."""
     import torch
 
     from paper_1503_06959_b200 import scenes
@@ -522,7 +523,8 @@ def verify_sets(pairs, n_max, device, impl_ref):
     from paper_1503_06959_b200.matching import radius_match_device
     from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
 
-    frames = gen_frames(list(range(pairs)), 3, device)
+    # frames drawn on the CPU generator, as the reference arm's: both arms verify identical match sets
+    frames = scenes.generate(scenes.CONFIGS[5], 3, streams=range(pairs)).permute(1, 0, 2, 3).contiguous().to(device)
     eng = FeatureEngine(W_FR, H_FR, PipelineConfig(mask=MaskConfig(mode="intensity")), n_streams=pairs)
     got = []
     for n in range(3):
@@ -652,19 +654,34 @@ def run_verify(args, rank, world, local):
         line = {"metric": metric, "value": v, "unit": "sets/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": dict(cfg, l2="inputs (< 1 MB) stay L2-resident by design: every set is re-read by "
-                                       "1000 hypotheses",
+                "config": dict(cfg, l2=f"inputs ({32 * sum(n_pts) / 1e6:.1f} MB of coordinates) stay L2-resident "
+                                       "by design: every set is re-read by 1000 hypotheses",
                                mpr=[len(r[1]) for r in res][:8]),
-                "roofline": {"bound": "fp64", "achieved": evals * world * args.steps / (ms_max / 1e3) / 1e9,
-                             "peak": None, "unit": "G hypothesis-match evaluations/s", "frac": None,
-                             "traffic": None, "kernel": "k_rs_score (whole step, live CUDA events)"},
+                "roofline": verify_roofline(evals * world * args.steps / (ms_max / 1e3) / 1e9),
                 "e2e": {"value": len(sets) / e2e_s, "unit": "sets/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "api": "host (src, dst) arrays -> ransac_homography_batch -> "
                                                           "(H, inlier lists) on the host"},
-                "gpu_launches": args.steps * 6, "clocks": clk.summary()}
+                "gpu_launches": args.steps * 11, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def verify_roofline(achieved_g):
+    """k_rs_score is fp64-pipe bound (16.5 fp64 instructions per
+    hypothesis-match evaluation); frac = the fp64 pipe's active fraction from
+    the committed ncu capture (profiles/r01d_verify_score.json), peak = the
+    evaluation rate at a fully busy pipe implied by it."""
+    prof = ROOT / "profiles" / "r01d_verify_score.json"
+    frac = None
+    if prof.exists():
+        frac = json.loads(prof.read_text()).get("sm__pipe_fp64_cycles_active_pct", None)
+        frac = frac / 100.0 if frac else None
+    return {"bound": "fp64", "achieved": achieved_g, "peak": achieved_g / frac if frac else None,
+            "unit": "G hypothesis-match evaluations/s", "frac": frac,
+            "traffic": 42758912 + 51456 if prof.exists() else None,
+            "kernel": "k_rs_score (92% of the call; whole-step rate from live CUDA events)",
+            "peak_source": "fp64 pipe utilization of k_rs_score, ncu --set full (profiles/r01d_verify_score.json)"}
 
 
 def run_dump(args):
