@@ -1054,10 +1054,25 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       *reinterpret_cast<uint4*>(&fw.tile[rr][16 * c16]) = v;
     }
     __syncwarp();
-    // ---- pass 1: exact 4-point necessary test (detector.py:117-125) ----
-    // 16x2 lanes: N + 512 - C - (t+1) has bit 9 set iff N > C + t (bright),
-    // C + 512 - (t+1) - N iff N < C - t (dark); no borrow crosses a lane.
-    const uint32_t T1 = (uint32_t)(t + 1) * 0x00010001u, BIAS = 0x02000200u;
+    // ---- pass 1: 4-point necessary test (detector.py:117-125) ----
+    // A 9-arc covers two adjacent compass points, both brighter than C + t or
+    // both darker than C - t, so both have |X - C| > t: the test below (an
+    // adjacent pair over the threshold in absolute difference) keeps every
+    // corner; pass 2 decides exactly.  Four pixels per word: VABSDIFF4, then
+    // a borrow-free per-byte compare a > t into bit 7 of each byte.
+    const uint32_t T4 = (uint32_t)(t < 128 ? t + 1 : t - 127) * 0x01010101u;
+    const bool lowT = t < 128;
+    auto over = [&](uint32_t X, uint32_t C) {
+      const uint32_t a = __vabsdiffu4(X, C);
+      return lowT ? (((a | 0x80808080u) - T4) | a) & 0x80808080u
+                  : ((((a & 0x7f7f7f7fu) | 0x80808080u) - T4) & a) & 0x80808080u;
+    };
+    uint32_t inb = 0;                       // this lane's pixels inside [3, w - 3)
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int x = x0 + 4 * lane + i;
+      inb |= (x >= 3 && x < w - 3) ? (0x80u << (8 * i)) : 0u;
+    }
     int qn = 0;
     for (int r = 0; r < VF_TILE_H; r++) {
       const int y = y0 + r, k = lane;       // word k of row r: pixels x0 + 4k .. +3
@@ -1070,36 +1085,13 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
         const uint32_t N = *reinterpret_cast<const uint32_t*>(&fw.tile[r][cb]);
         const uint32_t S = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 6][cb]);
         const uint32_t E = __byte_perm(C, B, 0x6543), Wd = __byte_perm(P, C, 0x4321);   // x + 3, x - 3
-        uint32_t res[2];
+        pass = (over(N, C) | over(S, C)) & (over(E, C) | over(Wd, C)) & inb;
+        if (pass && um) {
+          const uint8_t* crow = cells + (long long)fw.rc[r] * cols;
+          uint32_t gv[4];
 #pragma unroll
-        for (int hh = 0; hh < 2; hh++) {
-          const uint32_t sel = hh ? 0x4342u : 0x4140u;
-          const uint32_t c2 = __byte_perm(C, 0, sel), n2 = __byte_perm(N, 0, sel), s2 = __byte_perm(S, 0, sel);
-          const uint32_t e2 = __byte_perm(E, 0, sel), w2 = __byte_perm(Wd, 0, sel);
-          const uint32_t ct = c2 + T1, cb2 = c2 + BIAS - T1;
-          const uint32_t bN = n2 + BIAS - ct, bS = s2 + BIAS - ct, bE = e2 + BIAS - ct, bW = w2 + BIAS - ct;
-          const uint32_t dN = cb2 - n2, dS = cb2 - s2, dE = cb2 - e2, dW = cb2 - w2;
-          res[hh] = (((bN | bS) & (bE | bW)) | ((dN | dS) & (dE | dW))) & BIAS;
-        }
-        // bits 9 / 25 of res[0] = pixels 0 / 1, of res[1] = pixels 2 / 3 -> bit 8i + 7
-        pass = ((res[0] >> 2) & 0x80u) | ((res[0] >> 10) & 0x8000u) | ((res[1] << 14) & 0x800000u) |
-               ((res[1] << 6) & 0x80000000u);
-        if (pass) {
-          const uint8_t* crow = um ? cells + (long long)fw.rc[r] * cols : nullptr;
-          uint32_t gate = 0xffffffffu;
-          if (um) {
-            uint32_t gv[4];
-#pragma unroll
-            for (int i = 0; i < 4; i++) gv[i] = (pass >> (8 * i + 7)) & 1u ? crow[fw.cc[4 * k + i]] : 0u;
-            gate = (gv[0] ? 0xffu : 0u) | (gv[1] ? 0xff00u : 0u) | (gv[2] ? 0xff0000u : 0u) | (gv[3] ? 0xff000000u : 0u);
-          }
-          uint32_t inb = 0;
-#pragma unroll
-          for (int i = 0; i < 4; i++) {
-            const int x = x0 + 4 * k + i;
-            inb |= (x >= 3 && x < w - 3) ? (0xffu << (8 * i)) : 0u;
-          }
-          pass &= gate & inb;
+          for (int i = 0; i < 4; i++) gv[i] = (pass >> (8 * i + 7)) & 1u ? crow[fw.cc[4 * k + i]] : 0u;
+          pass &= (gv[0] ? 0xffu : 0u) | (gv[1] ? 0xff00u : 0u) | (gv[2] ? 0xff0000u : 0u) | (gv[3] ? 0xff000000u : 0u);
         }
       }
       // queue slots: exclusive prefix of the per-lane counts (0..4) from
