@@ -276,6 +276,9 @@ struct vf_ctx {
   std::vector<cudaEvent_t> ev_pool, ev_used;
   std::vector<int> ev_stage;   // stage index of each recorded interval start
   std::vector<int> ev_group;   // stream group of each mark
+  // side-stream kernel intervals (k_propagate): (stage, start, end) on the aux stream
+  std::vector<int> side_stage;
+  std::vector<cudaEvent_t> side_ev;
   int cur_group = 0;
   // stream groups: independent stream ranges launched on their own CUDA streams
   int n_groups_max = 0;
@@ -300,12 +303,18 @@ static void pack_free(vf_ctx* c)
 }
 
 #define VF_NSTAGES 9   // binmask, pyramid, worklist, fast, nms, sat, describe, propagate, finalize
-static void stage_mark(vf_ctx* c, int stage, cudaStream_t st)
+static cudaEvent_t pool_event(vf_ctx* c)
 {
-  if (!c->timing) return;
   cudaEvent_t e;
   if (c->ev_pool.empty()) cudaEventCreate(&e);
   else { e = c->ev_pool.back(); c->ev_pool.pop_back(); }
+  return e;
+}
+
+static void stage_mark(vf_ctx* c, int stage, cudaStream_t st)
+{
+  if (!c->timing) return;
+  cudaEvent_t e = pool_event(c);
   cudaEventRecord(e, st);
   c->ev_used.push_back(e);
   c->ev_stage.push_back(stage);
@@ -509,6 +518,7 @@ int vf_destroy(vf_ctx* c)
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   for (cudaEvent_t ev : c->ev_used) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->side_ev) cudaEventDestroy(ev);
   c->mem.release();
   delete c;
   return VF_OK;
@@ -557,8 +567,17 @@ int vf_get_stage_ms(vf_ctx* c, double* ms7, int* n_steps, void* stream)  /* ms7:
     if (std::find(groups_seen.begin(), groups_seen.end(), c->ev_group[i]) == groups_seen.end())
       groups_seen.push_back(c->ev_group[i]);
   }
+  // side-stream kernels: their own duration (they overlap the main stream)
+  for (size_t i = 0; i + 1 < c->side_ev.size(); i += 2) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->side_ev[i], c->side_ev[i + 1]);
+    ms7[c->side_stage[i / 2]] += ms;
+  }
   if (groups_seen.size() > 1)
     for (int k = 0; k < VF_NSTAGES; k++) ms7[k] /= (double)groups_seen.size();
+  for (cudaEvent_t ev : c->side_ev) c->ev_pool.push_back(ev);
+  c->side_ev.clear();
+  c->side_stage.clear();
   for (cudaEvent_t ev : c->ev_used) c->ev_pool.push_back(ev);
   c->ev_used.clear();
   c->ev_stage.clear();
@@ -617,7 +636,21 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   cudaEventRecord(c->aux_mid[gi], c->aux[gi]);
   // Eq. 1 propagation into the last n_prop slots of the list: independent of
   // the detection, so it runs beside k_fast / k_nms
-  if (prop) k_propagate<<<dim3(PROP_CTAS, n), 256, 0, c->aux[gi]>>>(g, b);
+  if (prop) {
+    cudaEvent_t p0 = nullptr, p1 = nullptr;
+    if (c->timing) {
+      p0 = pool_event(c);
+      p1 = pool_event(c);
+      cudaEventRecord(p0, c->aux[gi]);
+    }
+    k_propagate<<<dim3(PROP_CTAS, n), 256, 0, c->aux[gi]>>>(g, b);
+    if (c->timing) {
+      cudaEventRecord(p1, c->aux[gi]);
+      c->side_ev.push_back(p0);
+      c->side_ev.push_back(p1);
+      c->side_stage.push_back(7);
+    }
+  }
   cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
@@ -631,9 +664,10 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0);
   k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
   k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
-  stage_mark(c, 7, st);
-  cudaStreamWaitEvent(st, c->aux_out[gi], 0);
+  // k_propagate (stage 7) is timed on the side stream; the join wait counts
+  // toward the finalize stage
   stage_mark(c, 8, st);
+  cudaStreamWaitEvent(st, c->aux_out[gi], 0);
   k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
   stage_mark(c, -1, st);
   for (int s = s0; s < s0 + n; s++) c->frames_done[s]++;
