@@ -21,6 +21,7 @@ Python package that cannot travel to the GPU box), rank 0 only.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -310,6 +311,7 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------------------
 POPC_PEAK_PER_CLK_SM = 15.6   # measured, tools/micro/popc_bench.cu (profiles/r01_popc_peak.txt)
 IMMA_PEAK_TOPS = 1112.0       # measured mma.sync m16n8k32 u8, tools/micro/imma_bench.cu (same file)
+TC_I8_PEAK_TOPS = 4579.0      # measured tcgen05.mma.kind::i8 M=128 N>=128: 8192 MAC/clk/SM, tools/micro/tc_i8_peak.cu
 T_M = 102
 
 
@@ -419,6 +421,11 @@ def run_match(args, rank, world, local):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    from paper_1503_06959_b200 import _native
+
+    L = _native.lib()
+    kern_ms = ctypes.c_double(0.0)
+    _native.check(L.vf_match_timing(1, None))
     ms = 0.0
     with ClockSampler(local) as clk:
         time.sleep(1.0)
@@ -434,28 +441,18 @@ def run_match(args, rank, world, local):
             ms += e0.elapsed_time(e1)
         tw1 = time.time()
     clk.window(tw0, tw1)
+    _native.check(L.vf_match_timing(0, ctypes.byref(kern_ms)))
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0])
     pps = n_pairs_step * world * args.steps / (ms_max / 1e3)
-    # kernel-only time of the distance kernel (hamming_matrix over the same pairs)
-    from paper_1503_06959_b200.matching import hamming_matrix_device
-
-    for a, b in pairs[:1]:
-        hamming_matrix_device(a, b)
-    torch.cuda.synchronize()
-    k0 = torch.cuda.Event(enable_timing=True)
-    k1 = torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    for a, b in pairs:
-        hamming_matrix_device(a, b)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    kms = k0.elapsed_time(k1)
+    # distance kernel of the timed radius matches (operand images + k_radius_tc,
+    # CUDA events on the call's stream inside vf_radius_match)
+    kms = kern_ms.value / args.steps
     # tensor-core path: q.r of 512 0/1 bytes per pair (2 x 512 int8 ops per pair)
     ops = 2.0 * 512 * n_pairs_step
-    peak = IMMA_PEAK_TOPS
+    peak = TC_I8_PEAK_TOPS
     ach = ops / (kms / 1e3) / 1e12
     # e2e: host packed descriptors (pinned) -> H2D -> radius match -> D2H of the matches
     host = [(a.cpu().pin_memory(), b.cpu().pin_memory()) for a, b in pairs]
@@ -477,9 +474,12 @@ def run_match(args, rank, world, local):
                 "data": "synthetic", "config": dict(cfg, l2="256 MB buffer written between timed steps (outside "
                                                          "the events)", matches_per_step=n_match * world),
                 "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)",
-                             "frac": ach / peak, "traffic": None, "kernel": "k_hamming_mma (IMMA u8, same pairs, "
-                             "live CUDA events)", "peak_source": "measured mma.sync m16n8k32 u8 rate, "
-                             "tools/micro/imma_bench.cu", "kernel_ms_per_step": kms},
+                             "frac": ach / peak, "traffic": None,
+                             "kernel": "k_tc_images + k_radius_tc (tcgen05.mma.kind::i8, TMEM accumulators; live CUDA "
+                                       "events around the distance kernel of every timed radius match)",
+                             "peak_source": "measured tcgen05.mma.kind::i8 M=128 N=128 issue rate, 8192 MAC/clk/SM "
+                                            "(tools/micro/tc_i8_peak.cu, profiles/r01e_tc_i8_peak.txt)",
+                             "kernel_ms_per_step": kms},
                 "e2e": {"value": n_pairs_step / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "api": "pinned packed descriptors -> radius_match_device -> "
                                                           "matches to host"},

@@ -224,6 +224,10 @@ int vf_hamming_matrix(const uint8_t *q_dev, int64_t nq, const uint8_t *r_dev, in
 int vf_radius_match(const uint8_t *q_dev, int64_t nq, const uint8_t *r_dev, int64_t nr, int nbytes, int t_m,
                     int32_t *q_idx_dev, int32_t *r_idx_dev, int32_t *dist_dev, int64_t cap,
                     int64_t *n_matches, void *stream);
+/* Device time of the distance kernel of vf_radius_match (CUDA events around
+ * it on the call's stream), for benchmarks.  enable = 1: reset and start
+ * accumulating; enable = 0: stop; *ms (if non-null) = the accumulated time. */
+int vf_match_timing(int enable, double *ms);
 
 /* --- geometric verification (matching.py:97-220) ---- */
 /* ransac_homography (matching.py:151-192) for n_problems match sets at once.

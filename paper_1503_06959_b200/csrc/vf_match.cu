@@ -16,6 +16,8 @@
 // radius_match appends (q << 32 | r, d) for d <= t_m with warp-aggregated
 // atomics, then one device radix sort on the 64-bit key gives np.nonzero's
 // (query, reference) order.
+#include <climits>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
@@ -369,6 +371,10 @@ __device__ __forceinline__ void tc_expand(const TcRows<R>& t, uint32_t sm, int* 
 }
 static_assert((TC_M * 4) % TC_THREADS == 0 && (TC_N * 4) % TC_THREADS == 0, "whole (row, K block) items per thread");
 
+// Wait for the phase of parity `phase` of an mbarrier.  SLEEP: back off
+// between polls (waiting warps leave their scheduler's issue slots to the
+// single-thread producer lanes).
+template <bool SLEEP = false>
 __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase, unsigned* err)
 {
   uint32_t done = 0;
@@ -377,9 +383,12 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase, unsigned*
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
                  : "=r"(done)
                  : "r"(mbar), "r"(phase));
-    if (!done && ++spins > (1ll << 28)) {   // never expected: report instead of hanging the GPU
-      atomicOr(err, 1u);
-      return;
+    if (!done) {
+      if (SLEEP) __nanosleep(64);
+      if (++spins > (1ll << 28)) {   // never expected: report instead of hanging the GPU
+        atomicOr(err, 1u);
+        return;
+      }
     }
   }
 }
@@ -517,6 +526,361 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_hamming_tc(const uint8_t* q, 
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_N));
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined tcgen05 radius match (512-bit rows).  The packed rows of both
+// sides are first expanded ONCE (k_tc_images) into per-128-row tile images:
+// the exact shared-memory image the UMMA descriptors expect (K-major,
+// SWIZZLE_128B: K block kb = [128 rows][128 B], 16-B chunk c of row r at
+// c ^ (r & 7)), 64 KB per 128 rows, plus per-row popcounts.  k_radius_tc
+// then runs a warp-specialised pipeline, one persistent CTA per SM owning a
+// contiguous range of the (256-query, 128-reference) tile grid:
+//   * load lane: streams reference K blocks (16 KB each, 1-D bulk TMA,
+//     mbarrier complete_tx) through a ring of RT_STAGES stages;
+//   * MMA lane: keeps the 256-row query block A (128 KB) resident (reloaded
+//     when the range moves to the next query block) and issues, per K block,
+//     2 x 4 tcgen05.mma.kind::i8 (M = N = 128, K = 32) into two 128 x 128 s32
+//     TMEM accumulators; each K block's commit frees its stage, each tile's
+//     commit publishes the accumulator pair (double-buffered: 512 columns);
+//   * 16 epilogue warps: tcgen05.ld, a max-of-(2 v - |r|) test per 32
+//     columns (matches are sparse), exact hits buffered per warp in shared
+//     memory and flushed with one reservation per batch.
+// Reusing each reference block for 256 query rows halves the L2 -> SM traffic
+// of the expanded operands relative to a 128-row block.
+// ---------------------------------------------------------------------------
+#define RT_ROWS 128
+#define RT_IMG (RT_ROWS * 512)            // bytes per 128-row tile image
+#define RT_KBLK (RT_ROWS * 128)           // bytes per K block of a tile image (one ring stage)
+#define RT_STAGES 5
+#define RT_EPI 16                         // epilogue warps
+#define RT_THREADS (32 * RT_EPI + 64)     // + load warp + MMA warp
+#define RT_SMEM (2 * RT_IMG + RT_STAGES * RT_KBLK + 1024)
+#define RT_MBUF 32                        // matches buffered per epilogue warp
+
+constexpr uint32_t RT_IDESC = (2u << 4) | ((uint32_t)(RT_ROWS >> 3) << 17) | ((uint32_t)(RT_ROWS >> 4) << 24);
+
+// rows [0, n) of 64-byte packed rows -> tile images (rows past n are zero)
+// and popcounts; item = (row, K block), 16 packed bytes -> 128 expanded bytes
+__global__ void k_tc_images(const uint8_t* src, long long n, long long n_pad, uint8_t* img, int* pc)
+{
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad * 4; i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i >> 2;
+    const int kb = (int)(i & 3);
+    const uint4 v = row < n ? __ldg(reinterpret_cast<const uint4*>(src + row * 64) + kb) : make_uint4(0, 0, 0, 0);
+    const int r = (int)(row & (RT_ROWS - 1));
+    uint8_t* dst = img + (row / RT_ROWS) * RT_IMG + kb * (RT_ROWS * 128) + r * 128;
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      const uint32_t x = w[c >> 1] >> (16 * (c & 1));
+      uint4 o;
+      o.x = ((x & 0xfu) * 0x00204081u) & 0x01010101u;
+      o.y = (((x >> 4) & 0xfu) * 0x00204081u) & 0x01010101u;
+      o.z = (((x >> 8) & 0xfu) * 0x00204081u) & 0x01010101u;
+      o.w = (((x >> 12) & 0xfu) * 0x00204081u) & 0x01010101u;
+      *reinterpret_cast<uint4*>(dst + ((c ^ (r & 7)) << 4)) = o;
+    }
+    int cnt = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
+    if (kb == 0) pc[row] = cnt;
+  }
+}
+
+__device__ __forceinline__ void rt_expect_load(uint32_t mbar, uint32_t sdst, const void* gsrc, uint32_t bytes)
+{
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sdst),
+               "l"(gsrc), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(RT_THREADS, 1) k_radius_tc(const uint8_t* qimg, const int* qpc, long long nq,
+                                                             const uint8_t* rimg, const int* rpc, long long nr,
+                                                             int t_m, unsigned long long* keys, int32_t* dist,
+                                                             long long cap, unsigned long long* count, unsigned* err)
+{
+  extern __shared__ uint8_t rt_dsm[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rt_dsm) + 1023) & ~(uintptr_t)1023);
+  uint8_t* sR = sA + 2 * RT_IMG;   // ring of RT_STAGES K blocks
+  __shared__ __align__(8) uint64_t mb_full[RT_STAGES], mb_empty[RT_STAGES], mb_mma[2], mb_free[2], mb_a;
+  __shared__ uint32_t tslot;
+  __shared__ __align__(16) uint32_t prs[RT_EPI][32];            // per epilogue warp: column popcount pairs
+  __shared__ unsigned long long mkey[RT_EPI][RT_MBUF];          // per epilogue warp: buffered matches
+  __shared__ int mdist[RT_EPI][RT_MBUF];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long qt = (nq + 2 * RT_ROWS - 1) / (2 * RT_ROWS), rt = (nr + RT_ROWS - 1) / RT_ROWS;
+  const long long T = qt * rt;
+  const long long j0 = T * blockIdx.x / gridDim.x, j1 = T * (blockIdx.x + 1) / gridDim.x;
+  if (j0 >= j1) return;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_u32(&tslot)),
+                 "r"(4 * RT_ROWS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const uint32_t full0 = tc_smem_u32(&mb_full[0]), empty0 = tc_smem_u32(&mb_empty[0]);
+  const uint32_t mma0 = tc_smem_u32(&mb_mma[0]), free0 = tc_smem_u32(&mb_free[0]), mba = tc_smem_u32(&mb_a);
+  if (tid == 0) {
+    for (int k = 0; k < RT_STAGES; k++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8 * k));
+    }
+    for (int k = 0; k < 2; k++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mma0 + 8 * k));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(free0 + 8 * k), "r"(RT_EPI));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mba));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tslot;
+  const uint32_t sa = tc_smem_u32(sA), sr = tc_smem_u32(sR);
+  const long long n_loads = (j1 - j0) * 4;   // K blocks of the range, in order
+  if (warp == RT_EPI) {
+    // ---- load lane: reference K blocks through the ring ----
+    if (lane == 0) {
+      long long rtile = j0 % rt;
+      int kb = 0;
+#pragma unroll 1
+      for (long long i = 0; i < n_loads; i++) {
+        const int st = (int)(i % RT_STAGES);
+        const long long use = i / RT_STAGES;
+        if (use > 0) tc_wait(empty0 + 8 * st, (uint32_t)((use - 1) & 1), err);   // freed by the MMAs of load i - S
+        rt_expect_load(full0 + 8 * st, sr + st * RT_KBLK, rimg + rtile * RT_IMG + kb * RT_KBLK, RT_KBLK);
+        if (++kb == 4) {
+          kb = 0;
+          if (++rtile == rt) rtile = 0;
+        }
+      }
+    }
+  } else if (warp == RT_EPI + 1) {
+    // ---- MMA lane ----
+    if (lane == 0) {
+      uint32_t a_phase = 0;
+      long long a_tile = -1;
+      const uint64_t dA0 = tc_sdesc(sa), dR0 = tc_sdesc(sr);
+#ifdef RT_PROBE
+      unsigned long long probe_full = 0, probe_free = 0, probe_start = clock64();
+#endif
+#pragma unroll 1
+      for (long long j = j0; j < j1; j++) {
+        const long long jj = j - j0;
+        const int buf = (int)(jj & 1);
+        const long long qtile = j / rt;
+        if (qtile != a_tile) {
+          // A is read by the MMAs of tile j - 1: wait for them before reloading
+          if (jj > 0) tc_wait(mma0 + 8 * (buf ^ 1), (uint32_t)(((jj - 1) >> 1) & 1), err);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mba), "r"(2 * RT_IMG) : "memory");
+          for (int m = 0; m < 2; m++)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             sa + m * RT_IMG),
+                         "l"(qimg + (2 * qtile + m) * RT_IMG), "r"(RT_IMG), "r"(mba)
+                         : "memory");
+          tc_wait(mba, a_phase, err);
+          a_phase ^= 1u;
+          a_tile = qtile;
+        }
+#ifdef RT_PROBE
+        unsigned long long pt0 = clock64();
+#endif
+        if (jj >= 2) tc_wait(free0 + 8 * buf, (uint32_t)(((jj - 2) >> 1) & 1), err);   // accumulators read
+#ifdef RT_PROBE
+        probe_free += clock64() - pt0;
+#endif
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc0 = tmem + (uint32_t)(2 * buf * RT_ROWS);
+#pragma unroll
+        for (int kb = 0; kb < 4; kb++) {
+          const long long i = 4 * jj + kb;
+          const int st = (int)(i % RT_STAGES);
+#ifdef RT_PROBE
+          unsigned long long pt1 = clock64();
+#endif
+          tc_wait(full0 + 8 * st, (uint32_t)((i / RT_STAGES) & 1), err);
+#ifdef RT_PROBE
+          probe_full += clock64() - pt1;
+#endif
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          // descriptors: the start-address field is addr >> 4 (< 2^14), so
+          // offsets add to the base descriptor directly
+          const uint64_t db = dR0 + (uint64_t)((st * RT_KBLK) >> 4);
+#pragma unroll
+          for (int m = 0; m < 2; m++)
+#pragma unroll
+            for (int sub = 0; sub < 4; sub++) {
+              const uint64_t da = dA0 + (uint64_t)((m * RT_IMG + kb * RT_KBLK + sub * 32) >> 4);
+              asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                           " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(acc0 + m * RT_ROWS),
+                           "l"(da), "l"(db + (uint64_t)(sub * 2)), "r"(RT_IDESC), "r"((uint32_t)(kb | sub)));
+            }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma0 + 8 * buf));
+      }
+#ifdef RT_PROBE
+      if (blockIdx.x < 4)
+        printf("cta %d tiles %lld: total %llu clk, wait full %llu, wait free %llu\n", blockIdx.x, j1 - j0,
+               clock64() - probe_start, probe_full, probe_free);
+#endif
+    }
+  } else {
+    // ---- epilogue warps: warp w reads TMEM lanes 32 (w & 3) .. of sub-tile
+    // m = w >> 3 (query rows 128 m + ..), accumulator columns 64 ((w >> 2) & 1)
+    // .. + 64 in two 32-column chunks ----
+    const int m = warp >> 3, erow = 128 * m + 32 * (warp & 3) + lane, ecol = 64 * ((warp >> 2) & 1);
+    uint32_t* pw = prs[warp];
+    unsigned long long* bk = mkey[warp];
+    int* bd = mdist[warp];
+    int nb = 0;   // matches buffered by this warp (warp-uniform)
+    auto flush = [&]() {
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(count, (unsigned long long)nb);
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      for (int i = lane; i < nb; i += 32)
+        if ((long long)(pos + i) < cap) {
+          keys[pos + i] = bk[i];
+          dist[pos + i] = bd[i];
+        }
+      __syncwarp();
+      nb = 0;
+    };
+    long long qtile = j0 / rt, rtile = j0 - qtile * rt;
+    auto col_pc = [&](long long c) { return c < nr ? __ldg(rpc + c) : 0x7ff; };   // past nr: never passes the fast test
+    int prA = col_pc(rtile * RT_ROWS + ecol + lane), prB = col_pc(rtile * RT_ROWS + ecol + 32 + lane);
+    long long qi = -1;
+    int pa = 0, lim = INT_MAX;
+#pragma unroll 1
+    for (long long j = j0; j < j1; j++) {
+      const long long jj = j - j0;
+      const int buf = (int)(jj & 1);
+      if (qtile * 2 * RT_ROWS + erow != qi) {   // the query rows change with the query block only
+        qi = qtile * 2 * RT_ROWS + erow;
+        pa = qi < nq ? __ldg(qpc + qi) : 0;
+        lim = qi < nq ? pa - t_m : INT_MAX;   // hit iff pa + pr - 2 v <= t_m iff 2 v - pr >= pa - t_m
+      }
+      const long long rc0 = rtile * RT_ROWS + ecol;
+      // column popcounts of the two chunks as 16x2 pairs (col k | col 32 + k)
+      pw[lane] = (uint32_t)prA | ((uint32_t)prB << 16);
+      __syncwarp();
+      const long long qtile_n = rtile + 1 == rt ? qtile + 1 : qtile, rtile_n = rtile + 1 == rt ? 0 : rtile + 1;
+      tc_wait<true>(mma0 + 8 * buf, (uint32_t)((jj >> 1) & 1), err);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // both 32-column chunks into registers as 16x2 pairs (q.r <= 512), then
+      // the accumulator pair is released: the MMAs of tile j + 2 overlap this
+      // tile's tests
+      uint32_t w[32];
+      {
+        uint32_t t[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((2 * buf + m) * RT_ROWS + ecol);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                   "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                     "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
+                     "=r"(w[15]), "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]),
+                     "=r"(w[22]), "=r"(w[23]), "=r"(w[24]), "=r"(w[25]), "=r"(w[26]), "=r"(w[27]), "=r"(w[28]),
+                     "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+                   : "r"(ta));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                   "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]), "=r"(t[7]),
+                     "=r"(t[8]), "=r"(t[9]), "=r"(t[10]), "=r"(t[11]), "=r"(t[12]), "=r"(t[13]), "=r"(t[14]),
+                     "=r"(t[15]), "=r"(t[16]), "=r"(t[17]), "=r"(t[18]), "=r"(t[19]), "=r"(t[20]), "=r"(t[21]),
+                     "=r"(t[22]), "=r"(t[23]), "=r"(t[24]), "=r"(t[25]), "=r"(t[26]), "=r"(t[27]), "=r"(t[28]),
+                     "=r"(t[29]), "=r"(t[30]), "=r"(t[31])
+                   : "r"(ta + 32));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int k = 0; k < 32; k++) w[k] |= t[k] << 16;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(free0 + 8 * buf) : "memory");
+      if (j + 1 < j1) {   // next tile's column popcounts, in flight during the tests
+        prA = col_pc(rtile_n * RT_ROWS + ecol + lane);
+        prB = col_pc(rtile_n * RT_ROWS + ecol + 32 + lane);
+      }
+      // fast test: max over the 64 columns of 2 q.r - |r| (matches are sparse)
+      const uint4* p4 = reinterpret_cast<const uint4*>(pw);
+      uint32_t mx = 0x80008000u;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        const uint4 p = p4[k >> 2];
+        mx = __vimax3_s16x2(mx, __vsub2(__vadd2(w[k], w[k]), p.x), __vsub2(__vadd2(w[k + 1], w[k + 1]), p.y));
+        mx = __vimax3_s16x2(mx, __vsub2(__vadd2(w[k + 2], w[k + 2]), p.z), __vsub2(__vadd2(w[k + 3], w[k + 3]), p.w));
+      }
+      const unsigned cand = (__ballot_sync(0xffffffffu, (int)(short)(mx & 0xffffu) >= lim) ? 1u : 0u) |
+                            (__ballot_sync(0xffffffffu, (int)(short)(mx >> 16) >= lim) ? 2u : 0u);
+      if (cand) {
+#pragma unroll 1
+        for (int c = 0; c < 2; c++) {
+          if (!((cand >> c) & 1u)) continue;
+          const int c0 = 32 * c, sh = 16 * c;
+          const long long left = nr - (rc0 + c0);   // columns of the chunk inside the reference set
+          const uint32_t valid = left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : (1u << left) - 1u);
+          uint32_t hits = 0;
+          const uint4* q4 = reinterpret_cast<const uint4*>(pw);
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const uint4 p = q4[k >> 2];
+            hits |= (uint32_t)(2 * (int)((w[k] >> sh) & 0xffffu) - (int)((p.x >> sh) & 0xffffu) >= lim) << k;
+            hits |= (uint32_t)(2 * (int)((w[k + 1] >> sh) & 0xffffu) - (int)((p.y >> sh) & 0xffffu) >= lim) << (k + 1);
+            hits |= (uint32_t)(2 * (int)((w[k + 2] >> sh) & 0xffffu) - (int)((p.z >> sh) & 0xffffu) >= lim) << (k + 2);
+            hits |= (uint32_t)(2 * (int)((w[k + 3] >> sh) & 0xffffu) - (int)((p.w >> sh) & 0xffffu) >= lim) << (k + 3);
+          }
+          hits &= valid;
+          if (!__any_sync(0xffffffffu, hits != 0)) continue;
+          // buffer the chunk's matches (order is restored by the sort)
+          const int nh = __popc(hits);
+          int off = nh;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, off, o);
+            if (lane >= o) off += y;
+          }
+          const int tot = __shfl_sync(0xffffffffu, off, 31);
+          off -= nh;
+          if (nb + tot > RT_MBUF) flush();
+          unsigned long long* kd = bk;
+          int* dd = bd;
+          long long pos = nb + off;
+          if (tot > RT_MBUF) {   // more matches in one chunk than the buffer holds: direct
+            unsigned long long p0 = 0;
+            if (lane == 0) p0 = atomicAdd(count, (unsigned long long)tot);
+            pos = (long long)__shfl_sync(0xffffffffu, p0, 0) + off;
+            kd = keys;
+            dd = dist;
+          }
+          for (uint32_t h = hits; h; h &= h - 1) {
+            const int k = __ffs(h) - 1;
+            uint32_t wk = 0;   // w[k] without dynamic register indexing
+#pragma unroll
+            for (int kk = 0; kk < 32; kk++) wk = kk == k ? w[kk] : wk;
+            const int vk = (int)((wk >> sh) & 0xffffu), pk = (int)((pw[k] >> sh) & 0xffffu);
+            if (tot <= RT_MBUF || pos < cap) {
+              kd[pos] = ((unsigned long long)qi << 32) | (unsigned long long)(rc0 + c0 + k);
+              dd[pos] = pa + pk - 2 * vk;
+            }
+            pos++;
+          }
+          __syncwarp();
+          if (tot <= RT_MBUF) nb += tot;
+        }
+      }
+      __syncwarp();   // pw is rewritten for the next tile
+      qtile = qtile_n;
+      rtile = rtile_n;
+    }
+    if (nb) flush();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * RT_ROWS));
+  }
+}
+
 __global__ void k_split_keys(const unsigned long long* keys, long long n, int32_t* qi, int32_t* ri)
 {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -561,6 +925,69 @@ dim3 tc_grid(long long nq, long long nr)
   return dim3((unsigned)gx, (unsigned)qt);
 }
 
+// Stream-ordered scratch from a private pool that keeps its memory (release
+// threshold = max): repeated calls reuse it instead of remapping pages at
+// every synchronisation.
+cudaMemPool_t mt_pool()
+{
+  static cudaMemPool_t pool = [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &pp) != cudaSuccess) return (cudaMemPool_t) nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    return p;
+  }();
+  return pool;
+}
+
+template <typename T>
+cudaError_t mt_alloc(T** p, size_t bytes, cudaStream_t st)
+{
+  cudaMemPool_t pool = mt_pool();
+  if (!pool) return cudaErrorMemoryAllocation;
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, st);
+}
+
+// tile images of both sides, then the pipelined tensor-core radius kernel
+cudaError_t radius_tc(const uint8_t* q, long long nq, const uint8_t* r, long long nr, int t_m, unsigned long long* keys,
+                      int32_t* dist, long long cap, unsigned long long* count, unsigned* err, cudaStream_t st)
+{
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_radius_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, RT_SMEM);
+  }
+  const long long qt = 2 * ((nq + 2 * RT_ROWS - 1) / (2 * RT_ROWS)), rt = (nr + RT_ROWS - 1) / RT_ROWS;   // qt: 128-row images, even
+  uint8_t *qi = nullptr, *ri = nullptr;
+  int *qp = nullptr, *rp = nullptr;
+  cudaError_t e = mt_alloc(&qi, qt * RT_IMG, st);
+  if (e == cudaSuccess) e = mt_alloc(&ri, rt * RT_IMG, st);
+  if (e == cudaSuccess) e = mt_alloc(&qp, qt * RT_ROWS * sizeof(int), st);
+  if (e == cudaSuccess) e = mt_alloc(&rp, rt * RT_ROWS * sizeof(int), st);
+  if (e == cudaSuccess) {
+    k_tc_images<<<(unsigned)std::min<long long>(4 * sms, (qt * RT_ROWS * 4 + 255) / 256), 256, 0, st>>>(
+        q, nq, qt * RT_ROWS, qi, qp);
+    k_tc_images<<<(unsigned)std::min<long long>(4 * sms, (rt * RT_ROWS * 4 + 255) / 256), 256, 0, st>>>(
+        r, nr, rt * RT_ROWS, ri, rp);
+    const long long grid = std::min<long long>(qt / 2 * rt, sms);
+    k_radius_tc<<<(unsigned)grid, RT_THREADS, RT_SMEM, st>>>(qi, qp, nq, ri, rp, nr, t_m, keys, dist, cap, count, err);
+    e = cudaGetLastError();
+  }
+  if (qi) cudaFreeAsync(qi, st);
+  if (ri) cudaFreeAsync(ri, st);
+  if (qp) cudaFreeAsync(qp, st);
+  if (rp) cudaFreeAsync(rp, st);
+  return e;
+}
+
 // mma.sync path: whole 32-bit words (<= 16 per row) and 4-byte aligned rows;
 // VF_MATCH_POPC=1 forces the POPC kernels (A/B comparison)
 bool use_mma(const void* q, const void* r, int nbytes)
@@ -591,6 +1018,28 @@ extern "C" int vf_hamming_matrix(const uint8_t* q_dev, int64_t nq, const uint8_t
   return match_status(cudaGetLastError());
 }
 
+// vf_match_timing state (benchmarks only)
+struct MatchTiming {
+  bool on = false;
+  double ms = 0.0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+MatchTiming g_mt;
+
+extern "C" int vf_match_timing(int enable, double* ms)
+{
+  if (enable) {
+    if (!g_mt.e0 && (cudaEventCreate(&g_mt.e0) != cudaSuccess || cudaEventCreate(&g_mt.e1) != cudaSuccess))
+      return VF_ERR_CUDA;
+    g_mt.ms = 0.0;
+    g_mt.on = true;
+  } else {
+    g_mt.on = false;
+  }
+  if (ms) *ms = g_mt.ms;
+  return VF_OK;
+}
+
 extern "C" int vf_radius_match(const uint8_t* q_dev, int64_t nq, const uint8_t* r_dev, int64_t nr, int nbytes,
                                int t_m, int32_t* q_idx_dev, int32_t* r_idx_dev, int32_t* dist_dev, int64_t cap,
                                int64_t* n_matches, void* stream)
@@ -606,16 +1055,16 @@ extern "C" int vf_radius_match(const uint8_t* q_dev, int64_t nq, const uint8_t* 
   const long long kcap = cap > 0 ? cap : 1;
   unsigned long long *keys = nullptr, *keys_sorted = nullptr, *count = nullptr;
   int32_t* dist_tmp = nullptr;
-  cudaError_t e = cudaMallocAsync(&keys, kcap * sizeof(unsigned long long), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&keys_sorted, kcap * sizeof(unsigned long long), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dist_tmp, kcap * sizeof(int32_t), st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&count, 2 * sizeof(unsigned long long), st);
+  cudaError_t e = mt_alloc(&keys, kcap * sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = mt_alloc(&keys_sorted, kcap * sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = mt_alloc(&dist_tmp, kcap * sizeof(int32_t), st);
+  if (e == cudaSuccess) e = mt_alloc(&count, 2 * sizeof(unsigned long long), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(count, 0, 2 * sizeof(unsigned long long), st);
   unsigned* err = reinterpret_cast<unsigned*>(count + 1);
   if (e == cudaSuccess) {
+    if (g_mt.on) cudaEventRecord(g_mt.e0, st);
     if (use_tc(q_dev, r_dev, nbytes))
-      k_hamming_tc<true><<<tc_grid(nq, nr), TC_THREADS, TC_SMEM, st>>>(q_dev, nq, r_dev, nr, nullptr, 0, t_m, keys,
-                                                                       dist_tmp, cap, count, err);
+      e = radius_tc(q_dev, nq, r_dev, nr, t_m, keys, dist_tmp, cap, count, err, st);
     else if (use_mma(q_dev, r_dev, nbytes))
       k_hamming_mma<true><<<grid, HM_THREADS, 0, st>>>(q_dev, nq, r_dev, nr, nbytes, nullptr, 0, t_m, keys, dist_tmp,
                                                        cap, count);
@@ -623,9 +1072,14 @@ extern "C" int vf_radius_match(const uint8_t* q_dev, int64_t nq, const uint8_t* 
       k_radius_match<<<grid, HM_THREADS, 0, st>>>(q_dev, nq, r_dev, nr, nbytes, t_m, keys, dist_tmp, cap, count);
     e = cudaGetLastError();
   }
+  if (g_mt.on) cudaEventRecord(g_mt.e1, st);
   unsigned long long n2[2] = {0, 0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(n2, count, sizeof(n2), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (g_mt.on && e == cudaSuccess) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, g_mt.e0, g_mt.e1) == cudaSuccess) g_mt.ms += ms;
+  }
   const unsigned long long n = n2[0];
   int rc = match_status(e);
   if (rc == VF_OK && (n2[1] & 0xffffffffull)) rc = VF_ERR_CUDA;   // a tensor-core wait timed out
@@ -641,7 +1095,7 @@ extern "C" int vf_radius_match(const uint8_t* q_dev, int64_t nq, const uint8_t* 
       cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_sorted, dist_tmp, dist_dev, (int64_t)n, 0,
                                       end_bit, st);
       void* tmp = nullptr;
-      e = cudaMallocAsync(&tmp, tmp_bytes, st);
+      e = mt_alloc(&tmp, tmp_bytes, st);
       if (e == cudaSuccess)
         e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_sorted, dist_tmp, dist_dev, (int64_t)n, 0,
                                             end_bit, st);

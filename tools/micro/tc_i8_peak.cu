@@ -1,0 +1,90 @@
+// tc_i8_peak.cu -- tcgen05.mma.kind::i8 issue-rate microbenchmark: one CTA per
+// SM, one thread issuing back-to-back M x N x 32 MMAs from shared memory into
+// TMEM (no loads), for N = 64 / 128 / 256.  Prints MAC/clk/SM and POPS.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tc_i8_peak.cu -o tc_i8_peak
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t a)
+{
+  return (uint64_t)((a >> 4) & 0x3fff) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) |
+         ((uint64_t)2 << 61);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128, 1) k_peak(int iters, unsigned long long* clk)
+{
+  extern __shared__ uint8_t dsm[];
+  uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t mb;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < (128 + N) * 128 / 4; i += 128) reinterpret_cast<uint32_t*>(s)[i] = 0x01010101u;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(N < 32 ? 32 : N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mb)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = slot;
+  const uint32_t idesc = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  if (threadIdx.x == 0) {
+    const uint64_t da = sdesc(smem_u32(s)), db = sdesc(smem_u32(s + 128 * 128));
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+      asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+                   "l"(da + 2 * (i & 3)), "l"(db + 2 * (i & 3)), "r"(idesc), "r"(i));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mb)));
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+                   : "=r"(done) : "r"(smem_u32(&mb)));
+    unsigned long long t1 = clock64();
+    if (blockIdx.x == 0) *clk = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(N < 32 ? 32 : N));
+}
+
+template <int N>
+void run(int sms)
+{
+  const int iters = 200000, smem = (128 + N) * 128 + 1024;
+  cudaFuncSetAttribute(k_peak<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  unsigned long long* clk;
+  cudaMalloc(&clk, 8);
+  k_peak<N><<<sms, 128, smem>>>(1000, clk);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k_peak<N><<<sms, 128, smem>>>(iters, clk);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  unsigned long long c = 0;
+  cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
+  const double macs = (double)iters * 128 * N * 32;
+  printf("M=128 N=%3d K=32 i8: %.3f ms, %.1f MAC/clk/SM (clock64), %.0f TOPS over %d SMs (%s)\n", N, ms, macs / c,
+         2.0 * macs * sms / (ms * 1e-3) / 1e12, sms, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main()
+{
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<64>(sms);
+  run<128>(sms);
+  run<256>(sms);
+  return 0;
+}
