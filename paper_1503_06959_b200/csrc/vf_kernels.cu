@@ -1074,28 +1074,9 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       inb |= (x >= 3 && x < w - 3) ? (0x80u << (8 * i)) : 0u;
     }
     int qn = 0;
-    for (int r = 0; r < VF_TILE_H; r++) {
-      const int y = y0 + r, k = lane;       // word k of row r: pixels x0 + 4k .. +3
-      uint32_t pass = 0;                    // bit 8i + 7: pixel i passes
-      if (y >= 3 && y < h - 3) {
-        const int cb = 16 + 4 * k;
-        const uint32_t C = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb]);
-        const uint32_t P = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb - 4]);
-        const uint32_t B = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb + 4]);
-        const uint32_t N = *reinterpret_cast<const uint32_t*>(&fw.tile[r][cb]);
-        const uint32_t S = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 6][cb]);
-        const uint32_t E = __byte_perm(C, B, 0x6543), Wd = __byte_perm(P, C, 0x4321);   // x + 3, x - 3
-        pass = (over(N, C) | over(S, C)) & (over(E, C) | over(Wd, C)) & inb;
-        if (pass && um) {
-          const uint8_t* crow = cells + (long long)fw.rc[r] * cols;
-          uint32_t gv[4];
-#pragma unroll
-          for (int i = 0; i < 4; i++) gv[i] = (pass >> (8 * i + 7)) & 1u ? crow[fw.cc[4 * k + i]] : 0u;
-          pass &= (gv[0] ? 0xffu : 0u) | (gv[1] ? 0xff00u : 0u) | (gv[2] ? 0xff0000u : 0u) | (gv[3] ? 0xff000000u : 0u);
-        }
-      }
-      // queue slots: exclusive prefix of the per-lane counts (0..4) from
-      // bit-plane ballots; only set pass bits are written
+    // queue slots: exclusive prefix of the per-lane counts (0..4) from
+    // bit-plane ballots; only set pass bits are written
+    auto enqueue = [&](uint32_t pass, int r, int k) {
       const int np = __popc(pass);
       const unsigned b0 = __ballot_sync(0xffffffffu, np & 1), b1 = __ballot_sync(0xffffffffu, np & 2),
                      b2 = __ballot_sync(0xffffffffu, np & 4);
@@ -1104,6 +1085,68 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       for (uint32_t pm = pass; pm; pm &= pm - 1u)
         fw.queue[pos++] = (uint16_t)(r * VF_TILE_W + 4 * k + ((__ffs(pm) - 1) >> 3));
       qn += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+    };
+    // the 4-point test of word k of row r (pixels x0 + 4k .. +3)
+    auto pretest = [&](int r, int k) {
+      const int cb = 16 + 4 * k;
+      const uint32_t C = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb]);
+      const uint32_t P = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb - 4]);
+      const uint32_t B = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 3][cb + 4]);
+      const uint32_t N = *reinterpret_cast<const uint32_t*>(&fw.tile[r][cb]);
+      const uint32_t S = *reinterpret_cast<const uint32_t*>(&fw.tile[r + 6][cb]);
+      const uint32_t E = __byte_perm(C, B, 0x6543), Wd = __byte_perm(P, C, 0x4321);   // x + 3, x - 3
+      return (over(N, C) | over(S, C)) & (over(E, C) | over(Wd, C));
+    };
+    if (!um) {
+      for (int r = 0; r < VF_TILE_H; r++) {
+        const int y = y0 + r;
+        const uint32_t pass = (y >= 3 && y < h - 3) ? pretest(r, lane) & inb : 0u;
+        enqueue(pass, r, lane);
+      }
+    } else {
+      // Gated tile: most words of an active tile lie in inactive cells
+      // (detector.py:112-114 scores them 0).  List the (row, word) items with
+      // an active in-bounds pixel -- lane k looks up the cells of its four
+      // pixels once per cell row -- and run the 4-point test on the list only,
+      // 32 items per round, with the per-pixel gate folded in.
+      uint16_t* items = reinterpret_cast<uint16_t*>(&fw.sc[0][0]);   // zeroed again below
+      uint32_t inb4 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; i++) inb4 |= ((inb >> (8 * i + 7)) & 1u) << i;
+      int n_items = 0, prev_rc = -1;
+      uint32_t g4 = 0;
+      for (int r = 0; r < VF_TILE_H; r++) {
+        const int y = y0 + r;
+        uint32_t gr = 0;
+        if (y >= 3 && y < h - 3 && inb4) {
+          if (fw.rc[r] != prev_rc) {
+            prev_rc = fw.rc[r];
+            const uint8_t* crow = cells + (long long)prev_rc * cols;
+            g4 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; i++) g4 |= (crow[fw.cc[4 * lane + i]] ? 1u : 0u) << i;
+          }
+          gr = g4 & inb4;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, gr != 0);
+        if (gr) items[n_items + __popc(m & ((1u << lane) - 1u))] = (uint16_t)((r << 12) | (lane << 4) | gr);
+        n_items += __popc(m);
+      }
+      __syncwarp();
+      for (int base = 0; base < n_items; base += 32) {
+        uint32_t pass = 0;
+        int r = 0, k = 0;
+        if (base + lane < n_items) {
+          const int it = items[base + lane];
+          r = it >> 12;
+          k = (it >> 4) & 31;
+          const uint32_t gate = ((((uint32_t)it & 15u) * 0x00204081u) & 0x01010101u) * 0x80u;
+          pass = pretest(r, k) & gate;
+        }
+        enqueue(pass, r, k);
+      }
+      __syncwarp();
+      for (int i = lane; i < (n_items + 7) / 8; i += 32) reinterpret_cast<uint4*>(items)[i] = make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
     // ---- pass 2: exact score of queued pixels ----
