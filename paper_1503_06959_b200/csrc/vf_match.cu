@@ -641,13 +641,13 @@ __global__ void __launch_bounds__(RT_THREADS, 1) k_radius_tc(const uint8_t* qimg
     // ---- load lane: reference K blocks through the ring ----
     if (lane == 0) {
       long long rtile = j0 % rt;
-      int kb = 0;
+      int kb = 0, st = 0;
+      uint32_t ph = 1;   // parity of the empty phase to wait for (none in the first pass over the ring)
 #pragma unroll 1
       for (long long i = 0; i < n_loads; i++) {
-        const int st = (int)(i % RT_STAGES);
-        const long long use = i / RT_STAGES;
-        if (use > 0) tc_wait(empty0 + 8 * st, (uint32_t)((use - 1) & 1), err);   // freed by the MMAs of load i - S
+        if (i >= RT_STAGES) tc_wait(empty0 + 8 * st, ph, err);   // freed by the MMAs of load i - S
         rt_expect_load(full0 + 8 * st, sr + st * RT_KBLK, rimg + rtile * RT_IMG + kb * RT_KBLK, RT_KBLK);
+        if (++st == RT_STAGES) { st = 0; ph ^= 1u; }
         if (++kb == 4) {
           kb = 0;
           if (++rtile == rt) rtile = 0;
@@ -661,13 +661,15 @@ __global__ void __launch_bounds__(RT_THREADS, 1) k_radius_tc(const uint8_t* qimg
       long long a_tile = -1;
       const uint64_t dA0 = tc_sdesc(sa), dR0 = tc_sdesc(sr);
 #ifdef RT_PROBE
-      unsigned long long probe_full = 0, probe_free = 0, probe_start = clock64();
+      unsigned long long probe_full = 0, probe_free = 0, probe_issue = 0, probe_a = 0, probe_start = clock64();
 #endif
+      long long qtile = j0 / rt, rtile = j0 - qtile * rt;
+      int st = 0;
+      uint32_t fph = 0;   // parity of the next full phase of stage st
 #pragma unroll 1
       for (long long j = j0; j < j1; j++) {
         const long long jj = j - j0;
         const int buf = (int)(jj & 1);
-        const long long qtile = j / rt;
         if (qtile != a_tile) {
           // A is read by the MMAs of tile j - 1: wait for them before reloading
           if (jj > 0) tc_wait(mma0 + 8 * (buf ^ 1), (uint32_t)(((jj - 1) >> 1) & 1), err);
@@ -692,14 +694,13 @@ __global__ void __launch_bounds__(RT_THREADS, 1) k_radius_tc(const uint8_t* qimg
         const uint32_t acc0 = tmem + (uint32_t)(2 * buf * RT_ROWS);
 #pragma unroll
         for (int kb = 0; kb < 4; kb++) {
-          const long long i = 4 * jj + kb;
-          const int st = (int)(i % RT_STAGES);
 #ifdef RT_PROBE
           unsigned long long pt1 = clock64();
 #endif
-          tc_wait(full0 + 8 * st, (uint32_t)((i / RT_STAGES) & 1), err);
+          tc_wait(full0 + 8 * st, fph, err);
 #ifdef RT_PROBE
-          probe_full += clock64() - pt1;
+          unsigned long long pt2 = clock64();
+          probe_full += pt2 - pt1;
 #endif
           asm volatile("tcgen05.fence::after_thread_sync;");
           // descriptors: the start-address field is addr >> 4 (< 2^14), so
@@ -715,13 +716,18 @@ __global__ void __launch_bounds__(RT_THREADS, 1) k_radius_tc(const uint8_t* qimg
                            "l"(da), "l"(db + (uint64_t)(sub * 2)), "r"(RT_IDESC), "r"((uint32_t)(kb | sub)));
             }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st));
+#ifdef RT_PROBE
+          probe_issue += clock64() - pt2;
+#endif
+          if (++st == RT_STAGES) { st = 0; fph ^= 1u; }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mma0 + 8 * buf));
+        if (++rtile == rt) { rtile = 0; qtile++; }
       }
 #ifdef RT_PROBE
       if (blockIdx.x < 4)
-        printf("cta %d tiles %lld: total %llu clk, wait full %llu, wait free %llu\n", blockIdx.x, j1 - j0,
-               clock64() - probe_start, probe_full, probe_free);
+        printf("cta %d tiles %lld: total %llu clk, wait full %llu, wait free %llu, issue %llu\n", blockIdx.x, j1 - j0,
+               clock64() - probe_start, probe_full, probe_free, probe_issue);
 #endif
     }
   } else {
@@ -764,7 +770,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1) k_radius_tc(const uint8_t* qimg
       pw[lane] = (uint32_t)prA | ((uint32_t)prB << 16);
       __syncwarp();
       const long long qtile_n = rtile + 1 == rt ? qtile + 1 : qtile, rtile_n = rtile + 1 == rt ? 0 : rtile + 1;
-      tc_wait<true>(mma0 + 8 * buf, (uint32_t)((jj >> 1) & 1), err);
+      tc_wait(mma0 + 8 * buf, (uint32_t)((jj >> 1) & 1), err);
       asm volatile("tcgen05.fence::after_thread_sync;");
       // both 32-column chunks into registers as 16x2 pairs (q.r <= 512), then
       // the accumulator pair is released: the MMAs of tile j + 2 overlap this
