@@ -573,22 +573,32 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     // i0: 16 row pairs x 16 words, one 2x4 block per thread
     const int p = tid >> 4, q = tid & 15;
     const int base = 6 * q, al = base & ~3, sh = 8 * (base & 3);
-    uint32_t hs[3][4];
+    // row r's six input bytes c0..c5 as L = (c0, c1, c2, c3), M = (c3, c4, c5, -)
+    uint32_t L[3], M[3];
 #pragma unroll
     for (int r = 0; r < 3; r++) {
-      const uint8_t* row = t0 + (3 * p + r) * TW + al;
-      const unsigned long long lo =
-          (((unsigned long long)*reinterpret_cast<const uint32_t*>(row + 4) << 32) | *reinterpret_cast<const uint32_t*>(row)) >> sh;
-      const uint32_t c0 = lo & 0xff, c1 = (lo >> 8) & 0xff, c2 = (lo >> 16) & 0xff, c3 = (lo >> 24) & 0xff;
-      const uint32_t c4 = (lo >> 32) & 0xff, c5 = (lo >> 40) & 0xff;
-      hs[r][0] = 2 * c0 + c1; hs[r][1] = c1 + 2 * c2; hs[r][2] = 2 * c3 + c4; hs[r][3] = c4 + 2 * c5;
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(t0 + (3 * p + r) * TW + al);
+      const uint32_t w0 = row[0], w1 = row[1];   // the group starts at byte 0 or 2 of w0 (6q mod 4)
+      L[r] = __funnelshift_r(w0, w1, sh);
+      M[r] = sh == 0 ? (w1 << 8 | w0 >> 24) : (w1 >> 8);
     }
-    uint32_t e = 0, o = 0;
-#pragma unroll
-    for (int c = 0; c < 4; c++) {   // (v + 4) // 9 == ((v + 4) * 7282) >> 16 for v + 4 < 32768
-      e |= (((2 * hs[0][c] + hs[1][c] + 4) * 7282u) >> 16) << (8 * c);
-      o |= (((hs[1][c] + 2 * hs[2][c] + 4) * 7282u) >> 16) << (8 * c);
-    }
+    // each output is one dp4a of a 2x2 input block with the separable weights
+    // (2, 1) x (2, 1) of _two_thirds (pyramid.py:76-94): even output row from
+    // rows 0-1, odd from rows 1-2; left output column of a pair from columns
+    // (0, 1), right from (1, 2) of its 3-column group
+    auto div9 = [](uint32_t v) { return (v * 7282u + 29128u) >> 16; };   // (v + 4) // 9, v + 4 < 32768
+    const uint32_t WL = 0x01020204u, WR = 0x02010402u;                   // bytes (a0 a1 b0 b1): 4 2 2 1 | 2 4 1 2
+    const uint32_t WLo = 0x02040102u, WRo = 0x04020201u;                 // odd rows: 2 1 4 2 | 1 2 2 4
+    const uint32_t e0 = div9(__dp4a(__byte_perm(L[0], L[1], 0x5410), WL, 0u));
+    const uint32_t e1 = div9(__dp4a(__byte_perm(L[0], L[1], 0x6521), WR, 0u));
+    const uint32_t e2 = div9(__dp4a(__byte_perm(M[0], M[1], 0x5410), WL, 0u));
+    const uint32_t e3 = div9(__dp4a(__byte_perm(M[0], M[1], 0x6521), WR, 0u));
+    const uint32_t o0 = div9(__dp4a(__byte_perm(L[1], L[2], 0x5410), WLo, 0u));
+    const uint32_t o1 = div9(__dp4a(__byte_perm(L[1], L[2], 0x6521), WRo, 0u));
+    const uint32_t o2 = div9(__dp4a(__byte_perm(M[1], M[2], 0x5410), WLo, 0u));
+    const uint32_t o3 = div9(__dp4a(__byte_perm(M[1], M[2], 0x6521), WRo, 0u));
+    const uint32_t e = __byte_perm(__byte_perm(e0, e1, 0x0040), __byte_perm(e2, e3, 0x0040), 0x5410);
+    const uint32_t o = __byte_perm(__byte_perm(o0, o1, 0x0040), __byte_perm(o2, o3, 0x0040), 0x5410);
     *reinterpret_cast<uint32_t*>(si0 + (2 * p) * 64 + 4 * q) = e;
     *reinterpret_cast<uint32_t*>(si0 + (2 * p + 1) * 64 + 4 * q) = o;
     put(1, 2 * X0 / 3, 2 * Y0 / 3, 2 * p, 4 * q, e);
