@@ -544,11 +544,26 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   // an o0 tile inside the frame has every derived tile inside its layer (the
   // tile origin is a multiple of 3 * 2^(O-1)): plain word stores, no bounds
   const bool interior = tw == TW && th == TH;
+  // derived tile origins of layer l (o0 tile origin x 2/3 and / 2^k; multiples
+  // of 3 * 2^(O-1) divide exactly) and their global base pointers, once per CTA
+  __shared__ uint8_t* lbase[8];
+  __shared__ int lgx[8], lgy[8];
+  if (tid >= 1 && tid < 8) {
+    const int k = (tid - 1) >> 1;                        // i_k (odd l) / o_(k+1) (even l)
+    const int gx0 = (tid & 1) ? (2 * X0 / 3) >> k : X0 >> (k + 1);
+    const int gy0 = (tid & 1) ? (2 * Y0 / 3) >> k : Y0 >> (k + 1);
+    const LayerGeo& L = g.L[tid];
+    lgx[tid] = gx0;
+    lgy[tid] = gy0;
+    lbase[tid] = b.layers + (long long)s * g.layer_slab + L.layer_off + (long long)gy0 * L.pitch + gx0;
+  }
   auto put = [&](int l, int gx0, int gy0, int y, int x, uint32_t w) {
+    (void)gx0;
+    (void)gy0;
     const LayerGeo& L = g.L[l];
-    uint8_t* gd = b.layers + (long long)s * g.layer_slab + L.layer_off + (long long)gy0 * L.pitch + gx0;
+    uint8_t* gd = lbase[l];
     if (interior) *reinterpret_cast<uint32_t*>(gd + y * L.pitch + x) = w;
-    else store_word(gd, L.pitch, y, x, L.w - gx0, L.h - gy0, w);
+    else store_word(gd, L.pitch, y, x, L.w - lgx[l], L.h - lgy[l], w);
   };
   // ---- o0 tile ----
   {
