@@ -1430,46 +1430,23 @@ __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int 
                                                int epoch)
 {
   // footprint bound of the 60 boxes (|p| <= 10.8, radius <= 1.69 sigma): tile
-  // rows x column runs set in the stream's tile bitmap; bits newly set by this
-  // call append their tiles to the k_sat list.  The atomics of up to four
-  // (row, word) runs are issued before any result is used.
+  // rows x column runs OR-ed into the stream's tile bitmap, which k_sat reads
   (void)epoch;
   const int F = (int)ceil(12.5 * sg) + 2;
   const int xi = (int)x, yi = (int)y;
   const int xa = max(0, xi - F), xb = min(g.W - 1, xi + F + 1);
   const int ya = max(0, yi - F), yb = min(g.H - 1, yi + F + 1);
   const int txa = xa / VF_ST, txb = xb / VF_ST, tya = ya / VF_ST, tyb = yb / VF_ST;
-  const int wa = txa >> 5, wb = txb >> 5, nw = wb - wa + 1;
-  const int nrun = (tyb - tya + 1) * nw;
+  const int wa = txa >> 5, wb = txb >> 5;
   unsigned* bits = b.sat_bits + (long long)s * g.sty * g.stw_words;
-  for (int r0 = 0; r0 < nrun; r0 += 4) {
-    unsigned got[4], msk[4];
-    int tyv[4], wv[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      got[u] = 0xffffffffu; msk[u] = 0; tyv[u] = 0; wv[u] = 0;
-      const int r = r0 + u;
-      if (r < nrun) {
-        const int ty = tya + r / nw, w = wa + r % nw;
-        const int lo = max(txa, 32 * w) - 32 * w, hi = min(txb, 32 * w + 31) - 32 * w;
-        const unsigned m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
-        tyv[u] = ty; wv[u] = w; msk[u] = m;
-        got[u] = atomicOr(bits + ty * g.stw_words + w, m);
-      }
+  // set the footprint's tiles in the stream's bitmap (no return value is
+  // consumed: k_sat lists the set tiles itself)
+  for (int ty = tya; ty <= tyb; ty++)
+    for (int w = wa; w <= wb; w++) {
+      const int lo = max(txa, 32 * w) - 32 * w, hi = min(txb, 32 * w + 31) - 32 * w;
+      const unsigned m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+      atomicOr(bits + ty * g.stw_words + w, m);
     }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      unsigned nb = msk[u] & ~got[u];
-      if (nb) {
-        int pos = atomicAdd(b.sat_count + s, __popc(nb));
-        while (nb) {
-          const int bit = __ffs(nb) - 1;
-          nb &= nb - 1;
-          b.sat_work[(long long)s * g.sat_tiles + pos++] = tyv[u] * g.stx + 32 * wv[u] + bit;
-        }
-      }
-    }
-  }
 }
 
 // Last warp of stream s: band offsets, propagation-chunk offsets, FrameReport.
@@ -1492,6 +1469,25 @@ __device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
     carry += tot;
   }
   const int n_det = carry;
+  // SAT tiles marked by the stream's bands (k_nms ORs footprints into the
+  // bitmap) -> the k_sat work list, in bitmap order
+  if (use_mask(g, b, s)) {
+    const int nw = g.sty * g.stw_words;
+    const unsigned* bits = b.sat_bits + (long long)s * nw;
+    int* work = b.sat_work + (long long)s * g.sat_tiles;
+    int cnt = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int wi = w0 + lane;
+      unsigned v = wi < nw ? __ldcg(bits + wi) : 0u;
+      int tot;
+      const int off = warp_excl_scan(__popc(v), lane, tot);
+      const int ty = wi / g.stw_words, t0 = ty * g.stx + 32 * (wi - ty * g.stw_words);
+      int pos = cnt + off;
+      for (; v; v &= v - 1u) work[pos++] = t0 + __ffs(v) - 1;
+      cnt += tot;
+    }
+    if (lane == 0) b.sat_count[s] = cnt;
+  }
   // propagated total: scanned by k_worklist (joined before this launch)
   const int n_prop = use_mask(g, b, s) ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
 #pragma unroll
