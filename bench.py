@@ -963,9 +963,9 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # per step: pyramid, worklist x2, fast, nms, sat, describe x3, finalize
+        # per step: pyramid, worklist x2, fast, nms, nms_finish, sat, describe x3, finalize
         # (+ propagate in the mask modes, + binmask in binning mode)
-        "gpu_launches": (10 + (1 if args.mode == "binning" else 0) + (1 if args.mode != "none" else 0)) * K,
+        "gpu_launches": (11 + (1 if args.mode == "binning" else 0) + (1 if args.mode != "none" else 0)) * K,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -1619,16 +1619,13 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
     int4* rec = reinterpret_cast<int4*>(b.band_rec) + ((long long)s * g.bands_per_stream + bid);
     *rec = make_int4(base, kept, n_ok, n_drop);
   }
-  // ---- last warp of the stream scans ----
-  __threadfence();
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) last = atomicAdd(&ctr[C_TICKET], 1) == g.bands_per_stream - 1;
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (last) {
-    __threadfence();
-    nms_last_warp(g, b, s, lane);
-  }
+}
+
+// After k_nms (stream order): per stream, the band offsets, the SAT-tile work
+// list and the FrameReport (nms_last_warp), one warp per stream.
+__global__ void __launch_bounds__(32) k_nms_finish(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  nms_last_warp(g, b, b.s0 + blockIdx.x, threadIdx.x);
 }
 
 // ============================================================================
