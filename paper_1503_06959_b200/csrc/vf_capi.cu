@@ -658,7 +658,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   stage_mark(c, 4, st);
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
-  k_nms_finish<<<n, 32, 0, st>>>(g, b);
+  k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
   k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
   stage_mark(c, 6, st);
@@ -1254,7 +1254,7 @@ int vf_nms_refine(const uint8_t* const* maps_dev, const int64_t* pitches, int W,
   cudaMemcpyAsync(b.band_stamp, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.band_cand, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), 1), NMS_THREADS, 0, st>>>(g, b);
-  k_nms_finish<<<1, 32, 0, st>>>(g, b);
+  k_nms_finish<<<1, NF_THREADS, 0, st>>>(g, b);
   k_gather_kps<<<g.bands_per_stream, 128, 0, st>>>(g, b, x_dev, y_dev, sigma_dev, score_dev, cap);
   int ctr[C_NCTR];
   cudaMemcpyAsync(ctr, b.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st);

@@ -1449,67 +1449,27 @@ __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int 
     }
 }
 
-// Last warp of stream s: band offsets, propagation-chunk offsets, FrameReport.
-__device__ void nms_last_warp(const Geo& g, const Bufs& b, int s, int lane)
+// Block-wide exclusive scan (blockDim.x = NF_THREADS) of one value per thread.
+#define NF_THREADS 256
+__device__ __forceinline__ int block_excl_scan(int v, int& total, int* sm)
 {
-  const int* rec = b.band_rec + (long long)s * g.bands_per_stream * 4;
-  int* bout = b.band_out + (long long)s * g.bands_per_stream;
-  int carry = 0, n_drop = 0, n_surv = 0, tot;
-  for (int base = 0; base < g.bands_per_stream; base += 32) {
-    const int i = base + lane;
-    int k = 0;
-    if (i < g.bands_per_stream) {
-      const int4 r = __ldcg(reinterpret_cast<const int4*>(rec) + i);
-      k = r.y;
-      n_drop += r.w;
-      n_surv += r.z + r.w;
-    }
-    const int ex = warp_excl_scan(k, lane, tot);
-    if (i < g.bands_per_stream) bout[i] = carry + ex;
-    carry += tot;
-  }
-  const int n_det = carry;
-  // SAT tiles marked by the stream's bands (k_nms ORs footprints into the
-  // bitmap) -> the k_sat work list, in bitmap order
-  if (use_mask(g, b, s)) {
-    const int nw = g.sty * g.stw_words;
-    const unsigned* bits = b.sat_bits + (long long)s * nw;
-    int* work = b.sat_work + (long long)s * g.sat_tiles;
-    int cnt = 0;
-    for (int w0 = 0; w0 < nw; w0 += 32) {
-      const int wi = w0 + lane;
-      unsigned v = wi < nw ? __ldcg(bits + wi) : 0u;
-      int tot;
-      const int off = warp_excl_scan(__popc(v), lane, tot);
-      const int ty = wi / g.stw_words, t0 = ty * g.stx + 32 * (wi - ty * g.stw_words);
-      int pos = cnt + off;
-      for (; v; v &= v - 1u) work[pos++] = t0 + __ffs(v) - 1;
-      cnt += tot;
-    }
-    if (lane == 0) b.sat_count[s] = cnt;
-  }
-  // propagated total: scanned by k_worklist (joined before this launch)
-  const int n_prop = use_mask(g, b, s) ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int wt;
+  const int ex = warp_excl_scan(v, lane, wt);
+  if (lane == 31) sm[wid] = wt;
+  __syncthreads();
+  int off = 0;
+  total = 0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_drop += __shfl_down_sync(0xffffffffu, n_drop, o);
-    n_surv += __shfl_down_sync(0xffffffffu, n_surv, o);
+  for (int w = 0; w < NF_THREADS / 32; w++) {
+    const int t = sm[w];
+    off += w < wid ? t : 0;
+    total += t;
   }
-  if (lane == 0) {
-    int* ctr = b.ctr + s * C_NCTR;
-    int n_total = n_det + n_prop;
-    if (n_total > g.kp_cap) { ctr[C_ERR] |= VF_ERRBIT_CAPACITY; n_total = g.kp_cap; }
-    ctr[C_NDET] = n_det; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
-    ctr[C_NSURV] = n_surv;
-    ctr[C_TICKET] = 0;
-    const int um = use_mask(g, b, s);
-    const double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
-    double* rp = b.report + (long long)s * 16;
-    rp[0] = n_det; rp[1] = n_prop; rp[2] = n_total; rp[3] = n_drop; rp[4] = cov;
-    rp[5] = ctr[C_FRAME]; rp[6] = n_surv; rp[7] = __ldcg(&ctr[C_NCAND]);
-    rp[8] += n_det; rp[9] += n_total; rp[10] += cov; rp[11] += 1.0;
-  }
+  __syncthreads();
+  return off + ex;
 }
+
 
 // One warp per band (8 rows of one layer).  Candidates come from the FAST
 // bitmap: lane l owns a contiguous run of bitmap words, so a warp scan gives
@@ -1621,11 +1581,83 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
   }
 }
 
-// After k_nms (stream order): per stream, the band offsets, the SAT-tile work
-// list and the FrameReport (nms_last_warp), one warp per stream.
-__global__ void __launch_bounds__(32) k_nms_finish(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+// After k_nms (stream order), one CTA per stream: band output offsets (scan
+// of the kept counts in band order), the SAT-tile work list (the bitmap's set
+// tiles in bitmap order) and the FrameReport.  Every load is issued up front.
+__global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
-  nms_last_warp(g, b, b.s0 + blockIdx.x, threadIdx.x);
+  __shared__ int sm[NF_THREADS / 32];
+  __shared__ int red[2][NF_THREADS / 32];
+  const int s = b.s0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nb = g.bands_per_stream;
+  const int4* rec = reinterpret_cast<const int4*>(b.band_rec) + (long long)s * nb;
+  int* bout = b.band_out + (long long)s * nb;
+  const int um = use_mask(g, b, s);
+  // ---- band offsets: thread t owns bands [t * per, t * per + per) ----
+  const int per = (nb + NF_THREADS - 1) / NF_THREADS;
+  int kept = 0, n_drop = 0, n_surv = 0;
+  for (int k = 0; k < per; k++) {
+    const int i = tid * per + k;
+    if (i < nb) {
+      const int4 r = __ldcg(rec + i);
+      kept += r.y;
+      n_drop += r.w;
+      n_surv += r.z + r.w;
+    }
+  }
+  int n_det;
+  int run = block_excl_scan(kept, n_det, sm);
+  for (int k = 0; k < per; k++) {
+    const int i = tid * per + k;
+    if (i < nb) {
+      bout[i] = run;
+      run += __ldcg(rec + i).y;
+    }
+  }
+  // ---- SAT tiles marked by the stream's bands (k_nms ORs footprints into
+  // the bitmap) -> the k_sat work list ----
+  if (um) {
+    const int nw = g.sty * g.stw_words;
+    const unsigned* bits = b.sat_bits + (long long)s * nw;
+    int* work = b.sat_work + (long long)s * g.sat_tiles;
+    int cnt = 0;
+    for (int w0 = 0; w0 < nw; w0 += NF_THREADS) {
+      const int wi = w0 + tid;
+      unsigned v = wi < nw ? __ldcg(bits + wi) : 0u;
+      int tot;
+      int pos = cnt + block_excl_scan(__popc(v), tot, sm);
+      const int ty = wi / g.stw_words, t0 = ty * g.stx + 32 * (wi - ty * g.stw_words);
+      for (; v; v &= v - 1u) work[pos++] = t0 + __ffs(v) - 1;
+      cnt += tot;
+    }
+    if (tid == 0) b.sat_count[s] = cnt;
+  }
+  // ---- FrameReport ----
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_drop += __shfl_down_sync(0xffffffffu, n_drop, o);
+    n_surv += __shfl_down_sync(0xffffffffu, n_surv, o);
+  }
+  if (lane == 0) { red[0][wid] = n_drop; red[1][wid] = n_surv; }
+  __syncthreads();
+  if (tid == 0) {
+    n_drop = 0;
+    n_surv = 0;
+    for (int w = 0; w < NF_THREADS / 32; w++) { n_drop += red[0][w]; n_surv += red[1][w]; }
+    // propagated total: scanned by k_worklist (joined before k_nms)
+    const int n_prop = um ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
+    int* ctr = b.ctr + s * C_NCTR;
+    int n_total = n_det + n_prop;
+    if (n_total > g.kp_cap) { ctr[C_ERR] |= VF_ERRBIT_CAPACITY; n_total = g.kp_cap; }
+    ctr[C_NDET] = n_det; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
+    ctr[C_NSURV] = n_surv;
+    ctr[C_TICKET] = 0;
+    const double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
+    double* rp = b.report + (long long)s * 16;
+    rp[0] = n_det; rp[1] = n_prop; rp[2] = n_total; rp[3] = n_drop; rp[4] = cov;
+    rp[5] = ctr[C_FRAME]; rp[6] = n_surv; rp[7] = __ldcg(&ctr[C_NCAND]);
+    rp[8] += n_det; rp[9] += n_total; rp[10] += cov; rp[11] += 1.0;
+  }
 }
 
 // ============================================================================
