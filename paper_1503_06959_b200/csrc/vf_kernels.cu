@@ -864,6 +864,8 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
   // bytes; the rectangle's words are loaded four at a time.
   const int tile = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = tile < g.tiles_per_stream;
+  int* st = b.tile_stamp + (long long)s * g.tiles_per_stream + tile;
+  const int old_stamp = valid ? *st : 0;   // issued with the mask loads below
   int l = 0, ty = 0;
   bool active = false;
   if (valid) {
@@ -939,14 +941,13 @@ __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g,
   // not now becomes a clear item (tile | VF_CLEAR) that k_fast zeroes.
   bool clear = false;
   if (valid) {
-    int* st = b.tile_stamp + (long long)s * g.tiles_per_stream + tile;
     if (active) {
       const LayerGeo& Lg = g.L[l];
       *st = epoch;
       b.band_stamp[(long long)s * g.bands_per_stream + Lg.band_base + ty] = epoch;
       b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty] = 0;
     } else {
-      clear = *st == epoch - 1;
+      clear = old_stamp == epoch - 1;
     }
   }
   // warp-aggregated append to the work list
