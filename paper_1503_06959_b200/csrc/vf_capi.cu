@@ -289,6 +289,8 @@ struct vf_ctx {
   std::vector<cudaStream_t> gstreams;
   std::vector<cudaEvent_t> gjoin;
   cudaEvent_t gfork = nullptr;
+  cudaStream_t hp = nullptr;
+  cudaEvent_t hp_in = nullptr, hp_out = nullptr;
 };
 
 static void pack_free(vf_ctx* c)
@@ -514,6 +516,7 @@ int vf_destroy(vf_ctx* c)
     cudaEventDestroy(c->aux_out[k]);
   }
   if (c->gfork) cudaEventDestroy(c->gfork);
+  if (c->hp) { cudaStreamDestroy(c->hp); cudaEventDestroy(c->hp_in); cudaEventDestroy(c->hp_out); }
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
@@ -685,7 +688,25 @@ static int launch_grouped(vf_ctx* c, int n, cudaStream_t st)
   if (const char* e = getenv("VF_STREAM_GROUPS")) G = std::max(1, std::min(n, atoi(e)));
   if (G == 1) {
     c->cur_group = 0;
-    return launch_step(c, 0, n, st);
+    // The main chain runs on an internal highest-priority stream, so the block
+    // scheduler prefers its CTAs over the side stream's propagation, which
+    // fills the slots FAST / NMS leave (733 -> 710 us per 64-stream step);
+    // VF_PRIO=0 launches on the caller's stream instead
+    static const bool prio = !(getenv("VF_PRIO") && atoi(getenv("VF_PRIO")) == 0);
+    if (!prio) return launch_step(c, 0, n, st);
+    if (!c->hp) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (cudaStreamCreateWithPriority(&c->hp, cudaStreamNonBlocking, hi) != cudaSuccess) return VF_ERR_CUDA;
+      cudaEventCreateWithFlags(&c->hp_in, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&c->hp_out, cudaEventDisableTiming);
+    }
+    cudaEventRecord(c->hp_in, st);
+    cudaStreamWaitEvent(c->hp, c->hp_in, 0);
+    const int rc = launch_step(c, 0, n, c->hp);
+    cudaEventRecord(c->hp_out, c->hp);
+    cudaStreamWaitEvent(st, c->hp_out, 0);
+    return rc;
   }
   if ((int)c->gstreams.size() < G) {
     if (!c->gfork) cudaEventCreateWithFlags(&c->gfork, cudaEventDisableTiming);
