@@ -917,7 +917,7 @@ def main():
         kernels.append(row)
     kernels.sort(key=lambda r: -r["ms_per_step"])
     traffic = None
-    tf = ROOT / "profiles" / "r01f_traffic.json"
+    tf = ROOT / "profiles" / "r01g_traffic.json"
     if tf.exists():
         try:
             tj = json.loads(tf.read_text())
@@ -928,7 +928,7 @@ def main():
         "bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s", "frac": step_achieved / peak,
         "traffic": traffic, "kernel": "detect+describe step (all launches of one step)",
         "algorithmic_bytes_per_step": b_alg / K,
-        "traffic_source": "profiles/r01f_traffic.json: sum of ncu dram__bytes_read+write over one step's launches (cold-cache replays)"
+        "traffic_source": "profiles/r01g_traffic.json: sum of ncu dram__bytes_read+write over one step's launches (cold-cache replays)"
                           if traffic is not None else None,
         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
         "dominant_kernel": kernels[0] if kernels else None,
