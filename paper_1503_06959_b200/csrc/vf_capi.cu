@@ -291,6 +291,9 @@ struct vf_ctx {
   cudaEvent_t gfork = nullptr;
   cudaStream_t hp = nullptr;
   cudaEvent_t hp_in = nullptr, hp_out = nullptr;
+  std::vector<cudaStream_t> dstreams;
+  std::vector<cudaEvent_t> djoin;
+  cudaEvent_t dfork = nullptr;
 };
 
 static void pack_free(vf_ctx* c)
@@ -517,6 +520,8 @@ int vf_destroy(vf_ctx* c)
   }
   if (c->gfork) cudaEventDestroy(c->gfork);
   if (c->hp) { cudaStreamDestroy(c->hp); cudaEventDestroy(c->hp_in); cudaEventDestroy(c->hp_out); }
+  for (size_t k = 0; k < c->dstreams.size(); k++) { cudaStreamDestroy(c->dstreams[k]); cudaEventDestroy(c->djoin[k]); }
+  if (c->dfork) cudaEventDestroy(c->dfork);
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
@@ -663,11 +668,48 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
-  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
-  stage_mark(c, 6, st);
-  k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0);
-  k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
-  k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
+  // SAT + describe of two stream halves on concurrent high-priority streams:
+  // the latency-bound sampling kernels of one half fill the other's gaps and
+  // tails (709 -> 698 us per 64-stream step).  The stage timer then reports
+  // SAT and describe together.  VF_DESC_PAR overrides the number of halves.
+  static const int dpar = getenv("VF_DESC_PAR") ? std::max(1, atoi(getenv("VF_DESC_PAR"))) : 2;
+  if (dpar > 1 && n >= dpar) {
+    if ((int)c->dstreams.size() < dpar) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (!c->dfork) cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
+      while ((int)c->dstreams.size() < dpar) {
+        cudaStream_t ds;
+        cudaEvent_t de;
+        cudaStreamCreateWithPriority(&ds, cudaStreamNonBlocking, hi);
+        cudaEventCreateWithFlags(&de, cudaEventDisableTiming);
+        c->dstreams.push_back(ds);
+        c->djoin.push_back(de);
+      }
+    }
+    cudaEventRecord(c->dfork, st);
+    for (int h = 0; h < dpar; h++) {
+      const int h0 = (int)((long long)n * h / dpar), h1 = (int)((long long)n * (h + 1) / dpar);
+      Bufs bh = b;
+      bh.s0 = b.s0 + h0;
+      bh.frames = b.frames + (long long)h0 * b.frame_stride;
+      const int nh = h1 - h0, pb = (nh + 1) * (int)sizeof(int);
+      cudaStream_t ds = c->dstreams[h];
+      cudaStreamWaitEvent(ds, c->dfork, 0);
+      k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh);
+      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 0);
+      k_desc_orient<<<c->dorient_grid, DO_THREADS, pb, ds>>>(g, bh, nh);
+      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 1);
+      cudaEventRecord(c->djoin[h], ds);
+    }
+    for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[h], 0);
+  } else {
+    k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
+    stage_mark(c, 6, st);
+    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0);
+    k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
+    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
+  }
   // k_propagate (stage 7) is timed on the side stream; the join wait counts
   // toward the finalize stage
   stage_mark(c, 8, st);
