@@ -74,6 +74,12 @@ def shard(n_total, rank, world):
     return list(range(lo, hi))
 
 
+def desc_halves(n_streams):
+    """Concurrent SAT + describe stream halves of one step (csrc/vf_capi.cu launch_step)."""
+    d = max(1, int(os.environ.get("VF_DESC_PAR", "2")))
+    return d if n_streams >= d > 1 else 1
+
+
 def hbm_peak():
     try:
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
@@ -969,9 +975,11 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # per step: pyramid, worklist x2, fast, nms, nms_finish, sat, describe x3, finalize
+        # per step: pyramid, worklist x2, fast, nms, nms_finish, finalize, and sat + describe x3
+        # once per concurrent stream half (VF_DESC_PAR, default 2 when >= 2 streams)
         # (+ propagate in the mask modes, + binmask in binning mode)
-        "gpu_launches": (11 + (1 if args.mode == "binning" else 0) + (1 if args.mode != "none" else 0)) * K,
+        "gpu_launches": (7 + 4 * desc_halves(S) + (1 if args.mode == "binning" else 0)
+                         + (1 if args.mode != "none" else 0)) * K,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
