@@ -1096,7 +1096,8 @@ extern "C" int vf_radius_match(const uint8_t* q_dev, int64_t nq, const uint8_t* 
     } else if (n > 0) {
       // (query, reference) order of np.nonzero: sort the 64-bit keys
       int end_bit = 64;
-      while (end_bit > 1 && !(((unsigned long long)(nq - 1) << 32) >> (end_bit - 1))) end_bit--;
+      // never below the 32 reference-index bits (a single query still sorts by r)
+      while (end_bit > 32 && !(((unsigned long long)(nq - 1) << 32) >> (end_bit - 1))) end_bit--;
       size_t tmp_bytes = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_sorted, dist_tmp, dist_dev, (int64_t)n, 0,
                                       end_bit, st);

@@ -145,3 +145,22 @@ def test_gloo_world2_stats_gather():
     assert a.shape == (5, 3, 8)
     assert a[:, 0, 0].tolist() == [0, 1, 2, 3, 4]
     assert a[3, 2, 2] == 32 and a[3, 2, 4] == 35
+
+
+def test_integration_stub_struct_matches_header():
+    """The ctypes stub a reference maintainer copies from INTEGRATION.md must
+    lay out vf_config / vf_report exactly as include/vidfeat_b200.h does
+    (vf_create copies the whole struct)."""
+    import ctypes
+
+    from paper_1503_06959_b200 import _native
+
+    text = (ROOT / "INTEGRATION.md").read_text()
+    ns = {"ctypes": ctypes}
+    for name in ("VfConfig", "VfReport"):
+        m = re.search(rf"^class {name}\(ctypes\.Structure\):\n(?:    .*\n|\s*#.*\n)+", text, re.M)
+        assert m, f"{name} stub missing from INTEGRATION.md"
+        exec(m.group(0), ns)
+        stub, real = ns[name], getattr(_native, name)
+        assert ctypes.sizeof(stub) == ctypes.sizeof(real), name
+        assert [f[0] for f in stub._fields_] == [f[0] for f in real._fields_], name

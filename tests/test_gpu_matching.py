@@ -59,6 +59,10 @@ def test_reference_unit_cases():
     assert len(radius_match(feats([base]), feats([flip(102)]), 102)) == 1
     assert len(radius_match(feats([base]), feats([flip(103)]), 102)) == 0
     assert len(radius_match(feats([base]), feats([flip(0), flip(10), flip(50)]), 102)) == 3
+    # one query, many references: np.nonzero order is reference order
+    refs = feats([flip(k) for k in (0, 90, 10, 200, 50, 3, 101, 7)])
+    got = [(m.ref_idx, m.distance) for m in radius_match(feats([base]), refs, 102)]
+    assert got == [(0, 0), (1, 90), (2, 10), (4, 50), (5, 3), (6, 101), (7, 7)]
     q, r = feats(rng.integers(0, 2, (6, 512))), feats(rng.integers(0, 2, (6, 512)))
     fwd = {(m.query_idx, m.ref_idx) for m in radius_match(q, r, 260)}
     rev = {(m.ref_idx, m.query_idx) for m in radius_match(r, q, 260)}
