@@ -1,21 +1,26 @@
 #!/usr/bin/env python
 """Benchmark: frames/s (and MPix/s) of the per-frame detect+describe hot path.
 
-Workload (BASELINE.json config 5): 64 independent 1920x1080 uint8 streams,
-seeded synthetic scenes (kind = s mod 3: static / pan / objects), reference
-defaults t = 55, O = 4, intensity mask t_i = 20 (the primary mode,
-BASELINE.md section 4).  Streams are sharded contiguously across ranks
-(strong scaling: total 64 streams).  One step = frame n of every local stream
-through the whole path (pyramid -> mask -> score -> NMS/refine -> describe ->
-Eq. 1 merge).  Frames are generated on the GPU and resident in HBM before the
-timed region; each step reads a fresh batch (8-64 x 2.07 MB).
+Workloads (BASELINE.json configs, --config, default 5 = the headline):
+  1  640x480, 1 stream, moving objects          2  1280x720, 1 stream, global pan
+  3  8 x 1920x1080 streams, one GPU             4  3840x2160, 1 stream, full change every frame
+  5  64 x 1920x1080 streams (static / pan / objects), sharded across ranks
+Reference defaults t = 55, O = 4; --mode intensity (t_i = 20, the primary
+mode), binning or none.  Streams are sharded
+contiguously across ranks (strong scaling); a config with fewer streams than
+ranks runs one replica per rank (weak scaling).  One step = frame n of every
+local stream through the whole path (pyramid -> mask -> score -> NMS/refine ->
+describe -> Eq. 1 merge).  Frames come from the CPU scene generator (the same
+bytes --impl reference and the parity tests use) and are resident in HBM
+before the timed region.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--config C] [--mode M] [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 --impl reference times the reference algorithm on the host cores through the
 CPU oracle port (oracle/vf_oracle.c, kind "port"; the reference itself is a
-Python package that cannot travel to the GPU box), rank 0 only.
+Python package that cannot travel to the GPU box), rank 0 only, on the same
+config and bytes.
 """
 
 from __future__ import annotations
@@ -49,7 +54,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="intensity", choices=["intensity", "binning", "none", "temporal"])
-    ap.add_argument("--streams", type=int, default=TOTAL_STREAMS)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (1: VGA, 2: 720p pan, 3: 8 x 1080p, 4: 4K dense, 5: 64 x 1080p)")
+    ap.add_argument("--streams", type=int, default=0, help="override the config's stream count (0 = the config's)")
+    ap.add_argument("--gen", default="cpu", choices=["cpu", "cuda"],
+                    help="scene generator: cpu = the bytes the reference arm and the parity tests use")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -240,14 +249,66 @@ def cpu_model():
 
 
 # ----------------------------------------------------------------------------
-def gen_frames(streams, n_frames, device):
-    """[n_frames, S, H, W] uint8 on `device` (config 5 scenes)."""
+# detect+describe workload: BASELINE.json configs 1..5
+# ----------------------------------------------------------------------------
+L2_BYTES = 126 << 20          # B200 L2
+FLUSH_BYTES = 256 << 20       # written between timed steps when a step's inputs fit in L2
+REF_TIME_BUDGET_S = 150.0     # --impl reference: stop timing after this much CPU time (bounded sample)
+
+
+def config_of(args):
+    from paper_1503_06959_b200 import scenes
+
+    cfg = scenes.CONFIGS[args.config]
+    n_streams = args.streams if args.streams > 0 else cfg.n_streams
+    return cfg, n_streams
+
+
+def workload_name(args, cfg, n_streams):
+    kinds = {"objects": "moving objects", "pan": "global pan + objects", "fresh": "fresh noise every frame",
+             "mixed": "static / pan / objects by stream mod 3", "static": "static"}
+    return (f"config{args.config}: {n_streams} x {cfg.width}x{cfg.height} uint8 stream{'s' if n_streams > 1 else ''} "
+            f"({kinds.get(cfg.kind, cfg.kind)}), mode {args.mode}, t=55, O=4"
+            + (", t_i=20" if args.mode == "intensity" else "") + (", 16x16 grid t_h=1" if args.mode == "binning" else ""))
+
+
+def gen_frames_cpu(cfg, streams, n_frames, device=None, threads=None):
+    """[n_frames, S, H, W] uint8 of the given streams from the CPU scene
+    generator (the bytes the reference arm and the parity tests use), uploaded
+    stream by stream to `device` (None: stays on the host)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import torch
 
     from paper_1503_06959_b200 import scenes
 
-    cfg = scenes.CONFIGS[5]
-    out = torch.empty((n_frames, len(streams), H_FR, W_FR), dtype=torch.uint8, device=device)
+    out = torch.empty((n_frames, len(streams), cfg.height, cfg.width), dtype=torch.uint8,
+                      device=device if device is not None else "cpu")
+
+    def one(j):
+        st = scenes.SceneStream(cfg, streams[j], "cpu")
+        buf = torch.stack([st.next_frame() for _ in range(n_frames)])
+        out[:, j].copy_(buf, non_blocking=False)
+        return j
+
+    nt = threads or host_threads()
+    old = torch.get_num_threads()
+    torch.set_num_threads(max(1, old // max(1, min(nt, len(streams)))))
+    try:
+        with ThreadPoolExecutor(max_workers=max(1, min(nt, len(streams)))) as ex:
+            list(ex.map(one, range(len(streams))))
+    finally:
+        torch.set_num_threads(old)
+    return out
+
+
+def gen_frames_cuda(cfg, streams, n_frames, device):
+    """[n_frames, S, H, W] uint8 on `device` from the CUDA scene generator (fast; different RNG bytes)."""
+    import torch
+
+    from paper_1503_06959_b200 import scenes
+
+    out = torch.empty((n_frames, len(streams), cfg.height, cfg.width), dtype=torch.uint8, device=device)
     for j, s in enumerate(streams):
         st = scenes.SceneStream(cfg, s, device)
         for n in range(n_frames):
@@ -255,61 +316,406 @@ def gen_frames(streams, n_frames, device):
     return out
 
 
-def algorithmic_bytes(n_frames, cov_sum, k_out, k_prop, O=4):
-    """B_alg = W*H*[1 + 2*4^-(O-1) + 2*a*(rho - 4^-(O-1))] + 109*(K_out + K_prop)."""
-    rho = 0.918
-    top = 4.0 ** -(O - 1)
-    wh = W_FR * H_FR
-    return wh * (n_frames * (1 + 2 * top) + 2 * cov_sum * (rho - top)) + 109.0 * (k_out + k_prop)
+def gen_frames(streams, n_frames, device):
+    """Config-5 frames on the CUDA generator (match / dump workloads)."""
+    from paper_1503_06959_b200 import scenes
+
+    return gen_frames_cuda(scenes.CONFIGS[5], streams, n_frames, device)
+
+
+def layer_areas(W, H, O=4):
+    """(rho, top): derived-layer area / WH and top-octave area / WH (pyramid.py:97-125 geometry)."""
+    ws, hs = [], []
+    ow, oh, iw, ih = W, H, (2 * W) // 3, (2 * H) // 3
+    for o in range(O):
+        if o:
+            ow, oh, iw, ih = ow // 2, oh // 2, iw // 2, ih // 2
+        ws += [ow, iw]
+        hs += [oh, ih]
+    wh = float(W * H)
+    rho = sum(w * h for w, h in zip(ws[1:], hs[1:])) / wh
+    return rho, ws[2 * (O - 1)] * hs[2 * (O - 1)] / wh
+
+
+def algorithmic_bytes(W, H, n_frames, cov_sum, k_out, k_prop, k_prev_binning=0.0, O=4):
+    """B_alg = sum over frames of W*H*[1 + 2*top + 2*a*(rho - top)]
+    + 109*(K_out + K_prop) [+ 16*K_prev in binning mode], with K_out = |D_n| (the
+    emitted list, detected + propagated) and K_prop the propagated features read.
+    Returns (total, per-kernel shares) -- the shares sum to the total:
+      pyramid   reads the frame, writes + re-reads the top octave (IDDM state),
+                writes the derived layers within active cells;
+      fast      reads the derived layers within active cells;
+      describe  writes the detected feature records (109 B);
+      propagate reads + writes the propagated records;
+      binmask   reads the previous (x, y) pairs (binning mode)."""
+    rho, top = layer_areas(W, H, O)
+    wh = float(W * H)
+    derived = wh * cov_sum * (rho - top)
+    k_det = k_out - k_prop
+    parts = {
+        "pyramid": wh * n_frames * (1 + 2 * top) + derived,
+        "fast": derived,
+        "describe": 109.0 * k_det,
+        "propagate": 218.0 * k_prop,
+        "binmask": 16.0 * k_prev_binning,
+    }
+    return sum(parts.values()), parts
 
 
 def run_reference(args, rank, world):
+    """The reference algorithm on the host cores (oracle/vf_oracle.c, kind
+    "port"): the same config, scenes and bytes as the GPU arm (CPU scene
+    generator), one frame of each sampled stream per step, one stream per host
+    thread.  Streams are sequential in time, so a single-stream config uses one
+    core.  Bounded: timing stops after REF_TIME_BUDGET_S."""
     if rank != 0:
         return
-    from paper_1503_06959_b200 import scenes
-    import torch
-
-    threads = host_threads()
-    n_str = min(args.streams, threads)
-    streams = list(range(n_str))
-    steps = args.warmup + args.steps
-    # frames of the sample streams (CPU-generated; same generator as the GPU arm)
-    data = [scenes.generate(scenes.CONFIGS[5], steps, streams=[s])[0].numpy() for s in streams]
-    # warmup frames then timed frames, stream-sequential
-    from oracle import oracle
-    from paper_1503_06959_b200.pattern import default_pattern
     from concurrent.futures import ThreadPoolExecutor
 
+    from oracle import oracle
+    from paper_1503_06959_b200.pattern import default_pattern
+
+    cfg, n_total = config_of(args)
+    threads = host_threads()
+    n_str = min(n_total, threads)
+    streams = list(range(n_str))
+    steps = args.warmup + args.steps
+    data = gen_frames_cpu(cfg, streams, steps).numpy()       # [F, S, H, W]
     pat = default_pattern()
-    pipes = [oracle.OraclePipeline(W_FR, H_FR, pat, mode=args.mode) for _ in streams]
+    W, H = cfg.width, cfg.height
+    pipes = [oracle.OraclePipeline(W, H, pat, mode=args.mode) for _ in streams]
 
     def step(n):
-        with ThreadPoolExecutor(max_workers=threads) as ex:
-            list(ex.map(lambda i: pipes[i].process(data[i][n]), range(n_str)))
+        with ThreadPoolExecutor(max_workers=n_str) as ex:
+            list(ex.map(lambda i: pipes[i].process(data[n, i]), range(n_str)))
 
     for n in range(args.warmup):
         step(n)
     t0 = time.perf_counter()
+    done = 0
     for n in range(args.warmup, steps):
         step(n)
+        done += 1
+        if time.perf_counter() - t0 > REF_TIME_BUDGET_S:
+            break
     dt = time.perf_counter() - t0
     for p in pipes:
         p.close()
-    frames = n_str * args.steps
+    frames = n_str * done
     fps = frames / dt
+    sample = (f"{n_str} of {n_total} streams x {done} frames (after {args.warmup} warm-up frames), the GPU arm's "
+              f"bytes (CPU scene generator); C oracle (oracle/vf_oracle.c), one thread per stream on {cpu_model()}")
     line = {
         "impl": "reference", "metric": "frames/sec (detect+describe)", "value": fps, "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"config5: {TOTAL_STREAMS} x 1920x1080 streams, mode {args.mode}, t=55, O=4",
-                   "sample": f"{n_str} streams x 1 frame per step"},
-        "mpix_per_sec": fps * W_FR * H_FR / 1e6,
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{n_str} streams x {args.steps} frames after {args.warmup} warm-up frames; "
-                                   f"C oracle (oracle/vf_oracle.c) one thread per stream on {cpu_model()}"},
+        "n_gpus": args.gpus, "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(done, 1),
+        "higher_is_better": True, "scaling": "strong" if n_total > 1 else "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic", "same_config": True,
+        "config": {"workload": workload_name(args, cfg, n_total), "sample": sample, "frames": "cpu generator"},
+        "mpix_per_sec": fps * W * H / 1e6,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": n_str, "kind": "port", "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def init_process_group(world, local):
+    """NCCL process group (one process per GPU).  At N = 1 a world-size-1 group
+    on loopback is created too, so the end-of-run statistics gather is the same
+    collective on the measured path at every N."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return "nccl"
+    try:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(_free_port()))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        return "nccl"
+    except Exception as e:  # pragma: no cover - reported in the JSON line
+        return f"none ({type(e).__name__})"
+
+
+def launches_per_step(mode, n_streams):
+    # pyramid, worklist x2 (main + side stream), fast, nms, nms_finish, finalize;
+    # sat + describe x3 once per concurrent stream half; + propagate (mask
+    # modes), + binmask (binning)
+    return 7 + 4 * desc_halves(n_streams) + (1 if mode in ("intensity", "binning") else 0) + (
+        1 if mode == "binning" else 0)
+
+
+def run_detect(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1503_06959_b200.distributed import gather_stream_history
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    torch.cuda.set_device(local)
+    backend = init_process_group(world, local)
+    pg = dist.is_available() and dist.is_initialized()
+    cfg, n_total = config_of(args)
+    W, H = cfg.width, cfg.height
+    if n_total >= world:
+        streams = shard(n_total, rank, world)
+        scaling, ids = "strong", streams
+    else:   # fewer streams than GPUs (single-stream configs): independent replicas per rank
+        streams = list(range(n_total))
+        scaling, ids = "weak", [rank * n_total + s for s in streams]
+    S = len(streams)
+    Wm, K = args.warmup, args.steps
+    e2e_k = 0 if args.no_e2e else max(1, min(args.e2e_steps, K))
+    n_frames = Wm + K + e2e_k
+    dev = torch.device("cuda", local)
+    t0g = time.perf_counter()
+    if args.gen == "cpu":
+        frames = gen_frames_cpu(cfg, streams, n_frames, dev)
+    else:
+        frames = gen_frames_cuda(cfg, streams, n_frames, dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0g
+
+    eng = FeatureEngine(W, H, PipelineConfig(mask=MaskConfig(mode=args.mode)), n_streams=S)
+    hist = torch.zeros((S, Wm + K, 8), dtype=torch.float64, device=dev)
+    eng.set_history(hist)
+    stream = torch.cuda.current_stream()
+    for n in range(Wm):
+        eng.process(frames[n])
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device-resident inputs ----
+    step_bytes = S * W * H
+    flush = step_bytes <= L2_BYTES
+    flush_buf = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev) if flush else None
+    eng.set_timing(True)
+    eng.stage_ms()  # clear
+    if pg:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(1.0)  # let the samplers start
+        tw0 = time.time()
+        if flush:
+            # a step's inputs fit in L2: write 256 MB between steps, outside the events
+            evs = []
+            for n in range(Wm, Wm + K):
+                flush_buf.fill_(n & 255)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                eng.process(frames[n])
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            step_ms = [a.elapsed_time(b) for a, b in evs]
+            ms = float(sum(step_ms))
+        else:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            for n in range(Wm, Wm + K):
+                eng.process(frames[n])
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
+            step_ms = [ms / K] * K
+        tw1 = time.time()
+    clk.window(tw0, tw1)
+    if pg:
+        dist.barrier()
+    stage, n_steps = eng.stage_ms()
+    diag = eng.diag()
+    eng.set_timing(False)
+    eng.set_history(None)
+
+    # work of the timed frames from the device history (FrameReport rows)
+    h = hist.cpu().numpy()
+    ht = h[:, Wm:Wm + K]
+    k_det_l, k_tot_l = float(ht[:, :, 0].sum()), float(ht[:, :, 2].sum())
+    k_prop_l = float(ht[:, :, 1].sum())
+    cov_l = float(ht[:, :, 4].sum())
+    k_prev_l = float(h[:, Wm - 1:Wm + K - 1, 2].sum()) if (args.mode == "binning" and Wm >= 1) else 0.0
+    loc = torch.tensor([ms, k_det_l, k_tot_l, k_prop_l, cov_l, S * K, k_prev_l], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = loc.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        sm = loc.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, tot = float(mx[0]), sm.tolist()
+    else:
+        ms_max, tot = ms, loc.tolist()
+    _, k_det, k_tot, k_prop, cov_sum, frames_done, k_prev = tot
+    fps = frames_done / (ms_max / 1e3)
+
+    # ---- end-of-run per-stream statistics gather (NCCL all_gather) ----
+    t_g = time.perf_counter()
+    full = gather_stream_history(hist, ids, [0.0] * Wm + list(step_ms), max(n_total, S * world))
+    torch.cuda.synchronize()
+    gather_ms = 1e3 * (time.perf_counter() - t_g)
+    fs = full[:, Wm:].cpu().numpy()
+    stream_stats = {
+        "gathered_shape": list(full.shape), "backend": backend, "gather_ms": gather_ms,
+        "fields": ["stream", "n_detected", "n_propagated", "n_total", "n_dropped", "coverage", "frame",
+                   "n_survivors", "n_candidates", "step_ms"],
+        "features_per_frame_by_stream": {"min": float(fs[:, :, 3].mean(1).min()), "max": float(fs[:, :, 3].mean(1).max())},
+        "coverage_by_stream": {"min": float(fs[:, :, 5].mean(1).min()), "max": float(fs[:, :, 5].mean(1).max())},
+    }
+
+    # ---- e2e: public API with host buffers (H2D of frames + D2H of features inside) ----
+    e2e = None
+    if e2e_k:
+        host = frames[Wm + K:Wm + K + e2e_k].cpu().pin_memory()
+        h2d = S * H * W
+        out = eng.alloc_host(S * max(65536, W * H // 8))
+        d2h_total = 0
+        eng.submit(frames[Wm + K - 1].cpu().numpy())   # untimed warm-up of the pipelined path
+        eng.collect(out)
+        torch.cuda.synchronize()
+        if pg:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.submit(host[0].numpy())
+        for n in range(e2e_k):
+            if n + 1 < e2e_k:
+                eng.submit(host[n + 1].numpy())
+            eng.collect(out)
+            d2h_total += int(out["offsets"][S]) * (5 * 8 + 1 + 4 + 64)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
+        tt = torch.tensor([e2e_ms, S * e2e_k, float(d2h_total)], dtype=torch.float64, device=dev)
+        if world > 1:
+            m2 = tt.clone()
+            dist.all_reduce(m2[:1], op=dist.ReduceOp.MAX)
+            s2 = tt.clone()
+            dist.all_reduce(s2, op=dist.ReduceOp.SUM)
+            e2e_ms, e2e_frames, d2h_total = float(m2[0]), float(s2[1]), float(s2[2])
+        else:
+            e2e_frames = S * e2e_k
+        e2e = {"value": e2e_frames / (e2e_ms / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h_total / e2e_k),
+               "steps": e2e_k, "api": "vf_pipeline_submit (pinned frames, H2D) + vf_pipeline_collect (all features, "
+                                      "D2H to pinned), 2 steps in flight"}
+
+    if rank != 0:
+        eng.close()
+        if pg:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline (live CUDA events inside the timed region) ----
+    peak, peak_kind = hbm_peak()
+    b_alg, parts = algorithmic_bytes(W, H, frames_done, cov_sum, k_tot, k_prop, k_prev)
+    step_ms_avg = ms_max / K
+    step_achieved = b_alg / K / (step_ms_avg / 1e3) / 1e9
+    rho, top = layer_areas(W, H)
+    per_step = 1.0 / max(n_steps, 1)
+    # rank-0 shares of the per-kernel bytes (each rank times its own kernels)
+    share = S / max(frames_done / K, 1)
+    kbytes = {k: v / K * share for k, v in parts.items()}
+    overhead = {   # implementation traffic outside SURVEY 8(d)'s algorithmic bytes (per step, this rank)
+        "pyramid": W * H * (rho - top) * (S - cov_l / K),           # derived layers written outside active cells
+        "sat": 5.0 * 32 * 32 * diag["sat_tiles_built"],           # strip SAT: read 1 B + write 4 B per built pixel
+    }
+    if stage.get("describe", 0.0) <= 0 and stage.get("sat", 0.0) > 0:
+        stage = dict(stage)
+        stage["sat+describe"] = stage.pop("sat")
+        stage.pop("describe", None)
+        kbytes["sat+describe"] = kbytes.pop("describe", 0.0)
+        overhead["sat+describe"] = overhead.pop("sat")
+    kernels = []
+    for k, v in stage.items():
+        if v <= 0:
+            continue
+        ms_k = v * per_step
+        ach = kbytes.get(k, 0.0) / (ms_k / 1e3) / 1e9
+        row = {"kernel": k, "ms_per_step": ms_k, "share": ms_k / step_ms_avg,
+               "algorithmic_bytes": kbytes.get(k, 0.0), "achieved_gbs": ach, "frac": ach / peak}
+        if k in overhead:
+            row["overhead_bytes"] = overhead[k]
+        if k == "propagate":
+            row["stream"] = "side stream, overlapped with fast/nms (share = its duration / step)"
+        kernels.append(row)
+    kernels.sort(key=lambda r: -r["ms_per_step"])
+    traffic = None
+    tf = ROOT / "profiles" / f"r02_traffic_config{args.config}_{args.mode}.json"
+    if tf.exists():
+        try:
+            tj = json.loads(tf.read_text())
+            traffic = tj["dram_bytes_per_step"] * (S / tj.get("streams", S))
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s", "frac": step_achieved / peak,
+        "traffic": traffic, "kernel": "detect+describe step (all launches of one step)",
+        "algorithmic_bytes_per_step": b_alg / K,
+        "compulsory_bytes_per_step": (W * H * frames_done + 109.0 * k_tot) / K,
+        "bytes_model": "SURVEY.md 8(d): W*H*[1 + 2*top + 2*a*(rho - top)] + 109*(K_out + K_prop), K_out = |D_n|",
+        "traffic_source": (f"{tf.relative_to(ROOT)}: sum of ncu dram__bytes_read+write over one step's launches"
+                           if traffic is not None else None),
+        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
+        "dominant_kernel": kernels[0] if kernels else None,
+        "kernels": kernels,
+        "work_last_step": diag,
+    }
+
+    # ---- CPU baseline: oracle port on the host cores, bounded sample (rank 0, N = 1) ----
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        n_str = min(S, threads)
+        nf = min(4, Wm + K)  # frame 0 (full detection) + masked frames per sampled stream
+        sample = [frames[:nf, j].cpu().numpy() for j in range(n_str)]
+        n_cpu, dt = cpu_run(sample, args.mode, threads)
+        cpu = {"value": n_cpu / dt, "unit": "frames/s", "cores": n_str, "kind": "port",
+               "sample": f"{n_str} streams x {nf} frames (frame 0 full detection + {nf - 1} masked) of the "
+                         f"bench workload, C oracle one thread per stream on {cpu_model()}"}
+
+    lat = sorted(step_ms)
+    line = {
+        "metric": "frames/sec (detect+describe)", "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": Wm, "ms_per_step": step_ms_avg, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": workload_name(args, cfg, n_total), "config": args.config, "mode": args.mode,
+                   "width": W, "height": H, "streams_total": n_total, "streams_per_rank": S,
+                   "sharding": "contiguous streams per rank" if scaling == "strong" else "replicas (one stream)",
+                   "frames": (f"{args.gen} scene generator" + (" (same bytes as --impl reference and the parity tests)"
+                                                               if args.gen == "cpu" else "")),
+                   "frame_gen_s": gen_s,
+                   "l2": ("inputs fit in L2: 256 MB written between steps, outside the per-step CUDA events"
+                          if flush else "inputs larger than L2: every step reads a fresh batch of frames")},
+        "mpix_per_sec": fps * W * H / 1e6,
+        "latency_ms": {"p50": lat[len(lat) // 2], "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))],
+                       "per": "step (one frame of every local stream)"},
+        "features_per_frame": k_tot / max(frames_done, 1),
+        "detected_per_frame": (k_tot - k_prop) / max(frames_done, 1),
+        "mean_coverage": cov_sum / max(frames_done, 1),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "stream_stats": stream_stats,
+        "gpu_launches": launches_per_step(args.mode, S) * K,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    eng.close()
+    if pg:
+        dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------
@@ -701,7 +1107,7 @@ def run_dump(args):
     from paper_1503_06959_b200.report import format_features
     from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
 
-    streams = list(range(min(args.streams, 64)))
+    streams = list(range(min(args.streams or TOTAL_STREAMS, 64)))
     frames = gen_frames(streams, 3, torch.device("cuda", 0))
     eng = FeatureEngine(W_FR, H_FR, PipelineConfig(mask=MaskConfig(mode="intensity")), n_streams=len(streams))
     for n in range(3):
@@ -769,222 +1175,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    import torch
-    import torch.distributed as dist
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1503_06959_b200.engine import FeatureEngine
-    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
-
-    streams = shard(args.streams, rank, world)
-    S = len(streams)
-    W, K = args.warmup, args.steps
-    e2e_k = 0 if args.no_e2e else max(1, min(args.e2e_steps, K))
-    n_frames = W + K + e2e_k
-    dev = torch.device("cuda", local)
-    frames = gen_frames(streams, n_frames, dev)
-    torch.cuda.synchronize()
-
-    cfg = PipelineConfig(mask=MaskConfig(mode=args.mode))
-    eng = FeatureEngine(W_FR, H_FR, cfg, n_streams=S)
-    stream = torch.cuda.current_stream()
-    for n in range(W):
-        eng.process(frames[n])
-    torch.cuda.synchronize()
-    t_before = np.array([eng.totals(s) for s in range(S)])
-
-    # ---- timed region: K steps, device-resident inputs ----
-    eng.set_timing(True)
-    eng.stage_ms()  # clear
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        time.sleep(1.0)  # let nvidia-smi start sampling
-        tw0 = time.time()
-        ev0.record(stream)
-        for n in range(W, W + K):
-            eng.process(frames[n])
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        tw1 = time.time()
-    clk.window(tw0, tw1)
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    stage, n_steps = eng.stage_ms()
-    diag = eng.diag()
-    eng.set_timing(False)
-    t_after = np.array([eng.totals(s) for s in range(S)])
-    d = t_after - t_before  # per stream: sum n_det, sum n_total, sum coverage, frames
-    # per-rank stats -> max time over ranks, summed work
-    loc = torch.tensor([ms, d[:, 0].sum(), d[:, 1].sum(), d[:, 2].sum(), d[:, 3].sum()], dtype=torch.float64,
-                       device=dev)
-    if world > 1:
-        mx = loc.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        sm = loc.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max = float(mx[0])
-        tot = sm.tolist()
-    else:
-        ms_max = ms
-        tot = loc.tolist()
-    frames_done = tot[4]
-    fps = frames_done / (ms_max / 1e3)
-
-    # ---- e2e: public API with host buffers (H2D of frames + D2H of features inside) ----
-    # Per step: vf_process_host (pinned host frames -> device, the whole path)
-    # then vf_fetch_features (device-side pack of every stream's features, one
-    # D2H copy per field into pinned host arrays).
-    e2e = None
-    if e2e_k:
-        host = frames[W + K:W + K + e2e_k].cpu().pin_memory()
-        h2d = S * H_FR * W_FR
-        out = eng.alloc_host(S * 65536)
-        d2h_total = 0
-        # untimed warm-up of the pipelined path (stream / buffer creation)
-        eng.submit(frames[W + K - 1].cpu().numpy())
-        eng.collect(out)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        # pipelined: H2D of step n+1 and D2H of step n-1 overlap step n's compute
-        eng.submit(host[0].numpy())
-        for n in range(e2e_k):
-            if n + 1 < e2e_k:
-                eng.submit(host[n + 1].numpy())
-            eng.collect(out)
-            d2h_total += int(out["offsets"][S]) * (5 * 8 + 1 + 4 + 64)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
-        tt = torch.tensor([e2e_ms, S * e2e_k, float(d2h_total)], dtype=torch.float64, device=dev)
-        if world > 1:
-            m2 = tt.clone()
-            dist.all_reduce(m2[:1], op=dist.ReduceOp.MAX)
-            s2 = tt.clone()
-            dist.all_reduce(s2, op=dist.ReduceOp.SUM)
-            e2e_ms, e2e_frames, d2h_total = float(m2[0]), float(s2[1]), float(s2[2])
-        else:
-            e2e_frames = S * e2e_k
-        e2e = {"value": e2e_frames / (e2e_ms / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h_total / e2e_k),
-               "steps": e2e_k, "api": "vf_pipeline_submit (pinned frames, H2D) + vf_pipeline_collect (all features, D2H to pinned), "
-                      "2 steps in flight"}
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline (live CUDA events inside the timed region) ----
-    # The path is one step of 9 launches; SURVEY.md 8(d)'s algorithmic bytes are
-    # defined per frame for the whole path, so the primary roofline is the step:
-    # B_alg(step) / step time.  Each kernel is also listed with its own byte
-    # model and live average launch time.
-    peak, peak_kind = hbm_peak()
-    k_out = tot[1]
-    k_total = tot[2]
-    cov_sum = tot[3]
-    b_alg = algorithmic_bytes(frames_done, cov_sum, k_out, k_total - k_out)
-    step_ms = ms_max / K
-    step_achieved = b_alg / K / (step_ms / 1e3) / 1e9
-    f_loc = d[:, 3].sum()
-    det_loc, tot_loc = d[:, 0].sum(), d[:, 1].sum()
-    wh = W_FR * H_FR
-    per_step = 1.0 / max(n_steps, 1)
-    kbytes = {   # algorithmic bytes per step of each kernel (this rank)
-        "pyramid": (wh * (1 + 0.918) + 2 * wh / 64.0) * f_loc * per_step,
-        "fast": 2.0 * 1024 * diag["fast_tiles_active"],
-        "nms": 1.0 * 1024 * diag["fast_tiles_active"] + 32.0 * det_loc * per_step,
-        "sat": 5.0 * 32 * 32 * diag["sat_tiles_built"],   # read 1 B + write 4 B per pixel of a built 32x32 tile
-        "describe": (32.0 + 109.0) * det_loc * per_step,
-        "propagate": 218.0 * (tot_loc - det_loc) * per_step,
-    }
-    if stage.get("describe", 0.0) <= 0 and stage.get("sat", 0.0) > 0:
-        # SAT and describe run as concurrent stream halves: one timed interval
-        stage = dict(stage)
-        stage["sat+describe"] = stage.pop("sat")
-        stage.pop("describe", None)
-        kbytes["sat+describe"] = kbytes["sat"] + kbytes["describe"]
-    kernels = []
-    for k, v in stage.items():
-        if v <= 0:
-            continue
-        ms_k = v / max(n_steps, 1)
-        ach = kbytes.get(k, 0.0) / (ms_k / 1e3) / 1e9 if ms_k > 0 else 0.0
-        row = {"kernel": k, "ms_per_step": ms_k, "share": ms_k / (ms_max / K),
-               "algorithmic_bytes": kbytes.get(k, 0.0), "achieved_gbs": ach, "frac": ach / peak}
-        if k == "propagate":
-            row["stream"] = "side stream, overlapped with fast/nms (share = its duration / step)"
-        kernels.append(row)
-    kernels.sort(key=lambda r: -r["ms_per_step"])
-    traffic = None
-    tf = ROOT / "profiles" / "r01g_traffic.json"
-    if tf.exists():
-        try:
-            tj = json.loads(tf.read_text())
-            traffic = tj["dram_bytes_per_step"] * (S / tj.get("streams", S))
-        except Exception:
-            traffic = None
-    roofline = {
-        "bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s", "frac": step_achieved / peak,
-        "traffic": traffic, "kernel": "detect+describe step (all launches of one step)",
-        "algorithmic_bytes_per_step": b_alg / K,
-        "traffic_source": "profiles/r01g_traffic.json: sum of ncu dram__bytes_read+write over one step's launches (cold-cache replays)"
-                          if traffic is not None else None,
-        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else "fallback",
-        "dominant_kernel": kernels[0] if kernels else None,
-        "kernels": kernels,
-        "work_last_step": diag,
-    }
-
-    # ---- CPU baseline: oracle port on the host cores, bounded sample (rank 0, N = 1) ----
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        threads = host_threads()
-        n_str = min(S, threads)
-        nf = 4  # frame 0 (full detection) + 3 masked frames per sampled stream
-        sample = [frames[:nf, j].cpu().numpy() for j in range(n_str)]
-        n_cpu, dt = cpu_run(sample, args.mode, threads)
-        cpu = {"value": n_cpu / dt, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"{n_str} streams x {nf} frames (frame 0 full detection + {nf - 1} masked) of the "
-                         f"bench workload, C oracle one thread per stream on {cpu_model()}"}
-
-    line = {
-        "metric": "frames/sec (detect+describe)", "value": fps, "unit": "frames/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"config5: {args.streams} x 1920x1080 uint8 streams (static/pan/objects), "
-                               f"mode {args.mode}, t=55, O=4, t_i=20",
-                   "streams_total": args.streams, "streams_per_rank": S, "sharding": "contiguous streams per rank",
-                   "l2": "inputs larger than L2: every step reads a fresh batch of frames (no re-use)"},
-        "mpix_per_sec": fps * W_FR * H_FR / 1e6,
-        "features_per_frame": k_total / max(frames_done, 1),
-        "detected_per_frame": k_out / max(frames_done, 1),
-        "mean_coverage": cov_sum / max(frames_done, 1),
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        # per step: pyramid, worklist x2, fast, nms, nms_finish, finalize, and sat + describe x3
-        # once per concurrent stream half (VF_DESC_PAR, default 2 when >= 2 streams)
-        # (+ propagate in the mask modes, + binmask in binning mode)
-        "gpu_launches": (7 + 4 * desc_halves(S) + (1 if args.mode == "binning" else 0)
-                         + (1 if args.mode != "none" else 0)) * K,
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    run_detect(args, rank, world, local)
 
 
 if __name__ == "__main__":

@@ -157,6 +157,13 @@ int vf_get_stage_ms(vf_ctx *ctx, double *ms9, int32_t *n_steps, void *stream);
  * total FAST tiles, SAT tiles built, total SAT tiles, unmasked streams,
  * staged NMS candidates, bands per stream, feature capacity. */
 int vf_get_diag(vf_ctx *ctx, int64_t *out8, void *stream);
+/* Per-frame statistics history: every later step also writes, on the device,
+ * stream s's FrameReport row of frame f (f < max_frames) to
+ * hist_dev[(s * max_frames + f) * 8 + k], k = n_detected, n_propagated,
+ * n_total, n_dropped, coverage, frame, n_survivors, n_candidates (fp64).  The
+ * caller owns hist_dev ([max_streams][max_frames][8] doubles); max_frames = 0
+ * turns it off.  Used for the end-of-run per-stream statistics gather. */
+int vf_set_history(vf_ctx *ctx, double *hist_dev, int32_t max_frames);
 /* Per-stream totals since vf_create/vf_reset: sum n_detected, sum n_total, sum coverage, frames. */
 int vf_get_totals(vf_ctx *ctx, int s, double *out4, void *stream);
 

@@ -594,6 +594,14 @@ int vf_get_stage_ms(vf_ctx* c, double* ms7, int* n_steps, void* stream)  /* ms7:
   return VF_OK;
 }
 
+int vf_set_history(vf_ctx* c, double* hist_dev, int32_t max_frames)
+{
+  if (!c || max_frames < 0 || (max_frames > 0 && !hist_dev)) return VF_ERR_ARG;
+  c->b.hist = max_frames > 0 ? hist_dev : nullptr;
+  c->b.hist_frames = max_frames;
+  return VF_OK;
+}
+
 int vf_reset(vf_ctx* c, void* stream)
 {
   if (!c) return VF_ERR_ARG;

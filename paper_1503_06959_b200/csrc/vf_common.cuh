@@ -128,6 +128,7 @@ struct Bufs {
   unsigned long long* cov;  // [S] covered full-res pixels of this frame
   double* report;       // [S][8]: n_det, n_prop, n_total, n_dropped, coverage, frame, n_surv, n_cand
   int* worklist; int* work_count;  // [S][tiles_per_stream] / [S]: active FAST tiles per stream
+  double* hist; int hist_frames;  // optional [S][hist_frames][8]: report rows of every frame (vf_set_history)
 };
 
 // --------------------------------------------------------------------------

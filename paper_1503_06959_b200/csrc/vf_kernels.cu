@@ -2204,6 +2204,12 @@ __global__ void k_finalize(const __grid_constant__ Geo g, const __grid_constant_
     const int s = b.s0 + sl;
     int* ctr = b.ctr + s * C_NCTR;
     const int cur = ctr[C_FRAME] & 1;
+    if (b.hist && ctr[C_FRAME] < b.hist_frames) {   // per-frame FrameReport history (end-of-run gather)
+      const double* rp = b.report + (long long)s * 16;
+      double* h = b.hist + ((long long)s * b.hist_frames + ctr[C_FRAME]) * 8;
+#pragma unroll
+      for (int k = 0; k < 8; k++) h[k] = rp[k];
+    }
     ctr[C_NFEAT0 + cur] = ctr[C_NTOTAL];
     ctr[C_FRAME] += 1;
     ctr[C_EPOCH] += 1;

@@ -57,3 +57,41 @@ def gather_stats(local: np.ndarray, n_streams_total: int, device=None) -> np.nda
         full = full[full[:, 0, 0] >= 0] if full.shape[1] else full
     order = np.argsort(full[:, 0, 0], kind="stable") if full.shape[1] else np.arange(full.shape[0])
     return full[order]
+
+
+HIST_FIELDS = ("n_detected", "n_propagated", "n_total", "n_dropped", "coverage", "frame", "n_survivors",
+               "n_candidates")
+
+
+def gather_stream_history(hist, stream_ids, step_ms, n_streams_total: int):
+    """End-of-run statistics gather on the device (the path's one collective).
+
+    hist: this rank's [S_local, F, 8] float64 CUDA tensor filled by
+    FeatureEngine.set_history; step_ms: [F] per-frame device step times of this
+    rank.  Returns [n_streams_total, F, 10] (stream id, the 8 HIST_FIELDS, ms)
+    ordered by stream id, on every rank.  One all_gather over the process
+    group's backend (NCCL over NVLink on the GPU box, gloo in CPU tests)."""
+    import torch
+    import torch.distributed as dist
+
+    S, F = hist.shape[0], hist.shape[1]
+    ids = torch.as_tensor(list(stream_ids), dtype=torch.float64, device=hist.device)
+    ms = torch.as_tensor(step_ms, dtype=torch.float64, device=hist.device).reshape(1, F, 1).expand(S, F, 1)
+    local = torch.cat([ids.view(S, 1, 1).expand(S, F, 1), hist, ms], 2)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        full = local
+        if dist.is_available() and dist.is_initialized():
+            outs = [torch.empty_like(local)]
+            dist.all_gather(outs, local)
+            full = outs[0]
+    else:
+        world = dist.get_world_size()
+        max_local = -(-n_streams_total // world)
+        pad = torch.full((max_local, F, 10), -1.0, dtype=torch.float64, device=hist.device)
+        pad[:S] = local
+        outs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(outs, pad)
+        full = torch.cat(outs, 0)
+        full = full[full[:, 0, 0] >= 0] if F else full
+    order = torch.argsort(full[:, 0, 0], stable=True) if F else torch.arange(full.shape[0], device=full.device)
+    return full[order]

@@ -195,6 +195,23 @@ class FeatureEngine:
 
     STAGES = ("binmask", "pyramid", "worklist", "fast", "nms", "sat", "describe", "propagate", "finalize")
 
+    def set_history(self, hist=None) -> None:
+        """Record every later frame's FrameReport row on the device into `hist`
+        (a CUDA float64 tensor [n_streams, max_frames, 8]: n_detected,
+        n_propagated, n_total, n_dropped, coverage, frame, n_survivors,
+        n_candidates); None turns it off.  No host synchronization per frame."""
+        import torch
+
+        if hist is None:
+            _native.check(_native.lib().vf_set_history(self._h, None, 0))
+            self._hist = None
+            return
+        if (hist.dtype != torch.float64 or not hist.is_cuda or hist.dim() != 3 or hist.shape[0] != self.n_streams
+                or hist.shape[2] != 8 or not hist.is_contiguous()):
+            raise ValueError("history must be a contiguous CUDA float64 tensor [n_streams, max_frames, 8]")
+        self._hist = hist   # keep the buffer alive while the library writes into it
+        _native.check(_native.lib().vf_set_history(self._h, hist.data_ptr(), int(hist.shape[1])))
+
     def set_timing(self, enable: bool) -> None:
         _native.check(_native.lib().vf_set_timing(self._h, int(enable)))
 

@@ -1,49 +1,48 @@
-"""Per-CUDA-line summary of an ncu report's source page (cuda,sass view):
-instructions executed and warp-stall samples aggregated per source line.
+"""Pivot an ncu --metrics --csv launch list into one line per launch.
 
-    python tools/ncu_lines.py REPORT.ncu-rep KERNEL_REGEX [TOP]
-"""
+    python tools/ncu_lines.py FILE.csv [--md]
+Columns: id, kernel, us, DRAM read MB, DRAM write MB, SM thr %, warp inst (M), L2 hit %, warps active %."""
 import csv
-import io
-import subprocess
 import sys
 
+COLS = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "rd MB"), ("dram__bytes_write.sum", "wr MB"),
+        ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"), ("smsp__inst_executed.sum", "Minst"),
+        ("lts__t_sector_hit_rate.pct", "L2 hit %"), ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps %")]
+SCALE = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "%": 1.0,
+         "inst": 1e-6, "": 1.0}
 
-def main():
-    rep, kern = sys.argv[1], sys.argv[2]
-    top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                          "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    agg = {}
-    fname = "?"
-    hdr = None
-    tot_i = tot_s = 0
+
+def load(path):
+    rows = list(csv.reader(open(path)))
+    h, launches = None, {}
     for r in rows:
-        if len(r) >= 2 and r[0] == "File Path":
-            fname = r[1].rsplit("/", 1)[-1]
+        if r and r[0] == "ID":
+            h = r
             continue
-        if len(r) > 3 and r[0] == "Line No":
-            hdr = r
+        if not h or len(r) != len(h):
             continue
-        if hdr is None or len(r) < len(hdr) - 1:
+        i = int(r[h.index("ID")])
+        d = launches.setdefault(i, {"kernel": r[h.index("Kernel Name")].split("(")[0]})
+        name, unit = r[h.index("Metric Name")], r[h.index("Metric Unit")]
+        try:
+            v = float(r[h.index("Metric Value")].replace(",", ""))
+        except ValueError:
             continue
-        if r[0]:   # a CUDA line row carries the line's aggregate
-            try:
-                ins = int(r[hdr.index("Instructions Executed")])
-                smp = int(r[hdr.index("Warp Stall Sampling (All Samples)")])
-            except (ValueError, IndexError):
-                continue
-            key = (fname, int(r[0]))
-            a = agg.setdefault(key, [0, 0, r[1].strip()[:90]])
-            a[0] += ins
-            a[1] += smp
-            tot_i += ins
-            tot_s += smp
-    print(f"total warp-instructions {tot_i:,}  stall samples {tot_s:,}")
-    for (f, ln), (ins, smp, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
-        print(f"{f}:{ln:5d}  inst {100.0 * ins / max(tot_i, 1):5.1f}%  samp {100.0 * smp / max(tot_s, 1):5.1f}%  {src}")
+        d[name] = v * SCALE.get(unit, 1.0)
+    return launches
 
 
 if __name__ == "__main__":
-    main()
+    L = load(sys.argv[1])
+    md = "--md" in sys.argv
+    hdr = ["id", "kernel"] + [c[1] for c in COLS]
+    print(("| " + " | ".join(hdr) + " |") if md else "  ".join(hdr))
+    if md:
+        print("|" + "---|" * len(hdr))
+    tot = 0.0
+    for i in sorted(L):
+        d = L[i]
+        vals = [f"{d.get(m, float('nan')):.1f}" for m, _ in COLS]
+        tot += d.get("gpu__time_duration.sum", 0.0)
+        print(("| " + " | ".join([str(i), d["kernel"]] + vals) + " |") if md else f"{i:3d} {d['kernel']:16s} " + " ".join(f"{v:>8s}" for v in vals))
+    print(f"total us {tot:.1f}")
