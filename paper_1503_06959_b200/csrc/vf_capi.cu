@@ -115,6 +115,7 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   double sc[VF_MAXL];
   int rc = layer_dims(c.width, c.height, c.n_octaves, ws, hs, sc);
   if (rc) return rc;
+  if (c.width > 8192) return VF_ERR_ARG;   // NMS candidate encoding: x < 2^13
   g.W = c.width; g.H = c.height; g.O = c.n_octaves; g.NL = 2 * c.n_octaves;
   g.threshold = c.threshold;
   g.mask_mode = c.mask_mode;
@@ -129,7 +130,7 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   if (c.mask_mode == 1 && (g.mask_level < 0 || g.mask_level >= g.O)) return VF_ERR_OCTAVE_KEY;
   g.t_i = c.t_i; g.t_h = c.t_h;
   long long lay = 0, smo = 0, bmo = 0;
-  int tb = 0, bb = 0;
+  int tb = 0, bb = 0, rb = 0;
   for (int l = 0; l < g.NL; l++) {
     LayerGeo& L = g.L[l];
     L.w = ws[l]; L.h = hs[l];
@@ -140,12 +141,13 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
     L.tiles_x = cdiv(L.w, VF_TILE_W); L.tiles_y = cdiv(L.h, VF_TILE_H);
     L.tile_base = tb; tb += L.tiles_x * L.tiles_y;
     L.band_base = bb; bb += L.tiles_y;
+    L.row_base = rb; rb += L.h;
     L.bm_words = cdiv(L.w, 32);
     if (l >= 1) { L.layer_off = lay; lay += align_up((long long)L.pitch * L.h, 256); }
     L.sm_off = smo; smo += align_up((long long)L.pitch * L.h + 16, 256);
     L.bm_off = bmo; bmo += align_up((long long)L.bm_words * L.h, 64);
   }
-  g.tiles_per_stream = tb; g.bands_per_stream = bb;
+  g.tiles_per_stream = tb; g.bands_per_stream = bb; g.rows_per_stream = rb;
   g.layer_slab = std::max(lay, 256LL); g.sm_slab = smo; g.bm_slab_words = bmo;
   // mask grids (masking.py:139-148 cell geometry; binning masking.py:132-136)
   long long co = 0;
@@ -217,6 +219,17 @@ int pyramid_smem(const Geo& g)
 }
 
 int g_num_sms = 0;
+
+// NMS units per band for a batch of n streams: one warp per band (8 rows) when
+// the batch has enough bands to fill every SM many times over, else split
+// bands into 1-4-row units so single-stream frames get more warps.
+int nms_units(const Geo& g, int n)
+{
+  const long long bands = (long long)g.bands_per_stream * n, want = 32LL * (g_num_sms > 0 ? g_num_sms : 148);
+  int u = 1;
+  while (u < VF_TILE_H && bands * u < want) u *= 2;
+  return u;
+}
 
 int cuda_status(cudaError_t e)
 {
@@ -418,8 +431,9 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.bitmaps = A.get<uint32_t>((size_t)S * g.bm_slab_words);
   b.tile_stamp = A.get<int>((size_t)S * g.tiles_per_stream);
   b.band_stamp = A.get<int>((size_t)S * g.bands_per_stream);
-  b.band_rec = A.get<int>((size_t)S * g.bands_per_stream * 4);
-  b.band_out = A.get<int>((size_t)S * g.bands_per_stream);
+  b.unit_rec = A.get<int>((size_t)S * g.bands_per_stream * VF_TILE_H * 4);
+  b.unit_out = A.get<int>((size_t)S * g.bands_per_stream * VF_TILE_H);
+  b.nms_u = 1;
   b.band_cand = A.get<int>((size_t)S * g.bands_per_stream);
   b.gidx = A.get<int>((size_t)S * cap);
   b.prop_cnt = A.get<int>((size_t)S * g.prop_chunks);
@@ -673,7 +687,8 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n);
   stage_mark(c, 4, st);
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
-  k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
+  b.nms_u = nms_units(g, n);
+  k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b);
   stage_mark(c, 5, st);
   // SAT + describe of two stream halves on concurrent high-priority streams:
@@ -1242,7 +1257,7 @@ int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, c
   L.w = w; L.h = h; L.pitch = (int)align_up(w, 16); L.scale = 1.0; L.sigma = 1.0;
   L.rinv_h = 1.0 / h; L.rinv_w = 1.0 / w;
   L.tiles_x = cdiv(w, VF_TILE_W); L.tiles_y = cdiv(h, VF_TILE_H); L.bm_words = cdiv(w, 32);
-  g.tiles_per_stream = L.tiles_x * L.tiles_y; g.bands_per_stream = L.tiles_y;
+  g.tiles_per_stream = L.tiles_x * L.tiles_y; g.bands_per_stream = L.tiles_y; g.rows_per_stream = h;
   g.sm_slab = align_up((long long)L.pitch * h + 16, 256); g.bm_slab_words = (long long)L.bm_words * h;
   std::vector<int> lut;
   if (mask_dev) {
@@ -1293,9 +1308,9 @@ int vf_score_map(const uint8_t* layer_dev, int w, int h, int64_t pitch, int t, c
 __global__ void k_gather_kps(const __grid_constant__ Geo g, const __grid_constant__ Bufs b, double* x, double* y,
                              double* s, double* v, int cap)
 {
-  const int bid = blockIdx.x;
-  const int* rec = b.band_rec + bid * 4;
-  const int kept = rec[1], base = rec[0], o = b.band_out[bid];
+  const int rid = blockIdx.x;
+  const int* rec = b.unit_rec + rid * 4;
+  const int kept = rec[1], base = rec[0], o = b.unit_out[rid];
   for (int i = threadIdx.x; i < kept; i += blockDim.x) {
     if (o + i >= cap) break;
     x[o + i] = b.st_x[base + i]; y[o + i] = b.st_y[base + i]; s[o + i] = b.st_s[base + i]; v[o + i] = b.st_v[base + i];
@@ -1324,9 +1339,10 @@ int vf_nms_refine(const uint8_t* const* maps_dev, const int64_t* pitches, int W,
   cudaMemcpyAsync(b.tile_stamp, ones.data(), sizeof(int) * g.tiles_per_stream, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.band_stamp, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(b.band_cand, ones.data(), sizeof(int) * g.bands_per_stream, cudaMemcpyHostToDevice, st);
-  k_nms<<<dim3(cdiv(g.bands_per_stream, NMS_WARPS), 1), NMS_THREADS, 0, st>>>(g, b);
+  b.nms_u = VF_TILE_H;
+  k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), 1), NMS_THREADS, 0, st>>>(g, b);
   k_nms_finish<<<1, NF_THREADS, 0, st>>>(g, b);
-  k_gather_kps<<<g.bands_per_stream, 128, 0, st>>>(g, b, x_dev, y_dev, sigma_dev, score_dev, cap);
+  k_gather_kps<<<g.bands_per_stream * b.nms_u, 128, 0, st>>>(g, b, x_dev, y_dev, sigma_dev, score_dev, cap);
   int ctr[C_NCTR];
   cudaMemcpyAsync(ctr, b.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st);
   rc = cuda_status(cudaStreamSynchronize(st));

@@ -45,6 +45,7 @@ struct LayerGeo {
   int tiles_x, tiles_y; // FAST tiles
   int tile_base;        // first tile id of this layer within a stream
   int band_base;        // first band id (== tile row) of this layer
+  int row_base;         // first NMS row id of this layer (rows of all layers, layer order)
   int bm_words;         // candidate-bitmap words per row
   long long layer_off;  // byte offset of the derived layer in the layer slab (l >= 1)
   long long sm_off;     // byte offset of the score map in the score slab
@@ -70,7 +71,7 @@ struct Geo {
   int n_grids;
   GridGeo grid[VF_MAXG];
   LayerGeo L[VF_MAXL];
-  int tiles_per_stream, bands_per_stream;
+  int tiles_per_stream, bands_per_stream, rows_per_stream;
   long long layer_slab, sm_slab, bm_slab_words, cell_slab, lut_len;
   // pyramid tiles (kernel k_pyramid), also the SAT tiles
   int ptw, pth, ptx, pty;   // pyramid tiles (o0 pixels)
@@ -100,8 +101,9 @@ struct Bufs {
   uint32_t* bitmaps;    // [S][bm_slab_words]
   int* tile_stamp;      // [S][tiles_per_stream]
   int* band_stamp;      // [S][bands_per_stream]
-  int* band_rec;        // [S][bands_per_stream][4]: staging base, kept, border-ok, dropped
-  int* band_out;        // [S][bands_per_stream]: output offset of the band's kept keypoints
+  int nms_u;            // NMS units per band (1, 2, 4 or 8): a unit is VF_TILE_H / nms_u rows
+  int* unit_rec;        // [S][bands_per_stream * nms_u][4]: staging base, kept, border-ok, dropped per NMS unit
+  int* unit_out;        // [S][bands_per_stream * nms_u]: output offset of the unit's kept keypoints
   int* band_cand;       // [S][bands_per_stream]: FAST candidates of the band this step
   int* gidx;            // [S][kp_cap]: detected rank -> staging slot
   int* prop_cnt;        // [S][prop_chunks]

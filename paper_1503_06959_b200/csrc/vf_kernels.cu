@@ -402,14 +402,15 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
   int* pre = reinterpret_cast<int*>(smem + SAT_WARPS * VF_ST * SAT_PITCH * 4);
   __shared__ int sm_warp[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // detected rank -> staging slot map for k_desc_sample (thread per band)
-  for (long long il = (long long)blockIdx.x * blockDim.x + threadIdx.x; il < (long long)n_streams * g.bands_per_stream;
+  // detected rank -> staging slot map for k_desc_sample (thread per NMS unit)
+  const int nu = g.bands_per_stream * b.nms_u;
+  for (long long il = (long long)blockIdx.x * blockDim.x + threadIdx.x; il < (long long)n_streams * nu;
        il += (long long)gridDim.x * blockDim.x) {
-    const int s = b.s0 + (int)(il / g.bands_per_stream);
-    const long long i = (long long)b.s0 * g.bands_per_stream + il;
-    const int4 r = __ldcg(reinterpret_cast<const int4*>(b.band_rec) + i);
+    const int s = b.s0 + (int)(il / nu);
+    const long long i = (long long)b.s0 * nu + il;
+    const int4 r = __ldcg(reinterpret_cast<const int4*>(b.unit_rec) + i);
     if (r.y > 0) {
-      const int o = __ldcg(b.band_out + i);
+      const int o = __ldcg(b.unit_out + i);
       int* gidx = b.gidx + (long long)s * g.kp_cap;
       for (int k = 0; k < r.y && o + k < g.kp_cap; k++) gidx[o + k] = r.x + k;
     }
@@ -1472,41 +1473,54 @@ __device__ __forceinline__ int block_excl_scan(int v, int& total, int* sm)
 }
 
 
-// One warp per band (8 rows of one layer).  Candidates come from the FAST
-// bitmap: lane l owns a contiguous run of bitmap words, so a warp scan gives
-// every candidate its row-major rank.  Candidates are processed 32 at a time
-// (lane = candidate) and the kept ones are compacted in rank order with
-// ballots, so each band emits keypoints in (y, x) order and bands are ordered
-// (layer, y): the reference order.
+// Warp per NMS unit: R consecutive rows of a band (R = VF_TILE_H / b.nms_u;
+// R = 8 when many streams fill the GPU, fewer rows per warp for single-stream
+// batches so more warps share the work).  The unit's FAST bitmap words are
+// walked 32 at a time in row-major order, one word per lane: a warp scan of
+// the popcounts gives every candidate its rank and the lanes write their
+// candidates (row, x) into a per-warp list.  The list is tested 32 at a time
+// (lane = candidate: strict 3x3 + cross-layer), survivors are queued FIFO and
+// refined 32 at a time (fp64), and kept keypoints are compacted with ballots,
+// so each unit emits its keypoints in (y, x) order and units are ordered
+// (layer, y): the reference order (detector.py:251-253,303-306).
 #define NMS_WARPS 4
 #define NMS_THREADS (32 * NMS_WARPS)
+#define NMS_LIST (1024 + 32)   // candidates of 32 bitmap words + an untested remainder
 __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
-  __shared__ int cand[NMS_WARPS][32];
-  __shared__ int sq[NMS_WARPS][64];   // survivor queue (y << 16 | x)
-  const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int bid = blockIdx.x * NMS_WARPS + wid;
-  if (bid >= g.bands_per_stream) return;
+  // (row offset << 13) | x as 16 bits (x < 8192, row offset < 8): a small
+  // footprint leaves the L1 to the score-map reads
+  __shared__ uint16_t cand[NMS_WARPS][NMS_LIST];
+  __shared__ uint16_t sq[NMS_WARPS][64];      // survivor queue, same encoding
+  const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int U = b.nms_u, R = VF_TILE_H / U;
+  const int unit = blockIdx.x * NMS_WARPS + w;
+  if (unit >= g.bands_per_stream * U) return;
+  const int bid = unit / U, sub = unit - bid * U;
+  int4* rec = reinterpret_cast<int4*>(b.unit_rec) + ((long long)s * g.bands_per_stream * U + unit);
   const int epoch = stream_epoch(b, s);
-  const int um = use_mask(g, b, s) ? epoch : 0;   // nonzero: tile-stamp gating at this epoch
-  int* ctr = b.ctr + s * C_NCTR;
   int kept = 0, n_ok = 0, n_drop = 0, base = 0;
   if (b.band_stamp[(long long)s * g.bands_per_stream + bid] == epoch &&
       __ldcg(b.band_cand + (long long)s * g.bands_per_stream + bid) > 0) {
+    const int um = use_mask(g, b, s) ? epoch : 0;
+    int* ctr = b.ctr + s * C_NCTR;
     int l = 0;
     while (l + 1 < g.NL && bid >= g.L[l + 1].band_base) l++;
     const LayerGeo& Lg = g.L[l];
-    const int ty = bid - Lg.band_base;
-    const int y0 = ty * VF_TILE_H, nrows = min(Lg.h - y0, VF_TILE_H);
-    const int nwords = nrows * Lg.bm_words;
-    const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)y0 * Lg.bm_words;
-    const int per = (nwords + 31) / 32;
-    const int w0 = lane * per, w1 = min(nwords, w0 + per);
-    const int bmw = Lg.bm_words;
-    int cnt = 0;
-    for (int i = w0; i < w1; i++) cnt += __popc(__ldg(bm + i));   // inactive tiles hold zero words
-    int total;
-    const int ex = warp_excl_scan(cnt, lane, total);
+    const int ys = (bid - Lg.band_base) * VF_TILE_H + sub * R;
+    const int nrows = max(0, min(Lg.h - ys, R));
+    const int bmw = Lg.bm_words, nw = nrows * bmw;
+    const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)ys * bmw;
+    // candidates of the unit: the band's count from k_fast when the unit is the
+    // whole band, else the popcount of the unit's words (inactive tiles hold zero words)
+    int total = 0;
+    if (U == 1) {
+      total = __ldcg(b.band_cand + (long long)s * g.bands_per_stream + bid);
+    } else {
+      for (int k = lane; k < nw; k += 32) total += __popc(__ldg(bm + k));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    }
     if (total > 0) {
       int bs = 0;
       if (lane == 0) {
@@ -1514,72 +1528,85 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
         if (bs + total > g.kp_cap) { atomicOr(&ctr[C_ERR], VF_ERRBIT_STAGING); bs = -1; }
       }
       base = __shfl_sync(0xffffffffu, bs, 0);
-      if (base >= 0) {
-        int crow = w0 / bmw, ck = w0 - crow * bmw;   // row / column of the cursor word
-        auto load_word = [&]() -> uint32_t { return __ldg(bm + crow * bmw + ck); };
-        int cursor = w0, idx = ex;             // this lane's enumeration state
-        int qn = 0;                            // survivors queued (warp-uniform)
-        uint32_t pend = cursor < w1 ? load_word() : 0u;
-        for (int r0 = 0; r0 < total; r0 += 32) {
-          // emit this round's candidates (ranks r0 .. r0+31) into cand[]
-          while (idx < r0 + 32 && cursor < w1) {
-            if (!pend) {
-              cursor++;
-              if (++ck == bmw) { ck = 0; crow++; }
-              pend = cursor < w1 ? load_word() : 0u;
-              continue;
-            }
-            const int bit = __ffs(pend) - 1;
-            pend &= pend - 1;
-            if (idx >= r0) cand[wid][idx - r0] = ((y0 + crow) << 16) | (32 * ck + bit);
-            idx++;
+    }
+    if (total > 0 && base >= 0) {
+      // One loop with a single test site and a single refine site (the fp64
+      // refinement is large: inlining it twice made the kernel i-cache bound).
+      // cand[head, tail) holds listed, untested candidates; sq[0, qn) survivors.
+      int qn = 0, head = 0, tail = 0, k0 = 0;   // warp-uniform
+      for (;;) {
+        if (tail - head < 32 && k0 < nw) {
+          // refill: move the (< 32) untested remainder to the front, list 32 more words
+          if (head) {
+            const int rem = tail - head;
+            const uint16_t v = lane < rem ? cand[w][head + lane] : (uint16_t)0;
+            __syncwarp();
+            if (lane < rem) cand[w][lane] = v;
+            head = 0;
+            tail = rem;
           }
+          const int k = k0 + lane;
+          const uint32_t word = k < nw ? __ldg(bm + k) : 0u;
+          int tot;
+          int pos = tail + warp_excl_scan(__popc(word), lane, tot);
+          if (word) {
+            const int r = k / bmw, cw = k - r * bmw;
+            for (uint32_t m = word; m; m &= m - 1u) cand[w][pos++] = (uint16_t)((r << 13) | (32 * cw + __ffs(m) - 1));
+          }
+          tail += tot;
+          k0 += 32;
           __syncwarp();
-          const int nr = min(32, total - r0);
+          continue;
+        }
+        if (tail > head) {
+          // test up to 32 listed candidates (lane = candidate), queue the survivors
+          const int nr = min(32, tail - head);
           bool keep = false;
-          int yx = 0;
+          int v = 0;
           if (lane < nr) {
-            yx = cand[wid][lane];
-            keep = nms_test(g, b, s, um, l, yx >> 16, yx & 0xffff);
+            v = cand[w][head + lane];
+            keep = nms_test(g, b, s, um, l, ys + (v >> 13), v & 0x1fff);
           }
           const unsigned sm = __ballot_sync(0xffffffffu, keep);
-          if (keep) sq[wid][qn + __popc(sm & ((1u << lane) - 1))] = yx;
+          if (keep) sq[w][qn + __popc(sm & ((1u << lane) - 1))] = (uint16_t)v;
           qn += __popc(sm);
+          head += nr;
           __syncwarp();
-          // refine survivors 32 at a time (FIFO: rank order is preserved)
-          const bool last_round = r0 + 32 >= total;
-          while (qn >= 32 || (last_round && qn > 0)) {
-            const int nb = min(32, qn);
-            NmsOut o;
-            o.flags = 0;
-            if (lane < nb) {
-              const int v = sq[wid][lane];
-              o = nms_refine(g, b, s, um, l, v >> 16, v & 0xffff);
-            }
-            const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
-            n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
-            n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
-            if (o.flags & 4) {
-              const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
-              b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
-              if (um) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
-            }
-            kept += __popc(kb);
-            __syncwarp();
-            if (lane + nb < qn) sq[wid][lane] = sq[wid][lane + nb];
-            qn -= nb;
-            __syncwarp();
-          }
         }
-      } else {
-        base = 0;
+        const bool fin = k0 >= nw && head == tail;
+        if (qn >= 32 || (fin && qn > 0)) {
+          // refine the oldest nb survivors (FIFO keeps the (y, x) order)
+          const int nb = min(32, qn);
+          NmsOut o;
+          o.flags = 0;
+          if (lane < nb) {
+            const int v = sq[w][lane];
+            o = nms_refine(g, b, s, um, l, ys + (v >> 13), v & 0x1fff);
+          }
+          const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
+          n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
+          n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
+          if (o.flags & 4) {
+            const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
+            b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
+            if (um) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
+          }
+          kept += __popc(kb);
+          __syncwarp();
+          const uint16_t rest = lane + nb < qn ? sq[w][lane + nb] : (uint16_t)0;
+          __syncwarp();
+          if (lane + nb < qn) sq[w][lane] = rest;
+          qn -= nb;
+          __syncwarp();
+        } else if (fin) {
+          break;
+        }
       }
+    } else {
+      base = 0;
     }
   }
-  if (lane == 0) {
-    int4* rec = reinterpret_cast<int4*>(b.band_rec) + ((long long)s * g.bands_per_stream + bid);
-    *rec = make_int4(base, kept, n_ok, n_drop);
-  }
+  if (lane == 0) *rec = make_int4(base, kept, n_ok, n_drop);
 }
 
 // After k_nms (stream order), one CTA per stream: band output offsets (scan
@@ -1590,11 +1617,11 @@ __global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant
   __shared__ int sm[NF_THREADS / 32];
   __shared__ int red[2][NF_THREADS / 32];
   const int s = b.s0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nb = g.bands_per_stream;
-  const int4* rec = reinterpret_cast<const int4*>(b.band_rec) + (long long)s * nb;
-  int* bout = b.band_out + (long long)s * nb;
+  const int nb = g.bands_per_stream * b.nms_u;   // NMS units, (layer, y) order
+  const int4* rec = reinterpret_cast<const int4*>(b.unit_rec) + (long long)s * nb;
+  int* bout = b.unit_out + (long long)s * nb;
   const int um = use_mask(g, b, s);
-  // ---- band offsets: thread t owns bands [t * per, t * per + per) ----
+  // ---- unit offsets: thread t owns units [t * per, t * per + per) ----
   const int per = (nb + NF_THREADS - 1) / NF_THREADS;
   int kept = 0, n_drop = 0, n_surv = 0;
   for (int k = 0; k < per; k++) {

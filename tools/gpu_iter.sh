@@ -1,8 +1,13 @@
 #!/bin/bash
-# One GPU iteration: detect+describe parity tests, then the default bench
-# (no CPU baseline / e2e).  Usage: tools/gpu_iter.sh TAG
+# One GPU iteration: detect+describe parity tests, then benches of the headline
+# and the dense / single-stream configs.  Usage: tools/gpu_iter.sh TAG [long]
 tag=${1:-it}
-timeout 600 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_stages.py tests/test_gpu_configs.py -x -q \
-  > gpurun_out/${tag}_tests.log 2>&1
+tests="tests/test_gpu_pipeline.py tests/test_gpu_stages.py tests/test_gpu_configs.py"
+[ "$2" = "long" ] && tests="$tests tests/test_gpu_long.py"
+timeout 900 python -m pytest $tests -x -q -m gpu -k "not capacity" > gpurun_out/${tag}_tests.log 2>&1
 echo "rc=$?" >> gpurun_out/${tag}_tests.log
-timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/${tag}_bench.log 2>&1
+for cm in 5:intensity 5:none 4:intensity 1:intensity; do
+  c=${cm%%:*}; m=${cm##*:}
+  timeout 300 python bench.py --config $c --mode $m --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --gen cuda \
+    > gpurun_out/${tag}_c${c}_${m}.log 2>&1
+done
