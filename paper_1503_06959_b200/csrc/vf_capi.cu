@@ -14,6 +14,11 @@
 #include <climits>
 
 #define VF_VERSION "vidfeat-b200 0.1.0 (sm_100a)"
+#ifdef VF_DEBUG
+#define DBG_SYNC(st, name) do { (void)(st); cudaError_t e_ = cudaDeviceSynchronize(); if (e_ != cudaSuccess) fprintf(stderr, "vidfeat_b200 debug: %s after %s\n", cudaGetErrorString(e_), name); } while (0)
+#else
+#define DBG_SYNC(st, name) do { } while (0)
+#endif
 
 namespace {
 
@@ -199,6 +204,10 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   // bit-packed IDDM mask from k_pyramid4 (its geometry, default mask source)
   g.use_cbits = g.mask_mode == 1 && !g.per_layer && g.mask_level == 3 && g.O == 4 && g.ptw == 96 && g.pth == 48;
   g.cbits_words = g.use_cbits ? cdiv(g.grid[0].cols, 32) : 0;
+  // the warp-strip pyramid (k_pyr_o + k_pyr_i) for O = 4; VF_PYR_SPLIT=0 keeps the smem-tile k_pyramid4
+  g.pyr_split = g.O == 4 && (g.mask_mode != 1 || g.use_cbits) &&
+                !(getenv("VF_PYR_SPLIT") && atoi(getenv("VF_PYR_SPLIT")) == 0);
+  g.pyr_halo = 4 * std::max(cdiv(g.W, g.L[g.NL - 1].w), cdiv(g.H, g.L[g.NL - 1].h)) + 2;
   if (g.ptw % VF_ST) return VF_ERR_ARG;
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
@@ -634,14 +643,18 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     stage_mark(c, 0, st);
     int smem = g.grid[0].rows * g.grid[0].cols * 4;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_binmask, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_binmask<<<n, 1024, smem, st>>>(g, b);
+    k_binmask<<<n, 1024, smem, st>>>(g, b); DBG_SYNC(st, "k_binmask");
   }
   stage_mark(c, 1, st);
-  if (g.O == 4 && g.ptw == 96 && g.pth == 48 && !(g.mask_mode == 1 && !g.use_cbits))
-    k_pyramid4<<<dim3(g.ptx, g.pty, n), 256, 0, st>>>(g, b);
+  const bool pyr4 = g.O == 4 && g.ptw == 96 && g.pth == 48 && !(g.mask_mode == 1 && !g.use_cbits);
+  const int pyo_blocks = cdiv((long long)cdiv(g.W, PYO_COLS) * cdiv(g.L[2].h, 4), 8);
+  const int pyi_blocks = cdiv((long long)cdiv(g.W, PYI_COLS) * cdiv(g.L[1].h, 8), 8);
+  if (pyr4 && g.pyr_split)
+    { k_pyr_o<<<dim3(pyo_blocks, n), 256, 0, st>>>(g, b); DBG_SYNC(st, "k_pyr_o"); }
+  else if (pyr4)
+    { k_pyramid4<PYR_FULL><<<dim3(g.ptx, g.pty, n), 256, 0, st>>>(g, b); DBG_SYNC(st, "k_pyramid4"); }
   else
-    k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b);
-  stage_mark(c, 2, st);
+    { k_pyramid<<<dim3(g.ptx, g.pty, n), 256, c->pyr_smem, st>>>(g, b); DBG_SYNC(st, "k_pyramid"); }
   const int tile_ctas = cdiv(g.tiles_per_stream, 256);   // lane per FAST tile
   const int cov_ctas = (g.mask_mode == 1 && g.per_layer) ? cdiv(g.H, 8) : 0;
   const int carry_ctas = cdiv(g.sty, 8);
@@ -658,11 +671,14 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     c->aux.push_back(as); c->aux_in.push_back(ei); c->aux_mid.push_back(em); c->aux_out.push_back(eo);
   }
   cudaEventRecord(c->aux_in[gi], st);
-  k_worklist<<<dim3(tile_ctas, n), 256, 0, st>>>(g, b, tile_ctas, 0, 0);
+  // intra-octave chain of masked frames near active cells (after the IDDM bits)
+  if (pyr4 && g.pyr_split) k_pyr_i<<<dim3(pyi_blocks, n), 256, 0, st>>>(g, b); DBG_SYNC(st, "k_pyr_i");
+  stage_mark(c, 2, st);
+  k_worklist<<<dim3(tile_ctas, n), 256, 0, st>>>(g, b, tile_ctas, 0, 0); DBG_SYNC(st, "k_worklist");
   cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
   const bool prop = g.mask_mode == 1 || g.mask_mode == 2;
   k_worklist<<<dim3(cov_ctas + carry_ctas + (prop ? PROP_CTAS : 0), n), 256, 0, c->aux[gi]>>>(
-      g, b, 0, cov_ctas, carry_ctas);
+      g, b, 0, cov_ctas, carry_ctas); DBG_SYNC(c->aux[gi], "k_worklist");
   cudaEventRecord(c->aux_mid[gi], c->aux[gi]);
   // Eq. 1 propagation into the last n_prop slots of the list: independent of
   // the detection, so it runs beside k_fast / k_nms
@@ -673,7 +689,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
       p1 = pool_event(c);
       cudaEventRecord(p0, c->aux[gi]);
     }
-    k_propagate<<<dim3(PROP_CTAS, n), 256, 0, c->aux[gi]>>>(g, b);
+    k_propagate<<<dim3(PROP_CTAS, n), 256, 0, c->aux[gi]>>>(g, b); DBG_SYNC(c->aux[gi], "k_propagate");
     if (c->timing) {
       cudaEventRecord(p1, c->aux[gi]);
       c->side_ev.push_back(p0);
@@ -684,12 +700,12 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
-  k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n);
+  k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_fast");
   stage_mark(c, 4, st);
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
   b.nms_u = nms_units(g, n);
-  k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b);
-  k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b);
+  k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms");
+  k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
   stage_mark(c, 5, st);
   // SAT + describe of two stream halves on concurrent high-priority streams:
   // the latency-bound sampling kernels of one half fill the other's gaps and
@@ -719,25 +735,25 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
       const int nh = h1 - h0, pb = (nh + 1) * (int)sizeof(int);
       cudaStream_t ds = c->dstreams[h];
       cudaStreamWaitEvent(ds, c->dfork, 0);
-      k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh);
-      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 0);
-      k_desc_orient<<<c->dorient_grid, DO_THREADS, pb, ds>>>(g, bh, nh);
-      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 1);
+      k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh); DBG_SYNC(st, "k_sat");
+      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 0); DBG_SYNC(st, "k_desc_sample");
+      k_desc_orient<<<c->dorient_grid, DO_THREADS, pb, ds>>>(g, bh, nh); DBG_SYNC(st, "k_desc_orient");
+      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 1); DBG_SYNC(st, "k_desc_sample");
       cudaEventRecord(c->djoin[h], ds);
     }
     for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[h], 0);
   } else {
-    k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n);
+    k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n); DBG_SYNC(st, "k_sat");
     stage_mark(c, 6, st);
-    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0);
-    k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n);
-    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1);
+    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0); DBG_SYNC(st, "k_desc_sample");
+    k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_desc_orient");
+    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1); DBG_SYNC(st, "k_desc_sample");
   }
   // k_propagate (stage 7) is timed on the side stream; the join wait counts
   // toward the finalize stage
   stage_mark(c, 8, st);
   cudaStreamWaitEvent(st, c->aux_out[gi], 0);
-  k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n);
+  k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n); DBG_SYNC(st, "k_finalize");
   stage_mark(c, -1, st);
   for (int s = s0; s < s0 + n; s++) c->frames_done[s]++;
   return cuda_status(cudaGetLastError());

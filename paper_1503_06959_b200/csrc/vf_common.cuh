@@ -89,6 +89,8 @@ struct Geo {
   int sat_tiles;        // stx * sty
   unsigned sth_magic;   // ceil(2^32 / VF_ST): y / VF_ST == umulhi(y, sth_magic) for y < 2^16
   int nms_raw;          // stand-alone nms_and_refine: no border / merge filter
+  int pyr_split;        // masked frames build the intra-octave chain only near active cells (k_pyramid4)
+  int pyr_halo;         // o0 pixels a FAST ring reaches around a tile's derived pixels
   int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
 };
 

@@ -19,6 +19,7 @@
 #include "vf_common.cuh"
 #include <math_constants.h>
 #include <climits>
+#include <cstdio>
 
 // Descriptor sampling pattern (pattern.py:21-106), uploaded by vf_set_pattern.
 #define VF_NPTS 60
@@ -518,6 +519,19 @@ __device__ __forceinline__ void store_word(uint8_t* gdst, int gp, int y, int x, 
   else for (int c = 0; c < 4 && x + c < vw; c++) gdst[(long long)y * gp + x + c] = (uint8_t)(w >> (8 * c));
 }
 
+// PART selects the work (the split pyramid of masked frames):
+//   PYR_FULL   every level (frame 0, mode none, binning);
+//   PYR_OCHAIN o1, o2, o3 + IDDM + SAT row sums for every tile; streams whose
+//              frame is unmasked also get the intra-octave chain here;
+//   PYR_ICHAIN i0..i3 of masked streams, only for tiles whose derived pixels a
+//              FAST score can read: an active top-octave cell within
+//              g.pyr_halo o0 pixels of the tile (a FAST ring reaches 3 layer
+//              pixels, <= 3 * W / w_i3 o0 pixels).  FAST reads the other
+//              pixels only for gated-off positions, whose results are dropped.
+#define PYR_FULL 0
+#define PYR_OCHAIN 1
+#define PYR_ICHAIN 2
+template <int PART>
 __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   constexpr int TW = 96, TH = 48;
@@ -526,7 +540,27 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   __shared__ __align__(16) uint8_t so3[6 * 12 + 8];
   const int s = b.s0 + blockIdx.z, tid = threadIdx.x;
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
-  if (blockIdx.x == 0 && blockIdx.y == 0) {
+  const bool masked = PART != PYR_FULL && use_mask(g, b, s);
+  const bool do_o = PART != PYR_ICHAIN;
+  const bool do_i = PART != PYR_OCHAIN || !masked;
+  if (PART == PYR_ICHAIN) {
+    if (!masked) return;   // built by the PYR_OCHAIN launch
+    const GridGeo& G = g.grid[0];
+    const int cx0 = max(0, X0 - g.pyr_halo) / G.cw, cx1 = min(G.cols - 1, (X0 + TW - 1 + g.pyr_halo) / G.cw);
+    const int cy0 = max(0, Y0 - g.pyr_halo) / G.ch, cy1 = min(G.rows - 1, (Y0 + TH - 1 + g.pyr_halo) / G.ch);
+    const int wa = cx0 >> 5, nwd = (cx1 >> 5) - wa + 1, n = (cy1 - cy0 + 1) * nwd;
+    uint32_t any = 0;
+    if (tid < n) {
+      const int r = tid / nwd, k = tid - r * nwd;
+      const uint32_t* bits = b.cbits + ((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words;
+      uint32_t v = __ldcg(bits + (long long)(cy0 + r) * g.cbits_words + wa + k);
+      if (k == 0) v &= 0xffffffffu << (cx0 & 31);
+      if (k == nwd - 1) v &= 0xffffffffu >> (31 - (cx1 & 31));
+      any = v;
+    }
+    if (!__syncthreads_or(any != 0)) return;
+  }
+  if (PART != PYR_ICHAIN && blockIdx.x == 0 && blockIdx.y == 0) {
     if (tid == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
       b.sat_count[s] = 0;
@@ -585,7 +619,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   }
   __syncthreads();
   // ---- phase 1: i0 (2/3 resample) + o1 (halving) + row sums ----
-  {
+  if (do_i) {
     // i0: 16 row pairs x 16 words, one 2x4 block per thread
     const int p = tid >> 4, q = tid & 15;
     const int base = 6 * q, al = base & ~3, sh = 8 * (base & 3);
@@ -620,14 +654,14 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     put(1, 2 * X0 / 3, 2 * Y0 / 3, 2 * p, 4 * q, e);
     put(1, 2 * X0 / 3, 2 * Y0 / 3, 2 * p + 1, 4 * q, o);
   }
-  for (int i = tid; i < 24 * 12; i += 256) {
+  for (int i = tid; do_o && i < 24 * 12; i += 256) {
     const int y = i / 12, q = i - y * 12;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(t0 + (2 * y) * TW + 8 * q),
                               *reinterpret_cast<const uint2*>(t0 + (2 * y + 1) * TW + 8 * q));
     *reinterpret_cast<uint32_t*>(so1 + y * 48 + 4 * q) = w;
     put(2, X0 >> 1, Y0 >> 1, y, 4 * q, w);
   }
-  if (tid < 3 * th) {
+  if (do_o && tid < 3 * th) {
     // row sums per 32-px SAT column of the tile (strip carries of the SATs)
     const int y = tid / 3, k = tid - 3 * y, col = 3 * blockIdx.x + k;
     const uint32_t* row = reinterpret_cast<const uint32_t*>(t0 + y * TW + VF_ST * k);
@@ -639,12 +673,14 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   __syncthreads();
   // ---- phase 2: i1 from i0, o2 from o1 ----
   if (tid < 128) {
+    if (do_i) {
     const int y = tid >> 3, q = tid & 7;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si0 + (2 * y) * 64 + 8 * q),
                               *reinterpret_cast<const uint2*>(si0 + (2 * y + 1) * 64 + 8 * q));
     *reinterpret_cast<uint32_t*>(si1 + y * 32 + 4 * q) = w;
     put(3, (2 * X0 / 3) >> 1, (2 * Y0 / 3) >> 1, y, 4 * q, w);
-  } else if (tid < 128 + 72) {
+    }
+  } else if (do_o && tid < 128 + 72) {
     const int i = tid - 128, y = i / 6, q = i - y * 6;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(so1 + (2 * y) * 48 + 8 * q),
                               *reinterpret_cast<const uint2*>(so1 + (2 * y + 1) * 48 + 8 * q));
@@ -653,13 +689,13 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   }
   __syncthreads();
   // ---- phase 3: i2 from i1, o3 from o2 ----
-  if (tid < 32) {
+  if (do_i && tid < 32) {
     const int y = tid >> 2, q = tid & 3;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si1 + (2 * y) * 32 + 8 * q),
                               *reinterpret_cast<const uint2*>(si1 + (2 * y + 1) * 32 + 8 * q));
     *reinterpret_cast<uint32_t*>(si2 + y * 16 + 4 * q) = w;
     put(5, (2 * X0 / 3) >> 2, (2 * Y0 / 3) >> 2, y, 4 * q, w);
-  } else if (tid < 32 + 18) {
+  } else if (do_o && tid >= 32 && tid < 32 + 18) {
     const int i = tid - 32, y = i / 3, q = i - y * 3;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(so2 + (2 * y) * 24 + 8 * q),
                               *reinterpret_cast<const uint2*>(so2 + (2 * y + 1) * 24 + 8 * q));
@@ -668,13 +704,13 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   }
   __syncthreads();
   // ---- phase 4: i3 from i2; IDDM on o3 (masking.py:84-93) ----
-  if (tid < 8) {
+  if (do_i && tid < 8) {
     const int y = tid >> 1, q = tid & 1;
     const uint32_t w = halve4(*reinterpret_cast<const uint2*>(si2 + (2 * y) * 16 + 8 * q),
                               *reinterpret_cast<const uint2*>(si2 + (2 * y + 1) * 16 + 8 * q));
     put(7, (2 * X0 / 3) >> 3, (2 * Y0 / 3) >> 3, y, 4 * q, w);
   }
-  if (g.mask_mode == 1 && tid >= 32 && tid < 128) {
+  if (do_o && g.mask_mode == 1 && tid >= 32 && tid < 128) {
     unsigned long long covered = 0;
     const int i = tid - 32;
     const LayerGeo& L = g.L[6];
@@ -727,6 +763,315 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
         }
       }
     }
+  }
+}
+
+// ============================================================================
+// Warp-strip pyramid (O = 4): two launches without shared memory or block
+// barriers, every lane loading all of its input bytes at once.
+//
+// k_pyr_o: warp per strip of 8 o0 rows x 256 o0 columns (lane: 8 columns).
+//   o1 (4 rows x 4 px per lane), o2 (2 rows x 2 px), o3 (1 px) by the 2x2
+//   rounded halving of pyramid.py:67-73; the IDDM of masking.py:84-93 on o3
+//   (one lane per top-octave cell, a ballot is one word of the bit mask);
+//   the per-32-column SAT row sums of the 8 rows.  Block 0 of each stream
+//   also resets the per-step counters.
+// k_pyr_i: warp per strip of 12 o0 rows x 384 o0 columns (lane: 12 columns).
+//   i0 (8 rows x 8 px per lane) by the 2/3 area resample of pyramid.py:76-94
+//   (one dp4a of a 2x2 input block with the separable (2, 1) x (2, 1)
+//   weights, then (v + 4) // 9 by multiply-shift), i1 (4 x 4), i2 (2 x 2),
+//   i3 (1) by halving.  In masked frames only strips with an active top-octave
+//   cell within g.pyr_halo o0 pixels run (a FAST ring reaches 3 layer pixels
+//   of a gated pixel, <= 3 W / w_i3 o0 pixels); FAST reads the other pixels
+//   only for gated-off positions, whose scores are dropped.
+// ============================================================================
+#define PYO_COLS 256
+#define PYI_COLS 384
+__device__ __forceinline__ void store_bytes(uint8_t* row, int x, int valid, uint32_t w, int n)
+{
+  // n bytes of w at row[x..x+n) (x aligned to n), clipped to `valid` columns
+  if (x + n <= valid) {
+#ifdef VF_DEBUG
+    if (reinterpret_cast<uintptr_t>(row + x) & (n - 1)) printf("store_bytes x %d n %d\n", x, n);
+#endif
+    if (n == 4) *reinterpret_cast<uint32_t*>(row + x) = w;
+    else if (n == 2) *reinterpret_cast<uint16_t*>(row + x) = (uint16_t)w;
+    else row[x] = (uint8_t)w;
+  } else {
+    for (int c = 0; c < n && x + c < valid; c++) row[x + c] = (uint8_t)(w >> (8 * c));
+  }
+}
+
+// Up to 4 bytes at p (clipped to `valid` bytes), packed little-endian: the
+// edge lanes of the strip kernels (kept out of line; returns a value so the
+// callers' row arrays stay in registers).
+__device__ __noinline__ uint32_t load_edge4(const uint8_t* p, int valid)
+{
+  uint32_t w = 0u;
+  for (int c = 0; c < 4 && c < valid; c++) w |= (uint32_t)__ldg(p + c) << (8 * c);
+  return w;
+}
+
+__global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      b.ctr[s * C_NCTR + C_STAGE] = 0;
+      b.sat_count[s] = 0;
+      b.work_count[s] = 0;
+    }
+    for (int i = threadIdx.x; i < g.sty * g.stw_words; i += blockDim.x) b.sat_bits[(long long)s * g.sty * g.stw_words + i] = 0u;
+  }
+  const int nsx = (g.W + PYO_COLS - 1) / PYO_COLS;
+  const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int sy = strip / nsx, sx = strip - sy * nsx;
+  const int h1 = g.L[2].h;
+  if (sy * 4 >= h1) return;
+  const int X = sx * PYO_COLS + 8 * lane, Y = sy * 8, W = g.W, H = g.H;
+  const int nr = min(8, H - Y);              // o0 rows present (>= 2)
+  // ---- 8 o0 rows x 8 columns of this lane ----
+  const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y * b.frame_pitch + X;
+  const int pitch = (int)b.frame_pitch;
+  const bool vec = ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) & 7) == 0;
+  uint2 r[8];
+  if (vec && X + 8 <= W && nr == 8) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+#ifdef VF_DEBUG
+      if ((reinterpret_cast<uintptr_t>(src + k * pitch) & 7)) printf("pyr_o load %p X %d Y %d k %d\n", src + k * pitch, X, Y, k);
+#endif
+      r[k] = __ldg(reinterpret_cast<const uint2*>(src + k * pitch));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const bool ok = k < nr && X < W;
+      r[k] = make_uint2(ok ? load_edge4(src + k * pitch, W - X) : 0u, ok ? load_edge4(src + k * pitch + 4, W - X - 4) : 0u);
+    }
+  }
+  // ---- SAT row sums: 32-column segments = 4 lanes ----
+  {
+    const int col = X / VF_ST;
+    uint32_t* rs = b.rowsum + ((long long)s * H + Y) * g.stx + col;
+    const bool wr = (lane & 3) == 0 && col < g.stx;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      uint32_t a = __dp4a(r[k].y, 0x01010101u, __dp4a(r[k].x, 0x01010101u, 0u));
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      if (wr && k < nr) rs[k * g.stx] = a;
+    }
+  }
+  uint8_t* lay = b.layers + (long long)s * g.layer_slab;
+  // ---- o1: 4 rows x 4 px ----
+  const LayerGeo& L1 = g.L[2];
+  uint32_t w1[4];
+  {
+    uint8_t* o1 = lay + L1.layer_off + (long long)(4 * sy) * L1.pitch + X / 2;
+    const int n1 = min(4, h1 - 4 * sy);
+    const bool full = X / 2 + 4 <= L1.w;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      w1[k] = halve4(r[2 * k], r[2 * k + 1]);
+      if (k < n1) {
+#ifdef VF_DEBUG
+        if (full && (reinterpret_cast<uintptr_t>(o1 + k * L1.pitch) & 3)) printf("pyr_o o1 X %d\n", X);
+#endif
+        if (full) *reinterpret_cast<uint32_t*>(o1 + k * L1.pitch) = w1[k];
+        else if (X / 2 < L1.w) store_bytes(o1 + k * L1.pitch - X / 2, X / 2, L1.w, w1[k], 4);
+      }
+    }
+  }
+  // ---- o2: 2 rows x 2 px (bytes 0, 1) ----
+  const LayerGeo& L2 = g.L[4];
+  uint32_t w2[2];
+  {
+    uint8_t* o2 = lay + L2.layer_off + (long long)(2 * sy) * L2.pitch + X / 4;
+    const int n2 = min(2, L2.h - 2 * sy);
+    const bool full = X / 4 + 2 <= L2.w;
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const uint32_t a = w1[2 * k], c = w1[2 * k + 1];
+      const uint32_t e = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu) + (c & 0x00ff00ffu) + ((c >> 8) & 0x00ff00ffu);
+      const uint32_t q = ((e + 0x00020002u) >> 2) & 0x00ff00ffu;
+      w2[k] = (q & 0xffu) | ((q >> 8) & 0xff00u);
+      if (k < n2) {
+#ifdef VF_DEBUG
+        if (full && (reinterpret_cast<uintptr_t>(o2 + k * L2.pitch) & 1)) printf("pyr_o o2 X %d\n", X);
+#endif
+        if (full) *reinterpret_cast<uint16_t*>(o2 + k * L2.pitch) = (uint16_t)w2[k];
+        else if (X / 4 < L2.w) o2[k * L2.pitch] = (uint8_t)w2[k];
+      }
+    }
+  }
+  // ---- o3: 1 px ----
+  const LayerGeo& L3 = g.L[6];
+  const uint32_t sum3 = (w2[0] & 0xffu) + (w2[0] >> 8) + (w2[1] & 0xffu) + (w2[1] >> 8);
+  const int c3 = (int)((sum3 + 2) >> 2);
+  const int x3 = X / 8, y3 = sy;
+  const bool in3 = x3 < L3.w && y3 < L3.h;
+  if (in3) lay[L3.layer_off + (long long)y3 * L3.pitch + x3] = (uint8_t)c3;
+  // ---- IDDM on o3 (masking.py:84-93): int16 diff vs float t_i, strict ----
+  if (g.mask_mode == 1) {
+    const GridGeo& G = g.grid[0];
+    const bool um = use_mask(g, b, s);
+    uint8_t* st = b.state + (long long)s * g.state_slab + g.state_off[3];
+    const int gi = y3 * L3.w + x3;
+    int bit = 0;
+    unsigned covered = 0;
+    if (in3) {
+      if (um) {
+        int d = c3 - (int)st[gi];
+        d = d < 0 ? -d : d;
+        bit = (double)d > g.t_i;
+        b.cells[(long long)s * g.cell_slab + G.cell_off + gi] = (uint8_t)bit;
+        if (bit) covered = (unsigned)(min(G.ch, H - y3 * G.ch) * min(G.cw, W - x3 * G.cw));
+      }
+      st[gi] = (uint8_t)c3;
+    }
+    if (um) {
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      if (bal) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) covered += __shfl_down_sync(0xffffffffu, covered, o);
+      }
+      if (lane == 0) {
+        if (covered) atomicAdd(b.cov + s, (unsigned long long)covered);
+        if (g.use_cbits && y3 < G.rows && sx < g.cbits_words)   // cells 32 sx .. 32 sx + 31 of row y3
+          b.cbits[((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words + (long long)y3 * g.cbits_words +
+                  sx] = bal;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t div9x(uint32_t v) { return (v * 7282u + 29128u) >> 16; }   // (v + 4) // 9
+
+__global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31;
+  const int nsx = (g.W + PYI_COLS - 1) / PYI_COLS;
+  const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int sy = strip / nsx, sx = strip - sy * nsx;
+  const LayerGeo& Li0 = g.L[1];
+  if (sy * 8 >= Li0.h) return;
+  const int X = sx * PYI_COLS + 12 * lane, Y = sy * 12;
+  if (g.use_cbits && use_mask(g, b, s)) {
+    // any active top-octave cell within pyr_halo o0 pixels of the strip?
+    const GridGeo& G = g.grid[0];
+    const int X0 = sx * PYI_COLS;
+    const int cx0 = max(0, X0 - g.pyr_halo) / G.cw, cx1 = min(G.cols - 1, (X0 + PYI_COLS - 1 + g.pyr_halo) / G.cw);
+    const int cy0 = max(0, Y - g.pyr_halo) / G.ch, cy1 = min(G.rows - 1, (Y + 11 + g.pyr_halo) / G.ch);
+    const int wa = cx0 >> 5, nwd = (cx1 >> 5) - wa + 1, n = (cy1 - cy0 + 1) * nwd;
+    const uint32_t* bits = b.cbits + ((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words;
+    uint32_t any = 0;
+    for (int i = lane; i < n; i += 32) {
+      const int r = i / nwd, k = i - r * nwd;
+      uint32_t v = __ldcg(bits + (long long)(cy0 + r) * g.cbits_words + wa + k);
+      if (k == 0) v &= 0xffffffffu << (cx0 & 31);
+      if (k == nwd - 1) v &= 0xffffffffu >> (31 - (cx1 & 31));
+      any |= v;
+    }
+    if (!__any_sync(0xffffffffu, any != 0u)) return;
+  }
+  // ---- 12 o0 rows x 12 columns of this lane (3 words per row) ----
+  const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y * b.frame_pitch + X;
+  const int pitch = (int)b.frame_pitch;
+  const bool vec = ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) & 3) == 0;
+  uint32_t r[12][3];
+  if (vec && X + 12 <= g.W && Y + 12 <= g.H) {
+#pragma unroll
+    for (int k = 0; k < 12; k++)
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+#ifdef VF_DEBUG
+        if ((reinterpret_cast<uintptr_t>(src + k * pitch) & 3)) printf("pyr_i load X %d\n", X);
+#endif
+        r[k][q] = __ldg(reinterpret_cast<const uint32_t*>(src + k * pitch) + q);
+      }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      const bool ok = Y + k < g.H && X < g.W;
+#pragma unroll
+      for (int q = 0; q < 3; q++) r[k][q] = ok ? load_edge4(src + k * pitch + 4 * q, g.W - X - 4 * q) : 0u;
+    }
+  }
+  // ---- i0: 8 rows x 8 px (2 words) per lane ----
+  // a 3-row x 6-column group gives a 2 x 4 output block: row bytes c0..c5 as
+  // L = (c0, c1, c2, c3), M = (c3, c4, c5, -); each output is one dp4a of a
+  // 2x2 input block with the weights 4 2 2 1 (and mirrors), then // 9
+  const uint32_t WL = 0x01020204u, WR = 0x02010402u, WLo = 0x02040102u, WRo = 0x04020201u;
+  uint32_t i0w[8][2];
+#pragma unroll
+  for (int t = 0; t < 4; t++) {          // row triple t -> i0 rows 2t, 2t + 1
+#pragma unroll
+    for (int h = 0; h < 2; h++) {        // 6-column half h -> i0 px 4h .. 4h + 3
+      uint32_t Lr[3], Mr[3];
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        const uint32_t* rw = r[3 * t + k];
+        // columns 6h .. 6h + 5: h = 0 -> bytes 0..5 (word 0, word 1 low half); h = 1 -> bytes 6..11
+        Lr[k] = h == 0 ? rw[0] : __funnelshift_r(rw[1], rw[2], 16);
+        Mr[k] = h == 0 ? __funnelshift_r(rw[0], rw[1], 24) : (rw[2] >> 8);
+      }
+      const uint32_t e0 = div9x(__dp4a(__byte_perm(Lr[0], Lr[1], 0x5410), WL, 0u));
+      const uint32_t e1 = div9x(__dp4a(__byte_perm(Lr[0], Lr[1], 0x6521), WR, 0u));
+      const uint32_t e2 = div9x(__dp4a(__byte_perm(Mr[0], Mr[1], 0x5410), WL, 0u));
+      const uint32_t e3 = div9x(__dp4a(__byte_perm(Mr[0], Mr[1], 0x6521), WR, 0u));
+      const uint32_t o0 = div9x(__dp4a(__byte_perm(Lr[1], Lr[2], 0x5410), WLo, 0u));
+      const uint32_t o1 = div9x(__dp4a(__byte_perm(Lr[1], Lr[2], 0x6521), WRo, 0u));
+      const uint32_t o2 = div9x(__dp4a(__byte_perm(Mr[1], Mr[2], 0x5410), WLo, 0u));
+      const uint32_t o3 = div9x(__dp4a(__byte_perm(Mr[1], Mr[2], 0x6521), WRo, 0u));
+      i0w[2 * t][h] = __byte_perm(__byte_perm(e0, e1, 0x0040), __byte_perm(e2, e3, 0x0040), 0x5410);
+      i0w[2 * t + 1][h] = __byte_perm(__byte_perm(o0, o1, 0x0040), __byte_perm(o2, o3, 0x0040), 0x5410);
+    }
+  }
+  uint8_t* lay = b.layers + (long long)s * g.layer_slab;
+  const int xi0 = 8 * (sx * 32 + lane);   // = 2 X / 3
+  {
+    uint8_t* row = lay + Li0.layer_off + (long long)(8 * sy) * Li0.pitch;
+    const int n0 = min(8, Li0.h - 8 * sy);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      if (k < n0 && xi0 < Li0.w) {
+#ifdef VF_DEBUG
+        if (xi0 + 8 <= Li0.w && (reinterpret_cast<uintptr_t>(row + xi0) & 7)) printf("pyr_i i0 store xi0 %d\n", xi0);
+#endif
+        if (xi0 + 8 <= Li0.w) *reinterpret_cast<uint2*>(row + xi0) = make_uint2(i0w[k][0], i0w[k][1]);
+        else { store_bytes(row, xi0, Li0.w, i0w[k][0], 4); if (xi0 + 4 < Li0.w) store_bytes(row, xi0 + 4, Li0.w, i0w[k][1], 4); }
+      }
+      row += Li0.pitch;
+    }
+  }
+  // ---- i1: 4 rows x 4 px ----
+  const LayerGeo& Li1 = g.L[3];
+  uint32_t i1w[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    i1w[k] = halve4(make_uint2(i0w[2 * k][0], i0w[2 * k][1]), make_uint2(i0w[2 * k + 1][0], i0w[2 * k + 1][1]));
+    const int y = 4 * sy + k, x = 4 * (sx * 32 + lane);
+    if (y < Li1.h && x < Li1.w) store_bytes(lay + Li1.layer_off + (long long)y * Li1.pitch, x, Li1.w, i1w[k], 4);
+  }
+  // ---- i2: 2 rows x 2 px ----
+  const LayerGeo& Li2 = g.L[5];
+  uint32_t i2w[2];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const uint32_t a = i1w[2 * k], c = i1w[2 * k + 1];
+    const uint32_t e = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu) + (c & 0x00ff00ffu) + ((c >> 8) & 0x00ff00ffu);
+    const uint32_t q = ((e + 0x00020002u) >> 2) & 0x00ff00ffu;
+    i2w[k] = (q & 0xffu) | ((q >> 8) & 0xff00u);
+    const int y = 2 * sy + k, x = 2 * (sx * 32 + lane);
+    if (y < Li2.h && x < Li2.w) store_bytes(lay + Li2.layer_off + (long long)y * Li2.pitch, x, Li2.w, i2w[k], 2);
+  }
+  // ---- i3: 1 px ----
+  const LayerGeo& Li3 = g.L[7];
+  const int y3 = sy, x3 = sx * 32 + lane;
+  if (y3 < Li3.h && x3 < Li3.w) {
+    const uint32_t sum = (i2w[0] & 0xffu) + (i2w[0] >> 8) + (i2w[1] & 0xffu) + (i2w[1] >> 8);
+    lay[Li3.layer_off + (long long)y3 * Li3.pitch + x3] = (uint8_t)((sum + 2) >> 2);
   }
 }
 
@@ -1485,6 +1830,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int& total, int* sm)
 // (layer, y): the reference order (detector.py:251-253,303-306).
 #define NMS_WARPS 4
 #define NMS_THREADS (32 * NMS_WARPS)
+#define NMS_PF 16       // bitmap words per lane staged at once
 #define NMS_LIST (1024 + 32)   // candidates of 32 bitmap words + an untested remainder
 __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
@@ -1492,6 +1838,7 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
   // footprint leaves the L1 to the score-map reads
   __shared__ uint16_t cand[NMS_WARPS][NMS_LIST];
   __shared__ uint16_t sq[NMS_WARPS][64];      // survivor queue, same encoding
+  __shared__ uint32_t wbuf[NMS_WARPS][32 * NMS_PF];   // staged bitmap words of the unit
   const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int U = b.nms_u, R = VF_TILE_H / U;
   const int unit = blockIdx.x * NMS_WARPS + w;
@@ -1534,9 +1881,25 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
       // refinement is large: inlining it twice made the kernel i-cache bound).
       // cand[head, tail) holds listed, untested candidates; sq[0, qn) survivors.
       int qn = 0, head = 0, tail = 0, k0 = 0;   // warp-uniform
+      int kb = 0, ke = 0;                       // words [kb, ke) of the unit are staged in wbuf
       for (;;) {
         if (tail - head < 32 && k0 < nw) {
-          // refill: move the (< 32) untested remainder to the front, list 32 more words
+          if (k0 == ke) {
+            // stage the next 512 bitmap words, 16 independent loads per lane in flight
+            kb = k0;
+            ke = min(nw, k0 + 32 * NMS_PF);
+#pragma unroll
+            for (int j = 0; j < NMS_PF; j++) {
+              const int k = kb + 32 * j + lane;
+              wbuf[w][32 * j + lane] = k < ke ? __ldg(bm + k) : 0u;
+            }
+            __syncwarp();
+          }
+          const int k = k0 + lane;
+          const uint32_t word = wbuf[w][k0 - kb + lane];   // zero past ke
+          k0 = min(ke, k0 + 32);
+          if (!__any_sync(0xffffffffu, word != 0u)) continue;   // 32 empty words (gated tiles)
+          // refill: move the (< 32) untested remainder to the front, list this pass
           if (head) {
             const int rem = tail - head;
             const uint16_t v = lane < rem ? cand[w][head + lane] : (uint16_t)0;
@@ -1545,8 +1908,6 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
             head = 0;
             tail = rem;
           }
-          const int k = k0 + lane;
-          const uint32_t word = k < nw ? __ldg(bm + k) : 0u;
           int tot;
           int pos = tail + warp_excl_scan(__popc(word), lane, tot);
           if (word) {
@@ -1554,7 +1915,6 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
             for (uint32_t m = word; m; m &= m - 1u) cand[w][pos++] = (uint16_t)((r << 13) | (32 * cw + __ffs(m) - 1));
           }
           tail += tot;
-          k0 += 32;
           __syncwarp();
           continue;
         }
