@@ -152,6 +152,10 @@ int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch)
  * vf_get_stage_ms synchronizes `stream`, returns the summed milliseconds per
  * stage since the last query and the number of steps, and clears. */
 int vf_set_timing(vf_ctx *ctx, int enable);
+/* CUDA graphs (default on): a batch of at most 12 MB of frames replays a
+ * captured graph of the step's launches (inputs copied into the graph's fixed
+ * input buffer first).  Off while stage timing is on and in temporal mode. */
+int vf_set_graphs(vf_ctx *ctx, int enable);
 int vf_get_stage_ms(vf_ctx *ctx, double *ms9, int32_t *n_steps, void *stream);
 /* Synchronizes `stream`; work counters of the last step: active FAST tiles,
  * total FAST tiles, SAT tiles built, total SAT tiles, unmasked streams,

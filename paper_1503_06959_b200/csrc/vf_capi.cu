@@ -316,6 +316,17 @@ struct vf_ctx {
   std::vector<cudaStream_t> dstreams;
   std::vector<cudaEvent_t> djoin;
   cudaEvent_t dfork = nullptr;
+  // CUDA graph of one step (small batches): the step's launches (all its
+  // streams) captured once per batch size and replayed; inputs are copied
+  // into a context-owned buffer first so the graph's pointers stay fixed
+  int graphs = 1;                       // vf_set_graphs
+  cudaGraphExec_t gexec = nullptr;
+  int g_n = 0;
+  int eager_n = 0;                      // batch size of the last eager step (streams / events exist)
+  uint8_t* gin = nullptr;
+  long long gin_bytes = 0;
+  bool capturing = false;
+  cudaStream_t cap = nullptr;           // capture stream
 };
 
 static void pack_free(vf_ctx* c)
@@ -536,6 +547,9 @@ int vf_destroy(vf_ctx* c)
   }
   pipe_free(c);
   pack_free(c);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->gin) cudaFree(c->gin);
+  if (c->cap) cudaStreamDestroy(c->cap);
   for (size_t k = 0; k < c->gstreams.size(); k++) { cudaStreamDestroy(c->gstreams[k]); cudaEventDestroy(c->gjoin[k]); }
   for (size_t k = 0; k < c->aux.size(); k++) {
     cudaStreamDestroy(c->aux[k]); cudaEventDestroy(c->aux_in[k]); cudaEventDestroy(c->aux_mid[k]);
@@ -622,6 +636,7 @@ int vf_set_history(vf_ctx* c, double* hist_dev, int32_t max_frames)
   if (!c || max_frames < 0 || (max_frames > 0 && !hist_dev)) return VF_ERR_ARG;
   c->b.hist = max_frames > 0 ? hist_dev : nullptr;
   c->b.hist_frames = max_frames;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }   // the graph bakes in the pointers
   return VF_OK;
 }
 
@@ -755,7 +770,8 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   cudaStreamWaitEvent(st, c->aux_out[gi], 0);
   k_finalize<<<cdiv(n, 128), 128, 0, st>>>(g, b, n); DBG_SYNC(st, "k_finalize");
   stage_mark(c, -1, st);
-  for (int s = s0; s < s0 + n; s++) c->frames_done[s]++;
+  if (!c->capturing)
+    for (int s = s0; s < s0 + n; s++) c->frames_done[s]++;
   return cuda_status(cudaGetLastError());
 }
 
@@ -899,11 +915,80 @@ int vf_block_match(const uint8_t* prev_dev, const uint8_t* cur_dev, int w, int h
   return cuda_status(e);
 }
 
+// Batches of at most this many frame bytes replay a captured CUDA graph of
+// the step: the launch sequence is latency-bound there (single 640x480 ..
+// 3840x2160 streams), and one copy of the inputs into the graph's fixed
+// input buffer is cheaper than ~20 host launches.
+#define VF_GRAPH_MAX_BYTES (12LL << 20)
+
+static int graph_step(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n,
+                      cudaStream_t st)
+{
+  const long long fb = (long long)c->g.W * c->g.H;
+  if (c->gin_bytes < fb * n) {
+    if (c->gin) cudaFree(c->gin);
+    c->gin = nullptr;
+    if (cudaMalloc(&c->gin, fb * n) != cudaSuccess) return VF_ERR_CUDA;
+    c->gin_bytes = fb * n;
+    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  }
+  cudaError_t e = cudaMemcpy2DAsync(c->gin, c->g.W, frames_dev, row_pitch, c->g.W, (size_t)c->g.H * 1, cudaMemcpyDeviceToDevice, st);
+  for (int s = 1; s < n && e == cudaSuccess; s++)
+    e = cudaMemcpy2DAsync(c->gin + s * fb, c->g.W, frames_dev + s * stream_stride, row_pitch, c->g.W, c->g.H,
+                          cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  c->b.frames = c->gin;
+  c->b.frame_stride = fb;
+  c->b.frame_pitch = c->g.W;
+  if ((!c->gexec || c->g_n != n) && c->eager_n != n) {
+    // the first step of a batch size runs eagerly: it creates the side streams
+    // and events the capture then records into
+    const int rc = launch_frames(c, n, st);
+    c->eager_n = n;
+    return rc;
+  }
+  if (!c->gexec || c->g_n != n) {
+    // capture on an internal non-blocking stream (the caller's may be the
+    // legacy default stream, which cannot be captured); replay on the caller's
+    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+    if (!c->cap && cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) return VF_ERR_CUDA;
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_status(e);
+    c->capturing = true;
+    const int rc = launch_frames(c, n, c->cap);
+    c->capturing = false;
+    e = cudaStreamEndCapture(c->cap, &graph);
+    if (rc != VF_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (e != cudaSuccess) return cuda_status(e);
+    e = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { c->gexec = nullptr; return cuda_status(e); }
+    c->g_n = n;
+  }
+  e = cudaGraphLaunch(c->gexec, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  for (int s = 0; s < n; s++) c->frames_done[s]++;
+  return VF_OK;
+}
+
+int vf_set_graphs(vf_ctx* c, int enable)
+{
+  if (!c) return VF_ERR_ARG;
+  c->graphs = enable;
+  if (!enable && c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  return VF_OK;
+}
+
 int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n_streams,
                void* stream)
 {
   if (!c || !frames_dev || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
   if (!g_pattern_ok) return VF_ERR_PATTERN;
+  static const bool env_off = getenv("VF_GRAPHS") && atoi(getenv("VF_GRAPHS")) == 0;
+  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3 &&
+      (long long)c->g.W * c->g.H * n_streams <= VF_GRAPH_MAX_BYTES)
+    return graph_step(c, frames_dev, stream_stride, row_pitch, n_streams, (cudaStream_t)stream);
   c->b.frames = frames_dev;
   c->b.frame_stride = stream_stride;
   c->b.frame_pitch = row_pitch;
