@@ -112,6 +112,16 @@ int vf_reset(vf_ctx *ctx, void *stream);
  * stream s's (height x width) uint8 frame with row pitch `row_pitch`. */
 int vf_process(vf_ctx *ctx, const uint8_t *frames_dev, int64_t stream_stride, int64_t row_pitch,
                int n_streams, void *stream);
+/* vf_process, then a capacity check (synchronizes `stream`): when a stream's
+ * features would overflow the per-stream capacity (VF_ERR_CAPACITY), the step
+ * is rolled back, every stream's capacity grows (the previous lists are kept)
+ * and the step is replayed from the same state, until it fits (SURVEY.md
+ * 8(b): "the wrapper grows the capacity and retries the frame from saved
+ * state").  Temporal mode returns VF_ERR_CAPACITY instead. */
+int vf_process_checked(vf_ctx *ctx, const uint8_t *frames_dev, int64_t stream_stride, int64_t row_pitch,
+                       int n_streams, void *stream);
+/* Current feature capacity per stream and buffer. */
+int vf_get_capacity(const vf_ctx *ctx, int32_t *kp_capacity);
 /* Same, from pinned or pageable HOST memory: the host->device copy is part of
  * the call (double-buffered device staging, stream-ordered). */
 int vf_process_host(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,
@@ -149,6 +159,9 @@ int vf_pipeline_collect(vf_ctx *ctx, int64_t cap, double *x, double *y, double *
 int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch);
 /* Live per-stage device timing with CUDA events on the launch stream:
  * stages = binmask, pyramid, worklist, fast, nms, sat, describe, propagate, finalize (9).
+ * With >= 2 streams per call the SAT and describe kernels run as two
+ * concurrent stream halves; their one joint interval is reported under "sat"
+ * and "describe" is 0.  propagate is timed on its own (side) stream.
  * vf_get_stage_ms synchronizes `stream`, returns the summed milliseconds per
  * stage since the last query and the number of steps, and clears. */
 int vf_set_timing(vf_ctx *ctx, int enable);

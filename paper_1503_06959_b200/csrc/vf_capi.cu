@@ -12,6 +12,7 @@
 #include <vector>
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #define VF_VERSION "vidfeat-b200 0.1.0 (sm_100a)"
 #ifdef VF_DEBUG
@@ -40,6 +41,10 @@ struct Alloc {
   void release() {
     for (void* p : ptrs) cudaFree(p);
     ptrs.clear();
+  }
+  void drop(void* p) {   // free one allocation made by get()
+    for (auto& q : ptrs)
+      if (q == p) { cudaFree(p); q = ptrs.back(); ptrs.pop_back(); return; }
   }
 };
 
@@ -315,7 +320,7 @@ struct vf_ctx {
   cudaEvent_t hp_in = nullptr, hp_out = nullptr;
   std::vector<cudaStream_t> dstreams;
   std::vector<cudaEvent_t> djoin;
-  cudaEvent_t dfork = nullptr;
+  std::vector<cudaEvent_t> dfork_g;     // per stream group
   // CUDA graph of one step (small batches): the step's launches (all its
   // streams) captured once per batch size and replayed; inputs are copied
   // into a context-owned buffer first so the graph's pointers stay fixed
@@ -460,7 +465,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.prop_out = A.get<int>((size_t)S * g.prop_chunks);
   b.cells = A.get<uint8_t>((size_t)S * g.cell_slab);
   b.cbits = g.use_cbits ? A.get<uint32_t>((size_t)S * 2 * g.grid[0].rows * g.cbits_words) : nullptr;
-  b.state = A.get<uint8_t>((size_t)S * g.state_slab);
+  b.state = A.get<uint8_t>((size_t)S * 2 * g.state_slab);   // two parities (iddm_state)
   int* dl = A.get<int>((size_t)g.lut_len);
   b.lut = dl;
   b.sat = A.get<uint32_t>((size_t)S * g.W * g.H);   // one strip SAT per stream
@@ -558,7 +563,7 @@ int vf_destroy(vf_ctx* c)
   if (c->gfork) cudaEventDestroy(c->gfork);
   if (c->hp) { cudaStreamDestroy(c->hp); cudaEventDestroy(c->hp_in); cudaEventDestroy(c->hp_out); }
   for (size_t k = 0; k < c->dstreams.size(); k++) { cudaStreamDestroy(c->dstreams[k]); cudaEventDestroy(c->djoin[k]); }
-  if (c->dfork) cudaEventDestroy(c->dfork);
+  for (cudaEvent_t ev : c->dfork_g) cudaEventDestroy(ev);
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
@@ -680,9 +685,9 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     cudaStream_t as;
     cudaEvent_t ei, em, eo;
     if (cudaStreamCreateWithFlags(&as, cudaStreamNonBlocking) != cudaSuccess) return VF_ERR_CUDA;
-    cudaEventCreateWithFlags(&ei, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&em, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&eo, cudaEventDisableTiming);
+    if (cudaEventCreateWithFlags(&ei, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&em, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&eo, cudaEventDisableTiming) != cudaSuccess) { cudaStreamDestroy(as); return VF_ERR_CUDA; }
     c->aux.push_back(as); c->aux_in.push_back(ei); c->aux_mid.push_back(em); c->aux_out.push_back(eo);
   }
   cudaEventRecord(c->aux_in[gi], st);
@@ -726,37 +731,44 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   // the latency-bound sampling kernels of one half fill the other's gaps and
   // tails (709 -> 698 us per 64-stream step).  The stage timer then reports
   // SAT and describe together.  VF_DESC_PAR overrides the number of halves.
+  // One set of half streams and events per stream group (index gi * dpar + h),
+  // so concurrent groups do not serialise on shared streams.
   static const int dpar = getenv("VF_DESC_PAR") ? std::max(1, atoi(getenv("VF_DESC_PAR"))) : 2;
   if (dpar > 1 && n >= dpar) {
-    if ((int)c->dstreams.size() < dpar) {
+    if ((int)c->dstreams.size() < (gi + 1) * dpar) {
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      if (!c->dfork) cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
-      while ((int)c->dstreams.size() < dpar) {
+      while ((int)c->dfork_g.size() <= gi) {
+        cudaEvent_t f;
+        if (cudaEventCreateWithFlags(&f, cudaEventDisableTiming) != cudaSuccess) return VF_ERR_CUDA;
+        c->dfork_g.push_back(f);
+      }
+      while ((int)c->dstreams.size() < (gi + 1) * dpar) {
         cudaStream_t ds;
         cudaEvent_t de;
-        cudaStreamCreateWithPriority(&ds, cudaStreamNonBlocking, hi);
-        cudaEventCreateWithFlags(&de, cudaEventDisableTiming);
+        if (cudaStreamCreateWithPriority(&ds, cudaStreamNonBlocking, hi) != cudaSuccess) return VF_ERR_CUDA;
+        if (cudaEventCreateWithFlags(&de, cudaEventDisableTiming) != cudaSuccess) { cudaStreamDestroy(ds); return VF_ERR_CUDA; }
         c->dstreams.push_back(ds);
         c->djoin.push_back(de);
       }
     }
-    cudaEventRecord(c->dfork, st);
+    cudaEvent_t dfork = c->dfork_g[gi];
+    cudaEventRecord(dfork, st);
     for (int h = 0; h < dpar; h++) {
       const int h0 = (int)((long long)n * h / dpar), h1 = (int)((long long)n * (h + 1) / dpar);
       Bufs bh = b;
       bh.s0 = b.s0 + h0;
       bh.frames = b.frames + (long long)h0 * b.frame_stride;
       const int nh = h1 - h0, pb = (nh + 1) * (int)sizeof(int);
-      cudaStream_t ds = c->dstreams[h];
-      cudaStreamWaitEvent(ds, c->dfork, 0);
+      cudaStream_t ds = c->dstreams[gi * dpar + h];
+      cudaStreamWaitEvent(ds, dfork, 0);
       k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh); DBG_SYNC(st, "k_sat");
       k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 0); DBG_SYNC(st, "k_desc_sample");
       k_desc_orient<<<c->dorient_grid, DO_THREADS, pb, ds>>>(g, bh, nh); DBG_SYNC(st, "k_desc_orient");
       k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 1); DBG_SYNC(st, "k_desc_sample");
-      cudaEventRecord(c->djoin[h], ds);
+      cudaEventRecord(c->djoin[gi * dpar + h], ds);
     }
-    for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[h], 0);
+    for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[gi * dpar + h], 0);
   } else {
     k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n); DBG_SYNC(st, "k_sat");
     stage_mark(c, 6, st);
@@ -993,6 +1005,107 @@ int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int6
   c->b.frame_stride = stream_stride;
   c->b.frame_pitch = row_pitch;
   return launch_frames(c, n_streams, (cudaStream_t)stream);
+}
+
+// Grow the feature capacity of every stream to new_cap, keeping each
+// stream's previous list (the buffer the next step reads) at the end of its
+// new buffer.  Called between a rolled-back step and its replay.
+static int regrow(vf_ctx* c, long long new_cap, cudaStream_t st)
+{
+  Geo& g = c->g;
+  Bufs& b = c->b;
+  const int S = c->S;
+  const long long cap = g.kp_cap;
+  new_cap = std::min(new_cap, 1LL << 28);
+  if (new_cap <= cap) return VF_ERR_CAPACITY;
+  std::vector<int> ctr((size_t)S * C_NCTR);
+  cudaError_t e = cudaMemcpyAsync(ctr.data(), b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  Alloc& A = c->mem;
+  const int chunks = cdiv(new_cap, 1024);
+  // per-stream scratch (no contents to keep)
+  auto fresh = [&](auto*& ptr, size_t n) {
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
+    using U = std::remove_const_t<T>;
+    U* q = A.get<U>(n);
+    if (!q) return false;
+    A.drop((void*)ptr);
+    ptr = q;
+    return true;
+  };
+  bool ok = fresh(b.gidx, (size_t)S * new_cap) && fresh(b.st_x, (size_t)S * new_cap) &&
+            fresh(b.st_y, (size_t)S * new_cap) && fresh(b.st_s, (size_t)S * new_cap) &&
+            fresh(b.st_v, (size_t)S * new_cap) && fresh(b.prop_cnt, (size_t)S * chunks) &&
+            fresh(b.prop_out, (size_t)S * chunks);
+  if (ok && b.bm_found) ok = fresh(b.bm_found, (size_t)S * new_cap) && fresh(b.bm_chunk, (size_t)S * chunks);
+  if (!ok) return cuda_status(A.err);
+  // feature lists [S][2][cap]: the previous buffer's list moves to the end of the new buffer
+  auto moved = [&](auto*& ptr, size_t esz) {
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
+    T* q = A.get<T>((size_t)S * 2 * new_cap * (esz / sizeof(T)));
+    if (!q) return false;
+    for (int s = 0; s < S; s++) {
+      const int* cs = &ctr[(size_t)s * C_NCTR];
+      const int prev = (cs[C_FRAME] & 1) ^ 1;
+      const long long n = std::min<long long>(cs[C_NFEAT0 + prev], cap);
+      if (cs[C_FRAME] == 0 || n <= 0) continue;
+      const char* src = reinterpret_cast<const char*>(ptr) + (((long long)s * 2 + prev) * cap + cap - n) * esz;
+      char* dst = reinterpret_cast<char*>(q) + (((long long)s * 2 + prev) * new_cap + new_cap - n) * esz;
+      if (cudaMemcpyAsync(dst, src, n * esz, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return false;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return false;
+    A.drop((void*)ptr);
+    ptr = q;
+    return true;
+  };
+  ok = moved(b.fx, 8) && moved(b.fy, 8) && moved(b.fs, 8) && moved(b.ft, 8) && moved(b.fv, 8) && moved(b.forg, 1) &&
+       moved(b.fage, 4) && moved(b.fdesc, 64);
+  if (!ok) return VF_ERR_CUDA;
+  g.kp_cap = (int)new_cap;
+  g.prop_chunks = chunks;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  pipe_free(c);   // re-created with the new capacity on the next submit
+  return VF_OK;
+}
+
+int vf_process_checked(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n_streams,
+                       void* stream)
+{
+  int rc = vf_process(c, frames_dev, stream_stride, row_pitch, n_streams, stream);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int attempt = 0; attempt < 16; attempt++) {
+    std::vector<int> ctr((size_t)n_streams * C_NCTR);
+    cudaError_t e = cudaMemcpyAsync(ctr.data(), c->b.ctr, sizeof(int) * ctr.size(), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_status(e);
+    long long need = 0;
+    bool over = false;
+    for (int s = 0; s < n_streams; s++) {
+      const int* cs = &ctr[(size_t)s * C_NCTR];
+      if (!cs[C_ERR]) continue;
+      over = true;
+      // staged candidates bound the detections; plus the propagated features
+      need = std::max(need, (long long)cs[C_STAGE] + cs[C_NPROP]);
+    }
+    if (!over) return VF_OK;
+    if (c->g.mask_mode == 3) return VF_ERR_CAPACITY;   // temporal mode keeps no replay state
+    k_rollback<<<cdiv(n_streams, 128), 128, 0, st>>>(c->b.ctr, c->b.report, 0, n_streams);
+    for (int s = 0; s < n_streams; s++) c->frames_done[s]--;
+    rc = regrow(c, std::max(2LL * c->g.kp_cap, need + need / 4 + 1024), st);
+    if (rc) return rc;
+    rc = vf_process(c, frames_dev, stream_stride, row_pitch, n_streams, stream);
+    if (rc) return rc;
+  }
+  return VF_ERR_CAPACITY;
+}
+
+int vf_get_capacity(const vf_ctx* c, int32_t* kp_capacity)
+{
+  if (!c || !kp_capacity) return VF_ERR_ARG;
+  *kp_capacity = c->g.kp_cap;
+  return VF_OK;
 }
 
 int vf_process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch, int n_streams,

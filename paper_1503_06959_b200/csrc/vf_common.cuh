@@ -149,6 +149,15 @@ __device__ __forceinline__ const uint8_t* layer_ptr(const Geo& g, const Bufs& b,
   return b.layers + (long long)s * g.layer_slab + g.L[l].layer_off;
 }
 
+// IDDM state of octave level lv: the source octave of frame f is kept at
+// parity f & 1 (prev = 1 reads the previous frame's, parity (f & 1) ^ 1), so a
+// step can be replayed (capacity retry) without losing the previous octave.
+__device__ __forceinline__ uint8_t* iddm_state(const Geo& g, const Bufs& b, int s, int lv, int prev)
+{
+  const int par = (b.ctr[s * C_NCTR + C_FRAME] & 1) ^ prev;
+  return b.state + ((long long)s * 2 + par) * g.state_slab + g.state_off[lv];
+}
+
 // Grid used to gate layer l (per_layer: its octave level's grid, else grid 0).
 __device__ __forceinline__ int grid_of_layer(const Geo& g, int l) { return g.per_layer ? (l >> 1) : 0; }
 

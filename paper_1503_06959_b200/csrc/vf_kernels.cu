@@ -327,14 +327,15 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
       if (vw <= 0 || vh <= 0) continue;
       const GridGeo& G = g.grid[g.per_layer ? lv : 0];
       const uint8_t* cur = smem + off[l];
-      uint8_t* st = b.state + (long long)s * g.state_slab + g.state_off[lv];
+      uint8_t* st = iddm_state(g, b, s, lv, 0);
+      const uint8_t* stp = iddm_state(g, b, s, lv, 1);
       uint8_t* cells = b.cells + (long long)s * g.cell_slab + G.cell_off;
       for (int i = tid; i < vw * vh; i += nt) {
         int y = i / vw, x = i - y * vw;
         long long gi = (long long)(gy0 + y) * g.L[l].w + gx0 + x;
         int c = cur[y * lw + x];
         if (um) {
-          int p = st[gi];
+          int p = stp[gi];
           int d = c - p;
           d = d < 0 ? -d : d;
           int bit = (double)d > g.t_i;   // int16 diff vs float t_i, strict
@@ -722,10 +723,10 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
       if (gy0 + y < L.h && gx0 + x < L.w) {
         const GridGeo& G = g.grid[0];
         const long long gi = (long long)(gy0 + y) * L.w + gx0 + x;
-        uint8_t* st = b.state + (long long)s * g.state_slab + g.state_off[3];
+        uint8_t* st = iddm_state(g, b, s, 3, 0);
         const int c = so3[y * 12 + x];
         if (um) {
-          int d = c - (int)st[gi];
+          int d = c - (int)iddm_state(g, b, s, 3, 1)[gi];
           d = d < 0 ? -d : d;
           const int bit = (double)d > g.t_i;   // int16 diff vs float t_i, strict
           b.cells[(long long)s * g.cell_slab + G.cell_off + gi] = (uint8_t)bit;
@@ -916,13 +917,13 @@ __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, co
   if (g.mask_mode == 1) {
     const GridGeo& G = g.grid[0];
     const bool um = use_mask(g, b, s);
-    uint8_t* st = b.state + (long long)s * g.state_slab + g.state_off[3];
+    uint8_t* st = iddm_state(g, b, s, 3, 0);
     const int gi = y3 * L3.w + x3;
     int bit = 0;
     unsigned covered = 0;
     if (in3) {
       if (um) {
-        int d = c3 - (int)st[gi];
+        int d = c3 - (int)iddm_state(g, b, s, 3, 1)[gi];
         d = d < 0 ? -d : d;
         bit = (double)d > g.t_i;
         b.cells[(long long)s * g.cell_slab + G.cell_off + gi] = (uint8_t)bit;
@@ -2036,8 +2037,15 @@ __global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant
     const int n_prop = um ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
     int* ctr = b.ctr + s * C_NCTR;
     int n_total = n_det + n_prop;
-    if (n_total > g.kp_cap) { ctr[C_ERR] |= VF_ERRBIT_CAPACITY; n_total = g.kp_cap; }
-    ctr[C_NDET] = n_det; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
+    int n_desc = n_det;   // detected records the describe kernels write
+    if (n_total > g.kp_cap) {
+      // overflow: flagged (vf_process_checked grows the capacity and replays);
+      // the describe writes are clamped so they cannot overlap the propagated tail
+      ctr[C_ERR] |= VF_ERRBIT_CAPACITY;
+      n_total = g.kp_cap;
+      n_desc = max(0, g.kp_cap - n_prop);
+    }
+    ctr[C_NDET] = n_desc; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
     ctr[C_NSURV] = n_surv;
     ctr[C_TICKET] = 0;
     const double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
@@ -2616,6 +2624,22 @@ __global__ void k_reset(int* ctr, unsigned long long* cov, double* report, int n
   ctr[s * C_NCTR + C_EPOCH] += 1;
   cov[s] = 0ull;
   for (int k = 0; k < 16; k++) report[(long long)s * 16 + k] = 0.0;
+}
+
+// Capacity retry (vf_process_checked): undo the counters of the step just run
+// on streams [s0, s0 + n) so it can be replayed from the same state.  The
+// previous feature buffer and the previous IDDM octave (the other parity)
+// were only read by the step; activity stamps are epoch-based and the epoch
+// stays monotonic.
+__global__ void k_rollback(int* ctr, double* report, int s0, int n)
+{
+  const int s = s0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s0 + n) return;
+  int* c = ctr + s * C_NCTR;
+  c[C_FRAME] -= 1;
+  c[C_ERR] = 0;
+  double* rp = report + (long long)s * 16;
+  rp[8] -= rp[0]; rp[9] -= rp[2]; rp[10] -= rp[4]; rp[11] -= 1.0;
 }
 
 // ============================================================================

@@ -67,8 +67,13 @@ class FeatureEngine:
         self.layer_w, self.layer_h, self.layer_scale = ws, hs, sc
 
     # -- processing -----------------------------------------------------------
-    def process(self, frames, stream=None) -> None:
-        """frames: CUDA uint8 tensor [S, H, W] (or [H, W] for S = 1), device-resident."""
+    def process(self, frames, stream=None, check: bool = False) -> None:
+        """frames: CUDA uint8 tensor [S, H, W] (or [H, W] for S = 1), device-resident.
+
+        check=True synchronizes after the step and, if a stream's features
+        overflowed the capacity, grows it and replays the step from the saved
+        state (vf_process_checked); the default leaves the step asynchronous
+        and a capacity overflow is reported by report()/features calls."""
         import torch
 
         if frames.dim() == 2:
@@ -80,8 +85,15 @@ class FeatureEngine:
             raise ValueError(f"frame {W}x{H} does not match the engine's {self.width}x{self.height}")
         if frames.stride(2) != 1:
             frames = frames.contiguous()
-        _native.check(_native.lib().vf_process(self._h, frames.data_ptr(), frames.stride(0), frames.stride(1), S,
-                                               _native.stream_handle(stream)), "vf_process")
+        fn = _native.lib().vf_process_checked if check else _native.lib().vf_process
+        _native.check(fn(self._h, frames.data_ptr(), frames.stride(0), frames.stride(1), S, _native.stream_handle(stream)),
+                      "vf_process")
+
+    @property
+    def kp_capacity(self) -> int:
+        n = ctypes.c_int32(0)
+        _native.check(_native.lib().vf_get_capacity(self._h, ctypes.byref(n)))
+        return int(n.value)
 
     def process_host(self, frames: np.ndarray, stream=None) -> None:
         """frames: host uint8 array [S, H, W]; the H2D copy is part of the call."""

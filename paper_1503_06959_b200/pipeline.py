@@ -59,7 +59,7 @@ def run_pipeline_arrays(frames: list[GrayFrame], cfg: PipelineConfig):
                 raise ValueError("all frames of a sequence must have the same size")
             wall0 = time.perf_counter_ns()
             dev = torch.from_numpy(np.ascontiguousarray(fr.data)).cuda(non_blocking=False)
-            eng.process(dev)
+            eng.process(dev, check=True)
             r = eng.report(0)
             stage, _ = eng.stage_ms()
             f = eng.features_host(0)
@@ -99,7 +99,7 @@ def run_streams(frames, cfg: PipelineConfig, collect: bool = True):
             batch = frames_t[:, n]
             if not batch.is_cuda:
                 batch = batch.cuda()
-            eng.process(batch.contiguous())
+            eng.process(batch.contiguous(), check=True)
             for s in range(S):
                 r = eng.report(s)
                 reps[s].append(FrameReport(frame=n, n_detected=r.n_detected, n_propagated=r.n_propagated,

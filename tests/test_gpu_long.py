@@ -71,7 +71,7 @@ def lockstep(cfg, streams, n_frames, mode="intensity", source=None, kp_capacity=
                 host = np.stack(list(pool.map(lambda g: g.next_frame().numpy(), gens)))
             else:
                 host = np.ascontiguousarray(source(n))
-            eng.process(torch.from_numpy(host).cuda())
+            eng.process(torch.from_numpy(host).cuda(), check=True)
             ref = list(pool.map(lambda i: pipes[i].process(host[i]), range(S)))
             eng.fetch_all(out)
             torch.cuda.synchronize()
@@ -155,3 +155,26 @@ def test_small_capacity_grows_and_matches(mode):
     overflows on the first frames; the engine grows the capacity and replays
     the frame from the saved state, so results still equal the oracle's."""
     assert lockstep(_cfg(5), [1, 2], 6, mode, kp_capacity=4096) == 12
+
+
+def test_capacity_grows_in_place():
+    """The capacity after the retries is large enough for a 1080p frame and
+    the engine keeps using it (no further overflow on later frames)."""
+    import torch
+
+    from paper_1503_06959_b200 import scenes
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    cfg = _cfg(5)
+    fr = scenes.generate(cfg, 3, streams=[2]).numpy()[:, :]          # [1, 3, H, W]
+    eng = FeatureEngine(cfg.width, cfg.height, PipelineConfig(mask=MaskConfig(mode="intensity")), n_streams=1,
+                        kp_capacity=1024)
+    try:
+        for n in range(3):
+            eng.process(torch.from_numpy(fr[:, n]).cuda(), check=True)
+            r = eng.report(0)
+            assert r.n_total <= eng.kp_capacity
+        assert eng.kp_capacity >= r.n_total > 1024
+    finally:
+        eng.close()

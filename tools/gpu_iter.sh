@@ -4,7 +4,7 @@
 tag=${1:-it}
 tests="tests/test_gpu_pipeline.py tests/test_gpu_stages.py tests/test_gpu_configs.py"
 [ "$2" = "long" ] && tests="$tests tests/test_gpu_long.py"
-timeout 900 python -m pytest $tests -x -q -m gpu -k "not capacity" > gpurun_out/${tag}_tests.log 2>&1
+timeout 900 python -m pytest $tests -x -q -m gpu > gpurun_out/${tag}_tests.log 2>&1
 echo "rc=$?" >> gpurun_out/${tag}_tests.log
 for cm in 5:intensity 5:none 4:intensity 1:intensity; do
   c=${cm%%:*}; m=${cm##*:}
