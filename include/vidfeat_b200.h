@@ -206,6 +206,13 @@ int vf_describe(const uint8_t *frame_dev, int W, int H, int64_t pitch, int n, co
 /* intensity_diff_mask (masking.py:84-93) over n pixels. */
 int vf_intensity_mask(const uint8_t *prev_dev, const uint8_t *cur_dev, int64_t n, double t_i,
                       uint8_t *out_dev, void *stream);
+/* ast_corner_score (detector.py:58-71) of n points (xs, ys: int32, each at
+ * least 3 pixels inside the layer; the caller validates) at any arc_len >= 1. */
+int vf_ast_corner_score(const uint8_t *layer_dev, int w, int h, int64_t pitch, int n, const int32_t *xs_dev,
+                        const int32_t *ys_dev, int arc_len, int32_t *out_dev, void *stream);
+/* sad_block (temporal.py:63-67) of `count` pairs of patch_bytes-byte patches. */
+int vf_sad_block(const uint8_t *a_dev, const uint8_t *b_dev, int64_t patch_bytes, int count, int64_t *out_dev,
+                 void *stream);
 /* binning_histogram (masking.py:96-119): hist_dev (rows x cols) uint64, zeroed by the call. */
 int vf_binning_histogram(int n, const double *xs_dev, const double *ys_dev, int W, int H, int rows,
                          int cols, uint64_t *hist_dev, void *stream);

@@ -22,7 +22,8 @@ _LAZY = {
     "orientations_batch": "descriptor", "describe_batch": "descriptor",
     "intensity_diff_mask": "masking", "keypoint_binning_mask": "masking", "upsample_mask": "masking",
     "merge_features": "masking", "binning_histogram": "masking",
-    "run_pipeline": "pipeline", "run_streams": "pipeline",
+    "run_pipeline": "pipeline", "run_streams": "pipeline", "divergence_report": "pipeline",
+    "DivergenceStat": "pipeline",
     "FeatureEngine": "engine",
     "hamming_matrix": "matching", "radius_match": "matching", "Match": "matching",
     "DEFAULT_MATCH_RADIUS": "matching", "MatchConfig": "matching", "project_points": "matching",
@@ -32,7 +33,7 @@ _LAZY = {
     "mean_average_precision": "evaluation", "corner_geometry": "evaluation", "locate_object": "evaluation",
     "tracking_accuracy": "evaluation", "save_ground_truth": "evaluation", "load_ground_truth": "evaluation",
     "load_relevance": "evaluation", "TRACKING_TOLERANCE_PX": "evaluation",
-    "spiral_offsets": "temporal", "spiral_search": "temporal", "baseline_step": "temporal",
+    "spiral_offsets": "temporal", "spiral_search": "temporal", "baseline_step": "temporal", "sad_block": "temporal",
     "dump_features": "report", "parse_features": "report", "emit_report": "report", "summarize": "report",
     "load_sequence": "io", "write_frame": "io",
 }

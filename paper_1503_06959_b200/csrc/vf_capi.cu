@@ -1602,6 +1602,27 @@ int vf_intensity_mask(const uint8_t* prev_dev, const uint8_t* cur_dev, int64_t n
   return cuda_status(cudaGetLastError());
 }
 
+int vf_ast_corner_score(const uint8_t* layer_dev, int w, int h, int64_t pitch, int n, const int32_t* xs_dev,
+                        const int32_t* ys_dev, int arc_len, int32_t* out_dev, void* stream)
+{
+  if (arc_len < 1) return VF_ERR_ARG;   // the reference's min over an empty arc raises
+  if (n < 0 || w < 7 || h < 7 || pitch < w) return VF_ERR_ARG;
+  if (n == 0) return VF_OK;
+  if (!layer_dev || !xs_dev || !ys_dev || !out_dev) return VF_ERR_ARG;
+  k_ast_score<<<cdiv(n, 128), 128, 0, (cudaStream_t)stream>>>(layer_dev, pitch, n, xs_dev, ys_dev, arc_len, out_dev);
+  return cuda_status(cudaGetLastError());
+}
+
+int vf_sad_block(const uint8_t* a_dev, const uint8_t* b_dev, int64_t patch_bytes, int count, int64_t* out_dev,
+                 void* stream)
+{
+  if (patch_bytes < 0 || count < 0) return VF_ERR_ARG;
+  if (count == 0) return VF_OK;
+  if (!a_dev || !b_dev || !out_dev) return VF_ERR_ARG;
+  k_sad_block<<<count, 256, 0, (cudaStream_t)stream>>>(a_dev, b_dev, patch_bytes, count, (long long*)out_dev);
+  return cuda_status(cudaGetLastError());
+}
+
 int vf_binning_histogram(int n, const double* xs_dev, const double* ys_dev, int W, int H, int rows, int cols,
                          uint64_t* hist_dev, void* stream)
 {

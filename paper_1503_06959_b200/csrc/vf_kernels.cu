@@ -2656,6 +2656,59 @@ __global__ void k_intensity_mask(const uint8_t* prev, const uint8_t* cur, long l
   }
 }
 
+// ast_corner_score (detector.py:58-71) at any arc length: the largest t with
+// arc_len contiguous circle pixels (arc starts 0..15, indices mod 16) all
+// > c + t or all < c - t, i.e. max over starts of (min over the arc) - 1,
+// clipped at 0.  Thread per query point (validated on the host).
+__constant__ signed char c_circle[16][2] = {{0, -3}, {1, -3}, {2, -2}, {3, -1}, {3, 0}, {3, 1}, {2, 2}, {1, 3},
+                                            {0, 3}, {-1, 3}, {-2, 2}, {-3, 1}, {-3, 0}, {-3, -1}, {-2, -2}, {-1, -3}};
+__global__ void k_ast_score(const uint8_t* layer, long long pitch, int n, const int* xs, const int* ys, int arc,
+                            int* out)
+{
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = xs[i], y = ys[i];
+  const int c = layer[(long long)y * pitch + x];
+  int d[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) d[k] = (int)layer[(long long)(y + c_circle[k][1]) * pitch + x + c_circle[k][0]] - c;
+  // an arc of >= 16 pixels covers the whole circle (indices repeat mod 16)
+  const int a = arc < 16 ? arc : 16;
+  int best = 0;
+#pragma unroll 1
+  for (int st = 0; st < 16; st++) {
+    int mb = d[st], md = -d[st];
+#pragma unroll 1
+    for (int k = 1; k < a; k++) {
+      int j = st + k;
+      j = j >= 16 ? j - 16 : j;
+      mb = min(mb, d[j]);
+      md = min(md, -d[j]);
+    }
+    best = max(best, max(mb - 1, md - 1));
+  }
+  out[i] = max(best, 0);
+}
+
+// sad_block (temporal.py:63-67): sum of |a - b| of n-byte patches, CTA per patch.
+__global__ void k_sad_block(const uint8_t* a, const uint8_t* b, long long n, int count, long long* out)
+{
+  __shared__ unsigned long long part[32];
+  const uint8_t* pa = a + (long long)blockIdx.x * n;
+  const uint8_t* pb = b + (long long)blockIdx.x * n;
+  unsigned long long acc = 0;
+  for (long long k = threadIdx.x; k < n; k += blockDim.x) acc += (unsigned)abs((int)pa[k] - (int)pb[k]);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+    out[blockIdx.x] = (long long)t;
+  }
+  (void)count;
+}
+
 // binning_histogram (masking.py:96-119)
 __global__ void k_binning_hist(int n, const double* xs, const double* ys, int W, int H, int rows, int cols,
                                unsigned long long* hist)

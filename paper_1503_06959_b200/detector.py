@@ -24,7 +24,7 @@ CIRCLE = np.array(
 )
 
 __all__ = ["CIRCLE", "Candidate", "Keypoint", "DEFAULT_THRESHOLD", "RETRIEVAL_THRESHOLD", "score_map",
-           "detect_candidates", "ast_corner_score", "nms_and_refine", "nms_from_maps"]
+           "detect_candidates", "ast_corner_score", "ast_corner_scores", "nms_and_refine", "nms_from_maps"]
 
 
 def score_map(data: np.ndarray, t: int, mask_bits: np.ndarray | None = None) -> np.ndarray:
@@ -58,16 +58,35 @@ def detect_candidates(layer: GrayFrame, t: int, mask=None, layer_id: tuple[str, 
 
 
 def ast_corner_score(layer: GrayFrame, x: int, y: int, arc_len: int = 9) -> int:
-    """detector.py:58-71 (arc length 9 only, the detector's segment test)."""
-    if arc_len != 9:
-        raise ValueError("the B200 segment test implements arc length 9 (FAST-9/16)")
+    """detector.py:58-71: largest integer t with arc_len contiguous circle
+    pixels all > c + t or all < c - t (any arc length; vf_ast_corner_score)."""
     h, w = layer.data.shape
     if not (3 <= x < w - 3 and 3 <= y < h - 3):
         raise ValueError(f"({x}, {y}) is within 3 pixels of the layer border")
-    y0, y1, x0, x1 = max(0, y - 3), min(h, y + 4), max(0, x - 3), min(w, x + 4)
-    patch = np.zeros((16, 16), np.uint8)
-    patch[8 - (y - y0):8 + (y1 - y), 8 - (x - x0):8 + (x1 - x)] = layer.data[y0:y1, x0:x1]
-    return int(score_map(patch, 1)[8, 8])
+    return int(ast_corner_scores(layer, np.array([x]), np.array([y]), arc_len)[0])
+
+
+def ast_corner_scores(layer: GrayFrame, xs, ys, arc_len: int = 9) -> np.ndarray:
+    """ast_corner_score of many points in one launch (int32 array)."""
+    h, w = layer.data.shape
+    xs = np.ascontiguousarray(xs, np.int32)
+    ys = np.ascontiguousarray(ys, np.int32)
+    if xs.shape != ys.shape:
+        raise ValueError("xs and ys must have the same shape")
+    if xs.size and not (((xs >= 3) & (xs < w - 3) & (ys >= 3) & (ys < h - 3)).all()):
+        bad = int(np.nonzero(~((xs >= 3) & (xs < w - 3) & (ys >= 3) & (ys < h - 3)))[0][0])
+        raise ValueError(f"({int(xs[bad])}, {int(ys[bad])}) is within 3 pixels of the layer border")
+    if int(arc_len) < 1:
+        raise ValueError("zero-size array to reduction operation minimum which has no identity")
+    if xs.size == 0:
+        return np.zeros(0, np.int32)
+    t_ = _dev.torch()
+    d = _dev.to_dev(layer.data)
+    out = _dev.empty(xs.shape, t_.int32)
+    xd, yd = _dev.to_dev(xs), _dev.to_dev(ys)   # keep both alive until the launch is enqueued
+    _native.check(_dev.lib().vf_ast_corner_score(d.data_ptr(), w, h, w, int(xs.size), xd.data_ptr(), yd.data_ptr(),
+                                                 int(arc_len), out.data_ptr(), _dev.stream()), "vf_ast_corner_score")
+    return out.cpu().numpy()
 
 
 def nms_from_maps(maps: list[np.ndarray], width: int, height: int, n_octaves: int,

@@ -13,13 +13,15 @@ equals run_pipeline on that stream alone.
 from __future__ import annotations
 
 import time
+from dataclasses import dataclass, replace
 
 import numpy as np
 
 from .engine import FeatureEngine
 from .types import DETECTED, PROPAGATED, Feature, FrameReport, GrayFrame, Keypoint, MaskConfig, PipelineConfig
 
-__all__ = ["PipelineConfig", "FrameReport", "run_pipeline", "run_pipeline_arrays", "run_streams", "features_from_arrays"]
+__all__ = ["PipelineConfig", "FrameReport", "DivergenceStat", "run_pipeline", "run_pipeline_arrays", "run_streams",
+           "features_from_arrays", "divergence_report", "divergence_from_arrays"]
 
 
 def features_from_arrays(f: dict) -> list[Feature]:
@@ -110,3 +112,83 @@ def run_streams(frames, cfg: PipelineConfig, collect: bool = True):
     finally:
         eng.close()
     return feats, reps
+
+
+# ---------------------------------------------------------------------------
+# divergence_report (pipeline.py:348-398): masked vs full detection, paired
+# keypoints.  Both runs are GPU pipelines; the greedy pairing is host code
+# over the two SoA lists (it is sequential by definition: each masked
+# keypoint takes the nearest unused full keypoint in list order).
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class DivergenceStat:
+    """pipeline.py:74-85."""
+
+    frame: int
+    only_masked: int
+    only_full: int
+    common: int
+
+    @property
+    def preserved(self) -> float:
+        """Fraction of full-detection keypoints present in the masked run."""
+        denom = self.common + self.only_full
+        return 1.0 if denom == 0 else self.common / denom
+
+
+def _match_keypoint_sets(masked: dict, full: dict, pos_tol: float = 1.0, scale_ratio_tol: float = 1.2):
+    """pipeline.py:348-381 on SoA dicts (x, y, sigma): greedy pairing within
+    pos_tol (Euclidean, <=) and scale ratio <= scale_ratio_tol, candidates
+    scanned cell by cell (integer-truncated positions, cells within
+    ceil(pos_tol)) and, inside a cell, in full-list order; a later candidate
+    at an equal distance replaces the earlier one (the reference's <=).
+    Returns (common, only_masked, only_full)."""
+    nm, nf = len(masked["x"]), len(full["x"])
+    if nm == 0 or nf == 0:
+        return 0, nm, nf
+    fx, fy, fs = full["x"], full["y"], full["sigma"]
+    cx_f = fx.astype(np.int64)   # int(f.kp.x): truncation toward zero
+    cy_f = fy.astype(np.int64)
+    order = np.lexsort((np.arange(nf), cx_f, cy_f))
+    keys = cy_f[order] * (1 << 32) + cx_f[order]
+    used = np.zeros(nf, bool)
+    reach = int(np.ceil(pos_tol))
+    mx, my, ms = masked["x"].tolist(), masked["y"].tolist(), masked["sigma"].tolist()
+    common = 0
+    for i in range(nm):
+        x, y, sg = mx[i], my[i], ms[i]
+        cx, cy = int(x), int(y)
+        best_j, best_d = -1, pos_tol
+        for gy in range(cy - reach, cy + reach + 1):
+            for gx in range(cx - reach, cx + reach + 1):
+                k = gy * (1 << 32) + gx
+                a = np.searchsorted(keys, k, "left")
+                b = np.searchsorted(keys, k, "right")
+                for j in order[a:b]:
+                    if used[j]:
+                        continue
+                    d = float(np.hypot(fx[j] - x, fy[j] - y))
+                    ratio = max(fs[j], sg) / min(fs[j], sg)
+                    if d <= best_d and ratio <= scale_ratio_tol:
+                        best_d, best_j = d, j
+        if best_j >= 0:
+            used[best_j] = True
+            common += 1
+    return common, nm - common, nf - common
+
+
+def divergence_from_arrays(masked_frames: list[dict], full_frames: list[dict]) -> list[DivergenceStat]:
+    out = []
+    for n, (m, f) in enumerate(zip(masked_frames, full_frames)):
+        common, only_m, only_f = _match_keypoint_sets(m, f)
+        out.append(DivergenceStat(n, only_m, only_f, common))
+    return out
+
+
+def divergence_report(frames: list[GrayFrame], cfg: PipelineConfig) -> list[DivergenceStat]:
+    """pipeline.py:384-398: run the masked and the full (mode none) pipelines
+    on the GPU side by side and diff their outputs (1 px / 1.2x pairing)."""
+    full_cfg = replace(cfg, mask=replace(cfg.mask, mode="none"))
+    masked, _ = run_pipeline_arrays(frames, cfg)
+    full, _ = run_pipeline_arrays(frames, full_cfg)
+    return divergence_from_arrays(masked, full)

@@ -20,7 +20,34 @@ import numpy as np
 from . import _dev, _native
 from .types import PROPAGATED, Feature, GopConfig, GrayFrame
 
-__all__ = ["GopConfig", "spiral_offsets", "spiral_search", "baseline_step", "block_match_device"]
+__all__ = ["GopConfig", "spiral_offsets", "spiral_search", "baseline_step", "block_match_device", "sad_block",
+           "sad_blocks"]
+
+
+def sad_block(a: np.ndarray, b: np.ndarray) -> int:
+    """temporal.py:63-67: sum of absolute pixel differences of two equal-size patches."""
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        raise ValueError(f"patch dimensions differ: {a.shape} vs {b.shape}")
+    return int(sad_blocks(a[None], b[None])[0])
+
+
+def sad_blocks(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """sad_block of count pairs of uint8 patches [count, ...] in one launch (vf_sad_block)."""
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    if a.shape != b.shape:
+        raise ValueError(f"patch dimensions differ: {a.shape} vs {b.shape}")
+    count = a.shape[0]
+    if count == 0:
+        return np.zeros(0, np.int64)
+    t_ = _dev.torch()
+    out = _dev.empty((count,), t_.int64)
+    n = int(np.prod(a.shape[1:]))
+    ad, bd = _dev.to_dev(a), _dev.to_dev(b)   # keep both alive until the launch is enqueued
+    _native.check(_dev.lib().vf_sad_block(ad.data_ptr(), bd.data_ptr(), n, count, out.data_ptr(), _dev.stream()),
+                  "vf_sad_block")
+    return out.cpu().numpy()
 
 
 def spiral_offsets(radius: float, step: float) -> np.ndarray:

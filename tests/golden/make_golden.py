@@ -592,7 +592,50 @@ def make_ransac():
           "mpr", out["mv_mpr"], "locate", int(est.object_id), int(est.mpr))
 
 
+def make_divergence():
+    """divergence_report (pipeline.py:348-398) on the first 6 frames of the
+    reference's acceptance-c03 trend scene (test_acceptance.py:57-73: a
+    textured object covering 25% of the VGA frame sweeping over a static
+    textured background), threshold 40, t_i = 20; plus ast_corner_score at
+    several arc lengths (detector.py:58-71) and sad_block (temporal.py:63-67)."""
+    import_reference()
+    from vidfeat import detector, temporal
+    from vidfeat.masking import MaskConfig
+    from vidfeat.pipeline import PipelineConfig, divergence_report
+    from vidfeat.pyramid import GrayFrame
+    from vidfeat.synth import SceneObject, SceneSpec, synth_sequence
+
+    w, h = 640, 480
+    obj = SceneObject(object_id=0, size=(w // 2, h // 2), start=(32.0, 24.0), velocity=(8.0, 0.0), texture_seed=7,
+                      block=8, block_parity=True)
+    scene = SceneSpec(background_seed=0, detail=60, blob_cell=16, objects=(obj,))
+    frames, _ = synth_sequence(scene, 6, (w, h), seed=1)
+    cfg = PipelineConfig(threshold=40, mask=MaskConfig(mode="intensity", t_i=20))
+    stats = divergence_report(frames, cfg)
+    out = {"frames": np.stack([f.data for f in frames]), "threshold": np.array(40), "t_i": np.array(20.0),
+           "only_masked": np.array([s.only_masked for s in stats]), "only_full": np.array([s.only_full for s in stats]),
+           "common": np.array([s.common for s in stats]), "preserved": np.array([s.preserved for s in stats])}
+    rng = np.random.default_rng(99)
+    layer = rng.integers(0, 256, (48, 64), dtype=np.uint8)
+    layer[20:28, 30:38] = 250   # bright blocks give long arcs
+    xs = rng.integers(3, 61, 200)
+    ys = rng.integers(3, 45, 200)
+    arcs = (1, 2, 5, 9, 12, 16, 20)
+    out["ast_layer"], out["ast_x"], out["ast_y"], out["ast_arcs"] = layer, xs, ys, np.array(arcs)
+    out["ast_scores"] = np.array([[detector.ast_corner_score(GrayFrame(layer), int(x), int(y), a) for x, y in zip(xs, ys)]
+                                  for a in arcs], np.int64)
+    pa = rng.integers(0, 256, (40, 16, 16), dtype=np.uint8)
+    pb = rng.integers(0, 256, (40, 16, 16), dtype=np.uint8)
+    out["sad_a"], out["sad_b"] = pa, pb
+    out["sad"] = np.array([temporal.sad_block(a, b) for a, b in zip(pa, pb)], np.int64)
+    np.savez_compressed(HERE / "divergence.npz", **out)
+    print("divergence", out["common"], out["only_full"], out["only_masked"], np.round(out["preserved"], 3))
+
+
 if __name__ == "__main__":
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "divergence":
+        make_divergence()
+        sys.exit(0)
     if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "formats":
         make_formats()
         sys.exit(0)
@@ -610,3 +653,4 @@ if __name__ == "__main__":
         make_temporal()
         make_formats()
         make_ransac()
+        make_divergence()

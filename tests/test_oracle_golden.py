@@ -212,3 +212,24 @@ def test_gop_config_validation():
                     ({"t_et": 0.0}, "SAD thresholds")]:
         with pytest.raises(ValueError, match=msg):
             GopConfig(**kw)
+
+
+def test_divergence_report_matches_reference():
+    """pipeline.divergence_from_arrays (the host pairing of divergence_report,
+    pipeline.py:348-398) applied to the oracle's masked and full runs equals
+    the reference's DivergenceStat counts on its c03 trend scene (half size)."""
+    from oracle import oracle
+    from paper_1503_06959_b200.pattern import default_pattern
+    from paper_1503_06959_b200.pipeline import divergence_from_arrays
+
+    g = golden("divergence.npz")
+    frames = list(g["frames"])
+    kw = dict(threshold=int(g["threshold"]), t_i=float(g["t_i"]))
+    m = oracle.run_sequence(frames, default_pattern(), mode="intensity", **kw)
+    f = oracle.run_sequence(frames, default_pattern(), mode="none", **kw)
+    soa = lambda r: {"x": r.x, "y": r.y, "sigma": r.sigma}  # noqa: E731
+    stats = divergence_from_arrays([soa(r) for r in m], [soa(r) for r in f])
+    assert [s.common for s in stats] == g["common"].tolist()
+    assert [s.only_masked for s in stats] == g["only_masked"].tolist()
+    assert [s.only_full for s in stats] == g["only_full"].tolist()
+    assert np.allclose([s.preserved for s in stats], g["preserved"])
