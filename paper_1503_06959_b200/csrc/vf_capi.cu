@@ -324,7 +324,11 @@ struct vf_ctx {
   // CUDA graph of one step (small batches): the step's launches (all its
   // streams) captured once per batch size and replayed; inputs are copied
   // into a context-owned buffer first so the graph's pointers stay fixed
+#ifdef VF_DEBUG
+  int graphs = 0;                       // debug builds synchronize after every launch: no capture
+#else
   int graphs = 1;                       // vf_set_graphs
+#endif
   cudaGraphExec_t gexec = nullptr;
   int g_n = 0;
   int eager_n = 0;                      // batch size of the last eager step (streams / events exist)

@@ -1,0 +1,86 @@
+"""Concurrency stress in place of compute-sanitizer racecheck (closed on this
+GPU pool): the step runs on up to three priority classes of CUDA streams
+(main, side-stream propagation / carries, two concurrent SAT + describe
+halves), with epoch stamps instead of clears and atomics for staging.  A race
+between them shows up as a result that depends on the launch arrangement.
+Every arrangement below -- CUDA graph or eager launches, one or two describe
+halves, one or three stream groups, the priority stream on or off -- must give
+bit-identical features (and equal the CPU oracle) over 8 frames of 6 config-5
+streams in each mode, each arrangement in a fresh process (the knobs are read
+once per process)."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+ARRANGEMENTS = {
+    "graph": {},
+    "eager": {"VF_GRAPHS": "0"},
+    "one_half": {"VF_DESC_PAR": "1", "VF_GRAPHS": "0"},
+    "groups3": {"VF_STREAM_GROUPS": "3", "VF_GRAPHS": "0"},
+    "no_prio": {"VF_PRIO": "0", "VF_GRAPHS": "0"},
+    "no_split_pyramid": {"VF_PYR_SPLIT": "0"},
+}
+
+CHILD = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1503_06959_b200 import scenes
+from paper_1503_06959_b200.engine import FeatureEngine
+from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+mode, out = sys.argv[2], sys.argv[3]
+cfg = scenes.CONFIGS[5]
+fr = scenes.generate(cfg, 8, streams=range(6)).permute(1, 0, 2, 3).contiguous()
+# a 720p crop keeps the batch under the graph threshold (6 x 0.9 MB)
+fr = fr[:, :, :720, :1280].contiguous().cuda()
+eng = FeatureEngine(1280, 720, PipelineConfig(mask=MaskConfig(mode=mode)), n_streams=6)
+res = {}
+for n in range(8):
+    eng.process(fr[n])
+    f = eng.fetch_all()
+    torch.cuda.synchronize()
+    o = f["offsets"][:7].copy()
+    res[n] = {k: f[k][:o[6]].copy() for k in ("x", "y", "sigma", "theta", "score", "origin", "age", "desc")}
+    res[n]["offsets"] = o
+eng.close()
+np.savez(out, **{f"{n}_{k}": v for n, d in res.items() for k, v in d.items()})
+"""
+
+
+def _run(mode, name, env_over, tmp):
+    out = tmp / f"{mode}_{name}.npz"
+    env = dict(os.environ, **env_over)
+    r = subprocess.run([sys.executable, "-c", CHILD, str(ROOT), mode, str(out)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return dict(np.load(out))
+
+
+@pytest.mark.parametrize("mode", ["intensity", "binning", "none"])
+def test_launch_arrangements_bit_identical(mode, tmp_path):
+    results = {name: _run(mode, name, env, tmp_path) for name, env in ARRANGEMENTS.items()}
+    base = results["graph"]
+    for name, r in results.items():
+        assert r.keys() == base.keys()
+        for k in base:
+            assert np.array_equal(r[k], base[k]), (name, k)
+    # and the arrangement-independent result is the oracle's
+    from oracle import oracle
+    from paper_1503_06959_b200 import scenes
+    from paper_1503_06959_b200.pattern import default_pattern
+
+    fr = scenes.generate(scenes.CONFIGS[5], 8, streams=range(6)).numpy()[:, :, :720, :1280]
+    for s in range(6):
+        ref = oracle.run_sequence(list(np.ascontiguousarray(fr[s])), default_pattern(), mode=mode)
+        for n, e in enumerate(ref):
+            o = base[f"{n}_offsets"]
+            a, b = int(o[s]), int(o[s + 1])
+            assert np.array_equal(base[f"{n}_x"][a:b], e.x) and np.array_equal(base[f"{n}_desc"][a:b], e.desc), (s, n)
