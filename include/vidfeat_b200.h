@@ -126,6 +126,9 @@ int vf_get_capacity(const vf_ctx *ctx, int32_t *kp_capacity);
  * the call (double-buffered device staging, stream-ordered). */
 int vf_process_host(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,
                     int n_streams, void *stream);
+/* vf_process_host with the capacity check / grow / replay of vf_process_checked. */
+int vf_process_host_checked(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,
+                            int n_streams, void *stream);
 /* Synchronizes `stream`, then reports the last processed frame of `s`.
  * Returns VF_ERR_CAPACITY if a capacity overflow was flagged on the device. */
 int vf_get_report(vf_ctx *ctx, int s, vf_report *out, void *stream);

@@ -1112,8 +1112,23 @@ int vf_get_capacity(const vf_ctx* c, int32_t* kp_capacity)
   return VF_OK;
 }
 
+static int process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch,
+                        int n_streams, void* stream, bool checked);
+
 int vf_process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch, int n_streams,
                     void* stream)
+{
+  return process_host(c, frames_host, stream_stride, row_pitch, n_streams, stream, false);
+}
+
+int vf_process_host_checked(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch,
+                            int n_streams, void* stream)
+{
+  return process_host(c, frames_host, stream_stride, row_pitch, n_streams, stream, true);
+}
+
+static int process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride, int64_t row_pitch,
+                        int n_streams, void* stream, bool checked)
 {
   if (!c || !frames_host || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1140,7 +1155,8 @@ int vf_process_host(vf_ctx* c, const uint8_t* frames_host, int64_t stream_stride
                             cudaMemcpyHostToDevice, st);
   }
   if (e != cudaSuccess) return cuda_status(e);
-  return vf_process(c, dst, fbytes, c->g.W, n_streams, stream);
+  return checked ? vf_process_checked(c, dst, fbytes, c->g.W, n_streams, stream)
+                 : vf_process(c, dst, fbytes, c->g.W, n_streams, stream);
 }
 
 int vf_get_report(vf_ctx* c, int s, vf_report* out, void* stream)
