@@ -478,7 +478,7 @@ def run_detect(args, rank, world, local):
     Wm, K = args.warmup, args.steps
     e2e_k = 0 if args.no_e2e else max(1, min(args.e2e_steps, K))
     stage_k = max(1, min(10, K))   # eager steps with per-stage CUDA events, after the timed region
-    n_frames = Wm + K + stage_k + e2e_k
+    n_frames = Wm + K + stage_k + 2 * e2e_k   # e2e: delta results, then full lists
     dev = torch.device("cuda", local)
     t0g = time.perf_counter()
     if args.gen == "cpu":
@@ -589,44 +589,63 @@ def run_detect(args, rank, world, local):
         "coverage_by_stream": {"min": float(fs[:, :, 5].mean(1).min()), "max": float(fs[:, :, 5].mean(1).max())},
     }
 
-    # ---- e2e: public API with host buffers (H2D of frames + D2H of features inside) ----
-    e2e = None
+    # ---- e2e: public API with host buffers (H2D of frames + D2H of results inside) ----
+    # Two runs of the pipelined API (vf_pipeline_submit / collect, two steps in
+    # flight: H2D of step n+1 and D2H of step n-1 overlap step n):
+    #   e2e            each step's result as a delta (vf_pipeline_collect_delta):
+    #                  the newly detected records + the Eq. 1 keep mask of every
+    #                  previous list; the consumer holds list n-1, and
+    #                  vf_delta_apply rebuilds list n bit-exactly (tested);
+    #   e2e_full_lists every stream's whole merged list copied every step.
+    e2e = e2e_full = None
     if e2e_k:
-        host = frames[Wm + K + stage_k:Wm + K + stage_k + e2e_k].cpu().pin_memory()
-        h2d = S * H * W
-        out = eng.alloc_host(S * max(65536, W * H // 8))
-        d2h_total = 0
-        eng.submit(frames[Wm + K + stage_k - 1].cpu().numpy())   # untimed warm-up of the pipelined path
-        eng.collect(out)
-        torch.cuda.synchronize()
-        if pg:
-            dist.barrier()
-        t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        eng.submit(host[0].numpy())
-        for n in range(e2e_k):
-            if n + 1 < e2e_k:
-                eng.submit(host[n + 1].numpy())
-            eng.collect(out)
-            d2h_total += int(out["offsets"][S]) * (5 * 8 + 1 + 4 + 64)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
-        tt = torch.tensor([e2e_ms, S * e2e_k, float(d2h_total)], dtype=torch.float64, device=dev)
-        if world > 1:
-            m2 = tt.clone()
-            dist.all_reduce(m2[:1], op=dist.ReduceOp.MAX)
-            s2 = tt.clone()
-            dist.all_reduce(s2, op=dist.ReduceOp.SUM)
-            e2e_ms, e2e_frames, d2h_total = float(m2[0]), float(s2[1]), float(s2[2])
-        else:
-            e2e_frames = S * e2e_k
-        e2e = {"value": e2e_frames / (e2e_ms / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h_total / e2e_k),
-               "steps": e2e_k, "api": "vf_pipeline_submit (pinned frames, H2D) + vf_pipeline_collect (all features, "
-                                      "D2H to pinned), 2 steps in flight"}
+        def e2e_run(first, delta):
+            host = frames[first:first + e2e_k].cpu().pin_memory()
+            out = eng.alloc_delta(S * max(65536, W * H // 8)) if delta else eng.alloc_host(S * max(65536, W * H // 8))
+            collect = eng.collect_delta if delta else eng.collect
+            eng.set_delta(delta)
+            eng.submit(frames[first - 1].cpu().numpy())   # untimed warm-up (buffers / streams)
+            collect(out)
+            torch.cuda.synchronize()
+            if pg:
+                dist.barrier()
+            d2h_total = 0
+            t0 = time.perf_counter()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.submit(host[0].numpy())
+            for n in range(e2e_k):
+                if n + 1 < e2e_k:
+                    eng.submit(host[n + 1].numpy())
+                collect(out)
+                if delta:
+                    d2h_total += int(out["offsets"][S]) * (5 * 8 + 64) + 4 * int(out["keep_offsets"][S]) + 12 * S
+                else:
+                    d2h_total += int(out["offsets"][S]) * (5 * 8 + 1 + 4 + 64)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_ = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
+            tt = torch.tensor([ms_, S * e2e_k, float(d2h_total)], dtype=torch.float64, device=dev)
+            if world > 1:
+                m2 = tt.clone()
+                dist.all_reduce(m2[:1], op=dist.ReduceOp.MAX)
+                s2 = tt.clone()
+                dist.all_reduce(s2, op=dist.ReduceOp.SUM)
+                ms_, fr_, d2h_total = float(m2[0]), float(s2[1]), float(s2[2])
+            else:
+                fr_ = S * e2e_k
+            return {"value": fr_ / (ms_ / 1e3), "unit": "frames/s", "h2d_bytes_per_step": int(S * H * W * world),
+                    "d2h_bytes_per_step": int(d2h_total / e2e_k), "steps": e2e_k}
+
+        base = Wm + K + stage_k
+        e2e = e2e_run(base, True)
+        e2e["api"] = ("vf_pipeline_submit (pinned frames, H2D) + vf_pipeline_collect_delta (every stream's new "
+                      "records + Eq. 1 keep mask of its previous list, D2H to pinned; vf_delta_apply rebuilds the "
+                      "merged lists bit-exactly), 2 steps in flight")
+        e2e_full = e2e_run(base + e2e_k, False)
+        e2e_full["api"] = ("vf_pipeline_submit + vf_pipeline_collect (every stream's whole merged list, D2H to "
+                           "pinned), 2 steps in flight")
 
     if rank != 0:
         eng.close()
@@ -727,6 +746,7 @@ def run_detect(args, rank, world, local):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_full_lists": e2e_full,
         "stream_stats": stream_stats,
         "gpu_launches": launches_per_step(args.mode, S) * K,
         "clocks": clk.summary(),

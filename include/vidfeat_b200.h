@@ -158,6 +158,28 @@ int vf_pipeline_submit(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_s
                        int n_streams);
 int vf_pipeline_collect(vf_ctx *ctx, int64_t cap, double *x, double *y, double *sigma, double *theta,
                         double *score, uint8_t *origin, int32_t *age, uint8_t *desc, int32_t *offsets);
+/* Delta results for the pipelined API: with vf_pipeline_set_delta(ctx, 1)
+ * (between steps), vf_pipeline_collect_delta returns each step's result as
+ * the DETECTED records of every stream (packed as in vf_fetch_features,
+ * stream s at det_offsets[s] .. det_offsets[s+1]; origin detected, age 0)
+ * plus the Eq. 1 keep mask of the stream's previous list (32-bit words at
+ * keep_offsets[s] .., bit i = previous feature i propagates) and counts[3 s ..]
+ * = n_detected, n_propagated, previous-list length covered by the mask.  The
+ * merged list (masking.py:176-183) is detected ++ [previous[i] with origin
+ * propagated and age + 1, for every kept i] -- vf_delta_apply rebuilds it on
+ * the host from the previous list.  D2H per step is the new records only. */
+int vf_pipeline_set_delta(vf_ctx *ctx, int enable);
+int vf_pipeline_collect_delta(vf_ctx *ctx, int64_t cap, double *x, double *y, double *sigma, double *theta,
+                              double *score, uint8_t *desc, int32_t *det_offsets, int64_t kcap, uint32_t *keep_bits,
+                              int32_t *keep_offsets, int32_t *counts);
+/* Host only: list n of one stream from list n-1 and the stream's delta. */
+int vf_delta_apply(int32_t n_prev, const double *prev_x, const double *prev_y, const double *prev_sigma,
+                   const double *prev_theta, const double *prev_score, const uint8_t *prev_origin,
+                   const int32_t *prev_age, const uint8_t *prev_desc, int32_t n_det, const double *det_x,
+                   const double *det_y, const double *det_sigma, const double *det_theta, const double *det_score,
+                   const uint8_t *det_desc, int32_t n_keep_bits, const uint32_t *keep_bits, int32_t out_cap,
+                   double *x, double *y, double *sigma, double *theta, double *score, uint8_t *origin, int32_t *age,
+                   uint8_t *desc, int32_t *n_out);
 /* Device pointers of layer l of stream s's current pyramid (l >= 1; l = 0 is the input frame). */
 int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch);
 /* Live per-stage device timing with CUDA events on the launch stream:

@@ -112,6 +112,9 @@ def lib():
     L.vf_ast_corner_score.argtypes = [_P, c_int, c_int, c_int64, c_int, _P, _P, c_int, _P, c_void_p]
     L.vf_sad_block.argtypes = [_P, _P, c_int64, c_int, _P, c_void_p]
     L.vf_process_host_checked.argtypes = [c_void_p, _P, c_int64, c_int64, c_int, c_void_p]
+    L.vf_pipeline_set_delta.argtypes = [c_void_p, c_int]
+    L.vf_pipeline_collect_delta.argtypes = [c_void_p, c_int64] + [_P] * 7 + [c_int64, _P, _P, _P]
+    L.vf_delta_apply.argtypes = [c_int32] + [_P] * 8 + [c_int32] + [_P] * 6 + [c_int32, _P, c_int32] + [_P] * 9
     L.vf_ransac_homography.argtypes = [c_int, _P, _P, _P, c_int, c_double, c_uint64, _P, _P, _P, c_void_p]
     L.vf_ransac_samples.argtypes = [c_uint64, c_int64, c_int, _P, c_void_p]
     L.vf_ransac_samples_host.argtypes = [c_uint64, c_int64, c_int, _P]
@@ -124,7 +127,8 @@ def lib():
                  "vf_pipeline_collect", "vf_hamming_matrix", "vf_radius_match", "vf_block_match",
                  "vf_format_features", "vf_ransac_homography", "vf_ransac_samples", "vf_ransac_samples_host",
                  "vf_match_timing", "vf_set_history", "vf_set_graphs", "vf_process_checked", "vf_get_capacity",
-                 "vf_ast_corner_score", "vf_sad_block", "vf_process_host_checked"):
+                 "vf_ast_corner_score", "vf_sad_block", "vf_process_host_checked", "vf_pipeline_set_delta",
+                 "vf_pipeline_collect_delta", "vf_delta_apply"):
         getattr(L, name).restype = c_int
     _lib = L
     return L
@@ -139,7 +143,8 @@ EXPORTS = (
     "vf_binning_histogram", "vf_upsample_mask", "vf_mask_values", "vf_hamming_matrix", "vf_radius_match",
     "vf_block_match", "vf_format_features", "vf_ransac_homography", "vf_ransac_samples", "vf_ransac_samples_host",
     "vf_match_timing", "vf_set_history", "vf_set_graphs", "vf_process_checked", "vf_get_capacity",
-    "vf_ast_corner_score", "vf_sad_block", "vf_process_host_checked",
+    "vf_ast_corner_score", "vf_sad_block", "vf_process_host_checked", "vf_pipeline_set_delta",
+    "vf_pipeline_collect_delta", "vf_delta_apply",
 )
 
 

@@ -297,6 +297,14 @@ struct vf_ctx {
     cudaEvent_t ev_h2d[2], ev_comp[2], ev_pre[2], ev_d2h[2];
     long long submitted = 0, collected = 0;
     int n_streams[2];
+    // delta results (vf_pipeline_set_delta): keep masks of the previous lists
+    bool delta = false;
+    uint32_t* kb[2] = {nullptr, nullptr};
+    int* kpre[2] = {nullptr, nullptr};
+    int* kpre_host[2] = {nullptr, nullptr};
+    int* cnt[2] = {nullptr, nullptr};
+    int* cnt_host[2] = {nullptr, nullptr};
+    long long kcap = 0;
   } pipe;
   // live per-stage timing (vf_set_timing): one event before each stage + end
   int timing = 0;
@@ -1043,6 +1051,10 @@ static int regrow(vf_ctx* c, long long new_cap, cudaStream_t st)
             fresh(b.st_v, (size_t)S * new_cap) && fresh(b.prop_cnt, (size_t)S * chunks) &&
             fresh(b.prop_out, (size_t)S * chunks);
   if (ok && b.bm_found) ok = fresh(b.bm_found, (size_t)S * new_cap) && fresh(b.bm_chunk, (size_t)S * chunks);
+  if (ok && b.keep_bits) {
+    ok = fresh(b.keep_bits, (size_t)S * (cdiv(new_cap, 32) + 1));
+    b.keep_words = cdiv(new_cap, 32) + 1;
+  }
   if (!ok) return cuda_status(A.err);
   // feature lists [S][2][cap]: the previous buffer's list moves to the end of the new buffer
   auto moved = [&](auto*& ptr, size_t esz) {
@@ -1302,7 +1314,13 @@ static int pipe_init(vf_ctx* c)
     ok = ok && cudaEventCreateWithFlags(&P.ev_comp[k], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&P.ev_pre[k], cudaEventDisableTiming) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&P.ev_d2h[k], cudaEventDisableTiming) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.kb[k], 4 * (size_t)c->S * c->b.keep_words) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.kpre[k], sizeof(int) * (c->S + 1)) == cudaSuccess;
+    ok = ok && cudaMallocHost(&P.kpre_host[k], sizeof(int) * (c->S + 1)) == cudaSuccess;
+    ok = ok && cudaMalloc(&P.cnt[k], sizeof(int) * 3 * c->S) == cudaSuccess;
+    ok = ok && cudaMallocHost(&P.cnt_host[k], sizeof(int) * 3 * c->S) == cudaSuccess;
   }
+  P.kcap = (long long)c->S * c->b.keep_words;
   if (!ok) return VF_ERR_CUDA;
   P.init = true;
   return VF_OK;
@@ -1319,6 +1337,8 @@ static void pipe_free(vf_ctx* c)
       cudaFree(p);
     cudaFreeHost(P.pre_host[k]);
     cudaFreeHost(P.ctr_host[k]);
+    cudaFree(P.kb[k]); cudaFree(P.kpre[k]); cudaFree(P.cnt[k]);
+    cudaFreeHost(P.kpre_host[k]); cudaFreeHost(P.cnt_host[k]);
     cudaEventDestroy(P.ev_h2d[k]); cudaEventDestroy(P.ev_comp[k]); cudaEventDestroy(P.ev_pre[k]);
     cudaEventDestroy(P.ev_d2h[k]);
   }
@@ -1349,14 +1369,19 @@ int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_str
   cudaEventRecord(P.ev_h2d[k], P.h2d);
   // the whole path, then pack (pack buffer k was last read by the d2h of step submitted-2)
   cudaStreamWaitEvent(P.comp, P.ev_h2d[k], 0);
-  c->b.frames = P.frames[k];
-  c->b.frame_stride = fbytes;
-  c->b.frame_pitch = c->g.W;
-  rc = launch_frames(c, n_streams, P.comp);
+  rc = vf_process(c, P.frames[k], fbytes, c->g.W, n_streams, P.comp);   // graph replay for small batches
   if (rc) return rc;
   cudaStreamWaitEvent(P.comp, P.ev_d2h[k], 0);
-  k_pack<<<g_num_sms * 8, 256, (n_streams + 1) * sizeof(int), P.comp>>>(
-      c->g, c->b, n_streams, -1, P.x[k], P.y[k], P.s[k], P.t[k], P.v[k], P.o[k], P.a[k], P.d[k], P.pre[k], P.cap);
+  if (P.delta) {
+    k_pack_delta<<<g_num_sms * 8, 256, 2 * (n_streams + 1) * sizeof(int), P.comp>>>(
+        c->g, c->b, n_streams, P.x[k], P.y[k], P.s[k], P.t[k], P.v[k], P.d[k], P.kb[k], P.pre[k], P.kpre[k],
+        P.cnt[k], P.cap, P.kcap);
+    cudaMemcpyAsync(P.kpre_host[k], P.kpre[k], sizeof(int) * (n_streams + 1), cudaMemcpyDeviceToHost, P.comp);
+    cudaMemcpyAsync(P.cnt_host[k], P.cnt[k], sizeof(int) * 3 * n_streams, cudaMemcpyDeviceToHost, P.comp);
+  } else {
+    k_pack<<<g_num_sms * 8, 256, (n_streams + 1) * sizeof(int), P.comp>>>(
+        c->g, c->b, n_streams, -1, P.x[k], P.y[k], P.s[k], P.t[k], P.v[k], P.o[k], P.a[k], P.d[k], P.pre[k], P.cap);
+  }
   cudaMemcpyAsync(P.pre_host[k], P.pre[k], sizeof(int) * (n_streams + 1), cudaMemcpyDeviceToHost, P.comp);
   cudaMemcpyAsync(P.ctr_host[k], c->b.ctr, sizeof(int) * n_streams * C_NCTR, cudaMemcpyDeviceToHost, P.comp);
   cudaEventRecord(P.ev_pre[k], P.comp);
@@ -1396,6 +1421,93 @@ int vf_pipeline_collect(vf_ctx* c, int64_t cap, double* x, double* y, double* si
   P.collected++;
   for (int s = 0; s < ns; s++)   // sticky device capacity flags of this step
     if (P.ctr_host[k][(size_t)s * C_NCTR + C_ERR]) return VF_ERR_CAPACITY;
+  return VF_OK;
+}
+
+int vf_pipeline_set_delta(vf_ctx* c, int enable)
+{
+  if (!c) return VF_ERR_ARG;
+  if (c->pipe.submitted != c->pipe.collected) return VF_ERR_ARG;   // only between steps
+  const bool on = enable != 0;
+  if (on && !c->b.keep_bits) {
+    const int kw = cdiv(c->g.kp_cap, 32) + 1;
+    uint32_t* kb = c->mem.get<uint32_t>((size_t)c->S * kw);
+    if (!kb) return cuda_status(c->mem.err);
+    c->b.keep_bits = kb;
+    c->b.keep_words = kw;
+    pipe_free(c);                                   // re-created with keep-mask buffers
+    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  }
+  c->pipe.delta = on;
+  return VF_OK;
+}
+
+int vf_pipeline_collect_delta(vf_ctx* c, int64_t cap, double* x, double* y, double* sigma, double* theta,
+                              double* score, uint8_t* desc, int32_t* det_offsets, int64_t kcap, uint32_t* keep_bits,
+                              int32_t* keep_offsets, int32_t* counts)
+{
+  if (!c || !det_offsets || !keep_offsets || !counts) return VF_ERR_ARG;
+  auto& P = c->pipe;
+  if (!P.init || !P.delta || P.collected >= P.submitted) return VF_ERR_ARG;
+  const int k = (int)(P.collected & 1);
+  cudaError_t e = cudaEventSynchronize(P.ev_pre[k]);
+  if (e != cudaSuccess) return cuda_status(e);
+  const int ns = P.n_streams[k];
+  const long long n = std::min((long long)P.pre_host[k][ns], P.cap);
+  const long long nw = std::min((long long)P.kpre_host[k][ns], P.kcap);
+  for (int s = 0; s <= ns; s++) { det_offsets[s] = P.pre_host[k][s]; keep_offsets[s] = P.kpre_host[k][s]; }
+  for (int i = 0; i < 3 * ns; i++) counts[i] = P.cnt_host[k][i];
+  if (n > cap || nw > kcap) return VF_ERR_CAPACITY;
+  cudaStreamWaitEvent(P.d2h, P.ev_comp[k], 0);
+  if (n > 0) {
+    if (x) cudaMemcpyAsync(x, P.x[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (y) cudaMemcpyAsync(y, P.y[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (sigma) cudaMemcpyAsync(sigma, P.s[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (theta) cudaMemcpyAsync(theta, P.t[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (score) cudaMemcpyAsync(score, P.v[k], 8 * n, cudaMemcpyDeviceToHost, P.d2h);
+    if (desc) cudaMemcpyAsync(desc, P.d[k], 64 * n, cudaMemcpyDeviceToHost, P.d2h);
+  }
+  if (nw > 0 && keep_bits) cudaMemcpyAsync(keep_bits, P.kb[k], 4 * nw, cudaMemcpyDeviceToHost, P.d2h);
+  cudaEventRecord(P.ev_d2h[k], P.d2h);
+  e = cudaEventSynchronize(P.ev_d2h[k]);
+  if (e != cudaSuccess) return cuda_status(e);
+  P.collected++;
+  for (int s = 0; s < ns; s++)
+    if (P.ctr_host[k][(size_t)s * C_NCTR + C_ERR]) return VF_ERR_CAPACITY;
+  return VF_OK;
+}
+
+int vf_delta_apply(int32_t n_prev, const double* prev_x, const double* prev_y, const double* prev_sigma,
+                   const double* prev_theta, const double* prev_score, const uint8_t* prev_origin,
+                   const int32_t* prev_age, const uint8_t* prev_desc, int32_t n_det, const double* det_x,
+                   const double* det_y, const double* det_sigma, const double* det_theta, const double* det_score,
+                   const uint8_t* det_desc, int32_t n_keep_bits, const uint32_t* keep_bits, int32_t out_cap,
+                   double* x, double* y, double* sigma, double* theta, double* score, uint8_t* origin, int32_t* age,
+                   uint8_t* desc, int32_t* n_out)
+{
+  if (!n_out || n_prev < 0 || n_det < 0 || n_keep_bits < 0 || n_keep_bits > n_prev) return VF_ERR_ARG;
+  long long n = n_det;
+  for (int w = 0; w < (n_keep_bits + 31) / 32; w++) n += __builtin_popcount(keep_bits[w]);
+  *n_out = (int32_t)n;
+  if (n > out_cap) return VF_ERR_CAPACITY;
+  // masking.py:176-183: the detected features (origin detected, age 0), then
+  // the kept previous features in their previous order (propagated, age + 1)
+  if (n_det) {
+    memcpy(x, det_x, 8 * (size_t)n_det); memcpy(y, det_y, 8 * (size_t)n_det);
+    memcpy(sigma, det_sigma, 8 * (size_t)n_det); memcpy(theta, det_theta, 8 * (size_t)n_det);
+    memcpy(score, det_score, 8 * (size_t)n_det); memcpy(desc, det_desc, 64 * (size_t)n_det);
+    memset(origin, 0, (size_t)n_det);
+    memset(age, 0, 4 * (size_t)n_det);
+  }
+  long long o = n_det;
+  for (int i = 0; i < n_keep_bits; i++) {
+    if (!((keep_bits[i >> 5] >> (i & 31)) & 1u)) continue;
+    x[o] = prev_x[i]; y[o] = prev_y[i]; sigma[o] = prev_sigma[i]; theta[o] = prev_theta[i]; score[o] = prev_score[i];
+    origin[o] = 1; age[o] = prev_age[i] + 1;
+    memcpy(desc + 64 * o, prev_desc + 64 * (size_t)i, 64);
+    o++;
+  }
+  (void)prev_origin;
   return VF_OK;
 }
 

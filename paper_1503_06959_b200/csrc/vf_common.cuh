@@ -133,6 +133,8 @@ struct Bufs {
   double* report;       // [S][8]: n_det, n_prop, n_total, n_dropped, coverage, frame, n_surv, n_cand
   int* worklist; int* work_count;  // [S][tiles_per_stream] / [S]: active FAST tiles per stream
   double* hist; int hist_frames;  // optional [S][hist_frames][8]: report rows of every frame (vf_set_history)
+  uint32_t* keep_bits;  // optional [S][keep_words]: Eq. 1 keep mask of the previous list (delta collect)
+  int keep_words;
 };
 
 // --------------------------------------------------------------------------

@@ -2496,6 +2496,8 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
       const bool f = e < n_prev && !merge_mask_at(g, b, s, xs[j], ys[j]);
       const unsigned bal = __ballot_sync(0xffffffffu, f);
       if (lane == 0) wsum[j][wid] = __popc(bal);
+      // keep mask of features e - lane .. e - lane + 31 (the delta result of vf_pipeline_collect_delta)
+      if (b.keep_bits && lane == 0 && e < n_prev) b.keep_bits[(long long)s * b.keep_words + (e >> 5)] = bal;
       fl |= (f ? 1u : 0u) << j;
       fl |= (unsigned)__popc(bal & ((1u << lane) - 1)) << (4 + 6 * j);   // rank within the warp (<= 31)
     }
@@ -2586,6 +2588,60 @@ __global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, con
     const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + f * 64);
     uint4* dd = reinterpret_cast<uint4*>(pd + i * 64);
     dd[0] = sd[0]; dd[1] = sd[1]; dd[2] = sd[2]; dd[3] = sd[3];
+  }
+}
+
+// ============================================================================
+// k_pack_delta: the step's result as a delta against the previous lists
+// (vf_pipeline_collect_delta): every stream's DETECTED records (the head of
+// its list) packed contiguously, plus the Eq. 1 keep mask of its previous
+// list (masking.py:176-183).  With the previous list on the host, list n =
+// detected ++ [previous[i], origin propagated, age + 1, for each kept i],
+// exactly the merged list.  Runs after k_finalize (counters of frame f).
+// ============================================================================
+__global__ void __launch_bounds__(256) k_pack_delta(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
+                                                    int n_streams, double* px, double* py, double* ps, double* pt,
+                                                    double* pv, uint8_t* pd, uint32_t* pk, int* pre_det,
+                                                    int* pre_kw, int* counts, long long cap, long long kcap)
+{
+  __shared__ int sm_warp[32];
+  extern __shared__ int pre[];   // [2][n_streams + 1]: detected, keep words
+  int* pw = pre + n_streams + 1;
+  auto nbits = [&](int s) {
+    const int* ctr = b.ctr + s * C_NCTR;
+    const bool masked = (g.mask_mode == 1 || g.mask_mode == 2) && ctr[C_FRAME] >= 2;
+    return masked ? ctr[C_NFEAT0 + (ctr[C_FRAME] & 1)] : 0;   // the previous list's length
+  };
+  stream_prefix(n_streams, pre, sm_warp, [&](int s) { return b.ctr[s * C_NCTR + C_NDET]; });
+  stream_prefix(n_streams, pw, sm_warp, [&](int s) { return (nbits(s) + 31) >> 5; });
+  if (blockIdx.x == 0)
+    for (int s = threadIdx.x; s <= n_streams; s += blockDim.x) {
+      pre_det[s] = pre[s];
+      pre_kw[s] = pw[s];
+      if (s < n_streams) {
+        const int* ctr = b.ctr + s * C_NCTR;
+        counts[3 * s] = ctr[C_NDET]; counts[3 * s + 1] = ctr[C_NPROP]; counts[3 * s + 2] = nbits(s);
+      }
+    }
+  const int total = pre[n_streams], words = pw[n_streams];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total && i < cap;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = find_stream(pre, n_streams, (int)i), k = (int)(i - pre[s]);
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int buf = (ctr[C_FRAME] - 1) & 1;
+    const long long f = feat_base(g, s, buf, ctr[C_NFEAT0 + buf]) + k;
+    px[i] = b.fx[f]; py[i] = b.fy[f]; ps[i] = b.fs[f]; pt[i] = b.ft[f]; pv[i] = b.fv[f];
+    const uint4* sd = reinterpret_cast<const uint4*>(b.fdesc + f * 64);
+    uint4* dd = reinterpret_cast<uint4*>(pd + i * 64);
+    dd[0] = sd[0]; dd[1] = sd[1]; dd[2] = sd[2]; dd[3] = sd[3];
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words && i < kcap;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = find_stream(pw, n_streams, (int)i), k = (int)(i - pw[s]);
+    const int nb = nbits(s);
+    uint32_t v = b.keep_bits[(long long)s * b.keep_words + k];
+    if (32 * k + 32 > nb) v &= (1u << (nb - 32 * k)) - 1u;   // bits past the list (last word)
+    pk[i] = v;
   }
 }
 

@@ -189,6 +189,59 @@ class FeatureEngine:
             out["offsets"].ctypes.data), "vf_pipeline_collect")
         return out
 
+    def set_delta(self, enable: bool = True) -> None:
+        """Pipelined API: collect_delta returns new records + keep masks (see vf_pipeline_collect_delta)."""
+        _native.check(_native.lib().vf_pipeline_set_delta(self._h, int(enable)), "vf_pipeline_set_delta")
+
+    def collect_delta(self, out: dict) -> dict:
+        """The oldest submitted step's result as a delta: out["x"..] detected records (packed over streams,
+        out["offsets"]), out["keep"] keep-mask words (out["keep_offsets"]), out["counts"] [S, 3]."""
+        n = ctypes.c_int64(len(out["x"]))
+        _native.check(_native.lib().vf_pipeline_collect_delta(
+            self._h, n, out["x"].ctypes.data, out["y"].ctypes.data, out["sigma"].ctypes.data, out["theta"].ctypes.data,
+            out["score"].ctypes.data, out["desc"].ctypes.data, out["offsets"].ctypes.data, len(out["keep"]),
+            out["keep"].ctypes.data, out["keep_offsets"].ctypes.data, out["counts"].ctypes.data),
+            "vf_pipeline_collect_delta")
+        return out
+
+    def alloc_delta(self, cap: int, pinned: bool = True) -> dict:
+        """Host buffers for collect_delta (pinned)."""
+        import torch
+
+        out = self.alloc_host(cap, pinned)
+        kw = self.n_streams * (max(self.kp_capacity, cap) // 32 + 2)
+        out["keep"] = torch.empty(kw, dtype=torch.int32, pin_memory=pinned).numpy().view(np.uint32)
+        out["keep_offsets"] = np.zeros(self.n_streams + 1, np.int32)
+        out["counts"] = np.zeros((self.n_streams, 3), np.int32)
+        return out
+
+    @staticmethod
+    def delta_apply(prev: dict, delta: dict, s: int) -> dict:
+        """Stream s's merged list from its previous list (SoA dict) and a collect_delta result."""
+        a, b = int(delta["offsets"][s]), int(delta["offsets"][s + 1])
+        ka, kb = int(delta["keep_offsets"][s]), int(delta["keep_offsets"][s + 1])
+        nbits = int(delta["counts"][s][2])
+        n_det = b - a
+        cap = n_det + nbits
+        out = {k: np.zeros(cap, np.float64) for k in ("x", "y", "sigma", "theta", "score")}
+        out["origin"] = np.zeros(cap, np.uint8)
+        out["age"] = np.zeros(cap, np.int32)
+        out["desc"] = np.zeros((cap, 64), np.uint8)
+        n_prev = len(prev["x"])
+        pv = {k: np.ascontiguousarray(prev[k]) for k in ("x", "y", "sigma", "theta", "score", "origin", "age", "desc")}
+        dv = {k: np.ascontiguousarray(delta[k][a:b]) for k in ("x", "y", "sigma", "theta", "score", "desc")}
+        keep = np.ascontiguousarray(delta["keep"][ka:kb])
+        n_out = ctypes.c_int32(0)
+        _native.check(_native.lib().vf_delta_apply(
+            n_prev, *(pv[k].ctypes.data for k in ("x", "y", "sigma", "theta", "score", "origin", "age", "desc")),
+            n_det, *(dv[k].ctypes.data for k in ("x", "y", "sigma", "theta", "score", "desc")), nbits,
+            keep.ctypes.data, cap, *(out[k].ctypes.data for k in ("x", "y", "sigma", "theta", "score", "origin", "age",
+                                                                  "desc")), ctypes.byref(n_out)), "vf_delta_apply")
+        n = int(n_out.value)
+        res = {k: v[:n] for k, v in out.items()}
+        res["n"] = n
+        return res
+
     @staticmethod
     def alloc_host(cap: int, pinned: bool = True) -> dict:
         """Host SoA buffers for fetch_all (torch pinned memory viewed as numpy)."""

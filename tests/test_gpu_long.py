@@ -178,3 +178,42 @@ def test_capacity_grows_in_place():
         assert eng.kp_capacity >= r.n_total > 1024
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("mode", ["intensity", "binning", "none"])
+def test_delta_results_rebuild_the_lists(mode):
+    """vf_pipeline_collect_delta (new records + Eq. 1 keep masks of the previous
+    lists) rebuilt on the host with vf_delta_apply gives exactly the oracle's
+    merged lists, frame after frame (6 config-5 streams x 8 frames)."""
+    from oracle import oracle
+    from paper_1503_06959_b200 import scenes
+    from paper_1503_06959_b200.engine import FeatureEngine
+    from paper_1503_06959_b200.pattern import default_pattern
+    from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+
+    cfg = scenes.CONFIGS[5]
+    S, N = 6, 8
+    fr = scenes.generate(cfg, N, streams=range(S)).numpy()              # [S, N, H, W]
+    eng = FeatureEngine(cfg.width, cfg.height, PipelineConfig(mask=MaskConfig(mode=mode)), n_streams=S)
+    eng.set_delta(True)
+    out = eng.alloc_delta(S * 65536)
+    pipes = [oracle.OraclePipeline(cfg.width, cfg.height, default_pattern(), mode=mode) for _ in range(S)]
+    empty = {k: np.zeros(0, np.float64) for k in ("x", "y", "sigma", "theta", "score")}
+    empty.update(origin=np.zeros(0, np.uint8), age=np.zeros(0, np.int32), desc=np.zeros((0, 64), np.uint8))
+    lists = [empty] * S
+    d2h = 0
+    try:
+        for n in range(N):
+            eng.submit(np.ascontiguousarray(fr[:, n]))
+            eng.collect_delta(out)
+            d2h += int(out["offsets"][S]) * 104 + 4 * int(out["keep_offsets"][S])
+            for s in range(S):
+                lists[s] = {k: (v.copy() if k != "n" else v) for k, v in FeatureEngine.delta_apply(lists[s], out, s).items()}
+                e = pipes[s].process(fr[s, n])
+                assert int(out["counts"][s][0]) == e.n_detected and int(out["counts"][s][1]) == e.n_propagated
+                _compare(lists[s], e, f"delta {mode} stream {s} frame {n}")
+    finally:
+        eng.close()
+        for p in pipes:
+            p.close()
+    assert d2h > 0
