@@ -442,6 +442,15 @@ int vf_set_pattern(const double* points, const double* radii, int m, const int32
   e = e ? e : cudaMemcpyToSymbol(c_wx, wx, sizeof(double) * L);
   e = e ? e : cudaMemcpyToSymbol(c_wy, wy, sizeof(double) * L);
   e = e ? e : cudaMemcpyToSymbol(c_nlong, &L, sizeof(int));
+  uint32_t pairs[VF_NBITS];
+  double ptab[64][3];
+  for (int k = 0; k < nbits; k++) pairs[k] = (uint32_t)(uint16_t)si[k] | ((uint32_t)(uint16_t)sj[k] << 16);
+  for (int j = 0; j < 64; j++) {
+    const int jj = j < m ? j : 0;
+    ptab[j][0] = px[jj]; ptab[j][1] = py[jj]; ptab[j][2] = radii[jj];
+  }
+  e = e ? e : cudaMemcpyToSymbol(g_pairs, pairs, sizeof(pairs));
+  e = e ? e : cudaMemcpyToSymbol(g_ptab, ptab, sizeof(ptab));
   if (e != cudaSuccess) return cuda_status(e);
   g_pattern_ok = 1;
   return VF_OK;

@@ -30,6 +30,11 @@ __constant__ short c_si[VF_NBITS], c_sj[VF_NBITS];
 __constant__ short c_li[VF_MAXLONG], c_lj[VF_MAXLONG];
 __constant__ double c_wx[VF_MAXLONG], c_wy[VF_MAXLONG];
 __constant__ int c_nlong;
+// The same pattern as plain global tables for per-thread (divergent) reads in
+// kernel prologues: a constant-bank read with 32 different addresses per warp
+// is serialised, a global read is one coalesced request.
+__device__ uint32_t g_pairs[VF_NBITS];      // si | sj << 16
+__device__ double g_ptab[64][3];            // point x, y, smoothing radius (rows 60..63 repeat point 0)
 
 // ============================================================================
 // k_pyramid: pyramid.py:67-125 + masking.py:84-93 + descriptor.py:28-32
@@ -2118,17 +2123,17 @@ __device__ __forceinline__ void sample_pass(const Geo& g, DescWarp& w, int nk, i
       const double sg = w.sg[k];
       double fx, fy;
       if (rotated) {
-        const double c = w.cs[k], sn = w.sn[k], px = c_px[j], py = c_py[j];
+        const double c = w.cs[k], sn = w.sn[k], px = g_ptab[j][0], py = g_ptab[j][1];
         fx = w.kx[k] + sg * (c * px - sn * py) + 0.5;
         fy = w.ky[k] + sg * (sn * px + c * py) + 0.5;
       } else {
-        fx = w.kx[k] + sg * c_px[j] + 0.5;
-        fy = w.ky[k] + sg * c_py[j] + 0.5;
+        fx = w.kx[k] + sg * g_ptab[j][0] + 0.5;
+        fy = w.ky[k] + sg * g_ptab[j][1] + 0.5;
       }
       long long x = (long long)floor(fx), y = (long long)floor(fy);
       x = x < 0 ? 0 : (x > g.W - 1 ? g.W - 1 : x);
       y = y < 0 ? 0 : (y > g.H - 1 ? g.H - 1 : y);
-      const int r = (int)floor(c_rad[j] * sg + 0.5);
+      const int r = (int)floor(g_ptab[j][2] * sg + 0.5);
       const int x0 = max((int)x - r, 0), x1 = min((int)x + r, g.W - 1);
       const int y0 = max((int)y - r, 0), y1 = min((int)y + r, g.H - 1);
       const int ys = (int)__umulhi((uint32_t)y0, g.sth_magic) * TH;
@@ -2327,12 +2332,13 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
   __shared__ int sm_warp[32];
   extern __shared__ int pre[];   // [n_streams + 1]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
+  for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = g_pairs[k];
   stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NDET]; });
   const int total = pre[n_streams];
   for (int j = threadIdx.x; j < 64; j += 32 * DSW) {
     const int jj = j < VF_NPTS ? j : 0;
-    ptab[j][0] = c_px[jj]; ptab[j][1] = c_py[jj]; ptab[j][2] = c_rad[jj];
+    (void)jj;
+    ptab[j][0] = g_ptab[j][0]; ptab[j][1] = g_ptab[j][1]; ptab[j][2] = g_ptab[j][2];
   }
   __syncthreads();
   // this lane's two pattern points (lane, lane + 32; lanes 28-31 repeat their first)
@@ -2808,7 +2814,7 @@ __global__ void __launch_bounds__(DS_THREADS) k_describe_batch(const __grid_cons
   __shared__ DescWarp ws[DW_WARPS];
   __shared__ uint32_t pairs[VF_NBITS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < VF_NBITS; k += DS_THREADS) pairs[k] = (uint32_t)c_si[k] | ((uint32_t)c_sj[k] << 16);
+  for (int k = threadIdx.x; k < VF_NBITS; k += DS_THREADS) pairs[k] = g_pairs[k];
   __syncthreads();
   DescWarp& w = ws[wid];
   const int base = (blockIdx.x * DW_WARPS + wid) * 32;
