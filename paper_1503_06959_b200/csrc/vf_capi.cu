@@ -329,6 +329,8 @@ struct vf_ctx {
   std::vector<cudaStream_t> dstreams;
   std::vector<cudaEvent_t> djoin;
   std::vector<cudaEvent_t> dfork_g;     // per stream group
+  std::vector<cudaStream_t> pyi_s;      // per stream group: k_pyr_i beside the main work list
+  std::vector<cudaEvent_t> pyi_e;
   // CUDA graph of one step (small batches): the step's launches (all its
   // streams) captured once per batch size and replayed; inputs are copied
   // into a context-owned buffer first so the graph's pointers stay fixed
@@ -585,6 +587,7 @@ int vf_destroy(vf_ctx* c)
   if (c->hp) { cudaStreamDestroy(c->hp); cudaEventDestroy(c->hp_in); cudaEventDestroy(c->hp_out); }
   for (size_t k = 0; k < c->dstreams.size(); k++) { cudaStreamDestroy(c->dstreams[k]); cudaEventDestroy(c->djoin[k]); }
   for (cudaEvent_t ev : c->dfork_g) cudaEventDestroy(ev);
+  for (size_t k = 0; k < c->pyi_s.size(); k++) { cudaStreamDestroy(c->pyi_s[k]); cudaEventDestroy(c->pyi_e[k]); }
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
@@ -712,10 +715,28 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     c->aux.push_back(as); c->aux_in.push_back(ei); c->aux_mid.push_back(em); c->aux_out.push_back(eo);
   }
   cudaEventRecord(c->aux_in[gi], st);
-  // intra-octave chain of masked frames near active cells (after the IDDM bits)
-  if (pyr4 && g.pyr_split) k_pyr_i<<<dim3(pyi_blocks, n), 256, 0, st>>>(g, b); DBG_SYNC(st, "k_pyr_i");
   stage_mark(c, 2, st);
+  // intra-octave chain of masked frames near active cells (after the IDDM
+  // bits) on its own high-priority stream, concurrent with the main work list
+  // (both only read the bit mask); k_fast waits for both
+  const bool pyi = pyr4 && g.pyr_split;
+  if (pyi) {
+    while ((int)c->pyi_s.size() <= gi) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStream_t ps;
+      cudaEvent_t pe;
+      if (cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, hi) != cudaSuccess) return VF_ERR_CUDA;
+      if (cudaEventCreateWithFlags(&pe, cudaEventDisableTiming) != cudaSuccess) { cudaStreamDestroy(ps); return VF_ERR_CUDA; }
+      c->pyi_s.push_back(ps);
+      c->pyi_e.push_back(pe);
+    }
+    cudaStreamWaitEvent(c->pyi_s[gi], c->aux_in[gi], 0);
+    k_pyr_i<<<dim3(pyi_blocks, n), 256, 0, c->pyi_s[gi]>>>(g, b); DBG_SYNC(st, "k_pyr_i");
+    cudaEventRecord(c->pyi_e[gi], c->pyi_s[gi]);
+  }
   k_worklist<<<dim3(tile_ctas, n), 256, 0, st>>>(g, b, tile_ctas, 0, 0); DBG_SYNC(st, "k_worklist");
+  if (pyi) cudaStreamWaitEvent(st, c->pyi_e[gi], 0);
   cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
   const bool prop = g.mask_mode == 1 || g.mask_mode == 2;
   k_worklist<<<dim3(cov_ctas + carry_ctas + (prop ? PROP_CTAS : 0), n), 256, 0, c->aux[gi]>>>(
