@@ -217,6 +217,9 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
   g.prop_chunks = cdiv(g.kp_cap, 1024);
+  // describe regions; describe-list entries pack the NMS unit into 14 bits
+  g.rgx = cdiv(g.W, DR_RW); g.rgy = cdiv(g.H, DR_RH); g.nreg = g.rgx * g.rgy;
+  if ((long long)g.bands_per_stream * VF_TILE_H >= (1LL << (32 - DR_UNIT_SHIFT))) return VF_ERR_ARG;
   return VF_OK;
 }
 
@@ -264,7 +267,7 @@ struct vf_ctx {
   int pyr_smem;
   int fast_grid;
   int desc_grid;
-  int sat_grid, sat_smem, desc_smem, dsample_grid, dorient_grid;
+  int sat_grid, sat_smem, desc_smem, dsample_grid, dorient_grid, dregion_grid, dregion_smem, dfused_grid;
   vft::Setup bmq{};                     // temporal mode: block-match set-up (device offsets)
   int bm_grid = 0, bm_smem = 0;
   // host-input staging (vf_process_host)
@@ -444,6 +447,14 @@ int vf_set_pattern(const double* points, const double* radii, int m, const int32
   e = e ? e : cudaMemcpyToSymbol(c_wx, wx, sizeof(double) * L);
   e = e ? e : cudaMemcpyToSymbol(c_wy, wy, sizeof(double) * L);
   e = e ? e : cudaMemcpyToSymbol(c_nlong, &L, sizeof(int));
+  double pmax = 0.0, radmax = 0.0;   // footprint of the region describe path (k_desc_region)
+  for (int j = 0; j < m; j++) {
+    pmax = std::max(pmax, std::sqrt(px[j] * px[j] + py[j] * py[j]));
+    radmax = std::max(radmax, radii[j]);
+  }
+  pmax *= 1.0 + 1e-12;
+  e = e ? e : cudaMemcpyToSymbol(c_pmax, &pmax, sizeof(double));
+  e = e ? e : cudaMemcpyToSymbol(c_radmax, &radmax, sizeof(double));
   uint32_t pairs[VF_NBITS];
   double ptab[64][3];
   for (int k = 0; k < nbits; k++) pairs[k] = (uint32_t)(uint16_t)si[k] | ((uint32_t)(uint16_t)sj[k] << 16);
@@ -452,6 +463,25 @@ int vf_set_pattern(const double* points, const double* radii, int m, const int32
     ptab[j][0] = px[jj]; ptab[j][1] = py[jj]; ptab[j][2] = radii[jj];
   }
   e = e ? e : cudaMemcpyToSymbol(g_pairs, pairs, sizeof(pairs));
+  uint32_t lpair[VF_MAXLONG];
+  double2 lw[VF_MAXLONG];
+  for (int p = 0; p < L; p++) {
+    lpair[p] = (uint32_t)(uint16_t)li[p] | ((uint32_t)(uint16_t)lj[p] << 16);
+    lw[p] = make_double2(wx[p], wy[p]);
+  }
+  // orientation as a linear form of the 60 box means (k_desc_fused, dr_orient_lin)
+  double ow[64][4] = {};
+  for (int p = 0; p < L; p++) {
+    ow[li[p]][0] += wx[p]; ow[lj[p]][0] -= wx[p];
+    ow[li[p]][1] += wy[p]; ow[lj[p]][1] -= wy[p];
+    ow[li[p]][2] += std::fabs(wx[p]); ow[lj[p]][2] += std::fabs(wx[p]);
+    ow[li[p]][3] += std::fabs(wy[p]); ow[lj[p]][3] += std::fabs(wy[p]);
+  }
+  const double ogam = 2.0 * (L + 80) * 1.1102230246251565e-16;
+  e = e ? e : cudaMemcpyToSymbol(g_ow, ow, sizeof(ow));
+  e = e ? e : cudaMemcpyToSymbol(c_ogam, &ogam, sizeof(double));
+  e = e ? e : cudaMemcpyToSymbol(g_lpair, lpair, sizeof(uint32_t) * L);
+  e = e ? e : cudaMemcpyToSymbol(g_lw, lw, sizeof(double2) * L);
   e = e ? e : cudaMemcpyToSymbol(g_ptab, ptab, sizeof(ptab));
   if (e != cudaSuccess) return cuda_status(e);
   g_pattern_ok = 1;
@@ -497,6 +527,9 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.sat_bits = A.get<unsigned>((size_t)S * g.sty * g.stw_words);
   b.sat_work = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_count = A.get<int>((size_t)S);
+  b.reg_cnt = A.get<int>((size_t)S * g.nreg);
+  b.reg_list = A.get<uint32_t>((size_t)S * g.nreg * DR_RCAP);
+  b.reg_work = A.get<int>((size_t)S * g.nreg);
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -538,6 +571,14 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_orient, DO_THREADS, (S + 1) * sizeof(int));
   c->dorient_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_fused, 32 * DSW, (S + 1) * sizeof(int));
+  c->dfused_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  c->dregion_smem = (int)sizeof(DrShared) + (S + 1) * (int)sizeof(int);
+  cudaFuncSetAttribute(k_desc_region, cudaFuncAttributeMaxDynamicSharedMemorySize, c->dregion_smem);
+  occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_region, DR_THREADS, c->dregion_smem);
+  c->dregion_grid = std::max(1, g_num_sms * std::max(occ, 1));
   if (g.mask_mode == 3) {                    // temporal baseline state
     Gop o;
     gop_from_config(*cfg, o);
@@ -766,58 +807,54 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   stage_mark(c, 4, st);
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
   b.nms_u = nms_units(g, n);
+  static const int desc_region = getenv("VF_DESC_REGION") ? atoi(getenv("VF_DESC_REGION")) : 0;
+  b.desc_bin = desc_region ? 1 : 2;
   k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms");
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
   stage_mark(c, 5, st);
-  // SAT + describe of two stream halves on concurrent high-priority streams:
-  // the latency-bound sampling kernels of one half fill the other's gaps and
-  // tails (709 -> 698 us per 64-stream step).  The stage timer then reports
-  // SAT and describe together.  VF_DESC_PAR overrides the number of halves.
-  // One set of half streams and events per stream group (index gi * dpar + h),
-  // so concurrent groups do not serialise on shared streams.
-  static const int dpar = getenv("VF_DESC_PAR") ? std::max(1, atoi(getenv("VF_DESC_PAR"))) : 2;
-  if (dpar > 1 && n >= dpar) {
-    if ((int)c->dstreams.size() < (gi + 1) * dpar) {
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      while ((int)c->dfork_g.size() <= gi) {
-        cudaEvent_t f;
-        if (cudaEventCreateWithFlags(&f, cudaEventDisableTiming) != cudaSuccess) return VF_ERR_CUDA;
-        c->dfork_g.push_back(f);
-      }
-      while ((int)c->dstreams.size() < (gi + 1) * dpar) {
-        cudaStream_t ds;
-        cudaEvent_t de;
-        if (cudaStreamCreateWithPriority(&ds, cudaStreamNonBlocking, hi) != cudaSuccess) return VF_ERR_CUDA;
-        if (cudaEventCreateWithFlags(&de, cudaEventDisableTiming) != cudaSuccess) { cudaStreamDestroy(ds); return VF_ERR_CUDA; }
-        c->dstreams.push_back(ds);
-        c->djoin.push_back(de);
-      }
+  // Describe (descriptor.py:85-144).  Default: the strip SATs of the tiles
+  // k_nms marked, then k_desc_fused (warp per keypoint: theta = 0 means,
+  // orientation, rotated means, bits), for two stream halves on two
+  // concurrent high-priority describe streams (VF_DESC_PAR halves).
+  // VF_DESC_REGION=1: small-scale keypoints through k_desc_region on the main
+  // stream, the rest through the strip-SAT chain beside it.
+  static const int dpar_env = getenv("VF_DESC_PAR") ? std::max(1, std::min(2, atoi(getenv("VF_DESC_PAR")))) : 2;
+  const bool region = b.desc_bin == 1;
+  const int dpar = region ? 1 : std::min(dpar_env, n);
+  if ((int)c->dstreams.size() < 2 * (gi + 1)) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    while ((int)c->dfork_g.size() <= gi) {
+      cudaEvent_t f;
+      if (cudaEventCreateWithFlags(&f, cudaEventDisableTiming) != cudaSuccess) return VF_ERR_CUDA;
+      c->dfork_g.push_back(f);
     }
-    cudaEvent_t dfork = c->dfork_g[gi];
-    cudaEventRecord(dfork, st);
-    for (int h = 0; h < dpar; h++) {
-      const int h0 = (int)((long long)n * h / dpar), h1 = (int)((long long)n * (h + 1) / dpar);
-      Bufs bh = b;
-      bh.s0 = b.s0 + h0;
-      bh.frames = b.frames + (long long)h0 * b.frame_stride;
-      const int nh = h1 - h0, pb = (nh + 1) * (int)sizeof(int);
-      cudaStream_t ds = c->dstreams[gi * dpar + h];
-      cudaStreamWaitEvent(ds, dfork, 0);
-      k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh); DBG_SYNC(st, "k_sat");
-      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 0); DBG_SYNC(st, "k_desc_sample");
-      k_desc_orient<<<c->dorient_grid, DO_THREADS, pb, ds>>>(g, bh, nh); DBG_SYNC(st, "k_desc_orient");
-      k_desc_sample<<<c->dsample_grid, 32 * DSW, pb, ds>>>(g, bh, nh, 1); DBG_SYNC(st, "k_desc_sample");
-      cudaEventRecord(c->djoin[gi * dpar + h], ds);
+    while ((int)c->dstreams.size() < 2 * (gi + 1)) {
+      cudaStream_t ds;
+      cudaEvent_t de;
+      if (cudaStreamCreateWithPriority(&ds, cudaStreamNonBlocking, hi) != cudaSuccess) return VF_ERR_CUDA;
+      if (cudaEventCreateWithFlags(&de, cudaEventDisableTiming) != cudaSuccess) { cudaStreamDestroy(ds); return VF_ERR_CUDA; }
+      c->dstreams.push_back(ds);
+      c->djoin.push_back(de);
     }
-    for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[gi * dpar + h], 0);
-  } else {
-    k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(g, b, n); DBG_SYNC(st, "k_sat");
-    stage_mark(c, 6, st);
-    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 0); DBG_SYNC(st, "k_desc_sample");
-    k_desc_orient<<<c->dorient_grid, DO_THREADS, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_desc_orient");
-    k_desc_sample<<<c->dsample_grid, 32 * DSW, pre_bytes, st>>>(g, b, n, 1); DBG_SYNC(st, "k_desc_sample");
   }
+  cudaEventRecord(c->dfork_g[gi], st);
+  for (int h = 0; h < dpar; h++) {
+    const int h0 = (int)((long long)n * h / dpar), h1 = (int)((long long)n * (h + 1) / dpar);
+    Bufs bh = b;
+    bh.s0 = b.s0 + h0;
+    bh.frames = b.frames + (long long)h0 * b.frame_stride;
+    const int nh = h1 - h0, pb = (nh + 1) * (int)sizeof(int);
+    cudaStream_t ds = c->dstreams[2 * gi + h];
+    cudaStreamWaitEvent(ds, c->dfork_g[gi], 0);
+    k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh, 0); DBG_SYNC(ds, "k_sat");
+    k_desc_fused<<<c->dfused_grid, 32 * DSW, pb, ds>>>(g, bh, nh); DBG_SYNC(ds, "k_desc_fused");
+    cudaEventRecord(c->djoin[2 * gi + h], ds);
+  }
+  if (region) {
+    k_desc_region<<<c->dregion_grid, DR_THREADS, c->dregion_smem, st>>>(g, b, n); DBG_SYNC(st, "k_desc_region");
+  }
+  for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[2 * gi + h], 0);
   // k_propagate (stage 7) is timed on the side stream; the join wait counts
   // toward the finalize stage
   stage_mark(c, 8, st);
@@ -1749,7 +1786,7 @@ int vf_describe(const uint8_t* frame_dev, int W, int H, int64_t pitch, int n, co
   ctr0[C_NDET] = n;              // k_sat builds every tile of a stream with keypoints (unmasked)
   ctr0[C_NTOTAL] = n;            // the describe kernels write the n outputs as a full list
   cudaMemcpyAsync(b.ctr, ctr0, sizeof(ctr0), cudaMemcpyHostToDevice, st);
-  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1);   // stream 0 -> slot 0
+  k_sat<<<c->sat_grid, 256, c->sat_smem, st>>>(c->g, b, 1, 1);   // stream 0 -> slot 0, every tile
   k_describe_batch<<<cdiv(n, DS_THREADS), DS_THREADS, 0, st>>>(c->g, b.sat, n, kx_dev, ky_dev, sigma_dev,
                                                               theta_in_dev, theta_out_dev, desc_dev);
   return cuda_status(cudaStreamSynchronize(st));

@@ -31,6 +31,8 @@ enum {
   C_NCAND = 11,     // FAST candidates
   C_EPOCH = 12,     // monotonic step id (activity stamps), survives vf_reset
   C_PTICKET = 13,   // last-CTA ticket of the propagation-count CTAs (k_worklist)
+  C_NGLOB = 14,     // kept keypoints described from the strip SAT (b.gidx list) this step
+  C_NREGW = 15,     // describe regions with small-scale keypoints this step (b.reg_work)
   C_NCTR = 16
 };
 #define VF_ERRBIT_CAPACITY 1
@@ -38,6 +40,17 @@ enum {
 #define VF_ERRBIT_INDEX 4
 
 #define VF_ST 32   // strip-SAT tile edge and strip height (o0 pixels)
+
+// Describe regions (k_desc_region): keypoints whose 60 boxes stay within
+// DR_FMAX o0 pixels of floor(x, y) and are at most 15 x 15 (box sums < 2^16)
+// are binned by position into DR_RW x DR_RH regions; a CTA builds one uint16
+// SAT of the region's footprint box in shared memory and describes them all.
+#define DR_RW 64
+#define DR_RH 28
+#define DR_FMAX 53
+#define DR_RMAX 7
+#define DR_RCAP 512            // keypoints listed per region (more go to the strip-SAT path)
+#define DR_UNIT_SHIFT 18       // list entry = unit << 18 | index of the keypoint in its NMS unit
 
 struct LayerGeo {
   int w, h;
@@ -92,6 +105,7 @@ struct Geo {
   int pyr_split;        // masked frames build the intra-octave chain only near active cells (k_pyramid4)
   int pyr_halo;         // o0 pixels a FAST ring reaches around a tile's derived pixels
   int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
+  int rgx, rgy, nreg;   // describe regions (DR_RW x DR_RH o0 pixels) per stream: columns, rows, total
 };
 
 // Per-launch stream-batch pointers.
@@ -107,7 +121,12 @@ struct Bufs {
   int* unit_rec;        // [S][bands_per_stream * nms_u][4]: staging base, kept, border-ok, dropped per NMS unit
   int* unit_out;        // [S][bands_per_stream * nms_u]: output offset of the unit's kept keypoints
   int* band_cand;       // [S][bands_per_stream]: FAST candidates of the band this step
-  int* gidx;            // [S][kp_cap]: detected rank -> staging slot
+  int* gidx;            // [S][kp_cap]: kept keypoints of the strip-SAT describe path, (unit << 18 | index in
+                        // unit) from k_nms, replaced by the output rank (or -1) in k_desc_sample pass 0
+  int desc_bin;         // k_nms: 0 stand-alone (no describe lists), 1 region + strip-SAT paths, 2 strip SAT only
+  int* reg_cnt;         // [S][nreg] small-scale keypoints per describe region (zeroed by k_desc_region)
+  uint32_t* reg_list;   // [S][nreg][DR_RCAP] their (unit << 18 | index in unit) entries
+  int* reg_work;        // [S][nreg] regions with keypoints this step (k_nms_finish)
   int* prop_cnt;        // [S][prop_chunks]
   int* prop_out;        // [S][prop_chunks]
   uint8_t* cells;       // [S][cell_slab]

@@ -30,11 +30,20 @@ __constant__ short c_si[VF_NBITS], c_sj[VF_NBITS];
 __constant__ short c_li[VF_MAXLONG], c_lj[VF_MAXLONG];
 __constant__ double c_wx[VF_MAXLONG], c_wy[VF_MAXLONG];
 __constant__ int c_nlong;
+__constant__ double c_pmax, c_radmax;        // pattern footprint: max |p|, max smoothing radius
 // The same pattern as plain global tables for per-thread (divergent) reads in
 // kernel prologues: a constant-bank read with 32 different addresses per warp
 // is serialised, a global read is one coalesced request.
 __device__ uint32_t g_pairs[VF_NBITS];      // si | sj << 16
 __device__ double g_ptab[64][3];            // point x, y, smoothing radius (rows 60..63 repeat point 0)
+__device__ uint32_t g_lpair[VF_MAXLONG];     // long pairs li | lj << 16 (lane-strided reads: global, not constant)
+__device__ double2 g_lw[VF_MAXLONG];         // orientation weights (wx, wy) of the long pairs
+// Orientation as a linear form of the 60 box means: gx = sum_i v_i Wx_i with
+// Wx_i = sum over long pairs (i, j) of wx - sum over pairs (j, i) of wx (fp64
+// sums on the host), and the bound weights Ax_i = sum of |wx| over the pairs
+// touching i (same for y).  Rows 60..63 are zero.  [point][Wx, Wy, Ax, Ay]
+__device__ double g_ow[64][4];
+__constant__ double c_ogam;                  // certificate factor, see dr_orient_lin
 
 // ============================================================================
 // k_pyramid: pyramid.py:67-125 + masking.py:84-93 + descriptor.py:28-32
@@ -194,6 +203,7 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
   if (blockIdx.x == 0 && blockIdx.y == 0) {
     if (tid == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
+      b.ctr[s * C_NCTR + C_NGLOB] = 0;
       b.sat_count[s] = 0;
       b.work_count[s] = 0;
     }
@@ -402,29 +412,19 @@ __device__ __forceinline__ void stream_prefix(int n_streams, int* pre, int* sm_w
 #define SAT_WARPS 8
 #define SAT_PITCH (VF_ST + 4)   // words; 16-B row stores of 8 lanes hit distinct banks
 __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
-                                                        int n_streams)
+                                                        int n_streams, int all)
 {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* tile = reinterpret_cast<uint32_t*>(smem) + (threadIdx.x >> 5) * VF_ST * SAT_PITCH;
   int* pre = reinterpret_cast<int*>(smem + SAT_WARPS * VF_ST * SAT_PITCH * 4);
   __shared__ int sm_warp[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  // detected rank -> staging slot map for k_desc_sample (thread per NMS unit)
-  const int nu = g.bands_per_stream * b.nms_u;
-  for (long long il = (long long)blockIdx.x * blockDim.x + threadIdx.x; il < (long long)n_streams * nu;
-       il += (long long)gridDim.x * blockDim.x) {
-    const int s = b.s0 + (int)(il / nu);
-    const long long i = (long long)b.s0 * nu + il;
-    const int4 r = __ldcg(reinterpret_cast<const int4*>(b.unit_rec) + i);
-    if (r.y > 0) {
-      const int o = __ldcg(b.unit_out + i);
-      int* gidx = b.gidx + (long long)s * g.kp_cap;
-      for (int k = 0; k < r.y && o + k < g.kp_cap; k++) gidx[o + k] = r.x + k;
-    }
-  }
+  // all = 1 (stand-alone describe): every tile of a stream with keypoints;
+  // else the tiles k_nms marked for the strip-SAT path's keypoints
   stream_prefix(n_streams, pre, sm_warp, [&](int sl) {
     const int s = b.s0 + sl;
-    return b.ctr[s * C_NCTR + C_NDET] == 0 ? 0 : (use_mask(g, b, s) ? b.sat_count[s] : g.sat_tiles);
+    return all ? (b.ctr[s * C_NCTR + C_NDET] == 0 ? 0 : g.sat_tiles)
+               : (b.ctr[s * C_NCTR + C_NGLOB] == 0 ? 0 : b.sat_count[s]);
   });
   const int n = pre[n_streams];
   // one-tile software pipeline per warp: tile k + 1's work-list entry, carry
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
     int lo = 0, hi = n_streams;
     while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
     const int s = b.s0 + lo, i = item - pre[lo];
-    const int t = use_mask(g, b, s) ? b.sat_work[(long long)s * g.sat_tiles + i] : i;
+    const int t = all ? i : b.sat_work[(long long)s * g.sat_tiles + i];
     const int ty = t / g.stx, tx = t - ty * g.stx;
     in.s = s; in.X0 = tx * VF_ST; in.Y0 = ty * VF_ST;
     in.tw = min(VF_ST, g.W - in.X0); in.th = min(VF_ST, g.H - in.Y0);
@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
   if (PART != PYR_ICHAIN && blockIdx.x == 0 && blockIdx.y == 0) {
     if (tid == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
+      b.ctr[s * C_NCTR + C_NGLOB] = 0;
       b.sat_count[s] = 0;
       b.work_count[s] = 0;
     }
@@ -824,6 +825,7 @@ __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, co
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
+      b.ctr[s * C_NCTR + C_NGLOB] = 0;
       b.sat_count[s] = 0;
       b.work_count[s] = 0;
     }
@@ -1802,6 +1804,56 @@ __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int 
     }
 }
 
+// Footprint reach (o0 pixels around floor(x), floor(y)) of a keypoint's 60
+// boxes: sample offsets |p| <= c_pmax sigma (+ rounding), box radius rmax =
+// floor(c_radmax sigma + 0.5) (descriptor.py:56-60), one pixel of slack.
+__device__ __forceinline__ int desc_reach(double sg, int& rmax)
+{
+  rmax = __double2int_rd(c_radmax * sg + 0.5);
+  return (int)ceil(c_pmax * sg) + 2 + rmax;
+}
+
+// Warp-collective, at k_nms's kept-keypoint site: small-scale keypoints
+// (every box <= 15 x 15, footprint within DR_FMAX) are binned into their
+// DR_RW x DR_RH describe region (warp-aggregated atomics); the others, and the
+// overflow of a full region, are listed for the strip-SAT describe path and
+// their footprint's SAT tiles marked.  Entry e = unit << 18 | index in unit.
+__device__ __forceinline__ void desc_bin_kept(const Geo& g, const Bufs& b, int s, bool kp, double x, double y,
+                                              double sg, uint32_t e, int lane)
+{
+  const unsigned NONE = 0xffffffffu;
+  unsigned key = NONE;
+  if (kp && b.desc_bin == 1) {
+    int rmax;
+    const int reach = desc_reach(sg, rmax);
+    if (rmax <= DR_RMAX && reach <= DR_FMAX) key = (unsigned)(((int)y / DR_RH) * g.rgx + (int)x / DR_RW);
+  }
+  bool glob = kp && key == NONE;
+  if (__any_sync(0xffffffffu, key != NONE)) {
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    int bv = 0;
+    if (key != NONE && lane == leader) bv = atomicAdd(b.reg_cnt + (long long)s * g.nreg + key, __popc(peers));
+    bv = __shfl_sync(0xffffffffu, bv, leader);
+    if (key != NONE) {
+      const int li = bv + __popc(peers & ((1u << lane) - 1));
+      if (li < DR_RCAP) b.reg_list[((long long)s * g.nreg + key) * DR_RCAP + li] = e;
+      else glob = true;
+    }
+  }
+  const unsigned gm = __ballot_sync(0xffffffffu, glob);
+  if (gm) {
+    const int leader = __ffs(gm) - 1;
+    int gb = 0;
+    if (lane == leader) gb = atomicAdd(b.ctr + s * C_NCTR + C_NGLOB, __popc(gm));
+    gb = __shfl_sync(0xffffffffu, gb, leader);
+    if (glob) {
+      b.gidx[(long long)s * g.kp_cap + gb + __popc(gm & ((1u << lane) - 1))] = (int)e;
+      mark_sat_tiles(g, b, s, x, y, sg, 0);
+    }
+  }
+}
+
 // Block-wide exclusive scan (blockDim.x = NF_THREADS) of one value per thread.
 #define NF_THREADS 256
 __device__ __forceinline__ int block_excl_scan(int v, int& total, int* sm)
@@ -1952,11 +2004,15 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
           const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
           n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
           n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
+          const int kidx = kept + __popc(kb & ((1u << lane) - 1));   // index in the unit's kept list
           if (o.flags & 4) {
-            const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
+            const long long dst = (long long)s * g.kp_cap + base + kidx;
             b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
-            if (um) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
+            if (um && !b.desc_bin) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
           }
+          if (b.desc_bin)
+            desc_bin_kept(g, b, s, (o.flags & 4) != 0, o.x, o.y, o.sig,
+                          ((uint32_t)unit << DR_UNIT_SHIFT) | (uint32_t)kidx, lane);
           kept += __popc(kb);
           __syncwarp();
           const uint16_t rest = lane + nb < qn ? sq[w][lane + nb] : (uint16_t)0;
@@ -2010,7 +2066,7 @@ __global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant
   }
   // ---- SAT tiles marked by the stream's bands (k_nms ORs footprints into
   // the bitmap) -> the k_sat work list ----
-  if (um) {
+  if (um || b.desc_bin) {
     const int nw = g.sty * g.stw_words;
     const unsigned* bits = b.sat_bits + (long long)s * nw;
     int* work = b.sat_work + (long long)s * g.sat_tiles;
@@ -2025,6 +2081,21 @@ __global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant
       cnt += tot;
     }
     if (tid == 0) b.sat_count[s] = cnt;
+  }
+  // ---- describe regions holding small-scale keypoints -> k_desc_region's work list ----
+  if (b.desc_bin == 1) {
+    const int* rc = b.reg_cnt + (long long)s * g.nreg;
+    int* rw = b.reg_work + (long long)s * g.nreg;
+    int cnt = 0;
+    for (int r0 = 0; r0 < g.nreg; r0 += NF_THREADS) {
+      const int ri = r0 + tid;
+      const int v = ri < g.nreg && __ldcg(rc + ri) > 0;
+      int tot;
+      const int pos = cnt + block_excl_scan(v, tot, sm);
+      if (v) rw[pos] = ri;
+      cnt += tot;
+    }
+    if (tid == 0) b.ctr[s * C_NCTR + C_NREGW] = cnt;
   }
   // ---- FrameReport ----
 #pragma unroll
@@ -2242,6 +2313,7 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, const u
 // Corner addresses of the box of one sample point (descriptor.py:94-115):
 // fp64 position in the reference's op order, clamped box, strip-SAT corners.
 struct BoxQ {
+  double dist;   // distance of the unrounded sample position (x or y) to the nearest integer
   const uint32_t *r0, *r1, *r2;
   int xa, xb, area;
   uint32_t L, T, C;
@@ -2265,6 +2337,7 @@ __device__ __forceinline__ BoxQ box_query(const uint32_t* S, const Geo& g, doubl
   const int y = min(max(__double2int_rd(fy), 0), g.H - 1);
   const int r = __double2int_rd(rad * sg + 0.5);
   BoxQ q;
+  q.dist = fmin(fabs(fx - rint(fx)), fabs(fy - rint(fy)));
   q.x0 = max(x - r, 0); q.x1 = min(x + r, g.W - 1);
   q.y0 = max(y - r, 0); q.y1 = min(y + r, g.H - 1);
   const int TH = VF_ST;
@@ -2294,10 +2367,11 @@ __device__ __forceinline__ uint32_t exact_div(uint32_t sm, uint32_t a)
 // all 12 loads issued together (masked corners re-read corner A, times 0).
 __device__ __forceinline__ void point_means2(const uint32_t* S, const Geo& g, double kx, double ky, double sg,
                                              double cs, double sn, const double* pa, const double* pb, bool rotated,
-                                             uint32_t& ma, uint32_t& mb)
+                                             uint32_t& ma, uint32_t& mb, double* da = nullptr, double* db = nullptr)
 {
   const BoxQ a = box_query(S, g, kx, ky, sg, cs, sn, pa[0], pa[1], pa[2], rotated);
   const BoxQ c = box_query(S, g, kx, ky, sg, cs, sn, pb[0], pb[1], pb[2], rotated);
+  if (da) { *da = a.dist; *db = c.dist; }
   // predicated corner loads: a corner the box does not use issues no request
   auto ld = [](bool p, const uint32_t* q) -> uint32_t { return p ? __ldg(q) : 0u; };
   const uint32_t a0 = __ldg(a.r0 + a.xb), a1 = ld(a.L, a.r0 + a.xa), a2 = ld(a.T, a.r1 + a.xb);
@@ -2333,7 +2407,7 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
   extern __shared__ int pre[];   // [n_streams + 1]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = g_pairs[k];
-  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NDET]; });
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NGLOB]; });
   const int total = pre[n_streams];
   for (int j = threadIdx.x; j < 64; j += 32 * DSW) {
     const int jj = j < VF_NPTS ? j : 0;
@@ -2352,27 +2426,45 @@ __global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant_
     long long o_l = 0;
     int s_l = 0;
     double kx_l = 0.0, ky_l = 0.0, sg_l = 0.0, cs_l = 1.0, sn_l = 0.0;
+    o_l = -1;
     if (gl < total) {
       const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
       s_l = b.s0 + sl;
       const int cur = b.ctr[s_l * C_NCTR + C_FRAME] & 1;
-      o_l = feat_base(g, s_l, cur, b.ctr[s_l * C_NCTR + C_NTOTAL]) + i;
+      const long long fb = feat_base(g, s_l, cur, b.ctr[s_l * C_NCTR + C_NTOTAL]);
+      int* gl_e = b.gidx + (long long)s_l * g.kp_cap + i;
       if (pass == 0) {
-        const long long si = (long long)s_l * g.kp_cap + __ldg(b.gidx + (long long)s_l * g.kp_cap + i);   // staging slot
+        // list entry (unit, index in unit) -> staging slot and output rank;
+        // ranks past the (capacity-clamped) detected count are not written
+        const uint32_t e = (uint32_t)*gl_e;
+        const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
+        const long long ui = (long long)s_l * g.bands_per_stream * b.nms_u + u;
+        const long long si = (long long)s_l * g.kp_cap + __ldcg(b.unit_rec + 4 * ui) + k;   // staging slot
+        const int rank = __ldcg(b.unit_out + ui) + k;
+        const bool ok = rank < b.ctr[s_l * C_NCTR + C_NDET];
+        *gl_e = ok ? rank : -1;   // for k_desc_orient and pass 1
         kx_l = b.st_x[si]; ky_l = b.st_y[si]; sg_l = b.st_s[si];
-        b.fx[o_l] = kx_l; b.fy[o_l] = ky_l; b.fs[o_l] = sg_l; b.fv[o_l] = b.st_v[si];
-        b.forg[o_l] = 0; b.fage[o_l] = 0;
+        if (ok) {
+          o_l = fb + rank;
+          b.fx[o_l] = kx_l; b.fy[o_l] = ky_l; b.fs[o_l] = sg_l; b.fv[o_l] = b.st_v[si];
+          b.forg[o_l] = 0; b.fage[o_l] = 0;
+        }
       } else {
-        kx_l = b.fx[o_l]; ky_l = b.fy[o_l]; sg_l = b.fs[o_l];
-        const double* park = reinterpret_cast<const double*>(b.fdesc + o_l * 64);   // from k_desc_orient
-        cs_l = park[0];
-        sn_l = park[1];
+        const int rank = *gl_e;
+        if (rank >= 0) {
+          o_l = fb + rank;
+          kx_l = b.fx[o_l]; ky_l = b.fy[o_l]; sg_l = b.fs[o_l];
+          const double* park = reinterpret_cast<const double*>(b.fdesc + o_l * 64);   // from k_desc_orient
+          cs_l = park[0];
+          sn_l = park[1];
+        }
       }
     }
     const int nk = min(32, (total - g0 + Wt - 1) / Wt);
 #pragma unroll 1
   for (int k = 0; k < nk; k++) {
     const long long o = __shfl_sync(0xffffffffu, o_l, k);
+    if (o < 0) continue;   // warp-uniform: a rank past the clamped count
     const int s = __shfl_sync(0xffffffffu, s_l, k);
     const double kx = __shfl_sync(0xffffffffu, kx_l, k), ky = __shfl_sync(0xffffffffu, ky_l, k);
     const double sg = __shfl_sync(0xffffffffu, sg_l, k);
@@ -2413,15 +2505,16 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
   __shared__ __align__(16) uint8_t vv[DO_THREADS * DW_ROW];
   __shared__ int sm_warp[32];
   extern __shared__ int pre[];
-  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NDET]; });
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NGLOB]; });
   const int total = pre[n_streams];
   uint8_t* v = vv + threadIdx.x * DW_ROW;
   for (int base = blockIdx.x * DO_THREADS; base < total; base += gridDim.x * DO_THREADS) {
     const int gi = base + threadIdx.x;
     long long o = -1;
-    if (gi < total) {
-      const int sl = find_stream(pre, n_streams, gi), s = b.s0 + sl, i = gi - pre[sl];
-      o = feat_base(g, s, b.ctr[s * C_NCTR + C_FRAME] & 1, b.ctr[s * C_NCTR + C_NTOTAL]) + i;
+    const int sl = gi < total ? find_stream(pre, n_streams, gi) : 0, s = b.s0 + sl;
+    const int rank = gi < total ? __ldcg(b.gidx + (long long)s * g.kp_cap + gi - pre[sl]) : -1;
+    if (rank >= 0) {
+      o = feat_base(g, s, b.ctr[s * C_NCTR + C_FRAME] & 1, b.ctr[s * C_NCTR + C_NTOTAL]) + rank;
       const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + o * 64);
 #pragma unroll
       for (int q = 0; q < 4; q++) {
@@ -2459,6 +2552,503 @@ __global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constan
       double* park = reinterpret_cast<double*>(b.fdesc + o * 64);
       park[0] = cs;
       park[1] = sn;
+    }
+  }
+}
+
+// ============================================================================
+// k_desc_region: orientation + descriptor of the small-scale keypoints of one
+// describe region per CTA (descriptor.py:28-32,85-144,271-275), from a uint16
+// SAT of the region's footprint box built in shared memory from the frame.
+//   * every box of these keypoints is <= 15 x 15, so its sum is < 2^16 and
+//     the modular uint16 SAT gives it exactly;
+//   * the SAT is built by 8 warps over row blocks (lane = 4-pixel word: dp4a
+//     word prefixes, a warp scan per row, the block's column sums in
+//     registers; 4 rows of loads in flight), then each block adds the column
+//     totals of the blocks above;
+//   * then warp per keypoint, no further barriers: theta = 0 box means, the
+//     orientation sum (dr_orient), rotated means and the 16 ballots of the
+//     512 bits.
+// Region counts are zeroed here for the next step.
+// ============================================================================
+#define DR_THREADS 256
+#define DR_WARPS (DR_THREADS / 32)
+#define DR_SAT_MAX 24064         // (DR_RH - 1 + 2 DR_FMAX + 2) rows x (176 + 2) columns of uint16
+#define DR_CITEMS 5              // fix-up items per thread: 176 columns x 7 row blocks / 256 threads
+#define DR_PF 4                  // frame rows of loads in flight per warp while building the SAT
+
+struct DrShared {
+  uint16_t T[DR_SAT_MAX];
+  uint8_t v[DR_WARPS][DW_ROW];
+  int red[4][DR_WARPS];
+};
+
+// Box mean of one sample point from the region SAT T (pitch P entries): entry
+// (r, c) = sum over rows ylo .. ylo + r - 1 and columns ax0 .. ax0 + c - 2.
+// *dist receives the distance of the unrounded sample position to the nearest
+// integer (x or y, whichever is closer): how far theta may move before floor()
+// changes.
+__device__ __forceinline__ uint32_t dr_mean(const uint16_t* T, int P, int ax0, int ylo, int W, int H, double kx,
+                                            double ky, double sg, double cs, double sn, double px, double py,
+                                            double rad, bool rot, double* dist)
+{
+  double fx, fy;
+  if (rot) {
+    fx = kx + sg * (cs * px - sn * py) + 0.5;
+    fy = ky + sg * (sn * px + cs * py) + 0.5;
+  } else {
+    fx = kx + sg * px + 0.5;
+    fy = ky + sg * py + 0.5;
+  }
+  if (dist) *dist = fmin(fabs(fx - rint(fx)), fabs(fy - rint(fy)));
+  const int x = min(max(__double2int_rd(fx), 0), W - 1);
+  const int y = min(max(__double2int_rd(fy), 0), H - 1);
+  const int r = __double2int_rd(rad * sg + 0.5);
+  const int x0 = max(x - r, 0), x1 = min(x + r, W - 1), y0 = max(y - r, 0), y1 = min(y + r, H - 1);
+  const int c0 = x0 - ax0 + 1, c1 = x1 - ax0 + 2;          // columns of x0 - 1 and x1
+  const int r0 = (y0 - ylo) * P, r1 = (y1 - ylo + 1) * P;  // rows of y0 - 1 and y1
+  const uint32_t sm = ((uint32_t)T[r1 + c1] - (uint32_t)T[r0 + c1] - (uint32_t)T[r1 + c0] + (uint32_t)T[r0 + c0]) &
+                      0xffffu;
+  return exact_div(sm, (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1)));
+}
+
+__device__ __forceinline__ double dr_i2d(int n)   // exact int -> double without I2F
+{
+  return __hiloint2double(0x43380000, (int)(0x80000000u + (unsigned)n)) - 6755401588539392.0;
+}
+
+// The reference orientation (descriptor.py:132-144): gx, gy = sequential fp64
+// sums of dv_p * w_p in long-pair order, theta = atan2(gy, gx).  Here the warp
+// sums the same rounded products lane-strided + butterfly (every lane ends
+// with the identical value).  Both orders are within (n - 1 + 5) u sum|t| of
+// the exact sum (recursive / pairwise summation bounds), so |theta_warp -
+// theta_seq| <= dth.  Returns false -- the caller then uses dr_orient_seq --
+// when that bound is not small against |g| or theta may sit on the -pi / pi
+// branch cut.  The caller also falls back when a rotated sample position lies
+// within the induced position error of an integer, so floor() -- and every
+// descriptor bit -- is the one the sequential theta gives.
+__device__ __forceinline__ bool dr_orient_warp(const uint8_t* v, int lane, double& th, double& dth)
+{
+  double sx = 0.0, sy = 0.0, ax = 0.0, ay = 0.0;
+  const int L = c_nlong;
+  for (int p = lane; p < L; p += 32) {
+    const uint32_t pr = __ldg(g_lpair + p);
+    const double2 w = __ldg(g_lw + p);
+    const double dv = dr_i2d((int)v[pr & 0xffffu] - (int)v[pr >> 16]);
+    const double tx = dv * w.x, ty = dv * w.y;
+    sx += tx; sy += ty;
+    ax += fabs(tx); ay += fabs(ty);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    ax += __shfl_xor_sync(0xffffffffu, ax, o);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o);
+  }
+  const double gam = (double)(L + 8) * 1.1102230246251565e-16 * 1.01;
+  const double bx = 2.0 * gam * ax, by = 2.0 * gam * ay;   // |warp sum - sequential sum| per component
+  const double gn = sqrt(sx * sx + sy * sy);
+  if (!(bx + by < 1e-3 * gn)) return false;                // includes g == 0
+  if (sx < 0.0 && fabs(sy) <= by) return false;            // theta near the +-pi cut
+  dth = 2.0 * (bx + by) / gn + 1e-15;
+  th = atan2(sy, sx);
+  th = th <= -CUDART_PI ? CUDART_PI : th;
+  return true;
+}
+
+// Orientation from the lane's two box means m0 (point lane) and m1 (point
+// lane + 32) as the linear form sum_i v_i W_i, warp-reduced (every lane ends
+// with identical values).  The reference sums the 393 rounded products
+// dv_p * w_p sequentially (descriptor.py:132-144); the linear form, the host
+// rounding of W_i and that sequential order are all within c_ogam * sum_i v_i
+// A_i of the exact sum of the products (standard recursive / pairwise
+// summation bounds, c_ogam = 2 (L + 80) u), so |g_lin - g_seq| <= b per
+// component.  Returns false when that bound is not small against |g| or theta
+// may sit on the -pi / pi branch cut; else cs, sn = g / |g| and dth bounds the
+// angle between g_lin and g_seq plus the libm and rounding differences.
+__device__ __forceinline__ bool dr_orient_lin(uint32_t m0, uint32_t m1, const double (*ow)[4], int lane, double& gx,
+                                              double& gy, double& cs, double& sn, double& dth)
+{
+  const int l1 = lane + 32;
+  const double v0 = (double)m0, v1 = (double)m1;   // exact (<= 255)
+  double sx = v0 * ow[lane][0] + v1 * ow[l1][0];
+  double sy = v0 * ow[lane][1] + v1 * ow[l1][1];
+  double ax = v0 * ow[lane][2] + v1 * ow[l1][2];
+  double ay = v0 * ow[lane][3] + v1 * ow[l1][3];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    ax += __shfl_xor_sync(0xffffffffu, ax, o);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o);
+  }
+  gx = sx;
+  gy = sy;
+  const double bx = c_ogam * ax, by = c_ogam * ay;
+  const double g2 = sx * sx + sy * sy;
+  const double rn = rsqrt(g2);
+  const double gn = g2 * rn;
+  if (!(bx + by < 1e-3 * gn)) return false;                // includes g == 0
+  if (sx < 0.0 && fabs(sy) <= by) return false;            // theta near the +-pi cut
+  cs = sx * rn;
+  sn = sy * rn;
+  dth = 2.0 * (bx + by) / gn + 1e-14;
+  return true;
+}
+
+// The reference's sequential sums (one lane): the rare fallback of dr_orient_lin.
+__device__ __noinline__ void dr_orient_seq_g(const uint8_t* v, double& gx_out, double& gy_out)
+{
+  double gx = 0.0, gy = 0.0;
+  const int L = c_nlong;
+  for (int p = 0; p < L; p++) {
+    const double dv = dr_i2d((int)v[c_li[p]] - (int)v[c_lj[p]]);
+    gx += dv * c_wx[p];
+    gy += dv * c_wy[p];
+  }
+  gx_out = gx;
+  gy_out = gy;
+}
+
+// The reference order itself (one lane): the rare fallback of dr_orient_warp.
+__device__ __noinline__ double dr_orient_seq(const uint8_t* v)
+{
+  double gx = 0.0, gy = 0.0;
+  const int L = c_nlong;
+  for (int p = 0; p < L; p++) {
+    const double dv = dr_i2d((int)v[c_li[p]] - (int)v[c_lj[p]]);
+    gx += dv * c_wx[p];
+    gy += dv * c_wy[p];
+  }
+  const double th = atan2(gy, gx);
+  return th <= -CUDART_PI ? CUDART_PI : th;
+}
+
+__global__ void __launch_bounds__(DR_THREADS, 4) k_desc_region(const __grid_constant__ Geo g,
+                                                               const __grid_constant__ Bufs b, int n_streams)
+{
+  extern __shared__ __align__(16) uint8_t dsm[];
+  DrShared& sh = *reinterpret_cast<DrShared*>(dsm);
+  int* pre = reinterpret_cast<int*>(dsm + sizeof(DrShared));
+  __shared__ int sm_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NREGW]; });
+  const int total = pre[n_streams];
+  const int NU = g.bands_per_stream * b.nms_u;
+  const bool vec = (((uintptr_t)b.frames | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) & 3) == 0;
+  // this lane's two pattern points (lane, lane + 32)
+  const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
+  const bool has1 = lane + 32 < VF_NPTS;
+  const double p0x = __ldg(&g_ptab[lane][0]), p0y = __ldg(&g_ptab[lane][1]), p0r = __ldg(&g_ptab[lane][2]);
+  const double p1x = __ldg(&g_ptab[j1][0]), p1y = __ldg(&g_ptab[j1][1]), p1r = __ldg(&g_ptab[j1][2]);
+  // |p| of the two points: a centre point's position does not depend on theta
+  const double pn0 = sqrt(p0x * p0x + p0y * p0y), pn1 = has1 ? sqrt(p1x * p1x + p1y * p1y) : 0.0;
+  uint8_t* v = sh.v[wid];
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int sl = find_stream(pre, n_streams, item), s = b.s0 + sl;
+    const long long rslot = (long long)s * g.nreg + __ldcg(b.reg_work + (long long)s * g.nreg + item - pre[sl]);
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int cnt = min(__ldcg(b.reg_cnt + rslot), DR_RCAP);
+    const int ndesc = ctr[C_NDET];
+    const long long fb = feat_base(g, s, ctr[C_FRAME] & 1, ctr[C_NTOTAL]);
+    const uint32_t* list = b.reg_list + rslot * DR_RCAP;
+    const int* urec = b.unit_rec + 4LL * s * NU;
+    const int* uout = b.unit_out + (long long)s * NU;
+    const long long sbase = (long long)s * g.kp_cap;
+    // ---- footprint box of the region's keypoints ----
+    int xlo = 1 << 30, ylo = 1 << 30, xhi = -1, yhi = -1;
+    for (int i = tid; i < cnt; i += DR_THREADS) {
+      const uint32_t e = __ldcg(list + i);
+      const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
+      const long long slot = sbase + __ldcg(urec + 4 * u) + k;
+      int rmax;
+      const int reach = desc_reach(__ldcg(b.st_s + slot), rmax);
+      const int xi = (int)__ldcg(b.st_x + slot), yi = (int)__ldcg(b.st_y + slot);
+      xlo = min(xlo, xi - reach); xhi = max(xhi, xi + reach);
+      ylo = min(ylo, yi - reach); yhi = max(yhi, yi + reach);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o)); xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
+      ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o)); yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+    }
+    if (lane == 0) { sh.red[0][wid] = xlo; sh.red[1][wid] = xhi; sh.red[2][wid] = ylo; sh.red[3][wid] = yhi; }
+    __syncthreads();
+    if (tid == 0) b.reg_cnt[rslot] = 0;   // every thread has read cnt
+#pragma unroll
+    for (int w = 0; w < DR_WARPS; w++) {
+      xlo = min(xlo, sh.red[0][w]); xhi = max(xhi, sh.red[1][w]);
+      ylo = min(ylo, sh.red[2][w]); yhi = max(yhi, sh.red[3][w]);
+    }
+    xlo = max(xlo, 0); xhi = min(xhi, g.W - 1);
+    ylo = max(ylo, 0); yhi = min(yhi, g.H - 1);
+    const int ax0 = xlo & ~3, nwd = (xhi - ax0 + 4) >> 2, wc = 4 * nwd, P = wc + 2, hb = yhi - ylo + 1;
+    // ---- SAT, phase 1: row prefixes + column sums within 8 row blocks ----
+    const int RB = (hb + DR_WARPS - 1) / DR_WARPS;
+    for (int i = tid; i < P / 2; i += DR_THREADS) reinterpret_cast<uint32_t*>(sh.T)[i] = 0u;   // row ylo - 1
+    {
+      const int ra = 1 + wid * RB, rb = min(hb, (wid + 1) * RB);
+      uint32_t acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) acc[q] = 0u;
+      const uint8_t* fr = b.frames + (long long)(s - b.s0) * b.frame_stride + ax0;
+      const bool two = nwd > 32;
+      for (int r0 = ra; r0 <= rb; r0 += DR_PF) {
+        uint32_t wv[DR_PF][2];
+#pragma unroll
+        for (int q = 0; q < DR_PF; q++) {
+          const uint8_t* row = fr + (long long)(ylo + r0 + q - 1) * b.frame_pitch;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int j = lane + 32 * h, x = ax0 + 4 * j;
+            uint32_t w = 0u;
+            if (r0 + q <= rb && j < nwd) {
+              if (vec && x + 3 < g.W) w = __ldg(reinterpret_cast<const uint32_t*>(row + 4 * j));
+              else
+                for (int c = 0; c < 4; c++)
+                  if (x + c < g.W) w |= (uint32_t)__ldg(row + 4 * j + c) << (8 * c);
+            }
+            wv[q][h] = w;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < DR_PF; q++) {
+          const int r = r0 + q;
+          if (r > rb) break;
+          uint32_t* trow = reinterpret_cast<uint32_t*>(sh.T + r * P);
+          if (lane == 0) trow[0] = 0u;   // column ax0 - 1
+          uint32_t carry = 0u;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            if (h == 1 && !two) break;
+            const int j = lane + 32 * h;
+            const uint32_t w = wv[q][h];
+            const uint32_t q0 = w & 0xffu, q1 = __dp4a(w, 0x00000101u, 0u), q2 = __dp4a(w, 0x00010101u, 0u),
+                           q3 = __dp4a(w, 0x01010101u, 0u);
+            uint32_t inc = q3;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+              if (lane >= o) inc += t;
+            }
+            const uint32_t ex = carry + inc - q3;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+            acc[4 * h + 0] += ex + q0; acc[4 * h + 1] += ex + q1;
+            acc[4 * h + 2] += ex + q2; acc[4 * h + 3] += ex + q3;
+            if (j < nwd) {
+              trow[1 + 2 * j] = __byte_perm(acc[4 * h + 0], acc[4 * h + 1], 0x5410);
+              trow[2 + 2 * j] = __byte_perm(acc[4 * h + 2], acc[4 * h + 3], 0x5410);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: rows of block k += column totals of blocks 0 .. k - 1 ----
+    {
+      const int nfix = wc * (DR_WARPS - 1);
+      uint32_t off[DR_CITEMS];
+#pragma unroll
+      for (int q = 0; q < DR_CITEMS; q++) {
+        const int it = tid + q * DR_THREADS;
+        uint32_t o = 0u;
+        if (it < nfix) {
+          const int bk = 1 + it / wc, c = 2 + it % wc;
+          for (int k = 0; k < bk; k++) {
+            const int rl = min(hb, (k + 1) * RB);
+            if (rl >= 1 + k * RB) o += sh.T[rl * P + c];
+          }
+        }
+        off[q] = o;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < DR_CITEMS; q++) {
+        const int it = tid + q * DR_THREADS;
+        if (it < nfix && (off[q] & 0xffffu)) {
+          const int bk = 1 + it / wc, c = 2 + it % wc;
+          const int ra = 1 + bk * RB, rb = min(hb, (bk + 1) * RB);
+          for (int r = ra; r <= rb; r++) sh.T[r * P + c] = (uint16_t)(sh.T[r * P + c] + off[q]);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- warp per keypoint ----
+    for (int i = wid; i < cnt; i += DR_WARPS) {
+      const uint32_t e = __ldcg(list + i);
+      const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
+      const int rank = __ldcg(uout + u) + k;
+      if (rank >= ndesc) continue;   // capacity clamp (warp-uniform)
+      const long long slot = sbase + __ldcg(urec + 4 * u) + k;
+      const double kx = __ldcg(b.st_x + slot), ky = __ldcg(b.st_y + slot), sg = __ldcg(b.st_s + slot);
+      const long long o = fb + rank;
+      if (lane == 0) {
+        b.fx[o] = kx; b.fy[o] = ky; b.fs[o] = sg; b.fv[o] = __ldcg(b.st_v + slot);
+        b.forg[o] = 0; b.fage[o] = 0;
+      }
+      // theta = 0 box means (descriptor.py:128-131)
+      const uint32_t a0 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, 1.0, 0.0, p0x, p0y, p0r, false, nullptr);
+      const uint32_t a1 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, 1.0, 0.0, p1x, p1y, p1r, false, nullptr);
+      v[lane] = (uint8_t)a0;
+      if (has1) v[lane + 32] = (uint8_t)a1;
+      __syncwarp();
+      double th = 0.0, dth = 0.0;
+      bool ok = dr_orient_warp(v, lane, th, dth);
+      double cs = 0.0, sn = 0.0;
+      uint32_t m0 = 0u, m1 = 0u;
+      if (ok) {
+        sincos(th, &sn, &cs);
+        // rotated means; keep them only if no sample position is within the
+        // theta bound's reach of an integer
+        const double ue = 1.5 * sg * (dth + 4e-16);
+        double d0, d1;
+        m0 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p0x, p0y, p0r, true, &d0);
+        m1 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p1x, p1y, p1r, true, &d1);
+        const bool near0 = pn0 > 0.0 && d0 < ue * pn0 + 4e-12;
+        const bool near1 = has1 && pn1 > 0.0 && d1 < ue * pn1 + 4e-12;
+        ok = !__any_sync(0xffffffffu, near0 || near1);
+      }
+      if (!ok) {   // rare: the reference's sequential sum
+        double t = 0.0;
+        if (lane == 0) t = dr_orient_seq(v);
+        th = __shfl_sync(0xffffffffu, t, 0);
+        sincos(th, &sn, &cs);
+        m0 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p0x, p0y, p0r, true, nullptr);
+        m1 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p1x, p1y, p1r, true, nullptr);
+      }
+      if (lane == 0) b.ft[o] = th;
+      __syncwarp();
+      v[lane] = (uint8_t)m0;
+      if (has1) v[lane + 32] = (uint8_t)m1;
+      __syncwarp();
+      // 512 bits, MSB-first (descriptor.py:117-126,271-275)
+      uint32_t mine = 0u;
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        const uint32_t pr = __ldg(g_pairs + 32 * q + lane);   // si | sj << 16
+        const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
+        if (lane == q) mine = word;
+      }
+      if (lane < 16) reinterpret_cast<uint32_t*>(b.fdesc + o * 64)[lane] = __byte_perm(__brev(mine), 0, 0x0123);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================
+// k_desc_fused: the strip-SAT describe of one keypoint per warp in a single
+// pass (descriptor.py:85-144,271-275): theta = 0 box means -> orientation
+// (dr_orient_warp, certified against the sequential sum; dr_orient_seq when
+// the certificate fails) -> rotated box means -> 16 ballots.  The rotated
+// samples cover the same disk as the theta = 0 ones, so their SAT corners are
+// mostly L1 hits of the first pass.  Keypoints: the k_nms list b.gidx
+// (unit << 18 | index in unit) of the streams [s0, s0 + n).
+// ============================================================================
+__global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constant__ Geo g,
+                                                         const __grid_constant__ Bufs b, int n_streams)
+{
+  __shared__ __align__(16) uint8_t vals[DSW][DW_ROW];
+  __shared__ uint32_t pairs[VF_NBITS];
+  __shared__ double ptab[64][3];   // pattern point x, y, smoothing radius
+  __shared__ double ow[64][4];     // orientation linear form (g_ow)
+  __shared__ int sm_warp[32];
+  extern __shared__ int pre[];     // [n_streams + 1]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = g_pairs[k];
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NGLOB]; });
+  const int total = pre[n_streams];
+  for (int j = threadIdx.x; j < 64; j += 32 * DSW) {
+    ptab[j][0] = g_ptab[j][0]; ptab[j][1] = g_ptab[j][1]; ptab[j][2] = g_ptab[j][2];
+    ow[j][0] = g_ow[j][0]; ow[j][1] = g_ow[j][1]; ow[j][2] = g_ow[j][2]; ow[j][3] = g_ow[j][3];
+  }
+  __syncthreads();
+  const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
+  const bool has1 = lane + 32 < VF_NPTS;
+  const double pn0 = sqrt(ptab[lane][0] * ptab[lane][0] + ptab[lane][1] * ptab[lane][1]);
+  const double pn1 = has1 ? sqrt(ptab[j1][0] * ptab[j1][0] + ptab[j1][1] * ptab[j1][1]) : 0.0;
+  uint8_t* v = vals[wid];
+  // The warp's keypoints are gi = g0 + k * Wt; their headers (position, scale,
+  // output slot) are fetched 32 at a time, lane k for keypoint k, and lane k
+  // computes keypoint k's theta = atan2(gy, gx) after the batch.
+  const int Wt = gridDim.x * DSW;
+  for (int g0 = blockIdx.x * DSW + wid; g0 < total; g0 += 32 * Wt) {
+    const int gl = g0 + lane * Wt;
+    long long o_l = -1;
+    int s_l = 0;
+    double kx_l = 0.0, ky_l = 0.0, sg_l = 0.0;
+    if (gl < total) {
+      const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
+      s_l = b.s0 + sl;
+      const int* ctr = b.ctr + s_l * C_NCTR;
+      const uint32_t e = (uint32_t)__ldcg(b.gidx + (long long)s_l * g.kp_cap + i);
+      const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
+      const long long ui = (long long)s_l * g.bands_per_stream * b.nms_u + u;
+      const long long si = (long long)s_l * g.kp_cap + __ldcg(b.unit_rec + 4 * ui) + k;   // staging slot
+      const int rank = __ldcg(b.unit_out + ui) + k;
+      kx_l = __ldcg(b.st_x + si); ky_l = __ldcg(b.st_y + si); sg_l = __ldcg(b.st_s + si);
+      if (rank < ctr[C_NDET]) {   // ranks past the capacity-clamped count are not written
+        o_l = feat_base(g, s_l, ctr[C_FRAME] & 1, ctr[C_NTOTAL]) + rank;
+        b.fx[o_l] = kx_l; b.fy[o_l] = ky_l; b.fs[o_l] = sg_l; b.fv[o_l] = __ldcg(b.st_v + si);
+        b.forg[o_l] = 0; b.fage[o_l] = 0;
+      }
+    }
+    const int nk = min(32, (total - g0 + Wt - 1) / Wt);
+    double gx_l = 0.0, gy_l = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < nk; k++) {
+      const long long o = __shfl_sync(0xffffffffu, o_l, k);
+      if (o < 0) continue;   // warp-uniform
+      const int s = __shfl_sync(0xffffffffu, s_l, k);
+      const double kx = __shfl_sync(0xffffffffu, kx_l, k), ky = __shfl_sync(0xffffffffu, ky_l, k);
+      const double sg = __shfl_sync(0xffffffffu, sg_l, k);
+      const uint32_t* S = b.sat + (long long)s * g.W * g.H;
+      uint32_t m0, m1;
+      point_means2(S, g, kx, ky, sg, 1.0, 0.0, ptab[lane], ptab[j1], false, m0, m1);
+      if (!has1) m1 = 0u;
+      const uint32_t z0 = m0, z1 = m1;   // theta = 0 means (for the fallback)
+      double gx, gy, cs = 1.0, sn = 0.0, dth = 0.0;
+      bool ok = dr_orient_lin(m0, m1, ow, lane, gx, gy, cs, sn, dth);
+      if (ok) {
+        double d0, d1;
+        point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], true, m0, m1, &d0, &d1);
+        const double ue = 1.5 * sg * dth;
+        const bool near0 = pn0 > 0.0 && d0 < ue * pn0 + 1e-11;
+        const bool near1 = has1 && pn1 > 0.0 && d1 < ue * pn1 + 1e-11;
+        ok = !__any_sync(0xffffffffu, near0 || near1);
+      }
+      if (!ok) {   // rare: the reference's sequential sum and the device libm
+        v[lane] = (uint8_t)z0;
+        if (has1) v[lane + 32] = (uint8_t)z1;
+        __syncwarp();
+        double tx = 0.0, ty = 0.0;
+        if (lane == 0) dr_orient_seq_g(v, tx, ty);
+        gx = __shfl_sync(0xffffffffu, tx, 0);
+        gy = __shfl_sync(0xffffffffu, ty, 0);
+        double th = atan2(gy, gx);
+        th = th <= -CUDART_PI ? CUDART_PI : th;
+        sincos(th, &sn, &cs);
+        point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], true, m0, m1);
+      }
+      if (lane == k) { gx_l = gx; gy_l = gy; }
+      __syncwarp();
+      v[lane] = (uint8_t)m0;
+      if (has1) v[lane + 32] = (uint8_t)m1;
+      __syncwarp();
+      uint32_t mine = 0u;
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        const uint32_t pr = pairs[32 * q + lane];   // si | sj << 16 (smem, conflict-free)
+        const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
+        if (lane == q) mine = word;
+      }
+      if (lane < 16) reinterpret_cast<uint32_t*>(b.fdesc + o * 64)[lane] = __byte_perm(__brev(mine), 0, 0x0123);
+      __syncwarp();
+    }
+    if (o_l >= 0) {   // theta of lane's keypoint (descriptor.py:142-143)
+      double th = atan2(gy_l, gx_l);
+      b.ft[o_l] = th <= -CUDART_PI ? CUDART_PI : th;
     }
   }
 }
