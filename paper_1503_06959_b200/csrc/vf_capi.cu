@@ -807,8 +807,9 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   stage_mark(c, 4, st);
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
   b.nms_u = nms_units(g, n);
-  static const int desc_region = getenv("VF_DESC_REGION") ? atoi(getenv("VF_DESC_REGION")) : 0;
+  const int desc_region = getenv("VF_DESC_REGION") ? atoi(getenv("VF_DESC_REGION")) : 0;
   b.desc_bin = desc_region ? 1 : 2;
+  b.orient_seq = getenv("VF_ORIENT_SEQ") && atoi(getenv("VF_ORIENT_SEQ")) != 0;
   k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms");
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
   stage_mark(c, 5, st);

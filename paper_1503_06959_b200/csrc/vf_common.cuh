@@ -124,6 +124,7 @@ struct Bufs {
   int* gidx;            // [S][kp_cap]: kept keypoints of the strip-SAT describe path, (unit << 18 | index in
                         // unit) from k_nms, replaced by the output rank (or -1) in k_desc_sample pass 0
   int desc_bin;         // k_nms: 0 stand-alone (no describe lists), 1 region + strip-SAT paths, 2 strip SAT only
+  int orient_seq;       // k_desc_fused: always take the sequential-sum orientation (test hook, VF_ORIENT_SEQ=1)
   int* reg_cnt;         // [S][nreg] small-scale keypoints per describe region (zeroed by k_desc_region)
   uint32_t* reg_list;   // [S][nreg][DR_RCAP] their (unit << 18 | index in unit) entries
   int* reg_work;        // [S][nreg] regions with keypoints this step (k_nms_finish)

@@ -3009,7 +3009,7 @@ __global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constan
       if (!has1) m1 = 0u;
       const uint32_t z0 = m0, z1 = m1;   // theta = 0 means (for the fallback)
       double gx, gy, cs = 1.0, sn = 0.0, dth = 0.0;
-      bool ok = dr_orient_lin(m0, m1, ow, lane, gx, gy, cs, sn, dth);
+      bool ok = dr_orient_lin(m0, m1, ow, lane, gx, gy, cs, sn, dth) && !b.orient_seq;
       if (ok) {
         double d0, d1;
         point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], true, m0, m1, &d0, &d1);
