@@ -217,9 +217,8 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   long long cap = c.kp_capacity > 0 ? c.kp_capacity : std::max(65536LL, (long long)g.W * g.H / 8);
   g.kp_cap = (int)std::min(cap, 1LL << 28);
   g.prop_chunks = cdiv(g.kp_cap, 1024);
-  // describe regions; describe-list entries pack the NMS unit into 14 bits
-  g.rgx = cdiv(g.W, DR_RW); g.rgy = cdiv(g.H, DR_RH); g.nreg = g.rgx * g.rgy;
-  if ((long long)g.bands_per_stream * VF_TILE_H >= (1LL << (32 - DR_UNIT_SHIFT))) return VF_ERR_ARG;
+  g.nms_chunks = cdiv(g.kp_cap, 1 << NMS_CHUNK_LOG);
+  if (g.W > 8192 || g.NL > 16) return VF_ERR_ARG;   // NMS candidate code: layer << 26 | y << 13 | x
   return VF_OK;
 }
 
@@ -267,7 +266,7 @@ struct vf_ctx {
   int pyr_smem;
   int fast_grid;
   int desc_grid;
-  int sat_grid, sat_smem, desc_smem, dsample_grid, dorient_grid, dregion_grid, dregion_smem, dfused_grid;
+  int sat_grid, sat_smem, desc_smem, dfused_grid, nmst_grid;
   vft::Setup bmq{};                     // temporal mode: block-match set-up (device offsets)
   int bm_grid = 0, bm_smem = 0;
   // host-input staging (vf_process_host)
@@ -447,14 +446,6 @@ int vf_set_pattern(const double* points, const double* radii, int m, const int32
   e = e ? e : cudaMemcpyToSymbol(c_wx, wx, sizeof(double) * L);
   e = e ? e : cudaMemcpyToSymbol(c_wy, wy, sizeof(double) * L);
   e = e ? e : cudaMemcpyToSymbol(c_nlong, &L, sizeof(int));
-  double pmax = 0.0, radmax = 0.0;   // footprint of the region describe path (k_desc_region)
-  for (int j = 0; j < m; j++) {
-    pmax = std::max(pmax, std::sqrt(px[j] * px[j] + py[j] * py[j]));
-    radmax = std::max(radmax, radii[j]);
-  }
-  pmax *= 1.0 + 1e-12;
-  e = e ? e : cudaMemcpyToSymbol(c_pmax, &pmax, sizeof(double));
-  e = e ? e : cudaMemcpyToSymbol(c_radmax, &radmax, sizeof(double));
   uint32_t pairs[VF_NBITS];
   double ptab[64][3];
   for (int k = 0; k < nbits; k++) pairs[k] = (uint32_t)(uint16_t)si[k] | ((uint32_t)(uint16_t)sj[k] << 16);
@@ -527,9 +518,10 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.sat_bits = A.get<unsigned>((size_t)S * g.sty * g.stw_words);
   b.sat_work = A.get<int>((size_t)S * g.sat_tiles);
   b.sat_count = A.get<int>((size_t)S);
-  b.reg_cnt = A.get<int>((size_t)S * g.nreg);
-  b.reg_list = A.get<uint32_t>((size_t)S * g.nreg * DR_RCAP);
-  b.reg_work = A.get<int>((size_t)S * g.nreg);
+  b.cand = A.get<uint32_t>((size_t)S * cap);
+  b.cand_rank = A.get<int>((size_t)S * cap);
+  b.chunk_off = A.get<int>((size_t)S * g.nms_chunks);
+  b.nms_cnt = A.get<int>((size_t)S * 4);
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -566,19 +558,11 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sat, 256, c->sat_smem);
   c->sat_grid = std::max(1, g_num_sms * std::max(occ, 1));
   occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_sample, 32 * DSW, (S + 1) * sizeof(int));
-  c->dsample_grid = std::max(1, g_num_sms * std::max(occ, 1));
-  occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_orient, DO_THREADS, (S + 1) * sizeof(int));
-  c->dorient_grid = std::max(1, g_num_sms * std::max(occ, 1));
-  occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_fused, 32 * DSW, (S + 1) * sizeof(int));
   c->dfused_grid = std::max(1, g_num_sms * std::max(occ, 1));
-  c->dregion_smem = (int)sizeof(DrShared) + (S + 1) * (int)sizeof(int);
-  cudaFuncSetAttribute(k_desc_region, cudaFuncAttributeMaxDynamicSharedMemorySize, c->dregion_smem);
   occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_desc_region, DR_THREADS, c->dregion_smem);
-  c->dregion_grid = std::max(1, g_num_sms * std::max(occ, 1));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_nms_test, 1 << NMS_CHUNK_LOG, (S + 1) * sizeof(int));
+  c->nmst_grid = std::max(1, g_num_sms * std::max(occ, 1));
   if (g.mask_mode == 3) {                    // temporal baseline state
     Gop o;
     gop_from_config(*cfg, o);
@@ -806,22 +790,21 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_fast");
   stage_mark(c, 4, st);
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
-  b.nms_u = nms_units(g, n);
-  const int desc_region = getenv("VF_DESC_REGION") ? atoi(getenv("VF_DESC_REGION")) : 0;
-  b.desc_bin = desc_region ? 1 : 2;
+  // candidate-parallel NMS: ordered candidate list, thread-per-candidate test +
+  // refinement with chunk ranks, chunk offsets + FrameReport
+  b.nms_u = 1;
+  b.desc_bin = 1;
   b.orient_seq = getenv("VF_ORIENT_SEQ") && atoi(getenv("VF_ORIENT_SEQ")) != 0;
-  k_nms<<<dim3(cdiv((long long)g.bands_per_stream * b.nms_u, NMS_WARPS), n), NMS_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms");
+  k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
+  k_nms_test<<<c->nmst_grid, 1 << NMS_CHUNK_LOG, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_nms_test");
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
   stage_mark(c, 5, st);
-  // Describe (descriptor.py:85-144).  Default: the strip SATs of the tiles
-  // k_nms marked, then k_desc_fused (warp per keypoint: theta = 0 means,
-  // orientation, rotated means, bits), for two stream halves on two
-  // concurrent high-priority describe streams (VF_DESC_PAR halves).
-  // VF_DESC_REGION=1: small-scale keypoints through k_desc_region on the main
-  // stream, the rest through the strip-SAT chain beside it.
+  // Describe (descriptor.py:85-144): the strip SATs of the tiles k_nms_test
+  // marked, then k_desc_fused (warp per keypoint: theta = 0 means,
+  // orientation, rotated means, bits), for VF_DESC_PAR (default 2) stream
+  // halves on concurrent high-priority describe streams.
   static const int dpar_env = getenv("VF_DESC_PAR") ? std::max(1, std::min(2, atoi(getenv("VF_DESC_PAR")))) : 2;
-  const bool region = b.desc_bin == 1;
-  const int dpar = region ? 1 : std::min(dpar_env, n);
+  const int dpar = std::min(dpar_env, n);
   if ((int)c->dstreams.size() < 2 * (gi + 1)) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -851,9 +834,6 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh, 0); DBG_SYNC(ds, "k_sat");
     k_desc_fused<<<c->dfused_grid, 32 * DSW, pb, ds>>>(g, bh, nh); DBG_SYNC(ds, "k_desc_fused");
     cudaEventRecord(c->djoin[2 * gi + h], ds);
-  }
-  if (region) {
-    k_desc_region<<<c->dregion_grid, DR_THREADS, c->dregion_smem, st>>>(g, b, n); DBG_SYNC(st, "k_desc_region");
   }
   for (int h = 0; h < dpar; h++) cudaStreamWaitEvent(st, c->djoin[2 * gi + h], 0);
   // k_propagate (stage 7) is timed on the side stream; the join wait counts
@@ -1114,7 +1094,9 @@ static int regrow(vf_ctx* c, long long new_cap, cudaStream_t st)
     ptr = q;
     return true;
   };
-  bool ok = fresh(b.gidx, (size_t)S * new_cap) && fresh(b.st_x, (size_t)S * new_cap) &&
+  bool ok = fresh(b.gidx, (size_t)S * new_cap) && fresh(b.cand, (size_t)S * new_cap) &&
+            fresh(b.cand_rank, (size_t)S * new_cap) &&
+            fresh(b.chunk_off, (size_t)S * cdiv(new_cap, 1 << NMS_CHUNK_LOG)) && fresh(b.st_x, (size_t)S * new_cap) &&
             fresh(b.st_y, (size_t)S * new_cap) && fresh(b.st_s, (size_t)S * new_cap) &&
             fresh(b.st_v, (size_t)S * new_cap) && fresh(b.prop_cnt, (size_t)S * chunks) &&
             fresh(b.prop_out, (size_t)S * chunks);
@@ -1148,6 +1130,7 @@ static int regrow(vf_ctx* c, long long new_cap, cudaStream_t st)
   if (!ok) return VF_ERR_CUDA;
   g.kp_cap = (int)new_cap;
   g.prop_chunks = chunks;
+  g.nms_chunks = cdiv(new_cap, 1 << NMS_CHUNK_LOG);
   if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
   pipe_free(c);   // re-created with the new capacity on the next submit
   return VF_OK;

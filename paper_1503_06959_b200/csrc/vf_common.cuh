@@ -31,8 +31,7 @@ enum {
   C_NCAND = 11,     // FAST candidates
   C_EPOCH = 12,     // monotonic step id (activity stamps), survives vf_reset
   C_PTICKET = 13,   // last-CTA ticket of the propagation-count CTAs (k_worklist)
-  C_NGLOB = 14,     // kept keypoints described from the strip SAT (b.gidx list) this step
-  C_NREGW = 15,     // describe regions with small-scale keypoints this step (b.reg_work)
+  C_NGLOB = 14,     // kept keypoints in the describe list (b.gidx) this step
   C_NCTR = 16
 };
 #define VF_ERRBIT_CAPACITY 1
@@ -41,16 +40,7 @@ enum {
 
 #define VF_ST 32   // strip-SAT tile edge and strip height (o0 pixels)
 
-// Describe regions (k_desc_region): keypoints whose 60 boxes stay within
-// DR_FMAX o0 pixels of floor(x, y) and are at most 15 x 15 (box sums < 2^16)
-// are binned by position into DR_RW x DR_RH regions; a CTA builds one uint16
-// SAT of the region's footprint box in shared memory and describes them all.
-#define DR_RW 64
-#define DR_RH 28
-#define DR_FMAX 53
-#define DR_RMAX 7
-#define DR_RCAP 512            // keypoints listed per region (more go to the strip-SAT path)
-#define DR_UNIT_SHIFT 18       // list entry = unit << 18 | index of the keypoint in its NMS unit
+#define NMS_CHUNK_LOG 8          // NMS candidates per k_nms_test CTA pass: 256
 
 struct LayerGeo {
   int w, h;
@@ -105,7 +95,7 @@ struct Geo {
   int pyr_split;        // masked frames build the intra-octave chain only near active cells (k_pyramid4)
   int pyr_halo;         // o0 pixels a FAST ring reaches around a tile's derived pixels
   int nms_wrap;         // stand-alone: numpy negative-index wrap in the 3x3 test
-  int rgx, rgy, nreg;   // describe regions (DR_RW x DR_RH o0 pixels) per stream: columns, rows, total
+  int nms_chunks;       // NMS candidate chunks per stream: kp_cap / NMS_CHUNK_THREADS
 };
 
 // Per-launch stream-batch pointers.
@@ -121,13 +111,13 @@ struct Bufs {
   int* unit_rec;        // [S][bands_per_stream * nms_u][4]: staging base, kept, border-ok, dropped per NMS unit
   int* unit_out;        // [S][bands_per_stream * nms_u]: output offset of the unit's kept keypoints
   int* band_cand;       // [S][bands_per_stream]: FAST candidates of the band this step
-  int* gidx;            // [S][kp_cap]: kept keypoints of the strip-SAT describe path, (unit << 18 | index in
-                        // unit) from k_nms, replaced by the output rank (or -1) in k_desc_sample pass 0
-  int desc_bin;         // k_nms: 0 stand-alone (no describe lists), 1 region + strip-SAT paths, 2 strip SAT only
+  int* gidx;            // [S][kp_cap] describe list: candidate indices of the kept keypoints (k_nms_test)
+  int desc_bin;         // 1: pipeline NMS (k_nms_list / k_nms_test, describe list); 0: stand-alone k_nms
+  uint32_t* cand;       // [S][kp_cap] NMS candidates (layer << 26 | y << 13 | x) in (layer, y, x) order
+  int* cand_rank;       // [S][kp_cap] kept candidate's rank within its NMS chunk
+  int* chunk_off;       // [S][nms_chunks] kept count of each chunk (k_nms_test), then its output offset
+  int* nms_cnt;         // [S][4] survivors inside / outside the border margin (FrameReport)
   int orient_seq;       // k_desc_fused: always take the sequential-sum orientation (test hook, VF_ORIENT_SEQ=1)
-  int* reg_cnt;         // [S][nreg] small-scale keypoints per describe region (zeroed by k_desc_region)
-  uint32_t* reg_list;   // [S][nreg][DR_RCAP] their (unit << 18 | index in unit) entries
-  int* reg_work;        // [S][nreg] regions with keypoints this step (k_nms_finish)
   int* prop_cnt;        // [S][prop_chunks]
   int* prop_out;        // [S][prop_chunks]
   uint8_t* cells;       // [S][cell_slab]

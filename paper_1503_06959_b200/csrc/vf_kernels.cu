@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
     if (tid == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
       b.ctr[s * C_NCTR + C_NGLOB] = 0;
+      b.nms_cnt[4 * s] = 0; b.nms_cnt[4 * s + 1] = 0;
       b.sat_count[s] = 0;
       b.work_count[s] = 0;
     }
@@ -379,6 +380,14 @@ __global__ void __launch_bounds__(256) k_pyramid(const __grid_constant__ Geo g, 
     const int y = i / nseg, k = i - y * nseg, col = blockIdx.x * nseg + k;
     if (col < g.stx) b.rowsum[((long long)s * g.H + Y0 + y) * g.stx + col] = rsum[i];
   }
+}
+
+// Flattened item index -> stream via the per-stream prefix (stream_prefix).
+__device__ __forceinline__ int find_stream(const int* pre, int n_streams, int gi)
+{
+  int lo = 0, hi = n_streams;
+  while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= gi) lo = m; else hi = m; }
+  return lo;
 }
 
 // Exclusive prefix over streams of a per-stream count, computed by the whole
@@ -570,6 +579,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
     if (tid == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
       b.ctr[s * C_NCTR + C_NGLOB] = 0;
+      b.nms_cnt[4 * s] = 0; b.nms_cnt[4 * s + 1] = 0;
       b.sat_count[s] = 0;
       b.work_count[s] = 0;
     }
@@ -826,6 +836,7 @@ __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, co
     if (threadIdx.x == 0) {
       b.ctr[s * C_NCTR + C_STAGE] = 0;
       b.ctr[s * C_NCTR + C_NGLOB] = 0;
+      b.nms_cnt[4 * s] = 0; b.nms_cnt[4 * s + 1] = 0;
       b.sat_count[s] = 0;
       b.work_count[s] = 0;
     }
@@ -1804,51 +1815,20 @@ __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int 
     }
 }
 
-// Footprint reach (o0 pixels around floor(x), floor(y)) of a keypoint's 60
-// boxes: sample offsets |p| <= c_pmax sigma (+ rounding), box radius rmax =
-// floor(c_radmax sigma + 0.5) (descriptor.py:56-60), one pixel of slack.
-__device__ __forceinline__ int desc_reach(double sg, int& rmax)
+// Warp-collective, at k_nms_test's kept-keypoint site: append the kept
+// keypoints (candidate index c) to the stream's describe list (warp-aggregated
+// atomic) and mark the SAT tiles of their footprints.
+__device__ __forceinline__ void desc_list_kept(const Geo& g, const Bufs& b, int s, bool kp, double x, double y,
+                                               double sg, int c, int lane)
 {
-  rmax = __double2int_rd(c_radmax * sg + 0.5);
-  return (int)ceil(c_pmax * sg) + 2 + rmax;
-}
-
-// Warp-collective, at k_nms's kept-keypoint site: small-scale keypoints
-// (every box <= 15 x 15, footprint within DR_FMAX) are binned into their
-// DR_RW x DR_RH describe region (warp-aggregated atomics); the others, and the
-// overflow of a full region, are listed for the strip-SAT describe path and
-// their footprint's SAT tiles marked.  Entry e = unit << 18 | index in unit.
-__device__ __forceinline__ void desc_bin_kept(const Geo& g, const Bufs& b, int s, bool kp, double x, double y,
-                                              double sg, uint32_t e, int lane)
-{
-  const unsigned NONE = 0xffffffffu;
-  unsigned key = NONE;
-  if (kp && b.desc_bin == 1) {
-    int rmax;
-    const int reach = desc_reach(sg, rmax);
-    if (rmax <= DR_RMAX && reach <= DR_FMAX) key = (unsigned)(((int)y / DR_RH) * g.rgx + (int)x / DR_RW);
-  }
-  bool glob = kp && key == NONE;
-  if (__any_sync(0xffffffffu, key != NONE)) {
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(peers) - 1;
-    int bv = 0;
-    if (key != NONE && lane == leader) bv = atomicAdd(b.reg_cnt + (long long)s * g.nreg + key, __popc(peers));
-    bv = __shfl_sync(0xffffffffu, bv, leader);
-    if (key != NONE) {
-      const int li = bv + __popc(peers & ((1u << lane) - 1));
-      if (li < DR_RCAP) b.reg_list[((long long)s * g.nreg + key) * DR_RCAP + li] = e;
-      else glob = true;
-    }
-  }
-  const unsigned gm = __ballot_sync(0xffffffffu, glob);
+  const unsigned gm = __ballot_sync(0xffffffffu, kp);
   if (gm) {
     const int leader = __ffs(gm) - 1;
     int gb = 0;
     if (lane == leader) gb = atomicAdd(b.ctr + s * C_NCTR + C_NGLOB, __popc(gm));
     gb = __shfl_sync(0xffffffffu, gb, leader);
-    if (glob) {
-      b.gidx[(long long)s * g.kp_cap + gb + __popc(gm & ((1u << lane) - 1))] = (int)e;
+    if (kp) {
+      b.gidx[(long long)s * g.kp_cap + gb + __popc(gm & ((1u << lane) - 1))] = c;
       mark_sat_tiles(g, b, s, x, y, sg, 0);
     }
   }
@@ -2004,15 +1984,10 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
           const unsigned kb = __ballot_sync(0xffffffffu, o.flags & 4);
           n_ok += __popc(__ballot_sync(0xffffffffu, o.flags & 2));
           n_drop += __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
-          const int kidx = kept + __popc(kb & ((1u << lane) - 1));   // index in the unit's kept list
           if (o.flags & 4) {
-            const long long dst = (long long)s * g.kp_cap + base + kidx;
+            const long long dst = (long long)s * g.kp_cap + base + kept + __popc(kb & ((1u << lane) - 1));
             b.st_x[dst] = o.x; b.st_y[dst] = o.y; b.st_s[dst] = o.sig; b.st_v[dst] = o.v;
-            if (um && !b.desc_bin) mark_sat_tiles(g, b, s, o.x, o.y, o.sig, epoch);
           }
-          if (b.desc_bin)
-            desc_bin_kept(g, b, s, (o.flags & 4) != 0, o.x, o.y, o.sig,
-                          ((uint32_t)unit << DR_UNIT_SHIFT) | (uint32_t)kidx, lane);
           kept += __popc(kb);
           __syncwarp();
           const uint16_t rest = lane + nb < qn ? sq[w][lane + nb] : (uint16_t)0;
@@ -2031,6 +2006,159 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
   if (lane == 0) *rec = make_int4(base, kept, n_ok, n_drop);
 }
 
+// ============================================================================
+// Candidate-parallel scale-space NMS of the pipeline (detector.py:239-307):
+//   k_nms_list   warp per active band: the band's FAST bitmap words in
+//                row-major order -> candidate codes (layer, y, x) at the
+//                band's offset (prefix of the active bands' k_fast counts), so
+//                the list is in the reference's (layer, y, x) order;
+//   k_nms_test   thread per candidate, NMS_CHUNK candidates per CTA pass:
+//                nms_test + nms_refine (strict 3x3 + cross-layer maximum,
+//                fp64 refinement, border and merge filters), kept records in
+//                the candidate's staging slot, rank within the chunk by a
+//                block scan, the chunk's kept count; kept keypoints join the
+//                describe list and mark their SAT tiles;
+//   k_nms_finish chunk counts -> output offsets (k_desc_fused: rank = chunk
+//                offset + rank in chunk), FrameReport, SAT-tile work list.
+// ============================================================================
+#define NL_WARPS 8
+__device__ __forceinline__ int band_count(const Bufs& b, const Geo& g, int s, int bid, int epoch)
+{
+  const long long i = (long long)s * g.bands_per_stream + bid;
+  return b.band_stamp[i] == epoch ? __ldcg(b.band_cand + i) : 0;
+}
+
+__global__ void __launch_bounds__(32 * NL_WARPS) k_nms_list(const __grid_constant__ Geo g,
+                                                            const __grid_constant__ Bufs b)
+{
+  __shared__ int red[NL_WARPS], cnt[NL_WARPS];
+  const int s = b.s0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int epoch = stream_epoch(b, s);
+  const int band0 = blockIdx.x * NL_WARPS, nb = g.bands_per_stream;
+  // candidates of the active bands before this CTA's
+  int part = 0;
+  for (int i = tid; i < band0; i += 32 * NL_WARPS) part += band_count(b, g, s, i, epoch);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  const int bid = band0 + w;
+  const int mine = bid < nb ? band_count(b, g, s, bid, epoch) : 0;
+  if (lane == 0) { red[w] = part; cnt[w] = mine; }
+  __syncthreads();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int k = 0; k < NL_WARPS; k++) {
+    off += red[k] + (k < w ? cnt[k] : 0);
+    tot += cnt[k];
+  }
+  int* ctr = b.ctr + s * C_NCTR;
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) {
+    int all = tot;
+#pragma unroll
+    for (int k = 0; k < NL_WARPS; k++) all += red[k];
+    ctr[C_STAGE] = all;   // the stream's candidates (capacity retry sizing)
+    if (all > g.kp_cap) atomicOr(&ctr[C_ERR], VF_ERRBIT_STAGING);
+  }
+  if (mine == 0 || off + mine > g.kp_cap) return;
+  int l = 0;
+  while (l + 1 < g.NL && bid >= g.L[l + 1].band_base) l++;
+  const LayerGeo& Lg = g.L[l];
+  const int ys = (bid - Lg.band_base) * VF_TILE_H;
+  const int bmw = Lg.bm_words, nw = min(VF_TILE_H, Lg.h - ys) * bmw;
+  const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)ys * bmw;
+  uint32_t* out = b.cand + (long long)s * g.kp_cap;
+  const uint32_t lcode = (uint32_t)l << 26;
+  int pos = off;
+  for (int k0 = 0; k0 < nw; k0 += 128) {
+    uint32_t wd[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int k = k0 + 32 * q + lane;
+      wd[q] = k < nw ? __ldcg(bm + k) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const unsigned any = __ballot_sync(0xffffffffu, wd[q] != 0u);
+      if (!any) continue;
+      const int k = k0 + 32 * q + lane;
+      int t;
+      int p = pos + warp_excl_scan(__popc(wd[q]), lane, t);
+      if (wd[q]) {
+        const int r = k / bmw, cw = k - r * bmw;
+        const uint32_t base = lcode | ((uint32_t)(ys + r) << 13) | (uint32_t)(32 * cw);
+        for (uint32_t m = wd[q]; m; m &= m - 1u) out[p++] = base + (uint32_t)(__ffs(m) - 1);
+      }
+      pos += t;
+    }
+  }
+}
+
+#define NMS_CHUNK_THREADS (1 << NMS_CHUNK_LOG)
+#ifndef NMS_TEST_MINB
+#define NMS_TEST_MINB 4
+#endif
+__global__ void __launch_bounds__(NMS_CHUNK_THREADS, NMS_TEST_MINB) k_nms_test(const __grid_constant__ Geo g,
+                                                                const __grid_constant__ Bufs b, int n_streams)
+{
+  __shared__ int sm_warp[32];
+  __shared__ int red[2][NMS_CHUNK_THREADS / 32];
+  __shared__ short sq[NMS_CHUNK_THREADS];   // survivors of the chunk (offsets in the chunk)
+  extern __shared__ int pre[];   // [n_streams + 1]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  stream_prefix(n_streams, pre, sm_warp, [&](int sl) {
+    const int* ctr = b.ctr + (b.s0 + sl) * C_NCTR;
+    return (ctr[C_ERR] & VF_ERRBIT_STAGING) ? 0 : (ctr[C_STAGE] + NMS_CHUNK_THREADS - 1) >> NMS_CHUNK_LOG;
+  });
+  const int total = pre[n_streams];
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const int sl = find_stream(pre, n_streams, item), s = b.s0 + sl, ch = item - pre[sl];
+    const int c = (ch << NMS_CHUNK_LOG) + tid;
+    const int ncand = b.ctr[s * C_NCTR + C_STAGE];
+    const int um = use_mask(g, b, s);
+    const uint32_t* cl = b.cand + (long long)s * g.kp_cap;
+    bool surv = false;
+    if (c < ncand) {
+      const uint32_t code = __ldcg(cl + c);
+      surv = nms_test(g, b, s, um, (int)(code >> 26), (int)((code >> 13) & 0x1fffu), (int)(code & 0x1fffu));
+    }
+    // survivors compacted in candidate order, so the refinement runs on full warps
+    int nsurv;
+    const int sr = block_excl_scan<int>(surv ? 1 : 0, sm_warp, nsurv);
+    if (surv) sq[sr] = (short)tid;
+    __syncthreads();
+    NmsOut o;
+    o.flags = 0;
+    int cs = 0;
+    if (tid < nsurv) {
+      cs = (ch << NMS_CHUNK_LOG) + sq[tid];
+      const uint32_t code = __ldcg(cl + cs);
+      o = nms_refine(g, b, s, um, (int)(code >> 26), (int)((code >> 13) & 0x1fffu), (int)(code & 0x1fffu));
+    }
+    const bool kp = (o.flags & 4) != 0;
+    int nk;
+    const int r = block_excl_scan<int>(kp ? 1 : 0, sm_warp, nk);
+    const long long si = (long long)s * g.kp_cap + cs;
+    if (kp) {
+      b.st_x[si] = o.x; b.st_y[si] = o.y; b.st_s[si] = o.sig; b.st_v[si] = o.v;
+      b.cand_rank[si] = r;
+    }
+    desc_list_kept(g, b, s, kp, o.x, o.y, o.sig, cs, lane);
+    // FrameReport counts: survivors inside / outside the border margin
+    int n_ok = __popc(__ballot_sync(0xffffffffu, o.flags & 2));
+    int n_dr = __popc(__ballot_sync(0xffffffffu, (o.flags & 1) && !(o.flags & 2)));
+    if (lane == 0) { red[0][wid] = n_ok; red[1][wid] = n_dr; }
+    __syncthreads();
+    if (tid == 0) {
+      n_ok = 0; n_dr = 0;
+#pragma unroll
+      for (int k = 0; k < NMS_CHUNK_THREADS / 32; k++) { n_ok += red[0][k]; n_dr += red[1][k]; }
+      b.chunk_off[(long long)s * g.nms_chunks + ch] = nk;
+      if (n_ok) atomicAdd(b.nms_cnt + 4 * s + 0, n_ok);
+      if (n_dr) atomicAdd(b.nms_cnt + 4 * s + 1, n_dr);
+    }
+    __syncthreads();
+  }
+}
+
 // After k_nms (stream order), one CTA per stream: band output offsets (scan
 // of the kept counts in band order), the SAT-tile work list (the bitmap's set
 // tiles in bitmap order) and the FrameReport.  Every load is issued up front.
@@ -2039,29 +2167,51 @@ __global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant
   __shared__ int sm[NF_THREADS / 32];
   __shared__ int red[2][NF_THREADS / 32];
   const int s = b.s0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nb = g.bands_per_stream * b.nms_u;   // NMS units, (layer, y) order
-  const int4* rec = reinterpret_cast<const int4*>(b.unit_rec) + (long long)s * nb;
-  int* bout = b.unit_out + (long long)s * nb;
   const int um = use_mask(g, b, s);
-  // ---- unit offsets: thread t owns units [t * per, t * per + per) ----
-  const int per = (nb + NF_THREADS - 1) / NF_THREADS;
-  int kept = 0, n_drop = 0, n_surv = 0;
-  for (int k = 0; k < per; k++) {
-    const int i = tid * per + k;
-    if (i < nb) {
-      const int4 r = __ldcg(rec + i);
-      kept += r.y;
-      n_drop += r.w;
-      n_surv += r.z + r.w;
+  int n_det, n_drop = 0, n_surv = 0;
+  if (b.desc_bin) {
+    // ---- pipeline (k_nms_test): chunk kept counts -> output offsets, in place ----
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int nch = (ctr[C_ERR] & VF_ERRBIT_STAGING) ? 0 : (ctr[C_STAGE] + NMS_CHUNK_THREADS - 1) >> NMS_CHUNK_LOG;
+    int* co = b.chunk_off + (long long)s * g.nms_chunks;
+    int carry = 0;
+    for (int c0 = 0; c0 < nch; c0 += NF_THREADS) {
+      const int i = c0 + tid;
+      const int v = i < nch ? __ldcg(co + i) : 0;
+      int tot;
+      const int ex = block_excl_scan(v, tot, sm);
+      if (i < nch) co[i] = carry + ex;
+      carry += tot;
     }
-  }
-  int n_det;
-  int run = block_excl_scan(kept, n_det, sm);
-  for (int k = 0; k < per; k++) {
-    const int i = tid * per + k;
-    if (i < nb) {
-      bout[i] = run;
-      run += __ldcg(rec + i).y;
+    n_det = carry;
+    if (tid == 0) {
+      const int n_ok = __ldcg(b.nms_cnt + 4 * s), n_dr = __ldcg(b.nms_cnt + 4 * s + 1);
+      n_drop = n_dr;
+      n_surv = n_ok + n_dr;
+    }
+  } else {
+    // ---- stand-alone (k_nms): unit offsets, thread t owns units [t * per, t * per + per) ----
+    const int nb = g.bands_per_stream * b.nms_u;   // NMS units, (layer, y) order
+    const int4* rec = reinterpret_cast<const int4*>(b.unit_rec) + (long long)s * nb;
+    int* bout = b.unit_out + (long long)s * nb;
+    const int per = (nb + NF_THREADS - 1) / NF_THREADS;
+    int kept = 0;
+    for (int k = 0; k < per; k++) {
+      const int i = tid * per + k;
+      if (i < nb) {
+        const int4 r = __ldcg(rec + i);
+        kept += r.y;
+        n_drop += r.w;
+        n_surv += r.z + r.w;
+      }
+    }
+    int run = block_excl_scan(kept, n_det, sm);
+    for (int k = 0; k < per; k++) {
+      const int i = tid * per + k;
+      if (i < nb) {
+        bout[i] = run;
+        run += __ldcg(rec + i).y;
+      }
     }
   }
   // ---- SAT tiles marked by the stream's bands (k_nms ORs footprints into
@@ -2081,21 +2231,6 @@ __global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant
       cnt += tot;
     }
     if (tid == 0) b.sat_count[s] = cnt;
-  }
-  // ---- describe regions holding small-scale keypoints -> k_desc_region's work list ----
-  if (b.desc_bin == 1) {
-    const int* rc = b.reg_cnt + (long long)s * g.nreg;
-    int* rw = b.reg_work + (long long)s * g.nreg;
-    int cnt = 0;
-    for (int r0 = 0; r0 < g.nreg; r0 += NF_THREADS) {
-      const int ri = r0 + tid;
-      const int v = ri < g.nreg && __ldcg(rc + ri) > 0;
-      int tot;
-      const int pos = cnt + block_excl_scan(v, tot, sm);
-      if (v) rw[pos] = ri;
-      cnt += tot;
-    }
-    if (tid == 0) b.ctr[s * C_NCTR + C_NREGW] = cnt;
   }
   // ---- FrameReport ----
 #pragma unroll
@@ -2291,25 +2426,6 @@ __device__ __forceinline__ void describe_warp(const Geo& g, DescWarp& w, const u
   }
 }
 
-// Kept keypoints of all streams flattened: global index -> (stream, rank)
-// through the per-stream n_detected prefix, rank -> band by binary search of
-// the band output offsets, band -> staging slot.
-// ---------------------------------------------------------------------------
-// Pipeline describe in three launches, each shaped for its work:
-//   k_desc_sample(pass 0)  warp per kept keypoint, lanes = sample points:
-//                          theta = 0 box means (2 points per lane, every SAT
-//                          corner load in flight at once) -> 60 bytes parked in
-//                          the keypoint's descriptor slot; keypoint fields out
-//   k_desc_orient          thread per keypoint: the 393-term sequential fp64
-//                          orientation sum (descriptor.py:128-144), atan2
-//   k_desc_sample(pass 1)  warp per keypoint: rotated box means, 16 ballots ->
-//                          512 MSB-first bits (descriptor.py:117-126,271-275)
-// Kept keypoints of all streams are flattened (per-stream n_detected prefix).
-// ---------------------------------------------------------------------------
-// Box mean of pattern point j of a keypoint (descriptor.py:85-115): fp64
-// position in the reference's op order, clamped box, branch-free strip-SAT
-// corners (masked corners re-read corner A and are multiplied by 0), exact
-// sum // area.
 // Corner addresses of the box of one sample point (descriptor.py:94-115):
 // fp64 position in the reference's op order, clamped box, strip-SAT corners.
 struct BoxQ {
@@ -2388,273 +2504,14 @@ __device__ __forceinline__ void point_means2(const uint32_t* S, const Geo& g, do
   mb = exact_div(sc, (uint32_t)c.area);
 }
 
-// Flattened kept-keypoint index -> (stream, rank) via the per-stream prefix.
-__device__ __forceinline__ int find_stream(const int* pre, int n_streams, int gi)
-{
-  int lo = 0, hi = n_streams;
-  while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= gi) lo = m; else hi = m; }
-  return lo;
-}
-
-#define DSW 8   // warps per CTA in the warp-per-keypoint describe kernels
-__global__ void __launch_bounds__(32 * DSW) k_desc_sample(const __grid_constant__ Geo g,
-                                                          const __grid_constant__ Bufs b, int n_streams, int pass)
-{
-  __shared__ uint8_t vals[DSW][64];
-  __shared__ uint32_t pairs[VF_NBITS];
-  __shared__ double ptab[64][3];   // pattern point x, y, smoothing radius
-  __shared__ int sm_warp[32];
-  extern __shared__ int pre[];   // [n_streams + 1]
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < VF_NBITS; k += 32 * DSW) pairs[k] = g_pairs[k];
-  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NGLOB]; });
-  const int total = pre[n_streams];
-  for (int j = threadIdx.x; j < 64; j += 32 * DSW) {
-    const int jj = j < VF_NPTS ? j : 0;
-    (void)jj;
-    ptab[j][0] = g_ptab[j][0]; ptab[j][1] = g_ptab[j][1]; ptab[j][2] = g_ptab[j][2];
-  }
-  __syncthreads();
-  // this lane's two pattern points (lane, lane + 32; lanes 28-31 repeat their first)
-  const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
-  // The warp's keypoints are gi = g0 + k * Wt.  Their headers (position,
-  // scale, rotation, output slot) are fetched 32 at a time, lane k for
-  // keypoint k, so the per-keypoint loop only waits on its SAT corners.
-  const int Wt = gridDim.x * DSW;
-  for (int g0 = blockIdx.x * DSW + wid; g0 < total; g0 += 32 * Wt) {
-    const int gl = g0 + lane * Wt;
-    long long o_l = 0;
-    int s_l = 0;
-    double kx_l = 0.0, ky_l = 0.0, sg_l = 0.0, cs_l = 1.0, sn_l = 0.0;
-    o_l = -1;
-    if (gl < total) {
-      const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
-      s_l = b.s0 + sl;
-      const int cur = b.ctr[s_l * C_NCTR + C_FRAME] & 1;
-      const long long fb = feat_base(g, s_l, cur, b.ctr[s_l * C_NCTR + C_NTOTAL]);
-      int* gl_e = b.gidx + (long long)s_l * g.kp_cap + i;
-      if (pass == 0) {
-        // list entry (unit, index in unit) -> staging slot and output rank;
-        // ranks past the (capacity-clamped) detected count are not written
-        const uint32_t e = (uint32_t)*gl_e;
-        const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
-        const long long ui = (long long)s_l * g.bands_per_stream * b.nms_u + u;
-        const long long si = (long long)s_l * g.kp_cap + __ldcg(b.unit_rec + 4 * ui) + k;   // staging slot
-        const int rank = __ldcg(b.unit_out + ui) + k;
-        const bool ok = rank < b.ctr[s_l * C_NCTR + C_NDET];
-        *gl_e = ok ? rank : -1;   // for k_desc_orient and pass 1
-        kx_l = b.st_x[si]; ky_l = b.st_y[si]; sg_l = b.st_s[si];
-        if (ok) {
-          o_l = fb + rank;
-          b.fx[o_l] = kx_l; b.fy[o_l] = ky_l; b.fs[o_l] = sg_l; b.fv[o_l] = b.st_v[si];
-          b.forg[o_l] = 0; b.fage[o_l] = 0;
-        }
-      } else {
-        const int rank = *gl_e;
-        if (rank >= 0) {
-          o_l = fb + rank;
-          kx_l = b.fx[o_l]; ky_l = b.fy[o_l]; sg_l = b.fs[o_l];
-          const double* park = reinterpret_cast<const double*>(b.fdesc + o_l * 64);   // from k_desc_orient
-          cs_l = park[0];
-          sn_l = park[1];
-        }
-      }
-    }
-    const int nk = min(32, (total - g0 + Wt - 1) / Wt);
-#pragma unroll 1
-  for (int k = 0; k < nk; k++) {
-    const long long o = __shfl_sync(0xffffffffu, o_l, k);
-    if (o < 0) continue;   // warp-uniform: a rank past the clamped count
-    const int s = __shfl_sync(0xffffffffu, s_l, k);
-    const double kx = __shfl_sync(0xffffffffu, kx_l, k), ky = __shfl_sync(0xffffffffu, ky_l, k);
-    const double sg = __shfl_sync(0xffffffffu, sg_l, k);
-    const double cs = __shfl_sync(0xffffffffu, cs_l, k), sn = __shfl_sync(0xffffffffu, sn_l, k);
-    const uint32_t* S = b.sat + (long long)s * g.W * g.H;
-    uint32_t m0, m1;
-    point_means2(S, g, kx, ky, sg, cs, sn, ptab[lane], ptab[j1], pass != 0, m0, m1);
-    uint8_t* v = vals[wid];
-    v[lane] = (uint8_t)m0;
-    if (lane + 32 < VF_NPTS) v[lane + 32] = (uint8_t)m1;
-    __syncwarp();
-    uint32_t* dst = reinterpret_cast<uint32_t*>(b.fdesc + o * 64);
-    if (pass == 0) {
-      // park the 60 theta = 0 means (+4 pad) in the descriptor slot for k_desc_orient
-      if (lane < 16) dst[lane] = reinterpret_cast<const uint32_t*>(v)[lane];
-    } else {
-      uint32_t mine = 0;
-#pragma unroll
-      for (int q = 0; q < 16; q++) {
-        const uint32_t pr = pairs[32 * q + lane];
-        const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
-        if (lane == q) mine = word;
-      }
-      if (lane < 16) dst[lane] = __byte_perm(__brev(mine), 0, 0x0123);
-    }
-    __syncwarp();
-  }
-  }
-}
-
-// Thread per keypoint: theta from the parked theta = 0 means, summed
-// sequentially in long-pair order with fp64 products (no FMA), as
-// _orientations_jit; theta <= -pi maps to pi (descriptor.py:142-143).
-#define DO_THREADS 128
-__global__ void __launch_bounds__(DO_THREADS) k_desc_orient(const __grid_constant__ Geo g,
-                                                            const __grid_constant__ Bufs b, int n_streams)
-{
-  __shared__ __align__(16) uint8_t vv[DO_THREADS * DW_ROW];
-  __shared__ int sm_warp[32];
-  extern __shared__ int pre[];
-  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NGLOB]; });
-  const int total = pre[n_streams];
-  uint8_t* v = vv + threadIdx.x * DW_ROW;
-  for (int base = blockIdx.x * DO_THREADS; base < total; base += gridDim.x * DO_THREADS) {
-    const int gi = base + threadIdx.x;
-    long long o = -1;
-    const int sl = gi < total ? find_stream(pre, n_streams, gi) : 0, s = b.s0 + sl;
-    const int rank = gi < total ? __ldcg(b.gidx + (long long)s * g.kp_cap + gi - pre[sl]) : -1;
-    if (rank >= 0) {
-      o = feat_base(g, s, b.ctr[s * C_NCTR + C_FRAME] & 1, b.ctr[s * C_NCTR + C_NTOTAL]) + rank;
-      const uint4* src = reinterpret_cast<const uint4*>(b.fdesc + o * 64);
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint4 w4 = src[q];
-        uint32_t* d = reinterpret_cast<uint32_t*>(v + 16 * q);
-        d[0] = w4.x; d[1] = w4.y; d[2] = w4.z; d[3] = w4.w;
-      }
-      // exact int -> double without I2F: (2^52 + 2^51 + 2^31 + n) - (2^52 + 2^51 + 2^31)
-      auto i2d = [](int n) {
-        return __hiloint2double(0x43380000, (int)(0x80000000u + (unsigned)n)) - 6755401588539392.0;
-      };
-      double gx = 0.0, gy = 0.0;
-      const int L = c_nlong;
-      int p = 0;
-#pragma unroll 1
-      for (; p + 4 <= L; p += 4) {
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          const double dv = i2d((int)v[c_li[p + k]] - (int)v[c_lj[p + k]]);
-          gx += dv * c_wx[p + k];
-          gy += dv * c_wy[p + k];
-        }
-      }
-      for (; p < L; p++) {
-        const double dv = i2d((int)v[c_li[p]] - (int)v[c_lj[p]]);
-        gx += dv * c_wx[p];
-        gy += dv * c_wy[p];
-      }
-      double th = atan2(gy, gx);
-      th = th <= -CUDART_PI ? CUDART_PI : th;
-      b.ft[o] = th;
-      // park cos / sin for the rotated pass in the (consumed) descriptor slot
-      double sn, cs;
-      sincos(th, &sn, &cs);
-      double* park = reinterpret_cast<double*>(b.fdesc + o * 64);
-      park[0] = cs;
-      park[1] = sn;
-    }
-  }
-}
+#define DSW 8   // warps per CTA of k_desc_fused
 
 // ============================================================================
-// k_desc_region: orientation + descriptor of the small-scale keypoints of one
-// describe region per CTA (descriptor.py:28-32,85-144,271-275), from a uint16
-// SAT of the region's footprint box built in shared memory from the frame.
-//   * every box of these keypoints is <= 15 x 15, so its sum is < 2^16 and
-//     the modular uint16 SAT gives it exactly;
-//   * the SAT is built by 8 warps over row blocks (lane = 4-pixel word: dp4a
-//     word prefixes, a warp scan per row, the block's column sums in
-//     registers; 4 rows of loads in flight), then each block adds the column
-//     totals of the blocks above;
-//   * then warp per keypoint, no further barriers: theta = 0 box means, the
-//     orientation sum (dr_orient), rotated means and the 16 ballots of the
-//     512 bits.
-// Region counts are zeroed here for the next step.
+// Orientation helpers of k_desc_fused
 // ============================================================================
-#define DR_THREADS 256
-#define DR_WARPS (DR_THREADS / 32)
-#define DR_SAT_MAX 24064         // (DR_RH - 1 + 2 DR_FMAX + 2) rows x (176 + 2) columns of uint16
-#define DR_CITEMS 5              // fix-up items per thread: 176 columns x 7 row blocks / 256 threads
-#define DR_PF 4                  // frame rows of loads in flight per warp while building the SAT
-
-struct DrShared {
-  uint16_t T[DR_SAT_MAX];
-  uint8_t v[DR_WARPS][DW_ROW];
-  int red[4][DR_WARPS];
-};
-
-// Box mean of one sample point from the region SAT T (pitch P entries): entry
-// (r, c) = sum over rows ylo .. ylo + r - 1 and columns ax0 .. ax0 + c - 2.
-// *dist receives the distance of the unrounded sample position to the nearest
-// integer (x or y, whichever is closer): how far theta may move before floor()
-// changes.
-__device__ __forceinline__ uint32_t dr_mean(const uint16_t* T, int P, int ax0, int ylo, int W, int H, double kx,
-                                            double ky, double sg, double cs, double sn, double px, double py,
-                                            double rad, bool rot, double* dist)
-{
-  double fx, fy;
-  if (rot) {
-    fx = kx + sg * (cs * px - sn * py) + 0.5;
-    fy = ky + sg * (sn * px + cs * py) + 0.5;
-  } else {
-    fx = kx + sg * px + 0.5;
-    fy = ky + sg * py + 0.5;
-  }
-  if (dist) *dist = fmin(fabs(fx - rint(fx)), fabs(fy - rint(fy)));
-  const int x = min(max(__double2int_rd(fx), 0), W - 1);
-  const int y = min(max(__double2int_rd(fy), 0), H - 1);
-  const int r = __double2int_rd(rad * sg + 0.5);
-  const int x0 = max(x - r, 0), x1 = min(x + r, W - 1), y0 = max(y - r, 0), y1 = min(y + r, H - 1);
-  const int c0 = x0 - ax0 + 1, c1 = x1 - ax0 + 2;          // columns of x0 - 1 and x1
-  const int r0 = (y0 - ylo) * P, r1 = (y1 - ylo + 1) * P;  // rows of y0 - 1 and y1
-  const uint32_t sm = ((uint32_t)T[r1 + c1] - (uint32_t)T[r0 + c1] - (uint32_t)T[r1 + c0] + (uint32_t)T[r0 + c0]) &
-                      0xffffu;
-  return exact_div(sm, (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1)));
-}
-
 __device__ __forceinline__ double dr_i2d(int n)   // exact int -> double without I2F
 {
   return __hiloint2double(0x43380000, (int)(0x80000000u + (unsigned)n)) - 6755401588539392.0;
-}
-
-// The reference orientation (descriptor.py:132-144): gx, gy = sequential fp64
-// sums of dv_p * w_p in long-pair order, theta = atan2(gy, gx).  Here the warp
-// sums the same rounded products lane-strided + butterfly (every lane ends
-// with the identical value).  Both orders are within (n - 1 + 5) u sum|t| of
-// the exact sum (recursive / pairwise summation bounds), so |theta_warp -
-// theta_seq| <= dth.  Returns false -- the caller then uses dr_orient_seq --
-// when that bound is not small against |g| or theta may sit on the -pi / pi
-// branch cut.  The caller also falls back when a rotated sample position lies
-// within the induced position error of an integer, so floor() -- and every
-// descriptor bit -- is the one the sequential theta gives.
-__device__ __forceinline__ bool dr_orient_warp(const uint8_t* v, int lane, double& th, double& dth)
-{
-  double sx = 0.0, sy = 0.0, ax = 0.0, ay = 0.0;
-  const int L = c_nlong;
-  for (int p = lane; p < L; p += 32) {
-    const uint32_t pr = __ldg(g_lpair + p);
-    const double2 w = __ldg(g_lw + p);
-    const double dv = dr_i2d((int)v[pr & 0xffffu] - (int)v[pr >> 16]);
-    const double tx = dv * w.x, ty = dv * w.y;
-    sx += tx; sy += ty;
-    ax += fabs(tx); ay += fabs(ty);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sx += __shfl_xor_sync(0xffffffffu, sx, o);
-    sy += __shfl_xor_sync(0xffffffffu, sy, o);
-    ax += __shfl_xor_sync(0xffffffffu, ax, o);
-    ay += __shfl_xor_sync(0xffffffffu, ay, o);
-  }
-  const double gam = (double)(L + 8) * 1.1102230246251565e-16 * 1.01;
-  const double bx = 2.0 * gam * ax, by = 2.0 * gam * ay;   // |warp sum - sequential sum| per component
-  const double gn = sqrt(sx * sx + sy * sy);
-  if (!(bx + by < 1e-3 * gn)) return false;                // includes g == 0
-  if (sx < 0.0 && fabs(sy) <= by) return false;            // theta near the +-pi cut
-  dth = 2.0 * (bx + by) / gn + 1e-15;
-  th = atan2(sy, sx);
-  th = th <= -CUDART_PI ? CUDART_PI : th;
-  return true;
 }
 
 // Orientation from the lane's two box means m0 (point lane) and m1 (point
@@ -2711,240 +2568,14 @@ __device__ __noinline__ void dr_orient_seq_g(const uint8_t* v, double& gx_out, d
   gy_out = gy;
 }
 
-// The reference order itself (one lane): the rare fallback of dr_orient_warp.
-__device__ __noinline__ double dr_orient_seq(const uint8_t* v)
-{
-  double gx = 0.0, gy = 0.0;
-  const int L = c_nlong;
-  for (int p = 0; p < L; p++) {
-    const double dv = dr_i2d((int)v[c_li[p]] - (int)v[c_lj[p]]);
-    gx += dv * c_wx[p];
-    gy += dv * c_wy[p];
-  }
-  const double th = atan2(gy, gx);
-  return th <= -CUDART_PI ? CUDART_PI : th;
-}
-
-__global__ void __launch_bounds__(DR_THREADS, 4) k_desc_region(const __grid_constant__ Geo g,
-                                                               const __grid_constant__ Bufs b, int n_streams)
-{
-  extern __shared__ __align__(16) uint8_t dsm[];
-  DrShared& sh = *reinterpret_cast<DrShared*>(dsm);
-  int* pre = reinterpret_cast<int*>(dsm + sizeof(DrShared));
-  __shared__ int sm_warp[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  stream_prefix(n_streams, pre, sm_warp, [&](int sl) { return b.ctr[(b.s0 + sl) * C_NCTR + C_NREGW]; });
-  const int total = pre[n_streams];
-  const int NU = g.bands_per_stream * b.nms_u;
-  const bool vec = (((uintptr_t)b.frames | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) & 3) == 0;
-  // this lane's two pattern points (lane, lane + 32)
-  const int j1 = lane + 32 < VF_NPTS ? lane + 32 : lane;
-  const bool has1 = lane + 32 < VF_NPTS;
-  const double p0x = __ldg(&g_ptab[lane][0]), p0y = __ldg(&g_ptab[lane][1]), p0r = __ldg(&g_ptab[lane][2]);
-  const double p1x = __ldg(&g_ptab[j1][0]), p1y = __ldg(&g_ptab[j1][1]), p1r = __ldg(&g_ptab[j1][2]);
-  // |p| of the two points: a centre point's position does not depend on theta
-  const double pn0 = sqrt(p0x * p0x + p0y * p0y), pn1 = has1 ? sqrt(p1x * p1x + p1y * p1y) : 0.0;
-  uint8_t* v = sh.v[wid];
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int sl = find_stream(pre, n_streams, item), s = b.s0 + sl;
-    const long long rslot = (long long)s * g.nreg + __ldcg(b.reg_work + (long long)s * g.nreg + item - pre[sl]);
-    const int* ctr = b.ctr + s * C_NCTR;
-    const int cnt = min(__ldcg(b.reg_cnt + rslot), DR_RCAP);
-    const int ndesc = ctr[C_NDET];
-    const long long fb = feat_base(g, s, ctr[C_FRAME] & 1, ctr[C_NTOTAL]);
-    const uint32_t* list = b.reg_list + rslot * DR_RCAP;
-    const int* urec = b.unit_rec + 4LL * s * NU;
-    const int* uout = b.unit_out + (long long)s * NU;
-    const long long sbase = (long long)s * g.kp_cap;
-    // ---- footprint box of the region's keypoints ----
-    int xlo = 1 << 30, ylo = 1 << 30, xhi = -1, yhi = -1;
-    for (int i = tid; i < cnt; i += DR_THREADS) {
-      const uint32_t e = __ldcg(list + i);
-      const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
-      const long long slot = sbase + __ldcg(urec + 4 * u) + k;
-      int rmax;
-      const int reach = desc_reach(__ldcg(b.st_s + slot), rmax);
-      const int xi = (int)__ldcg(b.st_x + slot), yi = (int)__ldcg(b.st_y + slot);
-      xlo = min(xlo, xi - reach); xhi = max(xhi, xi + reach);
-      ylo = min(ylo, yi - reach); yhi = max(yhi, yi + reach);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      xlo = min(xlo, __shfl_xor_sync(0xffffffffu, xlo, o)); xhi = max(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
-      ylo = min(ylo, __shfl_xor_sync(0xffffffffu, ylo, o)); yhi = max(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
-    }
-    if (lane == 0) { sh.red[0][wid] = xlo; sh.red[1][wid] = xhi; sh.red[2][wid] = ylo; sh.red[3][wid] = yhi; }
-    __syncthreads();
-    if (tid == 0) b.reg_cnt[rslot] = 0;   // every thread has read cnt
-#pragma unroll
-    for (int w = 0; w < DR_WARPS; w++) {
-      xlo = min(xlo, sh.red[0][w]); xhi = max(xhi, sh.red[1][w]);
-      ylo = min(ylo, sh.red[2][w]); yhi = max(yhi, sh.red[3][w]);
-    }
-    xlo = max(xlo, 0); xhi = min(xhi, g.W - 1);
-    ylo = max(ylo, 0); yhi = min(yhi, g.H - 1);
-    const int ax0 = xlo & ~3, nwd = (xhi - ax0 + 4) >> 2, wc = 4 * nwd, P = wc + 2, hb = yhi - ylo + 1;
-    // ---- SAT, phase 1: row prefixes + column sums within 8 row blocks ----
-    const int RB = (hb + DR_WARPS - 1) / DR_WARPS;
-    for (int i = tid; i < P / 2; i += DR_THREADS) reinterpret_cast<uint32_t*>(sh.T)[i] = 0u;   // row ylo - 1
-    {
-      const int ra = 1 + wid * RB, rb = min(hb, (wid + 1) * RB);
-      uint32_t acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; q++) acc[q] = 0u;
-      const uint8_t* fr = b.frames + (long long)(s - b.s0) * b.frame_stride + ax0;
-      const bool two = nwd > 32;
-      for (int r0 = ra; r0 <= rb; r0 += DR_PF) {
-        uint32_t wv[DR_PF][2];
-#pragma unroll
-        for (int q = 0; q < DR_PF; q++) {
-          const uint8_t* row = fr + (long long)(ylo + r0 + q - 1) * b.frame_pitch;
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int j = lane + 32 * h, x = ax0 + 4 * j;
-            uint32_t w = 0u;
-            if (r0 + q <= rb && j < nwd) {
-              if (vec && x + 3 < g.W) w = __ldg(reinterpret_cast<const uint32_t*>(row + 4 * j));
-              else
-                for (int c = 0; c < 4; c++)
-                  if (x + c < g.W) w |= (uint32_t)__ldg(row + 4 * j + c) << (8 * c);
-            }
-            wv[q][h] = w;
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < DR_PF; q++) {
-          const int r = r0 + q;
-          if (r > rb) break;
-          uint32_t* trow = reinterpret_cast<uint32_t*>(sh.T + r * P);
-          if (lane == 0) trow[0] = 0u;   // column ax0 - 1
-          uint32_t carry = 0u;
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            if (h == 1 && !two) break;
-            const int j = lane + 32 * h;
-            const uint32_t w = wv[q][h];
-            const uint32_t q0 = w & 0xffu, q1 = __dp4a(w, 0x00000101u, 0u), q2 = __dp4a(w, 0x00010101u, 0u),
-                           q3 = __dp4a(w, 0x01010101u, 0u);
-            uint32_t inc = q3;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-              if (lane >= o) inc += t;
-            }
-            const uint32_t ex = carry + inc - q3;
-            carry += __shfl_sync(0xffffffffu, inc, 31);
-            acc[4 * h + 0] += ex + q0; acc[4 * h + 1] += ex + q1;
-            acc[4 * h + 2] += ex + q2; acc[4 * h + 3] += ex + q3;
-            if (j < nwd) {
-              trow[1 + 2 * j] = __byte_perm(acc[4 * h + 0], acc[4 * h + 1], 0x5410);
-              trow[2 + 2 * j] = __byte_perm(acc[4 * h + 2], acc[4 * h + 3], 0x5410);
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ---- phase 2: rows of block k += column totals of blocks 0 .. k - 1 ----
-    {
-      const int nfix = wc * (DR_WARPS - 1);
-      uint32_t off[DR_CITEMS];
-#pragma unroll
-      for (int q = 0; q < DR_CITEMS; q++) {
-        const int it = tid + q * DR_THREADS;
-        uint32_t o = 0u;
-        if (it < nfix) {
-          const int bk = 1 + it / wc, c = 2 + it % wc;
-          for (int k = 0; k < bk; k++) {
-            const int rl = min(hb, (k + 1) * RB);
-            if (rl >= 1 + k * RB) o += sh.T[rl * P + c];
-          }
-        }
-        off[q] = o;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < DR_CITEMS; q++) {
-        const int it = tid + q * DR_THREADS;
-        if (it < nfix && (off[q] & 0xffffu)) {
-          const int bk = 1 + it / wc, c = 2 + it % wc;
-          const int ra = 1 + bk * RB, rb = min(hb, (bk + 1) * RB);
-          for (int r = ra; r <= rb; r++) sh.T[r * P + c] = (uint16_t)(sh.T[r * P + c] + off[q]);
-        }
-      }
-    }
-    __syncthreads();
-    // ---- warp per keypoint ----
-    for (int i = wid; i < cnt; i += DR_WARPS) {
-      const uint32_t e = __ldcg(list + i);
-      const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
-      const int rank = __ldcg(uout + u) + k;
-      if (rank >= ndesc) continue;   // capacity clamp (warp-uniform)
-      const long long slot = sbase + __ldcg(urec + 4 * u) + k;
-      const double kx = __ldcg(b.st_x + slot), ky = __ldcg(b.st_y + slot), sg = __ldcg(b.st_s + slot);
-      const long long o = fb + rank;
-      if (lane == 0) {
-        b.fx[o] = kx; b.fy[o] = ky; b.fs[o] = sg; b.fv[o] = __ldcg(b.st_v + slot);
-        b.forg[o] = 0; b.fage[o] = 0;
-      }
-      // theta = 0 box means (descriptor.py:128-131)
-      const uint32_t a0 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, 1.0, 0.0, p0x, p0y, p0r, false, nullptr);
-      const uint32_t a1 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, 1.0, 0.0, p1x, p1y, p1r, false, nullptr);
-      v[lane] = (uint8_t)a0;
-      if (has1) v[lane + 32] = (uint8_t)a1;
-      __syncwarp();
-      double th = 0.0, dth = 0.0;
-      bool ok = dr_orient_warp(v, lane, th, dth);
-      double cs = 0.0, sn = 0.0;
-      uint32_t m0 = 0u, m1 = 0u;
-      if (ok) {
-        sincos(th, &sn, &cs);
-        // rotated means; keep them only if no sample position is within the
-        // theta bound's reach of an integer
-        const double ue = 1.5 * sg * (dth + 4e-16);
-        double d0, d1;
-        m0 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p0x, p0y, p0r, true, &d0);
-        m1 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p1x, p1y, p1r, true, &d1);
-        const bool near0 = pn0 > 0.0 && d0 < ue * pn0 + 4e-12;
-        const bool near1 = has1 && pn1 > 0.0 && d1 < ue * pn1 + 4e-12;
-        ok = !__any_sync(0xffffffffu, near0 || near1);
-      }
-      if (!ok) {   // rare: the reference's sequential sum
-        double t = 0.0;
-        if (lane == 0) t = dr_orient_seq(v);
-        th = __shfl_sync(0xffffffffu, t, 0);
-        sincos(th, &sn, &cs);
-        m0 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p0x, p0y, p0r, true, nullptr);
-        m1 = dr_mean(sh.T, P, ax0, ylo, g.W, g.H, kx, ky, sg, cs, sn, p1x, p1y, p1r, true, nullptr);
-      }
-      if (lane == 0) b.ft[o] = th;
-      __syncwarp();
-      v[lane] = (uint8_t)m0;
-      if (has1) v[lane + 32] = (uint8_t)m1;
-      __syncwarp();
-      // 512 bits, MSB-first (descriptor.py:117-126,271-275)
-      uint32_t mine = 0u;
-#pragma unroll
-      for (int q = 0; q < 16; q++) {
-        const uint32_t pr = __ldg(g_pairs + 32 * q + lane);   // si | sj << 16
-        const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
-        if (lane == q) mine = word;
-      }
-      if (lane < 16) reinterpret_cast<uint32_t*>(b.fdesc + o * 64)[lane] = __byte_perm(__brev(mine), 0, 0x0123);
-      __syncwarp();
-    }
-    __syncthreads();
-  }
-}
-
 // ============================================================================
 // k_desc_fused: the strip-SAT describe of one keypoint per warp in a single
 // pass (descriptor.py:85-144,271-275): theta = 0 box means -> orientation
 // (dr_orient_warp, certified against the sequential sum; dr_orient_seq when
 // the certificate fails) -> rotated box means -> 16 ballots.  The rotated
 // samples cover the same disk as the theta = 0 ones, so their SAT corners are
-// mostly L1 hits of the first pass.  Keypoints: the k_nms list b.gidx
-// (unit << 18 | index in unit) of the streams [s0, s0 + n).
+// mostly L1 hits of the first pass.  Keypoints: the describe list b.gidx
+// (candidate indices, from k_nms_test) of the streams [s0, s0 + n).
 // ============================================================================
 __global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constant__ Geo g,
                                                          const __grid_constant__ Bufs b, int n_streams)
@@ -2982,11 +2613,12 @@ __global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constan
       const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
       s_l = b.s0 + sl;
       const int* ctr = b.ctr + s_l * C_NCTR;
-      const uint32_t e = (uint32_t)__ldcg(b.gidx + (long long)s_l * g.kp_cap + i);
-      const int u = (int)(e >> DR_UNIT_SHIFT), k = (int)(e & ((1u << DR_UNIT_SHIFT) - 1u));
-      const long long ui = (long long)s_l * g.bands_per_stream * b.nms_u + u;
-      const long long si = (long long)s_l * g.kp_cap + __ldcg(b.unit_rec + 4 * ui) + k;   // staging slot
-      const int rank = __ldcg(b.unit_out + ui) + k;
+      // describe-list entry = candidate index c (staging slot); output rank =
+      // kept keypoints of the earlier candidate chunks + rank within the chunk
+      const int c = __ldcg(b.gidx + (long long)s_l * g.kp_cap + i);
+      const long long si = (long long)s_l * g.kp_cap + c;
+      const int rank = __ldcg(b.chunk_off + (long long)s_l * g.nms_chunks + (c >> NMS_CHUNK_LOG)) +
+                       __ldcg(b.cand_rank + si);
       kx_l = __ldcg(b.st_x + si); ky_l = __ldcg(b.st_y + si); sg_l = __ldcg(b.st_s + si);
       if (rank < ctr[C_NDET]) {   // ranks past the capacity-clamped count are not written
         o_l = feat_base(g, s_l, ctr[C_FRAME] & 1, ctr[C_NTOTAL]) + rank;
