@@ -236,17 +236,6 @@ int pyramid_smem(const Geo& g)
 
 int g_num_sms = 0;
 
-// NMS units per band for a batch of n streams: one warp per band (8 rows) when
-// the batch has enough bands to fill every SM many times over, else split
-// bands into 1-4-row units so single-stream frames get more warps.
-int nms_units(const Geo& g, int n)
-{
-  const long long bands = (long long)g.bands_per_stream * n, want = 32LL * (g_num_sms > 0 ? g_num_sms : 148);
-  int u = 1;
-  while (u < VF_TILE_H && bands * u < want) u *= 2;
-  return u;
-}
-
 int cuda_status(cudaError_t e)
 {
   if (e == cudaSuccess) return VF_OK;
