@@ -757,8 +757,11 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
       g, b, 0, cov_ctas, carry_ctas); DBG_SYNC(c->aux[gi], "k_worklist");
   cudaEventRecord(c->aux_mid[gi], c->aux[gi]);
   // Eq. 1 propagation into the last n_prop slots of the list: independent of
-  // the detection, so it runs beside k_fast / k_nms
-  if (prop) {
+  // the detection, so it runs beside k_fast / k_nms (VF_PROP_LATE=1: beside
+  // the describe kernels instead)
+  const bool prop_late = getenv("VF_PROP_LATE") && atoi(getenv("VF_PROP_LATE")) != 0;
+  auto launch_prop = [&]() {
+    if (!prop) return;
     cudaEvent_t p0 = nullptr, p1 = nullptr;
     if (c->timing) {
       p0 = pool_event(c);
@@ -772,13 +775,15 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
       c->side_ev.push_back(p1);
       c->side_stage.push_back(7);
     }
+  };
+  if (!prop_late) {
+    launch_prop();
+    cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   }
-  cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_fast");
   stage_mark(c, 4, st);
-  cudaStreamWaitEvent(st, c->aux_mid[gi], 0);
   // candidate-parallel NMS: ordered candidate list, thread-per-candidate test +
   // refinement with chunk ranks, chunk offsets + FrameReport
   b.nms_u = 1;
@@ -786,7 +791,14 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   b.orient_seq = getenv("VF_ORIENT_SEQ") && atoi(getenv("VF_ORIENT_SEQ")) != 0;
   k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
   k_nms_test<<<c->nmst_grid, 1 << NMS_CHUNK_LOG, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_nms_test");
+  cudaStreamWaitEvent(st, c->aux_mid[gi], 0);   // propagation count (k_nms_finish), strip carries (k_sat)
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
+  if (prop_late) {
+    cudaEventRecord(c->aux_in[gi], st);
+    cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
+    launch_prop();
+    cudaEventRecord(c->aux_out[gi], c->aux[gi]);
+  }
   stage_mark(c, 5, st);
   // Describe (descriptor.py:85-144): the strip SATs of the tiles k_nms_test
   // marked, then k_desc_fused (warp per keypoint: theta = 0 means,

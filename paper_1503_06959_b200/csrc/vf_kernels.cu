@@ -1144,7 +1144,9 @@ __global__ void __launch_bounds__(1024) k_binmask(const __grid_constant__ Geo g,
 // Extra CTAs compute the union coverage in per_layer mode.
 // ============================================================================
 #define PROP_CHUNK 1024
+#ifndef PROP_CTAS
 #define PROP_CTAS 16
+#endif
 #define VF_CLEAR (1 << 30)   // work-list flag: zero the tile's scores and bitmap words
 __global__ void __launch_bounds__(256) k_worklist(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
                                                    int tile_ctas, int cov_ctas, int carry_ctas)
