@@ -331,10 +331,13 @@ struct vf_ctx {
   int graphs = 1;                       // vf_set_graphs
 #endif
   cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t graph = nullptr;          // kept alive: its kernel nodes own the captured argument storage
+  std::vector<cudaGraphNode_t> gnodes;  // kernel nodes of the step graph (Bufs is argument 1 of each)
+  std::vector<Bufs> gbufs;              // their captured Bufs (frames re-pointed per step)
+  const uint8_t* g_frames = nullptr;    // frames / stride of the capture
+  long long g_stride = 0;
   int g_n = 0;
   int eager_n = 0;                      // batch size of the last eager step (streams / events exist)
-  uint8_t* gin = nullptr;
-  long long gin_bytes = 0;
   bool capturing = false;
   cudaStream_t cap = nullptr;           // capture stream
 };
@@ -580,6 +583,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
 
 static void pipe_free(vf_ctx* c);
 
+static void graph_drop(vf_ctx* c);
 int vf_destroy(vf_ctx* c)
 {
   if (!c) return VF_OK;
@@ -589,8 +593,7 @@ int vf_destroy(vf_ctx* c)
   }
   pipe_free(c);
   pack_free(c);
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
-  if (c->gin) cudaFree(c->gin);
+  graph_drop(c);
   if (c->cap) cudaStreamDestroy(c->cap);
   for (size_t k = 0; k < c->gstreams.size(); k++) { cudaStreamDestroy(c->gstreams[k]); cudaEventDestroy(c->gjoin[k]); }
   for (size_t k = 0; k < c->aux.size(); k++) {
@@ -679,7 +682,7 @@ int vf_set_history(vf_ctx* c, double* hist_dev, int32_t max_frames)
   if (!c || max_frames < 0 || (max_frames > 0 && !hist_dev)) return VF_ERR_ARG;
   c->b.hist = max_frames > 0 ? hist_dev : nullptr;
   c->b.hist_frames = max_frames;
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }   // the graph bakes in the pointers
+  graph_drop(c);   // the graph bakes in the pointers
   return VF_OK;
 }
 
@@ -988,31 +991,44 @@ int vf_block_match(const uint8_t* prev_dev, const uint8_t* cur_dev, int w, int h
   return cuda_status(e);
 }
 
-// Batches of at most this many frame bytes replay a captured CUDA graph of
-// the step: the launch sequence is latency-bound there (single 640x480 ..
-// 3840x2160 streams), and one copy of the inputs into the graph's fixed
-// input buffer is cheaper than ~20 host launches.
-#define VF_GRAPH_MAX_BYTES (12LL << 20)
+// Every step replays a CUDA graph of the launch sequence, captured once per
+// batch size: the path is a chain of ~12 dependent, individually latency-bound
+// kernels (plus the side / describe streams), and a graph launch removes the
+// per-launch host work and most of the inter-kernel gaps.  The caller's frame
+// pointer changes every step: each kernel node's Bufs argument is re-pointed
+// with cudaGraphExecKernelNodeSetParams (streams of a describe half keep their
+// offset), so no input copy is needed.
+// Argument count of each kernel launch_step launches (all take (Geo, Bufs, ...)).
+static int step_kernel_arity(const void* f)
+{
+  if (f == (const void*)k_worklist) return 5;
+  if (f == (const void*)k_sat) return 4;
+  if (f == (const void*)k_fast || f == (const void*)k_nms_test || f == (const void*)k_desc_fused ||
+      f == (const void*)k_finalize)
+    return 3;
+  if (f == (const void*)k_binmask || f == (const void*)k_pyr_o || f == (const void*)k_pyr_i ||
+      f == (const void*)k_pyramid4<PYR_FULL> || f == (const void*)k_pyramid || f == (const void*)k_propagate ||
+      f == (const void*)k_nms_list || f == (const void*)k_nms_finish)
+    return 2;
+  return 0;
+}
+
+static void graph_drop(vf_ctx* c)
+{
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  c->gexec = nullptr;
+  c->graph = nullptr;
+  c->gnodes.clear();
+  c->gbufs.clear();
+}
 
 static int graph_step(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int64_t row_pitch, int n,
                       cudaStream_t st)
 {
-  const long long fb = (long long)c->g.W * c->g.H;
-  if (c->gin_bytes < fb * n) {
-    if (c->gin) cudaFree(c->gin);
-    c->gin = nullptr;
-    if (cudaMalloc(&c->gin, fb * n) != cudaSuccess) return VF_ERR_CUDA;
-    c->gin_bytes = fb * n;
-    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
-  }
-  cudaError_t e = cudaMemcpy2DAsync(c->gin, c->g.W, frames_dev, row_pitch, c->g.W, (size_t)c->g.H * 1, cudaMemcpyDeviceToDevice, st);
-  for (int s = 1; s < n && e == cudaSuccess; s++)
-    e = cudaMemcpy2DAsync(c->gin + s * fb, c->g.W, frames_dev + s * stream_stride, row_pitch, c->g.W, c->g.H,
-                          cudaMemcpyDeviceToDevice, st);
-  if (e != cudaSuccess) return cuda_status(e);
-  c->b.frames = c->gin;
-  c->b.frame_stride = fb;
-  c->b.frame_pitch = c->g.W;
+  c->b.frames = frames_dev;
+  c->b.frame_stride = stream_stride;
+  c->b.frame_pitch = row_pitch;
   if ((!c->gexec || c->g_n != n) && c->eager_n != n) {
     // the first step of a batch size runs eagerly: it creates the side streams
     // and events the capture then records into
@@ -1020,10 +1036,11 @@ static int graph_step(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_strid
     c->eager_n = n;
     return rc;
   }
+  cudaError_t e = cudaSuccess;
   if (!c->gexec || c->g_n != n) {
     // capture on an internal non-blocking stream (the caller's may be the
     // legacy default stream, which cannot be captured); replay on the caller's
-    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+    graph_drop(c);
     if (!c->cap && cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess) return VF_ERR_CUDA;
     cudaGraph_t graph = nullptr;
     e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
@@ -1034,10 +1051,47 @@ static int graph_step(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_strid
     e = cudaStreamEndCapture(c->cap, &graph);
     if (rc != VF_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (e != cudaSuccess) return cuda_status(e);
-    e = cudaGraphInstantiate(&c->gexec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) { c->gexec = nullptr; return cuda_status(e); }
+    size_t nn = 0;
+    e = cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (e == cudaSuccess && nn) e = cudaGraphGetNodes(graph, nodes.data(), &nn);
+    for (size_t i = 0; i < nn && e == cudaSuccess; i++) {
+      cudaGraphNodeType t;
+      e = cudaGraphNodeGetType(nodes[i], &t);
+      if (e != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp;
+      e = cudaGraphKernelNodeGetParams(nodes[i], &kp);
+      if (e != cudaSuccess) break;
+      c->gnodes.push_back(nodes[i]);
+      c->gbufs.push_back(*reinterpret_cast<const Bufs*>(kp.kernelParams[1]));
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->gexec, graph, 0);
+    if (e != cudaSuccess) { cudaGraphDestroy(graph); c->gexec = nullptr; graph_drop(c); return cuda_status(e); }
+    c->graph = graph;
     c->g_n = n;
+    c->g_frames = frames_dev;
+    c->g_stride = stream_stride;
+  } else if (frames_dev != c->g_frames || stream_stride != c->g_stride || row_pitch != c->gbufs[0].frame_pitch) {
+    for (size_t i = 0; i < c->gnodes.size() && e == cudaSuccess; i++) {
+      cudaKernelNodeParams kp;
+      e = cudaGraphKernelNodeGetParams(c->gnodes[i], &kp);
+      if (e != cudaSuccess) break;
+      Bufs& nb = c->gbufs[i];
+      const long long half = c->g_stride ? (long long)(nb.frames - c->g_frames) / c->g_stride : 0;   // describe half offset
+      nb.frames = frames_dev + half * stream_stride;
+      nb.frame_stride = stream_stride;
+      nb.frame_pitch = row_pitch;
+      const int na = step_kernel_arity(kp.func);
+      if (na < 2) return VF_ERR_CUDA;   // not a kernel of launch_step
+      void* args[8];
+      for (int a = 0; a < na; a++) args[a] = kp.kernelParams[a];
+      args[1] = &nb;
+      kp.kernelParams = args;
+      e = cudaGraphExecKernelNodeSetParams(c->gexec, c->gnodes[i], &kp);
+    }
+    if (e != cudaSuccess) return cuda_status(e);
+    c->g_frames = frames_dev;
+    c->g_stride = stream_stride;
   }
   e = cudaGraphLaunch(c->gexec, st);
   if (e != cudaSuccess) return cuda_status(e);
@@ -1049,7 +1103,7 @@ int vf_set_graphs(vf_ctx* c, int enable)
 {
   if (!c) return VF_ERR_ARG;
   c->graphs = enable;
-  if (!enable && c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  if (!enable) graph_drop(c);
   return VF_OK;
 }
 
@@ -1059,8 +1113,7 @@ int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int6
   if (!c || !frames_dev || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
   if (!g_pattern_ok) return VF_ERR_PATTERN;
   static const bool env_off = getenv("VF_GRAPHS") && atoi(getenv("VF_GRAPHS")) == 0;
-  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3 &&
-      (long long)c->g.W * c->g.H * n_streams <= VF_GRAPH_MAX_BYTES)
+  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3)
     return graph_step(c, frames_dev, stream_stride, row_pitch, n_streams, (cudaStream_t)stream);
   c->b.frames = frames_dev;
   c->b.frame_stride = stream_stride;
@@ -1132,7 +1185,7 @@ static int regrow(vf_ctx* c, long long new_cap, cudaStream_t st)
   g.kp_cap = (int)new_cap;
   g.prop_chunks = chunks;
   g.nms_chunks = cdiv(new_cap, 1 << NMS_CHUNK_LOG);
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  graph_drop(c);
   pipe_free(c);   // re-created with the new capacity on the next submit
   return VF_OK;
 }
@@ -1488,7 +1541,7 @@ int vf_pipeline_set_delta(vf_ctx* c, int enable)
     c->b.keep_bits = kb;
     c->b.keep_words = kw;
     pipe_free(c);                                   // re-created with keep-mask buffers
-    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+    graph_drop(c);
   }
   c->pipe.delta = on;
   return VF_OK;
