@@ -514,6 +514,7 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.cand_rank = A.get<int>((size_t)S * cap);
   b.chunk_off = A.get<int>((size_t)S * g.nms_chunks);
   b.nms_cnt = A.get<int>((size_t)S * 4);
+  b.band_off = A.get<int>((size_t)S * (g.bands_per_stream + 1));
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -792,7 +793,13 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   b.nms_u = 1;
   b.desc_bin = 1;
   b.orient_seq = getenv("VF_ORIENT_SEQ") && atoi(getenv("VF_ORIENT_SEQ")) != 0;
-  k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
+  static const bool nms_scan = getenv("VF_NMS_SCAN") && atoi(getenv("VF_NMS_SCAN")) != 0;
+  if (nms_scan) {
+    k_band_scan<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_band_scan");
+    k_nms_list_scanned<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list_scanned");
+  } else {
+    k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
+  }
   k_nms_test<<<c->nmst_grid, 1 << NMS_CHUNK_LOG, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_nms_test");
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);   // propagation count (k_nms_finish), strip carries (k_sat)
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
@@ -1008,7 +1015,8 @@ static int step_kernel_arity(const void* f)
     return 3;
   if (f == (const void*)k_binmask || f == (const void*)k_pyr_o || f == (const void*)k_pyr_i ||
       f == (const void*)k_pyramid4<PYR_FULL> || f == (const void*)k_pyramid || f == (const void*)k_propagate ||
-      f == (const void*)k_nms_list || f == (const void*)k_nms_finish)
+      f == (const void*)k_nms_list || f == (const void*)k_nms_finish || f == (const void*)k_band_scan ||
+      f == (const void*)k_nms_list_scanned)
     return 2;
   return 0;
 }
