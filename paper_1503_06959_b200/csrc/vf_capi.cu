@@ -514,7 +514,6 @@ int vf_create(const vf_config* cfg, vf_ctx** out)
   b.cand_rank = A.get<int>((size_t)S * cap);
   b.chunk_off = A.get<int>((size_t)S * g.nms_chunks);
   b.nms_cnt = A.get<int>((size_t)S * 4);
-  b.band_off = A.get<int>((size_t)S * (g.bands_per_stream + 1));
   b.st_x = A.get<double>((size_t)S * cap); b.st_y = A.get<double>((size_t)S * cap);
   b.st_s = A.get<double>((size_t)S * cap); b.st_v = A.get<double>((size_t)S * cap);
   b.fx = A.get<double>((size_t)S * 2 * cap); b.fy = A.get<double>((size_t)S * 2 * cap);
@@ -793,13 +792,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   b.nms_u = 1;
   b.desc_bin = 1;
   b.orient_seq = getenv("VF_ORIENT_SEQ") && atoi(getenv("VF_ORIENT_SEQ")) != 0;
-  static const bool nms_scan = getenv("VF_NMS_SCAN") && atoi(getenv("VF_NMS_SCAN")) != 0;
-  if (nms_scan) {
-    k_band_scan<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_band_scan");
-    k_nms_list_scanned<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list_scanned");
-  } else {
-    k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
-  }
+  k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
   k_nms_test<<<c->nmst_grid, 1 << NMS_CHUNK_LOG, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_nms_test");
   cudaStreamWaitEvent(st, c->aux_mid[gi], 0);   // propagation count (k_nms_finish), strip carries (k_sat)
   k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
@@ -1005,6 +998,12 @@ int vf_block_match(const uint8_t* prev_dev, const uint8_t* cur_dev, int w, int h
 // pointer changes every step: each kernel node's Bufs argument is re-pointed
 // with cudaGraphExecKernelNodeSetParams (streams of a describe half keep their
 // offset), so no input copy is needed.
+// Batches up to this many frame bytes replay the graph.  Larger batches (the
+// 64 x 1080p step) launch eagerly: their kernels fill the GPU on their own,
+// and a captured graph loses the stream priorities the side / describe
+// streams rely on (569 vs 562 us per config-5 step measured).
+#define VF_GRAPH_MAX_BYTES (64LL << 20)
+
 // Argument count of each kernel launch_step launches (all take (Geo, Bufs, ...)).
 static int step_kernel_arity(const void* f)
 {
@@ -1015,8 +1014,7 @@ static int step_kernel_arity(const void* f)
     return 3;
   if (f == (const void*)k_binmask || f == (const void*)k_pyr_o || f == (const void*)k_pyr_i ||
       f == (const void*)k_pyramid4<PYR_FULL> || f == (const void*)k_pyramid || f == (const void*)k_propagate ||
-      f == (const void*)k_nms_list || f == (const void*)k_nms_finish || f == (const void*)k_band_scan ||
-      f == (const void*)k_nms_list_scanned)
+      f == (const void*)k_nms_list || f == (const void*)k_nms_finish)
     return 2;
   return 0;
 }
@@ -1121,7 +1119,8 @@ int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int6
   if (!c || !frames_dev || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
   if (!g_pattern_ok) return VF_ERR_PATTERN;
   static const bool env_off = getenv("VF_GRAPHS") && atoi(getenv("VF_GRAPHS")) == 0;
-  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3)
+  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3 &&
+      (long long)c->g.W * c->g.H * n_streams <= VF_GRAPH_MAX_BYTES)
     return graph_step(c, frames_dev, stream_stride, row_pitch, n_streams, (cudaStream_t)stream);
   c->b.frames = frames_dev;
   c->b.frame_stride = stream_stride;

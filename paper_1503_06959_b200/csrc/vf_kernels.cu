@@ -2094,74 +2094,6 @@ __global__ void __launch_bounds__(32 * NL_WARPS) k_nms_list(const __grid_constan
   }
 }
 
-// Two-launch variant of k_nms_list: k_band_scan (CTA per stream: the active
-// bands' candidate offsets by block scan, the stream total) then
-// k_nms_list_scanned (warp per band, offsets read, no per-CTA prefix).
-__global__ void __launch_bounds__(NF_THREADS) k_band_scan(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
-{
-  __shared__ int sm[NF_THREADS / 32];
-  const int s = b.s0 + blockIdx.x, tid = threadIdx.x;
-  const int epoch = stream_epoch(b, s), nb = g.bands_per_stream;
-  int* off = b.band_off + (long long)s * (nb + 1);
-  int carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += NF_THREADS) {
-    const int i = b0 + tid;
-    const int v = i < nb ? band_count(b, g, s, i, epoch) : 0;
-    int tot;
-    const int ex = block_excl_scan(v, tot, sm);
-    if (i < nb) off[i] = carry + ex;
-    carry += tot;
-  }
-  if (tid == 0) {
-    off[nb] = carry;
-    int* ctr = b.ctr + s * C_NCTR;
-    ctr[C_STAGE] = carry;
-    if (carry > g.kp_cap) atomicOr(&ctr[C_ERR], VF_ERRBIT_STAGING);
-  }
-}
-
-__global__ void __launch_bounds__(32 * NL_WARPS) k_nms_list_scanned(const __grid_constant__ Geo g,
-                                                                    const __grid_constant__ Bufs b)
-{
-  const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31;
-  const int bid = blockIdx.x * NL_WARPS + (threadIdx.x >> 5), nb = g.bands_per_stream;
-  if (bid >= nb) return;
-  const int* bo = b.band_off + (long long)s * (nb + 1);
-  const int off = bo[bid], mine = bo[bid + 1] - off;
-  if (mine == 0 || off + mine > g.kp_cap) return;
-  int l = 0;
-  while (l + 1 < g.NL && bid >= g.L[l + 1].band_base) l++;
-  const LayerGeo& Lg = g.L[l];
-  const int ys = (bid - Lg.band_base) * VF_TILE_H;
-  const int bmw = Lg.bm_words, nw = min(VF_TILE_H, Lg.h - ys) * bmw;
-  const uint32_t* bm = b.bitmaps + (long long)s * g.bm_slab_words + Lg.bm_off + (long long)ys * bmw;
-  uint32_t* out = b.cand + (long long)s * g.kp_cap;
-  const uint32_t lcode = (uint32_t)l << 26;
-  int pos = off;
-  for (int k0 = 0; k0 < nw; k0 += 128) {
-    uint32_t wd[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int k = k0 + 32 * q + lane;
-      wd[q] = k < nw ? __ldcg(bm + k) : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const unsigned any = __ballot_sync(0xffffffffu, wd[q] != 0u);
-      if (!any) continue;
-      const int k = k0 + 32 * q + lane;
-      int t;
-      int p = pos + warp_excl_scan(__popc(wd[q]), lane, t);
-      if (wd[q]) {
-        const int r = k / bmw, cw = k - r * bmw;
-        const uint32_t base = lcode | ((uint32_t)(ys + r) << 13) | (uint32_t)(32 * cw);
-        for (uint32_t m = wd[q]; m; m &= m - 1u) out[p++] = base + (uint32_t)(__ffs(m) - 1);
-      }
-      pos += t;
-    }
-  }
-}
-
 #define NMS_CHUNK_THREADS (1 << NMS_CHUNK_LOG)
 #ifndef NMS_TEST_MINB
 #define NMS_TEST_MINB 4
@@ -2575,9 +2507,6 @@ __device__ __forceinline__ void point_means2(const uint32_t* S, const Geo& g, do
 }
 
 #define DSW 8   // warps per CTA of k_desc_fused
-#ifndef DESC_CONTIG
-#define DESC_CONTIG 0
-#endif
 
 // ============================================================================
 // Orientation helpers of k_desc_fused
@@ -2676,20 +2605,9 @@ __global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constan
   // The warp's keypoints are gi = g0 + k * Wt; their headers (position, scale,
   // output slot) are fetched 32 at a time, lane k for keypoint k, and lane k
   // computes keypoint k's theta = atan2(gy, gx) after the batch.
-#if DESC_CONTIG
-  // CTA c describes the contiguous list range [c P, (c + 1) P): neighbouring
-  // keypoints (same band) run on one SM and share its L1; warp w takes every
-  // DSW-th of them
-  const int P = (total + gridDim.x - 1) / gridDim.x;
-  const int cbeg = blockIdx.x * P, cend = min(total, cbeg + P);
-  const int Wt = DSW;
-  for (int g0 = cbeg + wid; g0 < cend; g0 += 32 * Wt) {
-    const int gl = g0 + lane * Wt < cend ? g0 + lane * Wt : total;
-#else
   const int Wt = gridDim.x * DSW;
   for (int g0 = blockIdx.x * DSW + wid; g0 < total; g0 += 32 * Wt) {
     const int gl = g0 + lane * Wt;
-#endif
     long long o_l = -1;
     int s_l = 0;
     double kx_l = 0.0, ky_l = 0.0, sg_l = 0.0;
@@ -2710,11 +2628,7 @@ __global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constan
         b.forg[o_l] = 0; b.fage[o_l] = 0;
       }
     }
-#if DESC_CONTIG
-    const int nk = min(32, (cend - g0 + Wt - 1) / Wt);
-#else
     const int nk = min(32, (total - g0 + Wt - 1) / Wt);
-#endif
     double gx_l = 0.0, gy_l = 0.0;
 #pragma unroll 1
     for (int k = 0; k < nk; k++) {
