@@ -102,6 +102,7 @@ int vf_set_pattern(const double *points, const double *radii, int m, const int32
                    int nbits, const int32_t *long_pairs, int L);
 
 /* --- the per-frame pipeline: run_pipeline's loop body (pipeline.py:222-277) -- */
+/* Frames up to 8192 x 8192 (VF_ERR_ARG beyond: NMS candidates are coded in 32 bits). */
 int vf_create(const vf_config *cfg, vf_ctx **out);
 int vf_destroy(vf_ctx *ctx);
 /* Geometry of the pyramid (layer order o0, i0, o1, ...): sizes and scales. */

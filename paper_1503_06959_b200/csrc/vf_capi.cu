@@ -218,7 +218,7 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
   g.kp_cap = (int)std::min(cap, 1LL << 28);
   g.prop_chunks = cdiv(g.kp_cap, 1024);
   g.nms_chunks = cdiv(g.kp_cap, 1 << NMS_CHUNK_LOG);
-  if (g.W > 8192 || g.NL > 16) return VF_ERR_ARG;   // NMS candidate code: layer << 26 | y << 13 | x
+  if (g.W > 8192 || g.H > 8192 || g.NL > 16) return VF_ERR_ARG;   // NMS candidate code: layer << 26 | y << 13 | x
   return VF_OK;
 }
 
