@@ -785,6 +785,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   }
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
+  b.nms_pre = !(getenv("VF_NMS_PRE") && atoi(getenv("VF_NMS_PRE")) == 0);
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_fast");
   stage_mark(c, 4, st);
   // candidate-parallel NMS: ordered candidate list, thread-per-candidate test +

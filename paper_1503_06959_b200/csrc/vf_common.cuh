@@ -117,6 +117,7 @@ struct Bufs {
   int* cand_rank;       // [S][kp_cap] kept candidate's rank within its NMS chunk
   int* chunk_off;       // [S][nms_chunks] kept count of each chunk (k_nms_test), then its output offset
   int* nms_cnt;         // [S][4] survivors inside / outside the border margin (FrameReport)
+  int nms_pre;          // k_fast drops candidates that fail the strict 3x3 test inside their tile (VF_NMS_PRE=0: off)
   int orient_seq;       // k_desc_fused: always take the sequential-sum orientation (test hook, VF_ORIENT_SEQ=1)
   int* prop_cnt;        // [S][prop_chunks]
   int* prop_out;        // [S][prop_chunks]

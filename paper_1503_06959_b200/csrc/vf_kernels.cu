@@ -1377,6 +1377,7 @@ struct FastWarp {
   uint8_t tile[FT_ROWS][FT_COLS];
   uint8_t sc[VF_TILE_H][VF_TILE_W];
   uint16_t queue[VF_TILE_H * VF_TILE_W];
+  uint32_t drop[VF_TILE_H][VF_TILE_W / 32];   // candidates dropped by the in-tile 3x3 test
   int rc[VF_TILE_H];          // cell row of each tile row (gating)
   uint16_t cc[VF_TILE_W];     // cell column of each tile column
 };
@@ -1411,6 +1412,7 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
     const uint8_t* lp = layer_ptr(g, b, s, l, pitch);
     for (int i = lane; i < VF_TILE_H * VF_TILE_W / 16; i += 32)
       reinterpret_cast<uint4*>(&fw.sc[0][0])[i] = make_uint4(0, 0, 0, 0);
+    (&fw.drop[0][0])[lane] = 0u;
     if (!clear_only) {
     const int um = use_mask(g, b, s);
     const uint8_t* cells = nullptr;
@@ -1563,6 +1565,26 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       if (score >= t) fw.sc[r][c] = (uint8_t)score;
     }
     __syncwarp();
+    // ---- pass 3 (b.nms_pre): a candidate whose 8 neighbours all lie in this
+    // tile and that is not their strict maximum would fail k_nms_test's strict
+    // 3x3 test (detector.py:255-262): drop it from the bitmap here, so only the
+    // NMS work shrinks.  Candidates on the tile's border wait for k_nms_test.
+    if (b.nms_pre) {
+      for (int qi = lane; qi < qn; qi += 32) {
+        const int p = fw.queue[qi];
+        const int r = p / VF_TILE_W, c = p - r * VF_TILE_W;
+        const int sv = fw.sc[r][c];
+        if (sv == 0 || r == 0 || r == VF_TILE_H - 1 || c == 0 || c == VF_TILE_W - 1) continue;
+        int m = 0;
+#pragma unroll
+        for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+          for (int dx = -1; dx <= 1; dx++)
+            if (dy || dx) m = max(m, (int)fw.sc[r + dy][c + dx]);
+        if (m >= sv) atomicOr(&fw.drop[r][c >> 5], 1u << (c & 31));
+      }
+      __syncwarp();
+    }
     }
     __syncwarp();
     // ---- store scores (whole tile: gated pixels read back as 0) + bitmap ----
@@ -1574,24 +1596,28 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       *reinterpret_cast<uint4*>(smap + (long long)y * Lg.pitch + x) = *reinterpret_cast<const uint4*>(&fw.sc[r][16 * cc]);
     }
     {
+      // Candidate bitmap (score >= t), minus the candidates pass 3 dropped.
       const int r = lane >> 2, kw = lane & 3;
       const int y = y0 + r;
-      uint32_t word = 0;
+      uint32_t word_all = 0;
 #pragma unroll
       for (int q = 0; q < 8; q++) {
         const uint32_t v = *reinterpret_cast<const uint32_t*>(&fw.sc[r][32 * kw + 4 * q]);
         const uint32_t nz = __vcmpne4(v, 0u);
-        const uint32_t bits = ((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) | ((nz >> 28) & 8u);
-        word |= bits << (4 * q);
+        word_all |= (((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) | ((nz >> 28) & 8u)) << (4 * q);
       }
+      const uint32_t word = word_all & ~fw.drop[r][kw];
       if (y < h && x0 + 32 * kw < w)
         b.bitmaps[(long long)s * g.bm_slab_words + Lg.bm_off + (long long)y * Lg.bm_words + 4 * tx + kw] = word;
-      int n = __popc(word);
+      int n = __popc(word), na = __popc(word_all);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
-      if (lane == 0 && n) {
-        atomicAdd(&b.ctr[s * C_NCTR + C_NCAND], n);
-        atomicAdd(&b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty], n);
+      for (int o = 16; o > 0; o >>= 1) {
+        n += __shfl_down_sync(0xffffffffu, n, o);
+        na += __shfl_down_sync(0xffffffffu, na, o);
+      }
+      if (lane == 0) {
+        if (na) atomicAdd(&b.ctr[s * C_NCTR + C_NCAND], na);
+        if (n) atomicAdd(&b.band_cand[(long long)s * g.bands_per_stream + Lg.band_base + ty], n);
       }
     }
     __syncwarp();
