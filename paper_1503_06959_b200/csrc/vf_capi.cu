@@ -695,6 +695,12 @@ int vf_reset(vf_ctx* c, void* stream)
   return cuda_status(cudaGetLastError());
 }
 
+// Batches up to this many frame bytes replay the graph.  Larger batches (the
+// 64 x 1080p step) launch eagerly: their kernels fill the GPU on their own,
+// and a captured graph loses the stream priorities the side / describe
+// streams rely on (569 vs 562 us per config-5 step measured).
+#define VF_GRAPH_MAX_BYTES (64LL << 20)
+
 static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
 {
   const Geo& g = c->g;
@@ -754,6 +760,14 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   }
   k_worklist<<<dim3(tile_ctas, n), 256, 0, st>>>(g, b, tile_ctas, 0, 0); DBG_SYNC(st, "k_worklist");
   if (pyi) cudaStreamWaitEvent(st, c->pyi_e[gi], 0);
+  // In large batches the side chain (carries, propagation counts, Eq. 1
+  // propagation) starts with k_fast rather than beside k_pyr_i / k_worklist,
+  // which are on the critical path (config 5: 553 -> 536 us per step; the
+  // single-stream configs measured 1-4 us better with the early start).
+  // VF_SIDE_LATE=0 / 1 forces either.
+  const char* sl_env = getenv("VF_SIDE_LATE");
+  const bool side_late = sl_env ? atoi(sl_env) != 0 : (long long)g.W * g.H * n > VF_GRAPH_MAX_BYTES;
+  if (side_late) cudaEventRecord(c->aux_in[gi], st);
   cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
   const bool prop = g.mask_mode == 1 || g.mask_mode == 2;
   k_worklist<<<dim3(cov_ctas + carry_ctas + (prop ? PROP_CTAS : 0), n), 256, 0, c->aux[gi]>>>(
@@ -999,11 +1013,6 @@ int vf_block_match(const uint8_t* prev_dev, const uint8_t* cur_dev, int w, int h
 // pointer changes every step: each kernel node's Bufs argument is re-pointed
 // with cudaGraphExecKernelNodeSetParams (streams of a describe half keep their
 // offset), so no input copy is needed.
-// Batches up to this many frame bytes replay the graph.  Larger batches (the
-// 64 x 1080p step) launch eagerly: their kernels fill the GPU on their own,
-// and a captured graph loses the stream priorities the side / describe
-// streams rely on (569 vs 562 us per config-5 step measured).
-#define VF_GRAPH_MAX_BYTES (64LL << 20)
 
 // Argument count of each kernel launch_step launches (all take (Geo, Bufs, ...)).
 static int step_kernel_arity(const void* f)
