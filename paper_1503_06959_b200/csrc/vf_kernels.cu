@@ -2605,7 +2605,10 @@ __device__ __noinline__ void dr_orient_seq_g(const uint8_t* v, double& gx_out, d
 // mostly L1 hits of the first pass.  Keypoints: the describe list b.gidx
 // (candidate indices, from k_nms_test) of the streams [s0, s0 + n).
 // ============================================================================
-__global__ void __launch_bounds__(32 * DSW, 3) k_desc_fused(const __grid_constant__ Geo g,
+#ifndef FUSED_MINB
+#define FUSED_MINB 2
+#endif
+__global__ void __launch_bounds__(32 * DSW, FUSED_MINB) k_desc_fused(const __grid_constant__ Geo g,
                                                          const __grid_constant__ Bufs b, int n_streams)
 {
   __shared__ __align__(16) uint8_t vals[DSW][DW_ROW];
