@@ -448,10 +448,10 @@ def init_process_group(world, local):
 
 
 def launches_per_step(mode, n_streams):
-    # pyramid, worklist x2 (main + side stream), fast, nms, nms_finish, finalize;
-    # sat + describe x3 once per concurrent stream half; + propagate (mask
-    # modes), + binmask (binning)
-    return 7 + 4 * desc_halves(n_streams) + (1 if mode in ("intensity", "binning") else 0) + (
+    # k_pyr_o, k_pyr_i, k_worklist x2 (main + side stream), k_fast, k_nms_list,
+    # k_nms_test, k_nms_finish, k_finalize; k_sat + k_desc_fused once per
+    # concurrent describe half; + k_propagate (mask modes), + k_binmask (binning)
+    return 9 + 2 * desc_halves(n_streams) + (1 if mode in ("intensity", "binning") else 0) + (
         1 if mode == "binning" else 0)
 
 
