@@ -320,6 +320,7 @@ struct vf_ctx {
   std::vector<cudaStream_t> dstreams;
   std::vector<cudaEvent_t> djoin;
   std::vector<cudaEvent_t> dfork_g;     // per stream group
+  std::vector<cudaEvent_t> dsat_e;      // per describe stream: its k_sat done (VF_DESC_STAGGER)
   std::vector<cudaStream_t> pyi_s;      // per stream group: k_pyr_i beside the main work list
   std::vector<cudaEvent_t> pyi_e;
   // CUDA graph of one step (small batches): the step's launches (all its
@@ -604,6 +605,7 @@ int vf_destroy(vf_ctx* c)
   if (c->hp) { cudaStreamDestroy(c->hp); cudaEventDestroy(c->hp_in); cudaEventDestroy(c->hp_out); }
   for (size_t k = 0; k < c->dstreams.size(); k++) { cudaStreamDestroy(c->dstreams[k]); cudaEventDestroy(c->djoin[k]); }
   for (cudaEvent_t ev : c->dfork_g) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->dsat_e) cudaEventDestroy(ev);
   for (size_t k = 0; k < c->pyi_s.size(); k++) { cudaStreamDestroy(c->pyi_s[k]); cudaEventDestroy(c->pyi_e[k]); }
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
@@ -841,6 +843,16 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
       c->djoin.push_back(de);
     }
   }
+  // Staggered halves (half 1's SAT build beside half 0's describe) pay off
+  // when every tile is built (modes none / binning: dense config 5 3100 ->
+  // 3007 us) but not in masked frames (533 -> 543 us); VF_DESC_STAGGER forces.
+  const char* stg = getenv("VF_DESC_STAGGER");
+  const bool desc_stagger = stg ? atoi(stg) != 0 : (g.mask_mode == 0 || g.mask_mode == 2);
+  while (c->dsat_e.size() < c->dstreams.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return VF_ERR_CUDA;
+    c->dsat_e.push_back(e);
+  }
   cudaEventRecord(c->dfork_g[gi], st);
   for (int h = 0; h < dpar; h++) {
     const int h0 = (int)((long long)n * h / dpar), h1 = (int)((long long)n * (h + 1) / dpar);
@@ -850,7 +862,11 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     const int nh = h1 - h0, pb = (nh + 1) * (int)sizeof(int);
     cudaStream_t ds = c->dstreams[2 * gi + h];
     cudaStreamWaitEvent(ds, c->dfork_g[gi], 0);
+    // staggered: half h's SAT build waits for half h-1's, so it runs beside
+    // half h-1's (L1-bound) describe instead of beside its SAT build
+    if (desc_stagger && h > 0) cudaStreamWaitEvent(ds, c->dsat_e[2 * gi + h - 1], 0);
     k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh, 0); DBG_SYNC(ds, "k_sat");
+    if (desc_stagger) cudaEventRecord(c->dsat_e[2 * gi + h], ds);
     k_desc_fused<<<c->dfused_grid, 32 * DSW, pb, ds>>>(g, bh, nh); DBG_SYNC(ds, "k_desc_fused");
     cudaEventRecord(c->djoin[2 * gi + h], ds);
   }
