@@ -4,7 +4,9 @@ GPU pool): the step runs on up to three priority classes of CUDA streams
 halves), with epoch stamps instead of clears and atomics for staging.  A race
 between them shows up as a result that depends on the launch arrangement.
 Every arrangement below -- CUDA graph or eager launches, one or two describe
-halves, one or three stream groups, the priority stream on or off -- must give
+halves (concurrent or staggered), one or three stream groups, the priority
+stream on or off, the side chain early or late, the k_fast NMS prefilter on or
+off, the certified or the sequential orientation -- must give
 bit-identical features (and equal the CPU oracle) over 8 frames of 6 config-5
 streams in each mode, each arrangement in a fresh process (the knobs are read
 once per process)."""
@@ -28,6 +30,14 @@ ARRANGEMENTS = {
     "groups3": {"VF_STREAM_GROUPS": "3", "VF_GRAPHS": "0"},
     "no_prio": {"VF_PRIO": "0", "VF_GRAPHS": "0"},
     "no_split_pyramid": {"VF_PYR_SPLIT": "0"},
+    # side chain beside k_pyr_i vs after it; staggered / concurrent describe
+    # halves; the k_fast NMS prefilter off; the sequential orientation forced
+    "side_late": {"VF_SIDE_LATE": "1", "VF_GRAPHS": "0"},
+    "side_early": {"VF_SIDE_LATE": "0", "VF_GRAPHS": "0"},
+    "stagger": {"VF_DESC_STAGGER": "1", "VF_GRAPHS": "0"},
+    "no_stagger": {"VF_DESC_STAGGER": "0", "VF_GRAPHS": "0"},
+    "no_nms_prefilter": {"VF_NMS_PRE": "0"},
+    "orient_seq": {"VF_ORIENT_SEQ": "1"},
 }
 
 CHILD = r"""
