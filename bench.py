@@ -708,7 +708,7 @@ def run_detect(args, rank, world, local):
         "kernels": kernels,
         "kernels_source": (f"per-stage CUDA events on the launch streams over {stage_k} eager steps after the timed "
                            f"region (step {stage_step_ms * 1e3:.1f} us there; the timed steps replay a CUDA graph "
-                           f"when a step's frames are <= 12 MB); share = stage time / that step time"),
+                           f"when a step's frames are <= 64 MB); share = stage time / that step time"),
         "work_last_step": diag,
     }
 

@@ -185,15 +185,17 @@ int vf_delta_apply(int32_t n_prev, const double *prev_x, const double *prev_y, c
 int vf_get_layer(vf_ctx *ctx, int s, int l, const uint8_t **ptr, int32_t *pitch);
 /* Live per-stage device timing with CUDA events on the launch stream:
  * stages = binmask, pyramid, worklist, fast, nms, sat, describe, propagate, finalize (9).
- * With >= 2 streams per call the SAT and describe kernels run as two
- * concurrent stream halves; their one joint interval is reported under "sat"
- * and "describe" is 0.  propagate is timed on its own (side) stream.
+ * The SAT build and the fused describe kernel run on describe streams (two
+ * stream halves with >= 2 streams per call); their one joint interval is
+ * reported under "sat" and "describe" is 0.  "nms" covers k_nms_list,
+ * k_nms_test and k_nms_finish.  propagate is timed on its own (side) stream.
  * vf_get_stage_ms synchronizes `stream`, returns the summed milliseconds per
  * stage since the last query and the number of steps, and clears. */
 int vf_set_timing(vf_ctx *ctx, int enable);
-/* CUDA graphs (default on): a batch of at most 12 MB of frames replays a
- * captured graph of the step's launches (inputs copied into the graph's fixed
- * input buffer first).  Off while stage timing is on and in temporal mode. */
+/* CUDA graphs (default on): a batch of at most 64 MB of frames replays a
+ * captured graph of the step's launches (captured once per batch size; the
+ * kernel nodes are re-pointed at each call's frames, nothing is copied).  Off
+ * while stage timing is on and in temporal mode. */
 int vf_set_graphs(vf_ctx *ctx, int enable);
 int vf_get_stage_ms(vf_ctx *ctx, double *ms9, int32_t *n_steps, void *stream);
 /* Synchronizes `stream`; work counters of the last step: active FAST tiles,
