@@ -1145,8 +1145,8 @@ int vf_process(vf_ctx* c, const uint8_t* frames_dev, int64_t stream_stride, int6
   if (!c || !frames_dev || n_streams < 1 || n_streams > c->S || row_pitch < c->g.W) return VF_ERR_ARG;
   if (!g_pattern_ok) return VF_ERR_PATTERN;
   static const bool env_off = getenv("VF_GRAPHS") && atoi(getenv("VF_GRAPHS")) == 0;
-  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3 &&
-      (long long)c->g.W * c->g.H * n_streams <= VF_GRAPH_MAX_BYTES)
+  static const long long gmax = getenv("VF_GRAPH_MAX_MB") ? atoll(getenv("VF_GRAPH_MAX_MB")) << 20 : VF_GRAPH_MAX_BYTES;
+  if (c->graphs && !env_off && !c->timing && c->g.mask_mode != 3 && (long long)c->g.W * c->g.H * n_streams <= gmax)
     return graph_step(c, frames_dev, stream_stride, row_pitch, n_streams, (cudaStream_t)stream);
   c->b.frames = frames_dev;
   c->b.frame_stride = stream_stride;
