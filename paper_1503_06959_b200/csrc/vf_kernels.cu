@@ -2578,7 +2578,7 @@ __device__ __forceinline__ bool dr_orient_lin(uint32_t m0, uint32_t m1, const do
   if (sx < 0.0 && fabs(sy) <= by) return false;            // theta near the +-pi cut
   cs = sx * rn;
   sn = sy * rn;
-  dth = 2.0 * (bx + by) / gn + 1e-14;
+  dth = 2.02 * (bx + by) * rn + 1e-14;   // rn = 1 / |g| (to ~1 ulp)
   return true;
 }
 
