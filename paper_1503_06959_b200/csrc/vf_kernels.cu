@@ -1430,24 +1430,30 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       }
     }
     // ---- stage rows y0-3 .. y0+10, cols x0-16 .. x0+143 ----
+    // interior 16-B chunks by cp.async (global -> shared, no register round
+    // trip, all of a lane's copies in flight together); chunks at the layer
+    // edge bytewise, chunks outside the layer zero
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(lp) | (uintptr_t)pitch) & 15) == 0;
     for (int i = lane; i < FT_ROWS * (FT_COLS / 16); i += 32) {
       const int rr = i / (FT_COLS / 16), c16 = i - rr * (FT_COLS / 16);
       const int y = y0 - 3 + rr, x = x0 - 16 + 16 * c16;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (y >= 0 && y < h && x + 16 > 0 && x < w) {   // chunks wholly outside the layer stay zero
+      uint8_t* dst = &fw.tile[rr][16 * c16];
+      if (y >= 0 && y < h && x + 16 > 0 && x < w) {
         const uint8_t* row = lp + (long long)y * pitch;
         if (vec_ok && x >= 0 && x + 16 <= pitch && x + 16 <= ((w + 15) & ~15)) {
-          v = __ldg(reinterpret_cast<const uint4*>(row + x));
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(row + x) : "memory");
         } else {
           uint8_t tmp[16];
 #pragma unroll
           for (int k = 0; k < 16; k++) tmp[k] = (x + k >= 0 && x + k < w) ? __ldg(row + x + k) : 0;
-          v = *reinterpret_cast<uint4*>(tmp);
+          *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(tmp);
         }
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
       }
-      *reinterpret_cast<uint4*>(&fw.tile[rr][16 * c16]) = v;
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
     // ---- pass 1: 4-point necessary test (detector.py:117-125) ----
     // A 9-arc covers two adjacent compass points, both brighter than C + t or
@@ -2186,6 +2192,8 @@ __global__ void __launch_bounds__(NMS_CHUNK_THREADS, NMS_TEST_MINB) k_nms_test(c
     __syncthreads();
   }
 }
+
+#endif
 
 // After k_nms (stream order), one CTA per stream: band output offsets (scan
 // of the kept counts in band order), the SAT-tile work list (the bitmap's set
