@@ -2193,8 +2193,6 @@ __global__ void __launch_bounds__(NMS_CHUNK_THREADS, NMS_TEST_MINB) k_nms_test(c
   }
 }
 
-#endif
-
 // After k_nms (stream order), one CTA per stream: band output offsets (scan
 // of the kept counts in band order), the SAT-tile work list (the bitmap's set
 // tiles in bitmap order) and the FrameReport.  Every load is issued up front.
