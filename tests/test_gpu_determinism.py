@@ -7,7 +7,7 @@ Every arrangement below -- CUDA graph or eager launches, one or two describe
 halves (concurrent or staggered), one or three stream groups, the priority
 stream on or off, the side chain early or late, the k_fast NMS prefilter on or
 off, the certified or the sequential orientation -- must give
-bit-identical features (and equal the CPU oracle) over 8 frames of 6 config-5
+bit-identical features (theta of the sequential orientation within 1e-9) (and equal the CPU oracle) over 8 frames of 6 config-5
 streams in each mode, each arrangement in a fresh process (the knobs are read
 once per process)."""
 
@@ -81,6 +81,11 @@ def test_launch_arrangements_bit_identical(mode, tmp_path):
     for name, r in results.items():
         assert r.keys() == base.keys()
         for k in base:
+            if name == "orient_seq" and k.endswith("_theta"):
+                # the reference's sequential sum vs the certified linear form
+                # (DESIGN.md section 5): theta within the bound, bits identical
+                assert np.abs(r[k] - base[k]).max(initial=0.0) <= 1e-9, (name, k)
+                continue
             assert np.array_equal(r[k], base[k]), (name, k)
     # and the arrangement-independent result is the oracle's
     from oracle import oracle
