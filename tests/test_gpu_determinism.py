@@ -6,10 +6,10 @@ between them shows up as a result that depends on the launch arrangement.
 Every arrangement below -- CUDA graph or eager launches, one or two describe
 halves (concurrent or staggered), one or three stream groups, the priority
 stream on or off, the side chain early or late, the k_fast NMS prefilter on or
-off, the certified or the sequential orientation -- must give
-bit-identical features (theta of the sequential orientation within 1e-9) (and equal the CPU oracle) over 8 frames of 6 config-5
-streams in each mode, each arrangement in a fresh process (the knobs are read
-once per process)."""
+off, the certified or the sequential orientation -- must give bit-identical
+features (theta of the sequential orientation within 1e-9) and equal the CPU
+oracle over 8 frames of 6 config-5 streams in each mode, each arrangement in a
+fresh process (some knobs are read once per process)."""
 
 import json
 import os
