@@ -390,6 +390,16 @@ __device__ __forceinline__ int find_stream(const int* pre, int n_streams, int gi
   return lo;
 }
 
+// Same, for a persistent loop that visits increasing items: start from the
+// previous item's stream (usually 0 or 1 steps instead of a binary search).
+__device__ __forceinline__ int find_stream_from(const int* pre, int n_streams, int gi, int& hint)
+{
+  int lo = hint;
+  while (lo + 1 < n_streams && pre[lo + 1] <= gi) lo++;
+  hint = lo;
+  return lo;
+}
+
 // Exclusive prefix over streams of a per-stream count, computed by the whole
 // block (one load per thread), into pre[0..n_streams].
 template <typename F>
@@ -441,9 +451,9 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
   struct TileIn { int s, X0, Y0, tw, th; uint32_t kr, w[8]; };
   const bool vec = ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) &
                     15) == 0;
+  int shint = 0;
   auto fetch = [&](int item, TileIn& in) {
-    int lo = 0, hi = n_streams;
-    while (hi - lo > 1) { int m = (lo + hi) >> 1; if (pre[m] <= item) lo = m; else hi = m; }
+    const int lo = find_stream_from(pre, n_streams, item, shint);
     const int s = b.s0 + lo, i = item - pre[lo];
     const int t = all ? i : b.sat_work[(long long)s * g.sat_tiles + i];
     const int ty = t / g.stx, tx = t - ty * g.stx;
@@ -2143,8 +2153,9 @@ __global__ void __launch_bounds__(NMS_CHUNK_THREADS, NMS_TEST_MINB) k_nms_test(c
     return (ctr[C_ERR] & VF_ERRBIT_STAGING) ? 0 : (ctr[C_STAGE] + NMS_CHUNK_THREADS - 1) >> NMS_CHUNK_LOG;
   });
   const int total = pre[n_streams];
+  int shint = 0;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const int sl = find_stream(pre, n_streams, item), s = b.s0 + sl, ch = item - pre[sl];
+    const int sl = find_stream_from(pre, n_streams, item, shint), s = b.s0 + sl, ch = item - pre[sl];
     const int c = (ch << NMS_CHUNK_LOG) + tid;
     const int ncand = b.ctr[s * C_NCTR + C_STAGE];
     const int um = use_mask(g, b, s);
@@ -2641,13 +2652,14 @@ __global__ void __launch_bounds__(32 * DSW, FUSED_MINB) k_desc_fused(const __gri
   // output slot) are fetched 32 at a time, lane k for keypoint k, and lane k
   // computes keypoint k's theta = atan2(gy, gx) after the batch.
   const int Wt = gridDim.x * DSW;
+  int shint = 0;   // each lane's items increase (by 32 Wt per batch)
   for (int g0 = blockIdx.x * DSW + wid; g0 < total; g0 += 32 * Wt) {
     const int gl = g0 + lane * Wt;
     long long o_l = -1;
     int s_l = 0;
     double kx_l = 0.0, ky_l = 0.0, sg_l = 0.0;
     if (gl < total) {
-      const int sl = find_stream(pre, n_streams, gl), i = gl - pre[sl];
+      const int sl = find_stream_from(pre, n_streams, gl, shint), i = gl - pre[sl];
       s_l = b.s0 + sl;
       const int* ctr = b.ctr + s_l * C_NCTR;
       // describe-list entry = candidate index c (staging slot); output rank =
