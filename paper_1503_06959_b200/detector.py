@@ -1,7 +1,9 @@
 """Segment-test detection + scale-space NMS (drop-in for vidfeat.detector).
 
 detect_candidates / ast_corner_score run k_fast (vf_score_map) and
-nms_and_refine runs k_nms (vf_nms_refine): the pipeline's own kernels.
+nms_and_refine runs k_nms (vf_nms_refine), which shares the pipeline's
+nms_test / nms_refine device code (the pipeline itself runs them thread per
+candidate in k_nms_test).
 Reference: detector.py:1-324.
 """
 
