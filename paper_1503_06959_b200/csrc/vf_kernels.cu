@@ -2622,6 +2622,9 @@ __device__ __noinline__ void dr_orient_seq_g(const uint8_t* v, double& gx_out, d
 // mostly L1 hits of the first pass.  Keypoints: the describe list b.gidx
 // (candidate indices, from k_nms_test) of the streams [s0, s0 + n).
 // ============================================================================
+#ifndef FUSED_PAIRS_REG
+#define FUSED_PAIRS_REG 1
+#endif
 #ifndef FUSED_MINB
 #define FUSED_MINB 2
 #endif
@@ -2648,6 +2651,11 @@ __global__ void __launch_bounds__(32 * DSW, FUSED_MINB) k_desc_fused(const __gri
   const double pn0 = sqrt(ptab[lane][0] * ptab[lane][0] + ptab[lane][1] * ptab[lane][1]);
   const double pn1 = has1 ? sqrt(ptab[j1][0] * ptab[j1][0] + ptab[j1][1] * ptab[j1][1]) : 0.0;
   uint8_t* v = vals[wid];
+#if FUSED_PAIRS_REG
+  uint32_t preg[16];   // this lane's 16 short pairs (bits 32 q + lane), in registers
+#pragma unroll
+  for (int q = 0; q < 16; q++) preg[q] = pairs[32 * q + lane];
+#endif
   // The warp's keypoints are gi = g0 + k * Wt; their headers (position, scale,
   // output slot) are fetched 32 at a time, lane k for keypoint k, and lane k
   // computes keypoint k's theta = atan2(gy, gx) after the batch.
@@ -2720,7 +2728,11 @@ __global__ void __launch_bounds__(32 * DSW, FUSED_MINB) k_desc_fused(const __gri
       uint32_t mine = 0u;
 #pragma unroll
       for (int q = 0; q < 16; q++) {
+#if FUSED_PAIRS_REG
+        const uint32_t pr = preg[q];
+#else
         const uint32_t pr = pairs[32 * q + lane];   // si | sj << 16 (smem, conflict-free)
+#endif
         const uint32_t word = __ballot_sync(0xffffffffu, v[pr & 0xffff] > v[pr >> 16]);
         if (lane == q) mine = word;
       }
