@@ -797,10 +797,11 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
 // Warp-strip pyramid (O = 4): two launches without shared memory or block
 // barriers, every lane loading all of its input bytes at once.
 //
-// k_pyr_o: warp per strip of 8 o0 rows x 256 o0 columns (lane: 8 columns).
-//   o1 (4 rows x 4 px per lane), o2 (2 rows x 2 px), o3 (1 px) by the 2x2
+// k_pyr_o: warp per strip of 8 o0 rows x 512 o0 columns (lane: 16 columns).
+//   o1 (4 rows x 8 px per lane), o2 (2 rows x 4 px), o3 (2 px) by the 2x2
 //   rounded halving of pyramid.py:67-73; the IDDM of masking.py:84-93 on o3
-//   (one lane per top-octave cell, a ballot is one word of the bit mask);
+//   (two top-octave cells per lane; two ballots are the strip's two words of
+//   the bit mask);
 //   the per-32-column SAT row sums of the 8 rows.  Block 0 of each stream
 //   also resets the per-step counters.
 // k_pyr_i: warp per strip of 12 o0 rows x 384 o0 columns (lane: 12 columns).
@@ -812,7 +813,7 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
 //   of a gated pixel, <= 3 W / w_i3 o0 pixels); FAST reads the other pixels
 //   only for gated-off positions, whose scores are dropped.
 // ============================================================================
-#define PYO_COLS 256
+#define PYO_COLS 512
 #define PYI_COLS 384
 __device__ __forceinline__ void store_bytes(uint8_t* row, int x, int valid, uint32_t w, int n)
 {
@@ -839,6 +840,12 @@ __device__ __noinline__ uint32_t load_edge4(const uint8_t* p, int valid)
   return w;
 }
 
+// 2x2 rounded halving of two rows of 16 bytes -> 8 bytes (pyramid.py:67-73)
+__device__ __forceinline__ uint2 halve8(const uint4 a, const uint4 c)
+{
+  return make_uint2(halve4(make_uint2(a.x, a.y), make_uint2(c.x, c.y)), halve4(make_uint2(a.z, a.w), make_uint2(c.z, c.w)));
+}
+
 __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
 {
   const int s = b.s0 + blockIdx.y, lane = threadIdx.x & 31;
@@ -857,119 +864,126 @@ __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, co
   const int sy = strip / nsx, sx = strip - sy * nsx;
   const int h1 = g.L[2].h;
   if (sy * 4 >= h1) return;
-  const int X = sx * PYO_COLS + 8 * lane, Y = sy * 8, W = g.W, H = g.H;
+  const int X = sx * PYO_COLS + 16 * lane, Y = sy * 8, W = g.W, H = g.H;
   const int nr = min(8, H - Y);              // o0 rows present (>= 2)
-  // ---- 8 o0 rows x 8 columns of this lane ----
+  // ---- 8 o0 rows x 16 columns of this lane ----
   const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y * b.frame_pitch + X;
   const int pitch = (int)b.frame_pitch;
-  const bool vec = ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) & 7) == 0;
-  uint2 r[8];
-  if (vec && X + 8 <= W && nr == 8) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(b.frames) | (uintptr_t)b.frame_pitch | (uintptr_t)b.frame_stride) & 15) == 0;
+  uint4 r[8];
+  if (vec && X + 16 <= W && nr == 8) {
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-#ifdef VF_DEBUG
-      if ((reinterpret_cast<uintptr_t>(src + k * pitch) & 7)) printf("pyr_o load %p X %d Y %d k %d\n", src + k * pitch, X, Y, k);
-#endif
-      r[k] = __ldg(reinterpret_cast<const uint2*>(src + k * pitch));
-    }
+    for (int k = 0; k < 8; k++) r[k] = __ldg(reinterpret_cast<const uint4*>(src + k * pitch));
   } else {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const bool ok = k < nr && X < W;
-      r[k] = make_uint2(ok ? load_edge4(src + k * pitch, W - X) : 0u, ok ? load_edge4(src + k * pitch + 4, W - X - 4) : 0u);
+      const uint8_t* p = src + k * pitch;
+      r[k] = make_uint4(ok ? load_edge4(p, W - X) : 0u, ok && X + 4 < W ? load_edge4(p + 4, W - X - 4) : 0u,
+                        ok && X + 8 < W ? load_edge4(p + 8, W - X - 8) : 0u,
+                        ok && X + 12 < W ? load_edge4(p + 12, W - X - 12) : 0u);
     }
   }
-  // ---- SAT row sums: 32-column segments = 4 lanes ----
+  // ---- SAT row sums: 32-column segments = 2 lanes ----
   {
     const int col = X / VF_ST;
     uint32_t* rs = b.rowsum + ((long long)s * H + Y) * g.stx + col;
-    const bool wr = (lane & 3) == 0 && col < g.stx;
+    const bool wr = (lane & 1) == 0 && col < g.stx;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      uint32_t a = __dp4a(r[k].y, 0x01010101u, __dp4a(r[k].x, 0x01010101u, 0u));
+      uint32_t a = __dp4a(r[k].w, 0x01010101u, __dp4a(r[k].z, 0x01010101u,
+                   __dp4a(r[k].y, 0x01010101u, __dp4a(r[k].x, 0x01010101u, 0u))));
       a += __shfl_xor_sync(0xffffffffu, a, 1);
-      a += __shfl_xor_sync(0xffffffffu, a, 2);
       if (wr && k < nr) rs[k * g.stx] = a;
     }
   }
   uint8_t* lay = b.layers + (long long)s * g.layer_slab;
-  // ---- o1: 4 rows x 4 px ----
+  // ---- o1: 4 rows x 8 px ----
   const LayerGeo& L1 = g.L[2];
-  uint32_t w1[4];
+  uint2 w1[4];
   {
-    uint8_t* o1 = lay + L1.layer_off + (long long)(4 * sy) * L1.pitch + X / 2;
+    const int x1 = X / 2;
+    uint8_t* o1 = lay + L1.layer_off + (long long)(4 * sy) * L1.pitch + x1;
     const int n1 = min(4, h1 - 4 * sy);
-    const bool full = X / 2 + 4 <= L1.w;
+    const bool full = x1 + 8 <= L1.w;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      w1[k] = halve4(r[2 * k], r[2 * k + 1]);
+      w1[k] = halve8(r[2 * k], r[2 * k + 1]);
       if (k < n1) {
-#ifdef VF_DEBUG
-        if (full && (reinterpret_cast<uintptr_t>(o1 + k * L1.pitch) & 3)) printf("pyr_o o1 X %d\n", X);
-#endif
-        if (full) *reinterpret_cast<uint32_t*>(o1 + k * L1.pitch) = w1[k];
-        else if (X / 2 < L1.w) store_bytes(o1 + k * L1.pitch - X / 2, X / 2, L1.w, w1[k], 4);
+        if (full) *reinterpret_cast<uint2*>(o1 + k * L1.pitch) = w1[k];
+        else if (x1 < L1.w) {
+          store_bytes(o1 + k * L1.pitch - x1, x1, L1.w, w1[k].x, 4);
+          if (x1 + 4 < L1.w) store_bytes(o1 + k * L1.pitch - x1, x1 + 4, L1.w, w1[k].y, 4);
+        }
       }
     }
   }
-  // ---- o2: 2 rows x 2 px (bytes 0, 1) ----
+  // ---- o2: 2 rows x 4 px ----
   const LayerGeo& L2 = g.L[4];
   uint32_t w2[2];
   {
-    uint8_t* o2 = lay + L2.layer_off + (long long)(2 * sy) * L2.pitch + X / 4;
+    const int x2 = X / 4;
+    uint8_t* o2 = lay + L2.layer_off + (long long)(2 * sy) * L2.pitch + x2;
     const int n2 = min(2, L2.h - 2 * sy);
-    const bool full = X / 4 + 2 <= L2.w;
 #pragma unroll
     for (int k = 0; k < 2; k++) {
-      const uint32_t a = w1[2 * k], c = w1[2 * k + 1];
-      const uint32_t e = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu) + (c & 0x00ff00ffu) + ((c >> 8) & 0x00ff00ffu);
-      const uint32_t q = ((e + 0x00020002u) >> 2) & 0x00ff00ffu;
-      w2[k] = (q & 0xffu) | ((q >> 8) & 0xff00u);
-      if (k < n2) {
-#ifdef VF_DEBUG
-        if (full && (reinterpret_cast<uintptr_t>(o2 + k * L2.pitch) & 1)) printf("pyr_o o2 X %d\n", X);
-#endif
-        if (full) *reinterpret_cast<uint16_t*>(o2 + k * L2.pitch) = (uint16_t)w2[k];
-        else if (X / 4 < L2.w) o2[k * L2.pitch] = (uint8_t)w2[k];
-      }
+      w2[k] = halve4(w1[2 * k], w1[2 * k + 1]);
+      if (k < n2 && x2 < L2.w) store_bytes(o2 + k * L2.pitch - x2, x2, L2.w, w2[k], 4);
     }
   }
-  // ---- o3: 1 px ----
+  // ---- o3: 1 row x 2 px ----
   const LayerGeo& L3 = g.L[6];
-  const uint32_t sum3 = (w2[0] & 0xffu) + (w2[0] >> 8) + (w2[1] & 0xffu) + (w2[1] >> 8);
-  const int c3 = (int)((sum3 + 2) >> 2);
+  const uint32_t e3 = (w2[0] & 0x00ff00ffu) + ((w2[0] >> 8) & 0x00ff00ffu) + (w2[1] & 0x00ff00ffu) +
+                      ((w2[1] >> 8) & 0x00ff00ffu);
+  const uint32_t q3 = ((e3 + 0x00020002u) >> 2) & 0x00ff00ffu;
+  const int c3a = (int)(q3 & 0xffu), c3b = (int)(q3 >> 16);
   const int x3 = X / 8, y3 = sy;
-  const bool in3 = x3 < L3.w && y3 < L3.h;
-  if (in3) lay[L3.layer_off + (long long)y3 * L3.pitch + x3] = (uint8_t)c3;
+  const bool in3a = x3 < L3.w && y3 < L3.h, in3b = x3 + 1 < L3.w && y3 < L3.h;
+  uint8_t* o3 = lay + L3.layer_off + (long long)y3 * L3.pitch + x3;
+  if (in3b) *reinterpret_cast<uint16_t*>(o3) = (uint16_t)(c3a | (c3b << 8));
+  else if (in3a) *o3 = (uint8_t)c3a;
   // ---- IDDM on o3 (masking.py:84-93): int16 diff vs float t_i, strict ----
   if (g.mask_mode == 1) {
     const GridGeo& G = g.grid[0];
     const bool um = use_mask(g, b, s);
     uint8_t* st = iddm_state(g, b, s, 3, 0);
     const int gi = y3 * L3.w + x3;
-    int bit = 0;
+    int bits = 0;
     unsigned covered = 0;
-    if (in3) {
-      if (um) {
-        int d = c3 - (int)iddm_state(g, b, s, 3, 1)[gi];
-        d = d < 0 ? -d : d;
-        bit = (double)d > g.t_i;
-        b.cells[(long long)s * g.cell_slab + G.cell_off + gi] = (uint8_t)bit;
-        if (bit) covered = (unsigned)(min(G.ch, H - y3 * G.ch) * min(G.cw, W - x3 * G.cw));
-      }
-      st[gi] = (uint8_t)c3;
-    }
     if (um) {
-      const unsigned bal = __ballot_sync(0xffffffffu, bit);
-      if (bal) {
+      const uint8_t* stp = iddm_state(g, b, s, 3, 1);
+      uint8_t* cl = b.cells + (long long)s * g.cell_slab + G.cell_off;
+      if (in3a) {
+        const int d = abs(c3a - (int)stp[gi]);
+        const int bit = (double)d > g.t_i;
+        cl[gi] = (uint8_t)bit;
+        bits = bit;
+        if (bit) covered += (unsigned)(min(G.ch, H - y3 * G.ch) * min(G.cw, W - x3 * G.cw));
+      }
+      if (in3b) {
+        const int d = abs(c3b - (int)stp[gi + 1]);
+        const int bit = (double)d > g.t_i;
+        cl[gi + 1] = (uint8_t)bit;
+        bits |= bit << 1;
+        if (bit) covered += (unsigned)(min(G.ch, H - y3 * G.ch) * min(G.cw, W - (x3 + 1) * G.cw));
+      }
+    }
+    if (in3a) st[gi] = (uint8_t)c3a;
+    if (in3b) st[gi + 1] = (uint8_t)c3b;
+    if (um) {
+      // cell 32 k + lane of the strip belongs to lane (32 k + lane) / 2, pixel lane & 1
+      const uint32_t wk0 = __ballot_sync(0xffffffffu, (__shfl_sync(0xffffffffu, bits, lane >> 1) >> (lane & 1)) & 1);
+      const uint32_t wk1 = __ballot_sync(0xffffffffu, (__shfl_sync(0xffffffffu, bits, 16 + (lane >> 1)) >> (lane & 1)) & 1);
+      if (wk0 | wk1) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) covered += __shfl_down_sync(0xffffffffu, covered, o);
       }
-      if (lane == 0) {
-        if (covered) atomicAdd(b.cov + s, (unsigned long long)covered);
-        if (g.use_cbits && y3 < G.rows && sx < g.cbits_words)   // cells 32 sx .. 32 sx + 31 of row y3
+      if (lane < 2) {
+        if (lane == 0 && covered) atomicAdd(b.cov + s, (unsigned long long)covered);
+        const int wd = 2 * sx + lane;   // cells 32 wd .. 32 wd + 31 of row y3
+        if (g.use_cbits && y3 < G.rows && wd < g.cbits_words)
           b.cbits[((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words + (long long)y3 * g.cbits_words +
-                  sx] = bal;
+                  wd] = lane ? wk1 : wk0;
       }
     }
   }
