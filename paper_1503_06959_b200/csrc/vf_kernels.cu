@@ -528,13 +528,18 @@ __global__ void k_carries(const __grid_constant__ Geo g, const __grid_constant__
 // maps: the eight levels are produced in four phases (level pairs that do not
 // depend on each other share a phase), four pixels per 32-bit word.
 // ============================================================================
+// 2x2 rounded halving of two rows of 4 bytes: the two outputs sit in bytes 0
+// and 2 of the result (16-bit lanes; bits above a lane's byte are garbage, the
+// callers extract bytes).  Byte gathers by PRMT instead of shift + mask.
+__device__ __forceinline__ uint32_t halve_w(uint32_t a, uint32_t c)
+{
+  const uint32_t e = __byte_perm(a, 0u, 0x4240) + __byte_perm(a, 0u, 0x4341) + __byte_perm(c, 0u, 0x4240) +
+                     __byte_perm(c, 0u, 0x4341) + 0x00020002u;   // lane sums <= 1022
+  return e >> 2;
+}
 __device__ __forceinline__ uint32_t halve4(const uint2 r0, const uint2 r1)
 {
-  uint32_t a0 = (r0.x & 0x00ff00ffu) + ((r0.x >> 8) & 0x00ff00ffu) + (r1.x & 0x00ff00ffu) + ((r1.x >> 8) & 0x00ff00ffu);
-  uint32_t a1 = (r0.y & 0x00ff00ffu) + ((r0.y >> 8) & 0x00ff00ffu) + (r1.y & 0x00ff00ffu) + ((r1.y >> 8) & 0x00ff00ffu);
-  a0 = ((a0 + 0x00020002u) >> 2) & 0x00ff00ffu;
-  a1 = ((a1 + 0x00020002u) >> 2) & 0x00ff00ffu;
-  return __byte_perm(a0, a1, 0x6420);
+  return __byte_perm(halve_w(r0.x, r1.x), halve_w(r0.y, r1.y), 0x6420);
 }
 
 __device__ __forceinline__ void store_word(uint8_t* gdst, int gp, int y, int x, int vw, int vh, uint32_t w)
@@ -884,6 +889,18 @@ __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, co
                         ok && X + 12 < W ? load_edge4(p + 12, W - X - 12) : 0u);
     }
   }
+  // the previous frame's top-octave pixels for the IDDM, loaded beside the rows
+  const LayerGeo& L3 = g.L[6];
+  const int x3 = X / 8, y3 = sy;
+  const bool in3a = x3 < L3.w && y3 < L3.h, in3b = x3 + 1 < L3.w && y3 < L3.h;
+  const int gi = y3 * L3.w + x3;
+  const bool um = g.mask_mode == 1 && use_mask(g, b, s);
+  int p3a = 0, p3b = 0;
+  if (um) {
+    const uint8_t* stp = iddm_state(g, b, s, 3, 1);
+    if (in3a) p3a = stp[gi];
+    if (in3b) p3b = stp[gi + 1];
+  }
   // ---- SAT row sums: 32-column segments = 2 lanes ----
   {
     const int col = X / VF_ST;
@@ -932,36 +949,28 @@ __global__ void __launch_bounds__(256) k_pyr_o(const __grid_constant__ Geo g, co
     }
   }
   // ---- o3: 1 row x 2 px ----
-  const LayerGeo& L3 = g.L[6];
-  const uint32_t e3 = (w2[0] & 0x00ff00ffu) + ((w2[0] >> 8) & 0x00ff00ffu) + (w2[1] & 0x00ff00ffu) +
-                      ((w2[1] >> 8) & 0x00ff00ffu);
-  const uint32_t q3 = ((e3 + 0x00020002u) >> 2) & 0x00ff00ffu;
-  const int c3a = (int)(q3 & 0xffu), c3b = (int)(q3 >> 16);
-  const int x3 = X / 8, y3 = sy;
-  const bool in3a = x3 < L3.w && y3 < L3.h, in3b = x3 + 1 < L3.w && y3 < L3.h;
+  const uint32_t q3 = halve_w(w2[0], w2[1]);
+  const int c3a = (int)(q3 & 0xffu), c3b = (int)((q3 >> 16) & 0xffu);
   uint8_t* o3 = lay + L3.layer_off + (long long)y3 * L3.pitch + x3;
   if (in3b) *reinterpret_cast<uint16_t*>(o3) = (uint16_t)(c3a | (c3b << 8));
   else if (in3a) *o3 = (uint8_t)c3a;
   // ---- IDDM on o3 (masking.py:84-93): int16 diff vs float t_i, strict ----
   if (g.mask_mode == 1) {
     const GridGeo& G = g.grid[0];
-    const bool um = use_mask(g, b, s);
     uint8_t* st = iddm_state(g, b, s, 3, 0);
-    const int gi = y3 * L3.w + x3;
     int bits = 0;
     unsigned covered = 0;
     if (um) {
-      const uint8_t* stp = iddm_state(g, b, s, 3, 1);
       uint8_t* cl = b.cells + (long long)s * g.cell_slab + G.cell_off;
       if (in3a) {
-        const int d = abs(c3a - (int)stp[gi]);
+        const int d = abs(c3a - p3a);
         const int bit = (double)d > g.t_i;
         cl[gi] = (uint8_t)bit;
         bits = bit;
         if (bit) covered += (unsigned)(min(G.ch, H - y3 * G.ch) * min(G.cw, W - x3 * G.cw));
       }
       if (in3b) {
-        const int d = abs(c3b - (int)stp[gi + 1]);
+        const int d = abs(c3b - p3b);
         const int bit = (double)d > g.t_i;
         cl[gi + 1] = (uint8_t)bit;
         bits |= bit << 1;
@@ -1006,15 +1015,18 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
     const int X0 = sx * PYI_COLS;
     const int cx0 = max(0, X0 - g.pyr_halo) / G.cw, cx1 = min(G.cols - 1, (X0 + PYI_COLS - 1 + g.pyr_halo) / G.cw);
     const int cy0 = max(0, Y - g.pyr_halo) / G.ch, cy1 = min(G.rows - 1, (Y + 11 + g.pyr_halo) / G.ch);
-    const int wa = cx0 >> 5, nwd = (cx1 >> 5) - wa + 1, n = (cy1 - cy0 + 1) * nwd;
-    const uint32_t* bits = b.cbits + ((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words;
+    const int wa = cx0 >> 5, wb = cx1 >> 5;
+    const uint32_t mh = 0xffffffffu << (cx0 & 31), mt = 0xffffffffu >> (31 - (cx1 & 31));
+    const uint32_t* bits = b.cbits + ((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words + wa;
     uint32_t any = 0;
-    for (int i = lane; i < n; i += 32) {
-      const int r = i / nwd, k = i - r * nwd;
-      uint32_t v = __ldcg(bits + (long long)(cy0 + r) * g.cbits_words + wa + k);
-      if (k == 0) v &= 0xffffffffu << (cx0 & 31);
-      if (k == nwd - 1) v &= 0xffffffffu >> (31 - (cx1 & 31));
-      any |= v;
+    for (int r = cy0 + lane; r <= cy1; r += 32) {   // lane per cell row
+      const uint32_t* rw = bits + (long long)r * g.cbits_words;
+      for (int k = 0; k <= wb - wa; k++) {
+        uint32_t v = __ldcg(rw + k);
+        if (k == 0) v &= mh;
+        if (k == wb - wa) v &= mt;
+        any |= v;
+      }
     }
     if (!__any_sync(0xffffffffu, any != 0u)) return;
   }
@@ -1103,9 +1115,7 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
 #pragma unroll
   for (int k = 0; k < 2; k++) {
     const uint32_t a = i1w[2 * k], c = i1w[2 * k + 1];
-    const uint32_t e = (a & 0x00ff00ffu) + ((a >> 8) & 0x00ff00ffu) + (c & 0x00ff00ffu) + ((c >> 8) & 0x00ff00ffu);
-    const uint32_t q = ((e + 0x00020002u) >> 2) & 0x00ff00ffu;
-    i2w[k] = (q & 0xffu) | ((q >> 8) & 0xff00u);
+    i2w[k] = __byte_perm(halve_w(a, c), 0u, 0x4420);
     const int y = 2 * sy + k, x = 2 * (sx * 32 + lane);
     if (y < Li2.h && x < Li2.w) store_bytes(lay + Li2.layer_off + (long long)y * Li2.pitch, x, Li2.w, i2w[k], 2);
   }
