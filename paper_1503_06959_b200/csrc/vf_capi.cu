@@ -157,6 +157,17 @@ int make_geo(const vf_config& c, Geo& g, std::vector<int>& lut)
     L.sm_off = smo; smo += align_up((long long)L.pitch * L.h + 16, 256);
     L.bm_off = bmo; bmo += align_up((long long)L.bm_words * L.h, 64);
   }
+  // Early SAT marks (k_fast): bound of the descriptor footprint of any keypoint
+  // the NMS can keep from a candidate of layer l.  The refined sigma lies
+  // between the layer's and a neighbour's (|delta| < 1, detector.py:287-297;
+  // layers 0 and NL - 1 keep theirs); the refined position is within one layer
+  // pixel of the candidate (|ox|, |oy| < 1, detector.py:207-228); + 3 covers
+  // the float candidate position (< 1 px) and the (int) truncations.
+  for (int l = 0; l < g.NL; l++) {
+    const double sg = (l >= 1 && l + 1 < g.NL) ? std::max(g.L[l].sigma, g.L[l + 1].sigma) : g.L[l].sigma;
+    g.L[l].sat_reach = (int)ceil(12.5 * sg) + 2 + (int)ceil(1.0 / g.L[l].scale) + 3;
+    g.L[l].inv_scale = (float)(1.0 / g.L[l].scale);
+  }
   g.tiles_per_stream = tb; g.bands_per_stream = bb; g.rows_per_stream = rb;
   g.layer_slab = std::max(lay, 256LL); g.sm_slab = smo; g.bm_slab_words = bmo;
   // mask grids (masking.py:139-148 cell geometry; binning masking.py:132-136)
@@ -321,6 +332,8 @@ struct vf_ctx {
   std::vector<cudaEvent_t> djoin;
   std::vector<cudaEvent_t> dfork_g;     // per stream group
   std::vector<cudaEvent_t> dsat_e;      // per describe stream: its k_sat done (VF_DESC_STAGGER)
+  std::vector<cudaEvent_t> dfast_e, dsatall_e;   // per group: k_fast done / the early k_sat done (sat_early)
+  std::vector<cudaStream_t> sat_s;               // per group: lowest-priority stream of the early k_sat (VF_SAT_LOW=1)
   std::vector<cudaStream_t> pyi_s;      // per stream group: k_pyr_i beside the main work list
   std::vector<cudaEvent_t> pyi_e;
   // CUDA graph of one step (small batches): the step's launches (all its
@@ -606,6 +619,9 @@ int vf_destroy(vf_ctx* c)
   for (size_t k = 0; k < c->dstreams.size(); k++) { cudaStreamDestroy(c->dstreams[k]); cudaEventDestroy(c->djoin[k]); }
   for (cudaEvent_t ev : c->dfork_g) cudaEventDestroy(ev);
   for (cudaEvent_t ev : c->dsat_e) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->dfast_e) cudaEventDestroy(ev);
+  for (cudaStream_t ss : c->sat_s) cudaStreamDestroy(ss);
+  for (cudaEvent_t ev : c->dsatall_e) cudaEventDestroy(ev);
   for (size_t k = 0; k < c->pyi_s.size(); k++) { cudaStreamDestroy(c->pyi_s[k]); cudaEventDestroy(c->pyi_e[k]); }
   if (c->pack.pre) cudaFree(c->pack.pre);
   if (c->pack.pre_host) cudaFreeHost(c->pack.pre_host);
@@ -717,7 +733,7 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   stage_mark(c, 1, st);
   const bool pyr4 = g.O == 4 && g.ptw == 96 && g.pth == 48 && !(g.mask_mode == 1 && !g.use_cbits);
   const int pyo_blocks = cdiv((long long)cdiv(g.W, PYO_COLS) * cdiv(g.L[2].h, 4), 8);
-  const int pyi_blocks = cdiv((long long)cdiv(g.W, PYI_COLS) * cdiv(g.L[1].h, 8), 8);
+  const int pyi_blocks = cdiv((long long)cdiv(g.W, PYI_COLS) * cdiv(g.L[1].h, 8 * PYI_RG), 8);
   if (pyr4 && g.pyr_split)
     { k_pyr_o<<<dim3(pyo_blocks, n), 256, 0, st>>>(g, b); DBG_SYNC(st, "k_pyr_o"); }
   else if (pyr4)
@@ -795,13 +811,28 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
       c->side_stage.push_back(7);
     }
   };
-  if (!prop_late) {
+  // VF_SAT_AUX=1: the early k_sat runs on the side stream, before k_propagate
+  static const bool sat_aux = getenv("VF_SAT_AUX") && atoi(getenv("VF_SAT_AUX")) != 0;
+  // Early SAT is off for large intensity-masked batches: there k_propagate
+  // already fills the NMS window, and k_sat beside it costs the NMS more than
+  // the describe stage gains (config 5: 533 vs 521 us per step).
+  const char* se_env = getenv("VF_SAT_EARLY");
+  const bool sat_early_env = se_env ? atoi(se_env) != 0
+                                    : !(g.mask_mode == 1 && (long long)g.W * g.H * n > VF_GRAPH_MAX_BYTES);
+  const bool prop_after_sat = sat_aux && sat_early_env && !prop_late;
+  if (!prop_late && !prop_after_sat) {
     launch_prop();
     cudaEventRecord(c->aux_out[gi], c->aux[gi]);
   }
   stage_mark(c, 3, st);
   const int pre_bytes = (n + 1) * (int)sizeof(int);
   b.nms_pre = !(getenv("VF_NMS_PRE") && atoi(getenv("VF_NMS_PRE")) == 0);
+  // Early SAT (default; VF_SAT_EARLY=0: the round-2 arrangement): k_fast marks
+  // the SAT tiles from footprint bounds of its candidates, so the strip SATs
+  // are built on the first describe stream beside the latency-bound NMS
+  // kernels instead of between k_nms_finish and k_desc_fused.
+  b.sat_early = sat_early_env;
+  b.sat_check = getenv("VF_SAT_CHECK") && atoi(getenv("VF_SAT_CHECK")) != 0;
   k_fast<<<c->fast_grid, 32 * FAST_WARPS, sizeof(FastWarp) * FAST_WARPS + pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_fast");
   stage_mark(c, 4, st);
   // candidate-parallel NMS: ordered candidate list, thread-per-candidate test +
@@ -809,21 +840,6 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
   b.nms_u = 1;
   b.desc_bin = 1;
   b.orient_seq = getenv("VF_ORIENT_SEQ") && atoi(getenv("VF_ORIENT_SEQ")) != 0;
-  k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
-  k_nms_test<<<c->nmst_grid, 1 << NMS_CHUNK_LOG, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_nms_test");
-  cudaStreamWaitEvent(st, c->aux_mid[gi], 0);   // propagation count (k_nms_finish), strip carries (k_sat)
-  k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
-  if (prop_late) {
-    cudaEventRecord(c->aux_in[gi], st);
-    cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
-    launch_prop();
-    cudaEventRecord(c->aux_out[gi], c->aux[gi]);
-  }
-  stage_mark(c, 5, st);
-  // Describe (descriptor.py:85-144): the strip SATs of the tiles k_nms_test
-  // marked, then k_desc_fused (warp per keypoint: theta = 0 means,
-  // orientation, rotated means, bits), for VF_DESC_PAR (default 2) stream
-  // halves on concurrent high-priority describe streams.
   static const int dpar_env = getenv("VF_DESC_PAR") ? std::max(1, std::min(2, atoi(getenv("VF_DESC_PAR")))) : 2;
   const int dpar = std::min(dpar_env, n);
   if ((int)c->dstreams.size() < 2 * (gi + 1)) {
@@ -853,6 +869,57 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return VF_ERR_CUDA;
     c->dsat_e.push_back(e);
   }
+  while ((int)c->dfast_e.size() <= gi) {
+    cudaEvent_t e0, e1;
+    if (cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) != cudaSuccess) return VF_ERR_CUDA;
+    if (cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess) { cudaEventDestroy(e0); return VF_ERR_CUDA; }
+    c->dfast_e.push_back(e0);
+    c->dsatall_e.push_back(e1);
+  }
+  if (b.sat_early) {
+    // after k_fast (tile marks) and the side stream's strip carries
+    // VF_SAT_LOW=1: on a dedicated lowest-priority stream; VF_SAT_CTAS=k: at
+    // most k CTAs per SM (the NMS kernels keep the rest of the SM)
+    // (default: low priority for multi-stream batches -- config 3 118 vs 125 us --
+    // and the describe stream for a single stream -- config 1 71 vs 75 us)
+    const char* sl = getenv("VF_SAT_LOW");
+    const bool sat_low = sl ? atoi(sl) != 0 : n > 1;
+    static const int sat_ctas = getenv("VF_SAT_CTAS") ? atoi(getenv("VF_SAT_CTAS")) : 0;
+    while ((int)c->sat_s.size() <= gi) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStream_t ss;
+      if (cudaStreamCreateWithPriority(&ss, cudaStreamNonBlocking, lo) != cudaSuccess) return VF_ERR_CUDA;
+      c->sat_s.push_back(ss);
+    }
+    cudaStream_t ds = sat_aux ? c->aux[gi] : sat_low ? c->sat_s[gi] : c->dstreams[2 * gi];
+    const int sgrid = sat_ctas > 0 ? std::min(c->sat_grid, g_num_sms * sat_ctas) : c->sat_grid;
+    cudaEventRecord(c->dfast_e[gi], st);
+    cudaStreamWaitEvent(ds, c->dfast_e[gi], 0);
+    cudaStreamWaitEvent(ds, c->aux_mid[gi], 0);
+    k_sat_list<<<n, NF_THREADS, 0, ds>>>(g, b); DBG_SYNC(ds, "k_sat_list");
+    k_sat<<<sgrid, 256, c->sat_smem, ds>>>(g, b, n, 0); DBG_SYNC(ds, "k_sat");
+    cudaEventRecord(c->dsatall_e[gi], ds);
+    if (prop_after_sat) {
+      launch_prop();
+      cudaEventRecord(c->aux_out[gi], c->aux[gi]);
+    }
+  }
+  k_nms_list<<<dim3(cdiv(g.bands_per_stream, NL_WARPS), n), 32 * NL_WARPS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_list");
+  k_nms_test<<<c->nmst_grid, 1 << NMS_CHUNK_LOG, pre_bytes, st>>>(g, b, n); DBG_SYNC(st, "k_nms_test");
+  cudaStreamWaitEvent(st, c->aux_mid[gi], 0);   // propagation count (k_nms_finish), strip carries (k_sat)
+  k_nms_finish<<<n, NF_THREADS, 0, st>>>(g, b); DBG_SYNC(st, "k_nms_finish");
+  if (prop_late) {
+    cudaEventRecord(c->aux_in[gi], st);
+    cudaStreamWaitEvent(c->aux[gi], c->aux_in[gi], 0);
+    launch_prop();
+    cudaEventRecord(c->aux_out[gi], c->aux[gi]);
+  }
+  stage_mark(c, 5, st);
+  // Describe (descriptor.py:85-144): the strip SATs of the tiles k_nms_test
+  // marked, then k_desc_fused (warp per keypoint: theta = 0 means,
+  // orientation, rotated means, bits), for VF_DESC_PAR (default 2) stream
+  // halves on concurrent high-priority describe streams.
   cudaEventRecord(c->dfork_g[gi], st);
   for (int h = 0; h < dpar; h++) {
     const int h0 = (int)((long long)n * h / dpar), h1 = (int)((long long)n * (h + 1) / dpar);
@@ -864,9 +931,13 @@ static int launch_step(vf_ctx* c, int s0, int n, cudaStream_t st)
     cudaStreamWaitEvent(ds, c->dfork_g[gi], 0);
     // staggered: half h's SAT build waits for half h-1's, so it runs beside
     // half h-1's (L1-bound) describe instead of beside its SAT build
-    if (desc_stagger && h > 0) cudaStreamWaitEvent(ds, c->dsat_e[2 * gi + h - 1], 0);
-    k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh, 0); DBG_SYNC(ds, "k_sat");
-    if (desc_stagger) cudaEventRecord(c->dsat_e[2 * gi + h], ds);
+    if (b.sat_early) {
+      cudaStreamWaitEvent(ds, c->dsatall_e[gi], 0);
+    } else {
+      if (desc_stagger && h > 0) cudaStreamWaitEvent(ds, c->dsat_e[2 * gi + h - 1], 0);
+      k_sat<<<c->sat_grid, 256, c->sat_smem, ds>>>(g, bh, nh, 0); DBG_SYNC(ds, "k_sat");
+      if (desc_stagger) cudaEventRecord(c->dsat_e[2 * gi + h], ds);
+    }
     k_desc_fused<<<c->dfused_grid, 32 * DSW, pb, ds>>>(g, bh, nh); DBG_SYNC(ds, "k_desc_fused");
     cudaEventRecord(c->djoin[2 * gi + h], ds);
   }
@@ -1040,7 +1111,7 @@ static int step_kernel_arity(const void* f)
     return 3;
   if (f == (const void*)k_binmask || f == (const void*)k_pyr_o || f == (const void*)k_pyr_i ||
       f == (const void*)k_pyramid4<PYR_FULL> || f == (const void*)k_pyramid || f == (const void*)k_propagate ||
-      f == (const void*)k_nms_list || f == (const void*)k_nms_finish)
+      f == (const void*)k_nms_list || f == (const void*)k_nms_finish || f == (const void*)k_sat_list)
     return 2;
   return 0;
 }

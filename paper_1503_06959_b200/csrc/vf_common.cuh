@@ -37,6 +37,7 @@ enum {
 #define VF_ERRBIT_CAPACITY 1
 #define VF_ERRBIT_STAGING 2
 #define VF_ERRBIT_INDEX 4
+#define VF_ERRBIT_SATMARK 8   // VF_SAT_CHECK=1: a kept keypoint's footprint tile was not marked by k_fast
 
 #define VF_ST 32   // strip-SAT tile edge and strip height (o0 pixels)
 
@@ -56,6 +57,8 @@ struct LayerGeo {
   int rc_off, cc_off;   // offsets of the row/col -> cell LUTs (per grid, see Geo)
   double scale, sigma;  // pyramid.py:122-124; detector.py:243
   double rinv_h, rinv_w;  // 1 / h, 1 / w (exact integer division by h, w)
+  int sat_reach;        // o0 pixels around floor(x / scale) that a kept keypoint's footprint box stays within
+  float inv_scale;      // 1 / scale (k_fast's early SAT-tile marks)
 };
 
 struct GridGeo {          // a cell grid of the detection mask (masking.py:30-55)
@@ -119,6 +122,8 @@ struct Bufs {
   int* nms_cnt;         // [S][4] survivors inside / outside the border margin (FrameReport)
   int nms_pre;          // k_fast drops candidates that fail the strict 3x3 test inside their tile (VF_NMS_PRE=0: off)
   int orient_seq;       // k_desc_fused: always take the sequential-sum orientation (test hook, VF_ORIENT_SEQ=1)
+  int sat_early;        // 1: k_fast marks the SAT tiles (candidate footprint bounds) and k_sat runs beside the NMS
+  int sat_check;        // VF_SAT_CHECK=1: k_nms_test asserts every kept footprint tile was marked (VF_ERRBIT_SATMARK)
   int* prop_cnt;        // [S][prop_chunks]
   int* prop_out;        // [S][prop_chunks]
   uint8_t* cells;       // [S][cell_slab]

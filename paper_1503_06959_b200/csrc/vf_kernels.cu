@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(32 * SAT_WARPS) k_sat(const __grid_constant__ 
   stream_prefix(n_streams, pre, sm_warp, [&](int sl) {
     const int s = b.s0 + sl;
     return all ? (b.ctr[s * C_NCTR + C_NDET] == 0 ? 0 : g.sat_tiles)
-               : (b.ctr[s * C_NCTR + C_NGLOB] == 0 ? 0 : b.sat_count[s]);
+               : (!b.sat_early && b.ctr[s * C_NCTR + C_NGLOB] == 0 ? 0 : b.sat_count[s]);
   });
   const int n = pre[n_streams];
   // one-tile software pipeline per warp: tile k + 1's work-list entry, carry
@@ -809,17 +809,24 @@ __global__ void __launch_bounds__(256) k_pyramid4(const __grid_constant__ Geo g,
 //   the bit mask);
 //   the per-32-column SAT row sums of the 8 rows.  Block 0 of each stream
 //   also resets the per-step counters.
-// k_pyr_i: warp per strip of 12 o0 rows x 384 o0 columns (lane: 12 columns).
+// k_pyr_i: warp per unit of 48 o0 rows x 96 o0 columns (lane: a 12 x 12 block;
+//   PYI_LPR lanes side by side, 32 / PYI_LPR row groups).  The unit is the
+//   granularity of the activity gate below: a compact unit plus its halo
+//   covers ~3x fewer o0 pixels per active cell than a 12 x 384 strip did.
 //   i0 (8 rows x 8 px per lane) by the 2/3 area resample of pyramid.py:76-94
 //   (one dp4a of a 2x2 input block with the separable (2, 1) x (2, 1)
 //   weights, then (v + 4) // 9 by multiply-shift), i1 (4 x 4), i2 (2 x 2),
-//   i3 (1) by halving.  In masked frames only strips with an active top-octave
+//   i3 (1) by halving.  In masked frames only units with an active top-octave
 //   cell within g.pyr_halo o0 pixels run (a FAST ring reaches 3 layer pixels
 //   of a gated pixel, <= 3 W / w_i3 o0 pixels); FAST reads the other pixels
 //   only for gated-off positions, whose scores are dropped.
 // ============================================================================
 #define PYO_COLS 512
-#define PYI_COLS 384
+#ifndef PYI_LPR
+#define PYI_LPR 8                 // lanes per row group of a k_pyr_i warp unit
+#endif
+#define PYI_COLS (12 * PYI_LPR)   // unit width (o0 columns)
+#define PYI_RG (32 / PYI_LPR)     // row groups (12 o0 rows each) per unit
 __device__ __forceinline__ void store_bytes(uint8_t* row, int x, int valid, uint32_t w, int n)
 {
   // n bytes of w at row[x..x+n) (x aligned to n), clipped to `valid` columns
@@ -1007,14 +1014,17 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
   const int strip = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int sy = strip / nsx, sx = strip - sy * nsx;
   const LayerGeo& Li0 = g.L[1];
-  if (sy * 8 >= Li0.h) return;
-  const int X = sx * PYI_COLS + 12 * lane, Y = sy * 12;
+  if (sy * PYI_RG * 8 >= Li0.h) return;
+  // the lane's 12 x 12 o0 block: row group ry (12 o0 rows -> 8 i0 rows),
+  // column group cx (12 o0 columns -> 8 i0 columns)
+  const int ry = sy * PYI_RG + lane / PYI_LPR, cx = sx * PYI_LPR + lane % PYI_LPR;
+  const int X = 12 * cx, Y = 12 * ry;
   if (g.use_cbits && use_mask(g, b, s)) {
-    // any active top-octave cell within pyr_halo o0 pixels of the strip?
+    // any active top-octave cell within pyr_halo o0 pixels of the unit?
     const GridGeo& G = g.grid[0];
-    const int X0 = sx * PYI_COLS;
+    const int X0 = sx * PYI_COLS, Y0 = sy * PYI_RG * 12;
     const int cx0 = max(0, X0 - g.pyr_halo) / G.cw, cx1 = min(G.cols - 1, (X0 + PYI_COLS - 1 + g.pyr_halo) / G.cw);
-    const int cy0 = max(0, Y - g.pyr_halo) / G.ch, cy1 = min(G.rows - 1, (Y + 11 + g.pyr_halo) / G.ch);
+    const int cy0 = max(0, Y0 - g.pyr_halo) / G.ch, cy1 = min(G.rows - 1, (Y0 + 12 * PYI_RG - 1 + g.pyr_halo) / G.ch);
     const int wa = cx0 >> 5, wb = cx1 >> 5;
     const uint32_t mh = 0xffffffffu << (cx0 & 31), mt = 0xffffffffu >> (31 - (cx1 & 31));
     const uint32_t* bits = b.cbits + ((long long)s * 2 + (stream_epoch(b, s) & 1)) * G.rows * g.cbits_words + wa;
@@ -1030,6 +1040,7 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
     }
     if (!__any_sync(0xffffffffu, any != 0u)) return;
   }
+  if (ry * 8 >= Li0.h) return;
   // ---- 12 o0 rows x 12 columns of this lane (3 words per row) ----
   const uint8_t* src = b.frames + (long long)(s - b.s0) * b.frame_stride + (long long)Y * b.frame_pitch + X;
   const int pitch = (int)b.frame_pitch;
@@ -1084,10 +1095,10 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
     }
   }
   uint8_t* lay = b.layers + (long long)s * g.layer_slab;
-  const int xi0 = 8 * (sx * 32 + lane);   // = 2 X / 3
+  const int xi0 = 8 * cx;   // = 2 X / 3
   {
-    uint8_t* row = lay + Li0.layer_off + (long long)(8 * sy) * Li0.pitch;
-    const int n0 = min(8, Li0.h - 8 * sy);
+    uint8_t* row = lay + Li0.layer_off + (long long)(8 * ry) * Li0.pitch;
+    const int n0 = min(8, Li0.h - 8 * ry);
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       if (k < n0 && xi0 < Li0.w) {
@@ -1106,7 +1117,7 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     i1w[k] = halve4(make_uint2(i0w[2 * k][0], i0w[2 * k][1]), make_uint2(i0w[2 * k + 1][0], i0w[2 * k + 1][1]));
-    const int y = 4 * sy + k, x = 4 * (sx * 32 + lane);
+    const int y = 4 * ry + k, x = 4 * cx;
     if (y < Li1.h && x < Li1.w) store_bytes(lay + Li1.layer_off + (long long)y * Li1.pitch, x, Li1.w, i1w[k], 4);
   }
   // ---- i2: 2 rows x 2 px ----
@@ -1116,12 +1127,12 @@ __global__ void __launch_bounds__(256) k_pyr_i(const __grid_constant__ Geo g, co
   for (int k = 0; k < 2; k++) {
     const uint32_t a = i1w[2 * k], c = i1w[2 * k + 1];
     i2w[k] = __byte_perm(halve_w(a, c), 0u, 0x4420);
-    const int y = 2 * sy + k, x = 2 * (sx * 32 + lane);
+    const int y = 2 * ry + k, x = 2 * cx;
     if (y < Li2.h && x < Li2.w) store_bytes(lay + Li2.layer_off + (long long)y * Li2.pitch, x, Li2.w, i2w[k], 2);
   }
   // ---- i3: 1 px ----
   const LayerGeo& Li3 = g.L[7];
-  const int y3 = sy, x3 = sx * 32 + lane;
+  const int y3 = ry, x3 = cx;
   if (y3 < Li3.h && x3 < Li3.w) {
     const uint32_t sum = (i2w[0] & 0xffu) + (i2w[0] >> 8) + (i2w[1] & 0xffu) + (i2w[1] >> 8);
     lay[Li3.layer_off + (long long)y3 * Li3.pitch + x3] = (uint8_t)((sum + 2) >> 2);
@@ -1404,6 +1415,35 @@ __device__ __forceinline__ int fast_best(const uint32_t w[8], int c)
   return max(max(bmax - c, c - dmin), 0);
 }
 
+// OR the SAT tiles covering the o0 pixel box [xa, xb] x [ya, yb] (clamped to
+// the frame) into the stream's tile bitmap: one atomic per tile row and word.
+__device__ __forceinline__ void mark_sat_box(const Geo& g, const Bufs& b, int s, int xa, int xb, int ya, int yb)
+{
+  xa = max(0, xa); xb = min(g.W - 1, xb);
+  ya = max(0, ya); yb = min(g.H - 1, yb);
+  const int txa = xa / VF_ST, txb = xb / VF_ST, tya = ya / VF_ST, tyb = yb / VF_ST;
+  const int wa = txa >> 5, wb = txb >> 5;
+  unsigned* bits = b.sat_bits + (long long)s * g.sty * g.stw_words;
+  for (int ty = tya; ty <= tyb; ty++)
+    for (int w = wa; w <= wb; w++) {
+      const int lo = max(txa, 32 * w) - 32 * w, hi = min(txb, 32 * w + 31) - 32 * w;
+      const unsigned m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+      atomicOr(bits + ty * g.stw_words + w, m);
+    }
+}
+
+// True when every SAT tile of the box is set in the bitmap (VF_SAT_CHECK).
+__device__ __forceinline__ bool sat_box_marked(const Geo& g, const Bufs& b, int s, int xa, int xb, int ya, int yb)
+{
+  xa = max(0, xa); xb = min(g.W - 1, xb);
+  ya = max(0, ya); yb = min(g.H - 1, yb);
+  const unsigned* bits = b.sat_bits + (long long)s * g.sty * g.stw_words;
+  bool ok = true;
+  for (int ty = ya / VF_ST; ty <= yb / VF_ST; ty++)
+    for (int tx = xa / VF_ST; tx <= xb / VF_ST; tx++) ok &= (__ldcg(bits + ty * g.stw_words + (tx >> 5)) >> (tx & 31)) & 1u;
+  return ok;
+}
+
 // Warp per tile (no block barriers): each warp stages its tile, runs the
 // pre-test, scores its queue and stores, with __syncwarp only.
 #define FAST_WARPS 8
@@ -1649,6 +1689,30 @@ __global__ void __launch_bounds__(32 * FAST_WARPS) k_fast(const __grid_constant_
       const uint32_t word = word_all & ~fw.drop[r][kw];
       if (y < h && x0 + 32 * kw < w)
         b.bitmaps[(long long)s * g.bm_slab_words + Lg.bm_off + (long long)y * Lg.bm_words + 4 * tx + kw] = word;
+      if (b.sat_early && __any_sync(0xffffffffu, word != 0u)) {
+        // SAT tiles any keypoint kept from this tile's candidates can read: the
+        // bounding box of the candidates, widened by LayerGeo.sat_reach (float
+        // positions are within 1 pixel, inside its margin).  One (tile row,
+        // word) pair per lane.
+        const bool hasc = word != 0u;
+        const int xl = __reduce_min_sync(0xffffffffu, hasc ? x0 + 32 * kw + __ffs(word) - 1 : INT_MAX);
+        const int xh = __reduce_max_sync(0xffffffffu, hasc ? x0 + 32 * kw + 31 - __clz(word) : -1);
+        const int yl = __reduce_min_sync(0xffffffffu, hasc ? y : INT_MAX);
+        const int yh = __reduce_max_sync(0xffffffffu, hasc ? y : -1);
+        const float inv = Lg.inv_scale;
+        const int F = Lg.sat_reach;
+        const int xa = max(0, (int)((float)xl * inv) - F), xb = min(g.W - 1, (int)((float)xh * inv) + F);
+        const int ya = max(0, (int)((float)yl * inv) - F), yb = min(g.H - 1, (int)((float)yh * inv) + F);
+        const int txa = xa / VF_ST, txb = xb / VF_ST, tya = ya / VF_ST, tyb = yb / VF_ST;
+        const int wa = txa >> 5, nw = (txb >> 5) - wa + 1, np = (tyb - tya + 1) * nw;
+        unsigned* bits = b.sat_bits + (long long)s * g.sty * g.stw_words;
+        for (int i = lane; i < np; i += 32) {
+          const int ty = tya + i / nw, wd = wa + i % nw;
+          const int lo = max(txa, 32 * wd) - 32 * wd, hi = min(txb, 32 * wd + 31) - 32 * wd;
+          const unsigned m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+          atomicOr(bits + ty * g.stw_words + wd, m);   // no return value: fire and forget
+        }
+      }
       int n = __popc(word), na = __popc(word_all);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1863,24 +1927,13 @@ __device__ NmsOut nms_refine(const Geo& g, const Bufs& b, int s, int um, int l, 
 __device__ __forceinline__ void mark_sat_tiles(const Geo& g, const Bufs& b, int s, double x, double y, double sg,
                                                int epoch)
 {
-  // footprint bound of the 60 boxes (|p| <= 10.8, radius <= 1.69 sigma): tile
-  // rows x column runs OR-ed into the stream's tile bitmap, which k_sat reads
+  // footprint bound of the 60 boxes (|p| <= 10.8, radius <= 1.69 sigma)
   (void)epoch;
   const int F = (int)ceil(12.5 * sg) + 2;
   const int xi = (int)x, yi = (int)y;
-  const int xa = max(0, xi - F), xb = min(g.W - 1, xi + F + 1);
-  const int ya = max(0, yi - F), yb = min(g.H - 1, yi + F + 1);
-  const int txa = xa / VF_ST, txb = xb / VF_ST, tya = ya / VF_ST, tyb = yb / VF_ST;
-  const int wa = txa >> 5, wb = txb >> 5;
-  unsigned* bits = b.sat_bits + (long long)s * g.sty * g.stw_words;
-  // set the footprint's tiles in the stream's bitmap (no return value is
-  // consumed: k_sat lists the set tiles itself)
-  for (int ty = tya; ty <= tyb; ty++)
-    for (int w = wa; w <= wb; w++) {
-      const int lo = max(txa, 32 * w) - 32 * w, hi = min(txb, 32 * w + 31) - 32 * w;
-      const unsigned m = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
-      atomicOr(bits + ty * g.stw_words + w, m);
-    }
+  if (!b.sat_early) mark_sat_box(g, b, s, xi - F, xi + F + 1, yi - F, yi + F + 1);
+  else if (b.sat_check && !sat_box_marked(g, b, s, xi - F, xi + F + 1, yi - F, yi + F + 1))
+    atomicOr(b.ctr + s * C_NCTR + C_ERR, VF_ERRBIT_SATMARK);
 }
 
 // Warp-collective, at k_nms_test's kept-keypoint site: append the kept
@@ -1904,6 +1957,7 @@ __device__ __forceinline__ void desc_list_kept(const Geo& g, const Bufs& b, int 
 
 // Block-wide exclusive scan (blockDim.x = NF_THREADS) of one value per thread.
 #define NF_THREADS 256
+#define NMS_CHUNK_THREADS (1 << NMS_CHUNK_LOG)
 __device__ __forceinline__ int block_excl_scan(int v, int& total, int* sm)
 {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -2160,7 +2214,133 @@ __global__ void __launch_bounds__(32 * NL_WARPS) k_nms_list(const __grid_constan
   }
 }
 
-#define NMS_CHUNK_THREADS (1 << NMS_CHUNK_LOG)
+// The set tiles of a stream's SAT-tile bitmap, in bitmap order -> the k_sat
+// work list (whole CTA of NF_THREADS threads).
+__device__ __forceinline__ void sat_work_list(const Geo& g, const Bufs& b, int s, int* sm)
+{
+  const int tid = threadIdx.x;
+  const int nw = g.sty * g.stw_words;
+  const unsigned* bits = b.sat_bits + (long long)s * nw;
+  int* work = b.sat_work + (long long)s * g.sat_tiles;
+  int cnt = 0;
+  for (int w0 = 0; w0 < nw; w0 += NF_THREADS) {
+    const int wi = w0 + tid;
+    unsigned v = wi < nw ? __ldcg(bits + wi) : 0u;
+    int tot;
+    int pos = cnt + block_excl_scan(__popc(v), tot, sm);
+    const int ty = wi / g.stw_words, t0 = ty * g.stx + 32 * (wi - ty * g.stw_words);
+    for (; v; v &= v - 1u) work[pos++] = t0 + __ffs(v) - 1;
+    cnt += tot;
+  }
+  if (tid == 0) b.sat_count[s] = cnt;
+}
+
+// Early SAT (b.sat_early): the work list of the tiles k_fast marked, one CTA
+// per stream, launched on the describe stream right after k_fast.
+__global__ void __launch_bounds__(NF_THREADS) k_sat_list(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  __shared__ int sm[NF_THREADS / 32];
+  sat_work_list(g, b, b.s0 + blockIdx.x, sm);
+}
+
+// After k_nms (stream order), one CTA per stream: band output offsets (scan
+// of the kept counts in band order), the SAT-tile work list (the bitmap's set
+// tiles in bitmap order) and the FrameReport.  Every load is issued up front.
+__device__ __forceinline__ void nms_finish_stream(const Geo& g, const Bufs& b, int s, int* sm, int (*red)[NF_THREADS / 32])
+{
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int um = use_mask(g, b, s);
+  int n_det, n_drop = 0, n_surv = 0;
+  if (b.desc_bin) {
+    // ---- pipeline (k_nms_test): chunk kept counts -> output offsets, in place ----
+    const int* ctr = b.ctr + s * C_NCTR;
+    const int nch = (ctr[C_ERR] & VF_ERRBIT_STAGING) ? 0 : (ctr[C_STAGE] + NMS_CHUNK_THREADS - 1) >> NMS_CHUNK_LOG;
+    int* co = b.chunk_off + (long long)s * g.nms_chunks;
+    int carry = 0;
+    for (int c0 = 0; c0 < nch; c0 += NF_THREADS) {
+      const int i = c0 + tid;
+      const int v = i < nch ? __ldcg(co + i) : 0;
+      int tot;
+      const int ex = block_excl_scan(v, tot, sm);
+      if (i < nch) co[i] = carry + ex;
+      carry += tot;
+    }
+    n_det = carry;
+    if (tid == 0) {
+      const int n_ok = __ldcg(b.nms_cnt + 4 * s), n_dr = __ldcg(b.nms_cnt + 4 * s + 1);
+      n_drop = n_dr;
+      n_surv = n_ok + n_dr;
+    }
+  } else {
+    // ---- stand-alone (k_nms): unit offsets, thread t owns units [t * per, t * per + per) ----
+    const int nb = g.bands_per_stream * b.nms_u;   // NMS units, (layer, y) order
+    const int4* rec = reinterpret_cast<const int4*>(b.unit_rec) + (long long)s * nb;
+    int* bout = b.unit_out + (long long)s * nb;
+    const int per = (nb + NF_THREADS - 1) / NF_THREADS;
+    int kept = 0;
+    for (int k = 0; k < per; k++) {
+      const int i = tid * per + k;
+      if (i < nb) {
+        const int4 r = __ldcg(rec + i);
+        kept += r.y;
+        n_drop += r.w;
+        n_surv += r.z + r.w;
+      }
+    }
+    int run = block_excl_scan(kept, n_det, sm);
+    for (int k = 0; k < per; k++) {
+      const int i = tid * per + k;
+      if (i < nb) {
+        bout[i] = run;
+        run += __ldcg(rec + i).y;
+      }
+    }
+  }
+  // ---- SAT tiles marked by the stream's bands (k_nms ORs footprints into
+  // the bitmap) -> the k_sat work list ----
+  if ((um || b.desc_bin) && !b.sat_early) sat_work_list(g, b, s, sm);
+  // ---- FrameReport ----
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_drop += __shfl_down_sync(0xffffffffu, n_drop, o);
+    n_surv += __shfl_down_sync(0xffffffffu, n_surv, o);
+  }
+  if (lane == 0) { red[0][wid] = n_drop; red[1][wid] = n_surv; }
+  __syncthreads();
+  if (tid == 0) {
+    n_drop = 0;
+    n_surv = 0;
+    for (int w = 0; w < NF_THREADS / 32; w++) { n_drop += red[0][w]; n_surv += red[1][w]; }
+    // propagated total: scanned by k_worklist (joined before k_nms)
+    const int n_prop = um ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
+    int* ctr = b.ctr + s * C_NCTR;
+    int n_total = n_det + n_prop;
+    int n_desc = n_det;   // detected records the describe kernels write
+    if (n_total > g.kp_cap) {
+      // overflow: flagged (vf_process_checked grows the capacity and replays);
+      // the describe writes are clamped so they cannot overlap the propagated tail
+      ctr[C_ERR] |= VF_ERRBIT_CAPACITY;
+      n_total = g.kp_cap;
+      n_desc = max(0, g.kp_cap - n_prop);
+    }
+    ctr[C_NDET] = n_desc; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
+    ctr[C_NSURV] = n_surv;
+    ctr[C_TICKET] = 0;
+    const double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
+    double* rp = b.report + (long long)s * 16;
+    rp[0] = n_det; rp[1] = n_prop; rp[2] = n_total; rp[3] = n_drop; rp[4] = cov;
+    rp[5] = ctr[C_FRAME]; rp[6] = n_surv; rp[7] = __ldcg(&ctr[C_NCAND]);
+    rp[8] += n_det; rp[9] += n_total; rp[10] += cov; rp[11] += 1.0;
+  }
+}
+
+__global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
+{
+  __shared__ int sm[NF_THREADS / 32];
+  __shared__ int red[2][NF_THREADS / 32];
+  nms_finish_stream(g, b, b.s0 + blockIdx.x, sm, red);
+}
+
 #ifndef NMS_TEST_MINB
 #define NMS_TEST_MINB 4
 #endif
@@ -2228,113 +2408,6 @@ __global__ void __launch_bounds__(NMS_CHUNK_THREADS, NMS_TEST_MINB) k_nms_test(c
   }
 }
 
-// After k_nms (stream order), one CTA per stream: band output offsets (scan
-// of the kept counts in band order), the SAT-tile work list (the bitmap's set
-// tiles in bitmap order) and the FrameReport.  Every load is issued up front.
-__global__ void __launch_bounds__(NF_THREADS) k_nms_finish(const __grid_constant__ Geo g, const __grid_constant__ Bufs b)
-{
-  __shared__ int sm[NF_THREADS / 32];
-  __shared__ int red[2][NF_THREADS / 32];
-  const int s = b.s0 + blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int um = use_mask(g, b, s);
-  int n_det, n_drop = 0, n_surv = 0;
-  if (b.desc_bin) {
-    // ---- pipeline (k_nms_test): chunk kept counts -> output offsets, in place ----
-    const int* ctr = b.ctr + s * C_NCTR;
-    const int nch = (ctr[C_ERR] & VF_ERRBIT_STAGING) ? 0 : (ctr[C_STAGE] + NMS_CHUNK_THREADS - 1) >> NMS_CHUNK_LOG;
-    int* co = b.chunk_off + (long long)s * g.nms_chunks;
-    int carry = 0;
-    for (int c0 = 0; c0 < nch; c0 += NF_THREADS) {
-      const int i = c0 + tid;
-      const int v = i < nch ? __ldcg(co + i) : 0;
-      int tot;
-      const int ex = block_excl_scan(v, tot, sm);
-      if (i < nch) co[i] = carry + ex;
-      carry += tot;
-    }
-    n_det = carry;
-    if (tid == 0) {
-      const int n_ok = __ldcg(b.nms_cnt + 4 * s), n_dr = __ldcg(b.nms_cnt + 4 * s + 1);
-      n_drop = n_dr;
-      n_surv = n_ok + n_dr;
-    }
-  } else {
-    // ---- stand-alone (k_nms): unit offsets, thread t owns units [t * per, t * per + per) ----
-    const int nb = g.bands_per_stream * b.nms_u;   // NMS units, (layer, y) order
-    const int4* rec = reinterpret_cast<const int4*>(b.unit_rec) + (long long)s * nb;
-    int* bout = b.unit_out + (long long)s * nb;
-    const int per = (nb + NF_THREADS - 1) / NF_THREADS;
-    int kept = 0;
-    for (int k = 0; k < per; k++) {
-      const int i = tid * per + k;
-      if (i < nb) {
-        const int4 r = __ldcg(rec + i);
-        kept += r.y;
-        n_drop += r.w;
-        n_surv += r.z + r.w;
-      }
-    }
-    int run = block_excl_scan(kept, n_det, sm);
-    for (int k = 0; k < per; k++) {
-      const int i = tid * per + k;
-      if (i < nb) {
-        bout[i] = run;
-        run += __ldcg(rec + i).y;
-      }
-    }
-  }
-  // ---- SAT tiles marked by the stream's bands (k_nms ORs footprints into
-  // the bitmap) -> the k_sat work list ----
-  if (um || b.desc_bin) {
-    const int nw = g.sty * g.stw_words;
-    const unsigned* bits = b.sat_bits + (long long)s * nw;
-    int* work = b.sat_work + (long long)s * g.sat_tiles;
-    int cnt = 0;
-    for (int w0 = 0; w0 < nw; w0 += NF_THREADS) {
-      const int wi = w0 + tid;
-      unsigned v = wi < nw ? __ldcg(bits + wi) : 0u;
-      int tot;
-      int pos = cnt + block_excl_scan(__popc(v), tot, sm);
-      const int ty = wi / g.stw_words, t0 = ty * g.stx + 32 * (wi - ty * g.stw_words);
-      for (; v; v &= v - 1u) work[pos++] = t0 + __ffs(v) - 1;
-      cnt += tot;
-    }
-    if (tid == 0) b.sat_count[s] = cnt;
-  }
-  // ---- FrameReport ----
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    n_drop += __shfl_down_sync(0xffffffffu, n_drop, o);
-    n_surv += __shfl_down_sync(0xffffffffu, n_surv, o);
-  }
-  if (lane == 0) { red[0][wid] = n_drop; red[1][wid] = n_surv; }
-  __syncthreads();
-  if (tid == 0) {
-    n_drop = 0;
-    n_surv = 0;
-    for (int w = 0; w < NF_THREADS / 32; w++) { n_drop += red[0][w]; n_surv += red[1][w]; }
-    // propagated total: scanned by k_worklist (joined before k_nms)
-    const int n_prop = um ? __ldcg(b.ctr + s * C_NCTR + C_NPROP) : 0;
-    int* ctr = b.ctr + s * C_NCTR;
-    int n_total = n_det + n_prop;
-    int n_desc = n_det;   // detected records the describe kernels write
-    if (n_total > g.kp_cap) {
-      // overflow: flagged (vf_process_checked grows the capacity and replays);
-      // the describe writes are clamped so they cannot overlap the propagated tail
-      ctr[C_ERR] |= VF_ERRBIT_CAPACITY;
-      n_total = g.kp_cap;
-      n_desc = max(0, g.kp_cap - n_prop);
-    }
-    ctr[C_NDET] = n_desc; ctr[C_NPROP] = n_prop; ctr[C_NTOTAL] = n_total; ctr[C_NDROP] = n_drop;
-    ctr[C_NSURV] = n_surv;
-    ctr[C_TICKET] = 0;
-    const double cov = um ? (double)__ldcg(b.cov + s) / ((double)g.W * (double)g.H) : 1.0;   // masking.py:44-46
-    double* rp = b.report + (long long)s * 16;
-    rp[0] = n_det; rp[1] = n_prop; rp[2] = n_total; rp[3] = n_drop; rp[4] = cov;
-    rp[5] = ctr[C_FRAME]; rp[6] = n_surv; rp[7] = __ldcg(&ctr[C_NCAND]);
-    rp[8] += n_det; rp[9] += n_total; rp[10] += cov; rp[11] += 1.0;
-  }
-}
 
 // ============================================================================
 // k_describe: descriptor.py:85-144 + pipeline.py:164-170 for kept keypoints,

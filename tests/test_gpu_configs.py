@@ -107,3 +107,26 @@ def test_full_size_determinism_and_gating_identity():
                 assert np.array_equal(a[s][n][k], b[s][n][k])
                 assert np.array_equal(c[s][n][k], d[s][n][k])
             assert rd[s][n].coverage == 1.0
+
+
+@pytest.mark.parametrize("cfg_id,mode,n_frames,streams", [(5, "intensity", 6, range(6)), (5, "none", 3, range(3)),
+                                                           (4, "intensity", 3, None), (2, "intensity", 10, None)])
+def test_early_sat_marks_cover_every_kept_footprint(cfg_id, mode, n_frames, streams, monkeypatch):
+    """Early SAT (k_fast marks SAT tiles from footprint bounds of its candidates, k_sat runs beside the
+    NMS): with VF_SAT_CHECK=1 k_nms_test asserts on the device that every tile a kept keypoint's
+    descriptor reads was marked (a miss sets a sticky error bit and the fetch raises); the features
+    must equal the oracle's, and those of the late arrangement (VF_SAT_EARLY=0), bit for bit."""
+    from paper_1503_06959_b200 import scenes
+
+    kw = {"streams": streams} if streams is not None else {}
+    frames = scenes.generate(scenes.CONFIGS[cfg_id], n_frames, **kw).numpy()
+    monkeypatch.setenv("VF_SAT_EARLY", "1")
+    monkeypatch.setenv("VF_SAT_CHECK", "1")
+    _check_vs_oracle(frames, mode, f"config{cfg_id}/{mode}/early-sat")
+    early, _ = _run_batch(frames, mode)
+    monkeypatch.setenv("VF_SAT_EARLY", "0")
+    late, _ = _run_batch(frames, mode)
+    for s in range(frames.shape[0]):
+        for n in range(n_frames):
+            for k in ("x", "y", "sigma", "theta", "score", "origin", "age", "desc"):
+                assert np.array_equal(early[s][n][k], late[s][n][k]), (s, n, k)

@@ -6,7 +6,8 @@ between them shows up as a result that depends on the launch arrangement.
 Every arrangement below -- CUDA graph or eager launches, one or two describe
 halves (concurrent or staggered), one or three stream groups, the priority
 stream on or off, the side chain early or late, the k_fast NMS prefilter on or
-off, the certified or the sequential orientation -- must give bit-identical
+off, the certified or the sequential orientation, the strip SATs built beside
+the NMS (early) or after it -- must give bit-identical
 features (theta of the sequential orientation within 1e-9) and equal the CPU
 oracle over 8 frames of 6 config-5 streams in each mode, each arrangement in a
 fresh process (some knobs are read once per process)."""
@@ -38,6 +39,16 @@ ARRANGEMENTS = {
     "no_stagger": {"VF_DESC_STAGGER": "0", "VF_GRAPHS": "0"},
     "no_nms_prefilter": {"VF_NMS_PRE": "0"},
     "orient_seq": {"VF_ORIENT_SEQ": "1"},
+    # early SAT (k_sat beside the NMS, tiles marked by k_fast) on / off, on the
+    # describe stream, a low-priority stream or the side stream; the device
+    # assertion that the early marks cover every kept footprint
+    "sat_late": {"VF_SAT_EARLY": "0", "VF_GRAPHS": "0"},
+    "sat_late_graph": {"VF_SAT_EARLY": "0"},
+    "sat_early_checked": {"VF_SAT_EARLY": "1", "VF_SAT_CHECK": "1"},
+    "sat_early_high": {"VF_SAT_EARLY": "1", "VF_SAT_LOW": "0", "VF_GRAPHS": "0"},
+    "sat_early_low": {"VF_SAT_EARLY": "1", "VF_SAT_LOW": "1", "VF_GRAPHS": "0"},
+    "sat_early_side": {"VF_SAT_EARLY": "1", "VF_SAT_AUX": "1", "VF_GRAPHS": "0"},
+    "sat_early_one_cta": {"VF_SAT_EARLY": "1", "VF_SAT_CTAS": "1"},
 }
 
 CHILD = r"""
