@@ -2949,7 +2949,7 @@ __global__ void __launch_bounds__(256, 4) k_propagate(const __grid_constant__ Ge
 __global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
                                               int n_streams, int buf_override, double* px, double* py, double* ps,
                                               double* pt, double* pv, uint8_t* po, int* pa, uint8_t* pd,
-                                              int* pre_out, long long pack_cap)
+                                              int* pre_out, long long pack_cap, int* err_out)
 {
   __shared__ int sm_warp[32];
   extern __shared__ int pre[];
@@ -2959,7 +2959,10 @@ __global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, con
     return ctr[C_NFEAT0 + buf];
   });
   if (blockIdx.x == 0)
-    for (int s = threadIdx.x; s <= n_streams; s += blockDim.x) pre_out[s] = pre[s];
+    for (int s = threadIdx.x; s <= n_streams; s += blockDim.x) {
+      pre_out[s] = pre[s];
+      if (err_out && s < n_streams) err_out[s] = b.ctr[s * C_NCTR + C_ERR];   // sticky capacity flags
+    }
   const int total = pre[n_streams];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total && i < pack_cap;
        i += (long long)gridDim.x * blockDim.x) {
@@ -2988,7 +2991,8 @@ __global__ void __launch_bounds__(256) k_pack(const __grid_constant__ Geo g, con
 __global__ void __launch_bounds__(256) k_pack_delta(const __grid_constant__ Geo g, const __grid_constant__ Bufs b,
                                                     int n_streams, double* px, double* py, double* ps, double* pt,
                                                     double* pv, uint8_t* pd, uint32_t* pk, int* pre_det,
-                                                    int* pre_kw, int* counts, long long cap, long long kcap)
+                                                    int* pre_kw, int* counts, long long cap, long long kcap,
+                                                    int* err_out)
 {
   __shared__ int sm_warp[32];
   extern __shared__ int pre[];   // [2][n_streams + 1]: detected, keep words
@@ -3007,6 +3011,7 @@ __global__ void __launch_bounds__(256) k_pack_delta(const __grid_constant__ Geo 
       if (s < n_streams) {
         const int* ctr = b.ctr + s * C_NCTR;
         counts[3 * s] = ctr[C_NDET]; counts[3 * s + 1] = ctr[C_NPROP]; counts[3 * s + 2] = nbits(s);
+        if (err_out) err_out[s] = ctr[C_ERR];   // sticky capacity flags
       }
     }
   const int total = pre[n_streams], words = pw[n_streams];
@@ -3028,6 +3033,30 @@ __global__ void __launch_bounds__(256) k_pack_delta(const __grid_constant__ Geo 
     uint32_t v = b.keep_bits[(long long)s * b.keep_words + k];
     if (32 * k + 32 > nb) v &= (1u << (nb - 32 * k)) - 1u;   // bits past the list (last word)
     pk[i] = v;
+  }
+}
+
+// ============================================================================
+// k_copy_out: the packed fields of a step -> the caller's host arrays in one
+// launch (vf_pipeline_collect*, when every destination is pinned host memory
+// the device can address): the SMs write over PCIe, so a step's result costs
+// one launch instead of one DMA copy (~10 us of fixed cost each) per field.
+// ============================================================================
+struct CopySeg { const uint8_t* src; uint8_t* dst; long long bytes; };
+struct CopySegs { CopySeg seg[8]; int n; };
+__global__ void __launch_bounds__(256) k_copy_out(const __grid_constant__ CopySegs cs)
+{
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+  for (int k = 0; k < cs.n; k++) {
+    const CopySeg sg = cs.seg[k];
+    if (((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 15) == 0) {
+      const long long nv = sg.bytes >> 4;
+      for (long long i = tid; i < nv; i += nt)
+        reinterpret_cast<uint4*>(sg.dst)[i] = __ldcs(reinterpret_cast<const uint4*>(sg.src) + i);
+      for (long long i = (nv << 4) + tid; i < sg.bytes; i += nt) sg.dst[i] = sg.src[i];
+    } else {
+      for (long long i = tid; i < sg.bytes; i += nt) sg.dst[i] = sg.src[i];
+    }
   }
 }
 
