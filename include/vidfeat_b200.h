@@ -150,9 +150,11 @@ int vf_fetch_features(vf_ctx *ctx, int n_streams, int64_t cap, double *x, double
  * host frames to the device on a copy stream, runs the path and packs the
  * features on a compute stream; collect returns the oldest submitted step's
  * features (all streams, packed as in vf_fetch_features) after its
- * device->host copy on a second copy stream.  At most two steps may be in
- * flight (submit, submit, collect, submit, collect, ...), so H2D of step n+1,
- * compute of step n and D2H of step n-1 overlap.  Stream-ordered with respect
+ * device->host copy on a second copy stream.  At most three steps may be in
+ * flight (submit, submit, submit, collect, submit, collect, ...; a fourth
+ * submit returns VF_ERR_ARG), so the H2D of step n+2 is already queued while
+ * step n+1 computes and step n's result is copied out: the slowest of the
+ * three sets the pace.  Two in flight (submit, submit, collect, ...) works too.  Stream-ordered with respect
  * to the context's own streams only; not to be mixed with vf_process on the
  * same context. */
 int vf_pipeline_submit(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,

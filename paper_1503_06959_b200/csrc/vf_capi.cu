@@ -256,6 +256,11 @@ int cuda_status(cudaError_t e)
 
 }  // namespace
 
+// Steps the pipelined API keeps in flight (vf_pipeline_submit before a collect
+// is due): with 3, the upload of step n + 2 is queued while step n + 1 computes
+// and step n's result is copied out, so the slowest of the three sets the pace.
+#define VF_PIPE_DEPTH 3
+
 struct vf_ctx {
   vf_config cfg;
   Geo g;
@@ -287,29 +292,29 @@ struct vf_ctx {
   struct Pipe {
     bool init = false;
     cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-    uint8_t* frames[2] = {nullptr, nullptr};
+    uint8_t* frames[VF_PIPE_DEPTH] = {};
     long long frame_bytes = 0;
-    double *x[2], *y[2], *s[2], *t[2], *v[2];
-    uint8_t *o[2], *d[2];
-    int* a[2];
-    int* pre[2];
-    int* pre_host[2];
-    int* meta[2] = {nullptr, nullptr};        // device blob: pre | kpre | cnt | err (pointers below point into it)
-    int* meta_host[2] = {nullptr, nullptr};   // pinned copy, one D2H per step
-    int* err[2] = {nullptr, nullptr};
-    int* err_host[2] = {nullptr, nullptr};    // sticky capacity flags of each stream after the step
+    double *x[VF_PIPE_DEPTH], *y[VF_PIPE_DEPTH], *s[VF_PIPE_DEPTH], *t[VF_PIPE_DEPTH], *v[VF_PIPE_DEPTH];
+    uint8_t *o[VF_PIPE_DEPTH], *d[VF_PIPE_DEPTH];
+    int* a[VF_PIPE_DEPTH];
+    int* pre[VF_PIPE_DEPTH];
+    int* pre_host[VF_PIPE_DEPTH];
+    int* meta[VF_PIPE_DEPTH] = {};        // device blob: pre | kpre | cnt | err (pointers below point into it)
+    int* meta_host[VF_PIPE_DEPTH] = {};   // pinned copy, one D2H per step
+    int* err[VF_PIPE_DEPTH] = {};
+    int* err_host[VF_PIPE_DEPTH] = {};    // sticky capacity flags of each stream after the step
     size_t meta_ints = 0;
     long long cap = 0;
-    cudaEvent_t ev_h2d[2], ev_comp[2], ev_pre[2], ev_d2h[2];
+    cudaEvent_t ev_h2d[VF_PIPE_DEPTH], ev_comp[VF_PIPE_DEPTH], ev_pre[VF_PIPE_DEPTH], ev_d2h[VF_PIPE_DEPTH];
     long long submitted = 0, collected = 0;
-    int n_streams[2];
+    int n_streams[VF_PIPE_DEPTH];
     // delta results (vf_pipeline_set_delta): keep masks of the previous lists
     bool delta = false;
-    uint32_t* kb[2] = {nullptr, nullptr};
-    int* kpre[2] = {nullptr, nullptr};
-    int* kpre_host[2] = {nullptr, nullptr};
-    int* cnt[2] = {nullptr, nullptr};
-    int* cnt_host[2] = {nullptr, nullptr};
+    uint32_t* kb[VF_PIPE_DEPTH] = {};
+    int* kpre[VF_PIPE_DEPTH] = {};
+    int* kpre_host[VF_PIPE_DEPTH] = {};
+    int* cnt[VF_PIPE_DEPTH] = {};
+    int* cnt_host[VF_PIPE_DEPTH] = {};
     long long kcap = 0;
   } pipe;
   // live per-stage timing (vf_set_timing): one event before each stage + end
@@ -1514,7 +1519,7 @@ static int pipe_init(vf_ctx* c)
   ok = ok && cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking) == cudaSuccess;
-  for (int k = 0; k < 2 && ok; k++) {
+  for (int k = 0; k < VF_PIPE_DEPTH && ok; k++) {
     ok = ok && cudaMalloc(&P.frames[k], fb) == cudaSuccess;
     ok = ok && cudaMalloc(&P.x[k], 8 * P.cap) == cudaSuccess && cudaMalloc(&P.y[k], 8 * P.cap) == cudaSuccess;
     ok = ok && cudaMalloc(&P.s[k], 8 * P.cap) == cudaSuccess && cudaMalloc(&P.t[k], 8 * P.cap) == cudaSuccess;
@@ -1549,7 +1554,7 @@ static void pipe_free(vf_ctx* c)
   auto& P = c->pipe;
   if (!P.init) return;
   cudaStreamSynchronize(P.h2d); cudaStreamSynchronize(P.comp); cudaStreamSynchronize(P.d2h);
-  for (int k = 0; k < 2; k++) {
+  for (int k = 0; k < VF_PIPE_DEPTH; k++) {
     for (void* p : {(void*)P.frames[k], (void*)P.x[k], (void*)P.y[k], (void*)P.s[k], (void*)P.t[k], (void*)P.v[k],
                     (void*)P.o[k], (void*)P.a[k], (void*)P.d[k], (void*)P.meta[k]})
       cudaFree(p);
@@ -1605,10 +1610,10 @@ int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_str
   int rc = pipe_init(c);
   if (rc) return rc;
   auto& P = c->pipe;
-  if (P.submitted - P.collected >= 2) return VF_ERR_ARG;   // collect the oldest step first
-  const int k = (int)(P.submitted & 1);
+  if (P.submitted - P.collected >= VF_PIPE_DEPTH) return VF_ERR_ARG;   // collect the oldest step first
+  const int k = (int)(P.submitted % VF_PIPE_DEPTH);
   const long long fbytes = (long long)c->g.W * c->g.H;
-  // frames -> device (buffer k was last read by compute of step submitted-2: ev_comp[k])
+  // frames -> device (buffer k was last read by compute of step submitted - VF_PIPE_DEPTH: ev_comp[k])
   cudaStreamWaitEvent(P.h2d, P.ev_comp[k], 0);
   cudaError_t e = cudaSuccess;
   if (row_pitch == c->g.W && stream_stride == fbytes)
@@ -1619,7 +1624,7 @@ int vf_pipeline_submit(vf_ctx* c, const uint8_t* frames_host, int64_t stream_str
                             c->g.H, cudaMemcpyHostToDevice, P.h2d);
   if (e != cudaSuccess) return cuda_status(e);
   cudaEventRecord(P.ev_h2d[k], P.h2d);
-  // the whole path, then pack (pack buffer k was last read by the d2h of step submitted-2)
+  // the whole path, then pack (pack buffer k was last read by the d2h of step submitted - VF_PIPE_DEPTH)
   cudaStreamWaitEvent(P.comp, P.ev_h2d[k], 0);
   rc = vf_process(c, P.frames[k], fbytes, c->g.W, n_streams, P.comp);   // graph replay for small batches
   if (rc) return rc;
@@ -1649,7 +1654,7 @@ int vf_pipeline_collect(vf_ctx* c, int64_t cap, double* x, double* y, double* si
   if (!c || !offsets) return VF_ERR_ARG;
   auto& P = c->pipe;
   if (!P.init || P.collected >= P.submitted) return VF_ERR_ARG;
-  const int k = (int)(P.collected & 1);
+  const int k = (int)(P.collected % VF_PIPE_DEPTH);
   cudaError_t e = cudaEventSynchronize(P.ev_pre[k]);
   if (e != cudaSuccess) return cuda_status(e);
   const int ns = P.n_streams[k];
@@ -1698,7 +1703,7 @@ int vf_pipeline_collect_delta(vf_ctx* c, int64_t cap, double* x, double* y, doub
   if (!c || !det_offsets || !keep_offsets || !counts) return VF_ERR_ARG;
   auto& P = c->pipe;
   if (!P.init || !P.delta || P.collected >= P.submitted) return VF_ERR_ARG;
-  const int k = (int)(P.collected & 1);
+  const int k = (int)(P.collected % VF_PIPE_DEPTH);
   cudaError_t e = cudaEventSynchronize(P.ev_pre[k]);
   if (e != cudaSuccess) return cuda_status(e);
   const int ns = P.n_streams[k];

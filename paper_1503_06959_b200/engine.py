@@ -177,7 +177,7 @@ class FeatureEngine:
         if a.ndim == 2:
             a = a[None]
         S, H, W = a.shape
-        self._keep = getattr(self, "_keep", [])[-1:] + [a]   # host memory must live until its copy ran
+        self._keep = getattr(self, "_keep", [])[-2:] + [a]   # host memory must live until its copy ran (3 in flight)
         _native.check(_native.lib().vf_pipeline_submit(self._h, a.ctypes.data, H * W, W, S), "vf_pipeline_submit")
 
     def collect(self, out: dict) -> dict:

@@ -1,4 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_stages.py tests/test_gpu_pipeline.py tests/test_gpu_long.py -x -q -m gpu > gpurun_out/s4k_tests.log 2>&1; echo rc=$? >> gpurun_out/s4k_tests.log
-VF_D2H_KERNEL=0 timeout 900 python -m pytest tests/test_gpu_stages.py -x -q -m gpu > gpurun_out/s4k_tests_nok.log 2>&1; echo rc=$? >> gpurun_out/s4k_tests_nok.log
-for c in 1 2 3 4; do timeout 300 python tools/micro/host_submit_time.py $c > gpurun_out/s4k_host_c$c.log 2>&1; VF_D2H_KERNEL=0 timeout 300 python tools/micro/host_submit_time.py $c > gpurun_out/s4k_hostnok_c$c.log 2>&1; done
-for c in 5 2; do timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/s4k_bench_c$c.log 2>&1; VF_D2H_KERNEL=0 timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/s4k_benchnok_c$c.log 2>&1; done
+for c in 2 1 3 4 5; do timeout 600 python bench.py --config $c --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/s4o_bench_c$c.log 2>&1; done

@@ -31,22 +31,31 @@ for label, idx in (("same pointer", [4] * 200), ("alternating pointers", [4, 5] 
     print(f"config {cid} {label}: host enqueue {1e6 * (t1 - t0) / len(idx):.1f} us/step, "
           f"with the GPU {1e6 * (t2 - t0) / len(idx):.1f} us/step")
 host = fr.cpu().pin_memory()
-out = eng.alloc_delta(S * max(65536, cfg.width * cfg.height // 8))
-eng.set_delta(True)
-eng.submit(host[0].numpy())
-eng.collect_delta(out)
-ts, tc = 0.0, 0.0
-t0 = time.perf_counter()
-eng.submit(host[1].numpy())
-for n in range(1, 11):
-    a = time.perf_counter()
-    if n + 1 < 12:
-        eng.submit(host[n + 1].numpy())
-    b = time.perf_counter()
-    eng.collect_delta(out)
-    c = time.perf_counter()
-    ts += b - a
-    tc += c - b
-print(f"config {cid} pipelined: {1e6 * (time.perf_counter() - t0) / 10:.1f} us/step; submit {1e5 * ts:.1f} us, "
-      f"collect_delta {1e5 * tc:.1f} us (host time per call)")
+cap = S * max(65536, cfg.width * cfg.height // 8)
+for delta in (True, False, True):
+    out = eng.alloc_delta(cap) if delta else eng.alloc_host(cap)
+    collect = eng.collect_delta if delta else eng.collect
+    eng.set_delta(delta)
+    for n in range(3):
+        eng.submit(host[n].numpy())
+        collect(out)
+    N = 40
+    ts, tc, per = 0.0, 0.0, []
+    t0 = time.perf_counter()
+    eng.submit(host[3 % 12].numpy())
+    eng.submit(host[4 % 12].numpy())
+    for n in range(N):
+        a = time.perf_counter()
+        if n + 2 < N:
+            eng.submit(host[(n + 5) % 12].numpy())
+        b = time.perf_counter()
+        collect(out)
+        c = time.perf_counter()
+        ts += b - a
+        tc += c - b
+        per.append(1e6 * (c - a))
+    per_s = sorted(per)
+    print(f"config {cid} pipelined {'delta' if delta else 'full'}: {1e6 * (time.perf_counter() - t0) / N:.1f} us/step; "
+          f"submit {1e6 * ts / N:.1f} us, collect {1e6 * tc / N:.1f} us per call; per-step p10 {per_s[N // 10]:.0f} "
+          f"p50 {per_s[N // 2]:.0f} p90 {per_s[9 * N // 10]:.0f} us")
 eng.close()
