@@ -2146,8 +2146,10 @@ __global__ void __launch_bounds__(NMS_THREADS, 8) k_nms(const __grid_constant__ 
 #define NL_WARPS 8
 __device__ __forceinline__ int band_count(const Bufs& b, const Geo& g, int s, int bid, int epoch)
 {
+  // both loads issued together (a stale count of an inactive band is discarded)
   const long long i = (long long)s * g.bands_per_stream + bid;
-  return b.band_stamp[i] == epoch ? __ldcg(b.band_cand + i) : 0;
+  const int st = b.band_stamp[i], cnt = __ldcg(b.band_cand + i);
+  return st == epoch ? cnt : 0;
 }
 
 __global__ void __launch_bounds__(32 * NL_WARPS) k_nms_list(const __grid_constant__ Geo g,
@@ -2159,6 +2161,7 @@ __global__ void __launch_bounds__(32 * NL_WARPS) k_nms_list(const __grid_constan
   const int band0 = blockIdx.x * NL_WARPS, nb = g.bands_per_stream;
   // candidates of the active bands before this CTA's
   int part = 0;
+#pragma unroll 2
   for (int i = tid; i < band0; i += 32 * NL_WARPS) part += band_count(b, g, s, i, epoch);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
