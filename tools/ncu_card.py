@@ -1,7 +1,7 @@
 """One markdown card per kernel from `ncu --set full` reports: SOL, occupancy,
 memory, the dominant stall reasons and the top source lines.
 
-    python tools/ncu_card.py OUT.md REP.ncu-rep[:kernel] ...
+    python tools/ncu_card.py OUT.md [--title=TEXT] REP.ncu-rep[:kernel] ...
 """
 import csv
 import subprocess
@@ -66,8 +66,15 @@ def hot(rep, kern, top=8):
 
 
 if __name__ == "__main__":
-    out = [f"# ncu --set full cards (config 5, intensity, one step after 3 warm-up steps; serialized replay)\n"]
-    for arg in sys.argv[2:]:
+    title = "config 5, intensity"
+    args = []
+    for a in sys.argv[2:]:
+        if a.startswith("--title="):
+            title = a[len("--title="):]
+        else:
+            args.append(a)
+    out = [f"# ncu --set full cards ({title}, one step after 3 warm-up steps; serialized replay)\n"]
+    for arg in args:
         rep, _, kern = arg.partition(":")
         kern = kern or rep.rsplit("_", 1)[-1].replace(".ncu-rep", "")
         out.append(f"## {kern}\n")
