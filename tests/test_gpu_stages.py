@@ -301,3 +301,82 @@ def test_packed_and_pipelined_outputs_match_per_stream():
                     assert np.array_equal(out[k][a:b], per[s][k]), (n, s, k)
     ref.close()
     pipe.close()
+
+
+@pytest.mark.parametrize("d2h_kernel", ["1", "0"])
+def test_pipelined_api_three_steps_in_flight(d2h_kernel):
+    """vf_pipeline_submit keeps up to three steps in flight (a fourth submit is refused) and
+    collect / collect_delta return them oldest first, identical to step-by-step processing --
+    with the results delivered by one k_copy_out launch (small results into pinned arrays) or by
+    the per-field copies (VF_D2H_KERNEL=0), into pinned and into pageable arrays."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    child = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1503_06959_b200 import scenes
+from paper_1503_06959_b200.engine import FeatureEngine
+from paper_1503_06959_b200.types import MaskConfig, PipelineConfig
+cfg = scenes.SceneConfig(320, 240, 9, 2, "mixed", (3, 6), (0.0, 4.0), (0.5, 2.0), noise_sigma=2.0,
+                         block_contrast=120.0, seed=17)
+frames = scenes.generate(cfg).numpy()
+S, N = frames.shape[:2]
+pcfg = PipelineConfig(mask=MaskConfig(mode="intensity"))
+ref = FeatureEngine(320, 240, pcfg, n_streams=S)
+dev = torch.from_numpy(np.ascontiguousarray(frames.transpose(1, 0, 2, 3))).cuda()
+want = []
+for n in range(N):
+    ref.process(dev[n])
+    want.append([ref.features_host(s) for s in range(S)])
+ref.close()
+host = [np.ascontiguousarray(frames[:, n]) for n in range(N)]
+keys = ("x", "y", "sigma", "theta", "score", "origin", "age", "desc")
+for pinned in (True, False):
+    pipe = FeatureEngine(320, 240, pcfg, n_streams=S)
+    out = pipe.alloc_host(S * 20000, pinned=pinned)
+    pipe.submit(host[0]); pipe.submit(host[1]); pipe.submit(host[2])
+    try:
+        pipe.submit(host[3])
+        raise SystemExit("a fourth step in flight was accepted")
+    except (RuntimeError, ValueError):
+        pass
+    for n in range(N):
+        pipe.collect(out)
+        if n + 3 < N:
+            pipe.submit(host[n + 3])
+        offs = out["offsets"]
+        for s in range(S):
+            a, b = int(offs[s]), int(offs[s + 1])
+            assert b - a == want[n][s]["n"], (pinned, n, s)
+            for k in keys:
+                assert np.array_equal(out[k][a:b], want[n][s][k]), (pinned, n, s, k)
+    pipe.close()
+    # delta delivery, three in flight: rebuild every merged list on the host
+    pipe = FeatureEngine(320, 240, pcfg, n_streams=S)
+    out = pipe.alloc_delta(S * 20000, pinned=pinned)
+    pipe.set_delta(True)
+    empty = {k: np.zeros(0, np.float64) for k in ("x", "y", "sigma", "theta", "score")}
+    empty.update(origin=np.zeros(0, np.uint8), age=np.zeros(0, np.int32), desc=np.zeros((0, 64), np.uint8))
+    prev = [empty] * S
+    for n in range(min(3, N)):
+        pipe.submit(host[n])
+    for n in range(N):
+        pipe.collect_delta(out)
+        if n + 3 < N:
+            pipe.submit(host[n + 3])
+        for s in range(S):
+            cur = FeatureEngine.delta_apply(prev[s], out, s)
+            assert cur["n"] == want[n][s]["n"], (pinned, n, s)
+            for k in keys:
+                assert np.array_equal(cur[k], want[n][s][k]), (pinned, n, s, k)
+            prev[s] = {k: (v.copy() if k != "n" else v) for k, v in cur.items()}
+    pipe.close()
+print("ok")
+"""
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, VF_D2H_KERNEL=d2h_kernel)   # read once per process
+    r = subprocess.run([sys.executable, "-c", child, str(root)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), (r.stdout[-500:], r.stderr[-2000:])
