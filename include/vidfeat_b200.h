@@ -154,7 +154,12 @@ int vf_fetch_features(vf_ctx *ctx, int n_streams, int64_t cap, double *x, double
  * flight (submit, submit, submit, collect, submit, collect, ...; a fourth
  * submit returns VF_ERR_ARG), so the H2D of step n+2 is already queued while
  * step n+1 computes and step n's result is copied out: the slowest of the
- * three sets the pace.  Two in flight (submit, submit, collect, ...) works too.  Stream-ordered with respect
+ * three sets the pace.  Two in flight (submit, submit, collect, ...) works too.
+ * collect reads the step's offsets, counts and error flags from one pinned
+ * meta-data copy, then delivers the fields: results up to 64 KB into pinned
+ * (device-addressable) arrays by one kernel launch that writes over PCIe,
+ * anything else by one cudaMemcpyAsync per field (VF_D2H_KERNEL=0 forces the
+ * copies).  Stream-ordered with respect
  * to the context's own streams only; not to be mixed with vf_process on the
  * same context. */
 int vf_pipeline_submit(vf_ctx *ctx, const uint8_t *frames_host, int64_t stream_stride, int64_t row_pitch,
