@@ -2649,7 +2649,9 @@ __device__ __forceinline__ void point_means2(const uint32_t* S, const Geo& g, do
   mb = exact_div(sc, (uint32_t)c.area);
 }
 
+#ifndef DSW
 #define DSW 8   // warps per CTA of k_desc_fused
+#endif
 
 // ============================================================================
 // Orientation helpers of k_desc_fused
