@@ -447,11 +447,17 @@ def init_process_group(world, local):
         return f"none ({type(e).__name__})"
 
 
-def launches_per_step(mode, n_streams):
+def launches_per_step(mode, n_streams, width, height):
     # k_pyr_o, k_pyr_i, k_worklist x2 (main + side stream), k_fast, k_nms_list,
-    # k_nms_test, k_nms_finish, k_finalize; k_sat + k_desc_fused once per
-    # concurrent describe half; + k_propagate (mask modes), + k_binmask (binning)
-    return 9 + 2 * desc_halves(n_streams) + (1 if mode in ("intensity", "binning") else 0) + (
+    # k_nms_test, k_nms_finish, k_finalize; + k_propagate (mask modes), + k_binmask
+    # (binning); the SATs and the describe kernel: early SATs (the default except
+    # for intensity-masked batches over 64 MB, vf_capi.cu launch_step) are
+    # k_sat_list + k_sat once and k_desc_fused per concurrent describe half, late
+    # SATs k_sat + k_desc_fused per half
+    env = os.environ.get("VF_SAT_EARLY")
+    early = (env != "0") if env is not None else not (mode == "intensity" and width * height * n_streams > (64 << 20))
+    halves = desc_halves(n_streams)
+    return 9 + (2 + halves if early else 2 * halves) + (1 if mode in ("intensity", "binning") else 0) + (
         1 if mode == "binning" else 0)
 
 
@@ -764,7 +770,7 @@ def run_detect(args, rank, world, local):
         "e2e": e2e,
         "e2e_full_lists": e2e_full,
         "stream_stats": stream_stats,
-        "gpu_launches": launches_per_step(args.mode, S) * K,
+        "gpu_launches": launches_per_step(args.mode, S, W, H) * K,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
